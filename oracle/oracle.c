@@ -1,0 +1,403 @@
+/*
+ * oracle.c -- plain CPU oracle of the electrostatic PIC step.  TEST
+ * INFRASTRUCTURE ONLY (see oracle.h): never used by the product path.
+ *
+ * Build: gcc -O2 -ffp-contract=off -fPIC -shared (fma() only where written).
+ * Every function follows the paper's definition in the paper's order; no
+ * blocking, fusion or reordering.  Citations: P:n = PAPER.md line n,
+ * S:n = SPEC.md line n, D#k = DESIGN.md reading k.
+ */
+#include "oracle.h"
+
+#include <complex.h>
+#include <math.h>
+#include <stdlib.h>
+#include <string.h>
+
+/* ------------------------------------------------------------------ RNG ---- */
+/* Philox4x32-10 (Salmon et al., Random123), D#10. */
+static void mulhilo32(uint32_t a, uint32_t b, uint32_t *hi, uint32_t *lo) {
+    uint64_t p = (uint64_t)a * (uint64_t)b;
+    *hi = (uint32_t)(p >> 32);
+    *lo = (uint32_t)p;
+}
+
+void oracle_philox4x32_10(const uint32_t ctr_in[4], const uint32_t key_in[2], uint32_t out[4]) {
+    const uint32_t M0 = 0xD2511F53u, M1 = 0xCD9E8D57u;
+    const uint32_t W0 = 0x9E3779B9u, W1 = 0xBB67AE85u;
+    uint32_t c[4] = {ctr_in[0], ctr_in[1], ctr_in[2], ctr_in[3]};
+    uint32_t k[2] = {key_in[0], key_in[1]};
+    for (int r = 0; r < 10; ++r) {
+        if (r > 0) { k[0] += W0; k[1] += W1; }
+        uint32_t hi0, lo0, hi1, lo1;
+        mulhilo32(M0, c[0], &hi0, &lo0);
+        mulhilo32(M1, c[2], &hi1, &lo1);
+        uint32_t n0 = hi1 ^ c[1] ^ k[0];
+        uint32_t n1 = lo1;
+        uint32_t n2 = hi0 ^ c[3] ^ k[1];
+        uint32_t n3 = lo0;
+        c[0] = n0; c[1] = n1; c[2] = n2; c[3] = n3;
+    }
+    out[0] = c[0]; out[1] = c[1]; out[2] = c[2]; out[3] = c[3];
+}
+
+/* u_t = (w_t >> 11) * 2^-53, w_{2b} = r0 | r1<<32, w_{2b+1} = r2 | r3<<32 with
+ * (r0..r3) = philox((j lo, j hi, b, 0), (seed lo, seed hi)), b = 0..3 (D#10). */
+void oracle_uniforms(uint64_t seed, uint64_t j, double u[8]) {
+    uint32_t key[2] = {(uint32_t)seed, (uint32_t)(seed >> 32)};
+    for (uint32_t b = 0; b < 4; ++b) {
+        uint32_t ctr[4] = {(uint32_t)j, (uint32_t)(j >> 32), b, 0u};
+        uint32_t r[4];
+        oracle_philox4x32_10(ctr, key, r);
+        uint64_t w0 = (uint64_t)r[0] | ((uint64_t)r[1] << 32);
+        uint64_t w1 = (uint64_t)r[2] | ((uint64_t)r[3] << 32);
+        u[2 * b] = (double)(w0 >> 11) * 0x1p-53;
+        u[2 * b + 1] = (double)(w1 >> 11) * 0x1p-53;
+    }
+}
+
+double oracle_wrap(double x, double L) {
+    /* wrap into [0, L); x = L maps to 0. */
+    if (x >= L) {
+        x = x - L;
+    } else if (x < 0.0) {
+        x = x + L;
+        if (x >= L) x = 0.0;
+    }
+    return x;
+}
+
+/* Inverse CDF of the 1D marginal (1 + alpha cos(k x))/L, P:143-146:
+ * F(x) = x + (alpha/k) sin(k x) - u L = 0, Newton from x = u L, |dx| < 1e-12 or
+ * 32 iterations. */
+static double landau_position(double u, double k, double L, double alpha) {
+    double target = u * L;
+    double x = target;
+    for (int it = 0; it < 32; ++it) {
+        double F = x + (alpha / k) * sin(k * x) - target;
+        double dF = 1.0 + alpha * cos(k * x);
+        double dx = F / dF;
+        x = x - dx;
+        if (fabs(dx) < 1e-12) break;
+    }
+    return oracle_wrap(x, L);
+}
+
+void oracle_sample_landau(int64_t np, double k, double L, double alpha, uint64_t seed,
+                          double *xv) {
+    const double two_pi = 6.283185307179586476925286766559;
+    for (int64_t j = 0; j < np; ++j) {
+        double u[8];
+        oracle_uniforms(seed, (uint64_t)j, u);
+        for (int d = 0; d < 3; ++d) xv[d * np + j] = landau_position(u[d], k, L, alpha);
+        /* Box-Muller: (vx, vy) from (u3, u4), vz from (u5, u6). */
+        double r1 = sqrt(-2.0 * log(1.0 - u[3]));
+        double r2 = sqrt(-2.0 * log(1.0 - u[5]));
+        xv[3 * np + j] = r1 * cos(two_pi * u[4]);
+        xv[4 * np + j] = r1 * sin(two_pi * u[4]);
+        xv[5 * np + j] = r2 * cos(two_pi * u[6]);
+    }
+}
+
+/* ------------------------------------------------------------ keys/sort ---- */
+int32_t oracle_cell_index(double x, double inv_h, int32_t n) {
+    int32_t i = (int32_t)floor(x * inv_h);
+    if (i >= n) i = n - 1;  /* x just below L rounding up (D#5) */
+    if (i < 0) i = 0;
+    return i;
+}
+
+uint32_t oracle_morton_key(int32_t ix, int32_t iy, int32_t iz, int32_t n) {
+    uint32_t key = 0;
+    for (int b = 0; (1 << b) < n; ++b) {
+        key |= (uint32_t)((ix >> b) & 1) << (3 * b);
+        key |= (uint32_t)((iy >> b) & 1) << (3 * b + 1);
+        key |= (uint32_t)((iz >> b) & 1) << (3 * b + 2);
+    }
+    return key;
+}
+
+void oracle_keys(int32_t n, double L, int64_t np, const double *xv, uint32_t *keys) {
+    const double inv_h = (double)n / L;
+    for (int64_t j = 0; j < np; ++j) {
+        int32_t ix = oracle_cell_index(xv[0 * np + j], inv_h, n);
+        int32_t iy = oracle_cell_index(xv[1 * np + j], inv_h, n);
+        int32_t iz = oracle_cell_index(xv[2 * np + j], inv_h, n);
+        keys[j] = oracle_morton_key(ix, iy, iz, n);
+    }
+}
+
+void oracle_sort(int32_t n, double L, int64_t np, double *xv, uint32_t *perm) {
+    /* Stable counting sort by cell key: ties keep the current order (D#14). */
+    const int64_t ncell = (int64_t)n * n * n;
+    uint32_t *keys = (uint32_t *)malloc(sizeof(uint32_t) * (size_t)(np > 0 ? np : 1));
+    int64_t *start = (int64_t *)calloc((size_t)ncell + 1, sizeof(int64_t));
+    double *tmp = (double *)malloc(sizeof(double) * (size_t)(np > 0 ? np : 1));
+    oracle_keys(n, L, np, xv, keys);
+    for (int64_t j = 0; j < np; ++j) start[keys[j] + 1] += 1;
+    for (int64_t c = 0; c < ncell; ++c) start[c + 1] += start[c];
+    for (int64_t j = 0; j < np; ++j) perm[start[keys[j]]++] = (uint32_t)j;
+    for (int a = 0; a < 6; ++a) {
+        double *col = xv + (int64_t)a * np;
+        for (int64_t i = 0; i < np; ++i) tmp[i] = col[perm[i]];
+        memcpy(col, tmp, sizeof(double) * (size_t)np);
+    }
+    free(tmp);
+    free(start);
+    free(keys);
+}
+
+/* ------------------------------------------------------------ scatter ----- */
+static int64_t node(int32_t n, int32_t ix, int32_t iy, int32_t iz) {
+    return ((int64_t)((iz % n + n) % n) * n + ((iy % n + n) % n)) * n + ((ix % n + n) % n);
+}
+
+void oracle_deposit(int32_t n, double L, int64_t np, const double *xv, double q, double *rho) {
+    const double inv_h = (double)n / L;
+    const int64_t nn = (int64_t)n * n * n;
+    for (int64_t m = 0; m < nn; ++m) rho[m] = 0.0;
+    for (int64_t j = 0; j < np; ++j) {
+        int32_t i[3];
+        double w[3][2];
+        for (int d = 0; d < 3; ++d) {
+            double s = xv[d * np + j] * inv_h;
+            i[d] = oracle_cell_index(xv[d * np + j], inv_h, n);
+            double f = s - (double)i[d];
+            w[d][0] = 1.0 - f;
+            w[d][1] = f;
+        }
+        for (int c = 0; c < 2; ++c)
+            for (int b = 0; b < 2; ++b)
+                for (int a = 0; a < 2; ++a) {
+                    double wt = (w[0][a] * w[1][b]) * w[2][c];
+                    rho[node(n, i[0] + a, i[1] + b, i[2] + c)] += wt;
+                }
+    }
+    const double scale = q * ((inv_h * inv_h) * inv_h);
+    for (int64_t m = 0; m < nn; ++m) rho[m] = scale * rho[m];
+}
+
+/* -------------------------------------------------------------- solve ----- */
+/* In-place radix-2 complex FFT of one strided line, sign = -1 forward
+ * (e^{-i k x}), +1 inverse (unnormalised).  Twiddles cos/sin(2 pi j / N). */
+static void fft_line(double complex *a, int32_t n, int64_t stride, int sign) {
+    const double two_pi = 6.283185307179586476925286766559;
+    for (int32_t i = 1, j = 0; i < n; ++i) {
+        int32_t bit = n >> 1;
+        for (; j & bit; bit >>= 1) j ^= bit;
+        j ^= bit;
+        if (i < j) {
+            double complex t = a[i * stride];
+            a[i * stride] = a[j * stride];
+            a[j * stride] = t;
+        }
+    }
+    for (int32_t len = 2; len <= n; len <<= 1) {
+        for (int32_t i = 0; i < n; i += len) {
+            for (int32_t m = 0; m < len / 2; ++m) {
+                double ang = sign * two_pi * (double)m / (double)len;
+                double complex w = cos(ang) + I * sin(ang);
+                double complex u = a[(i + m) * stride];
+                double complex v = a[(i + m + len / 2) * stride] * w;
+                a[(i + m) * stride] = u + v;
+                a[(i + m + len / 2) * stride] = u - v;
+            }
+        }
+    }
+}
+
+static void fft3d(double complex *c, int32_t n, int sign) {
+    for (int32_t iz = 0; iz < n; ++iz)          /* along x */
+        for (int32_t iy = 0; iy < n; ++iy) fft_line(c + ((int64_t)iz * n + iy) * n, n, 1, sign);
+    for (int32_t iz = 0; iz < n; ++iz)          /* along y */
+        for (int32_t ix = 0; ix < n; ++ix) fft_line(c + (int64_t)iz * n * n + ix, n, n, sign);
+    for (int32_t iy = 0; iy < n; ++iy)          /* along z */
+        for (int32_t ix = 0; ix < n; ++ix) fft_line(c + (int64_t)iy * n + ix, n, (int64_t)n * n, sign);
+}
+
+/* Mode number n_d in [-N/2, N/2-1] of array index idx. */
+static int32_t mode_of(int32_t idx, int32_t n) { return idx < n / 2 ? idx : idx - n; }
+
+/* Spectral field of mode (ix,iy,iz): E_d = -i k_d rho / |k|^2, with E = 0 at
+ * n = 0 and E_d = 0 where n_d = -N/2 (D#6). P:175. */
+static void spectral_field(int32_t n, double L, int32_t ix, int32_t iy, int32_t iz,
+                           double complex rhohat, double complex Ehat[3]) {
+    const double two_pi = 6.283185307179586476925286766559;
+    int32_t idx[3] = {ix, iy, iz};
+    double kv[3];
+    double k2 = 0.0;
+    for (int d = 0; d < 3; ++d) {
+        kv[d] = two_pi * (double)mode_of(idx[d], n) / L;
+        k2 += kv[d] * kv[d];
+    }
+    for (int d = 0; d < 3; ++d) {
+        if (k2 == 0.0 || idx[d] == n / 2) Ehat[d] = 0.0;
+        else Ehat[d] = -I * kv[d] * rhohat / k2;
+    }
+}
+
+double oracle_solve_fft(int32_t n, double L, const double *rho, double *E) {
+    const int64_t nn = (int64_t)n * n * n;
+    double complex *rh = (double complex *)malloc(sizeof(double complex) * (size_t)nn);
+    double complex *eh = (double complex *)malloc(sizeof(double complex) * (size_t)nn * 3);
+    for (int64_t m = 0; m < nn; ++m) rh[m] = rho[m];
+    fft3d(rh, n, -1);
+    for (int32_t iz = 0; iz < n; ++iz)
+        for (int32_t iy = 0; iy < n; ++iy)
+            for (int32_t ix = 0; ix < n; ++ix) {
+                int64_t m = ((int64_t)iz * n + iy) * n + ix;
+                double complex e3[3];
+                spectral_field(n, L, ix, iy, iz, rh[m], e3);
+                for (int d = 0; d < 3; ++d) eh[d * nn + m] = e3[d];
+            }
+    double max_imag = 0.0;
+    for (int d = 0; d < 3; ++d) {
+        fft3d(eh + d * nn, n, +1);
+        for (int64_t m = 0; m < nn; ++m) {
+            double complex v = eh[d * nn + m] / (double)nn;
+            E[d * nn + m] = creal(v);
+            if (fabs(cimag(v)) > max_imag) max_imag = fabs(cimag(v));
+        }
+    }
+    free(eh);
+    free(rh);
+    return max_imag;
+}
+
+double oracle_solve_dft(int32_t n, double L, const double *rho, double *E) {
+    /* rhohat(n) = sum_m rho(m) e^{-2 pi i n.m/N};  E_d(m) = N^-3 sum_n Ehat_d(n) e^{+2 pi i n.m/N}. */
+    const double two_pi = 6.283185307179586476925286766559;
+    const int64_t nn = (int64_t)n * n * n;
+    double complex *eh = (double complex *)malloc(sizeof(double complex) * (size_t)nn * 3);
+    for (int64_t kk = 0; kk < nn; ++kk) {
+        int32_t kx = (int32_t)(kk % n), ky = (int32_t)((kk / n) % n), kz = (int32_t)(kk / ((int64_t)n * n));
+        double complex acc = 0.0;
+        for (int64_t m = 0; m < nn; ++m) {
+            int32_t mx = (int32_t)(m % n), my = (int32_t)((m / n) % n), mz = (int32_t)(m / ((int64_t)n * n));
+            int64_t ph = ((int64_t)kx * mx + (int64_t)ky * my + (int64_t)kz * mz) % n;
+            double ang = -two_pi * (double)ph / (double)n;
+            acc += rho[m] * (cos(ang) + I * sin(ang));
+        }
+        double complex e3[3];
+        spectral_field(n, L, kx, ky, kz, acc, e3);
+        for (int d = 0; d < 3; ++d) eh[d * nn + kk] = e3[d];
+    }
+    double max_imag = 0.0;
+    for (int d = 0; d < 3; ++d) {
+        for (int64_t m = 0; m < nn; ++m) {
+            int32_t mx = (int32_t)(m % n), my = (int32_t)((m / n) % n), mz = (int32_t)(m / ((int64_t)n * n));
+            double complex acc = 0.0;
+            for (int64_t kk = 0; kk < nn; ++kk) {
+                int32_t kx = (int32_t)(kk % n), ky = (int32_t)((kk / n) % n), kz = (int32_t)(kk / ((int64_t)n * n));
+                int64_t ph = ((int64_t)kx * mx + (int64_t)ky * my + (int64_t)kz * mz) % n;
+                double ang = two_pi * (double)ph / (double)n;
+                acc += eh[d * nn + kk] * (cos(ang) + I * sin(ang));
+            }
+            acc = acc / (double)nn;
+            E[d * nn + m] = creal(acc);
+            if (fabs(cimag(acc)) > max_imag) max_imag = fabs(cimag(acc));
+        }
+    }
+    free(eh);
+    return max_imag;
+}
+
+void oracle_field_energy(int32_t n, double L, const double *E, double *wx, double *w) {
+    const int64_t nn = (int64_t)n * n * n;
+    const double h = L / (double)n;
+    const double h3 = (h * h) * h;
+    double sx = 0.0, s = 0.0;
+    for (int64_t m = 0; m < nn; ++m) {
+        double ex = E[m], ey = E[nn + m], ez = E[2 * nn + m];
+        sx += ex * ex;
+        s += ex * ex + ey * ey + ez * ez;
+    }
+    *wx = 0.5 * h3 * sx;
+    *w = 0.5 * h3 * s;
+}
+
+/* --------------------------------------------------------- gather/push ---- */
+void oracle_gather(int32_t n, double L, int64_t np, const double *xv, const double *E,
+                   double *Ep) {
+    const double inv_h = (double)n / L;
+    const int64_t nn = (int64_t)n * n * n;
+    for (int64_t j = 0; j < np; ++j) {
+        int32_t i[3];
+        double w[3][2];
+        for (int d = 0; d < 3; ++d) {
+            double s = xv[d * np + j] * inv_h;
+            i[d] = oracle_cell_index(xv[d * np + j], inv_h, n);
+            double f = s - (double)i[d];
+            w[d][0] = 1.0 - f;
+            w[d][1] = f;
+        }
+        double acc[3] = {0.0, 0.0, 0.0};
+        for (int c = 0; c < 2; ++c)
+            for (int b = 0; b < 2; ++b)
+                for (int a = 0; a < 2; ++a) {
+                    double wt = (w[0][a] * w[1][b]) * w[2][c];
+                    int64_t m = node(n, i[0] + a, i[1] + b, i[2] + c);
+                    for (int d = 0; d < 3; ++d) acc[d] = fma(wt, E[d * nn + m], acc[d]);
+                }
+        for (int d = 0; d < 3; ++d) Ep[d * np + j] = acc[d];
+    }
+}
+
+void oracle_push(double L, int64_t np, double *xv, const double *Ep, double qm_dt, double dt) {
+    for (int64_t j = 0; j < np; ++j) {
+        for (int d = 0; d < 3; ++d) {
+            double v = fma(qm_dt, Ep[d * np + j], xv[(3 + d) * np + j]);   /* kick */
+            double x = fma(v, dt, xv[d * np + j]);                        /* drift */
+            xv[(3 + d) * np + j] = v;
+            xv[d * np + j] = oracle_wrap(x, L);
+        }
+    }
+}
+
+/* ------------------------------------------------------------ PIC loop ---- */
+void oracle_half_kick(int32_t n, double L, double dt, int64_t np, double *xv) {
+    const int64_t nn = (int64_t)n * n * n;
+    const double q = -((L * L) * L) / (double)np;
+    const double qm = -1.0;
+    double *rho = (double *)malloc(sizeof(double) * (size_t)nn);
+    double *E = (double *)malloc(sizeof(double) * (size_t)nn * 3);
+    double *Ep = (double *)malloc(sizeof(double) * (size_t)(np > 0 ? np : 1) * 3);
+    oracle_deposit(n, L, np, xv, q, rho);
+    oracle_solve_fft(n, L, rho, E);
+    oracle_gather(n, L, np, xv, E, Ep);
+    const double hk = -0.5 * (qm * dt);    /* v_{-1/2} = v_0 - (q/m) E dt/2 */
+    for (int64_t j = 0; j < np; ++j)
+        for (int d = 0; d < 3; ++d)
+            xv[(3 + d) * np + j] = fma(hk, Ep[d * np + j], xv[(3 + d) * np + j]);
+    free(Ep);
+    free(E);
+    free(rho);
+}
+
+void oracle_run(int32_t n, double L, double dt, int64_t np, double *xv, int32_t nsteps,
+                double *ex_energy, double *tot_energy, uint32_t *perm_last) {
+    const int64_t nn = (int64_t)n * n * n;
+    const double q = -((L * L) * L) / (double)np;
+    const double qm_dt = -1.0 * dt;                  /* (q/m) dt, q/m = -1 */
+    double *rho = (double *)malloc(sizeof(double) * (size_t)nn);
+    double *E = (double *)malloc(sizeof(double) * (size_t)nn * 3);
+    double *Ep = (double *)malloc(sizeof(double) * (size_t)(np > 0 ? np : 1) * 3);
+    uint32_t *perm = (uint32_t *)malloc(sizeof(uint32_t) * (size_t)(np > 0 ? np : 1));
+    oracle_sort(n, L, np, xv, perm);                    /* canonical order */
+    for (int32_t s = 0; s < nsteps; ++s) {
+        oracle_deposit(n, L, np, xv, q, rho);           /* SCATTER */
+        oracle_solve_fft(n, L, rho, E);                 /* SOLVE */
+        double wx, w;
+        oracle_field_energy(n, L, E, &wx, &w);
+        if (ex_energy) ex_energy[s] = wx;
+        if (tot_energy) tot_energy[s] = w;
+        oracle_gather(n, L, np, xv, E, Ep);             /* GATHER */
+        oracle_push(L, np, xv, Ep, qm_dt, dt);          /* PUSH + wrap */
+        oracle_sort(n, L, np, xv, perm);                /* per-step sort by cell key */
+    }
+    if (perm_last && nsteps > 0) memcpy(perm_last, perm, sizeof(uint32_t) * (size_t)np);
+    free(perm);
+    free(Ep);
+    free(E);
+    free(rho);
+}

@@ -1,0 +1,80 @@
+/*
+ * oracle.h -- plain, slow, obviously-correct CPU oracle of the electrostatic
+ * PIC step (3D Landau damping, FFT pseudo-spectral Poisson solve, CIC, leapfrog).
+ *
+ * TEST INFRASTRUCTURE ONLY.  Only tests/, __graft_entry__.smoke() and
+ * bench.py's cpu_baseline / --impl reference leg may load this library.
+ * The product path (paper_2605_05469_b200/) never imports, links or executes
+ * anything under oracle/, and this file shares no code, header, table or
+ * constant generator with the CUDA path.
+ *
+ * Citation key: "P:n" = PAPER.md line n, "S:n" = SPEC.md line n,
+ * "D#k" = reading k in DESIGN.md section "Readings of the paper".
+ *
+ * Conventions (all fp64):
+ *   grid arrays      : [iz][iy][ix] row-major, index (iz*N + iy)*N + ix, N^3 doubles.
+ *   vector fields    : E[d][N^3], d = 0 (x), 1 (y), 2 (z).
+ *   particle state   : xv[6][np] structure of arrays: x, y, z, vx, vy, vz.
+ *   units            : eps0 = 1, q_e = -1, m_e = 1, mean density 1,
+ *                      so macro charge q = -L^3/np and q/m = -1 (D#2).
+ */
+#ifndef PIC_ORACLE_H
+#define PIC_ORACLE_H
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Philox4x32-10 counter-based RNG (D#10); out = philox(ctr, key). */
+void oracle_philox4x32_10(const uint32_t ctr[4], const uint32_t key[2], uint32_t out[4]);
+/* The 8 uniforms u_0..u_7 in [0,1) of particle j (D#10). */
+void oracle_uniforms(uint64_t seed, uint64_t j, double u[8]);
+/* Landau initial condition: x_d ~ (1+alpha cos(k x))/L by inverse CDF
+ * (Newton), v ~ N(0,1)^3 by Box-Muller.  Writes xv[6][np] in index order j. */
+void oracle_sample_landau(int64_t np, double k, double L, double alpha, uint64_t seed,
+                          double *xv);
+
+/* Cell index along one dim: floor(x*inv_h) clamped to N-1 (D#5). */
+int32_t oracle_cell_index(double x, double inv_h, int32_t n);
+/* Cell key: Morton (bit-interleaved) order of (ix, iy, iz), x fastest (D#14). */
+uint32_t oracle_morton_key(int32_t ix, int32_t iy, int32_t iz, int32_t n);
+/* keys[j] of every particle from its current position. */
+void oracle_keys(int32_t n, double L, int64_t np, const double *xv, uint32_t *keys);
+/* Stable sort of the particles by cell key (D#14); perm[i] = old index of the
+ * particle now at i; xv is permuted in place. */
+void oracle_sort(int32_t n, double L, int64_t np, double *xv, uint32_t *perm);
+
+/* CIC deposit, P:105 / S:132-140: rho[node] = q/h^3 * sum_j w(node, x_j). */
+void oracle_deposit(int32_t n, double L, int64_t np, const double *xv, double q, double *rho);
+/* Pseudo-spectral solve: E = F^-1(-i k F(rho)/|k|^2), zero mode and
+ * the d-th Nyquist plane removed from E_d (D#6).  radix-2 FFT along each axis on
+ * the full complex array.  Returns max |imag| of the inverse transforms. */
+double oracle_solve_fft(int32_t n, double L, const double *rho, double *E);
+/* The same solve by brute-force direct DFT (O(N^6)); N <= 16 only. */
+double oracle_solve_dft(int32_t n, double L, const double *rho, double *E);
+/* Field energy, P:231 / S:72-80: wx = 1/2 h^3 sum E_x^2, w = 1/2 h^3 sum |E|^2. */
+void oracle_field_energy(int32_t n, double L, const double *E, double *wx, double *w);
+/* CIC gather, P:105 / S:141-149: Ep[d][j] = sum_corners w * E_d(node). */
+void oracle_gather(int32_t n, double L, int64_t np, const double *xv, const double *E,
+                   double *Ep);
+/* Leapfrog kick-drift + periodic wrap, P:106-109 / S:150-167:
+ * v <- v + (q/m) dt E_p ; x <- x + v dt ; wrap into [0, L). */
+void oracle_push(double L, int64_t np, double *xv, const double *Ep, double qm_dt, double dt);
+/* Periodic wrap of one coordinate. */
+double oracle_wrap(double x, double L);
+
+/* Whole PIC loop (Fig. 1).  State (x_n, v_{n-1/2}) in xv, any order.
+ * The particles are first put in canonical order (stable sort by key); then
+ * nsteps x {scatter -> solve (+energy) -> gather -> push -> wrap -> sort}.
+ * ex_energy / tot_energy (nullable) receive W_x(t_n), W(t_n) for each step.
+ * perm_last (nullable, np entries) receives the last step's sort permutation. */
+void oracle_run(int32_t n, double L, double dt, int64_t np, double *xv, int32_t nsteps,
+                double *ex_energy, double *tot_energy, uint32_t *perm_last);
+/* Backward half kick: v <- v - (q/m) E(x_0) dt/2, x unchanged. */
+void oracle_half_kick(int32_t n, double L, double dt, int64_t np, double *xv);
+
+#ifdef __cplusplus
+}
+#endif
+#endif
