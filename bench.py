@@ -1,0 +1,336 @@
+#!/usr/bin/env python
+"""Benchmark of the fp64 FFT-PIC step (3D Landau damping) -- driver contract.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Metric (BASELINE.json): particle-pushes/s (whole job) and ms per PIC step.
+N=1 workload: 512^3 grid x 8 ppc (1,073,741,824 particles), k=0.5, alpha=0.05,
+dt=0.05 (BASELINE.json configs[2], the paper's case A).
+One "step" = one full PIC step: FFT solve + field energy, gather+push, counting
+sort by cell key, reorder + CIC deposit.  Inputs live in HBM (51.5 GB of
+particle state >> 126 MB L2, so no L2 flush is needed between steps).
+
+Prints ONE JSON line on rank 0.  For N > 1 (torchrun) every rank runs its own
+independent replica (domain decomposition is not in this build).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "particle-pushes/sec (fp64 FFT-PIC step, Landau damping 3D)"
+UNIT = "particle-pushes/s"
+
+# Algorithmic bytes per launch:
+# per particle, per grid node (ncell = N^3).
+ALG_BYTES = {
+    "reorder_deposit": (4 + 48 + 48, 4 + 16 + 24),  # perm, x/v gather, x/v store | offs, rho RMW, E
+    "push_key": (48 + 4, 24 + 4),                    # x/v read, key | E read, count RMW (amortised)
+    "place": (4 + 4, 4),                             # key read, perm write | cursor
+    "scan": (0, 16),                                 # count read x2, offs + cursor write
+    "fft_x_fwd": (0, 8 + 8),
+    "fft_y_fwd": (0, 8 + 8),
+    "fft_z_mul": (0, 8 + 24),
+    "fft_y_inv": (0, 24 + 24),
+    "fft_x_inv": (0, 24 + 24),
+    "clear": (0, 4 + 8),
+}
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+# ------------------------------------------------------------------ clocks --
+class ClockSampler:
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([c.strip() for c in line.split(",")])
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, smax, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in self.rows:
+            try:
+                sm.append(float(r[1]))
+                smax = float(r[2])
+                for k, nm in enumerate(names):
+                    if r[5 + k].lower() == "active":
+                        reasons.add(nm)
+            except (ValueError, IndexError):
+                pass
+        busy = sorted(sm)[len(sm) // 4:] if sm else []
+        return {"sm_mhz": statistics.median(busy) if busy else None, "sm_max_mhz": smax,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def measured_peaks():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        return {}
+
+
+def ncu_traffic(config_name: str):
+    """Per-launch DRAM bytes of the dominant kernel from the committed ncu summary."""
+    try:
+        d = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json")))
+        return d.get(config_name)
+    except Exception:
+        return None
+
+
+# ------------------------------------------------------------ oracle (CPU) --
+def oracle_sample(steps: int, n: int = 64, ppc: int = 8):
+    """Time the CPU oracle, as it stands, on a bounded sample of the workload."""
+    from oracle import oracle as O
+    from pic_inputs import landau_state
+
+    import numpy as np
+
+    L = 4 * np.pi
+    xv = landau_state(n, ppc, seed=1)
+    O.run(n, L, 0.05, xv, 1)   # warm (build, page-in)
+    t0 = time.perf_counter()
+    O.run(n, L, 0.05, xv, steps)
+    dt = time.perf_counter() - t0
+    npart = ppc * n ** 3
+    return {"value": npart * steps / dt, "unit": UNIT, "cores": 1, "kind": "oracle",
+            "sample": f"oracle_run (serial C, -O2) on Landau {n}^3 x {ppc} ppc "
+                      f"({npart} particles), {steps} steps, {dt:.1f} s; same per-particle "
+                      f"step as the {{n}}^3 workload, smaller grid"}
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return 0
+    from oracle import oracle as O
+    from pic_inputs import landau_state
+    import numpy as np
+
+    n, ppc = 64, 8
+    L = 4 * np.pi
+    xv = landau_state(n, ppc, seed=1)
+    xs = O.run(n, L, 0.05, xv, max(args.warmup, 0))[0] if args.warmup else xv
+    t0 = time.perf_counter()
+    O.run(n, L, 0.05, xs, args.steps)
+    dt = time.perf_counter() - t0
+    npart = ppc * n ** 3
+    value = npart * args.steps / dt
+    sample = (f"CPU oracle (serial C) on Landau {n}^3 x {ppc} ppc ({npart} particles) per step, "
+              f"a bounded sample of the {args.n}^3 x {args.ppc} workload")
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * dt / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic",
+        "config": {"workload": f"landau3d_{args.n}^3x{args.ppc}ppc_fft (reference arm: "
+                               f"{n}^3x{ppc} sample)", "grid": args.n, "ppc": args.ppc},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ---------------------------------------------------------------- our arm --
+def run_ours(args, rank, world):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    local = int(os.environ.get("LOCAL_RANK", 0))
+    torch.cuda.set_device(local)
+    from paper_2605_05469_b200 import Simulation, STAGES
+
+    n, ppc = args.n, args.ppc
+    np_ = ppc * n ** 3
+    t_init = time.perf_counter()
+    sim = Simulation(n=n, ppc=ppc, k=0.5, alpha=0.05, dt=0.05, seed=1 + rank, device=f"cuda:{local}")
+    torch.cuda.synchronize()
+    log(f"[rank {rank}] init {n}^3 x {ppc}: {time.perf_counter() - t_init:.1f} s, "
+        f"workspace {sim.workspace.numel() / 2**30:.1f} GiB")
+    stream = sim.stream
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    for _ in range(args.warmup):
+        sim.step(1)
+    sim.set_timing(True)
+    sim.reset_timings()
+    barrier()
+    torch.cuda.synchronize()
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        ev0.record(stream)
+        ex = sim.step(args.steps)
+        ev1.record(stream)
+        ev1.synchronize()
+    barrier()
+    torch.cuda.synchronize()
+    ms = ev0.elapsed_time(ev1)
+    stages = sim.timings()
+    sim.set_timing(False)
+    if world > 1:
+        t = torch.tensor([ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    ms_step = ms / args.steps
+    value = world * np_ * args.steps / (ms / 1e3)
+
+    # ---- end to end through the C ABI with host buffers ----------------------
+    e2e = None
+    if not args.no_e2e:
+        host = torch.empty((6, np_), dtype=torch.float64, pin_memory=True)
+        hv = host.numpy()
+        sim.get_particles(out=hv)
+        barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        sim.set_particles(hv)                 # H2D of the state (+ sort + deposit)
+        e2e_ex = sim.step(args.steps)        # per-step energies D2H
+        sim.get_particles(out=hv)             # D2H of the final state
+        torch.cuda.synchronize()
+        t_e2e = time.perf_counter() - t0
+        if world > 1:
+            t = torch.tensor([t_e2e], device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            t_e2e = float(t.item())
+        state_bytes = 48 * np_
+        e2e = {"value": world * np_ * args.steps / t_e2e, "unit": UNIT,
+               "h2d_bytes_per_step": state_bytes / args.steps,
+               "d2h_bytes_per_step": (state_bytes + 8 * args.steps) / args.steps,
+               "what": "pic_set_particles(host pinned state) + pic_step(K) with per-step W_x to host "
+                       "+ pic_get_particles(host); wall clock, max over ranks"}
+        del host
+
+    if rank != 0:
+        sim.close()
+        return 0
+
+    # ---- roofline of the dominant kernel --------------------------------------
+    ncell = n ** 3
+    per_stage = {}
+    for name in STAGES:
+        tot, nl = stages[name]
+        if nl == 0 and name != "clear":
+            continue
+        bp, bn = ALG_BYTES.get(name, (0, 0))
+        alg = bp * np_ + bn * ncell
+        per_stage[name] = {"ms_per_step": tot / args.steps, "launches": nl,
+                           "alg_GBps": (alg * args.steps / (tot / 1e3) / 1e9) if tot > 0 else None}
+    dom = max((s for s in per_stage if s != "clear"), key=lambda s: per_stage[s]["ms_per_step"])
+    tot, nl = stages[dom]
+    bp, bn = ALG_BYTES[dom]
+    # per-launch algorithmic bytes / per-launch duration (scan = 3 launches -> per stage call)
+    calls = args.steps
+    alg_per_call = bp * np_ + bn * ncell
+    achieved = alg_per_call / (tot / calls / 1e3) / 1e9
+    peaks = measured_peaks()
+    peak = peaks.get("hbm_gbs") or 6650.0
+    cfg_name = f"landau3d_{n}^3x{ppc}ppc_fft"
+    traffic = ncu_traffic(cfg_name)
+    roof = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
+            "frac": achieved / peak, "traffic": traffic,
+            "peak_source": "measured (MEASURED_PEAKS.json hbm_gbs)" if peaks.get("hbm_gbs") else "fallback 6650 GB/s",
+            "alg_bytes_per_launch": alg_per_call}
+
+    cpu = None if args.no_cpu_baseline else oracle_sample(steps=args.cpu_steps)
+    if cpu:
+        cpu["sample"] = cpu["sample"].replace("{n}", str(n))
+    launches = sim.launches_per_step() * args.steps
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": cfg_name, "grid": n, "ppc": ppc, "particles_per_rank": np_,
+                   "k": 0.5, "alpha": 0.05, "dt": 0.05,
+                   "parallelism": "1 GPU" if world == 1 else f"{world} independent replicas",
+                   "l2": "inputs larger than L2 (particle state 48 B x N_p per rank)"},
+        "roofline": roof,
+        "cpu_baseline": cpu,
+        "e2e": e2e,
+        "gpu_launches": launches,
+        "clocks": clk.summary(),
+        "stages": per_stage,
+        "w_x_first_last": [float(ex[0]), float(ex[-1])],
+    }
+    print(json.dumps(line), flush=True)
+    sim.close()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--n", type=int, default=512)
+    ap.add_argument("--ppc", type=int, default=8)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-steps", type=int, default=20)
+    args = ap.parse_args()
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if args.impl == "reference":
+        return run_reference(args, rank, world)
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+
+        torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", 0)))
+        dist.init_process_group("nccl")
+    rc = run_ours(args, rank, world)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.destroy_process_group()
+    return rc
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,154 @@
+/*
+ * pic.h -- C ABI of the B200-native electrostatic PIC hot path
+ * (arxiv 2605.05469, "A Comparison of Massively Parallel Performance Portable
+ * Particle-in-Cell schemes ...", FFT pseudo-spectral PIC for 3D Landau damping).
+ *
+ * One call of pic_step() advances the PIC loop of PAPER.md Fig. 1:
+ *   SOLVE   rho -> E = F^-1(-i k F(rho)/|k|^2)
+ *   GATHER  E at the particles by CIC (same shape as scatter)
+ *   PUSH    v += (q/m) E dt ; x += v dt ; periodic wrap
+ *   SORT    stable counting sort of the particles by cell key   (BASELINE.json north_star)
+ *   SCATTER CIC charge deposit of the new positions
+ * for the Landau initial condition of P:140-146 in normalised units
+ * (eps0 = 1, q_e = -1, m_e = 1, mean density 1), fp64 throughout.
+ * "P:n" = PAPER.md line n, "S:n" = SPEC.md line n, "D#k" = DESIGN.md reading k.
+ *
+ * Conventions
+ *  - Every function returns PIC_OK (0) or a negative pic_status.  No exception
+ *    crosses the ABI and the library never prints.
+ *  - Device memory: the library allocates none.  The caller (PyTorch) owns one
+ *    workspace of pic_workspace_bytes() bytes on the current device and passes
+ *    it to pic_init(); it must stay alive until pic_free().
+ *  - Streams: every device operation is enqueued on the caller's stream
+ *    (a cudaStream_t passed as void*); pic_step() is asynchronous on it, except
+ *    that it copies the per-step energies to the host at the end (synchronous).
+ *  - A CUDA failure poisons the context: later calls return PIC_EPOISONED.
+ *  - Host buffers are plain host pointers (pageable or pinned), never retained.
+ *  - Grid arrays cross the ABI as [iz][iy][ix] row-major, N^3 doubles;
+ *    particle state as SoA [6][np] doubles (x, y, z, vx, vy, vz).
+ */
+#ifndef PIC_H
+#define PIC_H
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct pic_ctx pic_ctx;
+
+typedef enum {
+    PIC_OK = 0,
+    PIC_EINVAL = -1,       /* invalid argument (see pic_init)                      */
+    PIC_ENOMEM = -2,       /* workspace too small                                  */
+    PIC_ECUDA = -3,        /* a CUDA runtime call or kernel failed                 */
+    PIC_ENCCL = -4,        /* an NCCL call failed (multi-GPU)                      */
+    PIC_ENONFINITE = -5,   /* a field energy came out NaN/Inf                      */
+    PIC_EOVERFLOW = -6,    /* particle capacity exceeded                           */
+    PIC_EPOISONED = -7,    /* an earlier CUDA/NCCL error poisoned this context     */
+    PIC_EUNSUPPORTED = -8  /* valid request this build does not implement          */
+} pic_status;
+
+typedef struct {
+    int32_t  n;         /* cells per dimension (grid N^3); power of two, 16..1024     */
+    int32_t  ppc;       /* particles per cell, > 0; N_p = ppc * N^3 (Table 2)  */
+    double   k;         /* perturbation wavenumber, default 0.5               */
+    double   length;    /* domain length L; 0 => 2 pi / k (D#1)                */
+    double   alpha;     /* perturbation amplitude, 0 <= alpha < 1; default 0.05 */
+    double   dt;        /* time step > 0; default 0.05 (D#9)                   */
+    uint64_t seed;      /* Philox4x32-10 key of the initial sampler (D#10)            */
+    int32_t  half_kick; /* 1: v stored at half steps, backward half kick at init */
+    int32_t  pgrid[2];  /* {Py, Pz} rank grid; must be {1, 1} in this build           */
+} pic_params;
+
+/* Fill *p with the Landau-damping defaults of P:146 (N=16, ppc=8, k=0.5, alpha=0.05,
+ * dt=0.05, L=2 pi/k, seed=1, half_kick=1, pgrid={1,1}). */
+pic_status pic_params_default(pic_params *p);
+
+/* Bytes of device workspace pic_init needs for these parameters (rank/nranks as in
+ * pic_init).  PIC_EINVAL on invalid parameters. */
+pic_status pic_workspace_bytes(const pic_params *p, int32_t rank, int32_t nranks, size_t *bytes);
+
+/* Create a context and the Landau initial state: positions by inverse
+ * CDF (Newton) of (1 + alpha cos k x)/L per dimension, velocities N(0,1)^3 by
+ * Box-Muller, Philox counter = particle index; particles sorted by cell key and
+ * the charge deposited; optional backward half kick v <- v - (q/m) E dt/2.
+ *   nccl_id   : NULL when nranks == 1 (only nranks == 1 in this build).
+ *   workspace : device pointer, >= pic_workspace_bytes(), caller-owned.
+ *   cuda_stream: cudaStream_t (void*); NULL = legacy default stream.
+ * PIC_EINVAL: alpha not in [0,1), ppc <= 0, N not a power of two in [16,1024],
+ *   k <= 0, dt <= 0, k L / 2 pi not a positive integer, N_p >= 2^32, bad pgrid/rank.
+ * PIC_ENOMEM: workspace_bytes too small.  PIC_ECUDA: a kernel failed. */
+pic_status pic_init(const pic_params *p, int32_t rank, int32_t nranks, const uint8_t *nccl_id,
+                    void *workspace, size_t workspace_bytes, void *cuda_stream, pic_ctx **out);
+
+/* Advance nsteps PIC steps.  ex_energy (nullable, nsteps doubles, host) receives
+ * W_x(t_n) = 1/2 h^3 sum_nodes E_x^2 of the field solved at the start of each
+ * step; t_n = n dt.  PIC_ENONFINITE if an energy is NaN/Inf. */
+pic_status pic_step(pic_ctx *ctx, int32_t nsteps, double *ex_energy);
+
+/* W_x and W = 1/2 h^3 sum |E|^2 of the latest solve (synchronises the stream). */
+pic_status pic_field_energy(pic_ctx *ctx, double *ex_energy, double *total_energy);
+
+/* Destroy the context (NULL-safe).  Never frees the caller's workspace. */
+void pic_free(pic_ctx *ctx);
+
+/* Text of the last error of ctx; NULL ctx => this thread's last pic_init error. */
+const char *pic_last_error(const pic_ctx *ctx);
+
+/* ---- host-buffer and test/bench entry points (same library, stable ABI) ---- */
+
+/* Number of particles held by this context. */
+pic_status pic_num_particles(pic_ctx *ctx, int64_t *np);
+
+/* Copy the particle state to host xyzuvw[6][np] in canonical order (sorted by
+ * cell key, ties by the current order).  Synchronous. */
+pic_status pic_get_particles(pic_ctx *ctx, double *xyzuvw, int64_t np);
+
+/* Replace the particle state from host xyzuvw[6][np] (np must equal the context's
+ * N_p; every coordinate in [0, L)).  The state is interpreted as (x_n, v_{n-1/2})
+ * (no half kick); it is sorted by cell key (stable: ties keep the given order) and
+ * deposited.  With stream-ordered host copies; synchronous. */
+pic_status pic_set_particles(pic_ctx *ctx, const double *xyzuvw, int64_t np);
+
+/* Copy a grid to host [N][N][N]: which = 0 -> rho (charge density of the current
+ * positions, q/h^3 scaled); 1, 2, 3 -> E_x, E_y, E_z of the latest solve. */
+pic_status pic_get_grid(pic_ctx *ctx, int32_t which, double *host);
+
+/* Solve for an injected charge density rho_host[N^3] (true density, not
+ * scaled) and return E_host[3][N^3] and the energies.  Does not touch the
+ * particles, but overwrites the context's field and charge buffers. */
+pic_status pic_solve_injected(pic_ctx *ctx, const double *rho_host, double *E_host,
+                              double *ex_energy, double *total_energy);
+
+/* One gather+push+sort+deposit with an injected field E_host[3][N^3] instead of
+ * the solved one (the solve is skipped).  For bit-exact push parity tests. */
+pic_status pic_push_injected(pic_ctx *ctx, const double *E_host);
+
+/* Cell keys (uint32, of the current positions in canonical order) and the
+ * permutation of the latest sort (perm[i] = pre-sort index of the particle now
+ * at i).  Either pointer may be NULL. */
+pic_status pic_get_keys_perm(pic_ctx *ctx, uint32_t *keys, uint32_t *perm);
+
+/* Per-stage device time (CUDA events on the context's stream), accumulated since
+ * the last reset, in ms: stages[PIC_NSTAGES], launches[PIC_NSTAGES] (nullable).
+ * Timing is off until pic_set_timing(ctx, 1). */
+enum {
+    PIC_STAGE_FFT_X_FWD = 0, PIC_STAGE_FFT_Y_FWD, PIC_STAGE_FFT_Z_MUL, PIC_STAGE_FFT_Y_INV,
+    PIC_STAGE_FFT_X_INV, PIC_STAGE_ENERGY, PIC_STAGE_CLEAR, PIC_STAGE_PUSH_KEY,
+    PIC_STAGE_SCAN, PIC_STAGE_PLACE, PIC_STAGE_REORDER_DEPOSIT, PIC_NSTAGES
+};
+pic_status pic_set_timing(pic_ctx *ctx, int32_t enable);
+pic_status pic_get_timings(pic_ctx *ctx, double *ms, int64_t *launches);
+pic_status pic_reset_timings(pic_ctx *ctx);
+/* Name of a stage (static string) or NULL. */
+const char *pic_stage_name(int32_t stage);
+
+/* Number of kernel launches one pic_step(ctx, 1) makes (for the bench's count). */
+pic_status pic_launches_per_step(pic_ctx *ctx, int64_t *launches);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PIC_H */

@@ -1,0 +1,225 @@
+"""Thin ctypes binding of libpic.so (include/pic.h): argument marshalling only.
+
+Every step of the PIC path runs in the CUDA kernels behind the C ABI; this
+module converts Python/numpy/torch arguments to pointers and status codes to
+exceptions.  PyTorch supplies the device workspace and the stream.  There is no
+fallback: if libpic.so is missing or fails to load, importing the product path
+raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libpic.so")
+
+PIC_OK, PIC_EINVAL, PIC_ENOMEM, PIC_ECUDA, PIC_ENCCL = 0, -1, -2, -3, -4
+PIC_ENONFINITE, PIC_EOVERFLOW, PIC_EPOISONED, PIC_EUNSUPPORTED = -5, -6, -7, -8
+STATUS_NAMES = {0: "PIC_OK", -1: "PIC_EINVAL", -2: "PIC_ENOMEM", -3: "PIC_ECUDA", -4: "PIC_ENCCL",
+                -5: "PIC_ENONFINITE", -6: "PIC_EOVERFLOW", -7: "PIC_EPOISONED",
+                -8: "PIC_EUNSUPPORTED"}
+
+STAGES = ["fft_x_fwd", "fft_y_fwd", "fft_z_mul", "fft_y_inv", "fft_x_inv", "energy", "clear",
+          "push_key", "scan", "place", "reorder_deposit"]
+PIC_NSTAGES = len(STAGES)
+
+
+class pic_params(C.Structure):
+    _fields_ = [
+        ("n", C.c_int32),
+        ("ppc", C.c_int32),
+        ("k", C.c_double),
+        ("length", C.c_double),
+        ("alpha", C.c_double),
+        ("dt", C.c_double),
+        ("seed", C.c_uint64),
+        ("half_kick", C.c_int32),
+        ("pgrid", C.c_int32 * 2),
+    ]
+
+
+class PicError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"{STATUS_NAMES.get(status, status)}: {msg}")
+        self.status = status
+
+
+# Every symbol include/pic.h declares, with (restype, argtypes).
+_vp = C.c_void_p
+_dp = C.POINTER(C.c_double)
+_u32p = C.POINTER(C.c_uint32)
+_i64p = C.POINTER(C.c_int64)
+SYMBOLS = {
+    "pic_params_default": (C.c_int, [C.POINTER(pic_params)]),
+    "pic_workspace_bytes": (C.c_int, [C.POINTER(pic_params), C.c_int32, C.c_int32, C.POINTER(C.c_size_t)]),
+    "pic_init": (C.c_int, [C.POINTER(pic_params), C.c_int32, C.c_int32, _vp, _vp, C.c_size_t, _vp,
+                           C.POINTER(_vp)]),
+    "pic_step": (C.c_int, [_vp, C.c_int32, _dp]),
+    "pic_field_energy": (C.c_int, [_vp, _dp, _dp]),
+    "pic_free": (None, [_vp]),
+    "pic_last_error": (C.c_char_p, [_vp]),
+    "pic_num_particles": (C.c_int, [_vp, _i64p]),
+    "pic_get_particles": (C.c_int, [_vp, _dp, C.c_int64]),
+    "pic_set_particles": (C.c_int, [_vp, _dp, C.c_int64]),
+    "pic_get_grid": (C.c_int, [_vp, C.c_int32, _dp]),
+    "pic_solve_injected": (C.c_int, [_vp, _dp, _dp, _dp, _dp]),
+    "pic_push_injected": (C.c_int, [_vp, _dp]),
+    "pic_get_keys_perm": (C.c_int, [_vp, _u32p, _u32p]),
+    "pic_set_timing": (C.c_int, [_vp, C.c_int32]),
+    "pic_get_timings": (C.c_int, [_vp, _dp, _i64p]),
+    "pic_reset_timings": (C.c_int, [_vp]),
+    "pic_stage_name": (C.c_char_p, [C.c_int32]),
+    "pic_launches_per_step": (C.c_int, [_vp, _i64p]),
+}
+
+_lib = None
+
+
+def lib() -> C.CDLL:
+    """Load libpic.so (raises if it is missing: there is no fallback path)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} not built: run __graft_entry__.build()")
+        L = C.CDLL(LIB_PATH)
+        for name, (res, args) in SYMBOLS.items():
+            f = getattr(L, name)
+            f.restype = res
+            f.argtypes = args
+        _lib = L
+    return _lib
+
+
+def _check(st: int, ctx=None):
+    if st != PIC_OK:
+        msg = lib().pic_last_error(ctx)
+        raise PicError(st, msg.decode() if msg else "")
+
+
+def _d(a: np.ndarray):
+    assert a.dtype == np.float64 and a.flags.c_contiguous
+    return a.ctypes.data_as(_dp)
+
+
+def default_params(**kw) -> pic_params:
+    p = pic_params()
+    _check(lib().pic_params_default(C.byref(p)))
+    for k, v in kw.items():
+        if k == "pgrid":
+            p.pgrid[0], p.pgrid[1] = v
+        else:
+            setattr(p, k, v)
+    return p
+
+
+def workspace_bytes(p: pic_params, rank: int = 0, nranks: int = 1) -> int:
+    b = C.c_size_t()
+    _check(lib().pic_workspace_bytes(C.byref(p), rank, nranks, C.byref(b)))
+    return b.value
+
+
+class Simulation:
+    """One rank of the PIC simulation on the current CUDA device.
+
+    ``workspace`` is a torch uint8 CUDA tensor owned by this object; the stream
+    is torch's current stream at construction.
+    """
+
+    def __init__(self, n=16, ppc=8, k=0.5, alpha=0.05, dt=0.05, seed=1, half_kick=True,
+                 length=0.0, device=None):
+        import torch
+
+        self.params = default_params(n=n, ppc=ppc, k=k, alpha=alpha, dt=dt, seed=seed,
+                                     half_kick=int(bool(half_kick)), length=length)
+        self.device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+        nbytes = workspace_bytes(self.params)
+        with torch.cuda.device(self.device):
+            self.workspace = torch.empty(nbytes, dtype=torch.uint8, device=self.device)
+            self.stream = torch.cuda.current_stream(self.device)
+        ctx = C.c_void_p()
+        _check(lib().pic_init(C.byref(self.params), 0, 1, None, C.c_void_p(self.workspace.data_ptr()),
+                              nbytes, C.c_void_p(self.stream.cuda_stream), C.byref(ctx)))
+        self.ctx = ctx
+        n64 = C.c_int64()
+        _check(lib().pic_num_particles(self.ctx, C.byref(n64)), self.ctx)
+        self.np = n64.value
+        self.n = n
+        self.L = length if length else 2 * np.pi / k
+
+    # -- core --------------------------------------------------------------
+    def step(self, nsteps: int = 1) -> np.ndarray:
+        ex = np.zeros(max(nsteps, 1))
+        _check(lib().pic_step(self.ctx, nsteps, _d(ex)), self.ctx)
+        return ex[:nsteps]
+
+    def field_energy(self):
+        a, b = C.c_double(), C.c_double()
+        _check(lib().pic_field_energy(self.ctx, C.byref(a), C.byref(b)), self.ctx)
+        return a.value, b.value
+
+    # -- host buffers ------------------------------------------------------
+    def get_particles(self, out: np.ndarray | None = None) -> np.ndarray:
+        if out is None:
+            out = np.zeros((6, self.np))
+        assert out.shape == (6, self.np)
+        _check(lib().pic_get_particles(self.ctx, _d(out), self.np), self.ctx)
+        return out
+
+    def set_particles(self, xv: np.ndarray):
+        xv = np.ascontiguousarray(xv, dtype=np.float64)
+        assert xv.shape == (6, self.np)
+        _check(lib().pic_set_particles(self.ctx, _d(xv), self.np), self.ctx)
+
+    def get_grid(self, which: int) -> np.ndarray:
+        out = np.zeros((self.n, self.n, self.n))
+        _check(lib().pic_get_grid(self.ctx, which, _d(out)), self.ctx)
+        return out
+
+    def solve_injected(self, rho: np.ndarray):
+        rho = np.ascontiguousarray(rho, dtype=np.float64)
+        E = np.zeros((3, self.n, self.n, self.n))
+        a, b = C.c_double(), C.c_double()
+        _check(lib().pic_solve_injected(self.ctx, _d(rho), _d(E), C.byref(a), C.byref(b)), self.ctx)
+        return E, a.value, b.value
+
+    def push_injected(self, E: np.ndarray):
+        E = np.ascontiguousarray(E, dtype=np.float64)
+        _check(lib().pic_push_injected(self.ctx, _d(E)), self.ctx)
+
+    def keys_perm(self):
+        k = np.zeros(self.np, dtype=np.uint32)
+        p = np.zeros(self.np, dtype=np.uint32)
+        _check(lib().pic_get_keys_perm(self.ctx, k.ctypes.data_as(_u32p), p.ctypes.data_as(_u32p)), self.ctx)
+        return k, p
+
+    # -- timing ------------------------------------------------------------
+    def set_timing(self, on: bool = True):
+        _check(lib().pic_set_timing(self.ctx, int(on)), self.ctx)
+
+    def timings(self):
+        ms = np.zeros(PIC_NSTAGES)
+        la = np.zeros(PIC_NSTAGES, dtype=np.int64)
+        _check(lib().pic_get_timings(self.ctx, _d(ms), la.ctypes.data_as(_i64p)), self.ctx)
+        return {STAGES[i]: (ms[i], int(la[i])) for i in range(PIC_NSTAGES)}
+
+    def reset_timings(self):
+        _check(lib().pic_reset_timings(self.ctx), self.ctx)
+
+    def launches_per_step(self) -> int:
+        v = C.c_int64()
+        _check(lib().pic_launches_per_step(self.ctx, C.byref(v)), self.ctx)
+        return v.value
+
+    def close(self):
+        if getattr(self, "ctx", None):
+            lib().pic_free(self.ctx)
+            self.ctx = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

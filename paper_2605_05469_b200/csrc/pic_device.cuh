@@ -1,0 +1,154 @@
+// pic_device.cuh -- device-side helpers of the PIC hot path (sm_100a).
+//
+// Arithmetic that must be bit-identical between the two places it runs (the
+// push-key pass and the reorder-push-deposit pass recompute the same push) is
+// written once here with explicit round-to-nearest intrinsics, so no
+// contraction choice of the compiler can change a result (D#17).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace pic {
+
+// Grid geometry and step constants, passed by value to every kernel.
+struct Geom {
+    int n;          // cells per dimension (power of two)
+    int nmask;      // n - 1
+    int px;         // complex pitch of a spectral row: round_up(n/2 + 1, 8)
+    int rp;         // real pitch of a grid row in doubles: 2 * px
+    double L;       // domain length
+    double inv_h;   // (double)n / L  (D#5)
+    double dt;      // time step
+    double qm_dt;   // (q/m) dt = -dt
+};
+
+// Index of node (ix, iy, iz) in a pitched real grid [n][n][rp].
+__device__ __forceinline__ int64_t gidx(const Geom& g, int ix, int iy, int iz) {
+    return ((int64_t)iz * g.n + iy) * g.rp + ix;
+}
+
+// Cell index along one dimension: floor(x * inv_h), clamped to [0, n-1] (D#5).
+__device__ __forceinline__ int cell_of(double s, int n) {
+    int i = (int)floor(s);
+    i = i > n - 1 ? n - 1 : i;
+    return i < 0 ? 0 : i;
+}
+
+// Morton key (x fastest) of cell (ix, iy, iz), n <= 1024 (D#14).
+__device__ __forceinline__ uint32_t spread3(uint32_t v) {
+    v &= 0x3ffu;
+    v = (v | (v << 16)) & 0x030000FFu;
+    v = (v | (v << 8)) & 0x0300F00Fu;
+    v = (v | (v << 4)) & 0x030C30C3u;
+    v = (v | (v << 2)) & 0x09249249u;
+    return v;
+}
+__device__ __forceinline__ uint32_t compact3(uint32_t v) {
+    v &= 0x09249249u;
+    v = (v ^ (v >> 2)) & 0x030C30C3u;
+    v = (v ^ (v >> 4)) & 0x0300F00Fu;
+    v = (v ^ (v >> 8)) & 0x030000FFu;
+    v = (v ^ (v >> 16)) & 0x000003FFu;
+    return v;
+}
+__device__ __forceinline__ uint32_t morton(int ix, int iy, int iz) {
+    return spread3(ix) | (spread3(iy) << 1) | (spread3(iz) << 2);
+}
+__device__ __forceinline__ void unmorton(uint32_t k, int& ix, int& iy, int& iz) {
+    ix = (int)compact3(k);
+    iy = (int)compact3(k >> 1);
+    iz = (int)compact3(k >> 2);
+}
+
+// Periodic wrap into [0, L).
+__device__ __forceinline__ double wrap(double x, double L) {
+    if (x >= L) {
+        x = __dsub_rn(x, L);
+    } else if (x < 0.0) {
+        x = __dadd_rn(x, L);
+        if (x >= L) x = 0.0;
+    }
+    return x;
+}
+
+__device__ __forceinline__ uint32_t key_of(const Geom& g, const double x[3]) {
+    int i0 = cell_of(__dmul_rn(x[0], g.inv_h), g.n);
+    int i1 = cell_of(__dmul_rn(x[1], g.inv_h), g.n);
+    int i2 = cell_of(__dmul_rn(x[2], g.inv_h), g.n);
+    return morton(i0, i1, i2);
+}
+
+// CIC weights of one position: cell index i[d] and w[d][0] = 1 - f, w[d][1] = f,
+// f = x inv_h - i.
+__device__ __forceinline__ void cic_weights(const Geom& g, const double x[3], int i[3],
+                                            double w[3][2]) {
+#pragma unroll
+    for (int d = 0; d < 3; ++d) {
+        double s = __dmul_rn(x[d], g.inv_h);
+        i[d] = cell_of(s, g.n);
+        double f = __dsub_rn(s, (double)i[d]);
+        w[d][0] = __dsub_rn(1.0, f);
+        w[d][1] = f;
+    }
+}
+
+// CIC gather of E at x (corner order z outer, y, x inner; fma accumulation
+// from 0: S:141-149, D#17).
+__device__ __forceinline__ void gather_E(const Geom& g, const double* __restrict__ Ex,
+                                         const double* __restrict__ Ey,
+                                         const double* __restrict__ Ez, const double x[3],
+                                         double ep[3]) {
+    int i[3];
+    double w[3][2];
+    cic_weights(g, x, i, w);
+    double a0 = 0.0, a1 = 0.0, a2 = 0.0;
+#pragma unroll
+    for (int c = 0; c < 2; ++c) {
+#pragma unroll
+        for (int b = 0; b < 2; ++b) {
+            const int64_t row = ((int64_t)((i[2] + c) & g.nmask) * g.n + ((i[1] + b) & g.nmask)) * g.rp;
+#pragma unroll
+            for (int a = 0; a < 2; ++a) {
+                const double wt = __dmul_rn(__dmul_rn(w[0][a], w[1][b]), w[2][c]);
+                const int64_t m = row + ((i[0] + a) & g.nmask);
+                a0 = __fma_rn(wt, __ldg(Ex + m), a0);
+                a1 = __fma_rn(wt, __ldg(Ey + m), a1);
+                a2 = __fma_rn(wt, __ldg(Ez + m), a2);
+            }
+        }
+    }
+    ep[0] = a0;
+    ep[1] = a1;
+    ep[2] = a2;
+}
+
+// Gather + leapfrog kick-drift + wrap:
+//   v <- fma(qm_dt, E_p, v) ; x <- wrap(fma(v, dt, x)).
+__device__ __forceinline__ void gather_push(const Geom& g, const double* __restrict__ Ex,
+                                            const double* __restrict__ Ey,
+                                            const double* __restrict__ Ez, double x[3],
+                                            double v[3]) {
+    double ep[3];
+    gather_E(g, Ex, Ey, Ez, x, ep);
+#pragma unroll
+    for (int d = 0; d < 3; ++d) {
+        v[d] = __fma_rn(g.qm_dt, ep[d], v[d]);
+        x[d] = wrap(__fma_rn(v[d], g.dt, x[d]), g.L);
+    }
+}
+
+// ---------------------------------------------------------------- Philox ----
+// Philox4x32-10 (D#10): counter (j lo, j hi, b, 0), key (seed lo, seed hi).
+__device__ __forceinline__ void philox4x32_10(uint32_t c[4], uint32_t k0, uint32_t k1) {
+#pragma unroll
+    for (int r = 0; r < 10; ++r) {
+        const uint32_t lo0 = 0xD2511F53u * c[0], hi0 = __umulhi(0xD2511F53u, c[0]);
+        const uint32_t lo1 = 0xCD9E8D57u * c[2], hi1 = __umulhi(0xCD9E8D57u, c[2]);
+        const uint32_t n0 = hi1 ^ c[1] ^ k0, n2 = hi0 ^ c[3] ^ k1;
+        c[0] = n0; c[1] = lo1; c[2] = n2; c[3] = lo0;
+        k0 += 0x9E3779B9u;
+        k1 += 0xBB67AE85u;
+    }
+}
+
+}  // namespace pic

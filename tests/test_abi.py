@@ -1,0 +1,70 @@
+"""CPU-side checks of the C ABI library: it loads, exports every symbol
+include/pic.h declares, and its host-only entry points (parameter validation,
+workspace sizing) behave as documented.  No compute call needs a GPU here."""
+import os
+import re
+
+import pytest
+
+import paper_2605_05469_b200 as pkg
+from paper_2605_05469_b200 import _binding as B
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _declared_functions():
+    src = open(os.path.join(ROOT, "include", "pic.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(pic_[a-z_]+)\s*\(", src)))
+
+
+def test_header_declares_and_library_exports_every_symbol():
+    pkg.build_lib()
+    L = pkg.lib()
+    names = _declared_functions()
+    assert len(names) >= 15
+    for name in names:
+        assert hasattr(L, name), name
+        assert name in B.SYMBOLS, f"binding lacks {name}"
+
+
+def test_defaults_follow_the_paper():
+    p = B.default_params()
+    assert (p.n, p.ppc, p.k, p.alpha, p.dt, p.half_kick) == (16, 8, 0.5, 0.05, 0.05, 1)
+    assert tuple(p.pgrid) == (1, 1) and p.length == 0.0
+
+
+@pytest.mark.parametrize("bad", [
+    dict(n=12), dict(n=8), dict(n=2048), dict(ppc=0), dict(alpha=1.0), dict(alpha=-0.1),
+    dict(k=0.0), dict(dt=0.0), dict(length=5.0), dict(n=1024, ppc=8),
+])
+def test_invalid_parameters_rejected(bad):
+    p = B.default_params(**bad)
+    with pytest.raises(B.PicError) as e:
+        B.workspace_bytes(p)
+    assert e.value.status == B.PIC_EINVAL
+
+
+def test_multi_rank_request_is_reported():
+    p = B.default_params()
+    with pytest.raises(B.PicError) as e:
+        B.workspace_bytes(p, rank=0, nranks=2)
+    assert e.value.status in (B.PIC_EUNSUPPORTED, B.PIC_EINVAL)
+
+
+def test_workspace_bytes_model():
+    """Workspace = 2 x 48 B/particle state + 10 B/particle key/rank/perm + cell arrays + 4 grids."""
+    p = B.default_params(n=512, ppc=8)
+    b = B.workspace_bytes(p)
+    np_ = 8 * 512 ** 3
+    assert 106 * np_ <= b <= 106 * np_ + 6 * 2 ** 30
+    assert b < 170 * 2 ** 30     # fits one B200 (183 GB)
+    p = B.default_params(n=16, ppc=8, length=8 * 3.141592653589793)   # kL/2pi = 2
+    assert B.workspace_bytes(p) > 0
+
+
+def test_stage_names():
+    L = pkg.lib()
+    for i, s in enumerate(B.STAGES):
+        assert L.pic_stage_name(i).decode() == s
+    assert L.pic_stage_name(len(B.STAGES)) is None
