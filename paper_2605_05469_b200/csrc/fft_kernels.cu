@@ -95,9 +95,8 @@ __host__ __device__ inline int y_tw(int n) { int t = 4096 / n; return t > 8 ? 8 
 __host__ __device__ inline int z_tw(int n) { int t = 2048 / n; return t > 8 ? 8 : (t < 1 ? 1 : t); }
 
 // ------------------------------------------------------------ x R2C -------
-// Row r: n reals of `in` -> n/2 + 1 complex of `out` (same pitched row).
-__global__ void __launch_bounds__(kThreads) k_fft_x_fwd(Geom g, const double* __restrict__ in,
-                                                        double* __restrict__ out,
+// Row r of S0: n reals -> n/2 + 1 complex, in place (the CTA owns its rows).
+__global__ void __launch_bounds__(kThreads) k_fft_x_fwd(Geom g, double* buf,
                                                         const double2* __restrict__ tw) {
     extern __shared__ double2 sm[];
     const int len = g.n >> 1, logn = ilog2(len), R = x_rows(g.n), ls = len + 1;
@@ -106,7 +105,7 @@ __global__ void __launch_bounds__(kThreads) k_fft_x_fwd(Geom g, const double* __
     const int rows = (int)min((int64_t)R, nrows - row0);
     for (int t = threadIdx.x; t < rows * len; t += blockDim.x) {
         const int rl = t / len, m = t - rl * len;
-        const double2* src = reinterpret_cast<const double2*>(in + (row0 + rl) * g.rp);
+        const double2* src = reinterpret_cast<const double2*>(buf + (row0 + rl) * g.rp);
         sm[rl * ls + brev(m, logn)] = src[m];
     }
     __syncthreads();
@@ -122,7 +121,7 @@ __global__ void __launch_bounds__(kThreads) k_fft_x_fwd(Geom g, const double* __
         double2 X;
         if (k == len) X = csub(ze, zo);
         else X = cadd(ze, cmul(__ldg(tw + k), zo));
-        reinterpret_cast<double2*>(out + (row0 + rl) * g.rp)[k] = X;
+        reinterpret_cast<double2*>(buf + (row0 + rl) * g.rp)[k] = X;
     }
 }
 
@@ -153,12 +152,13 @@ __global__ void __launch_bounds__(kThreads) k_fft_y(Geom g, double* b0, double* 
 // --------------------------------------------------- z pass + multiply -----
 // blockIdx.x = ky * ntiles + tile.  Forward z FFT of rho^, then for d = x, y, z:
 // E^_d = -i k_d rho^ / |k|^2 * scale (zero at n = 0 and where n_d = -N/2, D#6),
-// inverse z FFT, store into E[d]'s spectrum.
-__global__ void __launch_bounds__(kThreads) k_fft_z_mul(Geom g, const double2* rho,
-                                                        double2* e0, double2* e1, double2* e2,
-                                                        double scale, const double2* __restrict__ tw) {
+// inverse z FFT, store: E^_x -> S1, E^_y -> S2, E^_z -> S0 (the CTA's own input
+// tile, already staged in shared memory).
+__global__ void __launch_bounds__(kThreads) k_fft_z_mul(Geom g, double2* rho, double2* e1,
+                                                        double2* e2, double scale,
+                                                        const double2* __restrict__ tw) {
     extern __shared__ double2 sm[];
-    double2* out[3] = {e0, e1, e2};
+    double2* out[3] = {e1, e2, rho};
     const int n = g.n, logn = ilog2(n), TW = z_tw(n), ls = n + 1;
     double2* s1 = sm;
     double2* s2 = sm + TW * ls;
@@ -205,45 +205,74 @@ __global__ void __launch_bounds__(kThreads) k_fft_z_mul(Geom g, const double2* r
 }
 
 // ------------------------------------------------------------ x C2R -------
-// blockIdx.y = component d.  Row: n/2 + 1 complex -> n reals (in place);
-// per-CTA partial sum of E_d^2 -> partials[d * gridDim.x + blockIdx.x].
-__global__ void __launch_bounds__(kThreads) k_fft_x_inv(Geom g, double* b0, double* b1, double* b2,
+// R rows of all three components per CTA: n/2 + 1 complex -> n reals each,
+// written as node records E4[row][x] = (E_x, E_y, E_z, 0) with 256-bit stores;
+// per-CTA partial sums of E_d^2 -> partials[d * gridDim.x + blockIdx.x].
+__host__ __device__ inline int xi_rows(int n) { int r = 1024 / (n / 2); return r < 1 ? 1 : r; }
+
+__device__ __forceinline__ void st_node(double* p, double a, double b, double c) {
+    asm volatile("st.global.v4.f64 [%0], {%1, %2, %3, %4};" ::"l"(p), "d"(a), "d"(b), "d"(c), "d"(0.0)
+                 : "memory");
+}
+
+__global__ void __launch_bounds__(kThreads) k_fft_x_inv(Geom g, const double* b0, const double* b1,
+                                                        const double* b2, double* __restrict__ E4,
                                                         const double2* __restrict__ tw,
                                                         double* __restrict__ partials) {
     extern __shared__ double2 sm[];
-    __shared__ double red[kThreads / 32];
-    double* buf = blockIdx.y == 0 ? b0 : (blockIdx.y == 1 ? b1 : b2);
-    const int len = g.n >> 1, logn = ilog2(len), R = x_rows(g.n), ls = len + 1;
+    __shared__ double red[3][kThreads / 32];
+    const int len = g.n >> 1, logn = ilog2(len), R = xi_rows(g.n), ls = len + 1;
     const int64_t row0 = (int64_t)blockIdx.x * R;
     const int rows = (int)min((int64_t)R, (int64_t)g.n * g.n - row0);
     // Z[k] = (X[k] + conj X[len-k]) + i (X[k] - conj X[len-k]) W_n^{-k}, k < len
-    for (int t = threadIdx.x; t < rows * len; t += blockDim.x) {
-        const int rl = t / len, k = t - rl * len;
+    for (int t = threadIdx.x; t < 3 * rows * len; t += blockDim.x) {
+        const int l = t / len, k = t - l * len;           // line l = d * rows + rl
+        const int d = l / rows, rl = l - d * rows;
+        const double* buf = d == 0 ? b0 : (d == 1 ? b1 : b2);
         const double2* X = reinterpret_cast<const double2*>(buf + (row0 + rl) * g.rp);
         const double2 xk = X[k], xc = conj2(X[len - k]);
         const double2 ze = cadd(xk, xc);
         const double2 zo = cmul(csub(xk, xc), conj2(__ldg(tw + k)));
-        sm[rl * ls + brev(k, logn)] = make_double2(ze.x - zo.y, ze.y + zo.x);
+        sm[l * ls + brev(k, logn)] = make_double2(ze.x - zo.y, ze.y + zo.x);
     }
     __syncthreads();
-    smem_fft<+1>(sm, rows, logn, ls, tw, 1);
-    double e2 = 0.0;
+    smem_fft<+1>(sm, 3 * rows, logn, ls, tw, 1);
+    double e2[3] = {0.0, 0.0, 0.0};
     for (int t = threadIdx.x; t < rows * len; t += blockDim.x) {
         const int rl = t / len, m = t - rl * len;
-        const double2 v = sm[rl * ls + m];
-        reinterpret_cast<double2*>(buf + (row0 + rl) * g.rp)[m] = v;
-        e2 = fma(v.x, v.x, e2);
-        e2 = fma(v.y, v.y, e2);
+        const double2 vx = sm[(0 * rows + rl) * ls + m];
+        const double2 vy = sm[(1 * rows + rl) * ls + m];
+        const double2 vz = sm[(2 * rows + rl) * ls + m];
+        double* node = E4 + 4 * ((row0 + rl) * g.n + 2 * m);
+        st_node(node, vx.x, vy.x, vz.x);
+        st_node(node + 4, vx.y, vy.y, vz.y);
+        e2[0] = fma(vx.x, vx.x, fma(vx.y, vx.y, e2[0]));
+        e2[1] = fma(vy.x, vy.x, fma(vy.y, vy.y, e2[1]));
+        e2[2] = fma(vz.x, vz.x, fma(vz.y, vz.y, e2[2]));
     }
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) e2 += __shfl_xor_sync(0xffffffffu, e2, o);
-    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = e2;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        double s = 0.0;
-        for (int w = 0; w < kThreads / 32; ++w) s += red[w];
-        partials[(int64_t)blockIdx.y * gridDim.x + blockIdx.x] = s;
+    for (int d = 0; d < 3; ++d) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) e2[d] += __shfl_xor_sync(0xffffffffu, e2[d], o);
+        if ((threadIdx.x & 31) == 0) red[d][threadIdx.x >> 5] = e2[d];
     }
+    __syncthreads();
+    if (threadIdx.x < 3) {
+        double s = 0.0;
+        for (int w = 0; w < kThreads / 32; ++w) s += red[threadIdx.x][w];
+        partials[(int64_t)threadIdx.x * gridDim.x + blockIdx.x] = s;
+    }
+}
+
+__global__ void k_e4_extract(const double* __restrict__ E4, int64_t nn, int d, double* __restrict__ out) {
+    const int64_t m = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (m < nn) out[m] = E4[4 * m + d];
+}
+
+__global__ void k_e4_pack(const double* __restrict__ a, const double* __restrict__ b,
+                          const double* __restrict__ c, int64_t nn, double* __restrict__ E4) {
+    const int64_t m = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (m < nn) st_node(E4 + 4 * m, a[m], b[m], c[m]);
 }
 
 // One CTA, fixed summation order (deterministic): energies = (W_x, W).
@@ -276,14 +305,14 @@ __global__ void __launch_bounds__(1024) k_energy_reduce(Geom g, const double* __
 
 int energy_partials(const Geom& g) {
     const int64_t nrows = (int64_t)g.n * g.n;
-    return (int)((nrows + x_rows(g.n) - 1) / x_rows(g.n));
+    return (int)((nrows + xi_rows(g.n) - 1) / xi_rows(g.n));
 }
 
-void launch_fft_x_fwd(const Geom& g, const double* rho_buf, double* spec, const double2* tw,
-                      cudaStream_t s) {
+void launch_fft_x_fwd(const Geom& g, double* S0, const double2* tw, cudaStream_t s) {
     const int len = g.n / 2, R = x_rows(g.n);
     const size_t smem = sizeof(double2) * (size_t)R * (len + 1);
-    k_fft_x_fwd<<<energy_partials(g), kThreads, smem, s>>>(g, rho_buf, spec, tw);
+    const int64_t nrows = (int64_t)g.n * g.n;
+    k_fft_x_fwd<<<(unsigned)((nrows + R - 1) / R), kThreads, smem, s>>>(g, S0, tw);
 }
 
 void launch_fft_y(const Geom& g, double* const buf[3], int ncomp, int inverse, const double2* tw,
@@ -295,21 +324,30 @@ void launch_fft_y(const Geom& g, double* const buf[3], int ncomp, int inverse, c
     else k_fft_y<-1><<<grid, kThreads, smem, s>>>(g, buf[0], buf[1], buf[2], tw);
 }
 
-void launch_fft_z_mul(const Geom& g, const double* rho_buf, double* const E[3], double scale,
+void launch_fft_z_mul(const Geom& g, double* S0, double* S1, double* S2, double scale,
                       const double2* tw, cudaStream_t s) {
     const int TW = z_tw(g.n), ntiles = (g.n / 2 + 1 + TW - 1) / TW;
     const size_t smem = 2 * sizeof(double2) * (size_t)TW * (g.n + 1);
     k_fft_z_mul<<<g.n * ntiles, kThreads, smem, s>>>(
-        g, reinterpret_cast<const double2*>(rho_buf), reinterpret_cast<double2*>(E[0]),
-        reinterpret_cast<double2*>(E[1]), reinterpret_cast<double2*>(E[2]), scale, tw);
+        g, reinterpret_cast<double2*>(S0), reinterpret_cast<double2*>(S1),
+        reinterpret_cast<double2*>(S2), scale, tw);
 }
 
-void launch_fft_x_inv(const Geom& g, double* const E[3], const double2* tw, double* partials,
-                      cudaStream_t s) {
-    const int len = g.n / 2, R = x_rows(g.n);
-    const size_t smem = sizeof(double2) * (size_t)R * (len + 1);
-    dim3 grid(energy_partials(g), 3);
-    k_fft_x_inv<<<grid, kThreads, smem, s>>>(g, E[0], E[1], E[2], tw, partials);
+void launch_fft_x_inv(const Geom& g, const double* const spec[3], double* E4, const double2* tw,
+                      double* partials, cudaStream_t s) {
+    const int len = g.n / 2, R = xi_rows(g.n);
+    const size_t smem = 3 * sizeof(double2) * (size_t)R * (len + 1);
+    k_fft_x_inv<<<energy_partials(g), kThreads, smem, s>>>(g, spec[0], spec[1], spec[2], E4, tw, partials);
+}
+
+void launch_e4_extract(const Geom& g, const double* E4, int d, double* out, cudaStream_t s) {
+    const int64_t nn = (int64_t)g.n * g.n * g.n;
+    k_e4_extract<<<(unsigned)((nn + 255) / 256), 256, 0, s>>>(E4, nn, d, out);
+}
+
+void launch_e4_pack(const Geom& g, const double* const comp[3], double* E4, cudaStream_t s) {
+    const int64_t nn = (int64_t)g.n * g.n * g.n;
+    k_e4_pack<<<(unsigned)((nn + 255) / 256), 256, 0, s>>>(comp[0], comp[1], comp[2], nn, E4);
 }
 
 void launch_energy_reduce(const Geom& g, const double* partials, double* energies, cudaStream_t s) {

@@ -1,20 +1,20 @@
 // particle_kernels.cu -- particle side of the PIC step on sm_100a.
 //
-// One step (after the solve) is four kernels over HBM-resident SoA fp64 state:
-//   push_key : stream x, v in sorted order, gather E (CIC), push, key of the new
-//              cell, count[key] += 1.  Nothing but the 4-byte key is written.
+// Particle state lives in HBM as three streams of 128-bit pairs (pic_device.cuh):
+// (x, y), (z, v_z), (v_x, v_y).  One step (after the solve) is four kernels:
+//   push_key : stream the sorted particles, gather E (eight 256-bit node loads),
+//              kick v in place, drift to x' (not stored), key of the new cell,
+//              rank = count[key]++ (arrival order).
 //   scan     : offs = exclusive scan of count (3 kernels, 4096-cell tiles).
-//   place    : perm[atomicAdd(cursor[key[i]], 1)] = i.
-//   reorder_deposit : one CTA per Morton brick of 256 cells (8 x 8 x 4).  Sorts
-//              each cell's perm segment ascending (= the stable order), gathers
-//              x, v through perm, recomputes the identical push, streams x', v'
-//              sorted into the other buffer, and deposits the new charge: each
-//              thread owns one cell and sums its particles' 8 corner weights in
-//              registers, the brick combines them into a 9 x 9 x 5 node tile in
-//              shared memory in eight conflict-free passes, and the tile is
-//              flushed with one fp64 global reduction per node.
-// The push is computed twice (push_key, reorder_deposit) from bit-identical code
-// (pic_device.cuh) instead of writing x', v' twice: 48 B/particle less traffic.
+//   place    : perm[offs[key] + rank] = i (no atomics).
+//   reorder_deposit : one CTA per Morton brick of 256 cells (8 x 8 x 4): stable
+//              order inside each cell (D#14), gather x, v' through perm, the
+//              identical drift x' = wrap(x + v' dt), x', v' streamed to the stable
+//              slot, CIC charge summed per cell in registers, folded into a node
+//              tile in shared memory, one fp64 global reduction per node.
+// The drift is computed twice from bit-identical code (pic_device.cuh) instead of
+// storing x' in push_key (24 B/particle less traffic), and reorder_deposit does
+// no field gather at the scattered pre-sort positions.
 #include <algorithm>
 
 #include "kernels.h"
@@ -25,7 +25,8 @@ namespace {
 
 constexpr int kThreads = 256;
 constexpr int kBrick = 256;     // cells per reorder/deposit CTA (Morton 8 bits)
-constexpr int kCap = 4096;      // particles staged per chunk
+constexpr int kCap = 2048;      // particles staged per chunk (29 B of shared memory each)
+constexpr int kBatch = 2;       // particles per thread with loads in flight together
 
 // ---------------------------------------------------------------- init -----
 // Landau initial condition: x_d by Newton on the inverse CDF of
@@ -46,59 +47,133 @@ __global__ void __launch_bounds__(kThreads) k_sample(Geom g, PState st, int64_t 
         u[2 * b + 1] = (double)(w1 >> 11) * 0x1p-53;
     }
     const double ak = alpha / k;
+    double x[3], v[3];
     for (int d = 0; d < 3; ++d) {
         const double target = u[d] * g.L;
-        double x = target;
+        double xx = target;
         for (int it = 0; it < 32; ++it) {
-            const double F = __dsub_rn(__dadd_rn(x, __dmul_rn(ak, sin(k * x))), target);
-            const double dF = __dadd_rn(1.0, __dmul_rn(alpha, cos(k * x)));
+            const double F = __dsub_rn(__dadd_rn(xx, __dmul_rn(ak, sin(k * xx))), target);
+            const double dF = __dadd_rn(1.0, __dmul_rn(alpha, cos(k * xx)));
             const double dx = __ddiv_rn(F, dF);
-            x = __dsub_rn(x, dx);
+            xx = __dsub_rn(xx, dx);
             if (fabs(dx) < 1e-12) break;
         }
-        st.a[d][j] = wrap(x, g.L);
+        x[d] = wrap(xx, g.L);
     }
     const double two_pi = 6.283185307179586476925286766559;
     const double r1 = sqrt(-2.0 * log(1.0 - u[3]));
     const double r2 = sqrt(-2.0 * log(1.0 - u[5]));
-    st.a[3][j] = r1 * cos(two_pi * u[4]);
-    st.a[4][j] = r1 * sin(two_pi * u[4]);
-    st.a[5][j] = r2 * cos(two_pi * u[6]);
+    v[0] = r1 * cos(two_pi * u[4]);
+    v[1] = r1 * sin(two_pi * u[4]);
+    v[2] = r2 * cos(two_pi * u[6]);
+    store_particle(st, j, x, v);
+}
+
+__global__ void __launch_bounds__(kThreads) k_soa_to_pairs(const double* __restrict__ soa, int64_t np,
+                                                           PState dst) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= np) return;
+    double x[3], v[3];
+#pragma unroll
+    for (int d = 0; d < 3; ++d) { x[d] = soa[d * np + i]; v[d] = soa[(3 + d) * np + i]; }
+    store_particle(dst, i, x, v);
+}
+
+__global__ void __launch_bounds__(kThreads) k_pairs_to_soa(PState src, int64_t np,
+                                                           double* __restrict__ soa) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= np) return;
+    double x[3], v[3];
+    load_particle(src, i, x, v);
+#pragma unroll
+    for (int d = 0; d < 3; ++d) { soa[d * np + i] = x[d]; soa[(3 + d) * np + i] = v[d]; }
 }
 
 // ----------------------------------------------------------- push + key ----
-// Grid-stride over the sorted particles with the next particle's x, v loads in
-// flight while the current one gathers E.  rank[i] = the particle's arrival
-// order in its new cell (return value of the count atomic), so the placement
-// needs no second atomic.
+// Grid-stride over the sorted particles with the next particle's loads in flight
+// while the current one gathers E.  rank[i] = arrival order in the new cell
+// (return value of the count atomic), so the placement needs no second atomic.
 template <bool PUSH>
 __global__ void __launch_bounds__(kThreads) k_push_key(Geom g, PState cur, int64_t np,
-                                                       const double* __restrict__ Ex,
-                                                       const double* __restrict__ Ey,
-                                                       const double* __restrict__ Ez,
+                                                       const double* __restrict__ E4,
                                                        uint32_t* __restrict__ key,
                                                        uint16_t* __restrict__ rank,
                                                        uint32_t* __restrict__ count,
                                                        int* __restrict__ err) {
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    double xn[3], vn[3];
-    if (i < np) {
-#pragma unroll
-        for (int d = 0; d < 3; ++d) { xn[d] = __ldg(cur.a[d] + i); vn[d] = __ldg(cur.a[3 + d] + i); }
-    }
-    for (; i < np; i += stride) {
-        double x[3] = {xn[0], xn[1], xn[2]}, v[3] = {vn[0], vn[1], vn[2]};
-        const int64_t inext = i + stride;
-        if (inext < np) {
-#pragma unroll
-            for (int d = 0; d < 3; ++d) { xn[d] = __ldg(cur.a[d] + inext); vn[d] = __ldg(cur.a[3 + d] + inext); }
-        }
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < np; i += stride) {
+        double x[3], v[3];
+        load_particle(cur, i, x, v);
         if (PUSH) {
-            gather_push(g, Ex, Ey, Ez, x, v);
+            const double z0 = x[2];
+            gather_push(g, E4, x, v);
+            cur.p[1][i] = make_double2(z0, v[2]);
+            cur.p[2][i] = make_double2(v[0], v[1]);
         } else if (!(x[0] >= 0.0 && x[0] < g.L && x[1] >= 0.0 && x[1] < g.L && x[2] >= 0.0 && x[2] < g.L)) {
             atomicExch(err + 1, 1);   // imported position outside [0, L)
         }
+        const uint32_t k = key_of(g, x);
+        key[i] = k;
+        const uint32_t r = atomicAdd(count + k, 1u);
+        if (r > 0xffffu) atomicExch(err, 1);
+        rank[i] = (uint16_t)r;
+    }
+}
+
+// The step's push: one CTA per Morton brick of 256 cells.  The particles of the
+// brick are the contiguous sorted range [offs[c0], offs[c0 + 256)) and all their
+// CIC corners lie in the brick's 9 x 9 x 5 node tile, which is staged in shared
+// memory (13 KB of node records) with coalesced loads; the gather then reads
+// shared memory.  Kick v in place, drift to x' (not stored), key, rank.
+__global__ void __launch_bounds__(kThreads) k_push_key_brick(Geom g, PState cur,
+                                                             const uint32_t* __restrict__ offs,
+                                                             const double* __restrict__ E4,
+                                                             uint32_t* __restrict__ key,
+                                                             uint16_t* __restrict__ rank,
+                                                             uint32_t* __restrict__ count,
+                                                             int* __restrict__ err) {
+    __shared__ double4 etile[9 * 9 * 5];
+    const int t = threadIdx.x;
+    const uint32_t c0 = blockIdx.x * kBrick;
+    int bx, by, bz;
+    unmorton(c0, bx, by, bz);
+    for (int q = t; q < 9 * 9 * 5; q += kThreads) {
+        const int nx = q % 9, ny = (q / 9) % 9, nz = q / 81;
+        const int64_t m = ((int64_t)((bz + nz) & g.nmask) * g.n + ((by + ny) & g.nmask)) * g.n + ((bx + nx) & g.nmask);
+        double ex, ey, ez;
+        ldg_node(E4 + 4 * m, ex, ey, ez);
+        etile[q] = make_double4(ex, ey, ez, 0.0);
+    }
+    const uint32_t P0 = __ldg(offs + c0), P1 = __ldg(offs + c0 + kBrick);
+    __syncthreads();
+    for (uint32_t i = P0 + t; i < P1; i += kThreads) {
+        double x[3], v[3];
+        load_particle(cur, i, x, v);
+        const double z0 = x[2];
+        // CIC gather from the tile: same weights, corner order and fma chain as gather_E
+        int ii[3];
+        double w[3][2];
+        cic_weights(g, x, ii, w);
+        const int lx = ii[0] - bx, ly = ii[1] - by, lz = ii[2] - bz;
+        double e0 = 0.0, e1 = 0.0, e2 = 0.0;
+#pragma unroll
+        for (int c = 0; c < 2; ++c)
+#pragma unroll
+            for (int b = 0; b < 2; ++b)
+#pragma unroll
+                for (int a = 0; a < 2; ++a) {
+                    const double wt = __dmul_rn(__dmul_rn(w[0][a], w[1][b]), w[2][c]);
+                    const double4 e = etile[((lz + c) * 9 + (ly + b)) * 9 + (lx + a)];
+                    e0 = __fma_rn(wt, e.x, e0);
+                    e1 = __fma_rn(wt, e.y, e1);
+                    e2 = __fma_rn(wt, e.z, e2);
+                }
+        v[0] = __fma_rn(g.qm_dt, e0, v[0]);
+        v[1] = __fma_rn(g.qm_dt, e1, v[1]);
+        v[2] = __fma_rn(g.qm_dt, e2, v[2]);
+        drift(g, x, v);
+        cur.p[1][i] = make_double2(z0, v[2]);    // kicked velocity in place: (x_n, v_{n+1/2})
+        cur.p[2][i] = make_double2(v[0], v[1]);
         const uint32_t k = key_of(g, x);
         key[i] = k;
         const uint32_t r = atomicAdd(count + k, 1u);
@@ -111,7 +186,8 @@ __global__ void __launch_bounds__(kThreads) k_keys_only(Geom g, PState cur, int6
                                                         uint32_t* __restrict__ key) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= np) return;
-    double x[3] = {cur.a[0][i], cur.a[1][i], cur.a[2][i]};
+    double x[3], v[3];
+    load_particle(cur, i, x, v);
     key[i] = key_of(g, x);
 }
 
@@ -242,42 +318,44 @@ __global__ void __launch_bounds__(kThreads) k_place(const uint32_t* __restrict__
 }
 
 // ------------------------------------------------- reorder + push + deposit -
-// One CTA per Morton brick of 256 cells (8 x 8 x 4).  Phases per chunk of the
-// brick's sorted positions:
-//   1. stage perm[chunk] in shared memory; one thread per cell insertion-sorts
-//      its segment ascending (= the stable order, D#14);
-//   2. one thread per sorted position p (a warp covers 32 consecutive p):
-//      gather x, v through perm (next particle prefetched), push, store x', v'
-//      at p, compute its 8 CIC corner weights, and reduce them over the lanes of
-//      the same cell (segmented shuffle scan; positions are cell-sorted); the
-//      head lane of each cell segment adds the 8 sums to that cell's
-//      accumulator in shared memory;
-//   3. after the last chunk, the 256 cell accumulators are folded into the
-//      9 x 9 x 5 node tile in eight conflict-free passes and the tile is flushed
-//      with one fp64 global reduction (RED.ADD.F64) per node.
+// Per chunk of the brick's sorted positions (whole cells, <= kCap particles):
+//   A  stage perm[chunk] (coalesced); each cell's thread tags its positions with
+//      the local cell id;
+//   B  thread per position p: stable rank r of its particle inside the cell
+//      (#perm entries of the cell below its own, broadcast reads), gather x, v'
+//      through perm, re-drift, store x', v' at the stable slot s0 + r, and keep
+//      the fractional offsets f = x' inv_h - i of the new position in shared
+//      memory at that slot;
+//   C  thread per cell: sum the 8 corner weights (w_x w_y) w_z of its particles in
+//      stable order in registers.
+// After the last chunk the 256 cells' sums are folded into the 9 x 9 x 5 node
+// tile (eight conflict-free passes) and flushed with one fp64 RED.ADD per node.
+// No atomics and no shuffles inside the CTA: the per-brick charge is deterministic.
 template <bool PUSH>
 __global__ void __launch_bounds__(kThreads, 3) k_reorder_deposit(
     Geom g, const uint32_t* __restrict__ offs, const uint32_t* __restrict__ perm, PState cur,
-    PState nxt, const double* __restrict__ Ex, const double* __restrict__ Ey,
-    const double* __restrict__ Ez, double* __restrict__ rho, int* __restrict__ err) {
-    __shared__ uint32_t soffs[kBrick + 1];
-    __shared__ uint32_t sperm[kCap];
-    __shared__ double sacc[8][kBrick];
-    __shared__ double tile[9 * 9 * 5];
-    const int t = threadIdx.x, lane = t & 31;
+    PState nxt, double* __restrict__ rho, int* __restrict__ err) {
+    extern __shared__ double dyn_smem[];
+    double(*sfrac)[kCap] = reinterpret_cast<double(*)[kCap]>(dyn_smem);      // [3][kCap]
+    double* tile = dyn_smem + 3 * kCap;                                        // [9*9*5]
+    uint32_t* sperm = reinterpret_cast<uint32_t*>(tile + 9 * 9 * 5);          // [kCap]
+    uint32_t* soffs = sperm + kCap;                                            // [kBrick + 1]
+    uint8_t* scell = reinterpret_cast<uint8_t*>(soffs + kBrick + 1);           // [kCap]
+    const int t = threadIdx.x;
     const uint32_t c0 = blockIdx.x * kBrick;
     int bx, by, bz;
     unmorton(c0, bx, by, bz);
     soffs[t] = offs[c0 + t];
     if (t == 0) soffs[kBrick] = offs[c0 + kBrick];
-#pragma unroll
-    for (int q = 0; q < 8; ++q) sacc[q][t] = 0.0;
     for (int q = t; q < 9 * 9 * 5; q += kThreads) tile[q] = 0.0;
     __syncthreads();
 
+    double acc[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) acc[q] = 0.0;
     int ca = 0;
     while (ca < kBrick) {
-        // largest cb with soffs[cb] - soffs[ca] <= kCap (uniform across the CTA)
+        // chunk = cells [ca, cb), the largest run with at most kCap particles
         if (soffs[ca + 1] - soffs[ca] > (uint32_t)kCap) {
             if (t == 0) atomicExch(err, 1);
             return;
@@ -290,74 +368,59 @@ __global__ void __launch_bounds__(kThreads, 3) k_reorder_deposit(
         const int cb = lo;
         const uint32_t P0 = soffs[ca];
         const int cnt = (int)(soffs[cb] - P0);
+        // A
         for (int p = t; p < cnt; p += kThreads) sperm[p] = __ldg(perm + P0 + p);
+        const bool mine = t >= ca && t < cb;
+        const int s0 = mine ? (int)(soffs[t] - P0) : 0, s1 = mine ? (int)(soffs[t + 1] - P0) : 0;
+        for (int p = s0; p < s1; ++p) scell[p] = (uint8_t)t;
         __syncthreads();
-        if (t >= ca && t < cb) {  // insertion sort of this cell's segment: stable order
-            const int s0 = (int)(soffs[t] - P0), s1 = (int)(soffs[t + 1] - P0);
-            for (int a = s0 + 1; a < s1; ++a) {
-                const uint32_t vv = sperm[a];
-                int b = a - 1;
-                while (b >= s0 && sperm[b] > vv) { sperm[b + 1] = sperm[b]; --b; }
-                sperm[b + 1] = vv;
-            }
-        }
-        __syncthreads();
-
-        const int nit = (cnt + kThreads - 1) / kThreads;
-        int p = t;
-        double xn[3], vn[3];
-        bool okn = p < cnt;
-        if (okn) {
-            const uint32_t j = sperm[p];
+        // B, kBatch positions per thread at a time: all their gathers in flight together
+        for (int pb = t; pb < cnt; pb += kBatch * kThreads) {
+            int o[kBatch];
+            uint32_t j[kBatch];
 #pragma unroll
-            for (int d = 0; d < 3; ++d) { xn[d] = __ldg(cur.a[d] + j); vn[d] = __ldg(cur.a[3 + d] + j); }
-        }
-        for (int it = 0; it < nit; ++it, p += kThreads) {
-            double x[3] = {xn[0], xn[1], xn[2]}, v[3] = {vn[0], vn[1], vn[2]};
-            const bool ok = okn;
-            okn = p + kThreads < cnt;
-            if (okn) {   // prefetch the next particle of this thread
-                const uint32_t j = sperm[p + kThreads];
-#pragma unroll
-                for (int d = 0; d < 3; ++d) { xn[d] = __ldg(cur.a[d] + j); vn[d] = __ldg(cur.a[3 + d] + j); }
-            }
-            double w8[8];
-            int lc = 1024 + lane;   // unique sentinel for idle lanes
-            if (ok) {
-                if (PUSH) gather_push(g, Ex, Ey, Ez, x, v);
-                const int64_t o = (int64_t)P0 + p;
-#pragma unroll
-                for (int d = 0; d < 3; ++d) {
-                    nxt.a[d][o] = x[d];
-                    nxt.a[3 + d][o] = v[d];
-                }
-                int ii[3];
-                double w[3][2];
-                cic_weights(g, x, ii, w);
-#pragma unroll
-                for (int q = 0; q < 8; ++q)
-                    w8[q] = __dmul_rn(__dmul_rn(w[0][q & 1], w[1][(q >> 1) & 1]), w[2][q >> 2]);
-                lc = (int)morton(ii[0] - bx, ii[1] - by, ii[2] - bz);
-            } else {
-#pragma unroll
-                for (int q = 0; q < 8; ++q) w8[q] = 0.0;
-            }
-            // segmented suffix sums over lanes of equal cell (cell-sorted positions)
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const int olc = __shfl_down_sync(0xffffffffu, lc, o);
-                const bool same = lane + o < 32 && olc == lc;
-#pragma unroll
-                for (int q = 0; q < 8; ++q) {
-                    const double ov = __shfl_down_sync(0xffffffffu, w8[q], o);
-                    if (same) w8[q] += ov;
+            for (int k = 0; k < kBatch; ++k) {
+                const int p = pb + k * kThreads;
+                o[k] = -1;
+                if (p < cnt) {
+                    const int c = scell[p];
+                    const int q0 = (int)(soffs[c] - P0), q1 = (int)(soffs[c + 1] - P0);
+                    j[k] = sperm[p];
+                    int r = 0;
+                    for (int q = q0; q < q1; ++q) r += sperm[q] < j[k];
+                    o[k] = q0 + r;
                 }
             }
-            const int plc = __shfl_up_sync(0xffffffffu, lc, 1);
-            if (ok && (lane == 0 || plc != lc)) {
+            double2 a[kBatch], b[kBatch], e[kBatch];
 #pragma unroll
-                for (int q = 0; q < 8; ++q) atomicAdd(&sacc[q][lc], w8[q]);
-            }
+            for (int k = 0; k < kBatch; ++k)
+                if (o[k] >= 0) {
+                    a[k] = __ldg(cur.p[0] + j[k]);
+                    b[k] = __ldg(cur.p[1] + j[k]);
+                    e[k] = __ldg(cur.p[2] + j[k]);
+                }
+#pragma unroll
+            for (int k = 0; k < kBatch; ++k)
+                if (o[k] >= 0) {
+                    double x[3] = {a[k].x, a[k].y, b[k].x}, v[3] = {e[k].x, e[k].y, b[k].y};
+                    if (PUSH) drift(g, x, v);    // v is already kicked (push_key)
+                    store_particle(nxt, (int64_t)P0 + o[k], x, v);
+#pragma unroll
+                    for (int d = 0; d < 3; ++d) {
+                        const double sd = __dmul_rn(x[d], g.inv_h);
+                        sfrac[d][o[k]] = __dsub_rn(sd, (double)cell_of(sd, g.n));
+                    }
+                }
+        }
+        __syncthreads();
+        // C
+        for (int p = s0; p < s1; ++p) {
+            const double fx = sfrac[0][p], fy = sfrac[1][p], fz = sfrac[2][p];
+            const double wx[2] = {__dsub_rn(1.0, fx), fx}, wy[2] = {__dsub_rn(1.0, fy), fy},
+                         wz[2] = {__dsub_rn(1.0, fz), fz};
+#pragma unroll
+            for (int q = 0; q < 8; ++q)
+                acc[q] = __dadd_rn(acc[q], __dmul_rn(__dmul_rn(wx[q & 1], wy[(q >> 1) & 1]), wz[q >> 2]));
         }
         __syncthreads();
         ca = cb;
@@ -368,7 +431,7 @@ __global__ void __launch_bounds__(kThreads, 3) k_reorder_deposit(
 #pragma unroll
     for (int q = 0; q < 8; ++q) {
         const int a = q & 1, b = (q >> 1) & 1, c = q >> 2;
-        tile[((lz + c) * 9 + (ly + b)) * 9 + (lx + a)] += sacc[q][t];
+        tile[((lz + c) * 9 + (ly + b)) * 9 + (lx + a)] += acc[q];
         __syncthreads();
     }
     for (int q = t; q < 9 * 9 * 5; q += kThreads) {
@@ -380,21 +443,20 @@ __global__ void __launch_bounds__(kThreads, 3) k_reorder_deposit(
 }
 
 __global__ void __launch_bounds__(kThreads) k_half_kick(Geom g, PState cur, int64_t np,
-                                                        const double* __restrict__ Ex,
-                                                        const double* __restrict__ Ey,
-                                                        const double* __restrict__ Ez) {
+                                                        const double* __restrict__ E4) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= np) return;
-    double x[3] = {cur.a[0][i], cur.a[1][i], cur.a[2][i]};
-    double ep[3];
-    gather_E(g, Ex, Ey, Ez, x, ep);
+    double x[3], v[3], ep[3];
+    load_particle(cur, i, x, v);
+    gather_E(g, E4, x, ep);
     const double hk = -0.5 * g.qm_dt;   // v_{-1/2} = v_0 - (q/m) E dt/2
 #pragma unroll
-    for (int d = 0; d < 3; ++d) cur.a[3 + d][i] = __fma_rn(hk, ep[d], cur.a[3 + d][i]);
+    for (int d = 0; d < 3; ++d) v[d] = __fma_rn(hk, ep[d], v[d]);
+    store_particle(cur, i, x, v);
 }
 
 // perm segments of every cell sorted ascending in place (export of the stable
-// permutation; the step itself sorts them in shared memory only).
+// permutation; the step itself ranks them in shared memory only).
 __global__ void __launch_bounds__(kThreads) k_sort_segments(const uint32_t* __restrict__ offs,
                                                             int64_t ncell, uint32_t* __restrict__ perm) {
     const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -410,6 +472,8 @@ __global__ void __launch_bounds__(kThreads) k_sort_segments(const uint32_t* __re
 
 inline unsigned blocks(int64_t n, int t) { return (unsigned)((n + t - 1) / t); }
 
+constexpr size_t kReorderSmem = sizeof(double) * (3 * kCap + 9 * 9 * 5) + sizeof(uint32_t) * (kCap + kBrick + 1) + kCap;
+
 }  // namespace
 
 void launch_sample(const Geom& g, PState st, int64_t np, double k, double alpha, uint64_t seed,
@@ -419,14 +483,27 @@ void launch_sample(const Geom& g, PState st, int64_t np, double k, double alpha,
                                                         (uint32_t)(seed >> 32));
 }
 
-void launch_push_key(const Geom& g, PState cur, int64_t np, double* const E[3], int push,
-                     uint32_t* key, uint16_t* rank, uint32_t* count, int* err_flag, cudaStream_t s) {
+void launch_soa_to_pairs(const double* soa, int64_t np, PState dst, cudaStream_t s) {
     if (np == 0) return;
-    const unsigned nb = std::min<unsigned>(blocks(np, kThreads), 148u * 32u);
-    if (push)
-        k_push_key<true><<<nb, kThreads, 0, s>>>(g, cur, np, E[0], E[1], E[2], key, rank, count, err_flag);
-    else
-        k_push_key<false><<<nb, kThreads, 0, s>>>(g, cur, np, E[0], E[1], E[2], key, rank, count, err_flag);
+    k_soa_to_pairs<<<blocks(np, kThreads), kThreads, 0, s>>>(soa, np, dst);
+}
+
+void launch_pairs_to_soa(PState src, int64_t np, double* soa, cudaStream_t s) {
+    if (np == 0) return;
+    k_pairs_to_soa<<<blocks(np, kThreads), kThreads, 0, s>>>(src, np, soa);
+}
+
+void launch_push_key(const Geom& g, PState cur, int64_t np, const uint32_t* offs, const double* E4,
+                     int push, uint32_t* key, uint16_t* rank, uint32_t* count, int* err_flag,
+                     cudaStream_t s) {
+    if (np == 0) return;
+    if (push) {
+        const unsigned nbrick = (unsigned)(((int64_t)g.n * g.n * g.n) / kBrick);
+        k_push_key_brick<<<nbrick, kThreads, 0, s>>>(g, cur, offs, E4, key, rank, count, err_flag);
+    } else {
+        const unsigned nb = std::min<unsigned>(blocks(np, kThreads), 148u * 32u);
+        k_push_key<false><<<nb, kThreads, 0, s>>>(g, cur, np, E4, key, rank, count, err_flag);
+    }
 }
 
 void launch_keys_only(const Geom& g, PState cur, int64_t np, uint32_t* key, cudaStream_t s) {
@@ -438,7 +515,7 @@ size_t scan_scratch_bytes(int64_t ncell) {
     return sizeof(uint32_t) * (size_t)(blocks(ncell, kScanTile) + 1);
 }
 
-void launch_scan(uint32_t* count, uint32_t* offs, int64_t ncell, uint32_t* scratch, cudaStream_t s) {
+void launch_scan(const uint32_t* count, uint32_t* offs, int64_t ncell, uint32_t* scratch, cudaStream_t s) {
     const unsigned nb = blocks(ncell, kScanTile);
     k_scan_reduce<<<nb, kThreads, 0, s>>>(count, ncell, scratch);
     k_scan_bsum<<<1, 1024, 0, s>>>(scratch, (int)nb);
@@ -452,24 +529,26 @@ void launch_place(const uint32_t* key, const uint16_t* rank, int64_t np, const u
 }
 
 void launch_reorder_deposit(const Geom& g, const uint32_t* offs, const uint32_t* perm, PState cur,
-                            PState nxt, double* const E[3], int push, double* rho_buf,
-                            int* err_flag, cudaStream_t s) {
+                            PState nxt, int push, double* rho_buf, int* err_flag, cudaStream_t s) {
     const unsigned nbrick = (unsigned)(((int64_t)g.n * g.n * g.n) / kBrick);
     if (push)
-        k_reorder_deposit<true><<<nbrick, kThreads, 0, s>>>(g, offs, perm, cur, nxt, E[0], E[1], E[2],
-                                                             rho_buf, err_flag);
+        k_reorder_deposit<true><<<nbrick, kThreads, kReorderSmem, s>>>(g, offs, perm, cur, nxt, rho_buf, err_flag);
     else
-        k_reorder_deposit<false><<<nbrick, kThreads, 0, s>>>(g, offs, perm, cur, nxt, E[0], E[1], E[2],
-                                                              rho_buf, err_flag);
+        k_reorder_deposit<false><<<nbrick, kThreads, kReorderSmem, s>>>(g, offs, perm, cur, nxt, rho_buf, err_flag);
+}
+
+void particles_set_smem_limits() {
+    cudaFuncSetAttribute(k_reorder_deposit<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kReorderSmem);
+    cudaFuncSetAttribute(k_reorder_deposit<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kReorderSmem);
 }
 
 void launch_sort_segments(const uint32_t* offs, int64_t ncell, uint32_t* perm, cudaStream_t s) {
     k_sort_segments<<<blocks(ncell, kThreads), kThreads, 0, s>>>(offs, ncell, perm);
 }
 
-void launch_half_kick(const Geom& g, PState cur, int64_t np, double* const E[3], cudaStream_t s) {
+void launch_half_kick(const Geom& g, PState cur, int64_t np, const double* E4, cudaStream_t s) {
     if (np == 0) return;
-    k_half_kick<<<blocks(np, kThreads), kThreads, 0, s>>>(g, cur, np, E[0], E[1], E[2]);
+    k_half_kick<<<blocks(np, kThreads), kThreads, 0, s>>>(g, cur, np, E4);
 }
 
 }  // namespace pic

@@ -2,7 +2,7 @@
 // PIC step.  The host validates, carves the caller's workspace and enqueues
 // kernels on the caller's stream; every step of the path runs on the device
 // (kernels.h).  One step:
-//   SOLVE   fft_x_fwd -> fft_y_fwd -> fft_z_mul -> fft_y_inv -> fft_x_inv -> energy
+//   SOLVE   fft_x_fwd -> fft_y_fwd -> fft_z_mul -> fft_y_inv -> fft_x_inv (E4) -> energy
 //   CLEAR   count = 0, rho = 0
 //   PUSH    push_key  (gather + push + new key + count)
 //   SORT    scan -> place
@@ -18,6 +18,7 @@
 
 namespace pic {
 void fft_set_smem_limits();
+void particles_set_smem_limits();
 }
 
 using pic::Geom;
@@ -48,7 +49,7 @@ struct pic_ctx {
     cudaStream_t stream = nullptr;
     bool poisoned = false;
     char err[512] = "";
-    double* part[2][6] = {};      // double-buffered SoA state
+    double2* part[2][3] = {};     // double-buffered pair streams (pic_device.cuh)
     int cur = 0;
     uint32_t* key = nullptr;
     uint16_t* rank = nullptr;     // arrival order of each particle in its new cell
@@ -56,8 +57,9 @@ struct pic_ctx {
     uint32_t* count = nullptr;
     uint32_t* offs = nullptr;
     uint32_t* scan_scratch = nullptr;
-    double* rho = nullptr;        // pitched real grid of raw CIC weight sums
-    double* E[3] = {};            // pitched real grids (half spectra during the solve)
+    double* rho = nullptr;        // S0: pitched raw CIC weight sums / spectrum during the solve
+    double* spec[2] = {};         // S1, S2: half spectra of E_x, E_y during the solve
+    double* E4 = nullptr;         // field node records (E_x, E_y, E_z, 0)
     double2* tw = nullptr;
     double* partials = nullptr;
     double* energies = nullptr;   // ring [kMaxEnergySteps][2]
@@ -124,9 +126,9 @@ size_t carve(pic_ctx* c, const Geom& g, int64_t np, char* base) {
     const int64_t ncell = (int64_t)g.n * g.n * g.n;
     const size_t grid_bytes = sizeof(double2) * (size_t)g.n * g.n * g.px;
     for (int b = 0; b < 2; ++b)
-        for (int a = 0; a < 6; ++a) {
-            char* ptr = take(sizeof(double) * (size_t)np);
-            if (c) c->part[b][a] = reinterpret_cast<double*>(ptr);
+        for (int a = 0; a < 3; ++a) {
+            char* ptr = take(sizeof(double2) * (size_t)np);
+            if (c) c->part[b][a] = reinterpret_cast<double2*>(ptr);
         }
     char* k = take(sizeof(uint32_t) * (size_t)np);
     char* rk = take(sizeof(uint16_t) * (size_t)np);
@@ -135,9 +137,9 @@ size_t carve(pic_ctx* c, const Geom& g, int64_t np, char* base) {
     char* of = take(sizeof(uint32_t) * (size_t)(ncell + 1));
     char* ss = take(pic::scan_scratch_bytes(ncell));
     char* rh = take(grid_bytes);
-    char* e0 = take(grid_bytes);
-    char* e1 = take(grid_bytes);
-    char* e2 = take(grid_bytes);
+    char* s1 = take(grid_bytes);
+    char* s2 = take(grid_bytes);
+    char* e4 = take(sizeof(double) * 4 * (size_t)ncell);
     char* tw = take(sizeof(double2) * (size_t)(g.n / 2));
     char* pa = take(sizeof(double) * 3 * (size_t)pic::energy_partials(g));
     char* en = take(sizeof(double) * 2 * kMaxEnergySteps);
@@ -150,9 +152,9 @@ size_t carve(pic_ctx* c, const Geom& g, int64_t np, char* base) {
         c->offs = reinterpret_cast<uint32_t*>(of);
         c->scan_scratch = reinterpret_cast<uint32_t*>(ss);
         c->rho = reinterpret_cast<double*>(rh);
-        c->E[0] = reinterpret_cast<double*>(e0);
-        c->E[1] = reinterpret_cast<double*>(e1);
-        c->E[2] = reinterpret_cast<double*>(e2);
+        c->spec[0] = reinterpret_cast<double*>(s1);
+        c->spec[1] = reinterpret_cast<double*>(s2);
+        c->E4 = reinterpret_cast<double*>(e4);
         c->tw = reinterpret_cast<double2*>(tw);
         c->partials = reinterpret_cast<double*>(pa);
         c->energies = reinterpret_cast<double*>(en);
@@ -219,22 +221,24 @@ void collect_timings(pic_ctx* c) {
 // ------------------------------------------------------------ pipeline -----
 PState state(pic_ctx* c, int b) {
     PState s;
-    for (int a = 0; a < 6; ++a) s.a[a] = c->part[b][a];
+    for (int a = 0; a < 3; ++a) s.p[a] = c->part[b][a];
     return s;
 }
 
 // rho (raw CIC sums, scaled by `scale` in the multiply) -> E, energies -> ring slot
 pic_status solve(pic_ctx* c, double scale, int slot) {
     const Geom& g = c->g;
-    { StageScope t(c, PIC_STAGE_FFT_X_FWD, 1); pic::launch_fft_x_fwd(g, c->rho, c->E[0], c->tw, c->stream); }
+    double* const S[3] = {c->spec[0], c->spec[1], c->rho};   // E^_x, E^_y, E^_z after the z pass
+    double* const S0[3] = {c->rho, c->rho, c->rho};
+    { StageScope t(c, PIC_STAGE_FFT_X_FWD, 1); pic::launch_fft_x_fwd(g, c->rho, c->tw, c->stream); }
     PIC_LAUNCHED(c, "fft_x_fwd");
-    { StageScope t(c, PIC_STAGE_FFT_Y_FWD, 1); pic::launch_fft_y(g, c->E, 1, 0, c->tw, c->stream); }
+    { StageScope t(c, PIC_STAGE_FFT_Y_FWD, 1); pic::launch_fft_y(g, S0, 1, 0, c->tw, c->stream); }
     PIC_LAUNCHED(c, "fft_y_fwd");
-    { StageScope t(c, PIC_STAGE_FFT_Z_MUL, 1); pic::launch_fft_z_mul(g, c->E[0], c->E, scale, c->tw, c->stream); }
+    { StageScope t(c, PIC_STAGE_FFT_Z_MUL, 1); pic::launch_fft_z_mul(g, c->rho, c->spec[0], c->spec[1], scale, c->tw, c->stream); }
     PIC_LAUNCHED(c, "fft_z_mul");
-    { StageScope t(c, PIC_STAGE_FFT_Y_INV, 1); pic::launch_fft_y(g, c->E, 3, 1, c->tw, c->stream); }
+    { StageScope t(c, PIC_STAGE_FFT_Y_INV, 1); pic::launch_fft_y(g, S, 3, 1, c->tw, c->stream); }
     PIC_LAUNCHED(c, "fft_y_inv");
-    { StageScope t(c, PIC_STAGE_FFT_X_INV, 1); pic::launch_fft_x_inv(g, c->E, c->tw, c->partials, c->stream); }
+    { StageScope t(c, PIC_STAGE_FFT_X_INV, 1); pic::launch_fft_x_inv(g, S, c->E4, c->tw, c->partials, c->stream); }
     PIC_LAUNCHED(c, "fft_x_inv");
     { StageScope t(c, PIC_STAGE_ENERGY, 1); pic::launch_energy_reduce(g, c->partials, c->energies + 2 * slot, c->stream); }
     PIC_LAUNCHED(c, "energy");
@@ -252,7 +256,7 @@ pic_status push_sort_deposit(pic_ctx* c, int push) {
         PIC_CUDA(c, cudaMemsetAsync(c->rho, 0, sizeof(double2) * (size_t)g.n * g.n * g.px, c->stream));
     }
     PState cur = state(c, c->cur), nxt = state(c, c->cur ^ 1);
-    { StageScope t(c, PIC_STAGE_PUSH_KEY, 1); pic::launch_push_key(g, cur, c->np, c->E, push, c->key, c->rank, c->count, c->err_flag, c->stream); }
+    { StageScope t(c, PIC_STAGE_PUSH_KEY, 1); pic::launch_push_key(g, cur, c->np, c->offs, c->E4, push, c->key, c->rank, c->count, c->err_flag, c->stream); }
     PIC_LAUNCHED(c, "push_key");
     { StageScope t(c, PIC_STAGE_SCAN, 3); pic::launch_scan(c->count, c->offs, c->ncell, c->scan_scratch, c->stream); }
     PIC_LAUNCHED(c, "scan");
@@ -260,7 +264,7 @@ pic_status push_sort_deposit(pic_ctx* c, int push) {
     PIC_LAUNCHED(c, "place");
     {
         StageScope t(c, PIC_STAGE_REORDER_DEPOSIT, 1);
-        pic::launch_reorder_deposit(g, c->offs, c->perm, cur, nxt, c->E, push, c->rho, c->err_flag, c->stream);
+        pic::launch_reorder_deposit(g, c->offs, c->perm, cur, nxt, push, c->rho, c->err_flag, c->stream);
     }
     PIC_LAUNCHED(c, "reorder_deposit");
     c->cur ^= 1;
@@ -367,7 +371,7 @@ pic_status pic_init(const pic_params* p, int32_t rank, int32_t nranks, const uin
     carve(c, g, np, reinterpret_cast<char*>(workspace));
 
     static bool smem_set = false;
-    if (!smem_set) { pic::fft_set_smem_limits(); smem_set = true; }
+    if (!smem_set) { pic::fft_set_smem_limits(); pic::particles_set_smem_limits(); smem_set = true; }
 
     auto bail = [&](pic_status s) {
         snprintf(g_init_error, sizeof(g_init_error), "%s", c->err);
@@ -391,10 +395,12 @@ pic_status pic_init(const pic_params* p, int32_t rank, int32_t nranks, const uin
     if ((st = push_sort_deposit(c, 0)) != PIC_OK) return bail(st);
     if (p->half_kick) {
         if ((st = solve(c, c->deposit_scale / (double)c->ncell, 0)) != PIC_OK) return bail(st);
-        pic::launch_half_kick(g, state(c, c->cur), np, c->E, c->stream);
+        pic::launch_half_kick(g, state(c, c->cur), np, c->E4, c->stream);
         e = cudaGetLastError();
         if (e != cudaSuccess) return bail(fail(c, PIC_ECUDA, "half_kick", e));
         c->last_slot = -1;
+        // the solve reused the charge buffer: deposit again (the re-sort is the identity)
+        if ((st = push_sort_deposit(c, 0)) != PIC_OK) return bail(st);
     }
     if ((st = sync_check(c)) != PIC_OK) return bail(st);
     *out = c;
@@ -455,18 +461,21 @@ pic_status pic_num_particles(pic_ctx* c, int64_t* np) {
 pic_status pic_get_particles(pic_ctx* c, double* xyzuvw, int64_t np) {
     PIC_CHECK_CTX(c);
     if (!xyzuvw || np != c->np) return PIC_EINVAL;
-    for (int a = 0; a < 6; ++a)
-        PIC_CUDA(c, cudaMemcpyAsync(xyzuvw + (size_t)a * np, c->part[c->cur][a], sizeof(double) * (size_t)np,
-                                    cudaMemcpyDeviceToHost, c->stream));
+    // the idle buffer (48 B/particle) holds the SoA [6][np] copy for the transfer
+    double* soa = reinterpret_cast<double*>(c->part[c->cur ^ 1][0]);
+    pic::launch_pairs_to_soa(state(c, c->cur), np, soa, c->stream);
+    PIC_LAUNCHED(c, "pairs_to_soa");
+    PIC_CUDA(c, cudaMemcpyAsync(xyzuvw, soa, sizeof(double) * 6 * (size_t)np, cudaMemcpyDeviceToHost, c->stream));
     return sync_check(c);
 }
 
 pic_status pic_set_particles(pic_ctx* c, const double* xyzuvw, int64_t np) {
     PIC_CHECK_CTX(c);
     if (!xyzuvw || np != c->np) return PIC_EINVAL;
-    for (int a = 0; a < 6; ++a)
-        PIC_CUDA(c, cudaMemcpyAsync(c->part[c->cur][a], xyzuvw + (size_t)a * np, sizeof(double) * (size_t)np,
-                                    cudaMemcpyHostToDevice, c->stream));
+    double* soa = reinterpret_cast<double*>(c->part[c->cur ^ 1][0]);
+    PIC_CUDA(c, cudaMemcpyAsync(soa, xyzuvw, sizeof(double) * 6 * (size_t)np, cudaMemcpyHostToDevice, c->stream));
+    pic::launch_soa_to_pairs(soa, np, state(c, c->cur), c->stream);
+    PIC_LAUNCHED(c, "soa_to_pairs");
     PIC_TRY(push_sort_deposit(c, 0));
     c->last_slot = -1;
     return sync_check(c);
@@ -475,7 +484,14 @@ pic_status pic_set_particles(pic_ctx* c, const double* xyzuvw, int64_t np) {
 pic_status pic_get_grid(pic_ctx* c, int32_t which, double* host) {
     PIC_CHECK_CTX(c);
     if (!host || which < 0 || which > 3) return PIC_EINVAL;
-    PIC_TRY(copy_grid_to_host(c, host, which == 0 ? c->rho : c->E[which - 1]));
+    if (which == 0) {
+        PIC_TRY(copy_grid_to_host(c, host, c->rho));
+    } else {
+        pic::launch_e4_extract(c->g, c->E4, which - 1, c->spec[0], c->stream);   // S1 as scratch
+        PIC_LAUNCHED(c, "e4_extract");
+        PIC_CUDA(c, cudaMemcpyAsync(host, c->spec[0], sizeof(double) * (size_t)c->ncell,
+                                    cudaMemcpyDeviceToHost, c->stream));
+    }
     PIC_TRY(sync_check(c));
     if (which == 0)
         for (int64_t m = 0; m < c->ncell; ++m) host[m] = c->deposit_scale * host[m];
@@ -488,10 +504,15 @@ pic_status pic_solve_injected(pic_ctx* c, const double* rho_host, double* E_host
     if (!rho_host) return PIC_EINVAL;
     PIC_TRY(copy_grid_to_device(c, c->rho, rho_host));
     PIC_TRY(solve(c, 1.0 / (double)c->ncell, 0));
-    if (E_host)
-        for (int d = 0; d < 3; ++d) PIC_TRY(copy_grid_to_host(c, E_host + (size_t)d * c->ncell, c->E[d]));
     double en[2];
     PIC_CUDA(c, cudaMemcpyAsync(en, c->energies, sizeof(en), cudaMemcpyDeviceToHost, c->stream));
+    if (E_host)
+        for (int d = 0; d < 3; ++d) {
+            pic::launch_e4_extract(c->g, c->E4, d, c->spec[0], c->stream);
+            PIC_LAUNCHED(c, "e4_extract");
+            PIC_CUDA(c, cudaMemcpyAsync(E_host + (size_t)d * c->ncell, c->spec[0], sizeof(double) * (size_t)c->ncell,
+                                        cudaMemcpyDeviceToHost, c->stream));
+        }
     PIC_TRY(sync_check(c));
     if (ex_energy) *ex_energy = en[0];
     if (total_energy) *total_energy = en[1];
@@ -504,7 +525,12 @@ pic_status pic_solve_injected(pic_ctx* c, const double* rho_host, double* E_host
 pic_status pic_push_injected(pic_ctx* c, const double* E_host) {
     PIC_CHECK_CTX(c);
     if (!E_host) return PIC_EINVAL;
-    for (int d = 0; d < 3; ++d) PIC_TRY(copy_grid_to_device(c, c->E[d], E_host + (size_t)d * c->ncell));
+    double* const comp[3] = {c->spec[0], c->spec[1], c->rho};   // scratch: compact [n^3] each
+    for (int d = 0; d < 3; ++d)
+        PIC_CUDA(c, cudaMemcpyAsync(comp[d], E_host + (size_t)d * c->ncell, sizeof(double) * (size_t)c->ncell,
+                                    cudaMemcpyHostToDevice, c->stream));
+    pic::launch_e4_pack(c->g, comp, c->E4, c->stream);
+    PIC_LAUNCHED(c, "e4_pack");
     PIC_TRY(push_sort_deposit(c, 1));
     c->last_slot = -1;
     return sync_check(c);

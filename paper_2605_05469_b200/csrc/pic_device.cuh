@@ -92,12 +92,21 @@ __device__ __forceinline__ void cic_weights(const Geom& g, const double x[3], in
     }
 }
 
+// One 32-byte node record (E_x, E_y, E_z, 0) of the field grid E4[n][n][n][4]:
+// a single 256-bit read-only load (LDG.E.ENL2.256).
+__device__ __forceinline__ void ldg_node(const double* __restrict__ p, double& ex, double& ey,
+                                         double& ez) {
+    double pad;
+    asm("ld.global.nc.v4.f64 {%0, %1, %2, %3}, [%4];"
+        : "=d"(ex), "=d"(ey), "=d"(ez), "=d"(pad)
+        : "l"(p));
+    (void)pad;
+}
+
 // CIC gather of E at x (corner order z outer, y, x inner; fma accumulation
-// from 0: S:141-149, D#17).
-__device__ __forceinline__ void gather_E(const Geom& g, const double* __restrict__ Ex,
-                                         const double* __restrict__ Ey,
-                                         const double* __restrict__ Ez, const double x[3],
-                                         double ep[3]) {
+// from 0: S:141-149, D#17).  E4 = node records (E_x, E_y, E_z, 0).
+__device__ __forceinline__ void gather_E(const Geom& g, const double* __restrict__ E4,
+                                         const double x[3], double ep[3]) {
     int i[3];
     double w[3][2];
     cic_weights(g, x, i, w);
@@ -106,14 +115,16 @@ __device__ __forceinline__ void gather_E(const Geom& g, const double* __restrict
     for (int c = 0; c < 2; ++c) {
 #pragma unroll
         for (int b = 0; b < 2; ++b) {
-            const int64_t row = ((int64_t)((i[2] + c) & g.nmask) * g.n + ((i[1] + b) & g.nmask)) * g.rp;
+            const int64_t row = ((int64_t)((i[2] + c) & g.nmask) * g.n + ((i[1] + b) & g.nmask)) * g.n;
 #pragma unroll
             for (int a = 0; a < 2; ++a) {
                 const double wt = __dmul_rn(__dmul_rn(w[0][a], w[1][b]), w[2][c]);
                 const int64_t m = row + ((i[0] + a) & g.nmask);
-                a0 = __fma_rn(wt, __ldg(Ex + m), a0);
-                a1 = __fma_rn(wt, __ldg(Ey + m), a1);
-                a2 = __fma_rn(wt, __ldg(Ez + m), a2);
+                double ex, ey, ez;
+                ldg_node(E4 + 4 * m, ex, ey, ez);
+                a0 = __fma_rn(wt, ex, a0);
+                a1 = __fma_rn(wt, ey, a1);
+                a2 = __fma_rn(wt, ez, a2);
             }
         }
     }
@@ -122,19 +133,44 @@ __device__ __forceinline__ void gather_E(const Geom& g, const double* __restrict
     ep[2] = a2;
 }
 
+// Drift + wrap: x <- wrap(fma(v, dt, x)).  Shared by the
+// push (which kicks first) and the reorder pass (which re-drifts from the kicked
+// velocity the push stored), so both produce bit-identical x'.
+__device__ __forceinline__ void drift(const Geom& g, double x[3], const double v[3]) {
+#pragma unroll
+    for (int d = 0; d < 3; ++d) x[d] = wrap(__fma_rn(v[d], g.dt, x[d]), g.L);
+}
+
 // Gather + leapfrog kick-drift + wrap:
 //   v <- fma(qm_dt, E_p, v) ; x <- wrap(fma(v, dt, x)).
-__device__ __forceinline__ void gather_push(const Geom& g, const double* __restrict__ Ex,
-                                            const double* __restrict__ Ey,
-                                            const double* __restrict__ Ez, double x[3],
-                                            double v[3]) {
+__device__ __forceinline__ void gather_push(const Geom& g, const double* __restrict__ E4,
+                                            double x[3], double v[3]) {
     double ep[3];
-    gather_E(g, Ex, Ey, Ez, x, ep);
+    gather_E(g, E4, x, ep);
 #pragma unroll
-    for (int d = 0; d < 3; ++d) {
-        v[d] = __fma_rn(g.qm_dt, ep[d], v[d]);
-        x[d] = wrap(__fma_rn(v[d], g.dt, x[d]), g.L);
-    }
+    for (int d = 0; d < 3; ++d) v[d] = __fma_rn(g.qm_dt, ep[d], v[d]);
+    drift(g, x, v);
+}
+
+// ------------------------------------------------------- particle layout ----
+// Three streams of 128-bit pairs per particle i: P0 = (x, y), P1 = (z, v_z),
+// P2 = (v_x, v_y).  A scattered gather of one particle touches 3 sectors (6 for
+// plain SoA); the kick rewrites P1 and P2 only.
+struct PState {
+    double2* p[3];
+};
+
+__device__ __forceinline__ void load_particle(const PState& s, int64_t i, double x[3], double v[3]) {
+    const double2 a = __ldg(s.p[0] + i), b = __ldg(s.p[1] + i), c = __ldg(s.p[2] + i);
+    x[0] = a.x; x[1] = a.y; x[2] = b.x;
+    v[0] = c.x; v[1] = c.y; v[2] = b.y;
+}
+
+__device__ __forceinline__ void store_particle(const PState& s, int64_t i, const double x[3],
+                                               const double v[3]) {
+    s.p[0][i] = make_double2(x[0], x[1]);
+    s.p[1][i] = make_double2(x[2], v[2]);
+    s.p[2][i] = make_double2(v[0], v[1]);
 }
 
 // ---------------------------------------------------------------- Philox ----

@@ -176,7 +176,7 @@ def test_steps_zero_and_errors(Sim):
 
     sim = Sim(n=16, ppc=1, half_kick=False)
     assert sim.step(0).size == 0
-    bad = np.zeros((6, sim.np))
+    bad = landau_state(16, 1, seed=2)
     bad[0, 0] = L            # out of [0, L)
     with pytest.raises(PicError):
         sim.set_particles(bad)
