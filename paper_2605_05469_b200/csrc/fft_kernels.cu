@@ -3,11 +3,12 @@
 //   rho (real, pitched)  --x R2C-->  --y FFT-->  --z FFT, E^_d = -i k_d rho^/|k|^2,
 //   3x inverse z-->  --3x inverse y-->  --3x x C2R (+ energy partials)-->  E_d.
 //
-// Every pass is HBM-bound (about 1.7 flop/B in fp64): each CTA stages a batch of
-// lines (a contiguous row segment for x, a (line x TW-column) tile for y and z,
-// so every global access is a contiguous 16*TW-byte run) in shared memory, runs
-// an in-place radix-4 (+ one radix-2) decimation-in-time FFT there with twiddles
-// from a precomputed fp64 table, and writes the lines back.  The spectral
+// Every pass is HBM-bound (about 1.7 flop/B in fp64): each CTA transforms a batch
+// of lines (contiguous rows for x; TW adjacent kx columns for y and z, so every
+// global access is a contiguous 16*TW-byte run) with a radix-8 Stockham FFT whose
+// first stage reads global memory, whose middle stages run in registers with one
+// padded shared-memory exchange each, and whose last stage writes global memory;
+// twiddles come from a precomputed fp64 table W_n^m, m < n.  The spectral
 // multiply and the three inverse z transforms are fused into the z pass, the
 // field-energy partial sums into the C2R x pass.
 #include <cstdio>
@@ -27,56 +28,157 @@ __device__ __forceinline__ double2 cmul(double2 a, double2 b) {
 }
 __device__ __forceinline__ double2 conj2(double2 a) { return make_double2(a.x, -a.y); }
 
-__device__ __forceinline__ unsigned brev(unsigned v, int logn) { return __brev(v) >> (32 - logn); }
 
-// In-place DIT FFT of nl lines of length len = 2^logn in shared memory; line l at
-// buf[l*ls ...].  Input in bit-reversed order, output in natural order.
-// SIGN = -1: forward e^{-i...}; +1: inverse (unnormalised).  tw[m] = W_M^m with
-// M = len << tshift, m < M/2.
+// ---------------------------------------------------------- Stockham FFT --
+// Radix-2/4/8 Stockham autosort FFT of nl lines of length len = 2^logn (natural
+// order in and out).  Stage s (radix R, Ns = product of the earlier radices):
+//   v[r] = in[j + r len/R] * W_{Ns R}^{(j mod Ns) r},  V = DFT_R(v),
+//   out[(j / Ns) Ns R + (j mod Ns) + r Ns] = V[r]          (j < len/R).
+// Stage 0 (the remainder radix 2 or 4, else 8) reads src(l, e) -- global memory
+// or an on-the-fly transform -- and writes shared memory; middle radix-8 stages
+// go through registers and one padded shared round trip each; the last stage
+// writes dst(l, e, v) (global) or, with DST_SMEM, shared memory in natural order.
+// Shared index of element e of line l: l * ls + pidx(e), pidx(e) = e + e/8 (one
+// pad per 8 elements keeps the stride-8 writes of radix-8 stages conflict free).
+__device__ __forceinline__ int pidx(int e) { return e + (e >> 3); }
+__host__ __device__ inline int line_stride(int len) { return len + len / 8 + 1; }
+
 template <int SIGN>
-__device__ void smem_fft(double2* buf, int nl, int logn, int ls, const double2* __restrict__ tw,
-                         int tshift) {
+__device__ __forceinline__ double2 mul_i(double2 a) {   // a * (-i) forward, a * (+i) inverse
+    return SIGN < 0 ? make_double2(a.y, -a.x) : make_double2(-a.y, a.x);
+}
+
+template <int SIGN>
+__device__ __forceinline__ void dft2(double2* v) {
+    const double2 a = v[0], b = v[1];
+    v[0] = cadd(a, b);
+    v[1] = csub(a, b);
+}
+
+template <int SIGN>
+__device__ __forceinline__ void dft4(double2& a0, double2& a1, double2& a2, double2& a3) {
+    const double2 t0 = cadd(a0, a2), t1 = csub(a0, a2);
+    const double2 t2 = cadd(a1, a3), t3 = mul_i<SIGN>(csub(a1, a3));
+    a0 = cadd(t0, t2);
+    a2 = csub(t0, t2);
+    a1 = cadd(t1, t3);
+    a3 = csub(t1, t3);
+}
+
+template <int SIGN>
+__device__ __forceinline__ void dft8(double2* v) {
+    // X[k] = E[k] + W8^k O[k], X[k+4] = E[k] - W8^k O[k]; E, O = DFT4 of evens, odds
+    double2 e0 = v[0], e1 = v[2], e2 = v[4], e3 = v[6];
+    double2 o0 = v[1], o1 = v[3], o2 = v[5], o3 = v[7];
+    dft4<SIGN>(e0, e1, e2, e3);
+    dft4<SIGN>(o0, o1, o2, o3);
+    const double h = 0.70710678118654752440084436210485;
+    // W8^1 = (1 -+ i)/sqrt2, W8^2 = -+i, W8^3 = (-1 -+ i)/sqrt2
+    const double2 w1o1 = SIGN < 0 ? make_double2(h * (o1.x + o1.y), h * (o1.y - o1.x))
+                                  : make_double2(h * (o1.x - o1.y), h * (o1.y + o1.x));
+    const double2 w2o2 = mul_i<SIGN>(o2);
+    const double2 w3o3 = SIGN < 0 ? make_double2(h * (o3.y - o3.x), -h * (o3.x + o3.y))
+                                  : make_double2(-h * (o3.x + o3.y), h * (o3.x - o3.y));
+    v[0] = cadd(e0, o0); v[4] = csub(e0, o0);
+    v[1] = cadd(e1, w1o1); v[5] = csub(e1, w1o1);
+    v[2] = cadd(e2, w2o2); v[6] = csub(e2, w2o2);
+    v[3] = cadd(e3, w3o3); v[7] = csub(e3, w3o3);
+}
+
+template <int SIGN>
+__device__ __forceinline__ void dft_r(double2* v, int R) {
+    if (R == 8) dft8<SIGN>(v);
+    else if (R == 4) dft4<SIGN>(v[0], v[1], v[2], v[3]);
+    else dft2<SIGN>(v);
+}
+
+// tw[m] = W_{N}^m = exp(-2 pi i m / N), m < N; a line of length len uses
+// W_len^q = tw[q << tws], tws = log2(N / len).
+template <int SIGN>
+__device__ __forceinline__ double2 twid(const double2* __restrict__ tw, int q, int tws) {
+    const double2 w = __ldg(tw + (q << tws));
+    return SIGN < 0 ? w : conj2(w);
+}
+
+// IPT = middle-stage work items held per thread (nl * len <= 8 * IPT * blockDim).
+template <int SIGN, bool DST_SMEM, int IPT = 1, class Src, class Dst>
+__device__ void fft_lines(double2* sm, int nl, int logn, int ls, const double2* __restrict__ tw,
+                          int tws, Src src, Dst dst) {
     const int len = 1 << logn;
-    int logh = 0;
-    if (logn & 1) {  // one radix-2 stage, span 2, twiddle 1
-        const int nb = len >> 1;
-        for (int t = threadIdx.x; t < nl * nb; t += blockDim.x) {
-            const int l = t >> (logn - 1), gi = t & (nb - 1);
-            double2* p = buf + l * ls + 2 * gi;
-            const double2 a = p[0], b = p[1];
-            p[0] = cadd(a, b);
-            p[1] = csub(a, b);
+    const int rem = logn % 3;
+    const int logR0 = rem == 0 ? 3 : rem;
+    const int nst = (logn - logR0) / 3 + 1;
+    // ---- stage 0: src -> shared (or dst when it is also the last stage)
+    {
+        const int R = 1 << logR0, nj = len >> logR0;
+        const bool last = nst == 1;
+        for (int it = threadIdx.x; it < nl * nj; it += blockDim.x) {
+            const int l = it % nl, j = it / nl;
+            double2 v[8];
+#pragma unroll
+            for (int r = 0; r < 8; ++r)
+                if (r < R) v[r] = src(l, j + r * nj);
+            dft_r<SIGN>(v, R);
+#pragma unroll
+            for (int r = 0; r < 8; ++r)
+                if (r < R) {
+                    const int e = j * R + r;        // Ns = 1
+                    if (last && !DST_SMEM) dst(l, e, v[r]);
+                    else sm[l * ls + pidx(e)] = v[r];
+                }
         }
-        __syncthreads();
-        logh = 1;
     }
-    // combined radix-2 stages of half-span h and 2h (span 4h), h = 2^logh
-    for (; logh < logn; logh += 2) {
-        const int h = 1 << logh;
-        const int nbl = len >> 2;  // radix-4 butterflies per line
-        const int sh1 = logn - logh - 1 + tshift;   // index of W_{2h}^k = k << sh1
-        const int sh2 = logn - logh - 2 + tshift;   // index of W_{4h}^k = k << sh2
-        for (int t = threadIdx.x; t < nl * nbl; t += blockDim.x) {
-            const int l = t >> (logn - 2), r = t & (nbl - 1);
-            const int gi = r >> logh, k = r & (h - 1);
-            double2* p = buf + l * ls + (gi << (logh + 2)) + k;
-            double2 w1 = __ldg(tw + (k << sh1));
-            double2 w2 = __ldg(tw + (k << sh2));
-            if (SIGN > 0) { w1 = conj2(w1); w2 = conj2(w2); }
-            const double2 a0 = p[0], a1 = p[h], a2 = p[2 * h], a3 = p[3 * h];
-            const double2 t1 = cmul(a1, w1), t3 = cmul(a3, w1);
-            const double2 x0 = cadd(a0, t1), x1 = csub(a0, t1);
-            const double2 x2 = cadd(a2, t3), x3 = csub(a2, t3);
-            const double2 u2 = cmul(x2, w2);
-            double2 u3 = cmul(x3, w2);
-            // times -i (forward) or +i (inverse): W_{4h}^h = e^{-/+ i pi/2}
-            u3 = SIGN < 0 ? make_double2(u3.y, -u3.x) : make_double2(-u3.y, u3.x);
-            p[0] = cadd(x0, u2);
-            p[2 * h] = csub(x0, u2);
-            p[h] = cadd(x1, u3);
-            p[3 * h] = csub(x1, u3);
+    __syncthreads();
+    int logNs = logR0;
+    for (int s = 1; s < nst; ++s) {
+        const int nj = len >> 3, Ns = 1 << logNs;
+        const int tsh = logn - logNs - 3;       // W_{Ns 8}^{q} = W_len^{q << tsh}
+        const bool last = s == nst - 1;
+        if (last && !DST_SMEM) {
+            for (int it = threadIdx.x; it < nl * nj; it += blockDim.x) {
+                const int l = it % nl, j = it / nl;
+                double2 v[8];
+#pragma unroll
+                for (int r = 0; r < 8; ++r) v[r] = sm[l * ls + pidx(j + r * nj)];
+                const int jm = j & (Ns - 1);
+#pragma unroll
+                for (int r = 1; r < 8; ++r) v[r] = cmul(v[r], twid<SIGN>(tw, (jm * r) << tsh, tws));
+                dft8<SIGN>(v);
+                const int base = ((j >> logNs) << (logNs + 3)) + jm;
+#pragma unroll
+                for (int r = 0; r < 8; ++r) dst(l, base + r * Ns, v[r]);
+            }
+        } else {
+            double2 v[IPT][8];
+            int lk[IPT], jk[IPT];
+#pragma unroll
+            for (int k = 0; k < IPT; ++k) {
+                const int it = threadIdx.x + k * blockDim.x;
+                lk[k] = -1;
+                if (it < nl * nj) {
+                    const int l = it % nl, j = it / nl;
+                    lk[k] = l;
+                    jk[k] = j;
+#pragma unroll
+                    for (int r = 0; r < 8; ++r) v[k][r] = sm[l * ls + pidx(j + r * nj)];
+                    const int jm = j & (Ns - 1);
+#pragma unroll
+                    for (int r = 1; r < 8; ++r) v[k][r] = cmul(v[k][r], twid<SIGN>(tw, (jm * r) << tsh, tws));
+                    dft8<SIGN>(v[k]);
+                }
+            }
+            __syncthreads();
+#pragma unroll
+            for (int k = 0; k < IPT; ++k)
+                if (lk[k] >= 0) {
+                    const int j = jk[k], jm = j & (Ns - 1);
+                    const int base = ((j >> logNs) << (logNs + 3)) + jm;
+#pragma unroll
+                    for (int r = 0; r < 8; ++r) sm[lk[k] * ls + pidx(base + r * Ns)] = v[k][r];
+                }
         }
         __syncthreads();
+        logNs += 3;
     }
 }
 
@@ -86,35 +188,31 @@ __host__ __device__ inline int ilog2(int v) {
     return l;
 }
 
-// rows per CTA of the x passes (len = n/2 complex per row)
-__host__ __device__ inline int x_rows(int n) {
-    int r = 4096 / (n / 2);
-    return r < 1 ? 1 : r;
-}
-__host__ __device__ inline int y_tw(int n) { int t = 4096 / n; return t > 8 ? 8 : (t < 1 ? 1 : t); }
+// Elements per CTA: rows of the x passes, TW columns of the y and z passes.
+__host__ __device__ inline int x_rows(int n) { int r = 2048 / (n / 2); return r < 1 ? 1 : r; }
+__host__ __device__ inline int xi_rows(int n) { int r = 1024 / (n / 2); return r < 1 ? 1 : r; }
+__host__ __device__ inline int y_tw(int n) { int t = 2048 / n; return t > 8 ? 8 : (t < 1 ? 1 : t); }
 __host__ __device__ inline int z_tw(int n) { int t = 2048 / n; return t > 8 ? 8 : (t < 1 ? 1 : t); }
 
 // ------------------------------------------------------------ x R2C -------
 // Row r of S0: n reals -> n/2 + 1 complex, in place (the CTA owns its rows).
-__global__ void __launch_bounds__(kThreads) k_fft_x_fwd(Geom g, double* buf,
+// z[m] = x[2m] + i x[2m+1] -> Z = FFT_{n/2}(z) -> X[k] = Ze[k] + W_n^k Zo[k],
+// Ze = (Z[k] + conj Z[n/2-k])/2, Zo = (Z[k] - conj Z[n/2-k])(-i/2).
+__global__ void __launch_bounds__(kThreads, 4) k_fft_x_fwd(Geom g, double* buf,
                                                         const double2* __restrict__ tw) {
     extern __shared__ double2 sm[];
-    const int len = g.n >> 1, logn = ilog2(len), R = x_rows(g.n), ls = len + 1;
+    const int len = g.n >> 1, logn = ilog2(len), R = x_rows(g.n), ls = line_stride(len);
     const int64_t row0 = (int64_t)blockIdx.x * R;
-    const int64_t nrows = (int64_t)g.n * g.n;
-    const int rows = (int)min((int64_t)R, nrows - row0);
-    for (int t = threadIdx.x; t < rows * len; t += blockDim.x) {
-        const int rl = t / len, m = t - rl * len;
-        const double2* src = reinterpret_cast<const double2*>(buf + (row0 + rl) * g.rp);
-        sm[rl * ls + brev(m, logn)] = src[m];
-    }
-    __syncthreads();
-    smem_fft<-1>(sm, rows, logn, ls, tw, 1);
-    // X[k] = Ze[k] + W_n^k Zo[k], Ze = (Z[k] + conj Z[len-k])/2, Zo = (Z[k] - conj Z[len-k])(-i/2)
+    const int rows = (int)min((int64_t)R, (int64_t)g.n * g.n - row0);
+    auto src = [&](int l, int e) {
+        return reinterpret_cast<const double2*>(buf + (row0 + l) * g.rp)[e];
+    };
+    auto dst = [&](int, int, double2) {};
+    fft_lines<-1, true>(sm, rows, logn, ls, tw, 1, src, dst);
     for (int t = threadIdx.x; t < rows * (len + 1); t += blockDim.x) {
         const int rl = t / (len + 1), k = t - rl * (len + 1);
-        const double2 zk = sm[rl * ls + (k & (len - 1))];
-        const double2 zc = conj2(sm[rl * ls + ((len - k) & (len - 1))]);
+        const double2 zk = sm[rl * ls + pidx(k & (len - 1))];
+        const double2 zc = conj2(sm[rl * ls + pidx((len - k) & (len - 1))]);
         const double2 ze = make_double2(0.5 * (zk.x + zc.x), 0.5 * (zk.y + zc.y));
         const double2 d = csub(zk, zc);
         const double2 zo = make_double2(0.5 * d.y, -0.5 * d.x);
@@ -127,80 +225,68 @@ __global__ void __launch_bounds__(kThreads) k_fft_x_fwd(Geom g, double* buf,
 
 // ------------------------------------------------------------- y pass ------
 // blockIdx.x = z * ntiles + tile, blockIdx.y = component.  Lines along y of TW
-// consecutive kx columns (valid columns kx <= n/2).
+// consecutive kx columns (valid columns kx <= n/2), in place: the first stage
+// reads the whole tile before the last stage writes it.
 template <int SIGN>
-__global__ void __launch_bounds__(kThreads) k_fft_y(Geom g, double* b0, double* b1, double* b2,
+__global__ void __launch_bounds__(kThreads, 3) k_fft_y(Geom g, double* b0, double* b1, double* b2,
                                                     const double2* __restrict__ tw) {
     extern __shared__ double2 sm[];
     double2* buf = reinterpret_cast<double2*>(blockIdx.y == 0 ? b0 : (blockIdx.y == 1 ? b1 : b2));
-    const int n = g.n, logn = ilog2(n), TW = y_tw(n), ls = n + 1;
+    const int n = g.n, logn = ilog2(n), TW = y_tw(n), ls = line_stride(n);
     const int ntiles = (n / 2 + 1 + TW - 1) / TW;
     const int z = blockIdx.x / ntiles, kx0 = (blockIdx.x - z * ntiles) * TW;
     const int ncol = min(TW, n / 2 + 1 - kx0);
-    for (int t = threadIdx.x; t < n * TW; t += blockDim.x) {
-        const int y = t / TW, c = t - y * TW;
-        if (c < ncol) sm[c * ls + brev(y, logn)] = buf[((int64_t)z * n + y) * g.px + kx0 + c];
-    }
-    __syncthreads();
-    smem_fft<SIGN>(sm, ncol, logn, ls, tw, 0);
-    for (int t = threadIdx.x; t < n * TW; t += blockDim.x) {
-        const int y = t / TW, c = t - y * TW;
-        if (c < ncol) buf[((int64_t)z * n + y) * g.px + kx0 + c] = sm[c * ls + y];
-    }
+    double2* base = buf + (int64_t)z * n * g.px + kx0;
+    auto src = [&](int l, int e) { return l < ncol ? base[(int64_t)e * g.px + l] : make_double2(0.0, 0.0); };
+    auto dst = [&](int l, int e, double2 v) { if (l < ncol) base[(int64_t)e * g.px + l] = v; };
+    fft_lines<SIGN, false>(sm, TW, logn, ls, tw, 0, src, dst);
 }
 
 // --------------------------------------------------- z pass + multiply -----
-// blockIdx.x = ky * ntiles + tile.  Forward z FFT of rho^, then for d = x, y, z:
-// E^_d = -i k_d rho^ / |k|^2 * scale (zero at n = 0 and where n_d = -N/2, D#6),
-// inverse z FFT, store: E^_x -> S1, E^_y -> S2, E^_z -> S0 (the CTA's own input
-// tile, already staged in shared memory).
-__global__ void __launch_bounds__(kThreads) k_fft_z_mul(Geom g, double2* rho, double2* e1,
+// blockIdx.x = ky * ntiles + tile.  Forward z FFT of rho^ into shared memory,
+// then for d = x, y, z an inverse z FFT whose first stage reads
+// E^_d = -i k_d rho^ / |k|^2 * scale (zero at n = 0 and where n_d = -N/2, D#6)
+// straight from it; stores E^_x -> S1, E^_y -> S2, E^_z -> S0 (the CTA's own,
+// already consumed, input tile).
+__global__ void __launch_bounds__(kThreads, 2) k_fft_z_mul(Geom g, double2* rho, double2* e1,
                                                         double2* e2, double scale,
                                                         const double2* __restrict__ tw) {
     extern __shared__ double2 sm[];
-    double2* out[3] = {e1, e2, rho};
-    const int n = g.n, logn = ilog2(n), TW = z_tw(n), ls = n + 1;
+    const int n = g.n, logn = ilog2(n), TW = z_tw(n), ls = line_stride(n);
     double2* s1 = sm;
     double2* s2 = sm + TW * ls;
     const int ntiles = (n / 2 + 1 + TW - 1) / TW;
     const int ky = blockIdx.x / ntiles, kx0 = (blockIdx.x - ky * ntiles) * TW;
     const int ncol = min(TW, n / 2 + 1 - kx0);
     const int64_t zstride = (int64_t)n * g.px;
-    const int64_t base = (int64_t)ky * g.px + kx0;
-    for (int t = threadIdx.x; t < n * TW; t += blockDim.x) {
-        const int z = t / TW, c = t - z * TW;
-        if (c < ncol) s1[c * ls + brev(z, logn)] = rho[base + z * zstride + c];
+    const int64_t off = (int64_t)ky * g.px + kx0;
+    {
+        auto src = [&](int l, int e) { return l < ncol ? rho[off + e * zstride + l] : make_double2(0.0, 0.0); };
+        auto dst = [&](int, int, double2) {};
+        fft_lines<-1, true>(s1, TW, logn, ls, tw, 0, src, dst);
     }
-    __syncthreads();
-    smem_fft<-1>(s1, ncol, logn, ls, tw, 0);
     const double kf = 6.283185307179586476925286766559 / g.L;
     const int half = n / 2;
     const double kyv = kf * (double)(ky < half ? ky : ky - n);
     for (int d = 0; d < 3; ++d) {
-        for (int t = threadIdx.x; t < n * TW; t += blockDim.x) {
-            const int kz = t / TW, c = t - kz * TW;
-            if (c >= ncol) continue;
-            const int kx = kx0 + c;
+        double2* out = d == 0 ? e1 : (d == 1 ? e2 : rho);
+        auto src = [&](int l, int kz) {
+            const int kx = kx0 + l;
             const double kxv = kf * (double)(kx < half ? kx : kx - n);
             const double kzv = kf * (double)(kz < half ? kz : kz - n);
             const double k2 = kxv * kxv + kyv * kyv + kzv * kzv;
             const int idx = d == 0 ? kx : (d == 1 ? ky : kz);
             const double kd = d == 0 ? kxv : (d == 1 ? kyv : kzv);
             double2 e = make_double2(0.0, 0.0);
-            if (k2 != 0.0 && idx != half) {
-                const double2 r = s1[c * ls + kz];
+            if (l < ncol && k2 != 0.0 && idx != half) {
+                const double2 r = s1[l * ls + pidx(kz)];
                 const double f = kd * scale / k2;
                 e = make_double2(f * r.y, -f * r.x);   // -i k_d rho^ / |k|^2
             }
-            s2[c * ls + brev(kz, logn)] = e;
-        }
-        __syncthreads();
-        smem_fft<+1>(s2, ncol, logn, ls, tw, 0);
-        for (int t = threadIdx.x; t < n * TW; t += blockDim.x) {
-            const int z = t / TW, c = t - z * TW;
-            if (c < ncol) out[d][base + z * zstride + c] = s2[c * ls + z];
-        }
-        __syncthreads();
+            return e;
+        };
+        auto dst = [&](int l, int z, double2 v) { if (l < ncol) out[off + z * zstride + l] = v; };
+        fft_lines<+1, false>(s2, TW, logn, ls, tw, 0, src, dst);
     }
 }
 
@@ -208,41 +294,38 @@ __global__ void __launch_bounds__(kThreads) k_fft_z_mul(Geom g, double2* rho, do
 // R rows of all three components per CTA: n/2 + 1 complex -> n reals each,
 // written as node records E4[row][x] = (E_x, E_y, E_z, 0) with 256-bit stores;
 // per-CTA partial sums of E_d^2 -> partials[d * gridDim.x + blockIdx.x].
-__host__ __device__ inline int xi_rows(int n) { int r = 1024 / (n / 2); return r < 1 ? 1 : r; }
-
+// Z[k] = (X[k] + conj X[n/2-k]) + i (X[k] - conj X[n/2-k]) W_n^{-k} (unnormalised).
 __device__ __forceinline__ void st_node(double* p, double a, double b, double c) {
     asm volatile("st.global.v4.f64 [%0], {%1, %2, %3, %4};" ::"l"(p), "d"(a), "d"(b), "d"(c), "d"(0.0)
                  : "memory");
 }
 
-__global__ void __launch_bounds__(kThreads) k_fft_x_inv(Geom g, const double* b0, const double* b1,
+__global__ void __launch_bounds__(kThreads, 3) k_fft_x_inv(Geom g, const double* b0, const double* b1,
                                                         const double* b2, double* __restrict__ E4,
                                                         const double2* __restrict__ tw,
                                                         double* __restrict__ partials) {
     extern __shared__ double2 sm[];
     __shared__ double red[3][kThreads / 32];
-    const int len = g.n >> 1, logn = ilog2(len), R = xi_rows(g.n), ls = len + 1;
+    const int len = g.n >> 1, logn = ilog2(len), R = xi_rows(g.n), ls = line_stride(len);
     const int64_t row0 = (int64_t)blockIdx.x * R;
     const int rows = (int)min((int64_t)R, (int64_t)g.n * g.n - row0);
-    // Z[k] = (X[k] + conj X[len-k]) + i (X[k] - conj X[len-k]) W_n^{-k}, k < len
-    for (int t = threadIdx.x; t < 3 * rows * len; t += blockDim.x) {
-        const int l = t / len, k = t - l * len;           // line l = d * rows + rl
-        const int d = l / rows, rl = l - d * rows;
+    auto src = [&](int l, int k) {          // line l = rl * 3 + d
+        const int rl = l / 3, d = l - 3 * rl;
         const double* buf = d == 0 ? b0 : (d == 1 ? b1 : b2);
         const double2* X = reinterpret_cast<const double2*>(buf + (row0 + rl) * g.rp);
         const double2 xk = X[k], xc = conj2(X[len - k]);
         const double2 ze = cadd(xk, xc);
         const double2 zo = cmul(csub(xk, xc), conj2(__ldg(tw + k)));
-        sm[l * ls + brev(k, logn)] = make_double2(ze.x - zo.y, ze.y + zo.x);
-    }
-    __syncthreads();
-    smem_fft<+1>(sm, 3 * rows, logn, ls, tw, 1);
+        return make_double2(ze.x - zo.y, ze.y + zo.x);
+    };
+    auto dst = [&](int, int, double2) {};
+    fft_lines<+1, true, 2>(sm, 3 * rows, logn, ls, tw, 1, src, dst);
     double e2[3] = {0.0, 0.0, 0.0};
     for (int t = threadIdx.x; t < rows * len; t += blockDim.x) {
         const int rl = t / len, m = t - rl * len;
-        const double2 vx = sm[(0 * rows + rl) * ls + m];
-        const double2 vy = sm[(1 * rows + rl) * ls + m];
-        const double2 vz = sm[(2 * rows + rl) * ls + m];
+        const double2 vx = sm[(3 * rl + 0) * ls + pidx(m)];
+        const double2 vy = sm[(3 * rl + 1) * ls + pidx(m)];
+        const double2 vz = sm[(3 * rl + 2) * ls + pidx(m)];
         double* node = E4 + 4 * ((row0 + rl) * g.n + 2 * m);
         st_node(node, vx.x, vy.x, vz.x);
         st_node(node + 4, vx.y, vy.y, vz.y);
@@ -310,7 +393,7 @@ int energy_partials(const Geom& g) {
 
 void launch_fft_x_fwd(const Geom& g, double* S0, const double2* tw, cudaStream_t s) {
     const int len = g.n / 2, R = x_rows(g.n);
-    const size_t smem = sizeof(double2) * (size_t)R * (len + 1);
+    const size_t smem = sizeof(double2) * (size_t)R * line_stride(len);
     const int64_t nrows = (int64_t)g.n * g.n;
     k_fft_x_fwd<<<(unsigned)((nrows + R - 1) / R), kThreads, smem, s>>>(g, S0, tw);
 }
@@ -318,7 +401,7 @@ void launch_fft_x_fwd(const Geom& g, double* S0, const double2* tw, cudaStream_t
 void launch_fft_y(const Geom& g, double* const buf[3], int ncomp, int inverse, const double2* tw,
                   cudaStream_t s) {
     const int TW = y_tw(g.n), ntiles = (g.n / 2 + 1 + TW - 1) / TW;
-    const size_t smem = sizeof(double2) * (size_t)TW * (g.n + 1);
+    const size_t smem = sizeof(double2) * (size_t)TW * line_stride(g.n);
     dim3 grid(g.n * ntiles, ncomp);
     if (inverse) k_fft_y<+1><<<grid, kThreads, smem, s>>>(g, buf[0], buf[1], buf[2], tw);
     else k_fft_y<-1><<<grid, kThreads, smem, s>>>(g, buf[0], buf[1], buf[2], tw);
@@ -327,7 +410,7 @@ void launch_fft_y(const Geom& g, double* const buf[3], int ncomp, int inverse, c
 void launch_fft_z_mul(const Geom& g, double* S0, double* S1, double* S2, double scale,
                       const double2* tw, cudaStream_t s) {
     const int TW = z_tw(g.n), ntiles = (g.n / 2 + 1 + TW - 1) / TW;
-    const size_t smem = 2 * sizeof(double2) * (size_t)TW * (g.n + 1);
+    const size_t smem = 2 * sizeof(double2) * (size_t)TW * line_stride(g.n);
     k_fft_z_mul<<<g.n * ntiles, kThreads, smem, s>>>(
         g, reinterpret_cast<double2*>(S0), reinterpret_cast<double2*>(S1),
         reinterpret_cast<double2*>(S2), scale, tw);
@@ -336,7 +419,7 @@ void launch_fft_z_mul(const Geom& g, double* S0, double* S1, double* S2, double 
 void launch_fft_x_inv(const Geom& g, const double* const spec[3], double* E4, const double2* tw,
                       double* partials, cudaStream_t s) {
     const int len = g.n / 2, R = xi_rows(g.n);
-    const size_t smem = 3 * sizeof(double2) * (size_t)R * (len + 1);
+    const size_t smem = 3 * sizeof(double2) * (size_t)R * line_stride(len);
     k_fft_x_inv<<<energy_partials(g), kThreads, smem, s>>>(g, spec[0], spec[1], spec[2], E4, tw, partials);
 }
 

@@ -15,7 +15,7 @@ namespace pic {
 //   S1, S2 : out of the z pass: E^_x, E^_y (then their y-inverses).
 //   E4     : out: node records (E_x, E_y, E_z, 0), [n][n][n][4].
 //   scale  : factor of the spectral multiply (q/h^3 / N^3 for raw weight sums).
-//   tw     : twiddle table W_n^m = exp(-2 pi i m / n), m < n/2.
+//   tw     : twiddle table W_n^m = exp(-2 pi i m / n), m < n.
 //   partials: 3 * energy_partials(g) doubles; energies: 2 doubles out
 //            (W_x, W) = 1/2 h^3 sum E_x^2, 1/2 h^3 sum |E|^2.
 int energy_partials(const Geom& g);

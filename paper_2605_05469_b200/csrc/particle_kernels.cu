@@ -146,9 +146,12 @@ __global__ void __launch_bounds__(kThreads) k_push_key_brick(Geom g, PState cur,
     }
     const uint32_t P0 = __ldg(offs + c0), P1 = __ldg(offs + c0 + kBrick);
     __syncthreads();
+    double xn[3], vn[3];
+    if (P0 + t < P1) load_particle(cur, P0 + t, xn, vn);
     for (uint32_t i = P0 + t; i < P1; i += kThreads) {
-        double x[3], v[3];
-        load_particle(cur, i, x, v);
+        double x[3] = {xn[0], xn[1], xn[2]}, v[3] = {vn[0], vn[1], vn[2]};
+        // next particle's loads in flight while this one waits on its count atomic
+        if (i + kThreads < P1) load_particle(cur, i + kThreads, xn, vn);
         const double z0 = x[2];
         // CIC gather from the tile: same weights, corner order and fma chain as gather_E
         int ii[3];

@@ -140,7 +140,7 @@ size_t carve(pic_ctx* c, const Geom& g, int64_t np, char* base) {
     char* s1 = take(grid_bytes);
     char* s2 = take(grid_bytes);
     char* e4 = take(sizeof(double) * 4 * (size_t)ncell);
-    char* tw = take(sizeof(double2) * (size_t)(g.n / 2));
+    char* tw = take(sizeof(double2) * (size_t)g.n);
     char* pa = take(sizeof(double) * 3 * (size_t)pic::energy_partials(g));
     char* en = take(sizeof(double) * 2 * kMaxEnergySteps);
     char* ef = take(sizeof(int) * 4);
@@ -379,8 +379,8 @@ pic_status pic_init(const pic_params* p, int32_t rank, int32_t nranks, const uin
         return s;
     };
     // twiddles W_n^m = exp(-2 pi i m / n), m < n/2
-    std::vector<double2> tw(g.n / 2);
-    for (int m = 0; m < g.n / 2; ++m) {
+    std::vector<double2> tw(g.n);   // W_n^m = exp(-2 pi i m / n), m < n
+    for (int m = 0; m < g.n; ++m) {
         const double ang = 2.0 * M_PI * (double)m / (double)g.n;
         tw[m] = make_double2(std::cos(ang), -std::sin(ang));
     }
