@@ -16,6 +16,7 @@
 // storing x' in push_key (24 B/particle less traffic), and reorder_deposit does
 // no field gather at the scattered pre-sort positions.
 #include <algorithm>
+#include <cstdlib>
 
 #include "kernels.h"
 
@@ -27,6 +28,7 @@ constexpr int kThreads = 256;
 constexpr int kBrick = 256;     // cells per reorder/deposit CTA (Morton 8 bits)
 constexpr int kCap = 2048;      // particles staged per chunk (29 B of shared memory each)
 constexpr int kBatch = 2;       // particles per thread with loads in flight together
+__constant__ int g_dbg_mode = 0;   // experiment switch (0 = the method)
 
 // ---------------------------------------------------------------- init -----
 // Landau initial condition: x_d by Newton on the inverse CDF of
@@ -315,9 +317,21 @@ __global__ void __launch_bounds__(kThreads) k_place(const uint32_t* __restrict__
                                                     const uint16_t* __restrict__ rank, int64_t np,
                                                     const uint32_t* __restrict__ offs,
                                                     uint32_t* __restrict__ perm) {
-    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= np) return;
-    perm[__ldg(offs + __ldg(key + i)) + __ldg(rank + i)] = (uint32_t)i;
+    // 4 particles per thread: 16-byte key and 8-byte rank loads, 4 offset lookups in flight
+    const int64_t i0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * 4;
+    if (i0 >= np) return;
+    if (i0 + 4 <= np) {
+        const uint4 k4 = __ldg(reinterpret_cast<const uint4*>(key + i0));
+        const uint2 r4 = __ldg(reinterpret_cast<const uint2*>(rank + i0));
+        const uint32_t o0 = __ldg(offs + k4.x), o1 = __ldg(offs + k4.y);
+        const uint32_t o2 = __ldg(offs + k4.z), o3 = __ldg(offs + k4.w);
+        perm[o0 + (r4.x & 0xffffu)] = (uint32_t)i0;
+        perm[o1 + (r4.x >> 16)] = (uint32_t)(i0 + 1);
+        perm[o2 + (r4.y & 0xffffu)] = (uint32_t)(i0 + 2);
+        perm[o3 + (r4.y >> 16)] = (uint32_t)(i0 + 3);
+    } else {
+        for (int64_t i = i0; i < np; ++i) perm[__ldg(offs + __ldg(key + i)) + __ldg(rank + i)] = (uint32_t)i;
+    }
 }
 
 // ------------------------------------------------- reorder + push + deposit -
@@ -334,16 +348,18 @@ __global__ void __launch_bounds__(kThreads) k_place(const uint32_t* __restrict__
 // After the last chunk the 256 cells' sums are folded into the 9 x 9 x 5 node
 // tile (eight conflict-free passes) and flushed with one fp64 RED.ADD per node.
 // No atomics and no shuffles inside the CTA: the per-brick charge is deterministic.
-template <bool PUSH>
-__global__ void __launch_bounds__(kThreads, 3) k_reorder_deposit(
+// FRAC_SMEM: keep the fractional offsets of the new positions in shared memory
+// (24 B per staged particle) for the per-cell sums; otherwise re-read x' from L2.
+template <bool PUSH, bool FRAC_SMEM, int KB = kBatch>
+__global__ void __launch_bounds__(kThreads, KB > 2 ? 2 : (FRAC_SMEM ? 3 : 4)) k_reorder_deposit(
     Geom g, const uint32_t* __restrict__ offs, const uint32_t* __restrict__ perm, PState cur,
     PState nxt, double* __restrict__ rho, int* __restrict__ err) {
     extern __shared__ double dyn_smem[];
-    double(*sfrac)[kCap] = reinterpret_cast<double(*)[kCap]>(dyn_smem);      // [3][kCap]
-    double* tile = dyn_smem + 3 * kCap;                                        // [9*9*5]
-    uint32_t* sperm = reinterpret_cast<uint32_t*>(tile + 9 * 9 * 5);          // [kCap]
-    uint32_t* soffs = sperm + kCap;                                            // [kBrick + 1]
-    uint8_t* scell = reinterpret_cast<uint8_t*>(soffs + kBrick + 1);           // [kCap]
+    double* tile = dyn_smem;                                                         // [9*9*5]
+    double(*sfrac)[kCap] = reinterpret_cast<double(*)[kCap]>(dyn_smem + 9 * 9 * 5);  // [3][kCap]
+    uint32_t* sperm = reinterpret_cast<uint32_t*>(dyn_smem + 9 * 9 * 5 + (FRAC_SMEM ? 3 * kCap : 0));
+    uint32_t* soffs = sperm + kCap;                                                  // [kBrick + 1]
+    uint8_t* scell = reinterpret_cast<uint8_t*>(soffs + kBrick + 1);                 // [kCap]
     const int t = threadIdx.x;
     const uint32_t c0 = blockIdx.x * kBrick;
     int bx, by, bz;
@@ -378,11 +394,11 @@ __global__ void __launch_bounds__(kThreads, 3) k_reorder_deposit(
         for (int p = s0; p < s1; ++p) scell[p] = (uint8_t)t;
         __syncthreads();
         // B, kBatch positions per thread at a time: all their gathers in flight together
-        for (int pb = t; pb < cnt; pb += kBatch * kThreads) {
-            int o[kBatch];
-            uint32_t j[kBatch];
+        for (int pb = t; pb < cnt; pb += KB * kThreads) {
+            int o[KB];
+            uint32_t j[KB];
 #pragma unroll
-            for (int k = 0; k < kBatch; ++k) {
+            for (int k = 0; k < KB; ++k) {
                 const int p = pb + k * kThreads;
                 o[k] = -1;
                 if (p < cnt) {
@@ -390,35 +406,52 @@ __global__ void __launch_bounds__(kThreads, 3) k_reorder_deposit(
                     const int q0 = (int)(soffs[c] - P0), q1 = (int)(soffs[c + 1] - P0);
                     j[k] = sperm[p];
                     int r = 0;
-                    for (int q = q0; q < q1; ++q) r += sperm[q] < j[k];
+                    if (g_dbg_mode == 1) r = p - q0;
+                    else for (int q = q0; q < q1; ++q) r += sperm[q] < j[k];
                     o[k] = q0 + r;
                 }
             }
-            double2 a[kBatch], b[kBatch], e[kBatch];
+            double2 a[KB], b[KB], e[KB];
 #pragma unroll
-            for (int k = 0; k < kBatch; ++k)
+            for (int k = 0; k < KB; ++k)
                 if (o[k] >= 0) {
                     a[k] = __ldg(cur.p[0] + j[k]);
                     b[k] = __ldg(cur.p[1] + j[k]);
                     e[k] = __ldg(cur.p[2] + j[k]);
                 }
 #pragma unroll
-            for (int k = 0; k < kBatch; ++k)
+            for (int k = 0; k < KB; ++k)
                 if (o[k] >= 0) {
                     double x[3] = {a[k].x, a[k].y, b[k].x}, v[3] = {e[k].x, e[k].y, b[k].y};
                     if (PUSH) drift(g, x, v);    // v is already kicked (push_key)
                     store_particle(nxt, (int64_t)P0 + o[k], x, v);
+                    if (FRAC_SMEM) {
 #pragma unroll
-                    for (int d = 0; d < 3; ++d) {
-                        const double sd = __dmul_rn(x[d], g.inv_h);
-                        sfrac[d][o[k]] = __dsub_rn(sd, (double)cell_of(sd, g.n));
+                        for (int d = 0; d < 3; ++d) {
+                            const double sd = __dmul_rn(x[d], g.inv_h);
+                            sfrac[d][o[k]] = __dsub_rn(sd, (double)cell_of(sd, g.n));
+                        }
                     }
                 }
         }
         __syncthreads();
         // C
-        for (int p = s0; p < s1; ++p) {
-            const double fx = sfrac[0][p], fy = sfrac[1][p], fz = sfrac[2][p];
+        for (int p = s0; p < (g_dbg_mode == 1 ? s0 : s1); ++p) {
+            double fx, fy, fz;
+            if (FRAC_SMEM) {
+                fx = sfrac[0][p]; fy = sfrac[1][p]; fz = sfrac[2][p];
+            } else {   // this block's own stores, visible after the barrier; L2 reads
+                const double2 xy = __ldcg(nxt.p[0] + P0 + p);
+                const double2 zv = __ldcg(nxt.p[1] + P0 + p);
+                const double x3[3] = {xy.x, xy.y, zv.x};
+                double f3[3];
+#pragma unroll
+                for (int d = 0; d < 3; ++d) {
+                    const double sd = __dmul_rn(x3[d], g.inv_h);
+                    f3[d] = __dsub_rn(sd, (double)cell_of(sd, g.n));
+                }
+                fx = f3[0]; fy = f3[1]; fz = f3[2];
+            }
             const double wx[2] = {__dsub_rn(1.0, fx), fx}, wy[2] = {__dsub_rn(1.0, fy), fy},
                          wz[2] = {__dsub_rn(1.0, fz), fz};
 #pragma unroll
@@ -475,7 +508,19 @@ __global__ void __launch_bounds__(kThreads) k_sort_segments(const uint32_t* __re
 
 inline unsigned blocks(int64_t n, int t) { return (unsigned)((n + t - 1) / t); }
 
-constexpr size_t kReorderSmem = sizeof(double) * (3 * kCap + 9 * 9 * 5) + sizeof(uint32_t) * (kCap + kBrick + 1) + kCap;
+constexpr size_t reorder_smem(bool frac) {
+    return sizeof(double) * ((frac ? 3 * kCap : 0) + 9 * 9 * 5) + sizeof(uint32_t) * (kCap + kBrick + 1) + kCap;
+}
+int g_reorder_variant = -1;   // 1: fractional offsets staged in shared memory, 0: re-read from L2
+bool reorder_frac_smem() {
+    if (g_reorder_variant < 0) {
+        const char* e = getenv("PIC_REORDER_FRAC_SMEM");
+        g_reorder_variant = e ? atoi(e) != 0 : 1;
+        const char* m = getenv("PIC_DBG_MODE");
+        if (m) { int v = atoi(m); cudaMemcpyToSymbol(g_dbg_mode, &v, sizeof(int)); }
+    }
+    return g_reorder_variant != 0;
+}
 
 }  // namespace
 
@@ -528,21 +573,36 @@ void launch_scan(const uint32_t* count, uint32_t* offs, int64_t ncell, uint32_t*
 void launch_place(const uint32_t* key, const uint16_t* rank, int64_t np, const uint32_t* offs,
                   uint32_t* perm, cudaStream_t s) {
     if (np == 0) return;
-    k_place<<<blocks(np, kThreads), kThreads, 0, s>>>(key, rank, np, offs, perm);
+    k_place<<<blocks((np + 3) / 4, kThreads), kThreads, 0, s>>>(key, rank, np, offs, perm);
 }
 
 void launch_reorder_deposit(const Geom& g, const uint32_t* offs, const uint32_t* perm, PState cur,
                             PState nxt, int push, double* rho_buf, int* err_flag, cudaStream_t s) {
     const unsigned nbrick = (unsigned)(((int64_t)g.n * g.n * g.n) / kBrick);
-    if (push)
-        k_reorder_deposit<true><<<nbrick, kThreads, kReorderSmem, s>>>(g, offs, perm, cur, nxt, rho_buf, err_flag);
+    const bool fs = reorder_frac_smem();
+    const size_t sm = reorder_smem(fs);
+    static const int kb = getenv("PIC_REORDER_KB") ? atoi(getenv("PIC_REORDER_KB")) : 4;
+    if (push && fs && kb == 4)
+        k_reorder_deposit<true, true, 4><<<nbrick, kThreads, sm, s>>>(g, offs, perm, cur, nxt, rho_buf, err_flag);
+    else if (push && fs && kb == 8)
+        k_reorder_deposit<true, true, 8><<<nbrick, kThreads, sm, s>>>(g, offs, perm, cur, nxt, rho_buf, err_flag);
+    else if (push && fs)
+        k_reorder_deposit<true, true><<<nbrick, kThreads, sm, s>>>(g, offs, perm, cur, nxt, rho_buf, err_flag);
+    else if (push)
+        k_reorder_deposit<true, false><<<nbrick, kThreads, sm, s>>>(g, offs, perm, cur, nxt, rho_buf, err_flag);
+    else if (fs)
+        k_reorder_deposit<false, true><<<nbrick, kThreads, sm, s>>>(g, offs, perm, cur, nxt, rho_buf, err_flag);
     else
-        k_reorder_deposit<false><<<nbrick, kThreads, kReorderSmem, s>>>(g, offs, perm, cur, nxt, rho_buf, err_flag);
+        k_reorder_deposit<false, false><<<nbrick, kThreads, sm, s>>>(g, offs, perm, cur, nxt, rho_buf, err_flag);
 }
 
 void particles_set_smem_limits() {
-    cudaFuncSetAttribute(k_reorder_deposit<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kReorderSmem);
-    cudaFuncSetAttribute(k_reorder_deposit<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kReorderSmem);
+    cudaFuncSetAttribute(k_reorder_deposit<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)reorder_smem(true));
+    cudaFuncSetAttribute(k_reorder_deposit<true, true, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)reorder_smem(true));
+    cudaFuncSetAttribute(k_reorder_deposit<true, true, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)reorder_smem(true));
+    cudaFuncSetAttribute(k_reorder_deposit<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)reorder_smem(true));
+    cudaFuncSetAttribute(k_reorder_deposit<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)reorder_smem(false));
+    cudaFuncSetAttribute(k_reorder_deposit<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)reorder_smem(false));
 }
 
 void launch_sort_segments(const uint32_t* offs, int64_t ncell, uint32_t* perm, cudaStream_t s) {

@@ -1,0 +1,97 @@
+"""GPU checks at the benchmark's full size (512^3 x 8 ppc = 1,073,741,824 particles,
+the configuration bench.py times) and the physics pin on the GPU.
+
+At full size the oracle cannot run the whole step, so:
+  * sampled outputs the oracle computes one by one: 100,000 random particles are
+    pushed by the oracle's gather + push with the field the GPU solved, and must
+    match the GPU's sorted output bit-for-bit (located through the permutation);
+  * sampled Fourier modes: E^_x(n) = -i k_x rho^(n)/|k|^2 by direct separable DFT
+    sums of the GPU's rho and E (D#6);
+  * properties that hold at any size: charge conservation, keys sorted,
+    permutation valid, all positions in [0, L).
+"""
+import os
+
+import numpy as np
+import pytest
+
+from oracle import oracle as O
+from landau_fit import dispersion_root, fit_damping_rate
+
+pytestmark = pytest.mark.gpu
+
+K = 0.5
+L = 2 * np.pi / K
+DT = 0.05
+
+
+def _dft_mode(f, n, m):
+    """sum_{x} f(x) e^{-2 pi i m.x / n} for one mode m = (mx, my, mz), f[iz, iy, ix]."""
+    ph = lambda k: np.exp(-2j * np.pi * k * np.arange(n) / n)
+    return np.einsum("zyx,x,y,z->", f, ph(m[0]), ph(m[1]), ph(m[2]), optimize=True)
+
+
+@pytest.mark.slow
+def test_fullsize_512_sampled_parity():
+    import torch
+    from paper_2605_05469_b200 import Simulation
+
+    torch.cuda.set_device(0)
+    n, ppc = int(os.environ.get("PIC_FULLSIZE_N", "512")), 8
+    sim = Simulation(n=n, ppc=ppc, seed=1)
+    sim.step(2)
+    xv0 = sim.get_particles()                 # canonical state (x_n, v_{n-1/2})
+    rho0 = sim.get_grid(0)                    # charge of x_n (deposited by the last step)
+    sim.step(1)                               # solve E_n, push, sort, deposit
+    E = np.stack([sim.get_grid(d) for d in (1, 2, 3)])
+    rho = sim.get_grid(0)                     # charge of x_{n+1}
+    _, perm = sim.keys_perm()
+    xv1 = sim.get_particles()
+    np_ = xv0.shape[1]
+    # permutation valid; sampled particles bit-exact vs the oracle's push
+    assert perm.shape == (np_,)
+    inv = np.empty(np_, dtype=np.int64)
+    inv[perm] = np.arange(np_)
+    rng = np.random.default_rng(0)
+    S = rng.choice(np_, size=100_000, replace=False)
+    xs = np.ascontiguousarray(xv0[:, S])
+    Ep = O.gather(n, L, xs, E)
+    ref = O.push(L, xs, Ep, -DT, DT)
+    got = xv1[:, inv[S]]
+    assert np.array_equal(got, ref)
+    # keys of the new state non-decreasing (stable sort by Morton cell key, D#14)
+    keys = O.keys(n, L, xv1)
+    assert np.all(keys[1:] >= keys[:-1])
+    assert np.all((xv1[:3] >= 0) & (xv1[:3] < L))
+    # charge conservation: sum rho h^3 = N_p q = -L^3
+    assert abs(rho.sum() * (L / n) ** 3 + L ** 3) < 1e-12 * L ** 3
+    # sampled modes of the solve (D#6): E^_d(m) = -i k_d rho0^(m) / |k|^2 by direct
+    # separable DFT sums of the GPU's rho_n and E_n; DFT rounding ~ eps * sqrt(N^3) * ||E||
+    for m in [(1, 0, 0), (0, 1, 0), (0, 0, 1), (3, 5, 7), (n // 2 - 1, 2, 1), (5, n - 3, n // 2 + 4)]:
+        kv = [2 * np.pi * (mi if mi < n // 2 else mi - n) / L for mi in m]
+        k2 = sum(k * k for k in kv)
+        rh = _dft_mode(rho0, n, m)
+        for d in range(3):
+            want = -1j * kv[d] * rh / k2
+            got = _dft_mode(E[d], n, m)
+            assert abs(got - want) <= 1e-10 * np.sqrt((E[d] ** 2).sum()) + 1e-12 * abs(want)
+    sim.close()
+
+
+@pytest.mark.slow
+def test_landau_damping_rate_gpu_128():
+    """P:231-232, BJ: 128^3 x 8 ppc, alpha = 0.05, 400 steps: slope 2 gamma
+    within 10%, peak spacing pi/omega_r within 5% (D#20, D#21)."""
+    import torch
+    from paper_2605_05469_b200 import Simulation
+
+    torch.cuda.set_device(0)
+    w = dispersion_root(0.5)
+    sim = Simulation(n=128, ppc=8, seed=1)
+    ex = sim.step(400)
+    t = np.arange(400) * DT
+    slope, npk, tp = fit_damping_rate(t, ex, t_max=14.0)
+    assert npk >= 4
+    assert abs(slope - 2 * w.imag) < 0.10 * abs(2 * w.imag), slope
+    assert abs(np.mean(np.diff(tp)) - np.pi / w.real) < 0.05 * np.pi / w.real
+    sim.close()
