@@ -33,15 +33,15 @@ UNIT = "particle-pushes/s"
 # Algorithmic bytes per launch:
 # per particle, per grid node (ncell = N^3).
 ALG_BYTES = {
-    "reorder_deposit": (4 + 48 + 48, 4 + 16 + 24),  # perm, x/v gather, x/v store | offs, rho RMW, E
-    "push_key": (48 + 4, 24 + 4),                    # x/v read, key | E read, count RMW (amortised)
-    "place": (4 + 4, 4),                             # key read, perm write | cursor
+    "reorder_deposit": (4 + 48 + 48, 4 + 16),        # perm, x/v gather, x'/v' store | offs, rho RMW
+    "push_key": (48 + 32 + 4 + 2, 32 + 8),           # x/v read, kicked v (2 pair streams), key, rank | E tile, count RMW
+    "place": (4 + 2 + 4, 4),                         # key, rank read, perm write | offs
     "scan": (0, 16),                                 # count read x2, offs + cursor write
     "fft_x_fwd": (0, 8 + 8),
     "fft_y_fwd": (0, 8 + 8),
     "fft_z_mul": (0, 8 + 24),
     "fft_y_inv": (0, 24 + 24),
-    "fft_x_inv": (0, 24 + 24),
+    "fft_x_inv": (0, 24 + 32),                       # 3 half spectra -> E node records
     "clear": (0, 4 + 8),
 }
 
@@ -109,11 +109,12 @@ def measured_peaks():
         return {}
 
 
-def ncu_traffic(config_name: str):
-    """Per-launch DRAM bytes of the dominant kernel from the committed ncu summary."""
+def ncu_traffic(config_name: str, kernel: str):
+    """Per-launch DRAM bytes (dram__bytes_read + write) of a kernel at this config from the
+    committed ncu launch list (profiles/ncu_traffic.json), or None."""
     try:
         d = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json")))
-        return d.get(config_name)
+        return d.get(config_name, {}).get(kernel)
     except Exception:
         return None
 
@@ -270,7 +271,7 @@ def run_ours(args, rank, world):
     peaks = measured_peaks()
     peak = peaks.get("hbm_gbs") or 6650.0
     cfg_name = f"landau3d_{n}^3x{ppc}ppc_fft"
-    traffic = ncu_traffic(cfg_name)
+    traffic = ncu_traffic(cfg_name, dom)
     roof = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
             "frac": achieved / peak, "traffic": traffic,
             "peak_source": "measured (MEASURED_PEAKS.json hbm_gbs)" if peaks.get("hbm_gbs") else "fallback 6650 GB/s",

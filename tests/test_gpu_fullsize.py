@@ -79,19 +79,20 @@ def test_fullsize_512_sampled_parity():
 
 
 @pytest.mark.slow
-def test_landau_damping_rate_gpu_128():
-    """P:231-232, BJ: 128^3 x 8 ppc, alpha = 0.05, 400 steps: slope 2 gamma
-    within 10%, peak spacing pi/omega_r within 5% (D#20, D#21)."""
+def test_landau_damping_rate_gpu_256():
+    """P:231-232, BJ: 256^3 x 8 ppc (134M particles), alpha = 0.05, 260 steps:
+    slope of the W_x peaks for t <= 12 within 10% of 2 gamma, peak spacing pi/omega_r
+    within 5% (D#20, D#21: at 128^3 x 8 the shot-noise floor bends the fit past t ~ 10)."""
     import torch
     from paper_2605_05469_b200 import Simulation
 
     torch.cuda.set_device(0)
     w = dispersion_root(0.5)
-    sim = Simulation(n=128, ppc=8, seed=1)
-    ex = sim.step(400)
-    t = np.arange(400) * DT
-    slope, npk, tp = fit_damping_rate(t, ex, t_max=14.0)
-    assert npk >= 4
+    sim = Simulation(n=256, ppc=8, seed=1)
+    ex = sim.step(260)
+    t = np.arange(260) * DT
+    slope, npk, tp = fit_damping_rate(t, ex, t_max=12.0)
+    assert npk >= 5
     assert abs(slope - 2 * w.imag) < 0.10 * abs(2 * w.imag), slope
     assert abs(np.mean(np.diff(tp)) - np.pi / w.real) < 0.05 * np.pi / w.real
     sim.close()
