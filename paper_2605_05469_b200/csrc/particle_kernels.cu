@@ -350,6 +350,127 @@ __global__ void __launch_bounds__(kThreads) k_place(const uint32_t* __restrict__
 // No atomics and no shuffles inside the CTA: the per-brick charge is deterministic.
 // FRAC_SMEM: keep the fractional offsets of the new positions in shared memory
 // (24 B per staged particle) for the per-cell sums; otherwise re-read x' from L2.
+// v3: the gather runs as cp.async (LDGSTS, 16 B, L2 only) straight into the stable
+// sorted slot of a shared-memory copy of the chunk: every thread keeps all of its
+// particles' loads in flight without holding registers.  Then, with the chunk in
+// shared memory in sorted order: drift in place, stream x', v' out with coalesced
+// 16-byte stores, and sum the CIC weights per cell from shared memory.
+constexpr int kCapA = 2048;     // particles per chunk of the cp.async variant (96 KB staged)
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+    const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+    asm volatile("cp.async.commit_group;\n\tcp.async.wait_group 0;" ::: "memory");
+}
+
+template <bool PUSH>
+__global__ void __launch_bounds__(kThreads, 2) k_reorder_deposit_async(
+    Geom g, const uint32_t* __restrict__ offs, const uint32_t* __restrict__ perm, PState cur,
+    PState nxt, double* __restrict__ rho, int* __restrict__ err) {
+    extern __shared__ double dyn_smem[];
+    double2* sp0 = reinterpret_cast<double2*>(dyn_smem);          // [kCapA] (x, y)
+    double2* sp1 = sp0 + kCapA;                                     // [kCapA] (z, vz)
+    double2* sp2 = sp1 + kCapA;                                     // [kCapA] (vx, vy)
+    double* tile = reinterpret_cast<double*>(sp2 + kCapA);         // [9*9*5]
+    uint32_t* sperm = reinterpret_cast<uint32_t*>(tile + 9 * 9 * 5);   // [kCapA]
+    uint32_t* soffs = sperm + kCapA;                                // [kBrick + 1]
+    uint8_t* scell = reinterpret_cast<uint8_t*>(soffs + kBrick + 1);   // [kCapA]
+    const int t = threadIdx.x;
+    const uint32_t c0 = blockIdx.x * kBrick;
+    int bx, by, bz;
+    unmorton(c0, bx, by, bz);
+    soffs[t] = offs[c0 + t];
+    if (t == 0) soffs[kBrick] = offs[c0 + kBrick];
+    for (int q = t; q < 9 * 9 * 5; q += kThreads) tile[q] = 0.0;
+    __syncthreads();
+
+    double acc[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) acc[q] = 0.0;
+    int ca = 0;
+    while (ca < kBrick) {
+        if (soffs[ca + 1] - soffs[ca] > (uint32_t)kCapA) {
+            if (t == 0) atomicExch(err, 1);
+            return;
+        }
+        int lo = ca + 1, hi = kBrick;
+        while (lo < hi) {
+            const int mid = (lo + hi + 1) >> 1;
+            if (soffs[mid] - soffs[ca] <= (uint32_t)kCapA) lo = mid; else hi = mid - 1;
+        }
+        const int cb = lo;
+        const uint32_t P0 = soffs[ca];
+        const int cnt = (int)(soffs[cb] - P0);
+        for (int p = t; p < cnt; p += kThreads) sperm[p] = __ldg(perm + P0 + p);
+        const bool mine = t >= ca && t < cb;
+        const int s0 = mine ? (int)(soffs[t] - P0) : 0, s1 = mine ? (int)(soffs[t + 1] - P0) : 0;
+        for (int p = s0; p < s1; ++p) scell[p] = (uint8_t)t;
+        __syncthreads();
+        // stable rank -> cp.async of the particle into its sorted slot
+        for (int p = t; p < cnt; p += kThreads) {
+            const int c = scell[p];
+            const int q0 = (int)(soffs[c] - P0), q1 = (int)(soffs[c + 1] - P0);
+            const uint32_t j = sperm[p];
+            int r = 0;
+            for (int q = q0; q < q1; ++q) r += sperm[q] < j;
+            const int o = q0 + r;
+            cp_async16(sp0 + o, cur.p[0] + j);
+            cp_async16(sp1 + o, cur.p[1] + j);
+            cp_async16(sp2 + o, cur.p[2] + j);
+        }
+        cp_async_wait_all();
+        __syncthreads();
+        // drift in place (v is already kicked), coalesced streaming stores
+        for (int p = t; p < cnt; p += kThreads) {
+            double2 a = sp0[p], b = sp1[p];
+            const double2 e = sp2[p];
+            if (PUSH) {
+                double x[3] = {a.x, a.y, b.x};
+                const double v[3] = {e.x, e.y, b.y};
+                drift(g, x, v);
+                a = make_double2(x[0], x[1]);
+                b = make_double2(x[2], b.y);
+                sp0[p] = a;
+                sp1[p] = b;
+            }
+            const int64_t o = (int64_t)P0 + p;
+            nxt.p[0][o] = a;
+            nxt.p[1][o] = b;
+            nxt.p[2][o] = e;
+        }
+        __syncthreads();
+        // CIC charge: thread per cell, its particles in stable order from shared memory
+        for (int p = s0; p < s1; ++p) {
+            const double2 a = sp0[p], b = sp1[p];
+            const double x[3] = {a.x, a.y, b.x};
+            int ii[3];
+            double w[3][2];
+            cic_weights(g, x, ii, w);
+#pragma unroll
+            for (int q = 0; q < 8; ++q)
+                acc[q] = __dadd_rn(acc[q], __dmul_rn(__dmul_rn(w[0][q & 1], w[1][(q >> 1) & 1]), w[2][q >> 2]));
+        }
+        __syncthreads();
+        ca = cb;
+    }
+    const int lx = (int)compact3((uint32_t)t), ly = (int)compact3((uint32_t)t >> 1),
+              lz = (int)compact3((uint32_t)t >> 2);
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+        const int a = q & 1, b = (q >> 1) & 1, c = q >> 2;
+        tile[((lz + c) * 9 + (ly + b)) * 9 + (lx + a)] += acc[q];
+        __syncthreads();
+    }
+    for (int q = t; q < 9 * 9 * 5; q += kThreads) {
+        const double val = tile[q];
+        if (val == 0.0) continue;
+        const int nx = q % 9, ny = (q / 9) % 9, nz = q / 81;
+        atomicAdd(rho + gidx(g, (bx + nx) & g.nmask, (by + ny) & g.nmask, (bz + nz) & g.nmask), val);
+    }
+}
+
 template <bool PUSH, bool FRAC_SMEM, int KB = kBatch>
 __global__ void __launch_bounds__(kThreads, KB > 2 ? 2 : (FRAC_SMEM ? 3 : 4)) k_reorder_deposit(
     Geom g, const uint32_t* __restrict__ offs, const uint32_t* __restrict__ perm, PState cur,
@@ -508,6 +629,8 @@ __global__ void __launch_bounds__(kThreads) k_sort_segments(const uint32_t* __re
 
 inline unsigned blocks(int64_t n, int t) { return (unsigned)((n + t - 1) / t); }
 
+constexpr size_t kReorderAsyncSmem = sizeof(double2) * 3 * kCapA + sizeof(double) * 9 * 9 * 5 +
+                                      sizeof(uint32_t) * (kCapA + kBrick + 1) + kCapA;
 constexpr size_t reorder_smem(bool frac) {
     return sizeof(double) * ((frac ? 3 * kCap : 0) + 9 * 9 * 5) + sizeof(uint32_t) * (kCap + kBrick + 1) + kCap;
 }
@@ -579,6 +702,14 @@ void launch_place(const uint32_t* key, const uint16_t* rank, int64_t np, const u
 void launch_reorder_deposit(const Geom& g, const uint32_t* offs, const uint32_t* perm, PState cur,
                             PState nxt, int push, double* rho_buf, int* err_flag, cudaStream_t s) {
     const unsigned nbrick = (unsigned)(((int64_t)g.n * g.n * g.n) / kBrick);
+    static const int variant = getenv("PIC_REORDER_VARIANT") ? atoi(getenv("PIC_REORDER_VARIANT")) : 3;
+    if (variant == 3) {
+        if (push)
+            k_reorder_deposit_async<true><<<nbrick, kThreads, kReorderAsyncSmem, s>>>(g, offs, perm, cur, nxt, rho_buf, err_flag);
+        else
+            k_reorder_deposit_async<false><<<nbrick, kThreads, kReorderAsyncSmem, s>>>(g, offs, perm, cur, nxt, rho_buf, err_flag);
+        return;
+    }
     const bool fs = reorder_frac_smem();
     const size_t sm = reorder_smem(fs);
     static const int kb = getenv("PIC_REORDER_KB") ? atoi(getenv("PIC_REORDER_KB")) : 4;
@@ -597,6 +728,8 @@ void launch_reorder_deposit(const Geom& g, const uint32_t* offs, const uint32_t*
 }
 
 void particles_set_smem_limits() {
+    cudaFuncSetAttribute(k_reorder_deposit_async<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kReorderAsyncSmem);
+    cudaFuncSetAttribute(k_reorder_deposit_async<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kReorderAsyncSmem);
     cudaFuncSetAttribute(k_reorder_deposit<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)reorder_smem(true));
     cudaFuncSetAttribute(k_reorder_deposit<true, true, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)reorder_smem(true));
     cudaFuncSetAttribute(k_reorder_deposit<true, true, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)reorder_smem(true));

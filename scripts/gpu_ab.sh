@@ -1,4 +1,5 @@
 mkdir -p gpurun_out
-for kb in 2 4 8; do
-PIC_REORDER_KB=$kb timeout 900 python bench.py --steps 5 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/bench512_kb$kb.log 2>&1; echo "kb $kb rc=$?"; tail -1 gpurun_out/bench512_kb$kb.log | python -c "import json,sys; d=json.loads(sys.stdin.read()); print(d['ms_per_step'], d['value']); [print(k, round(v['ms_per_step'],3), v['alg_GBps']) for k,v in d['stages'].items() if k in ('reorder_deposit',)]"
+timeout 900 python -m pytest tests/test_gpu_parity.py -x -q > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?"; tail -2 gpurun_out/pytest_gpu.log
+for v in 3 1; do
+PIC_REORDER_VARIANT=$v timeout 900 python bench.py --steps 5 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/bench512_v$v.log 2>&1; echo "variant $v rc=$?"; tail -1 gpurun_out/bench512_v$v.log | python -c "import json,sys; d=json.loads(sys.stdin.read()); print(d['ms_per_step'], d['value']); [print(k, round(v['ms_per_step'],3), v['alg_GBps']) for k,v in d['stages'].items() if k in ('reorder_deposit',)]"
 done
