@@ -59,12 +59,22 @@ typedef struct {
     double   dt;        /* time step > 0; default 0.05 (D#9)                   */
     uint64_t seed;      /* Philox4x32-10 key of the initial sampler (D#10)            */
     int32_t  half_kick; /* 1: v stored at half steps, backward half kick at init */
-    int32_t  pgrid[2];  /* {Py, Pz} rank grid; must be {1, 1} in this build           */
+    int32_t  pgrid[2];  /* {Py, Pz} rank grid: {1, nranks} (z-slabs; pencils not built) */
 } pic_params;
 
 /* Fill *p with the Landau-damping defaults of P:146 (N=16, ppc=8, k=0.5, alpha=0.05,
  * dt=0.05, L=2 pi/k, seed=1, half_kick=1, pgrid={1,1}). */
 pic_status pic_params_default(pic_params *p);
+
+/* Multi-GPU (one process per GPU, nranks in {1, 2, 4, 8}): rank r owns the z-slab of
+ * cell/node planes [r N/P, (r+1) N/P) and the particles whose cell lies in it
+ * (SURVEY §8(e)).  Rank 0 creates the NCCL id (128 bytes), the caller broadcasts it
+ * (torch.distributed) and every rank passes it to pic_init. */
+pic_status pic_nccl_unique_id(uint8_t id[128]);
+
+/* The slab of a rank: first plane z0, planes nz, particle capacity of the rank. */
+pic_status pic_slab(const pic_params *p, int32_t rank, int32_t nranks, int32_t *z0, int32_t *nz,
+                    int64_t *capacity);
 
 /* Bytes of device workspace pic_init needs for these parameters (rank/nranks as in
  * pic_init).  PIC_EINVAL on invalid parameters. */
@@ -74,11 +84,14 @@ pic_status pic_workspace_bytes(const pic_params *p, int32_t rank, int32_t nranks
  * CDF (Newton) of (1 + alpha cos k x)/L per dimension, velocities N(0,1)^3 by
  * Box-Muller, Philox counter = particle index; particles sorted by cell key and
  * the charge deposited; optional backward half kick v <- v - (q/m) E dt/2.
- *   nccl_id   : NULL when nranks == 1 (only nranks == 1 in this build).
+ *   nccl_id   : NULL when nranks == 1; else the id from pic_nccl_unique_id on rank 0.
+ *               Every rank calls every function of a context collectively (same order).
  *   workspace : device pointer, >= pic_workspace_bytes(), caller-owned.
  *   cuda_stream: cudaStream_t (void*); NULL = legacy default stream.
  * PIC_EINVAL: alpha not in [0,1), ppc <= 0, N not a power of two in [16,1024],
- *   k <= 0, dt <= 0, k L / 2 pi not a positive integer, N_p >= 2^32, bad pgrid/rank.
+ *   k <= 0, dt <= 0, k L / 2 pi not a positive integer, N_p per rank >= 2^32 / 1.3,
+ *   nranks not in {1,2,4,8}, N/nranks < 4, pgrid != {1, nranks}.
+ * PIC_EUNSUPPORTED: a pencil grid (pgrid = {Py > 1, Pz}); PIC_ENCCL: NCCL init failed.
  * PIC_ENOMEM: workspace_bytes too small.  PIC_ECUDA: a kernel failed. */
 pic_status pic_init(const pic_params *p, int32_t rank, int32_t nranks, const uint8_t *nccl_id,
                     void *workspace, size_t workspace_bytes, void *cuda_stream, pic_ctx **out);
@@ -102,28 +115,35 @@ const char *pic_last_error(const pic_ctx *ctx);
 /* Number of particles held by this context. */
 pic_status pic_num_particles(pic_ctx *ctx, int64_t *np);
 
+/* Particles this rank has sent to other ranks since pic_init (migration, P > 1). */
+pic_status pic_migrated(pic_ctx *ctx, int64_t *migrated);
+
 /* Copy the particle state to host xyzuvw[6][np] in canonical order (sorted by
  * cell key, ties by the current order).  Synchronous. */
 pic_status pic_get_particles(pic_ctx *ctx, double *xyzuvw, int64_t np);
 
-/* Replace the particle state from host xyzuvw[6][np] (np must equal the context's
- * N_p; every coordinate in [0, L)).  The state is interpreted as (x_n, v_{n-1/2})
+/* Replace the particle state from host xyzuvw[6][np] (P = 1: np = N_p; P > 1: this
+ * rank's particles, every one inside its slab, np <= its capacity; every coordinate
+ * in [0, L), else PIC_EINVAL).  Collective at P > 1.  The state is interpreted as (x_n, v_{n-1/2})
  * (no half kick); it is sorted by cell key (stable: ties keep the given order) and
  * deposited.  With stream-ordered host copies; synchronous. */
 pic_status pic_set_particles(pic_ctx *ctx, const double *xyzuvw, int64_t np);
 
-/* Copy a grid to host [N][N][N]: which = 0 -> rho (charge density of the current
- * positions, q/h^3 scaled); 1, 2, 3 -> E_x, E_y, E_z of the latest solve. */
+/* Copy this rank's slab of a grid to host [nz][N][N] (P = 1: [N][N][N]): which = 0
+ * -> rho (charge density of the current positions, q/h^3 scaled); 1, 2, 3 -> E_x,
+ * E_y, E_z of the latest solve. */
 pic_status pic_get_grid(pic_ctx *ctx, int32_t which, double *host);
 
-/* Solve for an injected charge density rho_host[N^3] (true density, not
- * scaled) and return E_host[3][N^3] and the energies.  Does not touch the
+/* Solve for an injected charge density rho_host[nz][N][N] (this rank's slab; true
+ * density, not scaled) and return E_host[3][nz][N][N] and the energies (of the
+ * whole box).  Collective at P > 1.  Does not touch the
  * particles, but overwrites the context's field and charge buffers. */
 pic_status pic_solve_injected(pic_ctx *ctx, const double *rho_host, double *E_host,
                               double *ex_energy, double *total_energy);
 
-/* One gather+push+sort+deposit with an injected field E_host[3][N^3] instead of
- * the solved one (the solve is skipped).  For bit-exact push parity tests. */
+/* One gather+push+sort+deposit with an injected field E_host[3][nz][N][N] (this
+ * rank's slab) instead of the solved one (the solve is skipped).  For bit-exact
+ * push parity tests.  Collective at P > 1. */
 pic_status pic_push_injected(pic_ctx *ctx, const double *E_host);
 
 /* Cell keys (uint32, of the current positions in canonical order) and the
@@ -137,7 +157,9 @@ pic_status pic_get_keys_perm(pic_ctx *ctx, uint32_t *keys, uint32_t *perm);
 enum {
     PIC_STAGE_FFT_X_FWD = 0, PIC_STAGE_FFT_Y_FWD, PIC_STAGE_FFT_Z_MUL, PIC_STAGE_FFT_Y_INV,
     PIC_STAGE_FFT_X_INV, PIC_STAGE_ENERGY, PIC_STAGE_CLEAR, PIC_STAGE_PUSH_KEY,
-    PIC_STAGE_SCAN, PIC_STAGE_PLACE, PIC_STAGE_REORDER_DEPOSIT, PIC_NSTAGES
+    PIC_STAGE_SCAN, PIC_STAGE_PLACE, PIC_STAGE_REORDER_DEPOSIT,
+    PIC_STAGE_EXCHANGE,   /* NCCL: transposes, halo/ghost planes, migration, energy */
+    PIC_NSTAGES
 };
 pic_status pic_set_timing(pic_ctx *ctx, int32_t enable);
 pic_status pic_get_timings(pic_ctx *ctx, double *ms, int64_t *launches);

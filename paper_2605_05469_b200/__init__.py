@@ -9,6 +9,8 @@ from ._binding import (  # noqa: F401
     STAGES,
     default_params,
     lib,
+    nccl_unique_id,
+    slab,
     workspace_bytes,
 )
 from ._build import build_lib  # noqa: F401

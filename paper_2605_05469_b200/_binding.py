@@ -23,7 +23,7 @@ STATUS_NAMES = {0: "PIC_OK", -1: "PIC_EINVAL", -2: "PIC_ENOMEM", -3: "PIC_ECUDA"
                 -8: "PIC_EUNSUPPORTED"}
 
 STAGES = ["fft_x_fwd", "fft_y_fwd", "fft_z_mul", "fft_y_inv", "fft_x_inv", "energy", "clear",
-          "push_key", "scan", "place", "reorder_deposit"]
+          "push_key", "scan", "place", "reorder_deposit", "exchange"]
 PIC_NSTAGES = len(STAGES)
 
 
@@ -54,6 +54,10 @@ _u32p = C.POINTER(C.c_uint32)
 _i64p = C.POINTER(C.c_int64)
 SYMBOLS = {
     "pic_params_default": (C.c_int, [C.POINTER(pic_params)]),
+    "pic_nccl_unique_id": (C.c_int, [C.c_void_p]),
+    "pic_slab": (C.c_int, [C.POINTER(pic_params), C.c_int32, C.c_int32, C.POINTER(C.c_int32),
+                           C.POINTER(C.c_int32), _i64p]),
+    "pic_migrated": (C.c_int, [_vp, _i64p]),
     "pic_workspace_bytes": (C.c_int, [C.POINTER(pic_params), C.c_int32, C.c_int32, C.POINTER(C.c_size_t)]),
     "pic_init": (C.c_int, [C.POINTER(pic_params), C.c_int32, C.c_int32, _vp, _vp, C.c_size_t, _vp,
                            C.POINTER(_vp)]),
@@ -121,6 +125,20 @@ def workspace_bytes(p: pic_params, rank: int = 0, nranks: int = 1) -> int:
     return b.value
 
 
+def nccl_unique_id() -> bytes:
+    """128-byte NCCL id (rank 0 creates it, the caller broadcasts it)."""
+    buf = (C.c_uint8 * 128)()
+    _check(lib().pic_nccl_unique_id(buf))
+    return bytes(buf)
+
+
+def slab(p: pic_params, rank: int, nranks: int):
+    """(z0, nz, capacity) of a rank's z-slab."""
+    z0, nz, cap = C.c_int32(), C.c_int32(), C.c_int64()
+    _check(lib().pic_slab(C.byref(p), rank, nranks, C.byref(z0), C.byref(nz), C.byref(cap)))
+    return z0.value, nz.value, cap.value
+
+
 class Simulation:
     """One rank of the PIC simulation on the current CUDA device.
 
@@ -129,25 +147,38 @@ class Simulation:
     """
 
     def __init__(self, n=16, ppc=8, k=0.5, alpha=0.05, dt=0.05, seed=1, half_kick=True,
-                 length=0.0, device=None):
+                 length=0.0, device=None, rank=0, nranks=1, nccl_id: bytes | None = None):
         import torch
 
         self.params = default_params(n=n, ppc=ppc, k=k, alpha=alpha, dt=dt, seed=seed,
-                                     half_kick=int(bool(half_kick)), length=length)
+                                     half_kick=int(bool(half_kick)), length=length,
+                                     pgrid=(1, nranks))
+        self.rank, self.nranks = rank, nranks
+        self.z0, self.nz, self.capacity = slab(self.params, rank, nranks)
         self.device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
-        nbytes = workspace_bytes(self.params)
+        nbytes = workspace_bytes(self.params, rank, nranks)
         with torch.cuda.device(self.device):
             self.workspace = torch.empty(nbytes, dtype=torch.uint8, device=self.device)
             self.stream = torch.cuda.current_stream(self.device)
         ctx = C.c_void_p()
-        _check(lib().pic_init(C.byref(self.params), 0, 1, None, C.c_void_p(self.workspace.data_ptr()),
+        idbuf = (C.c_uint8 * 128).from_buffer_copy(nccl_id) if nccl_id is not None else None
+        _check(lib().pic_init(C.byref(self.params), rank, nranks, idbuf, C.c_void_p(self.workspace.data_ptr()),
                               nbytes, C.c_void_p(self.stream.cuda_stream), C.byref(ctx)))
         self.ctx = ctx
-        n64 = C.c_int64()
-        _check(lib().pic_num_particles(self.ctx, C.byref(n64)), self.ctx)
-        self.np = n64.value
         self.n = n
         self.L = length if length else 2 * np.pi / k
+
+    @property
+    def np(self) -> int:
+        """Particles held by this rank now (changes with migration at nranks > 1)."""
+        n64 = C.c_int64()
+        _check(lib().pic_num_particles(self.ctx, C.byref(n64)), self.ctx)
+        return n64.value
+
+    def migrated(self) -> int:
+        v = C.c_int64()
+        _check(lib().pic_migrated(self.ctx, C.byref(v)), self.ctx)
+        return v.value
 
     # -- core --------------------------------------------------------------
     def step(self, nsteps: int = 1) -> np.ndarray:
@@ -162,25 +193,26 @@ class Simulation:
 
     # -- host buffers ------------------------------------------------------
     def get_particles(self, out: np.ndarray | None = None) -> np.ndarray:
+        npl = self.np
         if out is None:
-            out = np.zeros((6, self.np))
-        assert out.shape == (6, self.np)
-        _check(lib().pic_get_particles(self.ctx, _d(out), self.np), self.ctx)
+            out = np.zeros((6, npl))
+        assert out.shape == (6, npl)
+        _check(lib().pic_get_particles(self.ctx, _d(out), npl), self.ctx)
         return out
 
     def set_particles(self, xv: np.ndarray):
         xv = np.ascontiguousarray(xv, dtype=np.float64)
-        assert xv.shape == (6, self.np)
-        _check(lib().pic_set_particles(self.ctx, _d(xv), self.np), self.ctx)
+        assert xv.ndim == 2 and xv.shape[0] == 6
+        _check(lib().pic_set_particles(self.ctx, _d(xv), xv.shape[1]), self.ctx)
 
     def get_grid(self, which: int) -> np.ndarray:
-        out = np.zeros((self.n, self.n, self.n))
+        out = np.zeros((self.nz, self.n, self.n))
         _check(lib().pic_get_grid(self.ctx, which, _d(out)), self.ctx)
         return out
 
     def solve_injected(self, rho: np.ndarray):
         rho = np.ascontiguousarray(rho, dtype=np.float64)
-        E = np.zeros((3, self.n, self.n, self.n))
+        E = np.zeros((3, self.nz, self.n, self.n))
         a, b = C.c_double(), C.c_double()
         _check(lib().pic_solve_injected(self.ctx, _d(rho), _d(E), C.byref(a), C.byref(b)), self.ctx)
         return E, a.value, b.value
@@ -190,8 +222,12 @@ class Simulation:
         _check(lib().pic_push_injected(self.ctx, _d(E)), self.ctx)
 
     def keys_perm(self):
-        k = np.zeros(self.np, dtype=np.uint32)
-        p = np.zeros(self.np, dtype=np.uint32)
+        """Global Morton cell keys of the current state, and the permutation of the
+        latest sort (perm[i] = pre-sort index; P > 1: extended index of residents and
+        arrivals)."""
+        npl = self.np
+        k = np.zeros(npl, dtype=np.uint32)
+        p = np.zeros(npl, dtype=np.uint32)
         _check(lib().pic_get_keys_perm(self.ctx, k.ctypes.data_as(_u32p), p.ctypes.data_as(_u32p)), self.ctx)
         return k, p
 

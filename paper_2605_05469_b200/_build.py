@@ -18,6 +18,14 @@ NVCC_FLAGS = [
 ]
 
 
+def nccl_dirs():
+    """NCCL 2.28 headers and library bundled with torch (nvidia-nccl-cu12 wheel)."""
+    import nvidia.nccl as m
+
+    root = os.path.dirname(m.__file__) if getattr(m, "__file__", None) else list(m.__path__)[0]
+    return os.path.join(root, "include"), os.path.join(root, "lib")
+
+
 def sources():
     return sorted(glob.glob(os.path.join(CSRC, "*.cu")))
 
@@ -33,7 +41,9 @@ def build_lib(force: bool = False, verbose: bool = False) -> str:
         newest = max(os.path.getmtime(p) for p in srcs + headers())
         if os.path.getmtime(LIB) >= newest:
             return LIB
-    cmd = [NVCC, *NVCC_FLAGS, "-o", LIB, *srcs]
+    inc, libdir = nccl_dirs()
+    cmd = [NVCC, *NVCC_FLAGS, "-I" + inc, "-o", LIB, *srcs, "-L" + libdir, "-l:libnccl.so.2",
+           "-Xlinker", "-rpath," + libdir]
     if verbose:
         print(" ".join(cmd))
     subprocess.check_call(cmd)

@@ -195,15 +195,15 @@ __host__ __device__ inline int y_tw(int n) { int t = 2048 / n; return t > 8 ? 8 
 __host__ __device__ inline int z_tw(int n) { int t = 2048 / n; return t > 8 ? 8 : (t < 1 ? 1 : t); }
 
 // ------------------------------------------------------------ x R2C -------
-// Row r of S0: n reals -> n/2 + 1 complex, in place (the CTA owns its rows).
+// Row r of S0 (nzl * n rows): n reals -> n/2 + 1 complex, in place (the CTA owns its rows).
 // z[m] = x[2m] + i x[2m+1] -> Z = FFT_{n/2}(z) -> X[k] = Ze[k] + W_n^k Zo[k],
 // Ze = (Z[k] + conj Z[n/2-k])/2, Zo = (Z[k] - conj Z[n/2-k])(-i/2).
 __global__ void __launch_bounds__(kThreads, 4) k_fft_x_fwd(Geom g, double* buf,
-                                                        const double2* __restrict__ tw) {
+                                                           const double2* __restrict__ tw) {
     extern __shared__ double2 sm[];
     const int len = g.n >> 1, logn = ilog2(len), R = x_rows(g.n), ls = line_stride(len);
     const int64_t row0 = (int64_t)blockIdx.x * R;
-    const int rows = (int)min((int64_t)R, (int64_t)g.n * g.n - row0);
+    const int rows = (int)min((int64_t)R, (int64_t)g.nzl * g.n - row0);
     auto src = [&](int l, int e) {
         return reinterpret_cast<const double2*>(buf + (row0 + l) * g.rp)[e];
     };
@@ -223,45 +223,54 @@ __global__ void __launch_bounds__(kThreads, 4) k_fft_x_fwd(Geom g, double* buf,
     }
 }
 
+// Element (component d, slab plane zl, row y) of a spectral layout: row index * px.
+__device__ __forceinline__ int64_t spec_row(const Geom& g, const SpecLayout& L, int d, int zl, int y) {
+    if (!L.packed) return (((int64_t)d * g.nzl + zl) * g.n + y) * g.px;
+    const int q = y >> g.mz, yl = y & (g.nzl - 1);   // nyl = n / P = nzl
+    return ((((int64_t)q * L.ncomp + d) * g.nzl + zl) * g.nzl + yl) * g.px;
+}
+
 // ------------------------------------------------------------- y pass ------
-// blockIdx.x = z * ntiles + tile, blockIdx.y = component.  Lines along y of TW
-// consecutive kx columns (valid columns kx <= n/2), in place: the first stage
-// reads the whole tile before the last stage writes it.
+// blockIdx.x = zl * ntiles + tile, blockIdx.y = component.  Lines along y of TW
+// consecutive kx columns (valid columns kx <= n/2); the first stage reads the whole
+// tile before the last stage writes it, so src and dst may alias.
 template <int SIGN>
-__global__ void __launch_bounds__(kThreads, 3) k_fft_y(Geom g, double* b0, double* b1, double* b2,
-                                                    const double2* __restrict__ tw) {
+__global__ void __launch_bounds__(kThreads, 2) k_fft_y(Geom g, SpecLayout sl, SpecLayout dl,
+                                                       const double2* __restrict__ tw) {
     extern __shared__ double2 sm[];
-    double2* buf = reinterpret_cast<double2*>(blockIdx.y == 0 ? b0 : (blockIdx.y == 1 ? b1 : b2));
     const int n = g.n, logn = ilog2(n), TW = y_tw(n), ls = line_stride(n);
     const int ntiles = (n / 2 + 1 + TW - 1) / TW;
-    const int z = blockIdx.x / ntiles, kx0 = (blockIdx.x - z * ntiles) * TW;
+    const int zl = blockIdx.x / ntiles, kx0 = (blockIdx.x - zl * ntiles) * TW, d = blockIdx.y;
     const int ncol = min(TW, n / 2 + 1 - kx0);
-    double2* base = buf + (int64_t)z * n * g.px + kx0;
-    auto src = [&](int l, int e) { return l < ncol ? base[(int64_t)e * g.px + l] : make_double2(0.0, 0.0); };
-    auto dst = [&](int l, int e, double2 v) { if (l < ncol) base[(int64_t)e * g.px + l] = v; };
+    auto src = [&](int l, int y) {
+        return l < ncol ? sl.base[spec_row(g, sl, d, zl, y) + kx0 + l] : make_double2(0.0, 0.0);
+    };
+    auto dst = [&](int l, int y, double2 v) { if (l < ncol) dl.base[spec_row(g, dl, d, zl, y) + kx0 + l] = v; };
     fft_lines<SIGN, false>(sm, TW, logn, ls, tw, 0, src, dst);
 }
 
 // --------------------------------------------------- z pass + multiply -----
-// blockIdx.x = ky * ntiles + tile.  Forward z FFT of rho^ into shared memory,
-// then for d = x, y, z an inverse z FFT whose first stage reads
+// blockIdx.x = yl * ntiles + tile over the ky-pencil [z][yl][px] (all n planes,
+// nyl = n / P rows of ky, ky = rank nyl + yl).  Forward z FFT of rho^ into shared
+// memory, then for d = x, y, z an inverse z FFT whose first stage reads
 // E^_d = -i k_d rho^ / |k|^2 * scale (zero at n = 0 and where n_d = -N/2, D#6)
-// straight from it; stores E^_x -> S1, E^_y -> S2, E^_z -> S0 (the CTA's own,
-// already consumed, input tile).
-__global__ void __launch_bounds__(kThreads, 2) k_fft_z_mul(Geom g, double2* rho, double2* e1,
-                                                        double2* e2, double scale,
-                                                        const double2* __restrict__ tw) {
+// straight from it; stores PACKED [q][d][zl][yl][px] (q = z / nzl) for the return
+// transpose.
+__global__ void __launch_bounds__(kThreads, 2) k_fft_z_mul(Geom g, const double2* __restrict__ pencil,
+                                                           double2* __restrict__ out, double scale,
+                                                           const double2* __restrict__ tw) {
     extern __shared__ double2 sm[];
-    const int n = g.n, logn = ilog2(n), TW = z_tw(n), ls = line_stride(n);
+    const int n = g.n, logn = ilog2(n), TW = z_tw(n), ls = line_stride(n), nyl = n / g.P;
     double2* s1 = sm;
     double2* s2 = sm + TW * ls;
     const int ntiles = (n / 2 + 1 + TW - 1) / TW;
-    const int ky = blockIdx.x / ntiles, kx0 = (blockIdx.x - ky * ntiles) * TW;
+    const int yl = blockIdx.x / ntiles, kx0 = (blockIdx.x - yl * ntiles) * TW;
+    const int ky = g.rank * nyl + yl;
     const int ncol = min(TW, n / 2 + 1 - kx0);
-    const int64_t zstride = (int64_t)n * g.px;
-    const int64_t off = (int64_t)ky * g.px + kx0;
+    const int64_t zstride = (int64_t)nyl * g.px;
+    const int64_t off = (int64_t)yl * g.px + kx0;
     {
-        auto src = [&](int l, int e) { return l < ncol ? rho[off + e * zstride + l] : make_double2(0.0, 0.0); };
+        auto src = [&](int l, int e) { return l < ncol ? pencil[off + e * zstride + l] : make_double2(0.0, 0.0); };
         auto dst = [&](int, int, double2) {};
         fft_lines<-1, true>(s1, TW, logn, ls, tw, 0, src, dst);
     }
@@ -269,7 +278,6 @@ __global__ void __launch_bounds__(kThreads, 2) k_fft_z_mul(Geom g, double2* rho,
     const int half = n / 2;
     const double kyv = kf * (double)(ky < half ? ky : ky - n);
     for (int d = 0; d < 3; ++d) {
-        double2* out = d == 0 ? e1 : (d == 1 ? e2 : rho);
         auto src = [&](int l, int kz) {
             const int kx = kx0 + l;
             const double kxv = kf * (double)(kx < half ? kx : kx - n);
@@ -285,14 +293,19 @@ __global__ void __launch_bounds__(kThreads, 2) k_fft_z_mul(Geom g, double2* rho,
             }
             return e;
         };
-        auto dst = [&](int l, int z, double2 v) { if (l < ncol) out[off + z * zstride + l] = v; };
+        auto dst = [&](int l, int z, double2 v) {
+            if (l < ncol) {
+                const int q = z >> g.mz, zl = z - (q << g.mz);
+                out[((((int64_t)q * 3 + d) * g.nzl + zl) * nyl + yl) * g.px + kx0 + l] = v;
+            }
+        };
         fft_lines<+1, false>(s2, TW, logn, ls, tw, 0, src, dst);
     }
 }
 
 // ------------------------------------------------------------ x C2R -------
 // R rows of all three components per CTA: n/2 + 1 complex -> n reals each,
-// written as node records E4[row][x] = (E_x, E_y, E_z, 0) with 256-bit stores;
+// written as node records E4[zl][y][x] = (E_x, E_y, E_z, 0) with 256-bit stores;
 // per-CTA partial sums of E_d^2 -> partials[d * gridDim.x + blockIdx.x].
 // Z[k] = (X[k] + conj X[n/2-k]) + i (X[k] - conj X[n/2-k]) W_n^{-k} (unnormalised).
 __device__ __forceinline__ void st_node(double* p, double a, double b, double c) {
@@ -300,19 +313,19 @@ __device__ __forceinline__ void st_node(double* p, double a, double b, double c)
                  : "memory");
 }
 
-__global__ void __launch_bounds__(kThreads, 3) k_fft_x_inv(Geom g, const double* b0, const double* b1,
-                                                        const double* b2, double* __restrict__ E4,
-                                                        const double2* __restrict__ tw,
-                                                        double* __restrict__ partials) {
+__global__ void __launch_bounds__(kThreads, 3) k_fft_x_inv(Geom g, const double2* __restrict__ spec,
+                                                           double* __restrict__ E4,
+                                                           const double2* __restrict__ tw,
+                                                           double* __restrict__ partials) {
     extern __shared__ double2 sm[];
     __shared__ double red[3][kThreads / 32];
     const int len = g.n >> 1, logn = ilog2(len), R = xi_rows(g.n), ls = line_stride(len);
+    const int64_t nrows = (int64_t)g.nzl * g.n;
     const int64_t row0 = (int64_t)blockIdx.x * R;
-    const int rows = (int)min((int64_t)R, (int64_t)g.n * g.n - row0);
+    const int rows = (int)min((int64_t)R, nrows - row0);
     auto src = [&](int l, int k) {          // line l = rl * 3 + d
         const int rl = l / 3, d = l - 3 * rl;
-        const double* buf = d == 0 ? b0 : (d == 1 ? b1 : b2);
-        const double2* X = reinterpret_cast<const double2*>(buf + (row0 + rl) * g.rp);
+        const double2* X = spec + ((int64_t)d * nrows + row0 + rl) * g.px;
         const double2 xk = X[k], xc = conj2(X[len - k]);
         const double2 ze = cadd(xk, xc);
         const double2 zo = cmul(csub(xk, xc), conj2(__ldg(tw + k)));
@@ -387,49 +400,47 @@ __global__ void __launch_bounds__(1024) k_energy_reduce(Geom g, const double* __
 }  // namespace
 
 int energy_partials(const Geom& g) {
-    const int64_t nrows = (int64_t)g.n * g.n;
+    const int64_t nrows = (int64_t)g.nzl * g.n;
     return (int)((nrows + xi_rows(g.n) - 1) / xi_rows(g.n));
 }
 
 void launch_fft_x_fwd(const Geom& g, double* S0, const double2* tw, cudaStream_t s) {
     const int len = g.n / 2, R = x_rows(g.n);
     const size_t smem = sizeof(double2) * (size_t)R * line_stride(len);
-    const int64_t nrows = (int64_t)g.n * g.n;
+    const int64_t nrows = (int64_t)g.nzl * g.n;
     k_fft_x_fwd<<<(unsigned)((nrows + R - 1) / R), kThreads, smem, s>>>(g, S0, tw);
 }
 
-void launch_fft_y(const Geom& g, double* const buf[3], int ncomp, int inverse, const double2* tw,
-                  cudaStream_t s) {
+void launch_fft_y(const Geom& g, SpecLayout src, SpecLayout dst, int ncomp, int inverse,
+                  const double2* tw, cudaStream_t s) {
     const int TW = y_tw(g.n), ntiles = (g.n / 2 + 1 + TW - 1) / TW;
     const size_t smem = sizeof(double2) * (size_t)TW * line_stride(g.n);
-    dim3 grid(g.n * ntiles, ncomp);
-    if (inverse) k_fft_y<+1><<<grid, kThreads, smem, s>>>(g, buf[0], buf[1], buf[2], tw);
-    else k_fft_y<-1><<<grid, kThreads, smem, s>>>(g, buf[0], buf[1], buf[2], tw);
+    dim3 grid(g.nzl * ntiles, ncomp);
+    if (inverse) k_fft_y<+1><<<grid, kThreads, smem, s>>>(g, src, dst, tw);
+    else k_fft_y<-1><<<grid, kThreads, smem, s>>>(g, src, dst, tw);
 }
 
-void launch_fft_z_mul(const Geom& g, double* S0, double* S1, double* S2, double scale,
+void launch_fft_z_mul(const Geom& g, const double2* pencil, double2* out, double scale,
                       const double2* tw, cudaStream_t s) {
     const int TW = z_tw(g.n), ntiles = (g.n / 2 + 1 + TW - 1) / TW;
     const size_t smem = 2 * sizeof(double2) * (size_t)TW * line_stride(g.n);
-    k_fft_z_mul<<<g.n * ntiles, kThreads, smem, s>>>(
-        g, reinterpret_cast<double2*>(S0), reinterpret_cast<double2*>(S1),
-        reinterpret_cast<double2*>(S2), scale, tw);
+    k_fft_z_mul<<<(g.n / g.P) * ntiles, kThreads, smem, s>>>(g, pencil, out, scale, tw);
 }
 
-void launch_fft_x_inv(const Geom& g, const double* const spec[3], double* E4, const double2* tw,
+void launch_fft_x_inv(const Geom& g, const double2* spec, double* E4, const double2* tw,
                       double* partials, cudaStream_t s) {
     const int len = g.n / 2, R = xi_rows(g.n);
     const size_t smem = 3 * sizeof(double2) * (size_t)R * line_stride(len);
-    k_fft_x_inv<<<energy_partials(g), kThreads, smem, s>>>(g, spec[0], spec[1], spec[2], E4, tw, partials);
+    k_fft_x_inv<<<energy_partials(g), kThreads, smem, s>>>(g, spec, E4, tw, partials);
 }
 
 void launch_e4_extract(const Geom& g, const double* E4, int d, double* out, cudaStream_t s) {
-    const int64_t nn = (int64_t)g.n * g.n * g.n;
+    const int64_t nn = (int64_t)g.n * g.n * g.nzl;
     k_e4_extract<<<(unsigned)((nn + 255) / 256), 256, 0, s>>>(E4, nn, d, out);
 }
 
 void launch_e4_pack(const Geom& g, const double* const comp[3], double* E4, cudaStream_t s) {
-    const int64_t nn = (int64_t)g.n * g.n * g.n;
+    const int64_t nn = (int64_t)g.n * g.n * g.nzl;
     k_e4_pack<<<(unsigned)((nn + 255) / 256), 256, 0, s>>>(comp[0], comp[1], comp[2], nn, E4);
 }
 

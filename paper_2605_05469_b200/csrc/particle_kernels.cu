@@ -1,20 +1,23 @@
 // particle_kernels.cu -- particle side of the PIC step on sm_100a.
 //
 // Particle state lives in HBM as three streams of 128-bit pairs (pic_device.cuh):
-// (x, y), (z, v_z), (v_x, v_y).  One step (after the solve) is four kernels:
-//   push_key : stream the sorted particles, gather E (eight 256-bit node loads),
-//              kick v in place, drift to x' (not stored), key of the new cell,
-//              rank = count[key]++ (arrival order).
-//   scan     : offs = exclusive scan of count (3 kernels, 4096-cell tiles).
+// (x, y), (z, v_z), (v_x, v_y), sorted by the rank-local Morton cell key (D#14).
+// One step (after the solve) is:
+//   push_key : one CTA per brick of 256 cells: stage the brick's E node tile in
+//              shared memory, stream the brick's particles, gather E (CIC), kick v
+//              in place, drift to x' (not stored), key of the new cell and its
+//              arrival rank (count atomic).  P > 1: particles whose new cell lies in
+//              another slab go to that rank's send buffer (x', v', old global key,
+//              old index) instead.
+//   [P > 1: counts all-to-all, payload send/recv, arrivals keyed and counted]
+//   scan     : offs = exclusive scan of the cell counts.
 //   place    : perm[offs[key] + rank] = i (no atomics).
-//   reorder_deposit : one CTA per Morton brick of 256 cells (8 x 8 x 4): stable
-//              order inside each cell (D#14), gather x, v' through perm, the
-//              identical drift x' = wrap(x + v' dt), x', v' streamed to the stable
-//              slot, CIC charge summed per cell in registers, folded into a node
-//              tile in shared memory, one fp64 global reduction per node.
-// The drift is computed twice from bit-identical code (pic_device.cuh) instead of
-// storing x' in push_key (24 B/particle less traffic), and reorder_deposit does
-// no field gather at the scattered pre-sort positions.
+//   reorder_deposit : one CTA per brick: the stable order inside each cell (D#14),
+//              the particles gathered through perm with cp.async straight into
+//              their sorted slots in shared memory, the drift recomputed
+//              bit-identically from the stored v', x' v' streamed out coalesced,
+//              and the CIC charge summed per cell in stable order, folded into a
+//              node tile in shared memory and flushed with one fp64 RED.ADD per node.
 #include <algorithm>
 #include <cstdlib>
 
@@ -25,50 +28,129 @@ namespace pic {
 namespace {
 
 constexpr int kThreads = 256;
-constexpr int kBrick = 256;     // cells per reorder/deposit CTA (Morton 8 bits)
-constexpr int kCap = 2048;      // particles staged per chunk (29 B of shared memory each)
-constexpr int kBatch = 2;       // particles per thread with loads in flight together
-__constant__ int g_dbg_mode = 0;   // experiment switch (0 = the method)
+constexpr int kBrick = 256;     // cells per brick (Morton 8 bits: 8 x 8 x 4)
+constexpr int kCapA = 2048;     // particles per staged chunk of the P = 1 reorder (96 KB)
+constexpr int kCapG = 1024;     // particles per staged chunk of the P > 1 reorder
+constexpr uint32_t kNoKey = 0xffffffffu;
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+    const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
+    const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(s), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+    asm volatile("cp.async.commit_group;\n\tcp.async.wait_group 0;" ::: "memory");
+}
 
 // ---------------------------------------------------------------- init -----
 // Landau initial condition: x_d by Newton on the inverse CDF of
 // (1 + alpha cos(k x))/L from x = u_d L (|dx| < 1e-12 or 32 iterations),
-// velocities by Box-Muller from u_3..u_6, Philox counter = particle index (D#10).
-__global__ void __launch_bounds__(kThreads) k_sample(Geom g, PState st, int64_t np, double k,
-                                                     double alpha, uint32_t s0, uint32_t s1) {
-    const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (j >= np) return;
-    double u[8];
+// velocities by Box-Muller from u_3..u_6, Philox counter = global particle index
+// (D#10).
+__device__ __forceinline__ void uniforms(uint64_t j, uint32_t s0, uint32_t s1, double u[8]) {
 #pragma unroll
     for (int b = 0; b < 4; ++b) {
-        uint32_t c[4] = {(uint32_t)j, (uint32_t)((uint64_t)j >> 32), (uint32_t)b, 0u};
+        uint32_t c[4] = {(uint32_t)j, (uint32_t)(j >> 32), (uint32_t)b, 0u};
         philox4x32_10(c, s0, s1);
         const uint64_t w0 = (uint64_t)c[0] | ((uint64_t)c[1] << 32);
         const uint64_t w1 = (uint64_t)c[2] | ((uint64_t)c[3] << 32);
         u[2 * b] = (double)(w0 >> 11) * 0x1p-53;
         u[2 * b + 1] = (double)(w1 >> 11) * 0x1p-53;
     }
+}
+
+__device__ __forceinline__ double landau_x(const Geom& g, double u, double k, double alpha) {
     const double ak = alpha / k;
-    double x[3], v[3];
-    for (int d = 0; d < 3; ++d) {
-        const double target = u[d] * g.L;
-        double xx = target;
-        for (int it = 0; it < 32; ++it) {
-            const double F = __dsub_rn(__dadd_rn(xx, __dmul_rn(ak, sin(k * xx))), target);
-            const double dF = __dadd_rn(1.0, __dmul_rn(alpha, cos(k * xx)));
-            const double dx = __ddiv_rn(F, dF);
-            xx = __dsub_rn(xx, dx);
-            if (fabs(dx) < 1e-12) break;
-        }
-        x[d] = wrap(xx, g.L);
+    const double target = u * g.L;
+    double xx = target;
+    for (int it = 0; it < 32; ++it) {
+        const double F = __dsub_rn(__dadd_rn(xx, __dmul_rn(ak, sin(k * xx))), target);
+        const double dF = __dadd_rn(1.0, __dmul_rn(alpha, cos(k * xx)));
+        const double dx = __ddiv_rn(F, dF);
+        xx = __dsub_rn(xx, dx);
+        if (fabs(dx) < 1e-12) break;
     }
+    return wrap(xx, g.L);
+}
+
+__device__ __forceinline__ void landau_particle(const Geom& g, const double u[8], double k,
+                                                double alpha, double x[3], double v[3]) {
+    for (int d = 0; d < 3; ++d) x[d] = landau_x(g, u[d], k, alpha);
     const double two_pi = 6.283185307179586476925286766559;
     const double r1 = sqrt(-2.0 * log(1.0 - u[3]));
     const double r2 = sqrt(-2.0 * log(1.0 - u[5]));
     v[0] = r1 * cos(two_pi * u[4]);
     v[1] = r1 * sin(two_pi * u[4]);
     v[2] = r2 * cos(two_pi * u[6]);
+}
+
+__device__ __forceinline__ bool owns_z(const Geom& g, double z) {
+    const int iz = cell_of(__dmul_rn(z, g.inv_h), g.n);
+    return iz >= g.z0 && iz < g.z0 + g.nzl;
+}
+
+// P = 1: particle j at index j.
+__global__ void __launch_bounds__(kThreads) k_sample(Geom g, PState st, int64_t np, double k,
+                                                     double alpha, uint32_t s0, uint32_t s1) {
+    const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= np) return;
+    double u[8], x[3], v[3];
+    uniforms((uint64_t)j, s0, s1, u);
+    landau_particle(g, u, k, alpha, x, v);
     store_particle(st, j, x, v);
+}
+
+// P > 1, pass 1: owned particles of each block of 256 global indices (only z is
+// needed to decide ownership).
+__global__ void __launch_bounds__(kThreads) k_sample_count(Geom g, int64_t npg, double k, double alpha,
+                                                           uint32_t s0, uint32_t s1,
+                                                           uint32_t* __restrict__ bcount) {
+    __shared__ uint32_t red[kThreads / 32];
+    const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    bool own = false;
+    if (j < npg) {
+        double u[8];
+        uniforms((uint64_t)j, s0, s1, u);
+        own = owns_z(g, landau_x(g, u[2], k, alpha));
+    }
+    const uint32_t b = __popc(__ballot_sync(0xffffffffu, own));
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = b;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        uint32_t t = 0;
+        for (int w = 0; w < kThreads / 32; ++w) t += red[w];
+        bcount[blockIdx.x] = t;
+    }
+}
+
+// P > 1, pass 2: the owned particles written in ascending global index (the
+// oracle's initial order restricted to the slab, SURVEY c.1 Init 4).
+__global__ void __launch_bounds__(kThreads) k_sample_write(Geom g, PState st, int64_t npg, double k,
+                                                           double alpha, uint32_t s0, uint32_t s1,
+                                                           const uint32_t* __restrict__ boffs) {
+    __shared__ uint32_t wpre[kThreads / 32];
+    const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    double u[8];
+    bool own = false;
+    if (j < npg) {
+        uniforms((uint64_t)j, s0, s1, u);
+        own = owns_z(g, landau_x(g, u[2], k, alpha));
+    }
+    const unsigned bal = __ballot_sync(0xffffffffu, own);
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    if (lane == 0) wpre[wid] = __popc(bal);
+    __syncthreads();
+    uint32_t pre = 0;
+    for (int w = 0; w < wid; ++w) pre += wpre[w];
+    if (own) {
+        const int64_t o = (int64_t)boffs[blockIdx.x] + pre + __popc(bal & ((1u << lane) - 1u));
+        double x[3], v[3];
+        landau_particle(g, u, k, alpha, x, v);
+        store_particle(st, o, x, v);
+    }
 }
 
 __global__ void __launch_bounds__(kThreads) k_soa_to_pairs(const double* __restrict__ soa, int64_t np,
@@ -91,30 +173,27 @@ __global__ void __launch_bounds__(kThreads) k_pairs_to_soa(PState src, int64_t n
     for (int d = 0; d < 3; ++d) { soa[d * np + i] = x[d]; soa[(3 + d) * np + i] = v[d]; }
 }
 
-// ----------------------------------------------------------- push + key ----
-// Grid-stride over the sorted particles with the next particle's loads in flight
-// while the current one gathers E.  rank[i] = arrival order in the new cell
-// (return value of the count atomic), so the placement needs no second atomic.
-template <bool PUSH>
-__global__ void __launch_bounds__(kThreads) k_push_key(Geom g, PState cur, int64_t np,
-                                                       const double* __restrict__ E4,
-                                                       uint32_t* __restrict__ key,
-                                                       uint16_t* __restrict__ rank,
-                                                       uint32_t* __restrict__ count,
-                                                       int* __restrict__ err) {
+// ----------------------------------------------------------- key (import) ---
+// Particles in any order (init, pic_set_particles, re-deposit): key of the current
+// position, rank = count[key]++.  A position outside [0, L) or outside the slab
+// sets err[1].
+__global__ void __launch_bounds__(kThreads) k_key_import(Geom g, PState cur, int64_t np,
+                                                         uint32_t* __restrict__ key,
+                                                         uint16_t* __restrict__ rank,
+                                                         uint32_t* __restrict__ count,
+                                                         int* __restrict__ err) {
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < np; i += stride) {
         double x[3], v[3];
         load_particle(cur, i, x, v);
-        if (PUSH) {
-            const double z0 = x[2];
-            gather_push(g, E4, x, v);
-            cur.p[1][i] = make_double2(z0, v[2]);
-            cur.p[2][i] = make_double2(v[0], v[1]);
-        } else if (!(x[0] >= 0.0 && x[0] < g.L && x[1] >= 0.0 && x[1] < g.L && x[2] >= 0.0 && x[2] < g.L)) {
-            atomicExch(err + 1, 1);   // imported position outside [0, L)
+        int iz = 0;
+        uint32_t k = 0;
+        if (!(x[0] >= 0.0 && x[0] < g.L && x[1] >= 0.0 && x[1] < g.L && x[2] >= 0.0 && x[2] < g.L)) {
+            atomicExch(err + 1, 1);
+        } else {
+            k = key_of(g, x, &iz);
+            if (iz < g.z0 || iz >= g.z0 + g.nzl) { atomicExch(err + 1, 1); k = 0; }
         }
-        const uint32_t k = key_of(g, x);
         key[i] = k;
         const uint32_t r = atomicAdd(count + k, 1u);
         if (r > 0xffffu) atomicExch(err, 1);
@@ -122,26 +201,36 @@ __global__ void __launch_bounds__(kThreads) k_push_key(Geom g, PState cur, int64
     }
 }
 
-// The step's push: one CTA per Morton brick of 256 cells.  The particles of the
-// brick are the contiguous sorted range [offs[c0], offs[c0 + 256)) and all their
-// CIC corners lie in the brick's 9 x 9 x 5 node tile, which is staged in shared
-// memory (13 KB of node records) with coalesced loads; the gather then reads
-// shared memory.  Kick v in place, drift to x' (not stored), key, rank.
+// ----------------------------------------------------------- push + key ----
+// The step's push: one CTA per brick.  The brick's particles
+// are the contiguous sorted range [offs[c0], offs[c0 + 256)) and all their CIC
+// corners lie in the brick's 9 x 9 x 5 node tile (slab planes bz .. bz + 4, the
+// last possibly the halo), staged in shared memory; the gather reads it with the
+// same weights, corner order and fma chain as the oracle (D#17).  Kick v in place,
+// drift to x' (not stored), key, rank.  Leavers (P > 1) are packed into the send
+// buffer of their destination rank: 64 B = (x', y'), (z', vz'), (vx', vy'),
+// (old global key | old index << 32).
+struct SendBuf {
+    double2* data;        // [P][seg][4]
+    uint32_t* count;      // [P]
+    int seg;              // capacity per destination
+};
+
 __global__ void __launch_bounds__(kThreads) k_push_key_brick(Geom g, PState cur,
                                                              const uint32_t* __restrict__ offs,
                                                              const double* __restrict__ E4,
                                                              uint32_t* __restrict__ key,
                                                              uint16_t* __restrict__ rank,
                                                              uint32_t* __restrict__ count,
-                                                             int* __restrict__ err) {
+                                                             SendBuf sb, int* __restrict__ err) {
     __shared__ double4 etile[9 * 9 * 5];
     const int t = threadIdx.x;
     const uint32_t c0 = blockIdx.x * kBrick;
     int bx, by, bz;
-    unmorton(c0, bx, by, bz);
+    unlkey(g, c0, bx, by, bz);    // bz: slab plane
     for (int q = t; q < 9 * 9 * 5; q += kThreads) {
         const int nx = q % 9, ny = (q / 9) % 9, nz = q / 81;
-        const int64_t m = ((int64_t)((bz + nz) & g.nmask) * g.n + ((by + ny) & g.nmask)) * g.n + ((bx + nx) & g.nmask);
+        const int64_t m = ((int64_t)(bz + nz) * g.n + ((by + ny) & g.nmask)) * g.n + ((bx + nx) & g.nmask);
         double ex, ey, ez;
         ldg_node(E4 + 4 * m, ex, ey, ez);
         etile[q] = make_double4(ex, ey, ez, 0.0);
@@ -155,11 +244,12 @@ __global__ void __launch_bounds__(kThreads) k_push_key_brick(Geom g, PState cur,
         // next particle's loads in flight while this one waits on its count atomic
         if (i + kThreads < P1) load_particle(cur, i + kThreads, xn, vn);
         const double z0 = x[2];
-        // CIC gather from the tile: same weights, corner order and fma chain as gather_E
+        uint32_t oldg = 0;
+        if (g.P > 1) oldg = gkey_of(g, x);
         int ii[3];
         double w[3][2];
         cic_weights(g, x, ii, w);
-        const int lx = ii[0] - bx, ly = ii[1] - by, lz = ii[2] - bz;
+        const int lx = ii[0] - bx, ly = ii[1] - by, lz = ii[2] - g.z0 - bz;
         double e0 = 0.0, e1 = 0.0, e2 = 0.0;
 #pragma unroll
         for (int c = 0; c < 2; ++c)
@@ -179,7 +269,23 @@ __global__ void __launch_bounds__(kThreads) k_push_key_brick(Geom g, PState cur,
         drift(g, x, v);
         cur.p[1][i] = make_double2(z0, v[2]);    // kicked velocity in place: (x_n, v_{n+1/2})
         cur.p[2][i] = make_double2(v[0], v[1]);
-        const uint32_t k = key_of(g, x);
+        int iz;
+        uint32_t k = key_of(g, x, &iz);
+        if (g.P > 1 && (iz < g.z0 || iz >= g.z0 + g.nzl)) {   // leaver
+            const int dr = iz >> g.mz;
+            const uint32_t slot = atomicAdd(sb.count + dr, 1u);
+            if (slot < (uint32_t)sb.seg) {
+                double2* d = sb.data + ((int64_t)dr * sb.seg + slot) * 4;
+                d[0] = make_double2(x[0], x[1]);
+                d[1] = make_double2(x[2], v[2]);
+                d[2] = make_double2(v[0], v[1]);
+                d[3] = make_double2(__longlong_as_double((long long)((uint64_t)oldg | ((uint64_t)i << 32))), 0.0);
+            } else {
+                atomicExch(err + 2, 1);
+            }
+            key[i] = kNoKey;
+            continue;
+        }
         key[i] = k;
         const uint32_t r = atomicAdd(count + k, 1u);
         if (r > 0xffffu) atomicExch(err, 1);
@@ -187,13 +293,34 @@ __global__ void __launch_bounds__(kThreads) k_push_key_brick(Geom g, PState cur,
     }
 }
 
-__global__ void __launch_bounds__(kThreads) k_keys_only(Geom g, PState cur, int64_t np,
-                                                        uint32_t* __restrict__ key) {
+// Arrivals (P > 1): key and rank of each received particle, at extended index
+// n_old + a (the permutation addresses cur below n_old and the receive buffer above).
+__global__ void __launch_bounds__(kThreads) k_key_arrivals(Geom g, const double2* __restrict__ recv,
+                                                           int64_t narr, int64_t n_old,
+                                                           uint32_t* __restrict__ key,
+                                                           uint16_t* __restrict__ rank,
+                                                           uint32_t* __restrict__ count,
+                                                           int* __restrict__ err) {
+    const int64_t a = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (a >= narr) return;
+    const double2 p0 = recv[4 * a], p1 = recv[4 * a + 1];
+    const double x[3] = {p0.x, p0.y, p1.x};
+    int iz;
+    uint32_t k = key_of(g, x, &iz);
+    if (iz < g.z0 || iz >= g.z0 + g.nzl) { atomicExch(err + 1, 1); k = 0; }
+    key[n_old + a] = k;
+    const uint32_t r = atomicAdd(count + k, 1u);
+    if (r > 0xffffu) atomicExch(err, 1);
+    rank[n_old + a] = (uint16_t)r;
+}
+
+__global__ void __launch_bounds__(kThreads) k_gkeys(Geom g, PState cur, int64_t np,
+                                                    uint32_t* __restrict__ key) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= np) return;
     double x[3], v[3];
     load_particle(cur, i, x, v);
-    key[i] = key_of(g, x);
+    key[i] = gkey_of(g, x);
 }
 
 // ------------------------------------------------------------------ scan ---
@@ -312,75 +439,87 @@ __global__ void __launch_bounds__(kThreads) k_scan_apply(const uint32_t* __restr
 }
 
 // ----------------------------------------------------------------- place ---
-// perm[offs[key[i]] + rank[i]] = i  (no atomics: ranks came from push_key)
+// perm[offs[key[i]] + rank[i]] = i  (no atomics: ranks came from the count atomic);
+// leavers (key = kNoKey) are skipped.
 __global__ void __launch_bounds__(kThreads) k_place(const uint32_t* __restrict__ key,
                                                     const uint16_t* __restrict__ rank, int64_t np,
                                                     const uint32_t* __restrict__ offs,
                                                     uint32_t* __restrict__ perm) {
-    // 4 particles per thread: 16-byte key and 8-byte rank loads, 4 offset lookups in flight
     const int64_t i0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * 4;
     if (i0 >= np) return;
     if (i0 + 4 <= np) {
         const uint4 k4 = __ldg(reinterpret_cast<const uint4*>(key + i0));
         const uint2 r4 = __ldg(reinterpret_cast<const uint2*>(rank + i0));
-        const uint32_t o0 = __ldg(offs + k4.x), o1 = __ldg(offs + k4.y);
-        const uint32_t o2 = __ldg(offs + k4.z), o3 = __ldg(offs + k4.w);
-        perm[o0 + (r4.x & 0xffffu)] = (uint32_t)i0;
-        perm[o1 + (r4.x >> 16)] = (uint32_t)(i0 + 1);
-        perm[o2 + (r4.y & 0xffffu)] = (uint32_t)(i0 + 2);
-        perm[o3 + (r4.y >> 16)] = (uint32_t)(i0 + 3);
+        if (k4.x != kNoKey) perm[__ldg(offs + k4.x) + (r4.x & 0xffffu)] = (uint32_t)i0;
+        if (k4.y != kNoKey) perm[__ldg(offs + k4.y) + (r4.x >> 16)] = (uint32_t)(i0 + 1);
+        if (k4.z != kNoKey) perm[__ldg(offs + k4.z) + (r4.y & 0xffffu)] = (uint32_t)(i0 + 2);
+        if (k4.w != kNoKey) perm[__ldg(offs + k4.w) + (r4.y >> 16)] = (uint32_t)(i0 + 3);
     } else {
-        for (int64_t i = i0; i < np; ++i) perm[__ldg(offs + __ldg(key + i)) + __ldg(rank + i)] = (uint32_t)i;
+        for (int64_t i = i0; i < np; ++i) {
+            const uint32_t k = __ldg(key + i);
+            if (k != kNoKey) perm[__ldg(offs + k) + __ldg(rank + i)] = (uint32_t)i;
+        }
     }
 }
 
-// ------------------------------------------------- reorder + push + deposit -
-// Per chunk of the brick's sorted positions (whole cells, <= kCap particles):
-//   A  stage perm[chunk] (coalesced); each cell's thread tags its positions with
-//      the local cell id;
-//   B  thread per position p: stable rank r of its particle inside the cell
-//      (#perm entries of the cell below its own, broadcast reads), gather x, v'
-//      through perm, re-drift, store x', v' at the stable slot s0 + r, and keep
-//      the fractional offsets f = x' inv_h - i of the new position in shared
-//      memory at that slot;
-//   C  thread per cell: sum the 8 corner weights (w_x w_y) w_z of its particles in
-//      stable order in registers.
-// After the last chunk the 256 cells' sums are folded into the 9 x 9 x 5 node
-// tile (eight conflict-free passes) and flushed with one fp64 RED.ADD per node.
-// No atomics and no shuffles inside the CTA: the per-brick charge is deterministic.
-// FRAC_SMEM: keep the fractional offsets of the new positions in shared memory
-// (24 B per staged particle) for the per-cell sums; otherwise re-read x' from L2.
-// v3: the gather runs as cp.async (LDGSTS, 16 B, L2 only) straight into the stable
-// sorted slot of a shared-memory copy of the chunk: every thread keeps all of its
-// particles' loads in flight without holding registers.  Then, with the chunk in
-// shared memory in sorted order: drift in place, stream x', v' out with coalesced
-// 16-byte stores, and sum the CIC weights per cell from shared memory.
-constexpr int kCapA = 2048;     // particles per chunk of the cp.async variant (96 KB staged)
-
-__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
-    const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s), "l"(gmem) : "memory");
-}
-__device__ __forceinline__ void cp_async_wait_all() {
-    asm volatile("cp.async.commit_group;\n\tcp.async.wait_group 0;" ::: "memory");
+// Node tile of a brick: 9 x 9 x 5 nodes, slab planes bz .. bz + 4 (the last one
+// possibly the ghost plane nzl); x and y wrap periodically.
+__device__ __forceinline__ void fold_flush(const Geom& g, double* tile, const double acc[8], int t,
+                                           int bx, int by, int bz, double* __restrict__ rho) {
+    const int lx = (int)compact3((uint32_t)t), ly = (int)compact3((uint32_t)t >> 1),
+              lz = (int)compact3((uint32_t)t >> 2);
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+        const int a = q & 1, b = (q >> 1) & 1, c = q >> 2;
+        tile[((lz + c) * 9 + (ly + b)) * 9 + (lx + a)] += acc[q];
+        __syncthreads();
+    }
+    for (int q = t; q < 9 * 9 * 5; q += kThreads) {
+        const double val = tile[q];
+        if (val == 0.0) continue;
+        const int nx = q % 9, ny = (q / 9) % 9, nz = q / 81;
+        atomicAdd(rho + gidx(g, (bx + nx) & g.nmask, (by + ny) & g.nmask, bz + nz), val);
+    }
 }
 
+__device__ __forceinline__ void cic_acc(const Geom& g, const double x[3], double acc[8]) {
+    int ii[3];
+    double w[3][2];
+    cic_weights(g, x, ii, w);
+#pragma unroll
+    for (int q = 0; q < 8; ++q)
+        acc[q] = __dadd_rn(acc[q], __dmul_rn(__dmul_rn(w[0][q & 1], w[1][(q >> 1) & 1]), w[2][q >> 2]));
+}
+
+// Largest cb with soffs[cb] - soffs[ca] <= cap (uniform across the CTA).
+__device__ __forceinline__ int chunk_end(const uint32_t* soffs, int ca, int cap) {
+    int lo = ca + 1, hi = kBrick;
+    while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (soffs[mid] - soffs[ca] <= (uint32_t)cap) lo = mid; else hi = mid - 1;
+    }
+    return lo;
+}
+
+// ------------------------------------------------- reorder + deposit, P = 1 -
+// Ties inside a cell by pre-sort index (D#14).  The gather is cp.async (LDGSTS,
+// 16 B, L2 only) straight into the particle's stable slot of the staged chunk.
 template <bool PUSH>
-__global__ void __launch_bounds__(kThreads, 2) k_reorder_deposit_async(
+__global__ void __launch_bounds__(kThreads, 2) k_reorder_deposit(
     Geom g, const uint32_t* __restrict__ offs, const uint32_t* __restrict__ perm, PState cur,
     PState nxt, double* __restrict__ rho, int* __restrict__ err) {
     extern __shared__ double dyn_smem[];
-    double2* sp0 = reinterpret_cast<double2*>(dyn_smem);          // [kCapA] (x, y)
-    double2* sp1 = sp0 + kCapA;                                     // [kCapA] (z, vz)
-    double2* sp2 = sp1 + kCapA;                                     // [kCapA] (vx, vy)
-    double* tile = reinterpret_cast<double*>(sp2 + kCapA);         // [9*9*5]
-    uint32_t* sperm = reinterpret_cast<uint32_t*>(tile + 9 * 9 * 5);   // [kCapA]
-    uint32_t* soffs = sperm + kCapA;                                // [kBrick + 1]
-    uint8_t* scell = reinterpret_cast<uint8_t*>(soffs + kBrick + 1);   // [kCapA]
+    double2* sp0 = reinterpret_cast<double2*>(dyn_smem);               // [kCapA] (x, y)
+    double2* sp1 = sp0 + kCapA;                                          // [kCapA] (z, vz)
+    double2* sp2 = sp1 + kCapA;                                          // [kCapA] (vx, vy)
+    double* tile = reinterpret_cast<double*>(sp2 + kCapA);              // [9*9*5]
+    uint32_t* sperm = reinterpret_cast<uint32_t*>(tile + 9 * 9 * 5);    // [kCapA]
+    uint32_t* soffs = sperm + kCapA;                                     // [kBrick + 1]
+    uint8_t* scell = reinterpret_cast<uint8_t*>(soffs + kBrick + 1);    // [kCapA]
     const int t = threadIdx.x;
     const uint32_t c0 = blockIdx.x * kBrick;
     int bx, by, bz;
-    unmorton(c0, bx, by, bz);
+    unlkey(g, c0, bx, by, bz);
     soffs[t] = offs[c0 + t];
     if (t == 0) soffs[kBrick] = offs[c0 + kBrick];
     for (int q = t; q < 9 * 9 * 5; q += kThreads) tile[q] = 0.0;
@@ -395,12 +534,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_reorder_deposit_async(
             if (t == 0) atomicExch(err, 1);
             return;
         }
-        int lo = ca + 1, hi = kBrick;
-        while (lo < hi) {
-            const int mid = (lo + hi + 1) >> 1;
-            if (soffs[mid] - soffs[ca] <= (uint32_t)kCapA) lo = mid; else hi = mid - 1;
-        }
-        const int cb = lo;
+        const int cb = chunk_end(soffs, ca, kCapA);
         const uint32_t P0 = soffs[ca];
         const int cnt = (int)(soffs[cb] - P0);
         for (int p = t; p < cnt; p += kThreads) sperm[p] = __ldg(perm + P0 + p);
@@ -443,160 +577,123 @@ __global__ void __launch_bounds__(kThreads, 2) k_reorder_deposit_async(
         __syncthreads();
         // CIC charge: thread per cell, its particles in stable order from shared memory
         for (int p = s0; p < s1; ++p) {
-            const double2 a = sp0[p], b = sp1[p];
-            const double x[3] = {a.x, a.y, b.x};
-            int ii[3];
-            double w[3][2];
-            cic_weights(g, x, ii, w);
-#pragma unroll
-            for (int q = 0; q < 8; ++q)
-                acc[q] = __dadd_rn(acc[q], __dmul_rn(__dmul_rn(w[0][q & 1], w[1][(q >> 1) & 1]), w[2][q >> 2]));
+            const double x[3] = {sp0[p].x, sp0[p].y, sp1[p].x};
+            cic_acc(g, x, acc);
         }
         __syncthreads();
         ca = cb;
     }
-    const int lx = (int)compact3((uint32_t)t), ly = (int)compact3((uint32_t)t >> 1),
-              lz = (int)compact3((uint32_t)t >> 2);
-#pragma unroll
-    for (int q = 0; q < 8; ++q) {
-        const int a = q & 1, b = (q >> 1) & 1, c = q >> 2;
-        tile[((lz + c) * 9 + (ly + b)) * 9 + (lx + a)] += acc[q];
-        __syncthreads();
-    }
-    for (int q = t; q < 9 * 9 * 5; q += kThreads) {
-        const double val = tile[q];
-        if (val == 0.0) continue;
-        const int nx = q % 9, ny = (q / 9) % 9, nz = q / 81;
-        atomicAdd(rho + gidx(g, (bx + nx) & g.nmask, (by + ny) & g.nmask, (bz + nz) & g.nmask), val);
-    }
+    fold_flush(g, tile, acc, t, bx, by, bz, rho);
 }
 
-template <bool PUSH, bool FRAC_SMEM, int KB = kBatch>
-__global__ void __launch_bounds__(kThreads, KB > 2 ? 2 : (FRAC_SMEM ? 3 : 4)) k_reorder_deposit(
+// ------------------------------------------------- reorder + deposit, P > 1 -
+// Entries e < n_old are residents (cur, drifted here), e >= n_old arrivals (the
+// receive buffer, already drifted by their sender).  Ties inside a cell by (old
+// global key, old index) -- the order of the single-domain oracle's global stable
+// sort restricted to the slab (D#15).  Gather first (cp.async into slot p), then
+// rank, then stream out in sorted order.
+template <bool PUSH>
+__global__ void __launch_bounds__(kThreads, 2) k_reorder_deposit_mr(
     Geom g, const uint32_t* __restrict__ offs, const uint32_t* __restrict__ perm, PState cur,
-    PState nxt, double* __restrict__ rho, int* __restrict__ err) {
+    const double2* __restrict__ recv, int64_t n_old, PState nxt, double* __restrict__ rho,
+    int* __restrict__ err) {
     extern __shared__ double dyn_smem[];
-    double* tile = dyn_smem;                                                         // [9*9*5]
-    double(*sfrac)[kCap] = reinterpret_cast<double(*)[kCap]>(dyn_smem + 9 * 9 * 5);  // [3][kCap]
-    uint32_t* sperm = reinterpret_cast<uint32_t*>(dyn_smem + 9 * 9 * 5 + (FRAC_SMEM ? 3 * kCap : 0));
-    uint32_t* soffs = sperm + kCap;                                                  // [kBrick + 1]
-    uint8_t* scell = reinterpret_cast<uint8_t*>(soffs + kBrick + 1);                 // [kCap]
+    double2* sp0 = reinterpret_cast<double2*>(dyn_smem);               // [kCapG]
+    double2* sp1 = sp0 + kCapG;
+    double2* sp2 = sp1 + kCapG;
+    unsigned long long* stie = reinterpret_cast<unsigned long long*>(sp2 + kCapG);   // [kCapG]
+    double* tile = reinterpret_cast<double*>(stie + kCapG);              // [9*9*5]
+    uint32_t* sperm = reinterpret_cast<uint32_t*>(tile + 9 * 9 * 5);    // [kCapG]
+    uint32_t* soffs = sperm + kCapG;                                     // [kBrick + 1]
+    uint16_t* sidx = reinterpret_cast<uint16_t*>(soffs + kBrick + 1);   // [kCapG]
+    uint8_t* scell = reinterpret_cast<uint8_t*>(sidx + kCapG);          // [kCapG]
     const int t = threadIdx.x;
     const uint32_t c0 = blockIdx.x * kBrick;
     int bx, by, bz;
-    unmorton(c0, bx, by, bz);
+    unlkey(g, c0, bx, by, bz);
     soffs[t] = offs[c0 + t];
     if (t == 0) soffs[kBrick] = offs[c0 + kBrick];
     for (int q = t; q < 9 * 9 * 5; q += kThreads) tile[q] = 0.0;
     __syncthreads();
-
     double acc[8];
 #pragma unroll
     for (int q = 0; q < 8; ++q) acc[q] = 0.0;
     int ca = 0;
     while (ca < kBrick) {
-        // chunk = cells [ca, cb), the largest run with at most kCap particles
-        if (soffs[ca + 1] - soffs[ca] > (uint32_t)kCap) {
+        if (soffs[ca + 1] - soffs[ca] > (uint32_t)kCapG) {
             if (t == 0) atomicExch(err, 1);
             return;
         }
-        int lo = ca + 1, hi = kBrick;
-        while (lo < hi) {
-            const int mid = (lo + hi + 1) >> 1;
-            if (soffs[mid] - soffs[ca] <= (uint32_t)kCap) lo = mid; else hi = mid - 1;
-        }
-        const int cb = lo;
+        const int cb = chunk_end(soffs, ca, kCapG);
         const uint32_t P0 = soffs[ca];
         const int cnt = (int)(soffs[cb] - P0);
-        // A
-        for (int p = t; p < cnt; p += kThreads) sperm[p] = __ldg(perm + P0 + p);
+        for (int p = t; p < cnt; p += kThreads) {
+            const uint32_t e = __ldg(perm + P0 + p);
+            sperm[p] = e;
+            if (e < n_old) {
+                cp_async16(sp0 + p, cur.p[0] + e);
+                cp_async16(sp1 + p, cur.p[1] + e);
+                cp_async16(sp2 + p, cur.p[2] + e);
+            } else {
+                const double2* d = recv + 4 * ((int64_t)e - n_old);
+                cp_async16(sp0 + p, d);
+                cp_async16(sp1 + p, d + 1);
+                cp_async16(sp2 + p, d + 2);
+                cp_async8(stie + p, d + 3);      // old global key | old index << 32
+            }
+        }
         const bool mine = t >= ca && t < cb;
         const int s0 = mine ? (int)(soffs[t] - P0) : 0, s1 = mine ? (int)(soffs[t + 1] - P0) : 0;
         for (int p = s0; p < s1; ++p) scell[p] = (uint8_t)t;
+        cp_async_wait_all();
         __syncthreads();
-        // B, kBatch positions per thread at a time: all their gathers in flight together
-        for (int pb = t; pb < cnt; pb += KB * kThreads) {
-            int o[KB];
-            uint32_t j[KB];
-#pragma unroll
-            for (int k = 0; k < KB; ++k) {
-                const int p = pb + k * kThreads;
-                o[k] = -1;
-                if (p < cnt) {
-                    const int c = scell[p];
-                    const int q0 = (int)(soffs[c] - P0), q1 = (int)(soffs[c + 1] - P0);
-                    j[k] = sperm[p];
-                    int r = 0;
-                    if (g_dbg_mode == 1) r = p - q0;
-                    else for (int q = q0; q < q1; ++q) r += sperm[q] < j[k];
-                    o[k] = q0 + r;
+        // residents: tie key from x_n, then the drift; arrivals arrive drifted
+        for (int p = t; p < cnt; p += kThreads) {
+            const uint32_t e = sperm[p];
+            if (e < n_old) {
+                double x[3] = {sp0[p].x, sp0[p].y, sp1[p].x};
+                const double v[3] = {sp2[p].x, sp2[p].y, sp1[p].y};
+                const uint32_t og = gkey_of(g, x);
+                stie[p] = (unsigned long long)og | ((unsigned long long)e << 32);
+                if (PUSH) {
+                    drift(g, x, v);
+                    sp0[p] = make_double2(x[0], x[1]);
+                    sp1[p] = make_double2(x[2], v[2]);
                 }
             }
-            double2 a[KB], b[KB], e[KB];
-#pragma unroll
-            for (int k = 0; k < KB; ++k)
-                if (o[k] >= 0) {
-                    a[k] = __ldg(cur.p[0] + j[k]);
-                    b[k] = __ldg(cur.p[1] + j[k]);
-                    e[k] = __ldg(cur.p[2] + j[k]);
-                }
-#pragma unroll
-            for (int k = 0; k < KB; ++k)
-                if (o[k] >= 0) {
-                    double x[3] = {a[k].x, a[k].y, b[k].x}, v[3] = {e[k].x, e[k].y, b[k].y};
-                    if (PUSH) drift(g, x, v);    // v is already kicked (push_key)
-                    store_particle(nxt, (int64_t)P0 + o[k], x, v);
-                    if (FRAC_SMEM) {
-#pragma unroll
-                        for (int d = 0; d < 3; ++d) {
-                            const double sd = __dmul_rn(x[d], g.inv_h);
-                            sfrac[d][o[k]] = __dsub_rn(sd, (double)cell_of(sd, g.n));
-                        }
-                    }
-                }
         }
         __syncthreads();
-        // C
-        for (int p = s0; p < (g_dbg_mode == 1 ? s0 : s1); ++p) {
-            double fx, fy, fz;
-            if (FRAC_SMEM) {
-                fx = sfrac[0][p]; fy = sfrac[1][p]; fz = sfrac[2][p];
-            } else {   // this block's own stores, visible after the barrier; L2 reads
-                const double2 xy = __ldcg(nxt.p[0] + P0 + p);
-                const double2 zv = __ldcg(nxt.p[1] + P0 + p);
-                const double x3[3] = {xy.x, xy.y, zv.x};
-                double f3[3];
-#pragma unroll
-                for (int d = 0; d < 3; ++d) {
-                    const double sd = __dmul_rn(x3[d], g.inv_h);
-                    f3[d] = __dsub_rn(sd, (double)cell_of(sd, g.n));
-                }
-                fx = f3[0]; fy = f3[1]; fz = f3[2];
+        // stable rank by (old global key, old index): sidx[o] = staged slot
+        for (int p = t; p < cnt; p += kThreads) {
+            const int c = scell[p];
+            const int q0 = (int)(soffs[c] - P0), q1 = (int)(soffs[c + 1] - P0);
+            const unsigned long long me = stie[p];
+            const uint32_t mg = (uint32_t)me, mi = (uint32_t)(me >> 32);
+            int r = 0;
+            for (int q = q0; q < q1; ++q) {
+                const unsigned long long o = stie[q];
+                const uint32_t og = (uint32_t)o, oi = (uint32_t)(o >> 32);
+                r += (og < mg) || (og == mg && oi < mi);
             }
-            const double wx[2] = {__dsub_rn(1.0, fx), fx}, wy[2] = {__dsub_rn(1.0, fy), fy},
-                         wz[2] = {__dsub_rn(1.0, fz), fz};
-#pragma unroll
-            for (int q = 0; q < 8; ++q)
-                acc[q] = __dadd_rn(acc[q], __dmul_rn(__dmul_rn(wx[q & 1], wy[(q >> 1) & 1]), wz[q >> 2]));
+            sidx[q0 + r] = (uint16_t)p;
+        }
+        __syncthreads();
+        for (int o = t; o < cnt; o += kThreads) {
+            const int p = sidx[o];
+            const int64_t oo = (int64_t)P0 + o;
+            nxt.p[0][oo] = sp0[p];
+            nxt.p[1][oo] = sp1[p];
+            nxt.p[2][oo] = sp2[p];
+        }
+        for (int o = s0; o < s1; ++o) {
+            const int p = sidx[o];
+            const double x[3] = {sp0[p].x, sp0[p].y, sp1[p].x};
+            cic_acc(g, x, acc);
         }
         __syncthreads();
         ca = cb;
     }
-    // fold the cell sums into the node tile: pass q adds corner q of every cell
-    const int lx = (int)compact3((uint32_t)t), ly = (int)compact3((uint32_t)t >> 1),
-              lz = (int)compact3((uint32_t)t >> 2);
-#pragma unroll
-    for (int q = 0; q < 8; ++q) {
-        const int a = q & 1, b = (q >> 1) & 1, c = q >> 2;
-        tile[((lz + c) * 9 + (ly + b)) * 9 + (lx + a)] += acc[q];
-        __syncthreads();
-    }
-    for (int q = t; q < 9 * 9 * 5; q += kThreads) {
-        const double val = tile[q];
-        if (val == 0.0) continue;
-        const int nx = q % 9, ny = (q / 9) % 9, nz = q / 81;
-        atomicAdd(rho + gidx(g, (bx + nx) & g.nmask, (by + ny) & g.nmask, (bz + nz) & g.nmask), val);
-    }
+    fold_flush(g, tile, acc, t, bx, by, bz, rho);
 }
 
 __global__ void __launch_bounds__(kThreads) k_half_kick(Geom g, PState cur, int64_t np,
@@ -613,7 +710,7 @@ __global__ void __launch_bounds__(kThreads) k_half_kick(Geom g, PState cur, int6
 }
 
 // perm segments of every cell sorted ascending in place (export of the stable
-// permutation; the step itself ranks them in shared memory only).
+// permutation at P = 1; the step itself ranks them in shared memory only).
 __global__ void __launch_bounds__(kThreads) k_sort_segments(const uint32_t* __restrict__ offs,
                                                             int64_t ncell, uint32_t* __restrict__ perm) {
     const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -627,31 +724,45 @@ __global__ void __launch_bounds__(kThreads) k_sort_segments(const uint32_t* __re
     }
 }
 
+__global__ void k_add_plane(double* __restrict__ dst, const double* __restrict__ src, int64_t n) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) dst[i] += src[i];
+}
+
 inline unsigned blocks(int64_t n, int t) { return (unsigned)((n + t - 1) / t); }
 
-constexpr size_t kReorderAsyncSmem = sizeof(double2) * 3 * kCapA + sizeof(double) * 9 * 9 * 5 +
-                                      sizeof(uint32_t) * (kCapA + kBrick + 1) + kCapA;
-constexpr size_t reorder_smem(bool frac) {
-    return sizeof(double) * ((frac ? 3 * kCap : 0) + 9 * 9 * 5) + sizeof(uint32_t) * (kCap + kBrick + 1) + kCap;
-}
-int g_reorder_variant = -1;   // 1: fractional offsets staged in shared memory, 0: re-read from L2
-bool reorder_frac_smem() {
-    if (g_reorder_variant < 0) {
-        const char* e = getenv("PIC_REORDER_FRAC_SMEM");
-        g_reorder_variant = e ? atoi(e) != 0 : 1;
-        const char* m = getenv("PIC_DBG_MODE");
-        if (m) { int v = atoi(m); cudaMemcpyToSymbol(g_dbg_mode, &v, sizeof(int)); }
-    }
-    return g_reorder_variant != 0;
-}
+constexpr size_t kReorderSmem = sizeof(double2) * 3 * kCapA + sizeof(double) * 9 * 9 * 5 +
+                                sizeof(uint32_t) * (kCapA + kBrick + 1) + kCapA;
+constexpr size_t kReorderMrSmem = sizeof(double2) * 3 * kCapG + 8 * kCapG + sizeof(double) * 9 * 9 * 5 +
+                                  sizeof(uint32_t) * (kCapG + kBrick + 1) + 2 * kCapG + kCapG;
 
 }  // namespace
+
+void particles_set_smem_limits() {
+    cudaFuncSetAttribute(k_reorder_deposit<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kReorderSmem);
+    cudaFuncSetAttribute(k_reorder_deposit<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kReorderSmem);
+    cudaFuncSetAttribute(k_reorder_deposit_mr<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kReorderMrSmem);
+    cudaFuncSetAttribute(k_reorder_deposit_mr<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kReorderMrSmem);
+}
 
 void launch_sample(const Geom& g, PState st, int64_t np, double k, double alpha, uint64_t seed,
                    cudaStream_t s) {
     if (np == 0) return;
-    k_sample<<<blocks(np, kThreads), kThreads, 0, s>>>(g, st, np, k, alpha, (uint32_t)seed,
-                                                        (uint32_t)(seed >> 32));
+    k_sample<<<blocks(np, kThreads), kThreads, 0, s>>>(g, st, np, k, alpha, (uint32_t)seed, (uint32_t)(seed >> 32));
+}
+
+int64_t sample_blocks(int64_t npg) { return (npg + kThreads - 1) / kThreads; }
+
+void launch_sample_count(const Geom& g, int64_t npg, double k, double alpha, uint64_t seed,
+                         uint32_t* bcount, cudaStream_t s) {
+    k_sample_count<<<(unsigned)sample_blocks(npg), kThreads, 0, s>>>(g, npg, k, alpha, (uint32_t)seed,
+                                                                     (uint32_t)(seed >> 32), bcount);
+}
+
+void launch_sample_write(const Geom& g, PState st, int64_t npg, double k, double alpha, uint64_t seed,
+                         const uint32_t* boffs, cudaStream_t s) {
+    k_sample_write<<<(unsigned)sample_blocks(npg), kThreads, 0, s>>>(g, st, npg, k, alpha, (uint32_t)seed,
+                                                                     (uint32_t)(seed >> 32), boffs);
 }
 
 void launch_soa_to_pairs(const double* soa, int64_t np, PState dst, cudaStream_t s) {
@@ -664,33 +775,41 @@ void launch_pairs_to_soa(PState src, int64_t np, double* soa, cudaStream_t s) {
     k_pairs_to_soa<<<blocks(np, kThreads), kThreads, 0, s>>>(src, np, soa);
 }
 
-void launch_push_key(const Geom& g, PState cur, int64_t np, const uint32_t* offs, const double* E4,
-                     int push, uint32_t* key, uint16_t* rank, uint32_t* count, int* err_flag,
-                     cudaStream_t s) {
+void launch_key_import(const Geom& g, PState cur, int64_t np, uint32_t* key, uint16_t* rank,
+                       uint32_t* count, int* err_flag, cudaStream_t s) {
     if (np == 0) return;
-    if (push) {
-        const unsigned nbrick = (unsigned)(((int64_t)g.n * g.n * g.n) / kBrick);
-        k_push_key_brick<<<nbrick, kThreads, 0, s>>>(g, cur, offs, E4, key, rank, count, err_flag);
-    } else {
-        const unsigned nb = std::min<unsigned>(blocks(np, kThreads), 148u * 32u);
-        k_push_key<false><<<nb, kThreads, 0, s>>>(g, cur, np, E4, key, rank, count, err_flag);
-    }
+    const unsigned nb = std::min<unsigned>(blocks(np, kThreads), 148u * 32u);
+    k_key_import<<<nb, kThreads, 0, s>>>(g, cur, np, key, rank, count, err_flag);
 }
 
-void launch_keys_only(const Geom& g, PState cur, int64_t np, uint32_t* key, cudaStream_t s) {
+void launch_push_key(const Geom& g, PState cur, const uint32_t* offs, const double* E4, uint32_t* key,
+                     uint16_t* rank, uint32_t* count, double2* send, uint32_t* send_count, int seg,
+                     int* err_flag, cudaStream_t s) {
+    const unsigned nbrick = (unsigned)(((int64_t)g.n * g.n * g.nzl) / kBrick);
+    SendBuf sb{send, send_count, seg};
+    k_push_key_brick<<<nbrick, kThreads, 0, s>>>(g, cur, offs, E4, key, rank, count, sb, err_flag);
+}
+
+void launch_key_arrivals(const Geom& g, const double2* recv, int64_t narr, int64_t n_old, uint32_t* key,
+                         uint16_t* rank, uint32_t* count, int* err_flag, cudaStream_t s) {
+    if (narr == 0) return;
+    k_key_arrivals<<<blocks(narr, kThreads), kThreads, 0, s>>>(g, recv, narr, n_old, key, rank, count, err_flag);
+}
+
+void launch_gkeys(const Geom& g, PState cur, int64_t np, uint32_t* key, cudaStream_t s) {
     if (np == 0) return;
-    k_keys_only<<<blocks(np, kThreads), kThreads, 0, s>>>(g, cur, np, key);
+    k_gkeys<<<blocks(np, kThreads), kThreads, 0, s>>>(g, cur, np, key);
 }
 
-size_t scan_scratch_bytes(int64_t ncell) {
-    return sizeof(uint32_t) * (size_t)(blocks(ncell, kScanTile) + 1);
+size_t scan_scratch_bytes(int64_t n) {
+    return sizeof(uint32_t) * (size_t)(blocks(n, kScanTile) + 1);
 }
 
-void launch_scan(const uint32_t* count, uint32_t* offs, int64_t ncell, uint32_t* scratch, cudaStream_t s) {
-    const unsigned nb = blocks(ncell, kScanTile);
-    k_scan_reduce<<<nb, kThreads, 0, s>>>(count, ncell, scratch);
+void launch_scan(const uint32_t* count, uint32_t* offs, int64_t n, uint32_t* scratch, cudaStream_t s) {
+    const unsigned nb = blocks(n, kScanTile);
+    k_scan_reduce<<<nb, kThreads, 0, s>>>(count, n, scratch);
     k_scan_bsum<<<1, 1024, 0, s>>>(scratch, (int)nb);
-    k_scan_apply<<<nb, kThreads, 0, s>>>(count, offs, ncell, scratch);
+    k_scan_apply<<<nb, kThreads, 0, s>>>(count, offs, n, scratch);
 }
 
 void launch_place(const uint32_t* key, const uint16_t* rank, int64_t np, const uint32_t* offs,
@@ -700,42 +819,18 @@ void launch_place(const uint32_t* key, const uint16_t* rank, int64_t np, const u
 }
 
 void launch_reorder_deposit(const Geom& g, const uint32_t* offs, const uint32_t* perm, PState cur,
-                            PState nxt, int push, double* rho_buf, int* err_flag, cudaStream_t s) {
-    const unsigned nbrick = (unsigned)(((int64_t)g.n * g.n * g.n) / kBrick);
-    static const int variant = getenv("PIC_REORDER_VARIANT") ? atoi(getenv("PIC_REORDER_VARIANT")) : 3;
-    if (variant == 3) {
+                            const double2* recv, int64_t n_old, PState nxt, int push, double* rho_buf,
+                            int* err_flag, cudaStream_t s) {
+    const unsigned nbrick = (unsigned)(((int64_t)g.n * g.n * g.nzl) / kBrick);
+    if (g.P == 1) {
+        if (push) k_reorder_deposit<true><<<nbrick, kThreads, kReorderSmem, s>>>(g, offs, perm, cur, nxt, rho_buf, err_flag);
+        else k_reorder_deposit<false><<<nbrick, kThreads, kReorderSmem, s>>>(g, offs, perm, cur, nxt, rho_buf, err_flag);
+    } else {
         if (push)
-            k_reorder_deposit_async<true><<<nbrick, kThreads, kReorderAsyncSmem, s>>>(g, offs, perm, cur, nxt, rho_buf, err_flag);
+            k_reorder_deposit_mr<true><<<nbrick, kThreads, kReorderMrSmem, s>>>(g, offs, perm, cur, recv, n_old, nxt, rho_buf, err_flag);
         else
-            k_reorder_deposit_async<false><<<nbrick, kThreads, kReorderAsyncSmem, s>>>(g, offs, perm, cur, nxt, rho_buf, err_flag);
-        return;
+            k_reorder_deposit_mr<false><<<nbrick, kThreads, kReorderMrSmem, s>>>(g, offs, perm, cur, recv, n_old, nxt, rho_buf, err_flag);
     }
-    const bool fs = reorder_frac_smem();
-    const size_t sm = reorder_smem(fs);
-    static const int kb = getenv("PIC_REORDER_KB") ? atoi(getenv("PIC_REORDER_KB")) : 4;
-    if (push && fs && kb == 4)
-        k_reorder_deposit<true, true, 4><<<nbrick, kThreads, sm, s>>>(g, offs, perm, cur, nxt, rho_buf, err_flag);
-    else if (push && fs && kb == 8)
-        k_reorder_deposit<true, true, 8><<<nbrick, kThreads, sm, s>>>(g, offs, perm, cur, nxt, rho_buf, err_flag);
-    else if (push && fs)
-        k_reorder_deposit<true, true><<<nbrick, kThreads, sm, s>>>(g, offs, perm, cur, nxt, rho_buf, err_flag);
-    else if (push)
-        k_reorder_deposit<true, false><<<nbrick, kThreads, sm, s>>>(g, offs, perm, cur, nxt, rho_buf, err_flag);
-    else if (fs)
-        k_reorder_deposit<false, true><<<nbrick, kThreads, sm, s>>>(g, offs, perm, cur, nxt, rho_buf, err_flag);
-    else
-        k_reorder_deposit<false, false><<<nbrick, kThreads, sm, s>>>(g, offs, perm, cur, nxt, rho_buf, err_flag);
-}
-
-void particles_set_smem_limits() {
-    cudaFuncSetAttribute(k_reorder_deposit_async<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kReorderAsyncSmem);
-    cudaFuncSetAttribute(k_reorder_deposit_async<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kReorderAsyncSmem);
-    cudaFuncSetAttribute(k_reorder_deposit<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)reorder_smem(true));
-    cudaFuncSetAttribute(k_reorder_deposit<true, true, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)reorder_smem(true));
-    cudaFuncSetAttribute(k_reorder_deposit<true, true, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)reorder_smem(true));
-    cudaFuncSetAttribute(k_reorder_deposit<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)reorder_smem(true));
-    cudaFuncSetAttribute(k_reorder_deposit<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)reorder_smem(false));
-    cudaFuncSetAttribute(k_reorder_deposit<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)reorder_smem(false));
 }
 
 void launch_sort_segments(const uint32_t* offs, int64_t ncell, uint32_t* perm, cudaStream_t s) {
@@ -745,6 +840,10 @@ void launch_sort_segments(const uint32_t* offs, int64_t ncell, uint32_t* perm, c
 void launch_half_kick(const Geom& g, PState cur, int64_t np, const double* E4, cudaStream_t s) {
     if (np == 0) return;
     k_half_kick<<<blocks(np, kThreads), kThreads, 0, s>>>(g, cur, np, E4);
+}
+
+void launch_add_plane(double* dst, const double* src, int64_t n, cudaStream_t s) {
+    k_add_plane<<<blocks(n, kThreads), kThreads, 0, s>>>(dst, src, n);
 }
 
 }  // namespace pic

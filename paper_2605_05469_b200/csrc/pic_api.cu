@@ -1,12 +1,19 @@
 // pic_api.cu -- C ABI (include/pic.h) and the host-side orchestration of the
 // PIC step.  The host validates, carves the caller's workspace and enqueues
-// kernels on the caller's stream; every step of the path runs on the device
-// (kernels.h).  One step:
-//   SOLVE   fft_x_fwd -> fft_y_fwd -> fft_z_mul -> fft_y_inv -> fft_x_inv (E4) -> energy
+// kernels and NCCL calls on the caller's stream; every step of the path runs on
+// the device (kernels.h).  One rank owns a z-slab of nzl = N/P planes (P = 1: the
+// whole box).  One step:
+//   SOLVE   fft_x_fwd -> fft_y_fwd (-> ncclAlltoAll) -> fft_z_mul (-> ncclAlltoAll)
+//           -> fft_y_inv -> fft_x_inv (E4) -> energy (-> ncclAllReduce) -> E halo plane
 //   CLEAR   count = 0, rho = 0
-//   PUSH    push_key  (gather + push + new key + count)
+//   PUSH    push_key (gather + kick + drift + key/rank; leavers -> send buffers)
+//           [P > 1: counts ncclAlltoAll, payload ncclSend/ncclRecv, arrivals keyed]
 //   SORT    scan -> place
-//   SCATTER reorder_deposit (sorted gather + push + stream out + CIC deposit)
+//   SCATTER reorder_deposit (sorted gather + drift + stream out + CIC deposit)
+//           -> ghost plane folded into the next slab's plane 0
+#include <nccl.h>
+
+#include <algorithm>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -16,13 +23,9 @@
 #include "../../include/pic.h"
 #include "kernels.h"
 
-namespace pic {
-void fft_set_smem_limits();
-void particles_set_smem_limits();
-}
-
 using pic::Geom;
 using pic::PState;
+using pic::SpecLayout;
 
 namespace {
 
@@ -31,19 +34,27 @@ constexpr int kMaxEnergySteps = 4096;   // device ring of per-step (W_x, W)
 
 const char* kStageNames[PIC_NSTAGES] = {
     "fft_x_fwd", "fft_y_fwd", "fft_z_mul", "fft_y_inv", "fft_x_inv", "energy",
-    "clear",     "push_key",  "scan",      "place",     "reorder_deposit"};
+    "clear",     "push_key",  "scan",      "place",     "reorder_deposit", "exchange"};
 
 size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
 
 bool is_pow2(int v) { return v > 0 && (v & (v - 1)) == 0; }
+
+int ilog2i(int v) {
+    int l = 0;
+    while ((1 << l) < v) ++l;
+    return l;
+}
 
 }  // namespace
 
 struct pic_ctx {
     pic_params p{};
     Geom g{};
-    int64_t np = 0;
-    int64_t ncell = 0;
+    int64_t np = 0;               // particles on this rank now
+    int64_t np_cap = 0;           // capacity of the particle arrays of this rank
+    int64_t np_glob = 0;          // N_p of the whole box
+    int64_t ncell = 0;            // cells of the slab, n^2 nzl
     double q = 0.0;               // macro charge -L^3 / N_p
     double deposit_scale = 0.0;   // q inv_h^3 (raw CIC weight sums -> rho)
     cudaStream_t stream = nullptr;
@@ -51,27 +62,40 @@ struct pic_ctx {
     char err[512] = "";
     double2* part[2][3] = {};     // double-buffered pair streams (pic_device.cuh)
     int cur = 0;
-    uint32_t* key = nullptr;
-    uint16_t* rank = nullptr;     // arrival order of each particle in its new cell
-    uint32_t* perm = nullptr;
+    uint32_t* key = nullptr;      // [np_cap + recv_cap] (extended index space)
+    uint16_t* rank = nullptr;
+    uint32_t* perm = nullptr;     // [np_cap]
     uint32_t* count = nullptr;
     uint32_t* offs = nullptr;
     uint32_t* scan_scratch = nullptr;
-    double* rho = nullptr;        // S0: pitched raw CIC weight sums / spectrum during the solve
-    double* spec[2] = {};         // S1, S2: half spectra of E_x, E_y during the solve
-    double* E4 = nullptr;         // field node records (E_x, E_y, E_z, 0)
+    double* rho = nullptr;        // (nzl + 1) pitched real planes; half spectrum S0 in the solve
+    double2* specA = nullptr;     // forward transpose send (P = 1: rho)
+    double2* specB = nullptr;     // ky-pencil (P = 1: rho)
+    double2* specC = nullptr;     // 3 components: z-pass out, y-inverse out
+    double2* specD = nullptr;     // return transpose receive (P = 1: specC)
+    double* E4 = nullptr;         // (nzl + 1) planes of node records (E_x, E_y, E_z, 0)
+    double* ghost = nullptr;      // P > 1: received ghost plane of rho
     double2* tw = nullptr;
     double* partials = nullptr;
     double* energies = nullptr;   // ring [kMaxEnergySteps][2]
     int* err_flag = nullptr;
     int last_slot = -1;
+    // migration (P > 1)
+    double2* send = nullptr;      // [P][seg][4]
+    uint32_t* send_count = nullptr;
+    uint32_t* recv_count = nullptr;
+    int seg = 0;
+    double2* recv = nullptr;      // [recv_cap][4]
+    int64_t recv_cap = 0;
+    int64_t migrated = 0;         // particles sent by this rank (all steps)
+    ncclComm_t comm = nullptr;
     // timing
     bool timing = false;
     double stage_ms[PIC_NSTAGES] = {};
     int64_t stage_launches[PIC_NSTAGES] = {};
     std::vector<cudaEvent_t> ev_pool;
-    std::vector<int> ev_stage;    // stage of pending pair k (events 2k, 2k+1)
-    size_t ev_used = 0;           // pairs in use
+    std::vector<int> ev_stage;
+    size_t ev_used = 0;
 };
 
 namespace {
@@ -79,12 +103,17 @@ namespace {
 // ------------------------------------------------------------ validation ---
 pic_status validate(const pic_params* p, int32_t rank, int32_t nranks, char* msg, size_t msz) {
     if (!p) { snprintf(msg, msz, "params is NULL"); return PIC_EINVAL; }
-    if (nranks != 1 || rank != 0) {
-        snprintf(msg, msz, "nranks=%d rank=%d: this build runs one rank (nranks == 1)", nranks, rank);
-        return nranks < 1 || rank < 0 || rank >= nranks ? PIC_EINVAL : PIC_EUNSUPPORTED;
+    if (!(nranks == 1 || nranks == 2 || nranks == 4 || nranks == 8) || rank < 0 || rank >= nranks) {
+        snprintf(msg, msz, "nranks=%d rank=%d: nranks must be 1, 2, 4 or 8", nranks, rank);
+        return PIC_EINVAL;
     }
-    if (p->pgrid[0] != 1 || p->pgrid[1] != 1) { snprintf(msg, msz, "pgrid must be {1,1}"); return PIC_EINVAL; }
+    if (!(p->pgrid[0] == 1 && p->pgrid[1] == nranks)) {
+        snprintf(msg, msz, "pgrid = {%d, %d}: this build decomposes in z-slabs only, pgrid = {1, nranks}",
+                 p->pgrid[0], p->pgrid[1]);
+        return p->pgrid[0] * p->pgrid[1] == nranks && p->pgrid[0] > 0 ? PIC_EUNSUPPORTED : PIC_EINVAL;
+    }
     if (!is_pow2(p->n) || p->n < 16 || p->n > 1024) { snprintf(msg, msz, "n=%d: power of two in [16,1024]", p->n); return PIC_EINVAL; }
+    if (p->n / nranks < 4) { snprintf(msg, msz, "n/nranks = %d: slabs need >= 4 planes", p->n / nranks); return PIC_EINVAL; }
     if (p->ppc <= 0 || p->ppc > 1024) { snprintf(msg, msz, "ppc=%d: must be in [1,1024]", p->ppc); return PIC_EINVAL; }
     if (!(p->k > 0) || !std::isfinite(p->k)) { snprintf(msg, msz, "k must be > 0"); return PIC_EINVAL; }
     if (!(p->alpha >= 0 && p->alpha < 1)) { snprintf(msg, msz, "alpha=%g: need 0 <= alpha < 1", p->alpha); return PIC_EINVAL; }
@@ -96,12 +125,15 @@ pic_status validate(const pic_params* p, int32_t rank, int32_t nranks, char* msg
         snprintf(msg, msz, "k L / 2 pi = %g must be a positive integer", m);
         return PIC_EINVAL;
     }
-    const double np = (double)p->ppc * p->n * p->n * p->n;
-    if (np >= 4294967296.0) { snprintf(msg, msz, "N_p = %.0f >= 2^32 on one rank", np); return PIC_EINVAL; }
+    const double np = (double)p->ppc * p->n * p->n * p->n / nranks;
+    if (np * (nranks > 1 ? 1.3 : 1.0) >= 4294967296.0) {
+        snprintf(msg, msz, "N_p per rank = %.0f too large for 32-bit indices", np);
+        return PIC_EINVAL;
+    }
     return PIC_OK;
 }
 
-Geom make_geom(const pic_params* p) {
+Geom make_geom(const pic_params* p, int rank, int nranks) {
     Geom g{};
     g.n = p->n;
     g.nmask = p->n - 1;
@@ -111,11 +143,41 @@ Geom make_geom(const pic_params* p) {
     g.inv_h = (double)p->n / g.L;
     g.dt = p->dt;
     g.qm_dt = -1.0 * p->dt;     // q/m = -1
+    g.P = nranks;
+    g.rank = rank;
+    g.nzl = p->n / nranks;
+    g.mz = ilog2i(g.nzl);
+    g.z0 = rank * g.nzl;
     return g;
 }
 
+struct Sizes {
+    int64_t np_nom, np_cap, recv_cap, nkey;
+    int seg;
+};
+
+Sizes sizes(const pic_params* p, const Geom& g) {
+    Sizes s{};
+    const int64_t npg = (int64_t)p->ppc * p->n * p->n * p->n;
+    s.np_nom = npg / g.P;
+    if (g.P == 1) {
+        s.np_cap = s.np_nom;
+        s.recv_cap = 0;
+        s.seg = 0;
+    } else {
+        // slab imbalance <= alpha (density (1 + alpha cos k z)), plus fluctuations
+        s.np_cap = (int64_t)(s.np_nom * (1.0 + p->alpha) * 1.05) + 65536;
+        // a slab of nzl planes loses ~ 2 E[max(v_z, 0)] dt / (nzl h) per step (SURVEY
+        // A.4: 2.5% at 512^3 / 8 ranks); segments sized for 8% of the slab
+        s.seg = (int)std::min<int64_t>(s.np_cap, (int64_t)(0.08 * s.np_cap) + 4096);
+        s.recv_cap = 2 * (int64_t)s.seg;
+    }
+    s.nkey = s.np_cap + s.recv_cap;
+    return s;
+}
+
 // Carve the workspace; returns the bytes needed (pointers set when c != nullptr).
-size_t carve(pic_ctx* c, const Geom& g, int64_t np, char* base) {
+size_t carve(pic_ctx* c, const Geom& g, const Sizes& z, char* base) {
     size_t off = 0;
     auto take = [&](size_t bytes) -> char* {
         off = align_up(off, 256);
@@ -123,27 +185,35 @@ size_t carve(pic_ctx* c, const Geom& g, int64_t np, char* base) {
         off += bytes;
         return ptr;
     };
-    const int64_t ncell = (int64_t)g.n * g.n * g.n;
-    const size_t grid_bytes = sizeof(double2) * (size_t)g.n * g.n * g.px;
+    const int64_t ncell = (int64_t)g.n * g.n * g.nzl;
+    const size_t plane = sizeof(double) * (size_t)g.n * g.rp;          // one pitched real plane
+    const size_t unit = sizeof(double2) * (size_t)g.nzl * g.n * g.px;   // one slab half spectrum
     for (int b = 0; b < 2; ++b)
         for (int a = 0; a < 3; ++a) {
-            char* ptr = take(sizeof(double2) * (size_t)np);
+            char* ptr = take(sizeof(double2) * (size_t)z.np_cap);
             if (c) c->part[b][a] = reinterpret_cast<double2*>(ptr);
         }
-    char* k = take(sizeof(uint32_t) * (size_t)np);
-    char* rk = take(sizeof(uint16_t) * (size_t)np);
-    char* pm = take(sizeof(uint32_t) * (size_t)np);
+    const int64_t nblk = g.P > 1 ? pic::sample_blocks(z.np_nom * g.P) : 0;   // init scratch
+    char* k = take(sizeof(uint32_t) * (size_t)std::max(z.nkey, nblk));
+    char* rk = take(sizeof(uint16_t) * (size_t)z.nkey);
+    char* pm = take(sizeof(uint32_t) * (size_t)std::max(z.np_cap, nblk + 1));
     char* cn = take(sizeof(uint32_t) * (size_t)ncell);
     char* of = take(sizeof(uint32_t) * (size_t)(ncell + 1));
-    char* ss = take(pic::scan_scratch_bytes(ncell));
-    char* rh = take(grid_bytes);
-    char* s1 = take(grid_bytes);
-    char* s2 = take(grid_bytes);
-    char* e4 = take(sizeof(double) * 4 * (size_t)ncell);
+    char* ss = take(pic::scan_scratch_bytes(std::max(ncell, nblk)));
+    char* rh = take(plane * (size_t)(g.nzl + 1));
+    char* sA = g.P > 1 ? take(unit) : nullptr;
+    char* sB = g.P > 1 ? take(unit) : nullptr;
+    char* sC = take(3 * unit);
+    char* sD = g.P > 1 ? take(3 * unit) : nullptr;
+    char* e4 = take(sizeof(double) * 4 * (size_t)g.n * g.n * (g.nzl + 1));
+    char* gh = g.P > 1 ? take(plane) : nullptr;
     char* tw = take(sizeof(double2) * (size_t)g.n);
     char* pa = take(sizeof(double) * 3 * (size_t)pic::energy_partials(g));
     char* en = take(sizeof(double) * 2 * kMaxEnergySteps);
     char* ef = take(sizeof(int) * 4);
+    char* sd = g.P > 1 ? take(sizeof(double2) * 4 * (size_t)z.seg * g.P) : nullptr;
+    char* sc = take(sizeof(uint32_t) * 2 * 8);
+    char* rv = g.P > 1 ? take(sizeof(double2) * 4 * (size_t)z.recv_cap) : nullptr;
     if (c) {
         c->key = reinterpret_cast<uint32_t*>(k);
         c->rank = reinterpret_cast<uint16_t*>(rk);
@@ -152,13 +222,23 @@ size_t carve(pic_ctx* c, const Geom& g, int64_t np, char* base) {
         c->offs = reinterpret_cast<uint32_t*>(of);
         c->scan_scratch = reinterpret_cast<uint32_t*>(ss);
         c->rho = reinterpret_cast<double*>(rh);
-        c->spec[0] = reinterpret_cast<double*>(s1);
-        c->spec[1] = reinterpret_cast<double*>(s2);
+        c->specA = g.P > 1 ? reinterpret_cast<double2*>(sA) : reinterpret_cast<double2*>(rh);
+        c->specB = g.P > 1 ? reinterpret_cast<double2*>(sB) : reinterpret_cast<double2*>(rh);
+        c->specC = reinterpret_cast<double2*>(sC);
+        c->specD = g.P > 1 ? reinterpret_cast<double2*>(sD) : reinterpret_cast<double2*>(sC);
         c->E4 = reinterpret_cast<double*>(e4);
+        c->ghost = reinterpret_cast<double*>(gh);
         c->tw = reinterpret_cast<double2*>(tw);
         c->partials = reinterpret_cast<double*>(pa);
         c->energies = reinterpret_cast<double*>(en);
         c->err_flag = reinterpret_cast<int*>(ef);
+        c->send = reinterpret_cast<double2*>(sd);
+        c->send_count = reinterpret_cast<uint32_t*>(sc);
+        c->recv_count = reinterpret_cast<uint32_t*>(sc) + 8;
+        c->seg = z.seg;
+        c->recv = reinterpret_cast<double2*>(rv);
+        c->recv_cap = z.recv_cap;
+        c->np_cap = z.np_cap;
     }
     return align_up(off, 256);
 }
@@ -168,7 +248,7 @@ pic_status fail(pic_ctx* c, pic_status st, const char* what, cudaError_t e = cud
         snprintf(c->err, sizeof(c->err), "%s: %s", what, cudaGetErrorString(e));
     else
         snprintf(c->err, sizeof(c->err), "%s", what);
-    if (st == PIC_ECUDA) c->poisoned = true;
+    if (st == PIC_ECUDA || st == PIC_ENCCL || st == PIC_EOVERFLOW) c->poisoned = true;
     return st;
 }
 
@@ -182,6 +262,28 @@ pic_status fail(pic_ctx* c, pic_status st, const char* what, cudaError_t e = cud
     do {                                                                 \
         cudaError_t e_ = cudaGetLastError();                             \
         if (e_ != cudaSuccess) return fail((ctx), PIC_ECUDA, what, e_);  \
+    } while (0)
+
+#define PIC_NCCL(ctx, call)                                                                     \
+    do {                                                                                        \
+        ncclResult_t r_ = (call);                                                               \
+        if (r_ != ncclSuccess) {                                                                \
+            snprintf((ctx)->err, sizeof((ctx)->err), "%s: %s", #call, ncclGetErrorString(r_)); \
+            (ctx)->poisoned = true;                                                             \
+            return PIC_ENCCL;                                                                   \
+        }                                                                                       \
+    } while (0)
+
+#define PIC_TRY(expr)                       \
+    do {                                    \
+        pic_status s_ = (expr);             \
+        if (s_ != PIC_OK) return s_;        \
+    } while (0)
+
+#define PIC_CHECK_CTX(c)                                 \
+    do {                                                 \
+        if (!(c)) return PIC_EINVAL;                     \
+        if ((c)->poisoned) return PIC_EPOISONED;         \
     } while (0)
 
 // ---------------------------------------------------------------- timing ---
@@ -225,69 +327,184 @@ PState state(pic_ctx* c, int b) {
     return s;
 }
 
-// rho (raw CIC sums, scaled by `scale` in the multiply) -> E, energies -> ring slot
+int up(const pic_ctx* c) { return (c->g.rank + 1) % c->g.P; }
+int down(const pic_ctx* c) { return (c->g.rank + c->g.P - 1) % c->g.P; }
+
+// E halo plane nzl = the next slab's plane 0 (P = 1: own plane 0, periodic).
+pic_status fill_E_halo(pic_ctx* c) {
+    const Geom& g = c->g;
+    const size_t pl = (size_t)4 * g.n * g.n;   // doubles per E4 plane
+    double* halo = c->E4 + pl * g.nzl;
+    if (g.P == 1) {
+        PIC_CUDA(c, cudaMemcpyAsync(halo, c->E4, sizeof(double) * pl, cudaMemcpyDeviceToDevice, c->stream));
+        return PIC_OK;
+    }
+    PIC_NCCL(c, ncclGroupStart());
+    PIC_NCCL(c, ncclSend(c->E4, pl, ncclDouble, down(c), c->comm, c->stream));
+    PIC_NCCL(c, ncclRecv(halo, pl, ncclDouble, up(c), c->comm, c->stream));
+    PIC_NCCL(c, ncclGroupEnd());
+    return PIC_OK;
+}
+
+// rho ghost plane nzl (charge of the next slab's plane 0) folded into its owner.
+pic_status fold_rho_ghost(pic_ctx* c) {
+    const Geom& g = c->g;
+    const int64_t pl = (int64_t)g.n * g.rp;
+    double* ghost = c->rho + pl * g.nzl;
+    if (g.P == 1) {
+        pic::launch_add_plane(c->rho, ghost, pl, c->stream);
+        PIC_LAUNCHED(c, "add_plane");
+        return PIC_OK;
+    }
+    PIC_NCCL(c, ncclGroupStart());
+    PIC_NCCL(c, ncclSend(ghost, (size_t)pl, ncclDouble, up(c), c->comm, c->stream));
+    PIC_NCCL(c, ncclRecv(c->ghost, (size_t)pl, ncclDouble, down(c), c->comm, c->stream));
+    PIC_NCCL(c, ncclGroupEnd());
+    pic::launch_add_plane(c->rho, c->ghost, pl, c->stream);
+    PIC_LAUNCHED(c, "add_plane");
+    return PIC_OK;
+}
+
+// rho (raw CIC sums of the slab, scaled by `scale` in the multiply) -> E4 with its
+// halo plane, energies (summed over ranks) -> ring slot.
 pic_status solve(pic_ctx* c, double scale, int slot) {
     const Geom& g = c->g;
-    double* const S[3] = {c->spec[0], c->spec[1], c->rho};   // E^_x, E^_y, E^_z after the z pass
-    double* const S0[3] = {c->rho, c->rho, c->rho};
+    const size_t unit = (size_t)g.nzl * g.n * g.px;   // complex per slab half spectrum
+    const SpecLayout S0{reinterpret_cast<double2*>(c->rho), 0, 1};
+    const SpecLayout A{c->specA, 1, 1};
+    const SpecLayout D{c->specD, 1, 3};
+    const SpecLayout C{c->specC, 0, 3};
     { StageScope t(c, PIC_STAGE_FFT_X_FWD, 1); pic::launch_fft_x_fwd(g, c->rho, c->tw, c->stream); }
     PIC_LAUNCHED(c, "fft_x_fwd");
-    { StageScope t(c, PIC_STAGE_FFT_Y_FWD, 1); pic::launch_fft_y(g, S0, 1, 0, c->tw, c->stream); }
+    { StageScope t(c, PIC_STAGE_FFT_Y_FWD, 1); pic::launch_fft_y(g, S0, A, 1, 0, c->tw, c->stream); }
     PIC_LAUNCHED(c, "fft_y_fwd");
-    { StageScope t(c, PIC_STAGE_FFT_Z_MUL, 1); pic::launch_fft_z_mul(g, c->rho, c->spec[0], c->spec[1], scale, c->tw, c->stream); }
+    if (g.P > 1) {
+        StageScope t(c, PIC_STAGE_EXCHANGE, 0);
+        PIC_NCCL(c, ncclAlltoAll(c->specA, c->specB, 2 * unit / g.P, ncclDouble, c->comm, c->stream));
+    }
+    { StageScope t(c, PIC_STAGE_FFT_Z_MUL, 1); pic::launch_fft_z_mul(g, c->specB, c->specC, scale, c->tw, c->stream); }
     PIC_LAUNCHED(c, "fft_z_mul");
-    { StageScope t(c, PIC_STAGE_FFT_Y_INV, 1); pic::launch_fft_y(g, S, 3, 1, c->tw, c->stream); }
+    if (g.P > 1) {
+        StageScope t(c, PIC_STAGE_EXCHANGE, 0);
+        PIC_NCCL(c, ncclAlltoAll(c->specC, c->specD, 6 * unit / g.P, ncclDouble, c->comm, c->stream));
+    }
+    { StageScope t(c, PIC_STAGE_FFT_Y_INV, 1); pic::launch_fft_y(g, D, C, 3, 1, c->tw, c->stream); }
     PIC_LAUNCHED(c, "fft_y_inv");
-    { StageScope t(c, PIC_STAGE_FFT_X_INV, 1); pic::launch_fft_x_inv(g, S, c->E4, c->tw, c->partials, c->stream); }
+    { StageScope t(c, PIC_STAGE_FFT_X_INV, 1); pic::launch_fft_x_inv(g, c->specC, c->E4, c->tw, c->partials, c->stream); }
     PIC_LAUNCHED(c, "fft_x_inv");
     { StageScope t(c, PIC_STAGE_ENERGY, 1); pic::launch_energy_reduce(g, c->partials, c->energies + 2 * slot, c->stream); }
     PIC_LAUNCHED(c, "energy");
+    {
+        StageScope t(c, PIC_STAGE_EXCHANGE, 0);
+        if (g.P > 1)
+            PIC_NCCL(c, ncclAllReduce(c->energies + 2 * slot, c->energies + 2 * slot, 2, ncclDouble, ncclSum,
+                                      c->comm, c->stream));
+        PIC_TRY(fill_E_halo(c));
+    }
     c->last_slot = slot;
     return PIC_OK;
 }
 
-// (optionally pushed) particles of buffer cur -> sorted by key into cur^1, rho
-// deposited; cur flips.
+// push=1: the step's push of the sorted state (with migration at P > 1);
+// push=0: the state as is, any order.  The particles of buffer cur end sorted by
+// cell key in cur^1 and their charge is deposited; cur flips.
 pic_status push_sort_deposit(pic_ctx* c, int push) {
     const Geom& g = c->g;
     {
         StageScope t(c, PIC_STAGE_CLEAR, 0);
         PIC_CUDA(c, cudaMemsetAsync(c->count, 0, sizeof(uint32_t) * (size_t)c->ncell, c->stream));
-        PIC_CUDA(c, cudaMemsetAsync(c->rho, 0, sizeof(double2) * (size_t)g.n * g.n * g.px, c->stream));
+        PIC_CUDA(c, cudaMemsetAsync(c->rho, 0, sizeof(double) * (size_t)g.n * g.rp * (g.nzl + 1), c->stream));
+        if (g.P > 1) PIC_CUDA(c, cudaMemsetAsync(c->send_count, 0, sizeof(uint32_t) * g.P, c->stream));
     }
     PState cur = state(c, c->cur), nxt = state(c, c->cur ^ 1);
-    { StageScope t(c, PIC_STAGE_PUSH_KEY, 1); pic::launch_push_key(g, cur, c->np, c->offs, c->E4, push, c->key, c->rank, c->count, c->err_flag, c->stream); }
+    {
+        StageScope t(c, PIC_STAGE_PUSH_KEY, 1);
+        if (push)
+            pic::launch_push_key(g, cur, c->offs, c->E4, c->key, c->rank, c->count, c->send, c->send_count,
+                                 c->seg, c->err_flag, c->stream);
+        else
+            pic::launch_key_import(g, cur, c->np, c->key, c->rank, c->count, c->err_flag, c->stream);
+    }
     PIC_LAUNCHED(c, "push_key");
+    const int64_t n_old = c->np;
+    int64_t narr = 0, nleave = 0;
+    if (push && g.P > 1) {
+        StageScope t(c, PIC_STAGE_EXCHANGE, 0);
+        PIC_NCCL(c, ncclAlltoAll(c->send_count, c->recv_count, 1, ncclUint32, c->comm, c->stream));
+        uint32_t sc[8], rc[8];
+        PIC_CUDA(c, cudaMemcpyAsync(sc, c->send_count, sizeof(uint32_t) * g.P, cudaMemcpyDeviceToHost, c->stream));
+        PIC_CUDA(c, cudaMemcpyAsync(rc, c->recv_count, sizeof(uint32_t) * g.P, cudaMemcpyDeviceToHost, c->stream));
+        PIC_CUDA(c, cudaStreamSynchronize(c->stream));
+        for (int r = 0; r < g.P; ++r) {
+            if (sc[r] > (uint32_t)c->seg) return fail(c, PIC_EOVERFLOW, "migration send segment overflow");
+            nleave += sc[r];
+            narr += rc[r];
+        }
+        if (narr > c->recv_cap) return fail(c, PIC_EOVERFLOW, "migration receive buffer overflow");
+        PIC_NCCL(c, ncclGroupStart());
+        int64_t roff = 0;
+        for (int r = 0; r < g.P; ++r) {
+            if (r == g.rank) continue;
+            if (sc[r])
+                PIC_NCCL(c, ncclSend(c->send + (size_t)4 * c->seg * r, 8 * (size_t)sc[r], ncclDouble, r,
+                                     c->comm, c->stream));
+            if (rc[r])
+                PIC_NCCL(c, ncclRecv(c->recv + 4 * roff, 8 * (size_t)rc[r], ncclDouble, r, c->comm, c->stream));
+            roff += rc[r];
+        }
+        PIC_NCCL(c, ncclGroupEnd());
+        pic::launch_key_arrivals(g, c->recv, narr, n_old, c->key, c->rank, c->count, c->err_flag, c->stream);
+        PIC_LAUNCHED(c, "key_arrivals");
+        c->migrated += nleave;
+    }
+    const int64_t n_new = n_old - nleave + narr;
+    if (n_new > c->np_cap) return fail(c, PIC_EOVERFLOW, "slab holds more particles than its capacity");
     { StageScope t(c, PIC_STAGE_SCAN, 3); pic::launch_scan(c->count, c->offs, c->ncell, c->scan_scratch, c->stream); }
     PIC_LAUNCHED(c, "scan");
-    { StageScope t(c, PIC_STAGE_PLACE, 1); pic::launch_place(c->key, c->rank, c->np, c->offs, c->perm, c->stream); }
+    { StageScope t(c, PIC_STAGE_PLACE, 1); pic::launch_place(c->key, c->rank, n_old + narr, c->offs, c->perm, c->stream); }
     PIC_LAUNCHED(c, "place");
     {
         StageScope t(c, PIC_STAGE_REORDER_DEPOSIT, 1);
-        pic::launch_reorder_deposit(g, c->offs, c->perm, cur, nxt, push, c->rho, c->err_flag, c->stream);
+        pic::launch_reorder_deposit(g, c->offs, c->perm, cur, c->recv, n_old, nxt, push, c->rho, c->err_flag,
+                                    c->stream);
     }
     PIC_LAUNCHED(c, "reorder_deposit");
+    {
+        StageScope t(c, PIC_STAGE_EXCHANGE, 0);
+        PIC_TRY(fold_rho_ghost(c));
+    }
     c->cur ^= 1;
+    c->np = n_new;
     return PIC_OK;
 }
 
 pic_status sync_check(pic_ctx* c) {
     PIC_CUDA(c, cudaStreamSynchronize(c->stream));
-    int flag[2] = {0, 0};
+    int flag[3] = {0, 0, 0};
     PIC_CUDA(c, cudaMemcpy(flag, c->err_flag, sizeof(flag), cudaMemcpyDeviceToHost));
     if (flag[1]) {
         PIC_CUDA(c, cudaMemset(c->err_flag + 1, 0, sizeof(int)));
-        return fail(c, PIC_EINVAL, "imported position outside [0, L); particle state undefined");
+        return fail(c, PIC_EINVAL, "imported position outside [0, L) or outside this rank's slab");
     }
-    if (flag[0]) return fail(c, PIC_EOVERFLOW, "a cell holds more particles than one chunk (4096) or 65535");
+    if (flag[0] || flag[2])
+        return fail(c, PIC_EOVERFLOW, "capacity exceeded: > 2048 particles in one cell or a full migration segment (D#23)");
+    if (c->g.P > 1 && c->comm) {
+        ncclResult_t ar = ncclSuccess;
+        if (ncclCommGetAsyncError(c->comm, &ar) == ncclSuccess && ar != ncclSuccess) {
+            snprintf(c->err, sizeof(c->err), "NCCL async error: %s", ncclGetErrorString(ar));
+            c->poisoned = true;
+            return PIC_ENCCL;
+        }
+    }
     if (c->timing) collect_timings(c);
     return PIC_OK;
 }
 
+// Slab grid [nzl][n][n] host <-> pitched device planes [nzl][n][rp].
 pic_status copy_grid_to_device(pic_ctx* c, double* dst, const double* host) {
     const Geom& g = c->g;
     PIC_CUDA(c, cudaMemcpy2DAsync(dst, sizeof(double) * g.rp, host, sizeof(double) * g.n,
-                                  sizeof(double) * g.n, (size_t)g.n * g.n, cudaMemcpyHostToDevice,
+                                  sizeof(double) * g.n, (size_t)g.n * g.nzl, cudaMemcpyHostToDevice,
                                   c->stream));
     return PIC_OK;
 }
@@ -295,22 +512,14 @@ pic_status copy_grid_to_device(pic_ctx* c, double* dst, const double* host) {
 pic_status copy_grid_to_host(pic_ctx* c, double* host, const double* src) {
     const Geom& g = c->g;
     PIC_CUDA(c, cudaMemcpy2DAsync(host, sizeof(double) * g.n, src, sizeof(double) * g.rp,
-                                  sizeof(double) * g.n, (size_t)g.n * g.n, cudaMemcpyDeviceToHost,
+                                  sizeof(double) * g.n, (size_t)g.n * g.nzl, cudaMemcpyDeviceToHost,
                                   c->stream));
     return PIC_OK;
 }
 
-#define PIC_TRY(expr)                       \
-    do {                                    \
-        pic_status s_ = (expr);             \
-        if (s_ != PIC_OK) return s_;        \
-    } while (0)
-
-#define PIC_CHECK_CTX(c)                                 \
-    do {                                                 \
-        if (!(c)) return PIC_EINVAL;                     \
-        if ((c)->poisoned) return PIC_EPOISONED;         \
-    } while (0)
+double solve_scale(const pic_ctx* c) {
+    return c->deposit_scale / ((double)c->g.n * c->g.n * c->g.n);   // 1/N^3 of the whole box
+}
 
 }  // namespace
 
@@ -333,28 +542,52 @@ pic_status pic_params_default(pic_params* p) {
     return PIC_OK;
 }
 
+pic_status pic_nccl_unique_id(uint8_t* id) {
+    if (!id) return PIC_EINVAL;
+    ncclUniqueId u;
+    if (ncclGetUniqueId(&u) != ncclSuccess) return PIC_ENCCL;
+    static_assert(sizeof(u) <= 128, "ncclUniqueId larger than 128 bytes");
+    std::memset(id, 0, 128);
+    std::memcpy(id, &u, sizeof(u));
+    return PIC_OK;
+}
+
 pic_status pic_workspace_bytes(const pic_params* p, int32_t rank, int32_t nranks, size_t* bytes) {
     char msg[256];
     pic_status st = validate(p, rank, nranks, msg, sizeof(msg));
     if (st != PIC_OK) { snprintf(g_init_error, sizeof(g_init_error), "%s", msg); return st; }
     if (!bytes) return PIC_EINVAL;
-    const Geom g = make_geom(p);
-    const int64_t np = (int64_t)p->ppc * p->n * p->n * p->n;
-    *bytes = carve(nullptr, g, np, nullptr);
+    const Geom g = make_geom(p, rank, nranks);
+    *bytes = carve(nullptr, g, sizes(p, g), nullptr);
+    return PIC_OK;
+}
+
+pic_status pic_slab(const pic_params* p, int32_t rank, int32_t nranks, int32_t* z0, int32_t* nz,
+                    int64_t* capacity) {
+    char msg[256];
+    pic_status st = validate(p, rank, nranks, msg, sizeof(msg));
+    if (st != PIC_OK) { snprintf(g_init_error, sizeof(g_init_error), "%s", msg); return st; }
+    const Geom g = make_geom(p, rank, nranks);
+    if (z0) *z0 = g.z0;
+    if (nz) *nz = g.nzl;
+    if (capacity) *capacity = sizes(p, g).np_cap;
     return PIC_OK;
 }
 
 pic_status pic_init(const pic_params* p, int32_t rank, int32_t nranks, const uint8_t* nccl_id,
                     void* workspace, size_t workspace_bytes, void* cuda_stream, pic_ctx** out) {
-    (void)nccl_id;
     if (!out) return PIC_EINVAL;
     *out = nullptr;
     char msg[256];
     pic_status st = validate(p, rank, nranks, msg, sizeof(msg));
     if (st != PIC_OK) { snprintf(g_init_error, sizeof(g_init_error), "%s", msg); return st; }
-    const Geom g = make_geom(p);
-    const int64_t np = (int64_t)p->ppc * p->n * p->n * p->n;
-    const size_t need = carve(nullptr, g, np, nullptr);
+    if (nranks > 1 && !nccl_id) {
+        snprintf(g_init_error, sizeof(g_init_error), "nccl_id required for nranks > 1");
+        return PIC_EINVAL;
+    }
+    const Geom g = make_geom(p, rank, nranks);
+    const Sizes z = sizes(p, g);
+    const size_t need = carve(nullptr, g, z, nullptr);
     if (!workspace || workspace_bytes < need) {
         snprintf(g_init_error, sizeof(g_init_error), "workspace %zu B < %zu B needed", workspace_bytes, need);
         return PIC_ENOMEM;
@@ -363,23 +596,33 @@ pic_status pic_init(const pic_params* p, int32_t rank, int32_t nranks, const uin
     if (!c) return PIC_ENOMEM;
     c->p = *p;
     c->g = g;
-    c->np = np;
-    c->ncell = (int64_t)g.n * g.n * g.n;
-    c->q = -((g.L * g.L) * g.L) / (double)np;
+    c->np_glob = (int64_t)p->ppc * p->n * p->n * p->n;
+    c->ncell = (int64_t)g.n * g.n * g.nzl;
+    c->q = -((g.L * g.L) * g.L) / (double)c->np_glob;
     c->deposit_scale = c->q * ((g.inv_h * g.inv_h) * g.inv_h);
     c->stream = reinterpret_cast<cudaStream_t>(cuda_stream);
-    carve(c, g, np, reinterpret_cast<char*>(workspace));
+    carve(c, g, z, reinterpret_cast<char*>(workspace));
 
     static bool smem_set = false;
     if (!smem_set) { pic::fft_set_smem_limits(); pic::particles_set_smem_limits(); smem_set = true; }
 
     auto bail = [&](pic_status s) {
         snprintf(g_init_error, sizeof(g_init_error), "%s", c->err);
+        if (c->comm) ncclCommDestroy(c->comm);
         delete c;
         return s;
     };
-    // twiddles W_n^m = exp(-2 pi i m / n), m < n/2
-    std::vector<double2> tw(g.n);   // W_n^m = exp(-2 pi i m / n), m < n
+    if (nranks > 1) {
+        ncclUniqueId u;
+        std::memcpy(&u, nccl_id, sizeof(u));
+        ncclResult_t r = ncclCommInitRank(&c->comm, nranks, u, rank);
+        if (r != ncclSuccess) {
+            snprintf(c->err, sizeof(c->err), "ncclCommInitRank: %s", ncclGetErrorString(r));
+            return bail(PIC_ENCCL);
+        }
+    }
+    // twiddles W_n^m = exp(-2 pi i m / n), m < n
+    std::vector<double2> tw(g.n);
     for (int m = 0; m < g.n; ++m) {
         const double ang = 2.0 * M_PI * (double)m / (double)g.n;
         tw[m] = make_double2(std::cos(ang), -std::sin(ang));
@@ -388,14 +631,30 @@ pic_status pic_init(const pic_params* p, int32_t rank, int32_t nranks, const uin
     if (e == cudaSuccess) e = cudaMemsetAsync(c->err_flag, 0, sizeof(int) * 4, c->stream);
     if (e != cudaSuccess) return bail(fail(c, PIC_ECUDA, "init copies", e));
 
-    pic::launch_sample(g, state(c, 0), np, p->k, p->alpha, p->seed, c->stream);
+    if (g.P == 1) {
+        c->np = c->np_glob;
+        pic::launch_sample(g, state(c, 0), c->np, p->k, p->alpha, p->seed, c->stream);
+    } else {
+        // every rank samples the z coordinate of every global index j and keeps its own,
+        // in ascending j (the oracle's initial order restricted to the slab)
+        const int64_t nblk = pic::sample_blocks(c->np_glob);
+        pic::launch_sample_count(g, c->np_glob, p->k, p->alpha, p->seed, c->key, c->stream);
+        pic::launch_scan(c->key, c->perm, nblk, c->scan_scratch, c->stream);
+        uint32_t total = 0;
+        e = cudaMemcpyAsync(&total, c->perm + nblk, sizeof(uint32_t), cudaMemcpyDeviceToHost, c->stream);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
+        if (e != cudaSuccess) return bail(fail(c, PIC_ECUDA, "sample count", e));
+        if ((int64_t)total > c->np_cap) return bail(fail(c, PIC_EOVERFLOW, "slab capacity exceeded at init"));
+        c->np = total;
+        pic::launch_sample_write(g, state(c, 0), c->np_glob, p->k, p->alpha, p->seed, c->perm, c->stream);
+    }
     e = cudaGetLastError();
     if (e != cudaSuccess) return bail(fail(c, PIC_ECUDA, "sample", e));
     c->cur = 0;
     if ((st = push_sort_deposit(c, 0)) != PIC_OK) return bail(st);
     if (p->half_kick) {
-        if ((st = solve(c, c->deposit_scale / (double)c->ncell, 0)) != PIC_OK) return bail(st);
-        pic::launch_half_kick(g, state(c, c->cur), np, c->E4, c->stream);
+        if ((st = solve(c, solve_scale(c), 0)) != PIC_OK) return bail(st);
+        pic::launch_half_kick(g, state(c, c->cur), c->np, c->E4, c->stream);
         e = cudaGetLastError();
         if (e != cudaSuccess) return bail(fail(c, PIC_ECUDA, "half_kick", e));
         c->last_slot = -1;
@@ -403,6 +662,7 @@ pic_status pic_init(const pic_params* p, int32_t rank, int32_t nranks, const uin
         if ((st = push_sort_deposit(c, 0)) != PIC_OK) return bail(st);
     }
     if ((st = sync_check(c)) != PIC_OK) return bail(st);
+    c->migrated = 0;
     *out = c;
     return PIC_OK;
 }
@@ -410,7 +670,7 @@ pic_status pic_init(const pic_params* p, int32_t rank, int32_t nranks, const uin
 pic_status pic_step(pic_ctx* c, int32_t nsteps, double* ex_energy) {
     PIC_CHECK_CTX(c);
     if (nsteps < 0) return PIC_EINVAL;
-    const double scale = c->deposit_scale / (double)c->ncell;
+    const double scale = solve_scale(c);
     int32_t done = 0;
     while (done < nsteps) {
         const int chunk = std::min(nsteps - done, kMaxEnergySteps);
@@ -447,6 +707,7 @@ void pic_free(pic_ctx* c) {
     if (!c) return;
     if (c->stream) cudaStreamSynchronize(c->stream);
     for (cudaEvent_t e : c->ev_pool) cudaEventDestroy(e);
+    if (c->comm) ncclCommDestroy(c->comm);
     delete c;
 }
 
@@ -455,6 +716,12 @@ const char* pic_last_error(const pic_ctx* c) { return c ? c->err : g_init_error;
 pic_status pic_num_particles(pic_ctx* c, int64_t* np) {
     if (!c || !np) return PIC_EINVAL;
     *np = c->np;
+    return PIC_OK;
+}
+
+pic_status pic_migrated(pic_ctx* c, int64_t* migrated) {
+    if (!c || !migrated) return PIC_EINVAL;
+    *migrated = c->migrated;
     return PIC_OK;
 }
 
@@ -471,11 +738,12 @@ pic_status pic_get_particles(pic_ctx* c, double* xyzuvw, int64_t np) {
 
 pic_status pic_set_particles(pic_ctx* c, const double* xyzuvw, int64_t np) {
     PIC_CHECK_CTX(c);
-    if (!xyzuvw || np != c->np) return PIC_EINVAL;
+    if (!xyzuvw || np < 0 || np > c->np_cap || (c->g.P == 1 && np != c->np_glob)) return PIC_EINVAL;
     double* soa = reinterpret_cast<double*>(c->part[c->cur ^ 1][0]);
     PIC_CUDA(c, cudaMemcpyAsync(soa, xyzuvw, sizeof(double) * 6 * (size_t)np, cudaMemcpyHostToDevice, c->stream));
     pic::launch_soa_to_pairs(soa, np, state(c, c->cur), c->stream);
     PIC_LAUNCHED(c, "soa_to_pairs");
+    c->np = np;
     PIC_TRY(push_sort_deposit(c, 0));
     c->last_slot = -1;
     return sync_check(c);
@@ -487,9 +755,10 @@ pic_status pic_get_grid(pic_ctx* c, int32_t which, double* host) {
     if (which == 0) {
         PIC_TRY(copy_grid_to_host(c, host, c->rho));
     } else {
-        pic::launch_e4_extract(c->g, c->E4, which - 1, c->spec[0], c->stream);   // S1 as scratch
+        double* scratch = reinterpret_cast<double*>(c->specC);
+        pic::launch_e4_extract(c->g, c->E4, which - 1, scratch, c->stream);
         PIC_LAUNCHED(c, "e4_extract");
-        PIC_CUDA(c, cudaMemcpyAsync(host, c->spec[0], sizeof(double) * (size_t)c->ncell,
+        PIC_CUDA(c, cudaMemcpyAsync(host, scratch, sizeof(double) * (size_t)c->ncell,
                                     cudaMemcpyDeviceToHost, c->stream));
     }
     PIC_TRY(sync_check(c));
@@ -503,16 +772,18 @@ pic_status pic_solve_injected(pic_ctx* c, const double* rho_host, double* E_host
     PIC_CHECK_CTX(c);
     if (!rho_host) return PIC_EINVAL;
     PIC_TRY(copy_grid_to_device(c, c->rho, rho_host));
-    PIC_TRY(solve(c, 1.0 / (double)c->ncell, 0));
+    PIC_TRY(solve(c, 1.0 / ((double)c->g.n * c->g.n * c->g.n), 0));
     double en[2];
     PIC_CUDA(c, cudaMemcpyAsync(en, c->energies, sizeof(en), cudaMemcpyDeviceToHost, c->stream));
-    if (E_host)
+    if (E_host) {
+        double* scratch = reinterpret_cast<double*>(c->specC);
         for (int d = 0; d < 3; ++d) {
-            pic::launch_e4_extract(c->g, c->E4, d, c->spec[0], c->stream);
+            pic::launch_e4_extract(c->g, c->E4, d, scratch, c->stream);
             PIC_LAUNCHED(c, "e4_extract");
-            PIC_CUDA(c, cudaMemcpyAsync(E_host + (size_t)d * c->ncell, c->spec[0], sizeof(double) * (size_t)c->ncell,
+            PIC_CUDA(c, cudaMemcpyAsync(E_host + (size_t)d * c->ncell, scratch, sizeof(double) * (size_t)c->ncell,
                                         cudaMemcpyDeviceToHost, c->stream));
         }
+    }
     PIC_TRY(sync_check(c));
     if (ex_energy) *ex_energy = en[0];
     if (total_energy) *total_energy = en[1];
@@ -525,12 +796,14 @@ pic_status pic_solve_injected(pic_ctx* c, const double* rho_host, double* E_host
 pic_status pic_push_injected(pic_ctx* c, const double* E_host) {
     PIC_CHECK_CTX(c);
     if (!E_host) return PIC_EINVAL;
-    double* const comp[3] = {c->spec[0], c->spec[1], c->rho};   // scratch: compact [n^3] each
+    double* sc = reinterpret_cast<double*>(c->specC);   // scratch: 3 compact slab components
+    double* const comp[3] = {sc, sc + c->ncell, sc + 2 * c->ncell};
     for (int d = 0; d < 3; ++d)
         PIC_CUDA(c, cudaMemcpyAsync(comp[d], E_host + (size_t)d * c->ncell, sizeof(double) * (size_t)c->ncell,
                                     cudaMemcpyHostToDevice, c->stream));
     pic::launch_e4_pack(c->g, comp, c->E4, c->stream);
     PIC_LAUNCHED(c, "e4_pack");
+    PIC_TRY(fill_E_halo(c));
     PIC_TRY(push_sort_deposit(c, 1));
     c->last_slot = -1;
     return sync_check(c);
@@ -545,8 +818,8 @@ pic_status pic_get_keys_perm(pic_ctx* c, uint32_t* keys, uint32_t* perm) {
     }
     PIC_TRY(sync_check(c));
     if (keys) {
-        pic::launch_keys_only(c->g, state(c, c->cur), c->np, c->key, c->stream);
-        PIC_LAUNCHED(c, "keys_only");
+        pic::launch_gkeys(c->g, state(c, c->cur), c->np, c->key, c->stream);
+        PIC_LAUNCHED(c, "gkeys");
         PIC_CUDA(c, cudaMemcpyAsync(keys, c->key, sizeof(uint32_t) * (size_t)c->np, cudaMemcpyDeviceToHost, c->stream));
         PIC_TRY(sync_check(c));
     }
@@ -583,7 +856,8 @@ const char* pic_stage_name(int32_t stage) {
 
 pic_status pic_launches_per_step(pic_ctx* c, int64_t* launches) {
     if (!c || !launches) return PIC_EINVAL;
-    *launches = 6 /* solve */ + 1 /* push_key */ + 3 /* scan */ + 1 /* place */ + 1 /* reorder_deposit */;
+    *launches = 6 /* solve */ + 1 /* push_key */ + 3 /* scan */ + 1 /* place */ + 1 /* reorder_deposit */ +
+                1 /* ghost fold */ + (c->g.P > 1 ? 1 : 0) /* arrivals */;
     return PIC_OK;
 }
 

@@ -20,11 +20,15 @@ struct Geom {
     double inv_h;   // (double)n / L  (D#5)
     double dt;      // time step
     double qm_dt;   // (q/m) dt = -dt
+    // z-slab decomposition over P ranks (P = 1: the whole box): this rank owns the
+    // cell/node planes z0 .. z0 + nzl - 1, nzl = n / P = 2^mz.  Local grids carry
+    // one extra plane (nzl): the ghost of the charge, the halo of the field.
+    int P, rank, z0, nzl, mz;
 };
 
-// Index of node (ix, iy, iz) in a pitched real grid [n][n][rp].
-__device__ __forceinline__ int64_t gidx(const Geom& g, int ix, int iy, int iz) {
-    return ((int64_t)iz * g.n + iy) * g.rp + ix;
+// Index of node (ix, iy, slab plane izl) in a pitched real grid [nzl + 1][n][rp].
+__device__ __forceinline__ int64_t gidx(const Geom& g, int ix, int iy, int izl) {
+    return ((int64_t)izl * g.n + iy) * g.rp + ix;
 }
 
 // Cell index along one dimension: floor(x * inv_h), clamped to [0, n-1] (D#5).
@@ -71,11 +75,53 @@ __device__ __forceinline__ double wrap(double x, double L) {
     return x;
 }
 
-__device__ __forceinline__ uint32_t key_of(const Geom& g, const double x[3]) {
+// Global Morton key of the cell of x (the sort key of the paper-level order, D#14).
+__device__ __forceinline__ uint32_t gkey_of(const Geom& g, const double x[3]) {
     int i0 = cell_of(__dmul_rn(x[0], g.inv_h), g.n);
     int i1 = cell_of(__dmul_rn(x[1], g.inv_h), g.n);
     int i2 = cell_of(__dmul_rn(x[2], g.inv_h), g.n);
     return morton(i0, i1, i2);
+}
+
+// Rank-local key of cell (ix, iy, izl) of the slab: the global Morton key with the
+// slab's constant z bits (>= mz) removed -- low 3 mz bits interleave (x, y, izl),
+// the rest interleave the high bits of (x, y).  Dense on [0, n^2 nzl) and monotone
+// with the global key on the slab, so the rank's sorted array is the global sorted
+// array restricted to the slab.  P = 1: the global Morton key.
+__device__ __forceinline__ uint32_t spread2(uint32_t v) {
+    v &= 0x3ffu;
+    v = (v | (v << 8)) & 0x00FF00FFu;
+    v = (v | (v << 4)) & 0x0F0F0F0Fu;
+    v = (v | (v << 2)) & 0x33333333u;
+    v = (v | (v << 1)) & 0x55555555u;
+    return v;
+}
+__device__ __forceinline__ uint32_t compact2(uint32_t v) {
+    v &= 0x55555555u;
+    v = (v ^ (v >> 1)) & 0x33333333u;
+    v = (v ^ (v >> 2)) & 0x0F0F0F0Fu;
+    v = (v ^ (v >> 4)) & 0x00FF00FFu;
+    v = (v ^ (v >> 8)) & 0x0000FFFFu;
+    return v;
+}
+__device__ __forceinline__ uint32_t lkey(const Geom& g, int ix, int iy, int izl) {
+    const uint32_t m = (1u << g.mz) - 1u;
+    return morton(ix & m, iy & m, izl) | ((spread2(ix >> g.mz) | (spread2(iy >> g.mz) << 1)) << (3 * g.mz));
+}
+__device__ __forceinline__ void unlkey(const Geom& g, uint32_t k, int& ix, int& iy, int& izl) {
+    const uint32_t lo = k & ((1u << (3 * g.mz)) - 1u), hi = k >> (3 * g.mz);
+    ix = (int)(compact3(lo) | (compact2(hi) << g.mz));
+    iy = (int)(compact3(lo >> 1) | (compact2(hi >> 1) << g.mz));
+    izl = (int)compact3(lo >> 2);
+}
+
+// Local key of the cell of x on this rank; *izg = its global z plane.
+__device__ __forceinline__ uint32_t key_of(const Geom& g, const double x[3], int* izg = nullptr) {
+    int i0 = cell_of(__dmul_rn(x[0], g.inv_h), g.n);
+    int i1 = cell_of(__dmul_rn(x[1], g.inv_h), g.n);
+    int i2 = cell_of(__dmul_rn(x[2], g.inv_h), g.n);
+    if (izg) *izg = i2;
+    return lkey(g, i0, i1, i2 - g.z0);
 }
 
 // CIC weights of one position: cell index i[d] and w[d][0] = 1 - f, w[d][1] = f,
@@ -104,7 +150,8 @@ __device__ __forceinline__ void ldg_node(const double* __restrict__ p, double& e
 }
 
 // CIC gather of E at x (corner order z outer, y, x inner; fma accumulation
-// from 0: S:141-149, D#17).  E4 = node records (E_x, E_y, E_z, 0).
+// from 0: S:141-149, D#17).  E4 = the slab's node records (E_x, E_y, E_z, 0),
+// planes 0 .. nzl (the last one the halo copy of the next slab's plane 0).
 __device__ __forceinline__ void gather_E(const Geom& g, const double* __restrict__ E4,
                                          const double x[3], double ep[3]) {
     int i[3];
@@ -115,7 +162,7 @@ __device__ __forceinline__ void gather_E(const Geom& g, const double* __restrict
     for (int c = 0; c < 2; ++c) {
 #pragma unroll
         for (int b = 0; b < 2; ++b) {
-            const int64_t row = ((int64_t)((i[2] + c) & g.nmask) * g.n + ((i[1] + b) & g.nmask)) * g.n;
+            const int64_t row = ((int64_t)(i[2] - g.z0 + c) * g.n + ((i[1] + b) & g.nmask)) * g.n;
 #pragma unroll
             for (int a = 0; a < 2; ++a) {
                 const double wt = __dmul_rn(__dmul_rn(w[0][a], w[1][b]), w[2][c]);

@@ -1,7 +1,10 @@
 """Compile libpic's sources with -Xptxas -v and print registers/spills/smem per kernel."""
+import sys; sys.path.insert(0, ".")
 import glob, re, subprocess, sys
 srcs = sorted(glob.glob("paper_2605_05469_b200/csrc/*.cu"))
-out = subprocess.run(["nvcc", "-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-std=c++17", "-Xcompiler",
+import paper_2605_05469_b200._build as B
+inc, _ = B.nccl_dirs()
+out = subprocess.run(["nvcc", "-I" + inc, "-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-std=c++17", "-Xcompiler",
                       "-fPIC", "-shared", "-cudart", "static", "-Xptxas", "-v", "-o", "/tmp/ptxas_probe.so", *srcs],
                      capture_output=True, text=True).stderr
 name = None

@@ -45,11 +45,29 @@ def test_invalid_parameters_rejected(bad):
     assert e.value.status == B.PIC_EINVAL
 
 
-def test_multi_rank_request_is_reported():
-    p = B.default_params()
+def test_multi_rank_geometry():
+    """z-slabs: rank r owns planes [r N/P, (r+1) N/P); pgrid must be
+    {1, P}; P in {1, 2, 4, 8}; slabs need >= 4 planes; pencils are not built."""
+    for P in (1, 2, 4, 8):
+        p = B.default_params(n=64, pgrid=(1, P))
+        zs = [B.slab(p, r, P) for r in range(P)]
+        assert [z[0] for z in zs] == [r * 64 // P for r in range(P)]
+        assert all(z[1] == 64 // P for z in zs)
+        cap = zs[0][2]
+        assert cap >= 8 * 64 ** 3 // P
+        assert B.workspace_bytes(p, 0, P) > 48 * cap
     with pytest.raises(B.PicError) as e:
-        B.workspace_bytes(p, rank=0, nranks=2)
-    assert e.value.status in (B.PIC_EUNSUPPORTED, B.PIC_EINVAL)
+        B.workspace_bytes(B.default_params(n=64, pgrid=(1, 1)), rank=0, nranks=2)
+    assert e.value.status == B.PIC_EINVAL
+    with pytest.raises(B.PicError) as e:
+        B.workspace_bytes(B.default_params(n=64, pgrid=(2, 2)), rank=0, nranks=4)
+    assert e.value.status == B.PIC_EUNSUPPORTED
+    with pytest.raises(B.PicError) as e:
+        B.workspace_bytes(B.default_params(n=16, pgrid=(1, 8)), rank=0, nranks=8)
+    assert e.value.status == B.PIC_EINVAL
+    with pytest.raises(B.PicError) as e:
+        B.workspace_bytes(B.default_params(n=64, pgrid=(1, 3)), rank=0, nranks=3)
+    assert e.value.status == B.PIC_EINVAL
 
 
 def test_workspace_bytes_model():
