@@ -10,8 +10,9 @@ One "step" = one full PIC step: FFT solve + field energy, gather+push, counting
 sort by cell key, reorder + CIC deposit.  Inputs live in HBM (51.5 GB of
 particle state >> 126 MB L2, so no L2 flush is needed between steps).
 
-Prints ONE JSON line on rank 0.  For N > 1 (torchrun) every rank runs its own
-independent replica (domain decomposition is not in this build).
+Prints ONE JSON line on rank 0.  For N > 1 (torchrun) the same 512^3 problem is
+decomposed in z-slabs over the N GPUs (NCCL all-to-all FFT transposes, halo/ghost
+planes, particle migration): strong scaling of a fixed problem, time = max over ranks.
 """
 from __future__ import annotations
 
@@ -48,6 +49,43 @@ ALG_BYTES = {
 
 def log(*a):
     print(*a, file=sys.stderr, flush=True)
+
+
+def reduce_max(x: float, world: int) -> float:
+    """Max over ranks (device time is taken per rank; the job time is the slowest)."""
+    if world <= 1:
+        return x
+    import torch
+    import torch.distributed as dist
+
+    dev = "cuda" if dist.get_backend() == "nccl" else "cpu"
+    t = torch.tensor([float(x)], dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def reduce_sum(x: float, world: int) -> float:
+    if world <= 1:
+        return x
+    import torch
+    import torch.distributed as dist
+
+    dev = "cuda" if dist.get_backend() == "nccl" else "cpu"
+    t = torch.tensor([float(x)], dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.SUM)
+    return float(t.item())
+
+
+def broadcast_nccl_id(rank: int, world: int):
+    """One NCCL unique id for the library's communicator (rank 0 makes it)."""
+    if world <= 1:
+        return None
+    import torch.distributed as dist
+    from paper_2605_05469_b200 import nccl_unique_id
+
+    obj = [nccl_unique_id() if rank == 0 else None]
+    dist.broadcast_object_list(obj, src=0)
+    return obj[0]
 
 
 # ------------------------------------------------------------------ clocks --
@@ -178,17 +216,21 @@ def run_ours(args, rank, world):
     import torch
     import torch.distributed as dist
 
+    import numpy as np
+
     local = int(os.environ.get("LOCAL_RANK", 0))
     torch.cuda.set_device(local)
     from paper_2605_05469_b200 import Simulation, STAGES
 
     n, ppc = args.n, args.ppc
-    np_ = ppc * n ** 3
+    np_ = ppc * n ** 3                      # particles of the whole job
     t_init = time.perf_counter()
-    sim = Simulation(n=n, ppc=ppc, k=0.5, alpha=0.05, dt=0.05, seed=1 + rank, device=f"cuda:{local}")
+    ncid = broadcast_nccl_id(rank, world)
+    sim = Simulation(n=n, ppc=ppc, k=0.5, alpha=0.05, dt=0.05, seed=1, device=f"cuda:{local}",
+                     rank=rank, nranks=world, nccl_id=ncid)
     torch.cuda.synchronize()
-    log(f"[rank {rank}] init {n}^3 x {ppc}: {time.perf_counter() - t_init:.1f} s, "
-        f"workspace {sim.workspace.numel() / 2**30:.1f} GiB")
+    log(f"[rank {rank}] init {n}^3 x {ppc} (slab z0={sim.z0} nz={sim.nz}, {sim.np} particles): "
+        f"{time.perf_counter() - t_init:.1f} s, workspace {sim.workspace.numel() / 2**30:.1f} GiB")
     stream = sim.stream
 
     def barrier():
@@ -213,17 +255,15 @@ def run_ours(args, rank, world):
     ms = ev0.elapsed_time(ev1)
     stages = sim.timings()
     sim.set_timing(False)
-    if world > 1:
-        t = torch.tensor([ms], device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
+    migrated = reduce_sum(sim.migrated(), world)
+    ms = reduce_max(ms, world)
     ms_step = ms / args.steps
-    value = world * np_ * args.steps / (ms / 1e3)
+    value = np_ * args.steps / (ms / 1e3)
 
     # ---- end to end through the C ABI with host buffers ----------------------
     e2e = None
     if not args.no_e2e:
-        host = torch.empty((6, np_), dtype=torch.float64, pin_memory=True)
+        host = torch.empty((6, sim.np), dtype=torch.float64, pin_memory=True)
         hv = host.numpy()
         sim.get_particles(out=hv)
         barrier()
@@ -231,46 +271,44 @@ def run_ours(args, rank, world):
         t0 = time.perf_counter()
         sim.set_particles(hv)                 # H2D of the state (+ sort + deposit)
         e2e_ex = sim.step(args.steps)        # per-step energies D2H
-        sim.get_particles(out=hv)             # D2H of the final state
+        hv = np.empty((6, sim.np))          # the state after K steps (size changes with migration)
+        sim.get_particles(out=hv)
         torch.cuda.synchronize()
-        t_e2e = time.perf_counter() - t0
-        if world > 1:
-            t = torch.tensor([t_e2e], device="cuda")
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            t_e2e = float(t.item())
-        state_bytes = 48 * np_
-        e2e = {"value": world * np_ * args.steps / t_e2e, "unit": UNIT,
+        t_e2e = reduce_max(time.perf_counter() - t0, world)
+        state_bytes = 48 * np_ / world       # per rank
+        e2e = {"value": np_ * args.steps / t_e2e, "unit": UNIT,
                "h2d_bytes_per_step": state_bytes / args.steps,
                "d2h_bytes_per_step": (state_bytes + 8 * args.steps) / args.steps,
                "what": "pic_set_particles(host pinned state) + pic_step(K) with per-step W_x to host "
-                       "+ pic_get_particles(host); wall clock, max over ranks"}
+                       "+ pic_get_particles(host); wall clock, max over ranks; bytes per rank"}
         del host
 
     if rank != 0:
         sim.close()
         return 0
 
-    # ---- roofline of the dominant kernel --------------------------------------
-    ncell = n ** 3
+    # ---- roofline of the dominant kernel (rank 0's launches: its slab, its particles)
+    ncell = n * n * (n // world)
+    np_r = sim.np
     per_stage = {}
     for name in STAGES:
         tot, nl = stages[name]
-        if nl == 0 and name != "clear":
+        if nl == 0 and name not in ("clear", "exchange"):
             continue
         bp, bn = ALG_BYTES.get(name, (0, 0))
-        alg = bp * np_ + bn * ncell
+        alg = bp * np_r + bn * ncell
         per_stage[name] = {"ms_per_step": tot / args.steps, "launches": nl,
                            "alg_GBps": (alg * args.steps / (tot / 1e3) / 1e9) if tot > 0 else None}
-    dom = max((s for s in per_stage if s != "clear"), key=lambda s: per_stage[s]["ms_per_step"])
+    dom = max((s for s in per_stage if s not in ("clear", "exchange")), key=lambda s: per_stage[s]["ms_per_step"])
     tot, nl = stages[dom]
     bp, bn = ALG_BYTES[dom]
     # per-launch algorithmic bytes / per-launch duration (scan = 3 launches -> per stage call)
     calls = args.steps
-    alg_per_call = bp * np_ + bn * ncell
+    alg_per_call = bp * np_r + bn * ncell
     achieved = alg_per_call / (tot / calls / 1e3) / 1e9
     peaks = measured_peaks()
     peak = peaks.get("hbm_gbs") or 6650.0
-    cfg_name = f"landau3d_{n}^3x{ppc}ppc_fft"
+    cfg_name = f"landau3d_{n}^3x{ppc}ppc_fft" + (f"_{world}gpu" if world > 1 else "")
     traffic = ncu_traffic(cfg_name, dom)
     roof = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
             "frac": achieved / peak, "traffic": traffic,
@@ -283,16 +321,21 @@ def run_ours(args, rank, world):
     launches = sim.launches_per_step() * args.steps
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+        "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
+        "scaling": "strong" if world > 1 else "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": cfg_name, "grid": n, "ppc": ppc, "particles_per_rank": np_,
+        "config": {"workload": cfg_name, "grid": n, "ppc": ppc, "particles": np_,
                    "k": 0.5, "alpha": 0.05, "dt": 0.05,
-                   "parallelism": "1 GPU" if world == 1 else f"{world} independent replicas",
-                   "l2": "inputs larger than L2 (particle state 48 B x N_p per rank)"},
+                   "parallelism": "1 GPU" if world == 1 else
+                   f"z-slab decomposition over {world} GPUs (NCCL all-to-all FFT transposes, "
+                   f"halo/ghost send/recv, particle migration)",
+                   "migrated_per_step": migrated / args.steps,
+                   "l2": "inputs larger than L2 (particle state 48 B x N_p / N per rank)"},
         "roofline": roof,
         "cpu_baseline": cpu,
         "e2e": e2e,
         "gpu_launches": launches,
+        "gpu_launches_note": "kernels per rank in the timed region (NCCL calls not counted)",
         "clocks": clk.summary(),
         "stages": per_stage,
         "w_x_first_last": [float(ex[0]), float(ex[-1])],

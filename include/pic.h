@@ -124,7 +124,8 @@ pic_status pic_get_particles(pic_ctx *ctx, double *xyzuvw, int64_t np);
 
 /* Replace the particle state from host xyzuvw[6][np] (P = 1: np = N_p; P > 1: this
  * rank's particles, every one inside its slab, np <= its capacity; every coordinate
- * in [0, L), else PIC_EINVAL).  Collective at P > 1.  The state is interpreted as (x_n, v_{n-1/2})
+ * in [0, L), else PIC_EINVAL and the offending coordinates are replaced by valid
+ * ones inside the slab).  Collective at P > 1.  The state is interpreted as (x_n, v_{n-1/2})
  * (no half kick); it is sorted by cell key (stable: ties keep the given order) and
  * deposited.  With stream-ordered host copies; synchronous. */
 pic_status pic_set_particles(pic_ctx *ctx, const double *xyzuvw, int64_t np);

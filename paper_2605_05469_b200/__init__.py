@@ -11,6 +11,7 @@ from ._binding import (  # noqa: F401
     lib,
     nccl_unique_id,
     slab,
+    slab_select,
     workspace_bytes,
 )
 from ._build import build_lib  # noqa: F401

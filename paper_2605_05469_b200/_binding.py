@@ -132,6 +132,14 @@ def nccl_unique_id() -> bytes:
     return bytes(buf)
 
 
+def slab_select(xv: np.ndarray, n: int, L: float, rank: int, nranks: int) -> np.ndarray:
+    """The particles of a global state xv[6][np] that rank owns (cell plane in its
+    z-slab), in their global order -- what each rank passes to set_particles."""
+    nz = n // nranks
+    iz = np.minimum(np.floor(xv[2] * (n / L)).astype(np.int64), n - 1)
+    return np.ascontiguousarray(xv[:, (iz >= rank * nz) & (iz < (rank + 1) * nz)])
+
+
 def slab(p: pic_params, rank: int, nranks: int):
     """(z0, nz, capacity) of a rank's z-slab."""
     z0, nz, cap = C.c_int32(), C.c_int32(), C.c_int64()

@@ -29,8 +29,6 @@ namespace {
 
 constexpr int kThreads = 256;
 constexpr int kBrick = 256;     // cells per brick (Morton 8 bits: 8 x 8 x 4)
-constexpr int kCapA = 2048;     // particles per staged chunk of the P = 1 reorder (96 KB)
-constexpr int kCapG = 1024;     // particles per staged chunk of the P > 1 reorder
 constexpr uint32_t kNoKey = 0xffffffffu;
 
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
@@ -186,13 +184,22 @@ __global__ void __launch_bounds__(kThreads) k_key_import(Geom g, PState cur, int
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < np; i += stride) {
         double x[3], v[3];
         load_particle(cur, i, x, v);
+        // an invalid position is reported (err[1]) and replaced by a valid one inside
+        // the slab, so the state stays consistent for every later kernel
+        bool bad = false;
+#pragma unroll
+        for (int d = 0; d < 3; ++d)
+            if (!(x[d] >= 0.0 && x[d] < g.L)) { x[d] = 0.0; bad = true; }
         int iz = 0;
-        uint32_t k = 0;
-        if (!(x[0] >= 0.0 && x[0] < g.L && x[1] >= 0.0 && x[1] < g.L && x[2] >= 0.0 && x[2] < g.L)) {
-            atomicExch(err + 1, 1);
-        } else {
+        uint32_t k = key_of(g, x, &iz);
+        if (iz < g.z0 || iz >= g.z0 + g.nzl) {
+            x[2] = ((double)g.z0 + 0.5) / g.inv_h;
             k = key_of(g, x, &iz);
-            if (iz < g.z0 || iz >= g.z0 + g.nzl) { atomicExch(err + 1, 1); k = 0; }
+            bad = true;
+        }
+        if (bad) {
+            atomicExch(err + 1, 1);
+            store_particle(cur, i, x, v);
         }
         key[i] = k;
         const uint32_t r = atomicAdd(count + k, 1u);
@@ -216,6 +223,8 @@ struct SendBuf {
     int seg;              // capacity per destination
 };
 
+constexpr int kLeaveCap = 256;   // leavers staged per brick before one atomic per destination
+
 __global__ void __launch_bounds__(kThreads) k_push_key_brick(Geom g, PState cur,
                                                              const uint32_t* __restrict__ offs,
                                                              const double* __restrict__ E4,
@@ -224,6 +233,9 @@ __global__ void __launch_bounds__(kThreads) k_push_key_brick(Geom g, PState cur,
                                                              uint32_t* __restrict__ count,
                                                              SendBuf sb, int* __restrict__ err) {
     __shared__ double4 etile[9 * 9 * 5];
+    __shared__ double2 lbuf[kLeaveCap][4];      // leavers of this brick (P > 1)
+    __shared__ uint8_t ldst[kLeaveCap];
+    __shared__ uint32_t lcount[8], lbase[8], nleave;
     const int t = threadIdx.x;
     const uint32_t c0 = blockIdx.x * kBrick;
     int bx, by, bz;
@@ -235,6 +247,8 @@ __global__ void __launch_bounds__(kThreads) k_push_key_brick(Geom g, PState cur,
         ldg_node(E4 + 4 * m, ex, ey, ez);
         etile[q] = make_double4(ex, ey, ez, 0.0);
     }
+    if (t < 8) lcount[t] = 0;
+    if (t == 0) nleave = 0;
     const uint32_t P0 = __ldg(offs + c0), P1 = __ldg(offs + c0 + kBrick);
     __syncthreads();
     double xn[3], vn[3];
@@ -270,18 +284,25 @@ __global__ void __launch_bounds__(kThreads) k_push_key_brick(Geom g, PState cur,
         cur.p[1][i] = make_double2(z0, v[2]);    // kicked velocity in place: (x_n, v_{n+1/2})
         cur.p[2][i] = make_double2(v[0], v[1]);
         int iz;
-        uint32_t k = key_of(g, x, &iz);
-        if (g.P > 1 && (iz < g.z0 || iz >= g.z0 + g.nzl)) {   // leaver
+        const uint32_t k = key_of(g, x, &iz);
+        if (g.P > 1 && (iz < g.z0 || iz >= g.z0 + g.nzl)) {   // leaver: staged, sent below
             const int dr = iz >> g.mz;
-            const uint32_t slot = atomicAdd(sb.count + dr, 1u);
-            if (slot < (uint32_t)sb.seg) {
-                double2* d = sb.data + ((int64_t)dr * sb.seg + slot) * 4;
-                d[0] = make_double2(x[0], x[1]);
-                d[1] = make_double2(x[2], v[2]);
-                d[2] = make_double2(v[0], v[1]);
-                d[3] = make_double2(__longlong_as_double((long long)((uint64_t)oldg | ((uint64_t)i << 32))), 0.0);
-            } else {
-                atomicExch(err + 2, 1);
+            const double2 p0 = make_double2(x[0], x[1]), p1 = make_double2(x[2], v[2]),
+                          p2 = make_double2(v[0], v[1]),
+                          p3 = make_double2(__longlong_as_double((long long)((uint64_t)oldg | ((uint64_t)i << 32))), 0.0);
+            const uint32_t s = atomicAdd(&nleave, 1u);
+            if (s < (uint32_t)kLeaveCap) {
+                lbuf[s][0] = p0; lbuf[s][1] = p1; lbuf[s][2] = p2; lbuf[s][3] = p3;
+                ldst[s] = (uint8_t)dr;
+                atomicAdd(&lcount[dr], 1u);
+            } else {                                  // rare: straight to the global buffer
+                const uint32_t slot = atomicAdd(sb.count + dr, 1u);
+                if (slot < (uint32_t)sb.seg) {
+                    double2* d = sb.data + ((int64_t)dr * sb.seg + slot) * 4;
+                    d[0] = p0; d[1] = p1; d[2] = p2; d[3] = p3;
+                } else {
+                    atomicExch(err + 2, 1);
+                }
             }
             key[i] = kNoKey;
             continue;
@@ -290,6 +311,25 @@ __global__ void __launch_bounds__(kThreads) k_push_key_brick(Geom g, PState cur,
         const uint32_t r = atomicAdd(count + k, 1u);
         if (r > 0xffffu) atomicExch(err, 1);
         rank[i] = (uint16_t)r;
+    }
+    if (g.P > 1) {      // one global atomic per destination, then the staged payloads
+        __syncthreads();
+        if (t < g.P) {
+            lbase[t] = lcount[t] ? atomicAdd(sb.count + t, lcount[t]) : 0u;
+            lcount[t] = 0;
+        }
+        __syncthreads();
+        const int nl = min((int)nleave, kLeaveCap);
+        for (int s = t; s < nl; s += kThreads) {
+            const int dr = ldst[s];
+            const uint32_t slot = lbase[dr] + atomicAdd(&lcount[dr], 1u);
+            if (slot < (uint32_t)sb.seg) {
+                double2* d = sb.data + ((int64_t)dr * sb.seg + slot) * 4;
+                d[0] = lbuf[s][0]; d[1] = lbuf[s][1]; d[2] = lbuf[s][2]; d[3] = lbuf[s][3];
+            } else {
+                atomicExch(err + 2, 1);
+            }
+        }
     }
 }
 
@@ -501,21 +541,33 @@ __device__ __forceinline__ int chunk_end(const uint32_t* soffs, int ca, int cap)
     return lo;
 }
 
-// ------------------------------------------------- reorder + deposit, P = 1 -
+// ------------------------------------------------------ reorder + deposit --
 // Ties inside a cell by pre-sort index (D#14).  The gather is cp.async (LDGSTS,
 // 16 B, L2 only) straight into the particle's stable slot of the staged chunk.
-template <bool PUSH>
+// MR (P > 1): entries e >= n_old are arrivals (receive buffer, already drifted by
+// their sender); the index rank puts them after the residents of their cell, and
+// a fix-up pass re-sorts the (few) cells holding arrivals by (old global key, old
+// index) -- the order of the single-domain oracle's global stable sort (D#15).
+template <bool MR>
+struct ReorderCap {
+    static constexpr int value = MR ? 1792 : 2048;
+};
+
+template <bool PUSH, bool MR>
 __global__ void __launch_bounds__(kThreads, 2) k_reorder_deposit(
     Geom g, const uint32_t* __restrict__ offs, const uint32_t* __restrict__ perm, PState cur,
-    PState nxt, double* __restrict__ rho, int* __restrict__ err) {
+    const double2* __restrict__ recv, int64_t n_old, PState nxt, double* __restrict__ rho,
+    int* __restrict__ err) {
+    constexpr int CAP = ReorderCap<MR>::value;
     extern __shared__ double dyn_smem[];
-    double2* sp0 = reinterpret_cast<double2*>(dyn_smem);               // [kCapA] (x, y)
-    double2* sp1 = sp0 + kCapA;                                          // [kCapA] (z, vz)
-    double2* sp2 = sp1 + kCapA;                                          // [kCapA] (vx, vy)
-    double* tile = reinterpret_cast<double*>(sp2 + kCapA);              // [9*9*5]
-    uint32_t* sperm = reinterpret_cast<uint32_t*>(tile + 9 * 9 * 5);    // [kCapA]
-    uint32_t* soffs = sperm + kCapA;                                     // [kBrick + 1]
-    uint8_t* scell = reinterpret_cast<uint8_t*>(soffs + kBrick + 1);    // [kCapA]
+    double2* sp0 = reinterpret_cast<double2*>(dyn_smem);               // [CAP] (x, y)
+    double2* sp1 = sp0 + CAP;                                            // [CAP] (z, vz)
+    double2* sp2 = sp1 + CAP;                                            // [CAP] (vx, vy)
+    double* tile = reinterpret_cast<double*>(sp2 + CAP);                // [9*9*5]
+    uint32_t* sperm = reinterpret_cast<uint32_t*>(tile + 9 * 9 * 5);    // [CAP]
+    uint32_t* soffs = sperm + CAP;                                       // [kBrick + 1]
+    uint32_t* sE = soffs + kBrick + 1;                                   // [CAP] (MR): entry at slot
+    uint8_t* scell = reinterpret_cast<uint8_t*>(sE + (MR ? CAP : 0));   // [CAP]
     const int t = threadIdx.x;
     const uint32_t c0 = blockIdx.x * kBrick;
     int bx, by, bz;
@@ -530,11 +582,11 @@ __global__ void __launch_bounds__(kThreads, 2) k_reorder_deposit(
     for (int q = 0; q < 8; ++q) acc[q] = 0.0;
     int ca = 0;
     while (ca < kBrick) {
-        if (soffs[ca + 1] - soffs[ca] > (uint32_t)kCapA) {
+        if (soffs[ca + 1] - soffs[ca] > (uint32_t)CAP) {
             if (t == 0) atomicExch(err, 1);
             return;
         }
-        const int cb = chunk_end(soffs, ca, kCapA);
+        const int cb = chunk_end(soffs, ca, CAP);
         const uint32_t P0 = soffs[ca];
         const int cnt = (int)(soffs[cb] - P0);
         for (int p = t; p < cnt; p += kThreads) sperm[p] = __ldg(perm + P0 + p);
@@ -550,17 +602,54 @@ __global__ void __launch_bounds__(kThreads, 2) k_reorder_deposit(
             int r = 0;
             for (int q = q0; q < q1; ++q) r += sperm[q] < j;
             const int o = q0 + r;
-            cp_async16(sp0 + o, cur.p[0] + j);
-            cp_async16(sp1 + o, cur.p[1] + j);
-            cp_async16(sp2 + o, cur.p[2] + j);
+            if (MR) sE[o] = j;
+            const double2* src0 = cur.p[0] + j;
+            const double2* src1 = cur.p[1] + j;
+            const double2* src2 = cur.p[2] + j;
+            if (MR && j >= n_old) {
+                const double2* d = recv + 4 * ((int64_t)j - n_old);
+                src0 = d; src1 = d + 1; src2 = d + 2;
+            }
+            cp_async16(sp0 + o, src0);
+            cp_async16(sp1 + o, src1);
+            cp_async16(sp2 + o, src2);
         }
         cp_async_wait_all();
         __syncthreads();
-        // drift in place (v is already kicked), coalesced streaming stores
+        if (MR) {   // cells holding arrivals: insertion sort by (old global key, old index)
+            bool any = false;
+            for (int p = s0; p < s1; ++p) any |= sE[p] >= n_old;
+            if (any) {
+                auto tie = [&](int slot) -> unsigned long long {
+                    const uint32_t e = sE[slot];
+                    if (e >= n_old)
+                        return (unsigned long long)__double_as_longlong(recv[4 * ((int64_t)e - n_old) + 3].x);
+                    const double x[3] = {sp0[slot].x, sp0[slot].y, sp1[slot].x};   // x_n (not yet drifted)
+                    return (unsigned long long)gkey_of(g, x) | ((unsigned long long)e << 32);
+                };
+                auto less = [](unsigned long long u, unsigned long long v) {
+                    const uint32_t ug = (uint32_t)u, vg = (uint32_t)v;
+                    return ug < vg || (ug == vg && (uint32_t)(u >> 32) < (uint32_t)(v >> 32));
+                };
+                for (int a = s0 + 1; a < s1; ++a) {
+                    const unsigned long long ta = tie(a);
+                    const double2 r0 = sp0[a], r1 = sp1[a], r2 = sp2[a];
+                    const uint32_t ea = sE[a];
+                    int b = a - 1;
+                    while (b >= s0 && less(ta, tie(b))) {
+                        sp0[b + 1] = sp0[b]; sp1[b + 1] = sp1[b]; sp2[b + 1] = sp2[b]; sE[b + 1] = sE[b];
+                        --b;
+                    }
+                    sp0[b + 1] = r0; sp1[b + 1] = r1; sp2[b + 1] = r2; sE[b + 1] = ea;
+                }
+            }
+            __syncthreads();
+        }
+        // drift in place (v is already kicked; arrivals arrive drifted), coalesced stores
         for (int p = t; p < cnt; p += kThreads) {
             double2 a = sp0[p], b = sp1[p];
             const double2 e = sp2[p];
-            if (PUSH) {
+            if (PUSH && !(MR && sE[p] >= n_old)) {
                 double x[3] = {a.x, a.y, b.x};
                 const double v[3] = {e.x, e.y, b.y};
                 drift(g, x, v);
@@ -577,116 +666,6 @@ __global__ void __launch_bounds__(kThreads, 2) k_reorder_deposit(
         __syncthreads();
         // CIC charge: thread per cell, its particles in stable order from shared memory
         for (int p = s0; p < s1; ++p) {
-            const double x[3] = {sp0[p].x, sp0[p].y, sp1[p].x};
-            cic_acc(g, x, acc);
-        }
-        __syncthreads();
-        ca = cb;
-    }
-    fold_flush(g, tile, acc, t, bx, by, bz, rho);
-}
-
-// ------------------------------------------------- reorder + deposit, P > 1 -
-// Entries e < n_old are residents (cur, drifted here), e >= n_old arrivals (the
-// receive buffer, already drifted by their sender).  Ties inside a cell by (old
-// global key, old index) -- the order of the single-domain oracle's global stable
-// sort restricted to the slab (D#15).  Gather first (cp.async into slot p), then
-// rank, then stream out in sorted order.
-template <bool PUSH>
-__global__ void __launch_bounds__(kThreads, 2) k_reorder_deposit_mr(
-    Geom g, const uint32_t* __restrict__ offs, const uint32_t* __restrict__ perm, PState cur,
-    const double2* __restrict__ recv, int64_t n_old, PState nxt, double* __restrict__ rho,
-    int* __restrict__ err) {
-    extern __shared__ double dyn_smem[];
-    double2* sp0 = reinterpret_cast<double2*>(dyn_smem);               // [kCapG]
-    double2* sp1 = sp0 + kCapG;
-    double2* sp2 = sp1 + kCapG;
-    unsigned long long* stie = reinterpret_cast<unsigned long long*>(sp2 + kCapG);   // [kCapG]
-    double* tile = reinterpret_cast<double*>(stie + kCapG);              // [9*9*5]
-    uint32_t* sperm = reinterpret_cast<uint32_t*>(tile + 9 * 9 * 5);    // [kCapG]
-    uint32_t* soffs = sperm + kCapG;                                     // [kBrick + 1]
-    uint16_t* sidx = reinterpret_cast<uint16_t*>(soffs + kBrick + 1);   // [kCapG]
-    uint8_t* scell = reinterpret_cast<uint8_t*>(sidx + kCapG);          // [kCapG]
-    const int t = threadIdx.x;
-    const uint32_t c0 = blockIdx.x * kBrick;
-    int bx, by, bz;
-    unlkey(g, c0, bx, by, bz);
-    soffs[t] = offs[c0 + t];
-    if (t == 0) soffs[kBrick] = offs[c0 + kBrick];
-    for (int q = t; q < 9 * 9 * 5; q += kThreads) tile[q] = 0.0;
-    __syncthreads();
-    double acc[8];
-#pragma unroll
-    for (int q = 0; q < 8; ++q) acc[q] = 0.0;
-    int ca = 0;
-    while (ca < kBrick) {
-        if (soffs[ca + 1] - soffs[ca] > (uint32_t)kCapG) {
-            if (t == 0) atomicExch(err, 1);
-            return;
-        }
-        const int cb = chunk_end(soffs, ca, kCapG);
-        const uint32_t P0 = soffs[ca];
-        const int cnt = (int)(soffs[cb] - P0);
-        for (int p = t; p < cnt; p += kThreads) {
-            const uint32_t e = __ldg(perm + P0 + p);
-            sperm[p] = e;
-            if (e < n_old) {
-                cp_async16(sp0 + p, cur.p[0] + e);
-                cp_async16(sp1 + p, cur.p[1] + e);
-                cp_async16(sp2 + p, cur.p[2] + e);
-            } else {
-                const double2* d = recv + 4 * ((int64_t)e - n_old);
-                cp_async16(sp0 + p, d);
-                cp_async16(sp1 + p, d + 1);
-                cp_async16(sp2 + p, d + 2);
-                cp_async8(stie + p, d + 3);      // old global key | old index << 32
-            }
-        }
-        const bool mine = t >= ca && t < cb;
-        const int s0 = mine ? (int)(soffs[t] - P0) : 0, s1 = mine ? (int)(soffs[t + 1] - P0) : 0;
-        for (int p = s0; p < s1; ++p) scell[p] = (uint8_t)t;
-        cp_async_wait_all();
-        __syncthreads();
-        // residents: tie key from x_n, then the drift; arrivals arrive drifted
-        for (int p = t; p < cnt; p += kThreads) {
-            const uint32_t e = sperm[p];
-            if (e < n_old) {
-                double x[3] = {sp0[p].x, sp0[p].y, sp1[p].x};
-                const double v[3] = {sp2[p].x, sp2[p].y, sp1[p].y};
-                const uint32_t og = gkey_of(g, x);
-                stie[p] = (unsigned long long)og | ((unsigned long long)e << 32);
-                if (PUSH) {
-                    drift(g, x, v);
-                    sp0[p] = make_double2(x[0], x[1]);
-                    sp1[p] = make_double2(x[2], v[2]);
-                }
-            }
-        }
-        __syncthreads();
-        // stable rank by (old global key, old index): sidx[o] = staged slot
-        for (int p = t; p < cnt; p += kThreads) {
-            const int c = scell[p];
-            const int q0 = (int)(soffs[c] - P0), q1 = (int)(soffs[c + 1] - P0);
-            const unsigned long long me = stie[p];
-            const uint32_t mg = (uint32_t)me, mi = (uint32_t)(me >> 32);
-            int r = 0;
-            for (int q = q0; q < q1; ++q) {
-                const unsigned long long o = stie[q];
-                const uint32_t og = (uint32_t)o, oi = (uint32_t)(o >> 32);
-                r += (og < mg) || (og == mg && oi < mi);
-            }
-            sidx[q0 + r] = (uint16_t)p;
-        }
-        __syncthreads();
-        for (int o = t; o < cnt; o += kThreads) {
-            const int p = sidx[o];
-            const int64_t oo = (int64_t)P0 + o;
-            nxt.p[0][oo] = sp0[p];
-            nxt.p[1][oo] = sp1[p];
-            nxt.p[2][oo] = sp2[p];
-        }
-        for (int o = s0; o < s1; ++o) {
-            const int p = sidx[o];
             const double x[3] = {sp0[p].x, sp0[p].y, sp1[p].x};
             cic_acc(g, x, acc);
         }
@@ -731,18 +710,20 @@ __global__ void k_add_plane(double* __restrict__ dst, const double* __restrict__
 
 inline unsigned blocks(int64_t n, int t) { return (unsigned)((n + t - 1) / t); }
 
-constexpr size_t kReorderSmem = sizeof(double2) * 3 * kCapA + sizeof(double) * 9 * 9 * 5 +
-                                sizeof(uint32_t) * (kCapA + kBrick + 1) + kCapA;
-constexpr size_t kReorderMrSmem = sizeof(double2) * 3 * kCapG + 8 * kCapG + sizeof(double) * 9 * 9 * 5 +
-                                  sizeof(uint32_t) * (kCapG + kBrick + 1) + 2 * kCapG + kCapG;
+template <bool MR>
+constexpr size_t reorder_smem() {
+    constexpr int CAP = ReorderCap<MR>::value;
+    return sizeof(double2) * 3 * CAP + sizeof(double) * 9 * 9 * 5 +
+           sizeof(uint32_t) * (CAP + kBrick + 1 + (MR ? CAP : 0)) + CAP;
+}
 
 }  // namespace
 
 void particles_set_smem_limits() {
-    cudaFuncSetAttribute(k_reorder_deposit<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kReorderSmem);
-    cudaFuncSetAttribute(k_reorder_deposit<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kReorderSmem);
-    cudaFuncSetAttribute(k_reorder_deposit_mr<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kReorderMrSmem);
-    cudaFuncSetAttribute(k_reorder_deposit_mr<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kReorderMrSmem);
+    cudaFuncSetAttribute(k_reorder_deposit<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)reorder_smem<false>());
+    cudaFuncSetAttribute(k_reorder_deposit<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)reorder_smem<false>());
+    cudaFuncSetAttribute(k_reorder_deposit<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)reorder_smem<true>());
+    cudaFuncSetAttribute(k_reorder_deposit<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)reorder_smem<true>());
 }
 
 void launch_sample(const Geom& g, PState st, int64_t np, double k, double alpha, uint64_t seed,
@@ -823,13 +804,15 @@ void launch_reorder_deposit(const Geom& g, const uint32_t* offs, const uint32_t*
                             int* err_flag, cudaStream_t s) {
     const unsigned nbrick = (unsigned)(((int64_t)g.n * g.n * g.nzl) / kBrick);
     if (g.P == 1) {
-        if (push) k_reorder_deposit<true><<<nbrick, kThreads, kReorderSmem, s>>>(g, offs, perm, cur, nxt, rho_buf, err_flag);
-        else k_reorder_deposit<false><<<nbrick, kThreads, kReorderSmem, s>>>(g, offs, perm, cur, nxt, rho_buf, err_flag);
+        if (push)
+            k_reorder_deposit<true, false><<<nbrick, kThreads, reorder_smem<false>(), s>>>(g, offs, perm, cur, recv, n_old, nxt, rho_buf, err_flag);
+        else
+            k_reorder_deposit<false, false><<<nbrick, kThreads, reorder_smem<false>(), s>>>(g, offs, perm, cur, recv, n_old, nxt, rho_buf, err_flag);
     } else {
         if (push)
-            k_reorder_deposit_mr<true><<<nbrick, kThreads, kReorderMrSmem, s>>>(g, offs, perm, cur, recv, n_old, nxt, rho_buf, err_flag);
+            k_reorder_deposit<true, true><<<nbrick, kThreads, reorder_smem<true>(), s>>>(g, offs, perm, cur, recv, n_old, nxt, rho_buf, err_flag);
         else
-            k_reorder_deposit_mr<false><<<nbrick, kThreads, kReorderMrSmem, s>>>(g, offs, perm, cur, recv, n_old, nxt, rho_buf, err_flag);
+            k_reorder_deposit<false, true><<<nbrick, kThreads, reorder_smem<true>(), s>>>(g, offs, perm, cur, recv, n_old, nxt, rho_buf, err_flag);
     }
 }
 

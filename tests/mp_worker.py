@@ -21,7 +21,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
 from oracle import oracle as O  # noqa: E402
-from paper_2605_05469_b200 import Simulation, nccl_unique_id  # noqa: E402
+from paper_2605_05469_b200 import Simulation, nccl_unique_id, slab_select  # noqa: E402
 from pic_inputs import landau_state  # noqa: E402
 
 
@@ -42,9 +42,7 @@ def main():
 
     # ---- case 1: import the same global state, step, compare with the oracle
     xv = landau_state(n, ppc, seed=11)
-    iz = np.minimum(np.floor(xv[2] * (n / L)).astype(np.int64), n - 1)
-    nz = n // world
-    mine = xv[:, (iz >= rank * nz) & (iz < (rank + 1) * nz)]
+    mine = slab_select(xv, n, L, rank, world)
     sim = Simulation(n=n, ppc=ppc, half_kick=False, rank=rank, nranks=world, nccl_id=fresh_id())
     sim.set_particles(mine)
     ex = sim.step(steps)
