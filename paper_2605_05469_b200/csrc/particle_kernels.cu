@@ -225,6 +225,7 @@ struct SendBuf {
 
 constexpr int kLeaveCap = 256;   // leavers staged per brick before one atomic per destination
 
+template <bool MR>
 __global__ void __launch_bounds__(kThreads) k_push_key_brick(Geom g, PState cur,
                                                              const uint32_t* __restrict__ offs,
                                                              const double* __restrict__ E4,
@@ -233,8 +234,8 @@ __global__ void __launch_bounds__(kThreads) k_push_key_brick(Geom g, PState cur,
                                                              uint32_t* __restrict__ count,
                                                              SendBuf sb, int* __restrict__ err) {
     __shared__ double4 etile[9 * 9 * 5];
-    __shared__ double2 lbuf[kLeaveCap][4];      // leavers of this brick (P > 1)
-    __shared__ uint8_t ldst[kLeaveCap];
+    __shared__ double2 lbuf[MR ? kLeaveCap : 1][4];      // leavers of this brick (P > 1)
+    __shared__ uint8_t ldst[MR ? kLeaveCap : 1];
     __shared__ uint32_t lcount[8], lbase[8], nleave;
     const int t = threadIdx.x;
     const uint32_t c0 = blockIdx.x * kBrick;
@@ -259,7 +260,7 @@ __global__ void __launch_bounds__(kThreads) k_push_key_brick(Geom g, PState cur,
         if (i + kThreads < P1) load_particle(cur, i + kThreads, xn, vn);
         const double z0 = x[2];
         uint32_t oldg = 0;
-        if (g.P > 1) oldg = gkey_of(g, x);
+        if (MR) oldg = gkey_of(g, x);
         int ii[3];
         double w[3][2];
         cic_weights(g, x, ii, w);
@@ -285,7 +286,7 @@ __global__ void __launch_bounds__(kThreads) k_push_key_brick(Geom g, PState cur,
         cur.p[2][i] = make_double2(v[0], v[1]);
         int iz;
         const uint32_t k = key_of(g, x, &iz);
-        if (g.P > 1 && (iz < g.z0 || iz >= g.z0 + g.nzl)) {   // leaver: staged, sent below
+        if (MR && (iz < g.z0 || iz >= g.z0 + g.nzl)) {   // leaver: staged, sent below
             const int dr = iz >> g.mz;
             const double2 p0 = make_double2(x[0], x[1]), p1 = make_double2(x[2], v[2]),
                           p2 = make_double2(v[0], v[1]),
@@ -312,7 +313,7 @@ __global__ void __launch_bounds__(kThreads) k_push_key_brick(Geom g, PState cur,
         if (r > 0xffffu) atomicExch(err, 1);
         rank[i] = (uint16_t)r;
     }
-    if (g.P > 1) {      // one global atomic per destination, then the staged payloads
+    if (MR) {      // one global atomic per destination, then the staged payloads
         __syncthreads();
         if (t < g.P) {
             lbase[t] = lcount[t] ? atomicAdd(sb.count + t, lcount[t]) : 0u;
@@ -768,7 +769,8 @@ void launch_push_key(const Geom& g, PState cur, const uint32_t* offs, const doub
                      int* err_flag, cudaStream_t s) {
     const unsigned nbrick = (unsigned)(((int64_t)g.n * g.n * g.nzl) / kBrick);
     SendBuf sb{send, send_count, seg};
-    k_push_key_brick<<<nbrick, kThreads, 0, s>>>(g, cur, offs, E4, key, rank, count, sb, err_flag);
+    if (g.P > 1) k_push_key_brick<true><<<nbrick, kThreads, 0, s>>>(g, cur, offs, E4, key, rank, count, sb, err_flag);
+    else k_push_key_brick<false><<<nbrick, kThreads, 0, s>>>(g, cur, offs, E4, key, rank, count, sb, err_flag);
 }
 
 void launch_key_arrivals(const Geom& g, const double2* recv, int64_t narr, int64_t n_old, uint32_t* key,
