@@ -11,6 +11,8 @@
 // twiddles come from a precomputed fp64 table W_n^m, m < n.  The spectral
 // multiply and the three inverse z transforms are fused into the z pass, the
 // field-energy partial sums into the C2R x pass.
+#include <algorithm>
+#include <climits>
 #include <cstdio>
 
 #include "kernels.h"
@@ -42,6 +44,10 @@ __device__ __forceinline__ double2 conj2(double2 a) { return make_double2(a.x, -
 // pad per 8 elements keeps the stride-8 writes of radix-8 stages conflict free).
 __device__ __forceinline__ int pidx(int e) { return e + (e >> 3); }
 __host__ __device__ inline int line_stride(int len) { return len + len / 8 + 1; }
+// Line stride of the column passes (TW lines = lanes l of a quarter warp with two
+// or more j): stride = 8 / TW (mod 8) puts the 8 lanes of each 128-bit shared
+// access phase on 8 distinct 16-byte slots.
+__host__ __device__ constexpr int col_stride(int len, int TW) { return len + len / 8 + 8 / TW; }
 
 template <int SIGN>
 __device__ __forceinline__ double2 mul_i(double2 a) {   // a * (-i) forward, a * (+i) inverse
@@ -85,10 +91,10 @@ __device__ __forceinline__ void dft8(double2* v) {
     v[3] = cadd(e3, w3o3); v[7] = csub(e3, w3o3);
 }
 
-template <int SIGN>
-__device__ __forceinline__ void dft_r(double2* v, int R) {
-    if (R == 8) dft8<SIGN>(v);
-    else if (R == 4) dft4<SIGN>(v[0], v[1], v[2], v[3]);
+template <int SIGN, int R>
+__device__ __forceinline__ void dft_r(double2* v) {
+    if constexpr (R == 8) dft8<SIGN>(v);
+    else if constexpr (R == 4) dft4<SIGN>(v[0], v[1], v[2], v[3]);
     else dft2<SIGN>(v);
 }
 
@@ -100,49 +106,85 @@ __device__ __forceinline__ double2 twid(const double2* __restrict__ tw, int q, i
     return SIGN < 0 ? w : conj2(w);
 }
 
-// IPT = middle-stage work items held per thread (nl * len <= 8 * IPT * blockDim).
-template <int SIGN, bool DST_SMEM, int IPT = 1, class Src, class Dst>
-__device__ void fft_lines(double2* sm, int nl, int logn, int ls, const double2* __restrict__ tw,
-                          int tws, Src src, Dst dst) {
-    const int len = 1 << logn;
-    const int rem = logn % 3;
-    const int logR0 = rem == 0 ? 3 : rem;
-    const int nst = (logn - logR0) / 3 + 1;
+// v[r] *= W^{jm r << tsh}, r = 1..7, from three table loads (r = 1, 2, 4) and
+// four products (w3 = w1 w2, w5 = w1 w4, w6 = w2 w4, w7 = w3 w4).
+template <int SIGN>
+__device__ __forceinline__ void twiddle8(double2* v, const double2* __restrict__ tw, int jm, int tsh, int tws) {
+    const double2 w1 = twid<SIGN>(tw, jm << tsh, tws);
+    const double2 w2 = twid<SIGN>(tw, (2 * jm) << tsh, tws);
+    const double2 w4 = twid<SIGN>(tw, (4 * jm) << tsh, tws);
+    const double2 w3 = cmul(w1, w2);
+    v[1] = cmul(v[1], w1);
+    v[2] = cmul(v[2], w2);
+    v[3] = cmul(v[3], w3);
+    v[4] = cmul(v[4], w4);
+    v[5] = cmul(v[5], cmul(w1, w4));
+    v[6] = cmul(v[6], cmul(w2, w4));
+    v[7] = cmul(v[7], cmul(w3, w4));
+}
+
+// Work item it -> (line l, butterfly j): ROWS (lines contiguous in memory, the x
+// passes) puts consecutive lanes on consecutive j of one line, so every global
+// access of a warp is one contiguous run; otherwise (lines = adjacent columns,
+// the y and z passes) consecutive lanes take consecutive lines.
+template <bool ROWS>
+__device__ __forceinline__ void item_lj(int it, int nl, int nj, int lognj, int& l, int& j) {
+    if (ROWS) { l = it >> lognj; j = it & (nj - 1); }
+    else { l = it % nl; j = it / nl; }
+}
+
+// Lines of length 2^LOGN (compile time: every stage's radix, butterfly count and
+// twiddle stride are constants).  IPT = middle-stage work items held per thread
+// (nl * len <= 8 * IPT * blockDim).
+// after0() runs once every thread is past stage 0 (the persistent kernels issue
+// the next tile's input copies there: src is no longer read).
+struct NoHook {
+    __device__ void operator()() const {}
+};
+
+template <int SIGN, bool DST_SMEM, int LOGN, int IPT, bool ROWS, class Src, class Dst, class Hook = NoHook>
+__device__ __forceinline__ void fft_lines(double2* sm, int nl, int ls, const double2* __restrict__ tw,
+                                          int tws, Src src, Dst dst, Hook after0 = Hook()) {
+    constexpr int len = 1 << LOGN;
+    constexpr int logR0 = LOGN % 3 == 0 ? 3 : LOGN % 3;
+    constexpr int nst = (LOGN - logR0) / 3 + 1;
     // ---- stage 0: src -> shared (or dst when it is also the last stage)
     {
-        const int R = 1 << logR0, nj = len >> logR0;
-        const bool last = nst == 1;
+        constexpr int R = 1 << logR0, nj = len >> logR0;
+        constexpr bool last = nst == 1;
         for (int it = threadIdx.x; it < nl * nj; it += blockDim.x) {
-            const int l = it % nl, j = it / nl;
-            double2 v[8];
+            int l, j;
+            item_lj<ROWS>(it, nl, nj, LOGN - logR0, l, j);
+            double2 v[R];
 #pragma unroll
-            for (int r = 0; r < 8; ++r)
-                if (r < R) v[r] = src(l, j + r * nj);
-            dft_r<SIGN>(v, R);
+            for (int r = 0; r < R; ++r) v[r] = src(l, j + r * nj);
+            dft_r<SIGN, R>(v);
 #pragma unroll
-            for (int r = 0; r < 8; ++r)
-                if (r < R) {
-                    const int e = j * R + r;        // Ns = 1
-                    if (last && !DST_SMEM) dst(l, e, v[r]);
-                    else sm[l * ls + pidx(e)] = v[r];
-                }
+            for (int r = 0; r < R; ++r) {
+                const int e = j * R + r;        // Ns = 1
+                if (last && !DST_SMEM) dst(l, e, v[r]);
+                else sm[l * ls + pidx(e)] = v[r];
+            }
         }
     }
     __syncthreads();
-    int logNs = logR0;
+    after0();
+#pragma unroll
     for (int s = 1; s < nst; ++s) {
-        const int nj = len >> 3, Ns = 1 << logNs;
-        const int tsh = logn - logNs - 3;       // W_{Ns 8}^{q} = W_len^{q << tsh}
+        const int logNs = logR0 + 3 * (s - 1);
+        constexpr int nj = len >> 3;
+        const int Ns = 1 << logNs;
+        const int tsh = LOGN - logNs - 3;       // W_{Ns 8}^{q} = W_len^{q << tsh}
         const bool last = s == nst - 1;
         if (last && !DST_SMEM) {
             for (int it = threadIdx.x; it < nl * nj; it += blockDim.x) {
-                const int l = it % nl, j = it / nl;
+                int l, j;
+                item_lj<ROWS>(it, nl, nj, LOGN - 3, l, j);
                 double2 v[8];
 #pragma unroll
                 for (int r = 0; r < 8; ++r) v[r] = sm[l * ls + pidx(j + r * nj)];
                 const int jm = j & (Ns - 1);
-#pragma unroll
-                for (int r = 1; r < 8; ++r) v[r] = cmul(v[r], twid<SIGN>(tw, (jm * r) << tsh, tws));
+                twiddle8<SIGN>(v, tw, jm, tsh, tws);
                 dft8<SIGN>(v);
                 const int base = ((j >> logNs) << (logNs + 3)) + jm;
 #pragma unroll
@@ -156,14 +198,14 @@ __device__ void fft_lines(double2* sm, int nl, int logn, int ls, const double2* 
                 const int it = threadIdx.x + k * blockDim.x;
                 lk[k] = -1;
                 if (it < nl * nj) {
-                    const int l = it % nl, j = it / nl;
+                    int l, j;
+                    item_lj<ROWS>(it, nl, nj, LOGN - 3, l, j);
                     lk[k] = l;
                     jk[k] = j;
 #pragma unroll
                     for (int r = 0; r < 8; ++r) v[k][r] = sm[l * ls + pidx(j + r * nj)];
                     const int jm = j & (Ns - 1);
-#pragma unroll
-                    for (int r = 1; r < 8; ++r) v[k][r] = cmul(v[k][r], twid<SIGN>(tw, (jm * r) << tsh, tws));
+                    twiddle8<SIGN>(v[k], tw, jm, tsh, tws);
                     dft8<SIGN>(v[k]);
                 }
             }
@@ -178,7 +220,6 @@ __device__ void fft_lines(double2* sm, int nl, int logn, int ls, const double2* 
                 }
         }
         __syncthreads();
-        logNs += 3;
     }
 }
 
@@ -190,36 +231,60 @@ __host__ __device__ inline int ilog2(int v) {
 
 // Elements per CTA: rows of the x passes, TW columns of the y and z passes.
 __host__ __device__ inline int x_rows(int n) { int r = 2048 / (n / 2); return r < 1 ? 1 : r; }
-__host__ __device__ inline int xi_rows(int n) { int r = 1024 / (n / 2); return r < 1 ? 1 : r; }
-__host__ __device__ inline int y_tw(int n) { int t = 2048 / n; return t > 8 ? 8 : (t < 1 ? 1 : t); }
-__host__ __device__ inline int z_tw(int n) { int t = 2048 / n; return t > 8 ? 8 : (t < 1 ? 1 : t); }
+__host__ __device__ inline int xi_rows(int n) { int r = 512 / (n / 2); return r < 1 ? 1 : r; }
+__host__ __device__ constexpr int y_tw(int n) { int t = 2048 / n; return t > 8 ? 8 : (t < 1 ? 1 : t); }
+__host__ __device__ constexpr int z_tw(int n) { int t = 2048 / n; return t > 8 ? 8 : (t < 1 ? 1 : t); }
+
+// Every pass is a persistent loop over tiles (grid = resident CTAs): the input of
+// tile t + gridDim is copied into the shared input buffer with cp.async as soon as
+// stage 0 of tile t has consumed it, so the loads of one tile overlap the
+// butterflies and stores of the previous one.
 
 // ------------------------------------------------------------ x R2C -------
-// Row r of S0 (nzl * n rows): n reals -> n/2 + 1 complex, in place (the CTA owns its rows).
+// Row r of S0 (nzl * n rows): n reals -> n/2 + 1 complex, in place (a tile = R rows).
 // z[m] = x[2m] + i x[2m+1] -> Z = FFT_{n/2}(z) -> X[k] = Ze[k] + W_n^k Zo[k],
 // Ze = (Z[k] + conj Z[n/2-k])/2, Zo = (Z[k] - conj Z[n/2-k])(-i/2).
-__global__ void __launch_bounds__(kThreads, 4) k_fft_x_fwd(Geom g, double* buf,
+template <int LOGN>
+__global__ void __launch_bounds__(kThreads, 3) k_fft_x_fwd(Geom g, double* buf,
                                                            const double2* __restrict__ tw) {
-    extern __shared__ double2 sm[];
-    const int len = g.n >> 1, logn = ilog2(len), R = x_rows(g.n), ls = line_stride(len);
-    const int64_t row0 = (int64_t)blockIdx.x * R;
-    const int rows = (int)min((int64_t)R, (int64_t)g.nzl * g.n - row0);
-    auto src = [&](int l, int e) {
-        return reinterpret_cast<const double2*>(buf + (row0 + l) * g.rp)[e];
+    extern __shared__ double2 smx[];
+    constexpr int len = 1 << LOGN;
+    const int R = x_rows(g.n), ls = line_stride(len);
+    double2* in = smx;               // [R][len]
+    double2* sm = smx + R * len;     // [R][ls]
+    const int64_t nrows = (int64_t)g.nzl * g.n, ntile = (nrows + R - 1) / R;
+    auto prefetch = [&](int64_t t) {
+        const int64_t row0 = t * R;
+        const int rows = (int)min((int64_t)R, nrows - row0);
+        for (int i = threadIdx.x; i < rows * len; i += blockDim.x) {
+            const int rl = i >> LOGN, e = i & (len - 1);
+            cp_async16(in + i, reinterpret_cast<const double2*>(buf + (row0 + rl) * g.rp) + e);
+        }
+        cp_async_commit();
     };
-    auto dst = [&](int, int, double2) {};
-    fft_lines<-1, true>(sm, rows, logn, ls, tw, 1, src, dst);
-    for (int t = threadIdx.x; t < rows * (len + 1); t += blockDim.x) {
-        const int rl = t / (len + 1), k = t - rl * (len + 1);
-        const double2 zk = sm[rl * ls + pidx(k & (len - 1))];
-        const double2 zc = conj2(sm[rl * ls + pidx((len - k) & (len - 1))]);
-        const double2 ze = make_double2(0.5 * (zk.x + zc.x), 0.5 * (zk.y + zc.y));
-        const double2 d = csub(zk, zc);
-        const double2 zo = make_double2(0.5 * d.y, -0.5 * d.x);
-        double2 X;
-        if (k == len) X = csub(ze, zo);
-        else X = cadd(ze, cmul(__ldg(tw + k), zo));
-        reinterpret_cast<double2*>(buf + (row0 + rl) * g.rp)[k] = X;
+    int64_t t = blockIdx.x;
+    if (t < ntile) prefetch(t);
+    for (; t < ntile; t += gridDim.x) {
+        const int64_t row0 = t * R;
+        const int rows = (int)min((int64_t)R, nrows - row0);
+        cp_async_wait0();
+        __syncthreads();
+        auto src = [&](int l, int e) { return in[l * len + e]; };
+        auto dst = [&](int, int, double2) {};
+        auto next = [&]() { if (t + gridDim.x < ntile) prefetch(t + gridDim.x); };
+        fft_lines<-1, true, LOGN, 1, true>(sm, rows, ls, tw, 1, src, dst, next);
+        for (int i = threadIdx.x; i < rows * (len + 1); i += blockDim.x) {
+            const int rl = i / (len + 1), k = i - rl * (len + 1);
+            const double2 zk = sm[rl * ls + pidx(k & (len - 1))];
+            const double2 zc = conj2(sm[rl * ls + pidx((len - k) & (len - 1))]);
+            const double2 ze = make_double2(0.5 * (zk.x + zc.x), 0.5 * (zk.y + zc.y));
+            const double2 d = csub(zk, zc);
+            const double2 zo = make_double2(0.5 * d.y, -0.5 * d.x);
+            double2 X;
+            if (k == len) X = csub(ze, zo);
+            else X = cadd(ze, cmul(__ldg(tw + k), zo));
+            reinterpret_cast<double2*>(buf + (row0 + rl) * g.rp)[k] = X;
+        }
     }
 }
 
@@ -231,80 +296,131 @@ __device__ __forceinline__ int64_t spec_row(const Geom& g, const SpecLayout& L, 
 }
 
 // ------------------------------------------------------------- y pass ------
-// blockIdx.x = zl * ntiles + tile, blockIdx.y = component.  Lines along y of TW
-// consecutive kx columns (valid columns kx <= n/2); the first stage reads the whole
-// tile before the last stage writes it, so src and dst may alias.
-template <int SIGN>
-__global__ void __launch_bounds__(kThreads, 2) k_fft_y(Geom g, SpecLayout sl, SpecLayout dl,
+// Tile (component d, plane zl, kx tile): lines along y of TW consecutive kx columns
+// (valid columns kx <= n/2).  A tile's input is all in shared memory before its
+// last stage writes, so src and dst may alias.
+template <int SIGN, int LOGN>
+__global__ void __launch_bounds__(kThreads, 2) k_fft_y(Geom g, SpecLayout sl, SpecLayout dl, int ncomp,
                                                        const double2* __restrict__ tw) {
-    extern __shared__ double2 sm[];
-    const int n = g.n, logn = ilog2(n), TW = y_tw(n), ls = line_stride(n);
-    const int ntiles = (n / 2 + 1 + TW - 1) / TW;
-    const int zl = blockIdx.x / ntiles, kx0 = (blockIdx.x - zl * ntiles) * TW, d = blockIdx.y;
-    const int ncol = min(TW, n / 2 + 1 - kx0);
-    auto src = [&](int l, int y) {
-        return l < ncol ? sl.base[spec_row(g, sl, d, zl, y) + kx0 + l] : make_double2(0.0, 0.0);
+    extern __shared__ double2 smx[];
+    constexpr int n = 1 << LOGN, TW = y_tw(n);
+    constexpr int ls = col_stride(n, TW);
+    double2* in = smx;               // [n][TW]
+    double2* sm = smx + n * TW;      // [TW][ls]
+    constexpr int ntiles = (n / 2 + 1 + TW - 1) / TW;
+    const int64_t ntile = (int64_t)ncomp * g.nzl * ntiles;
+    auto prefetch = [&](int64_t t) {
+        const int d = (int)(t / ((int64_t)g.nzl * ntiles));
+        const int r = (int)(t - (int64_t)d * g.nzl * ntiles);
+        const int zl = r / ntiles, kx0 = (r - zl * ntiles) * TW;
+        const int ncol = min(TW, n / 2 + 1 - kx0);
+        for (int i = threadIdx.x; i < n * TW; i += blockDim.x) {
+            const int y = i / TW, l = i % TW;
+            if (l < ncol) cp_async16(in + i, sl.base + spec_row(g, sl, d, zl, y) + kx0 + l);
+        }
+        cp_async_commit();
     };
-    auto dst = [&](int l, int y, double2 v) { if (l < ncol) dl.base[spec_row(g, dl, d, zl, y) + kx0 + l] = v; };
-    fft_lines<SIGN, false>(sm, TW, logn, ls, tw, 0, src, dst);
+    int64_t t = blockIdx.x;
+    if (t < ntile) prefetch(t);
+    for (; t < ntile; t += gridDim.x) {
+        const int d = (int)(t / ((int64_t)g.nzl * ntiles));
+        const int r = (int)(t - (int64_t)d * g.nzl * ntiles);
+        const int zl = r / ntiles, kx0 = (r - zl * ntiles) * TW;
+        const int ncol = min(TW, n / 2 + 1 - kx0);
+        cp_async_wait0();
+        __syncthreads();
+        auto src = [&](int l, int y) { return l < ncol ? in[y * TW + l] : make_double2(0.0, 0.0); };
+        auto dst = [&](int l, int y, double2 v) { if (l < ncol) dl.base[spec_row(g, dl, d, zl, y) + kx0 + l] = v; };
+        auto next = [&]() { if (t + gridDim.x < ntile) prefetch(t + gridDim.x); };
+        fft_lines<SIGN, false, LOGN, 1, false>(sm, TW, ls, tw, 0, src, dst, next);
+    }
 }
 
 // --------------------------------------------------- z pass + multiply -----
-// blockIdx.x = yl * ntiles + tile over the ky-pencil [z][yl][px] (all n planes,
-// nyl = n / P rows of ky, ky = rank nyl + yl).  Forward z FFT of rho^ into shared
-// memory, then for d = x, y, z an inverse z FFT whose first stage reads
+// Tile (yl, kx tile) of the ky-pencil [z][yl][px] (all n planes, nyl = n / P rows
+// of ky, ky = rank nyl + yl).  Forward z FFT of rho^ into shared memory, then for
+// d = x, y, z an inverse z FFT whose first stage reads
 // E^_d = -i k_d rho^ / |k|^2 * scale (zero at n = 0 and where n_d = -N/2, D#6)
 // straight from it; stores PACKED [q][d][zl][yl][px] (q = z / nzl) for the return
 // transpose.
+template <int LOGN>
 __global__ void __launch_bounds__(kThreads, 2) k_fft_z_mul(Geom g, const double2* __restrict__ pencil,
                                                            double2* __restrict__ out, double scale,
                                                            const double2* __restrict__ tw) {
-    extern __shared__ double2 sm[];
-    const int n = g.n, logn = ilog2(n), TW = z_tw(n), ls = line_stride(n), nyl = n / g.P;
-    double2* s1 = sm;
-    double2* s2 = sm + TW * ls;
-    const int ntiles = (n / 2 + 1 + TW - 1) / TW;
-    const int yl = blockIdx.x / ntiles, kx0 = (blockIdx.x - yl * ntiles) * TW;
-    const int ky = g.rank * nyl + yl;
-    const int ncol = min(TW, n / 2 + 1 - kx0);
+    extern __shared__ double2 smx[];
+    constexpr int n = 1 << LOGN, TW = z_tw(n);
+    constexpr int ls = col_stride(n, TW);
+    const int nyl = n / g.P;
+    double2* in = smx;               // [n][TW]
+    double2* s1 = smx + n * TW;      // [TW][ls] forward result
+    double2* s2 = s1 + TW * ls;      // [TW][ls] inverse work
+    constexpr int ntiles = (n / 2 + 1 + TW - 1) / TW;
+    const int64_t ntile = (int64_t)nyl * ntiles;
     const int64_t zstride = (int64_t)nyl * g.px;
-    const int64_t off = (int64_t)yl * g.px + kx0;
-    {
-        auto src = [&](int l, int e) { return l < ncol ? pencil[off + e * zstride + l] : make_double2(0.0, 0.0); };
-        auto dst = [&](int, int, double2) {};
-        fft_lines<-1, true>(s1, TW, logn, ls, tw, 0, src, dst);
-    }
+    auto prefetch = [&](int64_t t) {
+        const int yl = (int)(t / ntiles), kx0 = (int)(t - (int64_t)yl * ntiles) * TW;
+        const int ncol = min(TW, n / 2 + 1 - kx0);
+        const double2* p = pencil + (int64_t)yl * g.px + kx0;
+        for (int i = threadIdx.x; i < n * TW; i += blockDim.x) {
+            const int z = i / TW, l = i % TW;
+            if (l < ncol) cp_async16(in + i, p + z * zstride + l);
+        }
+        cp_async_commit();
+    };
     const double kf = 6.283185307179586476925286766559 / g.L;
-    const int half = n / 2;
-    const double kyv = kf * (double)(ky < half ? ky : ky - n);
-    for (int d = 0; d < 3; ++d) {
-        auto src = [&](int l, int kz) {
-            const int kx = kx0 + l;
+    constexpr int half = n / 2;
+    int64_t t = blockIdx.x;
+    if (t < ntile) prefetch(t);
+    for (; t < ntile; t += gridDim.x) {
+        const int yl = (int)(t / ntiles), kx0 = (int)(t - (int64_t)yl * ntiles) * TW;
+        const int ncol = min(TW, n / 2 + 1 - kx0);
+        const int ky = g.rank * nyl + yl;
+        cp_async_wait0();
+        __syncthreads();
+        {
+            auto src = [&](int l, int e) { return l < ncol ? in[e * TW + l] : make_double2(0.0, 0.0); };
+            auto dst = [&](int, int, double2) {};
+            auto next = [&]() { if (t + gridDim.x < ntile) prefetch(t + gridDim.x); };
+            fft_lines<-1, true, LOGN, 1, false>(s1, TW, ls, tw, 0, src, dst, next);
+        }
+        const double kyv = kf * (double)(ky < half ? ky : ky - n);
+        // phi^ = rho^ scale / |k|^2 in place (0 at k = 0): one division per mode
+        for (int i = threadIdx.x; i < TW * n; i += blockDim.x) {
+            const int l = i / n, kz = i % n, kx = kx0 + l;
             const double kxv = kf * (double)(kx < half ? kx : kx - n);
             const double kzv = kf * (double)(kz < half ? kz : kz - n);
             const double k2 = kxv * kxv + kyv * kyv + kzv * kzv;
-            const int idx = d == 0 ? kx : (d == 1 ? ky : kz);
-            const double kd = d == 0 ? kxv : (d == 1 ? kyv : kzv);
-            double2 e = make_double2(0.0, 0.0);
-            if (l < ncol && k2 != 0.0 && idx != half) {
-                const double2 r = s1[l * ls + pidx(kz)];
-                const double f = kd * scale / k2;
-                e = make_double2(f * r.y, -f * r.x);   // -i k_d rho^ / |k|^2
-            }
-            return e;
-        };
-        auto dst = [&](int l, int z, double2 v) {
-            if (l < ncol) {
-                const int q = z >> g.mz, zl = z - (q << g.mz);
-                out[((((int64_t)q * 3 + d) * g.nzl + zl) * nyl + yl) * g.px + kx0 + l] = v;
-            }
-        };
-        fft_lines<+1, false>(s2, TW, logn, ls, tw, 0, src, dst);
+            const double f = k2 != 0.0 ? scale / k2 : 0.0;
+            double2& r = s1[l * ls + pidx(kz)];
+            r = make_double2(f * r.x, f * r.y);
+        }
+        __syncthreads();
+        for (int d = 0; d < 3; ++d) {
+            auto src = [&](int l, int kz) {
+                const int kx = kx0 + l;
+                const int idx = d == 0 ? kx : (d == 1 ? ky : kz);
+                const int m = idx < half ? idx : idx - n;
+                double2 e = make_double2(0.0, 0.0);
+                if (l < ncol && idx != half) {
+                    const double2 r = s1[l * ls + pidx(kz)];
+                    const double kd = kf * (double)m;
+                    e = make_double2(kd * r.y, -kd * r.x);   // E^_d = -i k_d phi^
+                }
+                return e;
+            };
+            auto dst = [&](int l, int z, double2 v) {
+                if (l < ncol) {
+                    const int q = z >> g.mz, zl = z - (q << g.mz);
+                    out[((((int64_t)q * 3 + d) * g.nzl + zl) * nyl + yl) * g.px + kx0 + l] = v;
+                }
+            };
+            fft_lines<+1, false, LOGN, 1, false>(s2, TW, ls, tw, 0, src, dst);
+        }
     }
 }
 
 // ------------------------------------------------------------ x C2R -------
-// R rows of all three components per CTA: n/2 + 1 complex -> n reals each,
+// A tile = R rows of all three components: n/2 + 1 complex -> n reals each,
 // written as node records E4[zl][y][x] = (E_x, E_y, E_z, 0) with 256-bit stores;
 // per-CTA partial sums of E_d^2 -> partials[d * gridDim.x + blockIdx.x].
 // Z[k] = (X[k] + conj X[n/2-k]) + i (X[k] - conj X[n/2-k]) W_n^{-k} (unnormalised).
@@ -313,38 +429,58 @@ __device__ __forceinline__ void st_node(double* p, double a, double b, double c)
                  : "memory");
 }
 
+template <int LOGN>
 __global__ void __launch_bounds__(kThreads, 3) k_fft_x_inv(Geom g, const double2* __restrict__ spec,
                                                            double* __restrict__ E4,
                                                            const double2* __restrict__ tw,
                                                            double* __restrict__ partials) {
-    extern __shared__ double2 sm[];
+    extern __shared__ double2 smx[];
     __shared__ double red[3][kThreads / 32];
-    const int len = g.n >> 1, logn = ilog2(len), R = xi_rows(g.n), ls = line_stride(len);
-    const int64_t nrows = (int64_t)g.nzl * g.n;
-    const int64_t row0 = (int64_t)blockIdx.x * R;
-    const int rows = (int)min((int64_t)R, nrows - row0);
-    auto src = [&](int l, int k) {          // line l = rl * 3 + d
-        const int rl = l / 3, d = l - 3 * rl;
-        const double2* X = spec + ((int64_t)d * nrows + row0 + rl) * g.px;
-        const double2 xk = X[k], xc = conj2(X[len - k]);
-        const double2 ze = cadd(xk, xc);
-        const double2 zo = cmul(csub(xk, xc), conj2(__ldg(tw + k)));
-        return make_double2(ze.x - zo.y, ze.y + zo.x);
+    constexpr int len = 1 << LOGN;
+    const int R = xi_rows(g.n), ls = line_stride(len), px = g.px;
+    double2* in = smx;                   // [3][R][px]
+    double2* sm = smx + 3 * R * px;      // [3 R][ls]
+    const int64_t nrows = (int64_t)g.nzl * g.n, ntile = (nrows + R - 1) / R;
+    auto prefetch = [&](int64_t t) {
+        const int64_t row0 = t * R;
+        const int per = (int)min((int64_t)R, nrows - row0) * px;
+        for (int i = threadIdx.x; i < 3 * per; i += blockDim.x) {
+            const int d = i / per, e = i - d * per;
+            cp_async16(in + d * R * px + e, spec + ((int64_t)d * nrows + row0) * px + e);
+        }
+        cp_async_commit();
     };
-    auto dst = [&](int, int, double2) {};
-    fft_lines<+1, true, 2>(sm, 3 * rows, logn, ls, tw, 1, src, dst);
     double e2[3] = {0.0, 0.0, 0.0};
-    for (int t = threadIdx.x; t < rows * len; t += blockDim.x) {
-        const int rl = t / len, m = t - rl * len;
-        const double2 vx = sm[(3 * rl + 0) * ls + pidx(m)];
-        const double2 vy = sm[(3 * rl + 1) * ls + pidx(m)];
-        const double2 vz = sm[(3 * rl + 2) * ls + pidx(m)];
-        double* node = E4 + 4 * ((row0 + rl) * g.n + 2 * m);
-        st_node(node, vx.x, vy.x, vz.x);
-        st_node(node + 4, vx.y, vy.y, vz.y);
-        e2[0] = fma(vx.x, vx.x, fma(vx.y, vx.y, e2[0]));
-        e2[1] = fma(vy.x, vy.x, fma(vy.y, vy.y, e2[1]));
-        e2[2] = fma(vz.x, vz.x, fma(vz.y, vz.y, e2[2]));
+    int64_t t = blockIdx.x;
+    if (t < ntile) prefetch(t);
+    for (; t < ntile; t += gridDim.x) {
+        const int64_t row0 = t * R;
+        const int rows = (int)min((int64_t)R, nrows - row0);
+        cp_async_wait0();
+        __syncthreads();
+        auto src = [&](int l, int k) {          // line l = rl * 3 + d
+            const int rl = l / 3, d = l - 3 * rl;
+            const double2* X = in + (d * R + rl) * px;
+            const double2 xk = X[k], xc = conj2(X[len - k]);
+            const double2 ze = cadd(xk, xc);
+            const double2 zo = cmul(csub(xk, xc), conj2(__ldg(tw + k)));
+            return make_double2(ze.x - zo.y, ze.y + zo.x);
+        };
+        auto dst = [&](int, int, double2) {};
+        auto next = [&]() { if (t + gridDim.x < ntile) prefetch(t + gridDim.x); };
+        fft_lines<+1, true, LOGN, 1, true>(sm, 3 * rows, ls, tw, 1, src, dst, next);
+        for (int i = threadIdx.x; i < rows * len; i += blockDim.x) {
+            const int rl = i >> LOGN, m = i & (len - 1);
+            const double2 vx = sm[(3 * rl + 0) * ls + pidx(m)];
+            const double2 vy = sm[(3 * rl + 1) * ls + pidx(m)];
+            const double2 vz = sm[(3 * rl + 2) * ls + pidx(m)];
+            double* node = E4 + 4 * ((row0 + rl) * g.n + 2 * m);
+            st_node(node, vx.x, vy.x, vz.x);
+            st_node(node + 4, vx.y, vy.y, vz.y);
+            e2[0] = fma(vx.x, vx.x, fma(vx.y, vx.y, e2[0]));
+            e2[1] = fma(vy.x, vy.x, fma(vy.y, vy.y, e2[1]));
+            e2[2] = fma(vz.x, vz.x, fma(vz.y, vz.y, e2[2]));
+        }
     }
 #pragma unroll
     for (int d = 0; d < 3; ++d) {
@@ -376,8 +512,18 @@ __global__ void __launch_bounds__(1024) k_energy_reduce(Geom g, const double* __
                                                         int nparts, double* __restrict__ energies) {
     __shared__ double red[3][32];
     double s[3] = {0.0, 0.0, 0.0};
+    // eight independent loads in flight per thread per round (latency, not bandwidth, bounds one CTA)
     for (int d = 0; d < 3; ++d)
-        for (int i = threadIdx.x; i < nparts; i += blockDim.x) s[d] += partials[(int64_t)d * nparts + i];
+        for (int i0 = threadIdx.x; i0 < nparts; i0 += 8 * blockDim.x) {
+            double t[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const int i = i0 + u * blockDim.x;
+                t[u] = i < nparts ? partials[(int64_t)d * nparts + i] : 0.0;
+            }
+#pragma unroll
+            for (int u = 0; u < 8; ++u) s[d] += t[u];
+        }
     for (int d = 0; d < 3; ++d) {
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) s[d] += __shfl_xor_sync(0xffffffffu, s[d], o);
@@ -399,39 +545,98 @@ __global__ void __launch_bounds__(1024) k_energy_reduce(Geom g, const double* __
 
 }  // namespace
 
-int energy_partials(const Geom& g) {
-    const int64_t nrows = (int64_t)g.nzl * g.n;
-    return (int)((nrows + xi_rows(g.n) - 1) / xi_rows(g.n));
+constexpr int kMaxPartials = 4096;
+
+// Upper bound of the per-CTA energy partials (the x C2R grid), for the workspace.
+int energy_partials(const Geom&) { return kMaxPartials; }
+
+// Persistent grid: the resident CTAs of the device (occupancy x SMs), <= ntile.
+template <class K>
+static unsigned persistent_grid(K kernel, size_t smem, int64_t ntile, int64_t cap = INT32_MAX) {
+    int dev = 0, sms = 148, occ = 1;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel, kThreads, smem);
+    if (occ < 1) occ = 1;
+    return (unsigned)std::max<int64_t>(1, std::min<int64_t>(std::min<int64_t>(ntile, cap), (int64_t)occ * sms));
+}
+
+// Dispatch on the line length: K = log2(len) of the x passes (len = n/2, n in
+// [16, 1024]) and of the y and z passes (len = n).
+#define PIC_X_SWITCH(lg, BODY)                                   \
+    switch (lg) {                                                \
+    case 3: { constexpr int K = 3; BODY; } break;                \
+    case 4: { constexpr int K = 4; BODY; } break;                \
+    case 5: { constexpr int K = 5; BODY; } break;                \
+    case 6: { constexpr int K = 6; BODY; } break;                \
+    case 7: { constexpr int K = 7; BODY; } break;                \
+    case 8: { constexpr int K = 8; BODY; } break;                \
+    case 9: { constexpr int K = 9; BODY; } break;                \
+    default: break;                                              \
+    }
+#define PIC_YZ_SWITCH(lg, BODY)                                  \
+    switch (lg) {                                                \
+    case 4: { constexpr int K = 4; BODY; } break;                \
+    case 5: { constexpr int K = 5; BODY; } break;                \
+    case 6: { constexpr int K = 6; BODY; } break;                \
+    case 7: { constexpr int K = 7; BODY; } break;                \
+    case 8: { constexpr int K = 8; BODY; } break;                \
+    case 9: { constexpr int K = 9; BODY; } break;                \
+    case 10: { constexpr int K = 10; BODY; } break;              \
+    default: break;                                              \
+    }
+
+static size_t x_fwd_smem(const Geom& g) {
+    const int len = g.n / 2, R = x_rows(g.n);
+    return sizeof(double2) * (size_t)R * (len + line_stride(len));
+}
+static size_t x_inv_smem(const Geom& g) {
+    const int len = g.n / 2, R = xi_rows(g.n);
+    return sizeof(double2) * 3 * (size_t)R * (g.px + line_stride(len));
+}
+static int64_t x_tiles(const Geom& g, int R) { return ((int64_t)g.nzl * g.n + R - 1) / R; }
+
+// Grid of the x C2R pass = number of energy partials it writes.
+static unsigned x_inv_grid(const Geom& g) {
+    const size_t smem = x_inv_smem(g);
+    const int64_t nt = x_tiles(g, xi_rows(g.n));
+    unsigned grid = 1;
+    PIC_X_SWITCH(ilog2(g.n / 2), (grid = persistent_grid(k_fft_x_inv<K>, smem, nt, kMaxPartials)))
+    return grid;
 }
 
 void launch_fft_x_fwd(const Geom& g, double* S0, const double2* tw, cudaStream_t s) {
-    const int len = g.n / 2, R = x_rows(g.n);
-    const size_t smem = sizeof(double2) * (size_t)R * line_stride(len);
-    const int64_t nrows = (int64_t)g.nzl * g.n;
-    k_fft_x_fwd<<<(unsigned)((nrows + R - 1) / R), kThreads, smem, s>>>(g, S0, tw);
+    const size_t smem = x_fwd_smem(g);
+    const int64_t nt = x_tiles(g, x_rows(g.n));
+    PIC_X_SWITCH(ilog2(g.n / 2), (k_fft_x_fwd<K><<<persistent_grid(k_fft_x_fwd<K>, smem, nt), kThreads, smem, s>>>(g, S0, tw)))
 }
 
 void launch_fft_y(const Geom& g, SpecLayout src, SpecLayout dst, int ncomp, int inverse,
                   const double2* tw, cudaStream_t s) {
     const int TW = y_tw(g.n), ntiles = (g.n / 2 + 1 + TW - 1) / TW;
-    const size_t smem = sizeof(double2) * (size_t)TW * line_stride(g.n);
-    dim3 grid(g.nzl * ntiles, ncomp);
-    if (inverse) k_fft_y<+1><<<grid, kThreads, smem, s>>>(g, src, dst, tw);
-    else k_fft_y<-1><<<grid, kThreads, smem, s>>>(g, src, dst, tw);
+    const size_t smem = sizeof(double2) * (size_t)TW * (g.n + col_stride(g.n, TW));
+    const int64_t nt = (int64_t)ncomp * g.nzl * ntiles;
+    if (inverse)
+        PIC_YZ_SWITCH(ilog2(g.n), (k_fft_y<+1, K><<<persistent_grid(k_fft_y<+1, K>, smem, nt), kThreads, smem, s>>>(g, src, dst, ncomp, tw)))
+    else
+        PIC_YZ_SWITCH(ilog2(g.n), (k_fft_y<-1, K><<<persistent_grid(k_fft_y<-1, K>, smem, nt), kThreads, smem, s>>>(g, src, dst, ncomp, tw)))
 }
 
 void launch_fft_z_mul(const Geom& g, const double2* pencil, double2* out, double scale,
                       const double2* tw, cudaStream_t s) {
     const int TW = z_tw(g.n), ntiles = (g.n / 2 + 1 + TW - 1) / TW;
-    const size_t smem = 2 * sizeof(double2) * (size_t)TW * line_stride(g.n);
-    k_fft_z_mul<<<(g.n / g.P) * ntiles, kThreads, smem, s>>>(g, pencil, out, scale, tw);
+    const size_t smem = sizeof(double2) * (size_t)TW * (g.n + 2 * col_stride(g.n, TW));
+    const int64_t nt = (int64_t)(g.n / g.P) * ntiles;
+    // one tile per CTA: the pass is bound by its four transforms, not its input
+    // loads, and measured faster without the persistent loop
+    PIC_YZ_SWITCH(ilog2(g.n), (k_fft_z_mul<K><<<(unsigned)nt, kThreads, smem, s>>>(g, pencil, out, scale, tw)))
 }
 
 void launch_fft_x_inv(const Geom& g, const double2* spec, double* E4, const double2* tw,
                       double* partials, cudaStream_t s) {
-    const int len = g.n / 2, R = xi_rows(g.n);
-    const size_t smem = 3 * sizeof(double2) * (size_t)R * line_stride(len);
-    k_fft_x_inv<<<energy_partials(g), kThreads, smem, s>>>(g, spec, E4, tw, partials);
+    const size_t smem = x_inv_smem(g);
+    const unsigned grid = x_inv_grid(g);
+    PIC_X_SWITCH(ilog2(g.n / 2), (k_fft_x_inv<K><<<grid, kThreads, smem, s>>>(g, spec, E4, tw, partials)))
 }
 
 void launch_e4_extract(const Geom& g, const double* E4, int d, double* out, cudaStream_t s) {
@@ -445,17 +650,21 @@ void launch_e4_pack(const Geom& g, const double* const comp[3], double* E4, cuda
 }
 
 void launch_energy_reduce(const Geom& g, const double* partials, double* energies, cudaStream_t s) {
-    k_energy_reduce<<<1, 1024, 0, s>>>(g, partials, energy_partials(g), energies);
+    k_energy_reduce<<<1, 1024, 0, s>>>(g, partials, (int)x_inv_grid(g), energies);
 }
 
 // Opt every FFT kernel into > 48 KB of dynamic shared memory once.
 void fft_set_smem_limits() {
     const int big = 200 * 1024;
-    cudaFuncSetAttribute(k_fft_x_fwd, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
-    cudaFuncSetAttribute(k_fft_y<-1>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
-    cudaFuncSetAttribute(k_fft_y<+1>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
-    cudaFuncSetAttribute(k_fft_z_mul, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
-    cudaFuncSetAttribute(k_fft_x_inv, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
+    for (int lg = 3; lg <= 9; ++lg) {
+        PIC_X_SWITCH(lg, (cudaFuncSetAttribute(k_fft_x_fwd<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, big),
+                          cudaFuncSetAttribute(k_fft_x_inv<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, big)))
+    }
+    for (int lg = 4; lg <= 10; ++lg) {
+        PIC_YZ_SWITCH(lg, (cudaFuncSetAttribute(k_fft_y<-1, K>, cudaFuncAttributeMaxDynamicSharedMemorySize, big),
+                           cudaFuncSetAttribute(k_fft_y<+1, K>, cudaFuncAttributeMaxDynamicSharedMemorySize, big),
+                           cudaFuncSetAttribute(k_fft_z_mul<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, big)))
+    }
 }
 
 }  // namespace pic

@@ -31,18 +31,6 @@ constexpr int kThreads = 256;
 constexpr int kBrick = 256;     // cells per brick (Morton 8 bits: 8 x 8 x 4)
 constexpr uint32_t kNoKey = 0xffffffffu;
 
-__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
-    const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s), "l"(gmem) : "memory");
-}
-__device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
-    const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(s), "l"(gmem) : "memory");
-}
-__device__ __forceinline__ void cp_async_wait_all() {
-    asm volatile("cp.async.commit_group;\n\tcp.async.wait_group 0;" ::: "memory");
-}
-
 // ---------------------------------------------------------------- init -----
 // Landau initial condition: x_d by Newton on the inverse CDF of
 // (1 + alpha cos(k x))/L from x = u_d L (|dx| < 1e-12 or 32 iterations),

@@ -220,6 +220,18 @@ __device__ __forceinline__ void store_particle(const PState& s, int64_t i, const
     s.p[2][i] = make_double2(v[0], v[1]);
 }
 
+// -------------------------------------------------------------- cp.async ----
+// 16-byte global -> shared copies (LDGSTS, L2 only) and their commit groups.
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+    const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait0() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() {
+    asm volatile("cp.async.commit_group;\n\tcp.async.wait_group 0;" ::: "memory");
+}
+
 // ---------------------------------------------------------------- Philox ----
 // Philox4x32-10 (D#10): counter (j lo, j hi, b, 0), key (seed lo, seed hi).
 __device__ __forceinline__ void philox4x32_10(uint32_t c[4], uint32_t k0, uint32_t k1) {
