@@ -42,7 +42,8 @@ def build_lib(force: bool = False, verbose: bool = False) -> str:
         if os.path.getmtime(LIB) >= newest:
             return LIB
     inc, libdir = nccl_dirs()
-    cmd = [NVCC, *NVCC_FLAGS, "-I" + inc, "-o", LIB, *srcs, "-L" + libdir, "-l:libnccl.so.2",
+    extra = os.environ.get("PIC_NVCC_EXTRA", "").split()   # tuning experiments, e.g. -DPIC_X=1
+    cmd = [NVCC, *NVCC_FLAGS, *extra, "-I" + inc, "-o", LIB, *srcs, "-L" + libdir, "-l:libnccl.so.2",
            "-Xlinker", "-rpath," + libdir]
     if verbose:
         print(" ".join(cmd))

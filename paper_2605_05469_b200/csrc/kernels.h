@@ -53,12 +53,18 @@ void launch_sample_write(const Geom& g, PState st, int64_t npg, double k, double
 // Outside [0, L) or the slab -> err_flag[1]; a rank > 65535 -> err_flag[0].
 void launch_key_import(const Geom& g, PState cur, int64_t np, uint32_t* key, uint16_t* rank,
                        uint32_t* count, int* err_flag, cudaStream_t s);
+// Per-destination segments of the migration send buffer: destination r's leavers
+// go to send + 4 * off[r] (64 B each), at most cap[r] of them (nranks <= 8).
+struct SendSegs {
+    int64_t off[8];
+    int cap[8];
+};
 // The push of the sorted state (cell offsets offs): gather E4 through a shared tile
 // per brick, kick v in place, drift; key/rank of residents; leavers (P > 1) packed
-// into send[dest][seg][4] (count send_count[dest]; full segment -> err_flag[2]).
+// into their destination's segment (count send_count[dest]; full segment -> err_flag[2]).
 void launch_push_key(const Geom& g, PState cur, const uint32_t* offs, const double* E4, uint32_t* key,
-                     uint16_t* rank, uint32_t* count, double2* send, uint32_t* send_count, int seg,
-                     int* err_flag, cudaStream_t s);
+                     uint16_t* rank, uint32_t* count, double2* send, uint32_t* send_count,
+                     const SendSegs& segs, int* err_flag, cudaStream_t s);
 // Arrivals: key/rank at extended index n_old + a.
 void launch_key_arrivals(const Geom& g, const double2* recv, int64_t narr, int64_t n_old, uint32_t* key,
                          uint16_t* rank, uint32_t* count, int* err_flag, cudaStream_t s);

@@ -206,9 +206,9 @@ __global__ void __launch_bounds__(kThreads) k_key_import(Geom g, PState cur, int
 // buffer of their destination rank: 64 B = (x', y'), (z', vz'), (vx', vy'),
 // (old global key | old index << 32).
 struct SendBuf {
-    double2* data;        // [P][seg][4]
+    double2* data;        // segment r at data + 4 * segs.off[r]
     uint32_t* count;      // [P]
-    int seg;              // capacity per destination
+    SendSegs segs;
 };
 
 constexpr int kLeaveCap = 256;   // leavers staged per brick before one atomic per destination
@@ -286,8 +286,8 @@ __global__ void __launch_bounds__(kThreads) k_push_key_brick(Geom g, PState cur,
                 atomicAdd(&lcount[dr], 1u);
             } else {                                  // rare: straight to the global buffer
                 const uint32_t slot = atomicAdd(sb.count + dr, 1u);
-                if (slot < (uint32_t)sb.seg) {
-                    double2* d = sb.data + ((int64_t)dr * sb.seg + slot) * 4;
+                if (slot < (uint32_t)sb.segs.cap[dr]) {
+                    double2* d = sb.data + (sb.segs.off[dr] + slot) * 4;
                     d[0] = p0; d[1] = p1; d[2] = p2; d[3] = p3;
                 } else {
                     atomicExch(err + 2, 1);
@@ -312,8 +312,8 @@ __global__ void __launch_bounds__(kThreads) k_push_key_brick(Geom g, PState cur,
         for (int s = t; s < nl; s += kThreads) {
             const int dr = ldst[s];
             const uint32_t slot = lbase[dr] + atomicAdd(&lcount[dr], 1u);
-            if (slot < (uint32_t)sb.seg) {
-                double2* d = sb.data + ((int64_t)dr * sb.seg + slot) * 4;
+            if (slot < (uint32_t)sb.segs.cap[dr]) {
+                double2* d = sb.data + (sb.segs.off[dr] + slot) * 4;
                 d[0] = lbuf[s][0]; d[1] = lbuf[s][1]; d[2] = lbuf[s][2]; d[3] = lbuf[s][3];
             } else {
                 atomicExch(err + 2, 1);
@@ -537,13 +537,15 @@ __device__ __forceinline__ int chunk_end(const uint32_t* soffs, int ca, int cap)
 // their sender); the index rank puts them after the residents of their cell, and
 // a fix-up pass re-sorts the (few) cells holding arrivals by (old global key, old
 // index) -- the order of the single-domain oracle's global stable sort (D#15).
+// Chunk capacity (particles staged per pass; a brick holds ~ppc * 256): 1344 lets
+// three CTAs share an SM, which measured faster than two with whole-brick chunks.
 template <bool MR>
 struct ReorderCap {
-    static constexpr int value = MR ? 1792 : 2048;
+    static constexpr int value = MR ? 1248 : 1344;   // MR: + the slot -> entry array
 };
 
 template <bool PUSH, bool MR>
-__global__ void __launch_bounds__(kThreads, 2) k_reorder_deposit(
+__global__ void __launch_bounds__(kThreads, 3) k_reorder_deposit(
     Geom g, const uint32_t* __restrict__ offs, const uint32_t* __restrict__ perm, PState cur,
     const double2* __restrict__ recv, int64_t n_old, PState nxt, double* __restrict__ rho,
     int* __restrict__ err) {
@@ -753,10 +755,10 @@ void launch_key_import(const Geom& g, PState cur, int64_t np, uint32_t* key, uin
 }
 
 void launch_push_key(const Geom& g, PState cur, const uint32_t* offs, const double* E4, uint32_t* key,
-                     uint16_t* rank, uint32_t* count, double2* send, uint32_t* send_count, int seg,
-                     int* err_flag, cudaStream_t s) {
+                     uint16_t* rank, uint32_t* count, double2* send, uint32_t* send_count,
+                     const SendSegs& segs, int* err_flag, cudaStream_t s) {
     const unsigned nbrick = (unsigned)(((int64_t)g.n * g.n * g.nzl) / kBrick);
-    SendBuf sb{send, send_count, seg};
+    SendBuf sb{send, send_count, segs};
     if (g.P > 1) k_push_key_brick<true><<<nbrick, kThreads, 0, s>>>(g, cur, offs, E4, key, rank, count, sb, err_flag);
     else k_push_key_brick<false><<<nbrick, kThreads, 0, s>>>(g, cur, offs, E4, key, rank, count, sb, err_flag);
 }

@@ -84,7 +84,7 @@ struct pic_ctx {
     double2* send = nullptr;      // [P][seg][4]
     uint32_t* send_count = nullptr;
     uint32_t* recv_count = nullptr;
-    int seg = 0;
+    pic::SendSegs segs{};
     double2* recv = nullptr;      // [recv_cap][4]
     int64_t recv_cap = 0;
     int64_t migrated = 0;         // particles sent by this rank (all steps)
@@ -152,8 +152,8 @@ Geom make_geom(const pic_params* p, int rank, int nranks) {
 }
 
 struct Sizes {
-    int64_t np_nom, np_cap, recv_cap, nkey;
-    int seg;
+    int64_t np_nom, np_cap, recv_cap, nkey, send_len;
+    pic::SendSegs segs;
 };
 
 Sizes sizes(const pic_params* p, const Geom& g) {
@@ -163,14 +163,27 @@ Sizes sizes(const pic_params* p, const Geom& g) {
     if (g.P == 1) {
         s.np_cap = s.np_nom;
         s.recv_cap = 0;
-        s.seg = 0;
+        s.send_len = 0;
     } else {
         // slab imbalance <= alpha (density (1 + alpha cos k z)), plus fluctuations
         s.np_cap = (int64_t)(s.np_nom * (1.0 + p->alpha) * 1.05) + 65536;
-        // a slab of nzl planes loses ~ 2 E[max(v_z, 0)] dt / (nzl h) per step (SURVEY
-        // A.4: 2.5% at 512^3 / 8 ranks); segments sized for 8% of the slab
-        s.seg = (int)std::min<int64_t>(s.np_cap, (int64_t)(0.08 * s.np_cap) + 4096);
-        s.recv_cap = 2 * (int64_t)s.seg;
+        // a slab of nzl planes loses ~ E[max(v_z, 0)] dt / (nzl h) per step to each z
+        // neighbour (1.3% at 512^3 / 8 ranks): neighbour segments hold 4%
+        // of the slab, the others (only reached by |v_z| dt > nzl h) 0.2%; at
+        // 1024^3 / 8 ranks this keeps the rank's workspace at ~144 GiB
+        const int nb = (int)std::min<int64_t>(s.np_cap, (int64_t)(0.04 * s.np_cap) + 4096);
+        const int far = (int)std::min<int64_t>(nb, (int64_t)(0.002 * s.np_cap) + 4096);
+        const int up = (g.rank + 1) % g.P, dn = (g.rank + g.P - 1) % g.P;
+        int64_t off = 0;
+        for (int r = 0; r < g.P; ++r) {
+            const int cap = r == g.rank ? 0 : (r == up || r == dn ? nb : far);
+            s.segs.off[r] = off;
+            s.segs.cap[r] = cap;
+            off += cap;
+        }
+        s.send_len = off;
+        // arrivals: every source's segment towards this rank (its neighbours' are nb)
+        s.recv_cap = g.P == 2 ? nb : 2 * (int64_t)nb + (int64_t)(g.P - 3) * far;
     }
     s.nkey = s.np_cap + s.recv_cap;
     return s;
@@ -211,7 +224,7 @@ size_t carve(pic_ctx* c, const Geom& g, const Sizes& z, char* base) {
     char* pa = take(sizeof(double) * 3 * (size_t)pic::energy_partials(g));
     char* en = take(sizeof(double) * 2 * kMaxEnergySteps);
     char* ef = take(sizeof(int) * 4);
-    char* sd = g.P > 1 ? take(sizeof(double2) * 4 * (size_t)z.seg * g.P) : nullptr;
+    char* sd = g.P > 1 ? take(sizeof(double2) * 4 * (size_t)z.send_len) : nullptr;
     char* sc = take(sizeof(uint32_t) * 2 * 8);
     char* rv = g.P > 1 ? take(sizeof(double2) * 4 * (size_t)z.recv_cap) : nullptr;
     if (c) {
@@ -235,7 +248,7 @@ size_t carve(pic_ctx* c, const Geom& g, const Sizes& z, char* base) {
         c->send = reinterpret_cast<double2*>(sd);
         c->send_count = reinterpret_cast<uint32_t*>(sc);
         c->recv_count = reinterpret_cast<uint32_t*>(sc) + 8;
-        c->seg = z.seg;
+        c->segs = z.segs;
         c->recv = reinterpret_cast<double2*>(rv);
         c->recv_cap = z.recv_cap;
         c->np_cap = z.np_cap;
@@ -421,7 +434,7 @@ pic_status push_sort_deposit(pic_ctx* c, int push) {
         StageScope t(c, PIC_STAGE_PUSH_KEY, 1);
         if (push)
             pic::launch_push_key(g, cur, c->offs, c->E4, c->key, c->rank, c->count, c->send, c->send_count,
-                                 c->seg, c->err_flag, c->stream);
+                                 c->segs, c->err_flag, c->stream);
         else
             pic::launch_key_import(g, cur, c->np, c->key, c->rank, c->count, c->err_flag, c->stream);
     }
@@ -436,7 +449,7 @@ pic_status push_sort_deposit(pic_ctx* c, int push) {
         PIC_CUDA(c, cudaMemcpyAsync(rc, c->recv_count, sizeof(uint32_t) * g.P, cudaMemcpyDeviceToHost, c->stream));
         PIC_CUDA(c, cudaStreamSynchronize(c->stream));
         for (int r = 0; r < g.P; ++r) {
-            if (sc[r] > (uint32_t)c->seg) return fail(c, PIC_EOVERFLOW, "migration send segment overflow");
+            if (sc[r] > (uint32_t)c->segs.cap[r]) return fail(c, PIC_EOVERFLOW, "migration send segment overflow");
             nleave += sc[r];
             narr += rc[r];
         }
@@ -446,7 +459,7 @@ pic_status push_sort_deposit(pic_ctx* c, int push) {
         for (int r = 0; r < g.P; ++r) {
             if (r == g.rank) continue;
             if (sc[r])
-                PIC_NCCL(c, ncclSend(c->send + (size_t)4 * c->seg * r, 8 * (size_t)sc[r], ncclDouble, r,
+                PIC_NCCL(c, ncclSend(c->send + (size_t)4 * c->segs.off[r], 8 * (size_t)sc[r], ncclDouble, r,
                                      c->comm, c->stream));
             if (rc[r])
                 PIC_NCCL(c, ncclRecv(c->recv + 4 * roff, 8 * (size_t)rc[r], ncclDouble, r, c->comm, c->stream));

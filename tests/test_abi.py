@@ -77,6 +77,13 @@ def test_workspace_bytes_model():
     np_ = 8 * 512 ** 3
     assert 106 * np_ <= b <= 106 * np_ + 12 * 2 ** 30
     assert b < 170 * 2 ** 30     # fits one B200 (183 GB)
+    # the north-star run, 1024^3 x 8 ppc on 8 z-slabs: state (1.1 x nominal slab),
+    # neighbour-sized migration segments and slab grids fit every rank's B200
+    p = B.default_params(n=1024, ppc=8, pgrid=(1, 8))
+    np_r = 8 * 1024 ** 3 // 8
+    for r in range(8):
+        b = B.workspace_bytes(p, r, 8)
+        assert 106 * np_r < b < 160 * 2 ** 30
     p = B.default_params(n=16, ppc=8, length=8 * 3.141592653589793)   # kL/2pi = 2
     assert B.workspace_bytes(p) > 0
 
