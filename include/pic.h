@@ -118,6 +118,14 @@ pic_status pic_num_particles(pic_ctx *ctx, int64_t *np);
 /* Particles this rank has sent to other ranks since pic_init (migration, P > 1). */
 pic_status pic_migrated(pic_ctx *ctx, int64_t *migrated);
 
+/* Transport of the P > 1 exchanges: *peer = 1 when every rank's workspace is
+ * mapped (CUDA IPC over NVLink) and the transposes, halo/ghost planes and
+ * migration are stores of the producing kernels into the peers' buffers; 0 for
+ * the NCCL transport (all-to-all, send/recv), used when the mapping is not
+ * possible on every rank or when the environment sets PIC_P2P=0 at pic_init.
+ * Always 0 at P = 1. */
+pic_status pic_peer_transport(pic_ctx *ctx, int32_t *peer);
+
 /* Copy the particle state to host xyzuvw[6][np] in canonical order (sorted by
  * cell key, ties by the current order).  Synchronous. */
 pic_status pic_get_particles(pic_ctx *ctx, double *xyzuvw, int64_t np);

@@ -58,6 +58,7 @@ SYMBOLS = {
     "pic_slab": (C.c_int, [C.POINTER(pic_params), C.c_int32, C.c_int32, C.POINTER(C.c_int32),
                            C.POINTER(C.c_int32), _i64p]),
     "pic_migrated": (C.c_int, [_vp, _i64p]),
+    "pic_peer_transport": (C.c_int, [_vp, C.POINTER(C.c_int32)]),
     "pic_workspace_bytes": (C.c_int, [C.POINTER(pic_params), C.c_int32, C.c_int32, C.POINTER(C.c_size_t)]),
     "pic_init": (C.c_int, [C.POINTER(pic_params), C.c_int32, C.c_int32, _vp, _vp, C.c_size_t, _vp,
                            C.POINTER(_vp)]),
@@ -187,6 +188,12 @@ class Simulation:
         v = C.c_int64()
         _check(lib().pic_migrated(self.ctx, C.byref(v)), self.ctx)
         return v.value
+
+    def peer_transport(self) -> bool:
+        """True when the P > 1 exchanges are peer-memory stores (CUDA IPC over NVLink)."""
+        v = C.c_int32()
+        _check(lib().pic_peer_transport(self.ctx, C.byref(v)), self.ctx)
+        return bool(v.value)
 
     # -- core --------------------------------------------------------------
     def step(self, nsteps: int = 1) -> np.ndarray:

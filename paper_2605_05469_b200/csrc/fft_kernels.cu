@@ -288,11 +288,25 @@ __global__ void __launch_bounds__(kThreads, 3) k_fft_x_fwd(Geom g, double* buf,
     }
 }
 
-// Element (component d, slab plane zl, row y) of a spectral layout: row index * px.
+// Element (component d, slab plane zl, row y) of a local spectral layout: row index * px.
 __device__ __forceinline__ int64_t spec_row(const Geom& g, const SpecLayout& L, int d, int zl, int y) {
     if (!L.packed) return (((int64_t)d * g.nzl + zl) * g.n + y) * g.px;
     const int q = y >> g.mz, yl = y & (g.nzl - 1);   // nyl = n / P = nzl
     return ((((int64_t)q * L.ncomp + d) * g.nzl + zl) * g.nzl + yl) * g.px;
+}
+
+// Row (block q, component d, plane zl, row yl) of a transpose's send side: PACKED
+// into this rank's buffer at block q, or REMOTE into rank q's buffer at block rank.
+__device__ __forceinline__ double2* xpose_row(const Geom& g, const SpecLayout& L, int q, int d, int zl, int yl) {
+    if (L.packed == 2)
+        return L.peer[q] + ((((int64_t)g.rank * L.ncomp + d) * g.nzl + zl) * g.nzl + yl) * g.px;
+    return L.base + ((((int64_t)q * L.ncomp + d) * g.nzl + zl) * g.nzl + yl) * g.px;
+}
+
+// Destination row of element (d, zl, y) of any layout.
+__device__ __forceinline__ double2* dst_row(const Geom& g, const SpecLayout& L, int d, int zl, int y) {
+    if (!L.packed) return L.base + (((int64_t)d * g.nzl + zl) * g.n + y) * g.px;
+    return xpose_row(g, L, y >> g.mz, d, zl, y & (g.nzl - 1));
 }
 
 // ------------------------------------------------------------- y pass ------
@@ -330,10 +344,11 @@ __global__ void __launch_bounds__(kThreads, 2) k_fft_y(Geom g, SpecLayout sl, Sp
         cp_async_wait0();
         __syncthreads();
         auto src = [&](int l, int y) { return l < ncol ? in[y * TW + l] : make_double2(0.0, 0.0); };
-        auto dst = [&](int l, int y, double2 v) { if (l < ncol) dl.base[spec_row(g, dl, d, zl, y) + kx0 + l] = v; };
+        auto dst = [&](int l, int y, double2 v) { if (l < ncol) dst_row(g, dl, d, zl, y)[kx0 + l] = v; };
         auto next = [&]() { if (t + gridDim.x < ntile) prefetch(t + gridDim.x); };
         fft_lines<SIGN, false, LOGN, 1, false>(sm, TW, ls, tw, 0, src, dst, next);
     }
+    if (dl.packed == 2) __threadfence_system();   // peer stores complete before the barrier
 }
 
 // --------------------------------------------------- z pass + multiply -----
@@ -345,7 +360,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_fft_y(Geom g, SpecLayout sl, Sp
 // transpose.
 template <int LOGN>
 __global__ void __launch_bounds__(kThreads, 2) k_fft_z_mul(Geom g, const double2* __restrict__ pencil,
-                                                           double2* __restrict__ out, double scale,
+                                                           SpecLayout out, double scale,
                                                            const double2* __restrict__ tw) {
     extern __shared__ double2 smx[];
     constexpr int n = 1 << LOGN, TW = z_tw(n);
@@ -411,12 +426,13 @@ __global__ void __launch_bounds__(kThreads, 2) k_fft_z_mul(Geom g, const double2
             auto dst = [&](int l, int z, double2 v) {
                 if (l < ncol) {
                     const int q = z >> g.mz, zl = z - (q << g.mz);
-                    out[((((int64_t)q * 3 + d) * g.nzl + zl) * nyl + yl) * g.px + kx0 + l] = v;
+                    xpose_row(g, out, q, d, zl, yl)[kx0 + l] = v;
                 }
             };
             fft_lines<+1, false, LOGN, 1, false>(s2, TW, ls, tw, 0, src, dst);
         }
     }
+    if (out.packed == 2) __threadfence_system();
 }
 
 // ------------------------------------------------------------ x C2R -------
@@ -431,7 +447,7 @@ __device__ __forceinline__ void st_node(double* p, double a, double b, double c)
 
 template <int LOGN>
 __global__ void __launch_bounds__(kThreads, 3) k_fft_x_inv(Geom g, const double2* __restrict__ spec,
-                                                           double* __restrict__ E4,
+                                                           double* __restrict__ E4, double* halo,
                                                            const double2* __restrict__ tw,
                                                            double* __restrict__ partials) {
     extern __shared__ double2 smx[];
@@ -474,9 +490,13 @@ __global__ void __launch_bounds__(kThreads, 3) k_fft_x_inv(Geom g, const double2
             const double2 vx = sm[(3 * rl + 0) * ls + pidx(m)];
             const double2 vy = sm[(3 * rl + 1) * ls + pidx(m)];
             const double2 vz = sm[(3 * rl + 2) * ls + pidx(m)];
-            double* node = E4 + 4 * ((row0 + rl) * g.n + 2 * m);
-            st_node(node, vx.x, vy.x, vz.x);
-            st_node(node + 4, vx.y, vy.y, vz.y);
+            const int64_t nd = 4 * ((row0 + rl) * g.n + 2 * m);
+            st_node(E4 + nd, vx.x, vy.x, vz.x);
+            st_node(E4 + nd + 4, vx.y, vy.y, vz.y);
+            if (halo && row0 + rl < g.n) {      // plane 0 -> the halo plane of the slab below
+                st_node(halo + nd, vx.x, vy.x, vz.x);
+                st_node(halo + nd + 4, vx.y, vy.y, vz.y);
+            }
             e2[0] = fma(vx.x, vx.x, fma(vx.y, vx.y, e2[0]));
             e2[1] = fma(vy.x, vy.x, fma(vy.y, vy.y, e2[1]));
             e2[2] = fma(vz.x, vz.x, fma(vz.y, vz.y, e2[2]));
@@ -494,6 +514,7 @@ __global__ void __launch_bounds__(kThreads, 3) k_fft_x_inv(Geom g, const double2
         for (int w = 0; w < kThreads / 32; ++w) s += red[threadIdx.x][w];
         partials[(int64_t)threadIdx.x * gridDim.x + blockIdx.x] = s;
     }
+    if (halo && g.P > 1) __threadfence_system();
 }
 
 __global__ void k_e4_extract(const double* __restrict__ E4, int64_t nn, int d, double* __restrict__ out) {
@@ -622,7 +643,7 @@ void launch_fft_y(const Geom& g, SpecLayout src, SpecLayout dst, int ncomp, int 
         PIC_YZ_SWITCH(ilog2(g.n), (k_fft_y<-1, K><<<persistent_grid(k_fft_y<-1, K>, smem, nt), kThreads, smem, s>>>(g, src, dst, ncomp, tw)))
 }
 
-void launch_fft_z_mul(const Geom& g, const double2* pencil, double2* out, double scale,
+void launch_fft_z_mul(const Geom& g, const double2* pencil, SpecLayout out, double scale,
                       const double2* tw, cudaStream_t s) {
     const int TW = z_tw(g.n), ntiles = (g.n / 2 + 1 + TW - 1) / TW;
     const size_t smem = sizeof(double2) * (size_t)TW * (g.n + 2 * col_stride(g.n, TW));
@@ -632,11 +653,11 @@ void launch_fft_z_mul(const Geom& g, const double2* pencil, double2* out, double
     PIC_YZ_SWITCH(ilog2(g.n), (k_fft_z_mul<K><<<(unsigned)nt, kThreads, smem, s>>>(g, pencil, out, scale, tw)))
 }
 
-void launch_fft_x_inv(const Geom& g, const double2* spec, double* E4, const double2* tw,
+void launch_fft_x_inv(const Geom& g, const double2* spec, double* E4, double* halo, const double2* tw,
                       double* partials, cudaStream_t s) {
     const size_t smem = x_inv_smem(g);
     const unsigned grid = x_inv_grid(g);
-    PIC_X_SWITCH(ilog2(g.n / 2), (k_fft_x_inv<K><<<grid, kThreads, smem, s>>>(g, spec, E4, tw, partials)))
+    PIC_X_SWITCH(ilog2(g.n / 2), (k_fft_x_inv<K><<<grid, kThreads, smem, s>>>(g, spec, E4, halo, tw, partials)))
 }
 
 void launch_e4_extract(const Geom& g, const double* E4, int d, double* out, cudaStream_t s) {

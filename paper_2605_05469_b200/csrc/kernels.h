@@ -13,10 +13,14 @@ namespace pic {
 // SpecLayout): NORMAL [comp][z_l][y][px]; PACKED [q][comp][z_l][y_l][px] with
 // y = q * nyl + y_l, nyl = n / P -- the all-to-all send/receive order of the
 // transposes (P = 1: identical to NORMAL).
+// REMOTE (P > 1, peer memory): the PACKED layout of the transpose's receiver --
+// block q of this rank's output goes straight into rank q's buffer peer[q] at block
+// `rank` (NVLink stores; no all-to-all).
 struct SpecLayout {
     double2* base;
-    int packed;     // 0: NORMAL, 1: PACKED
+    int packed;     // 0: NORMAL, 1: PACKED, 2: REMOTE
     int ncomp;      // components in the buffer (1 or 3)
+    double2* peer[8];
 };
 int energy_partials(const Geom& g);
 // rows of rho (nzl * n, real, pitch rp doubles) -> R2C in place
@@ -25,12 +29,14 @@ void launch_fft_x_fwd(const Geom& g, double* S0, const double2* tw, cudaStream_t
 void launch_fft_y(const Geom& g, SpecLayout src, SpecLayout dst, int ncomp, int inverse,
                   const double2* tw, cudaStream_t s);
 // z pass on the ky-pencil [z][y_l][px] (all n planes of nyl ky rows): forward z FFT,
-// E^_d = -i k_d rho^/|k|^2 * scale (D#6), 3 inverse z FFTs -> out PACKED
-// [q][d][z_l][y_l][px] (q = z / nzl).  ky0 = rank * nyl.
-void launch_fft_z_mul(const Geom& g, const double2* pencil, double2* out, double scale,
+// E^_d = -i k_d rho^/|k|^2 * scale (D#6), 3 inverse z FFTs -> out PACKED or REMOTE
+// (3 components; q = z / nzl).  ky0 = rank * nyl.
+void launch_fft_z_mul(const Geom& g, const double2* pencil, SpecLayout out, double scale,
                       const double2* tw, cudaStream_t s);
-// 3 components NORMAL (spec + d * nzl*n*px) -> E4 slab planes 0..nzl-1 + energy partials
-void launch_fft_x_inv(const Geom& g, const double2* spec, double* E4, const double2* tw,
+// 3 components NORMAL (spec + d * nzl*n*px) -> E4 slab planes 0..nzl-1 + energy
+// partials; plane 0 is also written to `halo` (the halo plane nzl of the slab below,
+// on its GPU; P = 1: this slab's own), if not null.
+void launch_fft_x_inv(const Geom& g, const double2* spec, double* E4, double* halo, const double2* tw,
                       double* partials, cudaStream_t s);
 void launch_energy_reduce(const Geom& g, const double* partials, double* energies, cudaStream_t s);
 // E4 component d <-> compact [nzl][n][n] doubles (host transfers of the field).
@@ -59,27 +65,52 @@ struct SendSegs {
     int64_t off[8];
     int cap[8];
 };
+// Peer-memory migration (P > 1): leavers go straight into the destination rank's
+// receive buffer peer_recv[r] (64 B records) at slots taken from its arrival counter
+// peer_arr[r] (system-scope atomics over NVLink), capacity recv_cap each.
+struct PeerRecv {
+    double2* peer_recv[8];
+    unsigned long long* peer_arr[8];
+    int64_t recv_cap;
+};
+// Device-side particle counts of a rank (peer-memory migration): n (before the step),
+// arrivals (peers add), leavers of the step, all leavers so far.
+enum { DC_N = 0, DC_ARR = 1, DC_LEAVE = 2, DC_MIGRATED = 3 };
 // The push of the sorted state (cell offsets offs): gather E4 through a shared tile
-// per brick, kick v in place, drift; key/rank of residents; leavers (P > 1) packed
-// into their destination's segment (count send_count[dest]; full segment -> err_flag[2]).
+// per brick, kick v in place, drift; key/rank of residents.  Leavers (P > 1): with
+// peers == nullptr packed into their destination's send segment (count
+// send_count[dest]; full segment -> err_flag[2]); else written into the destination's
+// receive buffer (full -> err_flag[2]) and counted in send_count[dest].
 void launch_push_key(const Geom& g, PState cur, const uint32_t* offs, const double* E4, uint32_t* key,
                      uint16_t* rank, uint32_t* count, double2* send, uint32_t* send_count,
-                     const SendSegs& segs, int* err_flag, cudaStream_t s);
-// Arrivals: key/rank at extended index n_old + a.
+                     const SendSegs& segs, const PeerRecv* peers, int* err_flag, cudaStream_t s);
+// Arrivals: key/rank at extended index n_old + a.  dcnt != null: n_old and the
+// number of arrivals are read on the device (dcnt[DC_N], dcnt[DC_ARR] <= max_arr).
 void launch_key_arrivals(const Geom& g, const double2* recv, int64_t narr, int64_t n_old, uint32_t* key,
-                         uint16_t* rank, uint32_t* count, int* err_flag, cudaStream_t s);
+                         uint16_t* rank, uint32_t* count, int* err_flag,
+                         const unsigned long long* dcnt, cudaStream_t s);
+// dcnt[DC_N] <- n - leavers + arrivals (> np_cap -> err_flag[2]); DC_MIGRATED += leavers;
+// the arrival counter is reset for the next step.
+void launch_counts_update(const Geom& g, unsigned long long* dcnt, const uint32_t* send_count,
+                          int64_t np_cap, int* err_flag, cudaStream_t s);
+void launch_set_u64(unsigned long long* p, unsigned long long v, cudaStream_t s);
 // global Morton keys of the state (export)
 void launch_gkeys(const Geom& g, PState cur, int64_t np, uint32_t* key, cudaStream_t s);
 size_t scan_scratch_bytes(int64_t n);
 void launch_scan(const uint32_t* count, uint32_t* offs, int64_t n, uint32_t* scratch, cudaStream_t s);
+// dcnt != null: the entries are dcnt[DC_N] + dcnt[DC_ARR] (<= np, read on the device).
+// Sorted positions >= cap are dropped and flag err_flag[2].
 void launch_place(const uint32_t* key, const uint16_t* rank, int64_t np, const uint32_t* offs,
-                  uint32_t* perm, cudaStream_t s);
+                  uint32_t* perm, const unsigned long long* dcnt, int64_t cap, int* err_flag, cudaStream_t s);
 // Per brick: stable order inside each cell, gather through perm (entries >= n_old
-// from recv), drift residents (push=1), store sorted into nxt, deposit the CIC
-// weight sums into rho_buf (slab planes 0..nzl, plane nzl = ghost).
+// from recv; dcnt != null: n_old = dcnt[DC_N]), drift residents (push=1), store
+// sorted into nxt, deposit the CIC weight sums into rho_buf planes 0..nzl-1; the
+// charge of node plane nzl goes to `ghost` (plane 0 of the next slab: this buffer at
+// P = 1, the peer's at P > 1 over NVLink, or this buffer's plane nzl for a separate
+// fold), with system-scope atomics on the planes two GPUs share when P > 1.
 void launch_reorder_deposit(const Geom& g, const uint32_t* offs, const uint32_t* perm, PState cur,
-                            const double2* recv, int64_t n_old, PState nxt, int push, double* rho_buf,
-                            int* err_flag, cudaStream_t s);
+                            const double2* recv, int64_t n_old, const unsigned long long* dcnt, PState nxt,
+                            int push, double* rho_buf, double* ghost, int* err_flag, cudaStream_t s);
 void launch_sort_segments(const uint32_t* offs, int64_t ncell, uint32_t* perm, cudaStream_t s);
 void launch_half_kick(const Geom& g, PState cur, int64_t np, const double* E4, cudaStream_t s);
 void launch_add_plane(double* dst, const double* src, int64_t n, cudaStream_t s);

@@ -202,14 +202,30 @@ __global__ void __launch_bounds__(kThreads) k_key_import(Geom g, PState cur, int
 // corners lie in the brick's 9 x 9 x 5 node tile (slab planes bz .. bz + 4, the
 // last possibly the halo), staged in shared memory; the gather reads it with the
 // same weights, corner order and fma chain as the oracle (D#17).  Kick v in place,
-// drift to x' (not stored), key, rank.  Leavers (P > 1) are packed into the send
-// buffer of their destination rank: 64 B = (x', y'), (z', vz'), (vx', vy'),
-// (old global key | old index << 32).
+// drift to x' (not stored), key, rank.  Leavers (P > 1) are 64-B records (x', y'),
+// (z', vz'), (vx', vy'), (old global key | old index << 32), staged per brick in
+// shared memory, then written either into this rank's send segment of their
+// destination (NCCL transport) or, with peer memory, straight into the
+// destination's receive buffer at slots from its arrival counter (one system-scope
+// atomic per brick and destination over NVLink).
 struct SendBuf {
     double2* data;        // segment r at data + 4 * segs.off[r]
-    uint32_t* count;      // [P]
+    uint32_t* count;      // [P] leavers per destination (both transports)
     SendSegs segs;
+    PeerRecv peers;
+    int remote;           // 1: peer-memory transport
 };
+
+// Slot base for n leavers to destination dr; their records go to dst_rec(dr, slot).
+__device__ __forceinline__ uint32_t leave_reserve(const SendBuf& sb, int dr, uint32_t n) {
+    if (!sb.remote) return atomicAdd(sb.count + dr, n);
+    atomicAdd(sb.count + dr, n);
+    return (uint32_t)atomicAdd_system(sb.peers.peer_arr[dr], (unsigned long long)n);
+}
+__device__ __forceinline__ double2* leave_rec(const SendBuf& sb, int dr, uint32_t slot) {
+    if (!sb.remote) return slot < (uint32_t)sb.segs.cap[dr] ? sb.data + (sb.segs.off[dr] + slot) * 4 : nullptr;
+    return slot < (uint64_t)sb.peers.recv_cap ? sb.peers.peer_recv[dr] + (int64_t)slot * 4 : nullptr;
+}
 
 constexpr int kLeaveCap = 256;   // leavers staged per brick before one atomic per destination
 
@@ -285,9 +301,8 @@ __global__ void __launch_bounds__(kThreads) k_push_key_brick(Geom g, PState cur,
                 ldst[s] = (uint8_t)dr;
                 atomicAdd(&lcount[dr], 1u);
             } else {                                  // rare: straight to the global buffer
-                const uint32_t slot = atomicAdd(sb.count + dr, 1u);
-                if (slot < (uint32_t)sb.segs.cap[dr]) {
-                    double2* d = sb.data + (sb.segs.off[dr] + slot) * 4;
+                double2* d = leave_rec(sb, dr, leave_reserve(sb, dr, 1u));
+                if (d) {
                     d[0] = p0; d[1] = p1; d[2] = p2; d[3] = p3;
                 } else {
                     atomicExch(err + 2, 1);
@@ -304,21 +319,21 @@ __global__ void __launch_bounds__(kThreads) k_push_key_brick(Geom g, PState cur,
     if (MR) {      // one global atomic per destination, then the staged payloads
         __syncthreads();
         if (t < g.P) {
-            lbase[t] = lcount[t] ? atomicAdd(sb.count + t, lcount[t]) : 0u;
+            lbase[t] = lcount[t] ? leave_reserve(sb, t, lcount[t]) : 0u;
             lcount[t] = 0;
         }
         __syncthreads();
         const int nl = min((int)nleave, kLeaveCap);
         for (int s = t; s < nl; s += kThreads) {
             const int dr = ldst[s];
-            const uint32_t slot = lbase[dr] + atomicAdd(&lcount[dr], 1u);
-            if (slot < (uint32_t)sb.segs.cap[dr]) {
-                double2* d = sb.data + (sb.segs.off[dr] + slot) * 4;
+            double2* d = leave_rec(sb, dr, lbase[dr] + atomicAdd(&lcount[dr], 1u));
+            if (d) {
                 d[0] = lbuf[s][0]; d[1] = lbuf[s][1]; d[2] = lbuf[s][2]; d[3] = lbuf[s][3];
             } else {
                 atomicExch(err + 2, 1);
             }
         }
+        if (sb.remote && nleave) __threadfence_system();   // peer stores done before the barrier
     }
 }
 
@@ -329,19 +344,40 @@ __global__ void __launch_bounds__(kThreads) k_key_arrivals(Geom g, const double2
                                                            uint32_t* __restrict__ key,
                                                            uint16_t* __restrict__ rank,
                                                            uint32_t* __restrict__ count,
-                                                           int* __restrict__ err) {
-    const int64_t a = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (a >= narr) return;
-    const double2 p0 = recv[4 * a], p1 = recv[4 * a + 1];
-    const double x[3] = {p0.x, p0.y, p1.x};
-    int iz;
-    uint32_t k = key_of(g, x, &iz);
-    if (iz < g.z0 || iz >= g.z0 + g.nzl) { atomicExch(err + 1, 1); k = 0; }
-    key[n_old + a] = k;
-    const uint32_t r = atomicAdd(count + k, 1u);
-    if (r > 0xffffu) atomicExch(err, 1);
-    rank[n_old + a] = (uint16_t)r;
+                                                           int* __restrict__ err,
+                                                           const unsigned long long* __restrict__ dcnt) {
+    if (dcnt) {          // peer-memory transport: counts on the device (narr = capacity)
+        narr = min((int64_t)dcnt[DC_ARR], narr);
+        n_old = (int64_t)dcnt[DC_N];
+    }
+    for (int64_t a = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; a < narr;
+         a += (int64_t)gridDim.x * blockDim.x) {
+        const double2 p0 = recv[4 * a], p1 = recv[4 * a + 1];
+        const double x[3] = {p0.x, p0.y, p1.x};
+        int iz;
+        uint32_t k = key_of(g, x, &iz);
+        if (iz < g.z0 || iz >= g.z0 + g.nzl) { atomicExch(err + 1, 1); k = 0; }
+        key[n_old + a] = k;
+        const uint32_t r = atomicAdd(count + k, 1u);
+        if (r > 0xffffu) atomicExch(err, 1);
+        rank[n_old + a] = (uint16_t)r;
+    }
 }
+
+// Peer-memory transport: n <- n - leavers + arrivals after the step's sort.
+__global__ void k_counts_update(int P, unsigned long long* dcnt, const uint32_t* __restrict__ send_count,
+                                int64_t np_cap, int* err) {
+    unsigned long long leave = 0;
+    for (int r = 0; r < P; ++r) leave += send_count[r];
+    const unsigned long long n = dcnt[DC_N] - leave + dcnt[DC_ARR];
+    if ((int64_t)n > np_cap) atomicExch(err + 2, 1);
+    dcnt[DC_N] = n;
+    dcnt[DC_LEAVE] = leave;
+    dcnt[DC_MIGRATED] += leave;
+    dcnt[DC_ARR] = 0;
+}
+
+__global__ void k_set_u64(unsigned long long* p, unsigned long long v) { *p = v; }
 
 __global__ void __launch_bounds__(kThreads) k_gkeys(Geom g, PState cur, int64_t np,
                                                     uint32_t* __restrict__ key) {
@@ -473,28 +509,37 @@ __global__ void __launch_bounds__(kThreads) k_scan_apply(const uint32_t* __restr
 __global__ void __launch_bounds__(kThreads) k_place(const uint32_t* __restrict__ key,
                                                     const uint16_t* __restrict__ rank, int64_t np,
                                                     const uint32_t* __restrict__ offs,
-                                                    uint32_t* __restrict__ perm) {
+                                                    uint32_t* __restrict__ perm,
+                                                    const unsigned long long* __restrict__ dcnt,
+                                                    int64_t cap, int* __restrict__ err) {
+    // peer-memory transport: the entry count is on the device, and a sorted position
+    // beyond the arrays (a slab over capacity) is dropped and flagged
+    if (dcnt) np = min(np, (int64_t)(dcnt[DC_N] + dcnt[DC_ARR]));
     const int64_t i0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * 4;
     if (i0 >= np) return;
+    auto put = [&](uint32_t k, uint32_t r, int64_t i) {
+        if (k == kNoKey) return;
+        const uint32_t pos = __ldg(offs + k) + r;
+        if (pos < (uint64_t)cap) perm[pos] = (uint32_t)i;
+        else atomicExch(err + 2, 1);
+    };
     if (i0 + 4 <= np) {
         const uint4 k4 = __ldg(reinterpret_cast<const uint4*>(key + i0));
         const uint2 r4 = __ldg(reinterpret_cast<const uint2*>(rank + i0));
-        if (k4.x != kNoKey) perm[__ldg(offs + k4.x) + (r4.x & 0xffffu)] = (uint32_t)i0;
-        if (k4.y != kNoKey) perm[__ldg(offs + k4.y) + (r4.x >> 16)] = (uint32_t)(i0 + 1);
-        if (k4.z != kNoKey) perm[__ldg(offs + k4.z) + (r4.y & 0xffffu)] = (uint32_t)(i0 + 2);
-        if (k4.w != kNoKey) perm[__ldg(offs + k4.w) + (r4.y >> 16)] = (uint32_t)(i0 + 3);
+        put(k4.x, r4.x & 0xffffu, i0);
+        put(k4.y, r4.x >> 16, i0 + 1);
+        put(k4.z, r4.y & 0xffffu, i0 + 2);
+        put(k4.w, r4.y >> 16, i0 + 3);
     } else {
-        for (int64_t i = i0; i < np; ++i) {
-            const uint32_t k = __ldg(key + i);
-            if (k != kNoKey) perm[__ldg(offs + k) + __ldg(rank + i)] = (uint32_t)i;
-        }
+        for (int64_t i = i0; i < np; ++i) put(__ldg(key + i), __ldg(rank + i), i);
     }
 }
 
 // Node tile of a brick: 9 x 9 x 5 nodes, slab planes bz .. bz + 4 (the last one
 // possibly the ghost plane nzl); x and y wrap periodically.
 __device__ __forceinline__ void fold_flush(const Geom& g, double* tile, const double acc[8], int t,
-                                           int bx, int by, int bz, double* __restrict__ rho) {
+                                           int bx, int by, int bz, double* __restrict__ rho,
+                                           double* ghost) {
     const int lx = (int)compact3((uint32_t)t), ly = (int)compact3((uint32_t)t >> 1),
               lz = (int)compact3((uint32_t)t >> 2);
 #pragma unroll
@@ -507,17 +552,30 @@ __device__ __forceinline__ void fold_flush(const Geom& g, double* tile, const do
         const double val = tile[q];
         if (val == 0.0) continue;
         const int nx = q % 9, ny = (q / 9) % 9, nz = q / 81;
-        atomicAdd(rho + gidx(g, (bx + nx) & g.nmask, (by + ny) & g.nmask, bz + nz), val);
+        const int ix = (bx + nx) & g.nmask, iy = (by + ny) & g.nmask, iz = bz + nz;
+        if (iz == g.nzl) {                  // node plane of the next slab (or own plane 0, P = 1)
+            if (g.P > 1) atomicAdd_system(ghost + gidx(g, ix, iy, 0), val);
+            else atomicAdd(ghost + gidx(g, ix, iy, 0), val);
+        } else if (iz == 0 && g.P > 1) {    // shared with the previous slab's ghost adds
+            atomicAdd_system(rho + gidx(g, ix, iy, 0), val);
+        } else {
+            atomicAdd(rho + gidx(g, ix, iy, iz), val);
+        }
     }
 }
 
+// Corner weight sums of one cell's particles: acc[q] += (w_x w_y) w_z, the last
+// product fused into the sum (the charge is compared to a tolerance, D#17 binds
+// only the gather and push).
 __device__ __forceinline__ void cic_acc(const Geom& g, const double x[3], double acc[8]) {
     int ii[3];
     double w[3][2];
     cic_weights(g, x, ii, w);
+    double wxy[4];
 #pragma unroll
-    for (int q = 0; q < 8; ++q)
-        acc[q] = __dadd_rn(acc[q], __dmul_rn(__dmul_rn(w[0][q & 1], w[1][(q >> 1) & 1]), w[2][q >> 2]));
+    for (int q = 0; q < 4; ++q) wxy[q] = __dmul_rn(w[0][q & 1], w[1][q >> 1]);
+#pragma unroll
+    for (int q = 0; q < 8; ++q) acc[q] = __fma_rn(wxy[q & 3], w[2][q >> 2], acc[q]);
 }
 
 // Largest cb with soffs[cb] - soffs[ca] <= cap (uniform across the CTA).
@@ -547,9 +605,10 @@ struct ReorderCap {
 template <bool PUSH, bool MR>
 __global__ void __launch_bounds__(kThreads, 3) k_reorder_deposit(
     Geom g, const uint32_t* __restrict__ offs, const uint32_t* __restrict__ perm, PState cur,
-    const double2* __restrict__ recv, int64_t n_old, PState nxt, double* __restrict__ rho,
-    int* __restrict__ err) {
+    const double2* __restrict__ recv, int64_t n_old, const unsigned long long* __restrict__ dcnt, PState nxt,
+    double* __restrict__ rho, double* ghost, int* __restrict__ err) {
     constexpr int CAP = ReorderCap<MR>::value;
+    if (MR && dcnt) n_old = (int64_t)dcnt[DC_N];
     extern __shared__ double dyn_smem[];
     double2* sp0 = reinterpret_cast<double2*>(dyn_smem);               // [CAP] (x, y)
     double2* sp1 = sp0 + CAP;                                            // [CAP] (z, vz)
@@ -580,6 +639,10 @@ __global__ void __launch_bounds__(kThreads, 3) k_reorder_deposit(
         const int cb = chunk_end(soffs, ca, CAP);
         const uint32_t P0 = soffs[ca];
         const int cnt = (int)(soffs[cb] - P0);
+        if ((int64_t)P0 + cnt > g.cap) {     // slab over capacity (flagged by place)
+            if (t == 0) atomicExch(err + 2, 1);
+            return;
+        }
         for (int p = t; p < cnt; p += kThreads) sperm[p] = __ldg(perm + P0 + p);
         const bool mine = t >= ca && t < cb;
         const int s0 = mine ? (int)(soffs[t] - P0) : 0, s1 = mine ? (int)(soffs[t + 1] - P0) : 0;
@@ -663,7 +726,8 @@ __global__ void __launch_bounds__(kThreads, 3) k_reorder_deposit(
         __syncthreads();
         ca = cb;
     }
-    fold_flush(g, tile, acc, t, bx, by, bz, rho);
+    fold_flush(g, tile, acc, t, bx, by, bz, rho, ghost);
+    if (MR && ghost != rho + (int64_t)g.nzl * g.n * g.rp) __threadfence_system();
 }
 
 __global__ void __launch_bounds__(kThreads) k_half_kick(Geom g, PState cur, int64_t np,
@@ -694,9 +758,13 @@ __global__ void __launch_bounds__(kThreads) k_sort_segments(const uint32_t* __re
     }
 }
 
-__global__ void k_add_plane(double* __restrict__ dst, const double* __restrict__ src, int64_t n) {
+// dst += src over n doubles (n even; src may be a peer's plane: 16-B loads over NVLink)
+__global__ void k_add_plane(double2* __restrict__ dst, const double2* __restrict__ src, int64_t n2) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i < n) dst[i] += src[i];
+    if (i < n2) {
+        const double2 a = dst[i], b = src[i];
+        dst[i] = make_double2(a.x + b.x, a.y + b.y);
+    }
 }
 
 inline unsigned blocks(int64_t n, int t) { return (unsigned)((n + t - 1) / t); }
@@ -756,17 +824,32 @@ void launch_key_import(const Geom& g, PState cur, int64_t np, uint32_t* key, uin
 
 void launch_push_key(const Geom& g, PState cur, const uint32_t* offs, const double* E4, uint32_t* key,
                      uint16_t* rank, uint32_t* count, double2* send, uint32_t* send_count,
-                     const SendSegs& segs, int* err_flag, cudaStream_t s) {
+                     const SendSegs& segs, const PeerRecv* peers, int* err_flag, cudaStream_t s) {
     const unsigned nbrick = (unsigned)(((int64_t)g.n * g.n * g.nzl) / kBrick);
-    SendBuf sb{send, send_count, segs};
+    SendBuf sb{};
+    sb.data = send;
+    sb.count = send_count;
+    sb.segs = segs;
+    if (peers) { sb.peers = *peers; sb.remote = 1; }
     if (g.P > 1) k_push_key_brick<true><<<nbrick, kThreads, 0, s>>>(g, cur, offs, E4, key, rank, count, sb, err_flag);
     else k_push_key_brick<false><<<nbrick, kThreads, 0, s>>>(g, cur, offs, E4, key, rank, count, sb, err_flag);
 }
 
 void launch_key_arrivals(const Geom& g, const double2* recv, int64_t narr, int64_t n_old, uint32_t* key,
-                         uint16_t* rank, uint32_t* count, int* err_flag, cudaStream_t s) {
+                         uint16_t* rank, uint32_t* count, int* err_flag,
+                         const unsigned long long* dcnt, cudaStream_t s) {
     if (narr == 0) return;
-    k_key_arrivals<<<blocks(narr, kThreads), kThreads, 0, s>>>(g, recv, narr, n_old, key, rank, count, err_flag);
+    const unsigned nb = std::min<unsigned>(blocks(narr, kThreads), 148u * 16u);
+    k_key_arrivals<<<nb, kThreads, 0, s>>>(g, recv, narr, n_old, key, rank, count, err_flag, dcnt);
+}
+
+void launch_counts_update(const Geom& g, unsigned long long* dcnt, const uint32_t* send_count,
+                          int64_t np_cap, int* err_flag, cudaStream_t s) {
+    k_counts_update<<<1, 1, 0, s>>>(g.P, dcnt, send_count, np_cap, err_flag);
+}
+
+void launch_set_u64(unsigned long long* p, unsigned long long v, cudaStream_t s) {
+    k_set_u64<<<1, 1, 0, s>>>(p, v);
 }
 
 void launch_gkeys(const Geom& g, PState cur, int64_t np, uint32_t* key, cudaStream_t s) {
@@ -786,25 +869,25 @@ void launch_scan(const uint32_t* count, uint32_t* offs, int64_t n, uint32_t* scr
 }
 
 void launch_place(const uint32_t* key, const uint16_t* rank, int64_t np, const uint32_t* offs,
-                  uint32_t* perm, cudaStream_t s) {
+                  uint32_t* perm, const unsigned long long* dcnt, int64_t cap, int* err_flag, cudaStream_t s) {
     if (np == 0) return;
-    k_place<<<blocks((np + 3) / 4, kThreads), kThreads, 0, s>>>(key, rank, np, offs, perm);
+    k_place<<<blocks((np + 3) / 4, kThreads), kThreads, 0, s>>>(key, rank, np, offs, perm, dcnt, cap, err_flag);
 }
 
 void launch_reorder_deposit(const Geom& g, const uint32_t* offs, const uint32_t* perm, PState cur,
-                            const double2* recv, int64_t n_old, PState nxt, int push, double* rho_buf,
-                            int* err_flag, cudaStream_t s) {
+                            const double2* recv, int64_t n_old, const unsigned long long* dcnt, PState nxt,
+                            int push, double* rho_buf, double* ghost, int* err_flag, cudaStream_t s) {
     const unsigned nbrick = (unsigned)(((int64_t)g.n * g.n * g.nzl) / kBrick);
     if (g.P == 1) {
         if (push)
-            k_reorder_deposit<true, false><<<nbrick, kThreads, reorder_smem<false>(), s>>>(g, offs, perm, cur, recv, n_old, nxt, rho_buf, err_flag);
+            k_reorder_deposit<true, false><<<nbrick, kThreads, reorder_smem<false>(), s>>>(g, offs, perm, cur, recv, n_old, dcnt, nxt, rho_buf, ghost, err_flag);
         else
-            k_reorder_deposit<false, false><<<nbrick, kThreads, reorder_smem<false>(), s>>>(g, offs, perm, cur, recv, n_old, nxt, rho_buf, err_flag);
+            k_reorder_deposit<false, false><<<nbrick, kThreads, reorder_smem<false>(), s>>>(g, offs, perm, cur, recv, n_old, dcnt, nxt, rho_buf, ghost, err_flag);
     } else {
         if (push)
-            k_reorder_deposit<true, true><<<nbrick, kThreads, reorder_smem<true>(), s>>>(g, offs, perm, cur, recv, n_old, nxt, rho_buf, err_flag);
+            k_reorder_deposit<true, true><<<nbrick, kThreads, reorder_smem<true>(), s>>>(g, offs, perm, cur, recv, n_old, dcnt, nxt, rho_buf, ghost, err_flag);
         else
-            k_reorder_deposit<false, true><<<nbrick, kThreads, reorder_smem<true>(), s>>>(g, offs, perm, cur, recv, n_old, nxt, rho_buf, err_flag);
+            k_reorder_deposit<false, true><<<nbrick, kThreads, reorder_smem<true>(), s>>>(g, offs, perm, cur, recv, n_old, dcnt, nxt, rho_buf, ghost, err_flag);
     }
 }
 
@@ -818,7 +901,8 @@ void launch_half_kick(const Geom& g, PState cur, int64_t np, const double* E4, c
 }
 
 void launch_add_plane(double* dst, const double* src, int64_t n, cudaStream_t s) {
-    k_add_plane<<<blocks(n, kThreads), kThreads, 0, s>>>(dst, src, n);
+    k_add_plane<<<blocks(n / 2, kThreads), kThreads, 0, s>>>(reinterpret_cast<double2*>(dst),
+                                                              reinterpret_cast<const double2*>(src), n / 2);
 }
 
 }  // namespace pic

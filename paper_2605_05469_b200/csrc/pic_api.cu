@@ -3,19 +3,26 @@
 // kernels and NCCL calls on the caller's stream; every step of the path runs on
 // the device (kernels.h).  One rank owns a z-slab of nzl = N/P planes (P = 1: the
 // whole box).  One step:
-//   SOLVE   fft_x_fwd -> fft_y_fwd (-> ncclAlltoAll) -> fft_z_mul (-> ncclAlltoAll)
-//           -> fft_y_inv -> fft_x_inv (E4) -> energy (-> ncclAllReduce) -> E halo plane
+//   SOLVE   fft_x_fwd -> fft_y_fwd -> [xpose] -> fft_z_mul -> [xpose] -> fft_y_inv
+//           -> fft_x_inv (E4 + the halo plane of the slab below) -> energy (-> ncclAllReduce)
 //   CLEAR   count = 0, rho = 0
-//   PUSH    push_key (gather + kick + drift + key/rank; leavers -> send buffers)
-//           [P > 1: counts ncclAlltoAll, payload ncclSend/ncclRecv, arrivals keyed]
+//   PUSH    push_key (gather + kick + drift + key/rank; leavers -> their destination)
+//           [P > 1: arrivals keyed]
 //   SORT    scan -> place
-//   SCATTER reorder_deposit (sorted gather + drift + stream out + CIC deposit)
-//           -> ghost plane folded into the next slab's plane 0
+//   SCATTER reorder_deposit (sorted gather + drift + stream out + CIC deposit; the charge
+//           of node plane nzl goes to the next slab's plane 0)
+// P > 1 has two transports.  Peer memory (default): every rank's workspace is mapped
+// (CUDA IPC, NVLink); fft_y_fwd / fft_z_mul store their transpose blocks, fft_x_inv
+// the halo plane, push_key the leavers and reorder_deposit the ghost charge straight
+// into the receiving GPU's buffers, and [xpose] is a stream barrier.  NCCL (PIC_P2P=0
+// or no IPC): [xpose] = ncclAlltoAll, halo/ghost planes by ncclSend/Recv, leavers by
+// counts all-to-all + grouped send/recv.
 #include <nccl.h>
 
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <new>
 #include <vector>
@@ -89,6 +96,19 @@ struct pic_ctx {
     int64_t recv_cap = 0;
     int64_t migrated = 0;         // particles sent by this rank (all steps)
     ncclComm_t comm = nullptr;
+    // peer-memory transport (P > 1): every rank's workspace mapped into this process
+    // (CUDA IPC over NVLink); transposes, halo/ghost planes and migration are stores
+    // and atomics of the producing kernels into the peers' buffers, ordered by
+    // stream barriers (a one-int ncclAllReduce) instead of NCCL data movement
+    bool p2p = false;
+    bool xpose_p2p = false;               // transposes too (PIC_P2P=2; slower, see solve())
+    bool ghost_p2p = false;               // ghost charge by peer atomics (else the NCCL fold)
+    char* ws = nullptr;                   // this rank's workspace base
+    char* peer_ws[8] = {};                // rank r's workspace base in this address space
+    void* ipc_open[8] = {};               // mapped peer allocations (closed by pic_free)
+    int* bar = nullptr;                   // barrier word
+    unsigned long long* dcnt = nullptr;   // device counts (pic::DC_*)
+    bool np_stale = false;                // np / migrated live on the device (dcnt) until the next sync
     // timing
     bool timing = false;
     double stage_ms[PIC_NSTAGES] = {};
@@ -226,6 +246,8 @@ size_t carve(pic_ctx* c, const Geom& g, const Sizes& z, char* base) {
     char* ef = take(sizeof(int) * 4);
     char* sd = g.P > 1 ? take(sizeof(double2) * 4 * (size_t)z.send_len) : nullptr;
     char* sc = take(sizeof(uint32_t) * 2 * 8);
+    char* br = take(sizeof(int) * 4);
+    char* dc = take(sizeof(unsigned long long) * 4);
     char* rv = g.P > 1 ? take(sizeof(double2) * 4 * (size_t)z.recv_cap) : nullptr;
     if (c) {
         c->key = reinterpret_cast<uint32_t*>(k);
@@ -247,6 +269,8 @@ size_t carve(pic_ctx* c, const Geom& g, const Sizes& z, char* base) {
         c->err_flag = reinterpret_cast<int*>(ef);
         c->send = reinterpret_cast<double2*>(sd);
         c->send_count = reinterpret_cast<uint32_t*>(sc);
+        c->bar = reinterpret_cast<int*>(br);
+        c->dcnt = reinterpret_cast<unsigned long long*>(dc);
         c->recv_count = reinterpret_cast<uint32_t*>(sc) + 8;
         c->segs = z.segs;
         c->recv = reinterpret_cast<double2*>(rv);
@@ -343,15 +367,27 @@ PState state(pic_ctx* c, int b) {
 int up(const pic_ctx* c) { return (c->g.rank + 1) % c->g.P; }
 int down(const pic_ctx* c) { return (c->g.rank + c->g.P - 1) % c->g.P; }
 
-// E halo plane nzl = the next slab's plane 0 (P = 1: own plane 0, periodic).
+// The same workspace object on rank r (peer-memory transport; every rank carves an
+// identical layout).
+template <class T>
+T* on_rank(const pic_ctx* c, int r, T* local) {
+    return reinterpret_cast<T*>(c->peer_ws[r] + (reinterpret_cast<char*>(local) - c->ws));
+}
+
+// Stream barrier of all ranks: the peer stores/atomics of the kernels before it are
+// complete (they end with a system fence) when any rank's work after it starts.
+pic_status barrier(pic_ctx* c) {
+    PIC_NCCL(c, ncclAllReduce(c->bar, c->bar, 1, ncclInt, ncclSum, c->comm, c->stream));
+    return PIC_OK;
+}
+
+// E halo plane nzl = the next slab's plane 0 (P = 1 and the peer-memory transport:
+// written by fft_x_inv itself).
 pic_status fill_E_halo(pic_ctx* c) {
     const Geom& g = c->g;
+    if (g.P == 1 || c->p2p) return PIC_OK;
     const size_t pl = (size_t)4 * g.n * g.n;   // doubles per E4 plane
     double* halo = c->E4 + pl * g.nzl;
-    if (g.P == 1) {
-        PIC_CUDA(c, cudaMemcpyAsync(halo, c->E4, sizeof(double) * pl, cudaMemcpyDeviceToDevice, c->stream));
-        return PIC_OK;
-    }
     PIC_NCCL(c, ncclGroupStart());
     PIC_NCCL(c, ncclSend(c->E4, pl, ncclDouble, down(c), c->comm, c->stream));
     PIC_NCCL(c, ncclRecv(halo, pl, ncclDouble, up(c), c->comm, c->stream));
@@ -359,13 +395,51 @@ pic_status fill_E_halo(pic_ctx* c) {
     return PIC_OK;
 }
 
-// rho ghost plane nzl (charge of the next slab's plane 0) folded into its owner.
+// Halo plane of a field written outside the solve (pic_push_injected).
+pic_status refresh_halo(pic_ctx* c) {
+    const Geom& g = c->g;
+    const size_t pl = (size_t)4 * g.n * g.n;
+    double* halo = c->E4 + pl * g.nzl;
+    if (g.P == 1) {
+        PIC_CUDA(c, cudaMemcpyAsync(halo, c->E4, sizeof(double) * pl, cudaMemcpyDeviceToDevice, c->stream));
+        return PIC_OK;
+    }
+    if (!c->p2p) return fill_E_halo(c);
+    PIC_TRY(barrier(c));     // the rank above has written its plane 0
+    PIC_CUDA(c, cudaMemcpyAsync(halo, on_rank(c, up(c), c->E4), sizeof(double) * pl, cudaMemcpyDeviceToDevice,
+                                c->stream));
+    return barrier(c);
+}
+
+// Destination of fft_x_inv's copy of plane 0: the halo plane of the slab below.
+double* halo_dst(pic_ctx* c) {
+    const Geom& g = c->g;
+    double* own = c->E4 + (size_t)4 * g.n * g.n * g.nzl;
+    if (g.P == 1) return own;
+    return c->p2p ? on_rank(c, down(c), own) : nullptr;
+}
+
+// Destination of reorder_deposit's charge on node plane nzl (plane 0 of the next slab).
+double* ghost_dst(pic_ctx* c) {
+    const Geom& g = c->g;
+    if (g.P == 1) return c->rho;
+    if (c->ghost_p2p) return on_rank(c, up(c), c->rho);   // PIC_P2P_GHOST=2 (slower, see below)
+    return c->rho + (int64_t)g.n * g.rp * g.nzl;
+}
+
+// NCCL transport: rho ghost plane nzl (charge of the next slab's plane 0) folded into its owner.
+// Peer transport: after a barrier, each rank pulls the ghost plane of the slab below
+// over NVLink (coalesced 16-B loads) and adds it to its plane 0.  Adding it from the
+// producer with system-scope RED.ADD.F64 inside reorder_deposit (PIC_P2P_GHOST=2) was
+// measured 2.6 ms slower at 512^3 / 2 ranks.
 pic_status fold_rho_ghost(pic_ctx* c) {
     const Geom& g = c->g;
+    if (g.P == 1 || c->ghost_p2p) return PIC_OK;
     const int64_t pl = (int64_t)g.n * g.rp;
     double* ghost = c->rho + pl * g.nzl;
-    if (g.P == 1) {
-        pic::launch_add_plane(c->rho, ghost, pl, c->stream);
+    if (c->p2p) {
+        PIC_TRY(barrier(c));
+        pic::launch_add_plane(c->rho, on_rank(c, down(c), ghost), pl, c->stream);
         PIC_LAUNCHED(c, "add_plane");
         return PIC_OK;
     }
@@ -383,35 +457,51 @@ pic_status fold_rho_ghost(pic_ctx* c) {
 pic_status solve(pic_ctx* c, double scale, int slot) {
     const Geom& g = c->g;
     const size_t unit = (size_t)g.nzl * g.n * g.px;   // complex per slab half spectrum
-    const SpecLayout S0{reinterpret_cast<double2*>(c->rho), 0, 1};
-    const SpecLayout A{c->specA, 1, 1};
-    const SpecLayout D{c->specD, 1, 3};
-    const SpecLayout C{c->specC, 0, 3};
+    const SpecLayout S0{reinterpret_cast<double2*>(c->rho), 0, 1, {}};
+    SpecLayout A{c->specA, 1, 1, {}};          // forward transpose, send side
+    SpecLayout Cz{c->specC, 1, 3, {}};         // return transpose, send side
+    const SpecLayout D{c->specD, 1, 3, {}};
+    const SpecLayout C{c->specC, 0, 3, {}};
+    // The transposes stay NCCL all-to-alls on both transports: storing the 64-byte
+    // column runs of the y/z passes straight into the peers (SpecLayout REMOTE) was
+    // measured slower at P = 2 (z pass 0.95 -> 2.6 ms, more than the all-to-all saves).
+    const bool xpose_p2p = c->p2p && c->xpose_p2p;
+    if (xpose_p2p) {
+        A.packed = Cz.packed = 2;
+        for (int r = 0; r < g.P; ++r) {
+            A.peer[r] = on_rank(c, r, c->specB);
+            Cz.peer[r] = on_rank(c, r, c->specD);
+        }
+    }
     { StageScope t(c, PIC_STAGE_FFT_X_FWD, 1); pic::launch_fft_x_fwd(g, c->rho, c->tw, c->stream); }
     PIC_LAUNCHED(c, "fft_x_fwd");
     { StageScope t(c, PIC_STAGE_FFT_Y_FWD, 1); pic::launch_fft_y(g, S0, A, 1, 0, c->tw, c->stream); }
     PIC_LAUNCHED(c, "fft_y_fwd");
     if (g.P > 1) {
         StageScope t(c, PIC_STAGE_EXCHANGE, 0);
-        PIC_NCCL(c, ncclAlltoAll(c->specA, c->specB, 2 * unit / g.P, ncclDouble, c->comm, c->stream));
+        if (xpose_p2p) PIC_TRY(barrier(c));
+        else PIC_NCCL(c, ncclAlltoAll(c->specA, c->specB, 2 * unit / g.P, ncclDouble, c->comm, c->stream));
     }
-    { StageScope t(c, PIC_STAGE_FFT_Z_MUL, 1); pic::launch_fft_z_mul(g, c->specB, c->specC, scale, c->tw, c->stream); }
+    { StageScope t(c, PIC_STAGE_FFT_Z_MUL, 1); pic::launch_fft_z_mul(g, c->specB, Cz, scale, c->tw, c->stream); }
     PIC_LAUNCHED(c, "fft_z_mul");
     if (g.P > 1) {
         StageScope t(c, PIC_STAGE_EXCHANGE, 0);
-        PIC_NCCL(c, ncclAlltoAll(c->specC, c->specD, 6 * unit / g.P, ncclDouble, c->comm, c->stream));
+        if (xpose_p2p) PIC_TRY(barrier(c));
+        else PIC_NCCL(c, ncclAlltoAll(c->specC, c->specD, 6 * unit / g.P, ncclDouble, c->comm, c->stream));
     }
     { StageScope t(c, PIC_STAGE_FFT_Y_INV, 1); pic::launch_fft_y(g, D, C, 3, 1, c->tw, c->stream); }
     PIC_LAUNCHED(c, "fft_y_inv");
-    { StageScope t(c, PIC_STAGE_FFT_X_INV, 1); pic::launch_fft_x_inv(g, c->specC, c->E4, c->tw, c->partials, c->stream); }
+    {
+        StageScope t(c, PIC_STAGE_FFT_X_INV, 1);
+        pic::launch_fft_x_inv(g, c->specC, c->E4, halo_dst(c), c->tw, c->partials, c->stream);
+    }
     PIC_LAUNCHED(c, "fft_x_inv");
     { StageScope t(c, PIC_STAGE_ENERGY, 1); pic::launch_energy_reduce(g, c->partials, c->energies + 2 * slot, c->stream); }
     PIC_LAUNCHED(c, "energy");
-    {
+    if (g.P > 1) {       // the energy sum is also the barrier for the halo stores
         StageScope t(c, PIC_STAGE_EXCHANGE, 0);
-        if (g.P > 1)
-            PIC_NCCL(c, ncclAllReduce(c->energies + 2 * slot, c->energies + 2 * slot, 2, ncclDouble, ncclSum,
-                                      c->comm, c->stream));
+        PIC_NCCL(c, ncclAllReduce(c->energies + 2 * slot, c->energies + 2 * slot, 2, ncclDouble, ncclSum,
+                                  c->comm, c->stream));
         PIC_TRY(fill_E_halo(c));
     }
     c->last_slot = slot;
@@ -423,25 +513,47 @@ pic_status solve(pic_ctx* c, double scale, int slot) {
 // cell key in cur^1 and their charge is deposited; cur flips.
 pic_status push_sort_deposit(pic_ctx* c, int push) {
     const Geom& g = c->g;
+    const bool peer_mig = push && g.P > 1 && c->p2p;
     {
         StageScope t(c, PIC_STAGE_CLEAR, 0);
         PIC_CUDA(c, cudaMemsetAsync(c->count, 0, sizeof(uint32_t) * (size_t)c->ncell, c->stream));
         PIC_CUDA(c, cudaMemsetAsync(c->rho, 0, sizeof(double) * (size_t)g.n * g.rp * (g.nzl + 1), c->stream));
         if (g.P > 1) PIC_CUDA(c, cudaMemsetAsync(c->send_count, 0, sizeof(uint32_t) * g.P, c->stream));
+        if (g.P > 1 && c->p2p && !push) pic::launch_set_u64(c->dcnt + pic::DC_N, (unsigned long long)c->np, c->stream);
+    }
+    if (g.P > 1 && c->p2p && !push) {   // peers add ghost charge only after everyone cleared
+        StageScope t(c, PIC_STAGE_EXCHANGE, 0);    // (in a step, the barrier after the push orders it)
+        PIC_TRY(barrier(c));
     }
     PState cur = state(c, c->cur), nxt = state(c, c->cur ^ 1);
+    pic::PeerRecv peers{};
+    if (peer_mig) {
+        for (int r = 0; r < g.P; ++r) {
+            peers.peer_recv[r] = on_rank(c, r, c->recv);
+            peers.peer_arr[r] = on_rank(c, r, c->dcnt + pic::DC_ARR);
+        }
+        peers.recv_cap = c->recv_cap;
+    }
     {
         StageScope t(c, PIC_STAGE_PUSH_KEY, 1);
         if (push)
             pic::launch_push_key(g, cur, c->offs, c->E4, c->key, c->rank, c->count, c->send, c->send_count,
-                                 c->segs, c->err_flag, c->stream);
+                                 c->segs, peer_mig ? &peers : nullptr, c->err_flag, c->stream);
         else
             pic::launch_key_import(g, cur, c->np, c->key, c->rank, c->count, c->err_flag, c->stream);
     }
     PIC_LAUNCHED(c, "push_key");
     const int64_t n_old = c->np;
-    int64_t narr = 0, nleave = 0;
-    if (push && g.P > 1) {
+    int64_t narr = 0, nleave = 0, n_bound = n_old;
+    const unsigned long long* dc = nullptr;
+    if (peer_mig) {
+        StageScope t(c, PIC_STAGE_EXCHANGE, 0);
+        PIC_TRY(barrier(c));
+        dc = c->dcnt;
+        pic::launch_key_arrivals(g, c->recv, c->recv_cap, 0, c->key, c->rank, c->count, c->err_flag, dc, c->stream);
+        PIC_LAUNCHED(c, "key_arrivals");
+        n_bound = c->np_cap + c->recv_cap;
+    } else if (push && g.P > 1) {
         StageScope t(c, PIC_STAGE_EXCHANGE, 0);
         PIC_NCCL(c, ncclAlltoAll(c->send_count, c->recv_count, 1, ncclUint32, c->comm, c->stream));
         uint32_t sc[8], rc[8];
@@ -466,33 +578,47 @@ pic_status push_sort_deposit(pic_ctx* c, int push) {
             roff += rc[r];
         }
         PIC_NCCL(c, ncclGroupEnd());
-        pic::launch_key_arrivals(g, c->recv, narr, n_old, c->key, c->rank, c->count, c->err_flag, c->stream);
+        pic::launch_key_arrivals(g, c->recv, narr, n_old, c->key, c->rank, c->count, c->err_flag, nullptr, c->stream);
         PIC_LAUNCHED(c, "key_arrivals");
         c->migrated += nleave;
+        n_bound = n_old + narr;
     }
     const int64_t n_new = n_old - nleave + narr;
-    if (n_new > c->np_cap) return fail(c, PIC_EOVERFLOW, "slab holds more particles than its capacity");
+    if (!peer_mig && n_new > c->np_cap) return fail(c, PIC_EOVERFLOW, "slab holds more particles than its capacity");
     { StageScope t(c, PIC_STAGE_SCAN, 3); pic::launch_scan(c->count, c->offs, c->ncell, c->scan_scratch, c->stream); }
     PIC_LAUNCHED(c, "scan");
-    { StageScope t(c, PIC_STAGE_PLACE, 1); pic::launch_place(c->key, c->rank, n_old + narr, c->offs, c->perm, c->stream); }
+    { StageScope t(c, PIC_STAGE_PLACE, 1); pic::launch_place(c->key, c->rank, n_bound, c->offs, c->perm, dc, c->np_cap, c->err_flag, c->stream); }
     PIC_LAUNCHED(c, "place");
     {
         StageScope t(c, PIC_STAGE_REORDER_DEPOSIT, 1);
-        pic::launch_reorder_deposit(g, c->offs, c->perm, cur, c->recv, n_old, nxt, push, c->rho, c->err_flag,
-                                    c->stream);
+        pic::launch_reorder_deposit(g, c->offs, c->perm, cur, c->recv, n_old, dc, nxt, push, c->rho, ghost_dst(c),
+                                    c->err_flag, c->stream);
     }
     PIC_LAUNCHED(c, "reorder_deposit");
-    {
+    if (peer_mig) {
+        pic::launch_counts_update(g, c->dcnt, c->send_count, c->np_cap, c->err_flag, c->stream);
+        PIC_LAUNCHED(c, "counts_update");
+        c->np_stale = true;
+    }
+    if (g.P > 1) {
         StageScope t(c, PIC_STAGE_EXCHANGE, 0);
-        PIC_TRY(fold_rho_ghost(c));
+        if (c->ghost_p2p) PIC_TRY(barrier(c));      // ghost charge in place before the next solve
+        else PIC_TRY(fold_rho_ghost(c));
     }
     c->cur ^= 1;
-    c->np = n_new;
+    if (!peer_mig) c->np = n_new;
     return PIC_OK;
 }
 
 pic_status sync_check(pic_ctx* c) {
     PIC_CUDA(c, cudaStreamSynchronize(c->stream));
+    if (c->np_stale) {
+        unsigned long long d[4];
+        PIC_CUDA(c, cudaMemcpy(d, c->dcnt, sizeof(d), cudaMemcpyDeviceToHost));
+        c->np = (int64_t)d[pic::DC_N];
+        c->migrated = (int64_t)d[pic::DC_MIGRATED];
+        c->np_stale = false;
+    }
     int flag[3] = {0, 0, 0};
     PIC_CUDA(c, cudaMemcpy(flag, c->err_flag, sizeof(flag), cudaMemcpyDeviceToHost));
     if (flag[1]) {
@@ -527,6 +653,74 @@ pic_status copy_grid_to_host(pic_ctx* c, double* host, const double* src) {
     PIC_CUDA(c, cudaMemcpy2DAsync(host, sizeof(double) * g.n, src, sizeof(double) * g.rp,
                                   sizeof(double) * g.n, (size_t)g.n * g.nzl, cudaMemcpyDeviceToHost,
                                   c->stream));
+    return PIC_OK;
+}
+
+// Map every rank's workspace into this process (CUDA IPC; NVLink peer access) so the
+// transposes, halo/ghost planes and migration become peer stores of the producing
+// kernels.  Every rank must succeed, else all keep the NCCL transport; PIC_P2P=0 in
+// the environment forces the NCCL transport.
+pic_status setup_p2p(pic_ctx* c) {
+    const Geom& g = c->g;
+    c->peer_ws[g.rank] = c->ws;
+    struct Rec {
+        cudaIpcMemHandle_t h;
+        long long off;
+        int ok, pad;
+    };
+    Rec mine{};
+    const char* env = getenv("PIC_P2P");
+    int ok = !(env && env[0] == '0');
+    if (ok) {
+        // the workspace may sit inside a larger allocation of the caller's allocator
+        void* fn = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        typedef int (*GetRange)(unsigned long long*, size_t*, unsigned long long);
+        unsigned long long base = 0;
+        size_t sz = 0;
+        if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &fn, cudaEnableDefault, &q) != cudaSuccess || !fn ||
+            reinterpret_cast<GetRange>(fn)(&base, &sz, (unsigned long long)c->ws) != 0 ||
+            cudaIpcGetMemHandle(&mine.h, reinterpret_cast<void*>(base)) != cudaSuccess) {
+            ok = 0;
+        } else {
+            mine.off = (long long)(c->ws - reinterpret_cast<char*>(base));
+        }
+        cudaGetLastError();
+    }
+    mine.ok = ok;
+    char* dsend = reinterpret_cast<char*>(c->specC);    // free at init
+    char* drecv = dsend + 256;
+    std::vector<Rec> all(g.P);
+    PIC_CUDA(c, cudaMemcpyAsync(dsend, &mine, sizeof(Rec), cudaMemcpyHostToDevice, c->stream));
+    PIC_NCCL(c, ncclAllGather(dsend, drecv, sizeof(Rec), ncclUint8, c->comm, c->stream));
+    PIC_CUDA(c, cudaMemcpyAsync(all.data(), drecv, sizeof(Rec) * g.P, cudaMemcpyDeviceToHost, c->stream));
+    PIC_CUDA(c, cudaStreamSynchronize(c->stream));
+    for (int r = 0; r < g.P; ++r) ok = ok && all[r].ok;
+    for (int r = 0; r < g.P && ok; ++r) {
+        if (r == g.rank) continue;
+        void* ptr = nullptr;
+        if (cudaIpcOpenMemHandle(&ptr, all[r].h, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
+            cudaGetLastError();
+            ok = 0;
+            break;
+        }
+        c->ipc_open[r] = ptr;
+        c->peer_ws[r] = reinterpret_cast<char*>(ptr) + all[r].off;
+    }
+    int* flag = reinterpret_cast<int*>(dsend);
+    PIC_CUDA(c, cudaMemcpyAsync(flag, &ok, sizeof(int), cudaMemcpyHostToDevice, c->stream));
+    PIC_NCCL(c, ncclAllReduce(flag, flag, 1, ncclInt, ncclMin, c->comm, c->stream));
+    int agreed = 0;
+    PIC_CUDA(c, cudaMemcpyAsync(&agreed, flag, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+    PIC_CUDA(c, cudaStreamSynchronize(c->stream));
+    if (!agreed) {
+        for (int r = 0; r < g.P; ++r)
+            if (c->ipc_open[r]) { cudaIpcCloseMemHandle(c->ipc_open[r]); c->ipc_open[r] = nullptr; }
+    }
+    c->p2p = agreed != 0;
+    c->xpose_p2p = c->p2p && env && env[0] == '2';
+    const char* genv = getenv("PIC_P2P_GHOST");
+    c->ghost_p2p = c->p2p && genv && genv[0] == '2';
     return PIC_OK;
 }
 
@@ -609,18 +803,22 @@ pic_status pic_init(const pic_params* p, int32_t rank, int32_t nranks, const uin
     if (!c) return PIC_ENOMEM;
     c->p = *p;
     c->g = g;
+    c->g.cap = z.np_cap;
+    c->ws = reinterpret_cast<char*>(workspace);
     c->np_glob = (int64_t)p->ppc * p->n * p->n * p->n;
     c->ncell = (int64_t)g.n * g.n * g.nzl;
     c->q = -((g.L * g.L) * g.L) / (double)c->np_glob;
     c->deposit_scale = c->q * ((g.inv_h * g.inv_h) * g.inv_h);
     c->stream = reinterpret_cast<cudaStream_t>(cuda_stream);
-    carve(c, g, z, reinterpret_cast<char*>(workspace));
+    carve(c, c->g, z, reinterpret_cast<char*>(workspace));
 
     static bool smem_set = false;
     if (!smem_set) { pic::fft_set_smem_limits(); pic::particles_set_smem_limits(); smem_set = true; }
 
     auto bail = [&](pic_status s) {
         snprintf(g_init_error, sizeof(g_init_error), "%s", c->err);
+        for (int r = 0; r < 8; ++r)
+            if (c->ipc_open[r]) cudaIpcCloseMemHandle(c->ipc_open[r]);
         if (c->comm) ncclCommDestroy(c->comm);
         delete c;
         return s;
@@ -633,6 +831,7 @@ pic_status pic_init(const pic_params* p, int32_t rank, int32_t nranks, const uin
             snprintf(c->err, sizeof(c->err), "ncclCommInitRank: %s", ncclGetErrorString(r));
             return bail(PIC_ENCCL);
         }
+        if ((st = setup_p2p(c)) != PIC_OK) return bail(st);
     }
     // twiddles W_n^m = exp(-2 pi i m / n), m < n
     std::vector<double2> tw(g.n);
@@ -642,6 +841,7 @@ pic_status pic_init(const pic_params* p, int32_t rank, int32_t nranks, const uin
     }
     cudaError_t e = cudaMemcpyAsync(c->tw, tw.data(), sizeof(double2) * tw.size(), cudaMemcpyHostToDevice, c->stream);
     if (e == cudaSuccess) e = cudaMemsetAsync(c->err_flag, 0, sizeof(int) * 4, c->stream);
+    if (e == cudaSuccess) e = cudaMemsetAsync(c->dcnt, 0, sizeof(unsigned long long) * 4, c->stream);
     if (e != cudaSuccess) return bail(fail(c, PIC_ECUDA, "init copies", e));
 
     if (g.P == 1) {
@@ -676,6 +876,10 @@ pic_status pic_init(const pic_params* p, int32_t rank, int32_t nranks, const uin
     }
     if ((st = sync_check(c)) != PIC_OK) return bail(st);
     c->migrated = 0;
+    if (c->p2p) {
+        pic::launch_set_u64(c->dcnt + pic::DC_MIGRATED, 0ull, c->stream);
+        if ((st = sync_check(c)) != PIC_OK) return bail(st);
+    }
     *out = c;
     return PIC_OK;
 }
@@ -720,6 +924,8 @@ void pic_free(pic_ctx* c) {
     if (!c) return;
     if (c->stream) cudaStreamSynchronize(c->stream);
     for (cudaEvent_t e : c->ev_pool) cudaEventDestroy(e);
+    for (int r = 0; r < 8; ++r)
+        if (c->ipc_open[r]) cudaIpcCloseMemHandle(c->ipc_open[r]);
     if (c->comm) ncclCommDestroy(c->comm);
     delete c;
 }
@@ -735,6 +941,12 @@ pic_status pic_num_particles(pic_ctx* c, int64_t* np) {
 pic_status pic_migrated(pic_ctx* c, int64_t* migrated) {
     if (!c || !migrated) return PIC_EINVAL;
     *migrated = c->migrated;
+    return PIC_OK;
+}
+
+pic_status pic_peer_transport(pic_ctx* c, int32_t* peer) {
+    if (!c || !peer) return PIC_EINVAL;
+    *peer = c->p2p ? 1 : 0;
     return PIC_OK;
 }
 
@@ -816,7 +1028,7 @@ pic_status pic_push_injected(pic_ctx* c, const double* E_host) {
                                     cudaMemcpyHostToDevice, c->stream));
     pic::launch_e4_pack(c->g, comp, c->E4, c->stream);
     PIC_LAUNCHED(c, "e4_pack");
-    PIC_TRY(fill_E_halo(c));
+    PIC_TRY(refresh_halo(c));
     PIC_TRY(push_sort_deposit(c, 1));
     c->last_slot = -1;
     return sync_check(c);
@@ -869,8 +1081,9 @@ const char* pic_stage_name(int32_t stage) {
 
 pic_status pic_launches_per_step(pic_ctx* c, int64_t* launches) {
     if (!c || !launches) return PIC_EINVAL;
-    *launches = 6 /* solve */ + 1 /* push_key */ + 3 /* scan */ + 1 /* place */ + 1 /* reorder_deposit */ +
-                1 /* ghost fold */ + (c->g.P > 1 ? 1 : 0) /* arrivals */;
+    // solve 6, push_key 1, scan 3, place 1, reorder_deposit 1; P > 1: arrivals 1, and
+    // the NCCL transport's ghost fold 1 or the peer transport's count update 1
+    *launches = 12 + (c->g.P > 1 ? 2 : 0);
     return PIC_OK;
 }
 

@@ -24,6 +24,7 @@ struct Geom {
     // cell/node planes z0 .. z0 + nzl - 1, nzl = n / P = 2^mz.  Local grids carry
     // one extra plane (nzl): the ghost of the charge, the halo of the field.
     int P, rank, z0, nzl, mz;
+    int64_t cap;    // particle capacity of this rank's arrays (sorted positions beyond it: overflow)
 };
 
 // Index of node (ix, iy, slab plane izl) in a pitched real grid [nzl + 1][n][rp].

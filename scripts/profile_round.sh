@@ -10,6 +10,5 @@ timeout 600 python bench.py --impl reference --steps 2 --warmup 1 > gpurun_out/b
 CMD="python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu-baseline"
 $CMD > gpurun_out/plain512_$R.log 2>&1 && \
 timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -s 20 -c 40 --csv --log-file gpurun_out/launches_512_$R.csv $CMD > gpurun_out/ncu_launch_$R.log 2>&1; echo "ncu launches rc=$?"
-CMD2="python bench.py --n 256 --steps 2 --warmup 3 --no-e2e --no-cpu-baseline"
-$CMD2 > gpurun_out/plain256_$R.log 2>&1 && \
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:"reorder_deposit|push_key_brick" -s 4 -c 2 -o gpurun_out/full256_$R -f $CMD2 > gpurun_out/ncu_full_$R.log 2>&1; echo "ncu full rc=$?"
+timeout 1500 ncu --set full --clock-control none --import-source on -k regex:"reorder_deposit|push_key_brick" -s 4 -c 2 -o gpurun_out/full512_$R -f $CMD > gpurun_out/ncu_full_$R.log 2>&1; echo "ncu full rc=$?"
+timeout 1200 ncu --set full --clock-control none --import-source on -k regex:"fft|place" -s 12 -c 6 -o gpurun_out/full512fft_$R -f $CMD > gpurun_out/ncu_fullfft_$R.log 2>&1; echo "ncu full fft rc=$?"

@@ -35,9 +35,13 @@ with open(f"{P}/{R}_launches_512.csv", "w") as f:
     for d in out:
         w.writerow([d["id"], d["kernel"], d["grid"], d["block"], round(d.get("time_us", 0), 2),
                     int(d.get("dram_read", 0)), int(d.get("dram_write", 0))])
-# per-kernel share of one step (cold-cache, serialised: compare shares)
+# per-kernel share of one step (cold-cache, serialised: compare shares); init-only
+# launches (the push-less re-sort after the half kick) are left out
+INIT_ONLY = ("k_reorder_deposit<0", "k_key_import", "k_sample", "k_half_kick")
 agg = {}
 for d in out:
+    if d["kernel"].startswith(INIT_ONLY):
+        continue
     a = agg.setdefault(d["kernel"], [0, 0.0, 0.0])
     a[0] += 1; a[1] += d.get("time_us", 0); a[2] += d.get("dram_read", 0) + d.get("dram_write", 0)
 tot = sum(a[1] for a in agg.values())
@@ -47,20 +51,29 @@ for k, (n, t, b) in sorted(agg.items(), key=lambda kv: -kv[1][1]):
     lines.append(f"{k},{n},{t:.1f},{t / tot:.3f},{b / n / 1e9:.3f},{b / (t * 1e-6) / 1e9 if t else 0:.0f}")
 open(f"{P}/{R}_launches_512_summary.csv", "w").write("\n".join(lines) + "\n")
 print("\n".join(lines))
-# traffic per launch of the dominant kernel for bench.py
+# 2. full-set captures at the bench config (512^3): summaries, hot source lines, and the
+#    per-launch DRAM traffic bench.py reports for the dominant kernel
 tr = {k: (b / n) for k, (n, t, b) in agg.items()}
-json.dump({"landau3d_512^3x8ppc_fft": {"reorder_deposit": tr.get("k_reorder_deposit", None),
-                                        "push_key_brick": tr.get("k_push_key_brick", None),
-                                        "source": f"profiles/{R}_launches_512.csv"}},
-          open(f"{P}/ncu_traffic.json", "w"), indent=1)
-# 2. full-set summary at 256^3
-if os.path.exists(f"{G}/full256_{R}.ncu-rep"):
-    s = subprocess.run([sys.executable, "scripts/ncu_summary.py", f"{G}/full256_{R}.ncu-rep"], capture_output=True, text=True).stdout
-    s2 = subprocess.run([sys.executable, "scripts/ncu_source.py", f"{G}/full256_{R}.ncu-rep", "reorder_deposit", "15"], capture_output=True, text=True).stdout
-    open(f"{P}/{R}_ncu_full_256.txt", "w").write(f"# {R}: ncu --set full, 256^3 x 8 ppc, step launches of reorder_deposit and push_key_brick\n" + s + "\n# top stall lines (reorder_deposit)\n" + s2)
-for f in (f"bench_{R}.json", f"bench_ref_{R}.json", f"pytest_gpu_{R}.log", f"smoke_{R}.log", f"gpu_{R}.txt"):
-    if os.path.exists(f"{G}/{f}"):
-        txt = open(f"{G}/{f}").read()
-        if f.startswith("pytest"):
-            txt = "\n".join(txt.splitlines()[-15:]) + "\n"
-        open(f"{P}/{R}_{f.replace('_' + R, '')}", "w").write(txt)
+full = {}
+for rep, kernels in ((f"{G}/full512_{R}.ncu-rep", ("reorder_deposit", "push_key_brick")),
+                     (f"{G}/full512fft_{R}.ncu-rep", ("fft_z_mul", "fft_x_inv", "place"))):
+    if not os.path.exists(rep):
+        continue
+    s = subprocess.run([sys.executable, "scripts/ncu_summary.py", rep], capture_output=True, text=True).stdout
+    for m in re.finditer(r"raw (?:void )?(?:unnamed>::)?(k_\w+)[^{]*(\{[^}]*\})", s):
+        d = eval(m.group(2))
+        full.setdefault(m.group(1), (float(d["dram__bytes_read.sum"]) + float(d["dram__bytes_write.sum"])) * 1e9)
+    hot = ""
+    for k in kernels:
+        hot += f"\n# hot source lines: {k}\n" + subprocess.run(
+            [sys.executable, "scripts/ncu_lines.py", rep, k, "14"], capture_output=True, text=True).stdout
+    tag = os.path.basename(rep).replace(".ncu-rep", "").replace(f"_{R}", "")
+    tag = {"full512": f"{R}_ncu_full_512", "full512fft": f"{R}_ncu_full_512_fft_place"}[tag]
+    open(f"{P}/{tag}.txt", "w").write(f"# {R}: ncu --set full --clock-control none, 512^3 x 8 ppc bench step launches\n"
+                                      + s + hot)
+traffic = {"reorder_deposit": full.get("k_reorder_deposit", tr.get("k_reorder_deposit")),
+           "push_key": full.get("k_push_key_brick", tr.get("k_push_key_brick")),
+           "source": f"dram__bytes_read.sum + dram__bytes_write.sum per launch, ncu --set full "
+                     f"(profiles/{R}_ncu_full_512.txt); launch list profiles/{R}_launches_512.csv"}
+json.dump({"landau3d_512^3x8ppc_fft": traffic}, open(f"{P}/ncu_traffic.json", "w"), indent=1)
+print(json.dumps(traffic, indent=1))

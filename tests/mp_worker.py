@@ -49,6 +49,9 @@ def main():
     got = sim.get_particles()
     keys, _ = sim.keys_perm()
     mig = sim.migrated()
+    transport = "peer" if sim.peer_transport() else "nccl"
+    want = os.environ.get("MP_EXPECT_TRANSPORT")
+    assert want is None or want == transport, f"transport {transport}, expected {want}"
     parts = [None] * world
     dist.all_gather_object(parts, (got, keys, mig, ex))
     if rank == 0:
@@ -86,7 +89,8 @@ def main():
         _, rex2, _, _ = O.run(n, L, dt, ref0, 10)
         rel2 = np.max(np.abs(ex2 - rex2) / rex2)
         assert rel2 <= 1e-9, rel2
-        print(f"MP OK P={world} n={n} ppc={ppc} steps={steps} | {msg1} | init: W_x rel {rel2:.1e} counts {counts}",
+        print(f"MP OK P={world} n={n} ppc={ppc} steps={steps} transport={transport} | {msg1} | "
+              f"init: W_x rel {rel2:.1e} counts {counts}",
               flush=True)
     sim.close()
     dist.barrier()

@@ -1,5 +1,7 @@
 """Multi-GPU z-slab decomposition against the single-domain oracle:
-runs tests/mp_worker.py under torchrun on 2 (and 4, when present) GPUs."""
+runs tests/mp_worker.py under torchrun on 2 (and 4, 8 when present) GPUs, with the
+peer-memory transport (the default; the worker asserts it is the one in use) and
+with the NCCL transport (PIC_P2P=0)."""
 import os
 import subprocess
 import sys
@@ -16,13 +18,20 @@ def _ngpus():
     return torch.cuda.device_count()
 
 
+@pytest.mark.parametrize("transport", ["peer", "nccl"])
 @pytest.mark.parametrize("world,n", [(2, 32), (4, 32), (8, 64)])
-def test_slab_decomposition_matches_oracle(world, n):
+def test_slab_decomposition_matches_oracle(world, n, transport):
     if _ngpus() < world:
         pytest.skip(f"needs {world} GPUs")
+    env = dict(os.environ, MP_EXPECT_TRANSPORT=transport)
+    if transport == "nccl":
+        env["PIC_P2P"] = "0"
+    else:
+        env.pop("PIC_P2P", None)
+    port = 29600 + 10 * world + (transport == "nccl")
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
-           "--master-addr", "127.0.0.1", "--master-port", str(29600 + world),
+           "--master-addr", "127.0.0.1", "--master-port", str(port),
            os.path.join(ROOT, "tests", "mp_worker.py"), str(n), "8", "20"]
-    r = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=ROOT)
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=ROOT, env=env)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
-    assert "MP OK" in r.stdout
+    assert "MP OK" in r.stdout and f"transport={transport}" in r.stdout
