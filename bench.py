@@ -40,8 +40,8 @@ ALG_BYTES = {
     "scan": (0, 16),                                 # count read x2, offs + cursor write
     "fft_x_fwd": (0, 8 + 8),
     "fft_y_fwd": (0, 8 + 8),
-    "fft_z_mul": (0, 8 + 24),
-    "fft_y_inv": (0, 24 + 24),
+    "fft_z_mul": (0, 8 + 16),                       # rho^ pencil -> phi^, E^_z
+    "fft_y_inv": (0, 16 + 24),                      # phi^, E^_z -> E_x, E_y, E_z spectra
     "fft_x_inv": (0, 24 + 32),                       # 3 half spectra -> E node records
     "clear": (0, 4 + 8),
 }

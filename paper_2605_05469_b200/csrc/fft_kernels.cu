@@ -313,7 +313,12 @@ __device__ __forceinline__ double2* dst_row(const Geom& g, const SpecLayout& L, 
 // Tile (component d, plane zl, kx tile): lines along y of TW consecutive kx columns
 // (valid columns kx <= n/2).  A tile's input is all in shared memory before its
 // last stage writes, so src and dst may alias.
-template <int SIGN, int LOGN>
+// EMODE (the inverse pass of the field): the input holds phi^ (component 0) and
+// E^_z (component 1), each inverse-z transformed; a phi tile yields two outputs,
+// E_x = -i k_x phi (applied to the output, zero on the k_x Nyquist column) and
+// E_y = -i k_y phi (applied to the input, zero on the k_y Nyquist row; D#6), an
+// E_z tile one.
+template <int SIGN, int LOGN, bool EMODE>
 __global__ void __launch_bounds__(kThreads, 2) k_fft_y(Geom g, SpecLayout sl, SpecLayout dl, int ncomp,
                                                        const double2* __restrict__ tw) {
     extern __shared__ double2 smx[];
@@ -334,6 +339,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_fft_y(Geom g, SpecLayout sl, Sp
         }
         cp_async_commit();
     };
+    const double kf = 6.283185307179586476925286766559 / g.L;
     int64_t t = blockIdx.x;
     if (t < ntile) prefetch(t);
     for (; t < ntile; t += gridDim.x) {
@@ -344,20 +350,42 @@ __global__ void __launch_bounds__(kThreads, 2) k_fft_y(Geom g, SpecLayout sl, Sp
         cp_async_wait0();
         __syncthreads();
         auto src = [&](int l, int y) { return l < ncol ? in[y * TW + l] : make_double2(0.0, 0.0); };
-        auto dst = [&](int l, int y, double2 v) { if (l < ncol) dst_row(g, dl, d, zl, y)[kx0 + l] = v; };
         auto next = [&]() { if (t + gridDim.x < ntile) prefetch(t + gridDim.x); };
-        fft_lines<SIGN, false, LOGN, 1, false>(sm, TW, ls, tw, 0, src, dst, next);
+        if (!EMODE) {
+            auto dst = [&](int l, int y, double2 v) { if (l < ncol) dst_row(g, dl, d, zl, y)[kx0 + l] = v; };
+            fft_lines<SIGN, false, LOGN, 1, false>(sm, TW, ls, tw, 0, src, dst, next);
+        } else if (d == 1) {             // E^_z -> E_z
+            auto dst = [&](int l, int y, double2 v) { if (l < ncol) dst_row(g, dl, 2, zl, y)[kx0 + l] = v; };
+            fft_lines<SIGN, false, LOGN, 1, false>(sm, TW, ls, tw, 0, src, dst, next);
+        } else {                         // phi -> (E_x = -i k_x phi, E_y = -i k_y phi)
+            auto dst0 = [&](int l, int y, double2 v) {
+                if (l < ncol) {
+                    const int kx = kx0 + l;       // half spectrum: k_x >= 0; zero on the Nyquist column
+                    const double k = kx == n / 2 ? 0.0 : kf * (double)kx;
+                    dst_row(g, dl, 0, zl, y)[kx] = make_double2(k * v.y, -k * v.x);
+                }
+            };
+            fft_lines<SIGN, false, LOGN, 1, false>(sm, TW, ls, tw, 0, src, dst0);
+            auto srcy = [&](int l, int ky) {
+                const double2 v = src(l, ky);
+                const double k = ky == n / 2 ? 0.0 : kf * (double)(ky < n / 2 ? ky : ky - n);
+                return make_double2(k * v.y, -k * v.x);     // -i k_y phi
+            };
+            auto dst1 = [&](int l, int y, double2 v) { if (l < ncol) dst_row(g, dl, 1, zl, y)[kx0 + l] = v; };
+            fft_lines<SIGN, false, LOGN, 1, false>(sm, TW, ls, tw, 0, srcy, dst1, next);
+        }
     }
     if (dl.packed == 2) __threadfence_system();   // peer stores complete before the barrier
 }
 
 // --------------------------------------------------- z pass + multiply -----
 // Tile (yl, kx tile) of the ky-pencil [z][yl][px] (all n planes, nyl = n / P rows
-// of ky, ky = rank nyl + yl).  Forward z FFT of rho^ into shared memory, then for
-// d = x, y, z an inverse z FFT whose first stage reads
-// E^_d = -i k_d rho^ / |k|^2 * scale (zero at n = 0 and where n_d = -N/2, D#6)
-// straight from it; stores PACKED [q][d][zl][yl][px] (q = z / nzl) for the return
-// transpose.
+// of ky, ky = rank nyl + yl).  Forward z FFT of rho^ into shared memory, phi^ =
+// rho^ scale / |k|^2 in place (0 at k = 0), then two inverse z FFTs whose first stage
+// reads from it: phi^ itself and E^_z = -i k_z phi^ (zero where n_z = -N/2, D#6); the
+// x and y components' -i k_d is applied in their own passes.  Stores the two
+// components PACKED [q][c][zl][yl][px] (q = z / nzl) for the return transpose (or
+// REMOTE).
 template <int LOGN>
 __global__ void __launch_bounds__(kThreads, 2) k_fft_z_mul(Geom g, const double2* __restrict__ pencil,
                                                            SpecLayout out, double scale,
@@ -410,16 +438,17 @@ __global__ void __launch_bounds__(kThreads, 2) k_fft_z_mul(Geom g, const double2
             r = make_double2(f * r.x, f * r.y);
         }
         __syncthreads();
-        for (int d = 0; d < 3; ++d) {
+        for (int d = 0; d < 2; ++d) {
             auto src = [&](int l, int kz) {
-                const int kx = kx0 + l;
-                const int idx = d == 0 ? kx : (d == 1 ? ky : kz);
-                const int m = idx < half ? idx : idx - n;
                 double2 e = make_double2(0.0, 0.0);
-                if (l < ncol && idx != half) {
+                if (l < ncol) {
                     const double2 r = s1[l * ls + pidx(kz)];
-                    const double kd = kf * (double)m;
-                    e = make_double2(kd * r.y, -kd * r.x);   // E^_d = -i k_d phi^
+                    if (d == 0) {
+                        e = r;                                       // phi^
+                    } else if (kz != half) {
+                        const double kd = kf * (double)(kz < half ? kz : kz - n);
+                        e = make_double2(kd * r.y, -kd * r.x);       // E^_z = -i k_z phi^
+                    }
                 }
                 return e;
             };
@@ -638,9 +667,16 @@ void launch_fft_y(const Geom& g, SpecLayout src, SpecLayout dst, int ncomp, int 
     const size_t smem = sizeof(double2) * (size_t)TW * (g.n + col_stride(g.n, TW));
     const int64_t nt = (int64_t)ncomp * g.nzl * ntiles;
     if (inverse)
-        PIC_YZ_SWITCH(ilog2(g.n), (k_fft_y<+1, K><<<persistent_grid(k_fft_y<+1, K>, smem, nt), kThreads, smem, s>>>(g, src, dst, ncomp, tw)))
+        PIC_YZ_SWITCH(ilog2(g.n), (k_fft_y<+1, K, false><<<persistent_grid(k_fft_y<+1, K, false>, smem, nt), kThreads, smem, s>>>(g, src, dst, ncomp, tw)))
     else
-        PIC_YZ_SWITCH(ilog2(g.n), (k_fft_y<-1, K><<<persistent_grid(k_fft_y<-1, K>, smem, nt), kThreads, smem, s>>>(g, src, dst, ncomp, tw)))
+        PIC_YZ_SWITCH(ilog2(g.n), (k_fft_y<-1, K, false><<<persistent_grid(k_fft_y<-1, K, false>, smem, nt), kThreads, smem, s>>>(g, src, dst, ncomp, tw)))
+}
+
+void launch_fft_y_field(const Geom& g, SpecLayout src, SpecLayout dst, const double2* tw, cudaStream_t s) {
+    const int TW = y_tw(g.n), ntiles = (g.n / 2 + 1 + TW - 1) / TW;
+    const size_t smem = sizeof(double2) * (size_t)TW * (g.n + col_stride(g.n, TW));
+    const int64_t nt = (int64_t)2 * g.nzl * ntiles;
+    PIC_YZ_SWITCH(ilog2(g.n), (k_fft_y<+1, K, true><<<persistent_grid(k_fft_y<+1, K, true>, smem, nt), kThreads, smem, s>>>(g, src, dst, 2, tw)))
 }
 
 void launch_fft_z_mul(const Geom& g, const double2* pencil, SpecLayout out, double scale,
@@ -682,8 +718,9 @@ void fft_set_smem_limits() {
                           cudaFuncSetAttribute(k_fft_x_inv<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, big)))
     }
     for (int lg = 4; lg <= 10; ++lg) {
-        PIC_YZ_SWITCH(lg, (cudaFuncSetAttribute(k_fft_y<-1, K>, cudaFuncAttributeMaxDynamicSharedMemorySize, big),
-                           cudaFuncSetAttribute(k_fft_y<+1, K>, cudaFuncAttributeMaxDynamicSharedMemorySize, big),
+        PIC_YZ_SWITCH(lg, (cudaFuncSetAttribute(k_fft_y<-1, K, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, big),
+                           cudaFuncSetAttribute(k_fft_y<+1, K, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, big),
+                           cudaFuncSetAttribute(k_fft_y<+1, K, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, big),
                            cudaFuncSetAttribute(k_fft_z_mul<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, big)))
     }
 }

@@ -19,8 +19,8 @@ namespace pic {
 struct SpecLayout {
     double2* base;
     int packed;     // 0: NORMAL, 1: PACKED, 2: REMOTE
-    int ncomp;      // components in the buffer (1 or 3)
-    double2* peer[8];
+    int ncomp;      // components in the buffer (1, 2 or 3)
+    double2* const* peer;   // REMOTE: device array [P] of the receivers' buffers
 };
 int energy_partials(const Geom& g);
 // rows of rho (nzl * n, real, pitch rp doubles) -> R2C in place
@@ -28,9 +28,12 @@ void launch_fft_x_fwd(const Geom& g, double* S0, const double2* tw, cudaStream_t
 // y FFT of component(s) d < ncomp of src -> dst (may alias src with the same layout)
 void launch_fft_y(const Geom& g, SpecLayout src, SpecLayout dst, int ncomp, int inverse,
                   const double2* tw, cudaStream_t s);
+// Inverse y pass of the field: src (PACKED, 2 components: phi^, E^_z after the inverse
+// z pass) -> dst NORMAL 3 components: E_x = -i k_x phi, E_y = -i k_y phi, E_z.
+void launch_fft_y_field(const Geom& g, SpecLayout src, SpecLayout dst, const double2* tw, cudaStream_t s);
 // z pass on the ky-pencil [z][y_l][px] (all n planes of nyl ky rows): forward z FFT,
-// E^_d = -i k_d rho^/|k|^2 * scale (D#6), 3 inverse z FFTs -> out PACKED or REMOTE
-// (3 components; q = z / nzl).  ky0 = rank * nyl.
+// phi^ = rho^ scale / |k|^2, 2 inverse z FFTs (phi^, E^_z = -i k_z phi^, D#6) -> out
+// PACKED or REMOTE (2 components; q = z / nzl).  ky0 = rank * nyl.
 void launch_fft_z_mul(const Geom& g, const double2* pencil, SpecLayout out, double scale,
                       const double2* tw, cudaStream_t s);
 // 3 components NORMAL (spec + d * nzl*n*px) -> E4 slab planes 0..nzl-1 + energy

@@ -103,6 +103,7 @@ struct pic_ctx {
     bool p2p = false;
     bool xpose_p2p = false;               // transposes too (PIC_P2P=2; slower, see solve())
     bool ghost_p2p = false;               // ghost charge by peer atomics (else the NCCL fold)
+    double2** peer_tab = nullptr;         // device [2][8]: every rank's specB, specD
     char* ws = nullptr;                   // this rank's workspace base
     char* peer_ws[8] = {};                // rank r's workspace base in this address space
     void* ipc_open[8] = {};               // mapped peer allocations (closed by pic_free)
@@ -237,7 +238,7 @@ size_t carve(pic_ctx* c, const Geom& g, const Sizes& z, char* base) {
     char* sA = g.P > 1 ? take(unit) : nullptr;
     char* sB = g.P > 1 ? take(unit) : nullptr;
     char* sC = take(3 * unit);
-    char* sD = g.P > 1 ? take(3 * unit) : nullptr;
+    char* sD = g.P > 1 ? take(2 * unit) : nullptr;
     char* e4 = take(sizeof(double) * 4 * (size_t)g.n * g.n * (g.nzl + 1));
     char* gh = g.P > 1 ? take(plane) : nullptr;
     char* tw = take(sizeof(double2) * (size_t)g.n);
@@ -247,6 +248,7 @@ size_t carve(pic_ctx* c, const Geom& g, const Sizes& z, char* base) {
     char* sd = g.P > 1 ? take(sizeof(double2) * 4 * (size_t)z.send_len) : nullptr;
     char* sc = take(sizeof(uint32_t) * 2 * 8);
     char* br = take(sizeof(int) * 4);
+    char* pt = take(sizeof(double2*) * 16);
     char* dc = take(sizeof(unsigned long long) * 4);
     char* rv = g.P > 1 ? take(sizeof(double2) * 4 * (size_t)z.recv_cap) : nullptr;
     if (c) {
@@ -260,7 +262,9 @@ size_t carve(pic_ctx* c, const Geom& g, const Sizes& z, char* base) {
         c->specA = g.P > 1 ? reinterpret_cast<double2*>(sA) : reinterpret_cast<double2*>(rh);
         c->specB = g.P > 1 ? reinterpret_cast<double2*>(sB) : reinterpret_cast<double2*>(rh);
         c->specC = reinterpret_cast<double2*>(sC);
-        c->specD = g.P > 1 ? reinterpret_cast<double2*>(sD) : reinterpret_cast<double2*>(sC);
+        // P = 1: the z pass's two components go to units 1-2 of specC; the field y pass
+        // reads each tile whole before writing units 0-2 over the same footprint
+        c->specD = reinterpret_cast<double2*>(g.P > 1 ? sD : sC + unit);
         c->E4 = reinterpret_cast<double*>(e4);
         c->ghost = reinterpret_cast<double*>(gh);
         c->tw = reinterpret_cast<double2*>(tw);
@@ -270,6 +274,7 @@ size_t carve(pic_ctx* c, const Geom& g, const Sizes& z, char* base) {
         c->send = reinterpret_cast<double2*>(sd);
         c->send_count = reinterpret_cast<uint32_t*>(sc);
         c->bar = reinterpret_cast<int*>(br);
+        c->peer_tab = reinterpret_cast<double2**>(pt);
         c->dcnt = reinterpret_cast<unsigned long long*>(dc);
         c->recv_count = reinterpret_cast<uint32_t*>(sc) + 8;
         c->segs = z.segs;
@@ -457,21 +462,19 @@ pic_status fold_rho_ghost(pic_ctx* c) {
 pic_status solve(pic_ctx* c, double scale, int slot) {
     const Geom& g = c->g;
     const size_t unit = (size_t)g.nzl * g.n * g.px;   // complex per slab half spectrum
-    const SpecLayout S0{reinterpret_cast<double2*>(c->rho), 0, 1, {}};
-    SpecLayout A{c->specA, 1, 1, {}};          // forward transpose, send side
-    SpecLayout Cz{c->specC, 1, 3, {}};         // return transpose, send side
-    const SpecLayout D{c->specD, 1, 3, {}};
-    const SpecLayout C{c->specC, 0, 3, {}};
+    const SpecLayout S0{reinterpret_cast<double2*>(c->rho), 0, 1, nullptr};
+    SpecLayout A{c->specA, 1, 1, nullptr};          // forward transpose, send side
+    SpecLayout Cz{g.P > 1 ? c->specC : c->specD, 1, 2, nullptr};   // return transpose, send side
+    const SpecLayout D{c->specD, 1, 2, nullptr};
+    const SpecLayout C{c->specC, 0, 3, nullptr};
     // The transposes stay NCCL all-to-alls on both transports: storing the 64-byte
     // column runs of the y/z passes straight into the peers (SpecLayout REMOTE) was
     // measured slower at P = 2 (z pass 0.95 -> 2.6 ms, more than the all-to-all saves).
     const bool xpose_p2p = c->p2p && c->xpose_p2p;
     if (xpose_p2p) {
         A.packed = Cz.packed = 2;
-        for (int r = 0; r < g.P; ++r) {
-            A.peer[r] = on_rank(c, r, c->specB);
-            Cz.peer[r] = on_rank(c, r, c->specD);
-        }
+        A.peer = c->peer_tab;
+        Cz.peer = c->peer_tab + 8;
     }
     { StageScope t(c, PIC_STAGE_FFT_X_FWD, 1); pic::launch_fft_x_fwd(g, c->rho, c->tw, c->stream); }
     PIC_LAUNCHED(c, "fft_x_fwd");
@@ -487,9 +490,9 @@ pic_status solve(pic_ctx* c, double scale, int slot) {
     if (g.P > 1) {
         StageScope t(c, PIC_STAGE_EXCHANGE, 0);
         if (xpose_p2p) PIC_TRY(barrier(c));
-        else PIC_NCCL(c, ncclAlltoAll(c->specC, c->specD, 6 * unit / g.P, ncclDouble, c->comm, c->stream));
+        else PIC_NCCL(c, ncclAlltoAll(c->specC, c->specD, 4 * unit / g.P, ncclDouble, c->comm, c->stream));
     }
-    { StageScope t(c, PIC_STAGE_FFT_Y_INV, 1); pic::launch_fft_y(g, D, C, 3, 1, c->tw, c->stream); }
+    { StageScope t(c, PIC_STAGE_FFT_Y_INV, 1); pic::launch_fft_y_field(g, D, C, c->tw, c->stream); }
     PIC_LAUNCHED(c, "fft_y_inv");
     {
         StageScope t(c, PIC_STAGE_FFT_X_INV, 1);
@@ -719,6 +722,14 @@ pic_status setup_p2p(pic_ctx* c) {
     }
     c->p2p = agreed != 0;
     c->xpose_p2p = c->p2p && env && env[0] == '2';
+    if (c->p2p) {
+        double2* tab[16] = {};
+        for (int r = 0; r < g.P; ++r) {
+            tab[r] = on_rank(c, r, c->specB);
+            tab[8 + r] = on_rank(c, r, c->specD);
+        }
+        PIC_CUDA(c, cudaMemcpy(c->peer_tab, tab, sizeof(tab), cudaMemcpyHostToDevice));
+    }
     const char* genv = getenv("PIC_P2P_GHOST");
     c->ghost_p2p = c->p2p && genv && genv[0] == '2';
     return PIC_OK;
