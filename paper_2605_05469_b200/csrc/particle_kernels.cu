@@ -609,6 +609,7 @@ __global__ void __launch_bounds__(kThreads, 3) k_reorder_deposit(
     double* __restrict__ rho, double* ghost, int* __restrict__ err) {
     constexpr int CAP = ReorderCap<MR>::value;
     if (MR && dcnt) n_old = (int64_t)dcnt[DC_N];
+
     extern __shared__ double dyn_smem[];
     double2* sp0 = reinterpret_cast<double2*>(dyn_smem);               // [CAP] (x, y)
     double2* sp1 = sp0 + CAP;                                            // [CAP] (z, vz)
@@ -643,7 +644,7 @@ __global__ void __launch_bounds__(kThreads, 3) k_reorder_deposit(
             if (t == 0) atomicExch(err + 2, 1);
             return;
         }
-        for (int p = t; p < cnt; p += kThreads) sperm[p] = __ldg(perm + P0 + p);
+        for (int p = t; p < cnt; p += kThreads) sperm[p] = __ldcs(perm + P0 + p);   // read once
         const bool mine = t >= ca && t < cb;
         const int s0 = mine ? (int)(soffs[t] - P0) : 0, s1 = mine ? (int)(soffs[t + 1] - P0) : 0;
         for (int p = s0; p < s1; ++p) scell[p] = (uint8_t)t;
@@ -713,9 +714,9 @@ __global__ void __launch_bounds__(kThreads, 3) k_reorder_deposit(
                 sp1[p] = b;
             }
             const int64_t o = (int64_t)P0 + p;
-            nxt.p[0][o] = a;
-            nxt.p[1][o] = b;
-            nxt.p[2][o] = e;
+            __stcs(nxt.p[0] + o, a);      // write-once: evict first, keep L2 for the gather
+            __stcs(nxt.p[1] + o, b);
+            __stcs(nxt.p[2] + o, e);
         }
         __syncthreads();
         // CIC charge: thread per cell, its particles in stable order from shared memory
