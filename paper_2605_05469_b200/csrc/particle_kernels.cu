@@ -286,8 +286,7 @@ __global__ void __launch_bounds__(kThreads) k_push_key_brick(Geom g, PState cur,
         v[1] = __fma_rn(g.qm_dt, e1, v[1]);
         v[2] = __fma_rn(g.qm_dt, e2, v[2]);
         drift(g, x, v);
-        cur.p[1][i] = make_double2(z0, v[2]);    // kicked velocity in place: (x_n, v_{n+1/2})
-        cur.p[2][i] = make_double2(v[0], v[1]);
+        st_zv(cur.zv + 2 * i, make_double2(z0, v[2]), make_double2(v[0], v[1]));   // kicked v in place
         int iz;
         const uint32_t k = key_of(g, x, &iz);
         if (MR && (iz < g.z0 || iz >= g.z0 + g.nzl)) {   // leaver: staged, sent below
@@ -658,9 +657,9 @@ __global__ void __launch_bounds__(kThreads, 3) k_reorder_deposit(
             for (int q = q0; q < q1; ++q) r += sperm[q] < j;
             const int o = q0 + r;
             if (MR) sE[o] = j;
-            const double2* src0 = cur.p[0] + j;
-            const double2* src1 = cur.p[1] + j;
-            const double2* src2 = cur.p[2] + j;
+            const double2* src0 = cur.xy + j;
+            const double2* src1 = cur.zv + 2 * (int64_t)j;
+            const double2* src2 = src1 + 1;
             if (MR && j >= n_old) {
                 const double2* d = recv + 4 * ((int64_t)j - n_old);
                 src0 = d; src1 = d + 1; src2 = d + 2;
@@ -714,9 +713,8 @@ __global__ void __launch_bounds__(kThreads, 3) k_reorder_deposit(
                 sp1[p] = b;
             }
             const int64_t o = (int64_t)P0 + p;
-            __stcs(nxt.p[0] + o, a);      // write-once: evict first, keep L2 for the gather
-            __stcs(nxt.p[1] + o, b);
-            __stcs(nxt.p[2] + o, e);
+            __stcs(nxt.xy + o, a);        // write-once: evict first, keep L2 for the gather
+            st_zv_cs(nxt.zv + 2 * o, b, e);
         }
         __syncthreads();
         // CIC charge: thread per cell, its particles in stable order from shared memory

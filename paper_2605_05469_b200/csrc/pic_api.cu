@@ -67,7 +67,7 @@ struct pic_ctx {
     cudaStream_t stream = nullptr;
     bool poisoned = false;
     char err[512] = "";
-    double2* part[2][3] = {};     // double-buffered pair streams (pic_device.cuh)
+    double2* part[2][2] = {};     // double-buffered particle streams XY, ZV (pic_device.cuh)
     int cur = 0;
     uint32_t* key = nullptr;      // [np_cap + recv_cap] (extended index space)
     uint16_t* rank = nullptr;
@@ -222,11 +222,14 @@ size_t carve(pic_ctx* c, const Geom& g, const Sizes& z, char* base) {
     const int64_t ncell = (int64_t)g.n * g.n * g.nzl;
     const size_t plane = sizeof(double) * (size_t)g.n * g.rp;          // one pitched real plane
     const size_t unit = sizeof(double2) * (size_t)g.nzl * g.n * g.px;   // one slab half spectrum
-    for (int b = 0; b < 2; ++b)
-        for (int a = 0; a < 3; ++a) {
-            char* ptr = take(sizeof(double2) * (size_t)z.np_cap);
-            if (c) c->part[b][a] = reinterpret_cast<double2*>(ptr);
+    for (int b = 0; b < 2; ++b) {      // XY then ZV back to back (48 B x cap: also the SoA scratch)
+        char* xy = take(sizeof(double2) * (size_t)z.np_cap);
+        char* zv = take(2 * sizeof(double2) * (size_t)z.np_cap);
+        if (c) {
+            c->part[b][0] = reinterpret_cast<double2*>(xy);
+            c->part[b][1] = reinterpret_cast<double2*>(zv);
         }
+    }
     const int64_t nblk = g.P > 1 ? pic::sample_blocks(z.np_nom * g.P) : 0;   // init scratch
     char* k = take(sizeof(uint32_t) * (size_t)std::max(z.nkey, nblk));
     char* rk = take(sizeof(uint16_t) * (size_t)z.nkey);
@@ -365,7 +368,8 @@ void collect_timings(pic_ctx* c) {
 // ------------------------------------------------------------ pipeline -----
 PState state(pic_ctx* c, int b) {
     PState s;
-    for (int a = 0; a < 3; ++a) s.p[a] = c->part[b][a];
+    s.xy = c->part[b][0];
+    s.zv = c->part[b][1];
     return s;
 }
 

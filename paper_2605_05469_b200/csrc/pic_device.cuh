@@ -201,24 +201,39 @@ __device__ __forceinline__ void gather_push(const Geom& g, const double* __restr
 }
 
 // ------------------------------------------------------- particle layout ----
-// Three streams of 128-bit pairs per particle i: P0 = (x, y), P1 = (z, v_z),
-// P2 = (v_x, v_y).  A scattered gather of one particle touches 3 sectors (6 for
-// plain SoA); the kick rewrites P1 and P2 only.
+// Two streams per particle i: XY[i] = (x, y) (16 B) and ZV[i] = (z, v_z, v_x, v_y)
+// (32 B, one sector; as double2: ZV2[2i] = (z, v_z), ZV2[2i+1] = (v_x, v_y)).  A
+// scattered gather of one particle touches 2 sectors and uses 48 of their 64 bytes
+// (three 16-B streams: 3 sectors, 48 of 96); the kick rewrites exactly the ZV record.
 struct PState {
-    double2* p[3];
+    double2* xy;    // [cap]
+    double2* zv;    // [2 cap]
 };
 
+__device__ __forceinline__ void ld_zv(const double2* p, double2& b, double2& c) {
+    asm("ld.global.nc.v4.f64 {%0, %1, %2, %3}, [%4];" : "=d"(b.x), "=d"(b.y), "=d"(c.x), "=d"(c.y) : "l"(p));
+}
+__device__ __forceinline__ void st_zv(double2* p, double2 b, double2 c) {
+    asm volatile("st.global.v4.f64 [%0], {%1, %2, %3, %4};" ::"l"(p), "d"(b.x), "d"(b.y), "d"(c.x), "d"(c.y)
+                 : "memory");
+}
+__device__ __forceinline__ void st_zv_cs(double2* p, double2 b, double2 c) {   // streaming (evict first)
+    asm volatile("st.global.cs.v4.f64 [%0], {%1, %2, %3, %4};" ::"l"(p), "d"(b.x), "d"(b.y), "d"(c.x), "d"(c.y)
+                 : "memory");
+}
+
 __device__ __forceinline__ void load_particle(const PState& s, int64_t i, double x[3], double v[3]) {
-    const double2 a = __ldg(s.p[0] + i), b = __ldg(s.p[1] + i), c = __ldg(s.p[2] + i);
+    const double2 a = __ldg(s.xy + i);
+    double2 b, c;
+    ld_zv(s.zv + 2 * i, b, c);
     x[0] = a.x; x[1] = a.y; x[2] = b.x;
     v[0] = c.x; v[1] = c.y; v[2] = b.y;
 }
 
 __device__ __forceinline__ void store_particle(const PState& s, int64_t i, const double x[3],
                                                const double v[3]) {
-    s.p[0][i] = make_double2(x[0], x[1]);
-    s.p[1][i] = make_double2(x[2], v[2]);
-    s.p[2][i] = make_double2(v[0], v[1]);
+    s.xy[i] = make_double2(x[0], x[1]);
+    st_zv(s.zv + 2 * i, make_double2(x[2], v[2]), make_double2(v[0], v[1]));
 }
 
 // -------------------------------------------------------------- cp.async ----
