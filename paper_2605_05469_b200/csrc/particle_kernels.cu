@@ -227,10 +227,10 @@ __device__ __forceinline__ double2* leave_rec(const SendBuf& sb, int dr, uint32_
     return slot < (uint64_t)sb.peers.recv_cap ? sb.peers.peer_recv[dr] + (int64_t)slot * 4 : nullptr;
 }
 
-constexpr int kLeaveCap = 256;   // leavers staged per brick before one atomic per destination
+constexpr int kLeaveCap = 128;   // leavers staged per brick before one atomic per destination
 
 template <bool MR>
-__global__ void __launch_bounds__(kThreads) k_push_key_brick(Geom g, PState cur,
+__global__ void __launch_bounds__(kThreads, MR ? 3 : 4) k_push_key_brick(Geom g, PState cur,
                                                              const uint32_t* __restrict__ offs,
                                                              const double* __restrict__ E4,
                                                              uint32_t* __restrict__ key,
@@ -262,9 +262,7 @@ __global__ void __launch_bounds__(kThreads) k_push_key_brick(Geom g, PState cur,
         double x[3] = {xn[0], xn[1], xn[2]}, v[3] = {vn[0], vn[1], vn[2]};
         // next particle's loads in flight while this one waits on its count atomic
         if (i + kThreads < P1) load_particle(cur, i + kThreads, xn, vn);
-        const double z0 = x[2];
-        uint32_t oldg = 0;
-        if (MR) oldg = gkey_of(g, x);
+        const double x0 = x[0], y0 = x[1], z0 = x[2];
         int ii[3];
         double w[3][2];
         cic_weights(g, x, ii, w);
@@ -291,6 +289,8 @@ __global__ void __launch_bounds__(kThreads) k_push_key_brick(Geom g, PState cur,
         const uint32_t k = key_of(g, x, &iz);
         if (MR && (iz < g.z0 || iz >= g.z0 + g.nzl)) {   // leaver: staged, sent below
             const int dr = iz >> g.mz;
+            const double xo[3] = {x0, y0, z0};
+            const uint32_t oldg = gkey_of(g, xo);           // its tie key (D#15)
             const double2 p0 = make_double2(x[0], x[1]), p1 = make_double2(x[2], v[2]),
                           p2 = make_double2(v[0], v[1]),
                           p3 = make_double2(__longlong_as_double((long long)((uint64_t)oldg | ((uint64_t)i << 32))), 0.0);
