@@ -255,6 +255,9 @@ def run_ours(args, rank, world):
     ms = ev0.elapsed_time(ev1)
     stages = sim.timings()
     sim.set_timing(False)
+    if world > 1:   # every rank's stage table (rank 0's goes into the JSON line)
+        log(f"[rank {rank}] np {sim.np} stages ms/step: " +
+            " ".join(f"{k}={v[0] / args.steps:.3f}" for k, v in stages.items() if v[0] > 0))
     migrated = reduce_sum(sim.migrated(), world)
     ms = reduce_max(ms, world)
     ms_step = ms / args.steps
@@ -293,13 +296,14 @@ def run_ours(args, rank, world):
     per_stage = {}
     for name in STAGES:
         tot, nl = stages[name]
-        if nl == 0 and name not in ("clear", "exchange"):
+        if nl == 0 and name not in ("clear", "exchange", "xpose"):
             continue
         bp, bn = ALG_BYTES.get(name, (0, 0))
         alg = bp * np_r + bn * ncell
         per_stage[name] = {"ms_per_step": tot / args.steps, "launches": nl,
                            "alg_GBps": (alg * args.steps / (tot / 1e3) / 1e9) if tot > 0 else None}
-    dom = max((s for s in per_stage if s not in ("clear", "exchange")), key=lambda s: per_stage[s]["ms_per_step"])
+    dom = max((s for s in per_stage if s not in ("clear", "exchange", "xpose")),
+              key=lambda s: per_stage[s]["ms_per_step"])
     tot, nl = stages[dom]
     bp, bn = ALG_BYTES[dom]
     # per-launch algorithmic bytes / per-launch duration (scan = 3 launches -> per stage call)
@@ -315,6 +319,23 @@ def run_ours(args, rank, world):
             "peak_source": "measured (MEASURED_PEAKS.json hbm_gbs)" if peaks.get("hbm_gbs") else "fallback 6650 GB/s",
             "alg_bytes_per_launch": alg_per_call}
 
+    # NVLink roofline of the exchange phases (P > 1): bytes rank 0 sends per step in the two
+    # FFT transposes (1 + 2 half-spectrum components, (P-1)/P of each leaves the GPU) and in
+    # the migration (64 B per leaver), against 900 GB/s per direction per GPU (NVLink 5)
+    nvlink = None
+    if world > 1:
+        px = -(-(n // 2 + 1) // 8) * 8
+        unit = 16 * (n // world) * n * px
+        xpose_b = 3 * unit * (world - 1) / world
+        xt = stages["xpose"][0] / args.steps
+        mig_b = 64 * migrated / args.steps / world
+        nvlink = {"peak_GBps": 900.0, "xpose_bytes_per_step": xpose_b, "xpose_ms_per_step": xt,
+                  "xpose_GBps": xpose_b / (xt / 1e3) / 1e9 if xt > 0 else None,
+                  "xpose_frac": (xpose_b / (xt / 1e3) / 1e9) / 900.0 if xt > 0 else None,
+                  "migration_bytes_per_step": mig_b,
+                  "exchange_ms_per_step": stages["exchange"][0] / args.steps,
+                  "transport": "peer" if sim.peer_transport() else "nccl"}
+
     cpu = None if args.no_cpu_baseline else oracle_sample(steps=args.cpu_steps)
     if cpu:
         cpu["sample"] = cpu["sample"].replace("{n}", str(n))
@@ -327,11 +348,13 @@ def run_ours(args, rank, world):
         "config": {"workload": cfg_name, "grid": n, "ppc": ppc, "particles": np_,
                    "k": 0.5, "alpha": 0.05, "dt": 0.05,
                    "parallelism": "1 GPU" if world == 1 else
-                   f"z-slab decomposition over {world} GPUs (NCCL all-to-all FFT transposes, "
-                   f"halo/ghost send/recv, particle migration)",
+                   f"z-slab decomposition over {world} GPUs (NCCL all-to-all FFT transposes; halo "
+                   f"plane, ghost plane and particle migration over "
+                   f"{'NVLink peer memory' if nvlink['transport'] == 'peer' else 'NCCL send/recv'})",
                    "migrated_per_step": migrated / args.steps,
                    "l2": "inputs larger than L2 (particle state 48 B x N_p / N per rank)"},
         "roofline": roof,
+        "nvlink": nvlink,
         "cpu_baseline": cpu,
         "e2e": e2e,
         "gpu_launches": launches,

@@ -167,7 +167,8 @@ enum {
     PIC_STAGE_FFT_X_FWD = 0, PIC_STAGE_FFT_Y_FWD, PIC_STAGE_FFT_Z_MUL, PIC_STAGE_FFT_Y_INV,
     PIC_STAGE_FFT_X_INV, PIC_STAGE_ENERGY, PIC_STAGE_CLEAR, PIC_STAGE_PUSH_KEY,
     PIC_STAGE_SCAN, PIC_STAGE_PLACE, PIC_STAGE_REORDER_DEPOSIT,
-    PIC_STAGE_EXCHANGE,   /* NCCL: transposes, halo/ghost planes, migration, energy */
+    PIC_STAGE_EXCHANGE,   /* P > 1: barriers, halo/ghost planes, migration, energy sum */
+    PIC_STAGE_XPOSE,      /* P > 1: the two FFT transposes (all-to-all) */
     PIC_NSTAGES
 };
 pic_status pic_set_timing(pic_ctx *ctx, int32_t enable);

@@ -23,7 +23,7 @@ STATUS_NAMES = {0: "PIC_OK", -1: "PIC_EINVAL", -2: "PIC_ENOMEM", -3: "PIC_ECUDA"
                 -8: "PIC_EUNSUPPORTED"}
 
 STAGES = ["fft_x_fwd", "fft_y_fwd", "fft_z_mul", "fft_y_inv", "fft_x_inv", "energy", "clear",
-          "push_key", "scan", "place", "reorder_deposit", "exchange"]
+          "push_key", "scan", "place", "reorder_deposit", "exchange", "xpose"]
 PIC_NSTAGES = len(STAGES)
 
 

@@ -726,7 +726,8 @@ __global__ void __launch_bounds__(kThreads, 3) k_reorder_deposit(
         ca = cb;
     }
     fold_flush(g, tile, acc, t, bx, by, bz, rho, ghost);
-    if (MR && ghost != rho + (int64_t)g.nzl * g.n * g.rp) __threadfence_system();
+    if (MR && bz + 4 == g.nzl && ghost != rho + (int64_t)g.nzl * g.n * g.rp)
+        __threadfence_system();   // peer ghost atomics (PIC_P2P_GHOST=2) complete before the barrier
 }
 
 __global__ void __launch_bounds__(kThreads) k_half_kick(Geom g, PState cur, int64_t np,
@@ -830,7 +831,8 @@ void launch_push_key(const Geom& g, PState cur, const uint32_t* offs, const doub
     sb.count = send_count;
     sb.segs = segs;
     if (peers) { sb.peers = *peers; sb.remote = 1; }
-    if (g.P > 1) k_push_key_brick<true><<<nbrick, kThreads, 0, s>>>(g, cur, offs, E4, key, rank, count, sb, err_flag);
+    static const bool force_mr = getenv("PIC_FORCE_MR") != nullptr;   // diagnostics
+    if (g.P > 1 || force_mr) k_push_key_brick<true><<<nbrick, kThreads, 0, s>>>(g, cur, offs, E4, key, rank, count, sb, err_flag);
     else k_push_key_brick<false><<<nbrick, kThreads, 0, s>>>(g, cur, offs, E4, key, rank, count, sb, err_flag);
 }
 
@@ -877,7 +879,8 @@ void launch_reorder_deposit(const Geom& g, const uint32_t* offs, const uint32_t*
                             const double2* recv, int64_t n_old, const unsigned long long* dcnt, PState nxt,
                             int push, double* rho_buf, double* ghost, int* err_flag, cudaStream_t s) {
     const unsigned nbrick = (unsigned)(((int64_t)g.n * g.n * g.nzl) / kBrick);
-    if (g.P == 1) {
+    static const bool force_mr = getenv("PIC_FORCE_MR") != nullptr;   // diagnostics
+    if (g.P == 1 && !force_mr) {
         if (push)
             k_reorder_deposit<true, false><<<nbrick, kThreads, reorder_smem<false>(), s>>>(g, offs, perm, cur, recv, n_old, dcnt, nxt, rho_buf, ghost, err_flag);
         else

@@ -41,7 +41,7 @@ constexpr int kMaxEnergySteps = 4096;   // device ring of per-step (W_x, W)
 
 const char* kStageNames[PIC_NSTAGES] = {
     "fft_x_fwd", "fft_y_fwd", "fft_z_mul", "fft_y_inv", "fft_x_inv", "energy",
-    "clear",     "push_key",  "scan",      "place",     "reorder_deposit", "exchange"};
+    "clear",     "push_key",  "scan",      "place",     "reorder_deposit", "exchange", "xpose"};
 
 size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
 
@@ -485,14 +485,14 @@ pic_status solve(pic_ctx* c, double scale, int slot) {
     { StageScope t(c, PIC_STAGE_FFT_Y_FWD, 1); pic::launch_fft_y(g, S0, A, 1, 0, c->tw, c->stream); }
     PIC_LAUNCHED(c, "fft_y_fwd");
     if (g.P > 1) {
-        StageScope t(c, PIC_STAGE_EXCHANGE, 0);
+        StageScope t(c, PIC_STAGE_XPOSE, 0);
         if (xpose_p2p) PIC_TRY(barrier(c));
         else PIC_NCCL(c, ncclAlltoAll(c->specA, c->specB, 2 * unit / g.P, ncclDouble, c->comm, c->stream));
     }
     { StageScope t(c, PIC_STAGE_FFT_Z_MUL, 1); pic::launch_fft_z_mul(g, c->specB, Cz, scale, c->tw, c->stream); }
     PIC_LAUNCHED(c, "fft_z_mul");
     if (g.P > 1) {
-        StageScope t(c, PIC_STAGE_EXCHANGE, 0);
+        StageScope t(c, PIC_STAGE_XPOSE, 0);
         if (xpose_p2p) PIC_TRY(barrier(c));
         else PIC_NCCL(c, ncclAlltoAll(c->specC, c->specD, 4 * unit / g.P, ncclDouble, c->comm, c->stream));
     }
