@@ -401,3 +401,209 @@ void oracle_run(int32_t n, double L, double dt, int64_t np, double *xv, int32_t 
     free(E);
     free(rho);
 }
+
+/* ================================================= FD-PCG Poisson solve ==== *
+ * P:179-181 (PCG solver: second-order central finite differences, matrix-free
+ * CG), P:260 (SSOR preconditioner, four inner and two outer iterations,
+ * damping factor pi/2; warm start from the previous time step)
+ * (tolerance 1e-4).  Readings D#26-D#31: A = -Delta_h (7-point,
+ * periodic), b = rho - mean(rho), red-black SSOR as `outer` x (`inner` forward
+ * red/black sweeps, `inner` backward black/red sweeps) from z = 0, stopping
+ * rule ||r||^2 <= tol^2 ||b||^2, E = -grad_h phi by central differences.
+ * Node colour: red = (ix + iy + iz) even. */
+
+/* y = A x = -Delta_h x: (6 x_m - sum of the six neighbours) / h^2. */
+static double nb_sum(int32_t n, const double *x, int32_t ix, int32_t iy, int32_t iz) {
+    return ((x[node(n, ix - 1, iy, iz)] + x[node(n, ix + 1, iy, iz)]) +
+            (x[node(n, ix, iy - 1, iz)] + x[node(n, ix, iy + 1, iz)])) +
+           (x[node(n, ix, iy, iz - 1)] + x[node(n, ix, iy, iz + 1)]);
+}
+
+void oracle_laplacian_fd(int32_t n, double L, const double *x, double *y) {
+    const double inv_h = (double)n / L;
+    const double ih2 = inv_h * inv_h;
+    for (int32_t iz = 0; iz < n; ++iz)
+        for (int32_t iy = 0; iy < n; ++iy)
+            for (int32_t ix = 0; ix < n; ++ix) {
+                int64_t m = node(n, ix, iy, iz);
+                y[m] = (6.0 * x[m] - nb_sum(n, x, ix, iy, iz)) * ih2;
+            }
+}
+
+/* One SOR half-sweep over the nodes of colour `colour` ("Gauss-Seidel",
+ * P:260 damping factor omega): z_m <- (1 - omega) z_m + (omega/6)(h^2 r_m + sum nb z).
+ * Every neighbour of a node has the other colour, so the order inside the colour
+ * does not matter. */
+static void sor_half_sweep(int32_t n, double h2, double c1, double c2, const double *r, double *z,
+                           int colour) {
+    for (int32_t iz = 0; iz < n; ++iz)
+        for (int32_t iy = 0; iy < n; ++iy)
+            for (int32_t ix = 0; ix < n; ++ix) {
+                if (((ix + iy + iz) & 1) != colour) continue;
+                int64_t m = node(n, ix, iy, iz);
+                z[m] = c1 * z[m] + c2 * (h2 * r[m] + nb_sum(n, z, ix, iy, iz));
+            }
+}
+
+/* z = M^-1 r, the SSOR preconditioner of P:260 (reading D#28): z = 0; outer times
+ * { inner times (red, black) ; inner times (black, red) }.  The half-sweep sequence
+ * is a palindrome, so M^-1 is symmetric (positive definite for 0 < omega < 2). */
+void oracle_ssor(int32_t n, double L, const double *r, double *z, double omega, int32_t inner,
+                 int32_t outer) {
+    const int64_t nn = (int64_t)n * n * n;
+    const double h = L / (double)n;
+    const double h2 = h * h;
+    const double c1 = 1.0 - omega, c2 = omega / 6.0;
+    for (int64_t m = 0; m < nn; ++m) z[m] = 0.0;
+    for (int32_t o = 0; o < outer; ++o) {
+        for (int32_t i = 0; i < inner; ++i) {
+            sor_half_sweep(n, h2, c1, c2, r, z, 0);
+            sor_half_sweep(n, h2, c1, c2, r, z, 1);
+        }
+        for (int32_t i = 0; i < inner; ++i) {
+            sor_half_sweep(n, h2, c1, c2, r, z, 1);
+            sor_half_sweep(n, h2, c1, c2, r, z, 0);
+        }
+    }
+}
+
+static double dot(int64_t nn, const double *a, const double *b) {
+    double s = 0.0;
+    for (int64_t m = 0; m < nn; ++m) s += a[m] * b[m];
+    return s;
+}
+
+/* Preconditioned CG (Saad Alg. 9.1) for A x = b from the initial guess in
+ * x (warm start).  precond = 1: SSOR(omega, inner, outer); 0: none (M = I).
+ * Stops when ||r||^2 <= tol^2 ||b||^2 (D#29); b = 0 gives x = 0.
+ * Returns the iteration count, or -1 if maxit iterations did not converge. */
+int32_t oracle_pcg(int32_t n, double L, const double *b, double *x, double tol, int32_t precond,
+                   double omega, int32_t inner, int32_t outer, int32_t maxit, double *relres) {
+    const int64_t nn = (int64_t)n * n * n;
+    double *r = (double *)malloc(sizeof(double) * (size_t)nn);
+    double *z = (double *)malloc(sizeof(double) * (size_t)nn);
+    double *p = (double *)malloc(sizeof(double) * (size_t)nn);
+    double *q = (double *)malloc(sizeof(double) * (size_t)nn);
+    const double bb = dot(nn, b, b);
+    const double stop = (tol * tol) * bb;
+    int32_t it = 0, status = -1;
+    double rr = 0.0;
+    if (bb == 0.0) {
+        for (int64_t m = 0; m < nn; ++m) x[m] = 0.0;
+        status = 0;
+        goto done;
+    }
+    oracle_laplacian_fd(n, L, x, q);                       /* r = b - A x */
+    for (int64_t m = 0; m < nn; ++m) r[m] = b[m] - q[m];
+    rr = dot(nn, r, r);
+    if (rr <= stop) { status = 0; goto done; }
+    if (precond) oracle_ssor(n, L, r, z, omega, inner, outer);
+    else memcpy(z, r, sizeof(double) * (size_t)nn);
+    memcpy(p, z, sizeof(double) * (size_t)nn);
+    double rz = dot(nn, r, z);
+    for (it = 1; it <= maxit; ++it) {
+        oracle_laplacian_fd(n, L, p, q);                   /* q = A p */
+        const double alpha = rz / dot(nn, p, q);
+        for (int64_t m = 0; m < nn; ++m) x[m] = x[m] + alpha * p[m];
+        for (int64_t m = 0; m < nn; ++m) r[m] = r[m] - alpha * q[m];
+        rr = dot(nn, r, r);
+        if (rr <= stop) { status = it; break; }
+        if (precond) oracle_ssor(n, L, r, z, omega, inner, outer);
+        else memcpy(z, r, sizeof(double) * (size_t)nn);
+        const double rz_new = dot(nn, r, z);
+        const double beta = rz_new / rz;
+        rz = rz_new;
+        for (int64_t m = 0; m < nn; ++m) p[m] = z[m] + beta * p[m];
+    }
+done:
+    if (relres) *relres = bb > 0.0 ? sqrt(rr / bb) : 0.0;
+    free(q);
+    free(p);
+    free(z);
+    free(r);
+    return status;
+}
+
+/* E = -grad_h phi by second-order central differences (D#30):
+ * E_d(m) = (phi(m - e_d) - phi(m + e_d)) * (inv_h / 2). */
+void oracle_gradient_central(int32_t n, double L, const double *phi, double *E) {
+    const int64_t nn = (int64_t)n * n * n;
+    const double c = 0.5 * ((double)n / L);
+    for (int32_t iz = 0; iz < n; ++iz)
+        for (int32_t iy = 0; iy < n; ++iy)
+            for (int32_t ix = 0; ix < n; ++ix) {
+                int64_t m = node(n, ix, iy, iz);
+                E[m] = (phi[node(n, ix - 1, iy, iz)] - phi[node(n, ix + 1, iy, iz)]) * c;
+                E[nn + m] = (phi[node(n, ix, iy - 1, iz)] - phi[node(n, ix, iy + 1, iz)]) * c;
+                E[2 * nn + m] = (phi[node(n, ix, iy, iz - 1)] - phi[node(n, ix, iy, iz + 1)]) * c;
+            }
+}
+
+/* The PCG solve of the PIC loop: b = rho - mean(rho) (ion background,
+ * P:103, D#3), A phi = b by SSOR-PCG warm-started from phi, E = -grad_h phi.
+ * Returns the iteration count (-1: not converged). */
+int32_t oracle_solve_pcg(int32_t n, double L, const double *rho, double *phi, double *E, double tol,
+                         double omega, int32_t inner, int32_t outer, int32_t maxit, double *relres) {
+    const int64_t nn = (int64_t)n * n * n;
+    double *b = (double *)malloc(sizeof(double) * (size_t)nn);
+    double mean = 0.0;
+    for (int64_t m = 0; m < nn; ++m) mean += rho[m];
+    mean = mean / (double)nn;
+    for (int64_t m = 0; m < nn; ++m) b[m] = rho[m] - mean;
+    int32_t it = oracle_pcg(n, L, b, phi, tol, 1, omega, inner, outer, maxit, relres);
+    oracle_gradient_central(n, L, phi, E);
+    free(b);
+    return it;
+}
+
+/* The PIC loop of oracle_run with the PCG solve in place of the FFT solve (BJ
+ * config 5).  phi (N^3, in/out) is the warm start of the first solve and holds the
+ * last solution on return; iters (nullable, nsteps) receives each solve's count. */
+void oracle_run_pcg(int32_t n, double L, double dt, int64_t np, double *xv, int32_t nsteps,
+                    double *ex_energy, double *tot_energy, double *phi, double tol, double omega,
+                    int32_t inner, int32_t outer, int32_t maxit, int32_t *iters) {
+    const int64_t nn = (int64_t)n * n * n;
+    const double q = -((L * L) * L) / (double)np;
+    const double qm_dt = -1.0 * dt;
+    double *rho = (double *)malloc(sizeof(double) * (size_t)nn);
+    double *E = (double *)malloc(sizeof(double) * (size_t)nn * 3);
+    double *Ep = (double *)malloc(sizeof(double) * (size_t)(np > 0 ? np : 1) * 3);
+    uint32_t *perm = (uint32_t *)malloc(sizeof(uint32_t) * (size_t)(np > 0 ? np : 1));
+    oracle_sort(n, L, np, xv, perm);
+    for (int32_t s = 0; s < nsteps; ++s) {
+        oracle_deposit(n, L, np, xv, q, rho);
+        int32_t it = oracle_solve_pcg(n, L, rho, phi, E, tol, omega, inner, outer, maxit, NULL);
+        if (iters) iters[s] = it;
+        double wx, w;
+        oracle_field_energy(n, L, E, &wx, &w);
+        if (ex_energy) ex_energy[s] = wx;
+        if (tot_energy) tot_energy[s] = w;
+        oracle_gather(n, L, np, xv, E, Ep);
+        oracle_push(L, np, xv, Ep, qm_dt, dt);
+        oracle_sort(n, L, np, xv, perm);
+    }
+    free(perm);
+    free(Ep);
+    free(E);
+    free(rho);
+}
+
+/* Backward half kick with the PCG field; phi (in/out) as in oracle_run_pcg. */
+void oracle_half_kick_pcg(int32_t n, double L, double dt, int64_t np, double *xv, double *phi, double tol,
+                          double omega, int32_t inner, int32_t outer, int32_t maxit) {
+    const int64_t nn = (int64_t)n * n * n;
+    const double q = -((L * L) * L) / (double)np;
+    double *rho = (double *)malloc(sizeof(double) * (size_t)nn);
+    double *E = (double *)malloc(sizeof(double) * (size_t)nn * 3);
+    double *Ep = (double *)malloc(sizeof(double) * (size_t)(np > 0 ? np : 1) * 3);
+    oracle_deposit(n, L, np, xv, q, rho);
+    oracle_solve_pcg(n, L, rho, phi, E, tol, omega, inner, outer, maxit, NULL);
+    oracle_gather(n, L, np, xv, E, Ep);
+    const double hk = -0.5 * (-1.0 * dt);
+    for (int64_t j = 0; j < np; ++j)
+        for (int d = 0; d < 3; ++d)
+            xv[(3 + d) * np + j] = fma(hk, Ep[d * np + j], xv[(3 + d) * np + j]);
+    free(Ep);
+    free(E);
+    free(rho);
+}

@@ -74,6 +74,29 @@ void oracle_run(int32_t n, double L, double dt, int64_t np, double *xv, int32_t 
 /* Backward half kick: v <- v - (q/m) E(x_0) dt/2, x unchanged. */
 void oracle_half_kick(int32_t n, double L, double dt, int64_t np, double *xv);
 
+/* ---- FD-PCG Poisson solve (BJ config 5; D#26-D#31) ---- */
+/* y = -Delta_h x, 7-point second-order stencil, periodic. */
+void oracle_laplacian_fd(int32_t n, double L, const double *x, double *y);
+/* z = M^-1 r: red-black SSOR, `outer` x (`inner` x red+black, `inner` x black+red)
+ * SOR half-sweeps with relaxation omega from z = 0 (D#28). */
+void oracle_ssor(int32_t n, double L, const double *r, double *z, double omega, int32_t inner,
+                 int32_t outer);
+/* Preconditioned CG for -Delta_h x = b from the guess in x (warm start); precond
+ * 1 = SSOR, 0 = none; stop at ||r||^2 <= tol^2 ||b||^2.  Returns iterations or -1. */
+int32_t oracle_pcg(int32_t n, double L, const double *b, double *x, double tol, int32_t precond,
+                   double omega, int32_t inner, int32_t outer, int32_t maxit, double *relres);
+/* E_d = (phi(m - e_d) - phi(m + e_d)) inv_h / 2 (D#30). */
+void oracle_gradient_central(int32_t n, double L, const double *phi, double *E);
+/* b = rho - mean(rho); PCG warm-started from phi; E = -grad_h phi. */
+int32_t oracle_solve_pcg(int32_t n, double L, const double *rho, double *phi, double *E, double tol,
+                         double omega, int32_t inner, int32_t outer, int32_t maxit, double *relres);
+/* oracle_run with the PCG solve; phi in/out (warm start); iters (nullable) per step. */
+void oracle_run_pcg(int32_t n, double L, double dt, int64_t np, double *xv, int32_t nsteps,
+                    double *ex_energy, double *tot_energy, double *phi, double tol, double omega,
+                    int32_t inner, int32_t outer, int32_t maxit, int32_t *iters);
+void oracle_half_kick_pcg(int32_t n, double L, double dt, int64_t np, double *xv, double *phi, double tol,
+                          double omega, int32_t inner, int32_t outer, int32_t maxit);
+
 #ifdef __cplusplus
 }
 #endif

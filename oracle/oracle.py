@@ -61,6 +61,14 @@ def lib():
             "oracle_wrap": (dbl, [dbl, dbl]),
             "oracle_run": (None, [i32, dbl, dbl, i64, dp, i32, dp, dp, u32p]),
             "oracle_half_kick": (None, [i32, dbl, dbl, i64, dp]),
+            "oracle_laplacian_fd": (None, [i32, dbl, dp, dp]),
+            "oracle_ssor": (None, [i32, dbl, dp, dp, dbl, i32, i32]),
+            "oracle_pcg": (i32, [i32, dbl, dp, dp, dbl, i32, dbl, i32, i32, i32, dp]),
+            "oracle_gradient_central": (None, [i32, dbl, dp, dp]),
+            "oracle_solve_pcg": (i32, [i32, dbl, dp, dp, dp, dbl, dbl, i32, i32, i32, dp]),
+            "oracle_run_pcg": (None, [i32, dbl, dbl, i64, dp, i32, dp, dp, dp, dbl, dbl, i32, i32,
+                                      i32, C.POINTER(C.c_int32)]),
+            "oracle_half_kick_pcg": (None, [i32, dbl, dbl, i64, dp, dp, dbl, dbl, i32, i32, i32]),
         }
         for name, (res, args) in sig.items():
             f = getattr(L, name)
@@ -201,3 +209,79 @@ def init_state(n: int, ppc: int, k: float = 0.5, alpha: float = 0.05, seed: int 
     if half_kick_:
         xv = half_kick(n, L, dt, xv)
     return xv
+
+
+# ------------------------------------------------ FD-PCG solve (BJ config 5) ----
+# P:179-181, P:226 (tol 1e-4), P:260 (SSOR: 4 inner, 2 outer, damping pi/2; warm start).
+PCG_DEFAULTS = dict(tol=1e-4, omega=np.pi / 2, inner=4, outer=2, maxit=1000)
+
+
+def laplacian_fd(n: int, L: float, x: np.ndarray) -> np.ndarray:
+    x = np.ascontiguousarray(x, dtype=np.float64)
+    y = np.zeros((n, n, n))
+    lib().oracle_laplacian_fd(n, L, _dp(x), _dp(y))
+    return y
+
+
+def ssor(n: int, L: float, r: np.ndarray, omega=np.pi / 2, inner=4, outer=2) -> np.ndarray:
+    r = np.ascontiguousarray(r, dtype=np.float64)
+    z = np.zeros((n, n, n))
+    lib().oracle_ssor(n, L, _dp(r), _dp(z), omega, inner, outer)
+    return z
+
+
+def pcg(n: int, L: float, b: np.ndarray, x0=None, tol=1e-4, precond=1, omega=np.pi / 2, inner=4,
+        outer=2, maxit=1000):
+    """Returns (x, iterations (-1: not converged), relative residual)."""
+    b = np.ascontiguousarray(b, dtype=np.float64)
+    x = np.zeros((n, n, n)) if x0 is None else np.ascontiguousarray(x0, dtype=np.float64).copy()
+    rel = C.c_double()
+    it = lib().oracle_pcg(n, L, _dp(b), _dp(x), tol, precond, omega, inner, outer, maxit, C.byref(rel))
+    return x, it, rel.value
+
+
+def gradient_central(n: int, L: float, phi: np.ndarray) -> np.ndarray:
+    phi = np.ascontiguousarray(phi, dtype=np.float64)
+    E = np.zeros((3, n, n, n))
+    lib().oracle_gradient_central(n, L, _dp(phi), _dp(E))
+    return E
+
+
+def solve_pcg(n: int, L: float, rho: np.ndarray, phi0=None, tol=1e-4, omega=np.pi / 2, inner=4,
+              outer=2, maxit=1000):
+    """Returns (E, phi, iterations, relative residual)."""
+    rho = np.ascontiguousarray(rho, dtype=np.float64)
+    phi = np.zeros((n, n, n)) if phi0 is None else np.ascontiguousarray(phi0, dtype=np.float64).copy()
+    E = np.zeros((3, n, n, n))
+    rel = C.c_double()
+    it = lib().oracle_solve_pcg(n, L, _dp(rho), _dp(phi), _dp(E), tol, omega, inner, outer, maxit,
+                                C.byref(rel))
+    return E, phi, it, rel.value
+
+
+def run_pcg(n: int, L: float, dt: float, xv: np.ndarray, nsteps: int, phi0=None, tol=1e-4,
+            omega=np.pi / 2, inner=4, outer=2, maxit=1000):
+    """oracle_run with the PCG solve.  Returns (xv, W_x[n], W[n], phi, iterations[n])."""
+    xs = np.ascontiguousarray(xv, dtype=np.float64).copy()
+    ex = np.zeros(max(nsteps, 1))
+    tot = np.zeros(max(nsteps, 1))
+    phi = np.zeros((n, n, n)) if phi0 is None else np.ascontiguousarray(phi0, dtype=np.float64).copy()
+    its = np.zeros(max(nsteps, 1), dtype=np.int32)
+    lib().oracle_run_pcg(n, L, dt, xs.shape[1], _dp(xs), nsteps, _dp(ex), _dp(tot), _dp(phi), tol, omega,
+                         inner, outer, maxit, its.ctypes.data_as(C.POINTER(C.c_int32)))
+    return xs, ex[:nsteps], tot[:nsteps], phi, its[:nsteps]
+
+
+def init_state_pcg(n: int, ppc: int, k: float = 0.5, alpha: float = 0.05, seed: int = 1,
+                   dt: float = 0.05, L: float | None = None, tol=1e-4, omega=np.pi / 2, inner=4,
+                   outer=2, maxit=1000):
+    """pic_init with the PCG solver: sample, canonicalise, half kick with the PCG field
+    (phi from 0).  Returns (xv, phi) -- phi is the warm start of the first step."""
+    if L is None:
+        L = 2.0 * np.pi / k
+    np_ = ppc * n ** 3
+    xv = sample_landau(np_, k, L, alpha, seed)
+    xv, _ = sort(n, L, xv)
+    phi = np.zeros((n, n, n))
+    lib().oracle_half_kick_pcg(n, L, dt, xv.shape[1], _dp(xv), _dp(phi), tol, omega, inner, outer, maxit)
+    return xv, phi
