@@ -47,8 +47,19 @@ typedef enum {
     PIC_ENONFINITE = -5,   /* a field energy came out NaN/Inf                      */
     PIC_EOVERFLOW = -6,    /* particle capacity exceeded                           */
     PIC_EPOISONED = -7,    /* an earlier CUDA/NCCL error poisoned this context     */
-    PIC_EUNSUPPORTED = -8  /* valid request this build does not implement          */
+    PIC_EUNSUPPORTED = -8, /* valid request this build does not implement          */
+    PIC_ENONCONV = -9      /* PCG solver: no convergence within pcg_maxit iterations
+                              (the field of the last iterate is kept; not poisoning) */
 } pic_status;
+
+/* Field solver of the PIC step.  FFT: the pseudo-spectral solve of P:171-177 (default).
+ * PCG: the matrix-free finite-difference solve of P:179-181 (BJ config 5): 7-point
+ * -Delta_h phi = rho - mean(rho) (periodic), conjugate gradients preconditioned by
+ * red-black SSOR with pcg_inner / pcg_outer sweeps and relaxation pcg_omega,
+ * warm-started from the previous step's phi, stopped at
+ * ||r||_2 <= pcg_tol ||b||_2, E = -grad_h phi by central differences
+ * (D#26-D#31). */
+typedef enum { PIC_SOLVER_FFT = 0, PIC_SOLVER_PCG = 1 } pic_solver;
 
 typedef struct {
     int32_t  n;         /* cells per dimension (grid N^3); power of two, 16..1024     */
@@ -60,10 +71,17 @@ typedef struct {
     uint64_t seed;      /* Philox4x32-10 key of the initial sampler (D#10)            */
     int32_t  half_kick; /* 1: v stored at half steps, backward half kick at init */
     int32_t  pgrid[2];  /* {Py, Pz} rank grid: {1, nranks} (z-slabs; pencils not built) */
+    int32_t  solver;    /* pic_solver; default PIC_SOLVER_FFT                             */
+    int32_t  pcg_inner; /* PCG: SSOR inner sweeps, >= 1; default 4                */
+    int32_t  pcg_outer; /* PCG: SSOR outer iterations, >= 1; default 2            */
+    int32_t  pcg_maxit; /* PCG: iteration cap, >= 1; default 1000                         */
+    double   pcg_tol;   /* PCG: relative residual tolerance, > 0; default 1e-4    */
+    double   pcg_omega; /* PCG: SSOR relaxation, 0 < omega < 2; default pi/2      */
 } pic_params;
 
 /* Fill *p with the Landau-damping defaults of P:146 (N=16, ppc=8, k=0.5, alpha=0.05,
- * dt=0.05, L=2 pi/k, seed=1, half_kick=1, pgrid={1,1}). */
+ * dt=0.05, L=2 pi/k, seed=1, half_kick=1, pgrid={1,1}), solver FFT and the PCG
+ * settings of P:226 / P:260 (tol 1e-4, SSOR omega = pi/2, 4 inner, 2 outer). */
 pic_status pic_params_default(pic_params *p);
 
 /* Multi-GPU (one process per GPU, nranks in {1, 2, 4, 8}): rank r owns the z-slab of
@@ -91,12 +109,17 @@ pic_status pic_workspace_bytes(const pic_params *p, int32_t rank, int32_t nranks
  * PIC_EINVAL: alpha not in [0,1), ppc <= 0, N not a power of two in [16,1024],
  *   k <= 0, dt <= 0, k L / 2 pi not a positive integer, N_p per rank >= 2^32 / 1.3,
  *   nranks not in {1,2,4,8}, N/nranks < 4, pgrid != {1, nranks}.
- * PIC_EUNSUPPORTED: a pencil grid (pgrid = {Py > 1, Pz}); PIC_ENCCL: NCCL init failed.
+ * PIC_EINVAL also: solver not a pic_solver; PCG settings out of range.
+ * PIC_EUNSUPPORTED: a pencil grid (pgrid = {Py > 1, Pz}); the PCG solver at nranks > 1
+ *   without the peer-memory transport (it reads the neighbour slabs' planes over NVLink);
+ * PIC_ENCCL: NCCL init failed.
  * PIC_ENOMEM: workspace_bytes too small.  PIC_ECUDA: a kernel failed. */
 pic_status pic_init(const pic_params *p, int32_t rank, int32_t nranks, const uint8_t *nccl_id,
                     void *workspace, size_t workspace_bytes, void *cuda_stream, pic_ctx **out);
 
-/* Advance nsteps PIC steps.  ex_energy (nullable, nsteps doubles, host) receives
+/* Advance nsteps PIC steps.  With the PCG solver each iteration reads the residual
+ * norm on the host (one stream synchronisation per CG iteration); PIC_ENONCONV if a
+ * solve does not converge.  ex_energy (nullable, nsteps doubles, host) receives
  * W_x(t_n) = 1/2 h^3 sum_nodes E_x^2 of the field solved at the start of each
  * step; t_n = n dt.  PIC_ENONFINITE if an energy is NaN/Inf. */
 pic_status pic_step(pic_ctx *ctx, int32_t nsteps, double *ex_energy);
@@ -130,7 +153,8 @@ pic_status pic_peer_transport(pic_ctx *ctx, int32_t *peer);
  * cell key, ties by the current order).  Synchronous. */
 pic_status pic_get_particles(pic_ctx *ctx, double *xyzuvw, int64_t np);
 
-/* Replace the particle state from host xyzuvw[6][np] (P = 1: np = N_p; P > 1: this
+/* (PCG: also resets the warm start phi to 0.)
+ * Replace the particle state from host xyzuvw[6][np] (P = 1: np = N_p; P > 1: this
  * rank's particles, every one inside its slab, np <= its capacity; every coordinate
  * in [0, L), else PIC_EINVAL and the offending coordinates are replaced by valid
  * ones inside the slab).  Collective at P > 1.  The state is interpreted as (x_n, v_{n-1/2})
@@ -140,13 +164,15 @@ pic_status pic_set_particles(pic_ctx *ctx, const double *xyzuvw, int64_t np);
 
 /* Copy this rank's slab of a grid to host [nz][N][N] (P = 1: [N][N][N]): which = 0
  * -> rho (charge density of the current positions, q/h^3 scaled); 1, 2, 3 -> E_x,
- * E_y, E_z of the latest solve. */
+ * E_y, E_z of the latest solve; 4 -> phi of the latest PCG solve (PCG only, else
+ * PIC_EINVAL). */
 pic_status pic_get_grid(pic_ctx *ctx, int32_t which, double *host);
 
 /* Solve for an injected charge density rho_host[nz][N][N] (this rank's slab; true
  * density, not scaled) and return E_host[3][nz][N][N] and the energies (of the
  * whole box).  Collective at P > 1.  Does not touch the
- * particles, but overwrites the context's field and charge buffers. */
+ * particles, but overwrites the context's field and charge buffers.  PCG: the
+ * solve starts from phi = 0 and leaves its phi as the next step's warm start. */
 pic_status pic_solve_injected(pic_ctx *ctx, const double *rho_host, double *E_host,
                               double *ex_energy, double *total_energy);
 
@@ -169,6 +195,9 @@ enum {
     PIC_STAGE_SCAN, PIC_STAGE_PLACE, PIC_STAGE_REORDER_DEPOSIT,
     PIC_STAGE_EXCHANGE,   /* P > 1: barriers, halo/ghost planes, migration, energy sum */
     PIC_STAGE_XPOSE,      /* P > 1: the two FFT transposes (all-to-all) */
+    PIC_STAGE_PCG_SSOR,   /* PCG: SSOR half-sweeps (+ barriers at P > 1) */
+    PIC_STAGE_PCG_CG,     /* PCG: rhs, residual, matvec, updates, dot products, host checks */
+    PIC_STAGE_PCG_FIELD,  /* PCG: central-difference gradient -> E4, energy partials */
     PIC_NSTAGES
 };
 pic_status pic_set_timing(pic_ctx *ctx, int32_t enable);
@@ -177,8 +206,15 @@ pic_status pic_reset_timings(pic_ctx *ctx);
 /* Name of a stage (static string) or NULL. */
 const char *pic_stage_name(int32_t stage);
 
-/* Number of kernel launches one pic_step(ctx, 1) makes (for the bench's count). */
+/* Number of kernel launches one pic_step(ctx, 1) makes (for the bench's count; PCG:
+ * with the latest solve's iteration count). */
 pic_status pic_launches_per_step(pic_ctx *ctx, int64_t *launches);
+
+/* PCG solver statistics: iterations of the latest solve (-1: not converged), total
+ * iterations and solves since pic_init, relative residual ||r||/||b|| of the latest
+ * solve.  Any pointer may be NULL.  PIC_EINVAL for an FFT context. */
+pic_status pic_pcg_stats(pic_ctx *ctx, int32_t *last_iters, int64_t *total_iters, int64_t *solves,
+                         double *last_relres);
 
 #ifdef __cplusplus
 }

@@ -18,12 +18,16 @@ LIB_PATH = os.path.join(_HERE, "libpic.so")
 
 PIC_OK, PIC_EINVAL, PIC_ENOMEM, PIC_ECUDA, PIC_ENCCL = 0, -1, -2, -3, -4
 PIC_ENONFINITE, PIC_EOVERFLOW, PIC_EPOISONED, PIC_EUNSUPPORTED = -5, -6, -7, -8
+PIC_ENONCONV = -9
 STATUS_NAMES = {0: "PIC_OK", -1: "PIC_EINVAL", -2: "PIC_ENOMEM", -3: "PIC_ECUDA", -4: "PIC_ENCCL",
                 -5: "PIC_ENONFINITE", -6: "PIC_EOVERFLOW", -7: "PIC_EPOISONED",
-                -8: "PIC_EUNSUPPORTED"}
+                -8: "PIC_EUNSUPPORTED", -9: "PIC_ENONCONV"}
+PIC_SOLVER_FFT, PIC_SOLVER_PCG = 0, 1
+SOLVERS = {"fft": PIC_SOLVER_FFT, "pcg": PIC_SOLVER_PCG}
 
 STAGES = ["fft_x_fwd", "fft_y_fwd", "fft_z_mul", "fft_y_inv", "fft_x_inv", "energy", "clear",
-          "push_key", "scan", "place", "reorder_deposit", "exchange", "xpose"]
+          "push_key", "scan", "place", "reorder_deposit", "exchange", "xpose", "pcg_ssor", "pcg_cg",
+          "pcg_field"]
 PIC_NSTAGES = len(STAGES)
 
 
@@ -38,6 +42,12 @@ class pic_params(C.Structure):
         ("seed", C.c_uint64),
         ("half_kick", C.c_int32),
         ("pgrid", C.c_int32 * 2),
+        ("solver", C.c_int32),
+        ("pcg_inner", C.c_int32),
+        ("pcg_outer", C.c_int32),
+        ("pcg_maxit", C.c_int32),
+        ("pcg_tol", C.c_double),
+        ("pcg_omega", C.c_double),
     ]
 
 
@@ -78,6 +88,7 @@ SYMBOLS = {
     "pic_reset_timings": (C.c_int, [_vp]),
     "pic_stage_name": (C.c_char_p, [C.c_int32]),
     "pic_launches_per_step": (C.c_int, [_vp, _i64p]),
+    "pic_pcg_stats": (C.c_int, [_vp, C.POINTER(C.c_int32), _i64p, _i64p, _dp]),
 }
 
 _lib = None
@@ -156,12 +167,16 @@ class Simulation:
     """
 
     def __init__(self, n=16, ppc=8, k=0.5, alpha=0.05, dt=0.05, seed=1, half_kick=True,
-                 length=0.0, device=None, rank=0, nranks=1, nccl_id: bytes | None = None):
+                 length=0.0, device=None, rank=0, nranks=1, nccl_id: bytes | None = None,
+                 solver="fft", **pcg):
+        """solver: "fft" or "pcg" (BJ config 5); pcg keywords
+        pcg_tol, pcg_omega, pcg_inner, pcg_outer, pcg_maxit override P:226 / P:260."""
         import torch
 
         self.params = default_params(n=n, ppc=ppc, k=k, alpha=alpha, dt=dt, seed=seed,
                                      half_kick=int(bool(half_kick)), length=length,
-                                     pgrid=(1, nranks))
+                                     pgrid=(1, nranks), solver=SOLVERS[solver], **pcg)
+        self.solver = solver
         self.rank, self.nranks = rank, nranks
         self.z0, self.nz, self.capacity = slab(self.params, rank, nranks)
         self.device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
@@ -258,6 +273,17 @@ class Simulation:
 
     def reset_timings(self):
         _check(lib().pic_reset_timings(self.ctx), self.ctx)
+
+    def pcg_stats(self):
+        """(iterations of the latest solve (-1: not converged), total iterations, solves,
+        relative residual of the latest solve) of a PCG simulation."""
+        it, tot, ns, rel = C.c_int32(), C.c_int64(), C.c_int64(), C.c_double()
+        _check(lib().pic_pcg_stats(self.ctx, C.byref(it), C.byref(tot), C.byref(ns), C.byref(rel)), self.ctx)
+        return it.value, tot.value, ns.value, rel.value
+
+    def get_phi(self) -> np.ndarray:
+        """phi of the latest PCG solve, this rank's slab [nz][N][N]."""
+        return self.get_grid(4)
 
     def launches_per_step(self) -> int:
         v = C.c_int64()

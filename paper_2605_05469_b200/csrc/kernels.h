@@ -117,6 +117,37 @@ void launch_reorder_deposit(const Geom& g, const uint32_t* offs, const uint32_t*
 void launch_sort_segments(const uint32_t* offs, int64_t ncell, uint32_t* perm, cudaStream_t s);
 void launch_half_kick(const Geom& g, PState cur, int64_t np, const double* E4, cudaStream_t s);
 void launch_add_plane(double* dst, const double* src, int64_t n, cudaStream_t s);
+// -------------------------------------------------------- FD-PCG solve ----
+// (pcg_kernels.cu; BJ config 5, D#26-D#31.)  Fields are
+// colour-split: F[c][zl][y][x/2], c = (x + y + zl) & 1.  A PcgNbr names one field
+// on this rank and on the ranks below/above (planes -1 and nzl; P = 1: own).
+// Scalars sc[]: 0 sum rho, 1 (b,b), 2 (r,r), 3 (r,z), 4 previous (r,z), 5 (p,Ap).
+// Every launcher ends with its one-CTA fixed-order reduction into sc (or energies).
+struct PcgNbr {
+    const double* own;
+    const double* below;
+    const double* above;
+};
+void launch_pcg_rho_sum(const Geom& g, const double* raw, double dscale, double* partials, double* sc,
+                        cudaStream_t s);
+// r = (dscale raw - sc[0]/nn) - A x -> sc[1] = (b,b), sc[2] = (r,r)
+void launch_pcg_resid0(const Geom& g, const double* raw, double dscale, double* sc, double nn, PcgNbr x,
+                       double* r, double* partials, cudaStream_t s);
+// One red (0) / black (1) SOR half-sweep of z (in place, z.own); mode 2: z == 0 before
+// (first half-sweep), 1: this colour of z == 0; dot: sc[4] = sc[3], sc[3] = (r, z).
+void launch_pcg_sor(const Geom& g, int colour, int mode, bool dot, const double* r, PcgNbr z, double omega,
+                    double* partials, double* sc, cudaStream_t s);
+// pout = z + beta p (first: z), q = A pout, sc[5] = (pout, q); beta = sc[3]/sc[4].
+void launch_pcg_matvec(const Geom& g, bool first, PcgNbr z, PcgNbr p, double* pout, double* q, double* sc,
+                       double* partials, cudaStream_t s);
+// alpha = sc[3]/sc[5]: x += alpha p, r -= alpha q, sc[2] = (r, r).
+void launch_pcg_update(const Geom& g, double* x, const double* p, double* r, const double* q, double* sc,
+                       double* partials, cudaStream_t s);
+// E = -grad_h x -> E4 (+ plane 0 into halo if not null); energies = (W_x, W) of the slab.
+void launch_pcg_gradient(const Geom& g, PcgNbr x, double* E4, double* halo, double* partials, double* energies,
+                         cudaStream_t s);
+void launch_pcg_unsplit(const Geom& g, const double* f, double* out, cudaStream_t s);
+
 void particles_set_smem_limits();
 void fft_set_smem_limits();
 

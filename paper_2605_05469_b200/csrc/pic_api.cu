@@ -41,7 +41,8 @@ constexpr int kMaxEnergySteps = 4096;   // device ring of per-step (W_x, W)
 
 const char* kStageNames[PIC_NSTAGES] = {
     "fft_x_fwd", "fft_y_fwd", "fft_z_mul", "fft_y_inv", "fft_x_inv", "energy",
-    "clear",     "push_key",  "scan",      "place",     "reorder_deposit", "exchange", "xpose"};
+    "clear",     "push_key",  "scan",      "place",     "reorder_deposit", "exchange", "xpose",
+    "pcg_ssor",  "pcg_cg",    "pcg_field"};
 
 size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
 
@@ -110,6 +111,19 @@ struct pic_ctx {
     int* bar = nullptr;                   // barrier word
     unsigned long long* dcnt = nullptr;   // device counts (pic::DC_*)
     bool np_stale = false;                // np / migrated live on the device (dcnt) until the next sync
+    // FD-PCG solver (p.solver == PIC_SOLVER_PCG): colour-split fields of the slab
+    double* pcg_x = nullptr;      // phi: the solution, kept as the next solve's warm start
+    double* pcg_r = nullptr;
+    double* pcg_z = nullptr;
+    double* pcg_p[2] = {};        // search direction, ping-pong (the matvec forms p' = z + beta p)
+    double* pcg_q = nullptr;      // A p
+    double* pcg_sc = nullptr;     // device scalars (kernels.h)
+    int pcg_pi = 0;
+    int32_t pcg_last_iters = 0;
+    int64_t pcg_total_iters = 0;
+    int64_t pcg_solves = 0;
+    int64_t pcg_launches = 0;     // kernel launches of the latest solve
+    double pcg_last_relres = 0.0;
     // timing
     bool timing = false;
     double stage_ms[PIC_NSTAGES] = {};
@@ -146,6 +160,16 @@ pic_status validate(const pic_params* p, int32_t rank, int32_t nranks, char* msg
         snprintf(msg, msz, "k L / 2 pi = %g must be a positive integer", m);
         return PIC_EINVAL;
     }
+    if (p->solver != PIC_SOLVER_FFT && p->solver != PIC_SOLVER_PCG) {
+        snprintf(msg, msz, "solver=%d: PIC_SOLVER_FFT (0) or PIC_SOLVER_PCG (1)", p->solver);
+        return PIC_EINVAL;
+    }
+    if (p->solver == PIC_SOLVER_PCG &&
+        (!(p->pcg_tol > 0) || !(p->pcg_omega > 0 && p->pcg_omega < 2) || p->pcg_inner < 1 || p->pcg_outer < 1 ||
+         p->pcg_maxit < 1)) {
+        snprintf(msg, msz, "PCG: need tol > 0, 0 < omega < 2, inner >= 1, outer >= 1, maxit >= 1");
+        return PIC_EINVAL;
+    }
     const double np = (double)p->ppc * p->n * p->n * p->n / nranks;
     if (np * (nranks > 1 ? 1.3 : 1.0) >= 4294967296.0) {
         snprintf(msg, msz, "N_p per rank = %.0f too large for 32-bit indices", np);
@@ -173,12 +197,14 @@ Geom make_geom(const pic_params* p, int rank, int nranks) {
 }
 
 struct Sizes {
+    int pcg;
     int64_t np_nom, np_cap, recv_cap, nkey, send_len;
     pic::SendSegs segs;
 };
 
 Sizes sizes(const pic_params* p, const Geom& g) {
     Sizes s{};
+    s.pcg = p->solver == PIC_SOLVER_PCG;
     const int64_t npg = (int64_t)p->ppc * p->n * p->n * p->n;
     s.np_nom = npg / g.P;
     if (g.P == 1) {
@@ -254,7 +280,17 @@ size_t carve(pic_ctx* c, const Geom& g, const Sizes& z, char* base) {
     char* pt = take(sizeof(double2*) * 16);
     char* dc = take(sizeof(unsigned long long) * 4);
     char* rv = g.P > 1 ? take(sizeof(double2) * 4 * (size_t)z.recv_cap) : nullptr;
+    char* pv[6] = {};
+    for (int k = 0; k < 6 && z.pcg; ++k) pv[k] = take(sizeof(double) * (size_t)ncell);
+    char* psc = z.pcg ? take(sizeof(double) * 8) : nullptr;
     if (c) {
+        c->pcg_x = reinterpret_cast<double*>(pv[0]);
+        c->pcg_r = reinterpret_cast<double*>(pv[1]);
+        c->pcg_z = reinterpret_cast<double*>(pv[2]);
+        c->pcg_p[0] = reinterpret_cast<double*>(pv[3]);
+        c->pcg_p[1] = reinterpret_cast<double*>(pv[4]);
+        c->pcg_q = reinterpret_cast<double*>(pv[5]);
+        c->pcg_sc = reinterpret_cast<double*>(psc);
         c->key = reinterpret_cast<uint32_t*>(k);
         c->rank = reinterpret_cast<uint16_t*>(rk);
         c->perm = reinterpret_cast<uint32_t*>(pm);
@@ -515,6 +551,140 @@ pic_status solve(pic_ctx* c, double scale, int slot) {
     return PIC_OK;
 }
 
+// ------------------------------------------------------------- FD-PCG -------
+// A field of the slab with its neighbours' copies (planes -1 and nzl, kernels.h).
+pic::PcgNbr pcg_nbr(pic_ctx* c, double* f) {
+    if (c->g.P == 1) return pic::PcgNbr{f, f, f};
+    return pic::PcgNbr{f, on_rank(c, down(c), f), on_rank(c, up(c), f)};
+}
+
+pic_status pcg_allreduce(pic_ctx* c, double* v, int n) {
+    if (c->g.P > 1) PIC_NCCL(c, ncclAllReduce(v, v, n, ncclDouble, ncclSum, c->comm, c->stream));
+    return PIC_OK;
+}
+
+pic_status pcg_read(pic_ctx* c, double* host, const double* dev, int n) {
+    PIC_CUDA(c, cudaMemcpyAsync(host, dev, sizeof(double) * n, cudaMemcpyDeviceToHost, c->stream));
+    PIC_CUDA(c, cudaStreamSynchronize(c->stream));
+    return PIC_OK;
+}
+
+// z = M^-1 r (D#28): outer x {inner x (red, black), inner x (black, red)} SOR
+// half-sweeps from z = 0; the last one also leaves (r, z) in sc[3] (old value in sc[4]).
+// P > 1: a barrier before every half-sweep that reads the other colour from the peers.
+pic_status pcg_precondition(pic_ctx* c) {
+    const Geom& g = c->g;
+    const int inner = c->p.pcg_inner, outer = c->p.pcg_outer;
+    const int total = 4 * inner * outer;
+    int k = 0;
+    auto sweep = [&](int colour) -> pic_status {
+        const int mode = k == 0 ? 2 : (k == 1 ? 1 : 0);
+        const bool dot = k == total - 1;
+        if (g.P > 1 && mode != 2) PIC_TRY(barrier(c));
+        StageScope t(c, PIC_STAGE_PCG_SSOR, dot ? 2 : 1);
+        pic::launch_pcg_sor(g, colour, mode, dot, c->pcg_r, pcg_nbr(c, c->pcg_z), c->p.pcg_omega, c->partials,
+                            c->pcg_sc, c->stream);
+        PIC_LAUNCHED(c, "pcg_sor");
+        c->pcg_launches += dot ? 2 : 1;
+        ++k;
+        if (dot) PIC_TRY(pcg_allreduce(c, c->pcg_sc + 3, 1));
+        return PIC_OK;
+    };
+    for (int o = 0; o < outer; ++o) {
+        for (int i = 0; i < inner; ++i) { PIC_TRY(sweep(0)); PIC_TRY(sweep(1)); }
+        for (int i = 0; i < inner; ++i) { PIC_TRY(sweep(1)); PIC_TRY(sweep(0)); }
+    }
+    return PIC_OK;
+}
+
+// The PCG solve (BJ config 5; D#26-D#31): rho = dscale * raw,
+// b = rho - mean(rho), -Delta_h phi = b by SSOR-PCG warm-started from pcg_x, then
+// E = -grad_h phi -> E4 (+ the halo plane of the slab below) and the energies.  The
+// host reads (r, r) after every update (one stream synchronisation per iteration) to
+// stop at ||r||^2 <= tol^2 ||b||^2.
+pic_status solve_pcg(pic_ctx* c, double dscale, int slot) {
+    const Geom& g = c->g;
+    double* sc = c->pcg_sc;
+    const double nn = (double)g.n * g.n * g.n;
+    const double tol = c->p.pcg_tol;
+    c->pcg_launches = 0;
+    if (g.P > 1) PIC_TRY(barrier(c));          // the warm start x of every slab is in place
+    {
+        StageScope t(c, PIC_STAGE_PCG_CG, 4);
+        pic::launch_pcg_rho_sum(g, c->rho, dscale, c->partials, sc, c->stream);
+        PIC_LAUNCHED(c, "pcg_rho_sum");
+        PIC_TRY(pcg_allreduce(c, sc, 1));
+        pic::launch_pcg_resid0(g, c->rho, dscale, sc, nn, pcg_nbr(c, c->pcg_x), c->pcg_r, c->partials, c->stream);
+        PIC_LAUNCHED(c, "pcg_resid0");
+        PIC_TRY(pcg_allreduce(c, sc + 1, 2));
+        c->pcg_launches += 4;
+    }
+    double h[3];
+    PIC_TRY(pcg_read(c, h, sc + 1, 2));
+    const double bb = h[0], stop = (tol * tol) * bb;
+    double rr = h[1];
+    int it = 0;
+    bool converged = false;
+    if (bb == 0.0) {
+        PIC_CUDA(c, cudaMemsetAsync(c->pcg_x, 0, sizeof(double) * (size_t)c->ncell, c->stream));
+        converged = true;
+        rr = 0.0;
+    } else if (rr <= stop) {
+        converged = true;
+    } else {
+        PIC_TRY(pcg_precondition(c));                          // z = M^-1 r, sc[3] = (r, z)
+        for (it = 1; it <= c->p.pcg_maxit; ++it) {
+            const bool first = it == 1;
+            double* pold = c->pcg_p[c->pcg_pi];
+            double* pnew = c->pcg_p[c->pcg_pi ^ 1];
+            {
+                StageScope t(c, PIC_STAGE_PCG_CG, 4);
+                pic::launch_pcg_matvec(g, first, pcg_nbr(c, c->pcg_z), pcg_nbr(c, pold), pnew, c->pcg_q, sc,
+                                       c->partials, c->stream);    // p = z + beta p, q = A p, sc[5]
+                PIC_LAUNCHED(c, "pcg_matvec");
+                PIC_TRY(pcg_allreduce(c, sc + 5, 1));
+                pic::launch_pcg_update(g, c->pcg_x, pnew, c->pcg_r, c->pcg_q, sc, c->partials, c->stream);
+                PIC_LAUNCHED(c, "pcg_update");
+                PIC_TRY(pcg_allreduce(c, sc + 2, 1));
+                c->pcg_launches += 4;
+            }
+            c->pcg_pi ^= 1;
+            PIC_TRY(pcg_read(c, &rr, sc + 2, 1));
+            if (rr <= stop) { converged = true; break; }
+            PIC_TRY(pcg_precondition(c));                      // z = M^-1 r, sc[3] = (r, z), sc[4] old
+        }
+    }
+    c->pcg_last_iters = converged ? it : -1;
+    c->pcg_total_iters += it > c->p.pcg_maxit ? c->p.pcg_maxit : it;
+    c->pcg_solves += 1;
+    c->pcg_last_relres = bb > 0.0 ? std::sqrt(rr / bb) : 0.0;
+    {
+        StageScope t(c, PIC_STAGE_PCG_FIELD, 2);
+        pic::launch_pcg_gradient(g, pcg_nbr(c, c->pcg_x), c->E4, halo_dst(c), c->partials, c->energies + 2 * slot,
+                                 c->stream);
+        PIC_LAUNCHED(c, "pcg_gradient");
+        c->pcg_launches += 2;
+    }
+    if (g.P > 1) {       // the energy sum is also the barrier for the halo stores
+        StageScope t(c, PIC_STAGE_EXCHANGE, 0);
+        PIC_NCCL(c, ncclAllReduce(c->energies + 2 * slot, c->energies + 2 * slot, 2, ncclDouble, ncclSum,
+                                  c->comm, c->stream));
+    }
+    c->last_slot = slot;
+    if (!converged) {
+        snprintf(c->err, sizeof(c->err), "PCG did not converge in %d iterations (relative residual %.3e)",
+                 c->p.pcg_maxit, c->pcg_last_relres);
+        return PIC_ENONCONV;
+    }
+    return PIC_OK;
+}
+
+// The field solve of the configured solver; rho = dscale * (the raw charge planes).
+pic_status solve_field(pic_ctx* c, double dscale, int slot) {
+    if (c->p.solver == PIC_SOLVER_PCG) return solve_pcg(c, dscale, slot);
+    return solve(c, dscale / ((double)c->g.n * c->g.n * c->g.n), slot);   // 1/N^3 of the whole box
+}
+
 // push=1: the step's push of the sorted state (with migration at P > 1);
 // push=0: the state as is, any order.  The particles of buffer cur end sorted by
 // cell key in cur^1 and their charge is deposited; cur flips.
@@ -739,9 +909,6 @@ pic_status setup_p2p(pic_ctx* c) {
     return PIC_OK;
 }
 
-double solve_scale(const pic_ctx* c) {
-    return c->deposit_scale / ((double)c->g.n * c->g.n * c->g.n);   // 1/N^3 of the whole box
-}
 
 }  // namespace
 
@@ -761,6 +928,12 @@ pic_status pic_params_default(pic_params* p) {
     p->half_kick = 1;
     p->pgrid[0] = 1;
     p->pgrid[1] = 1;
+    p->solver = PIC_SOLVER_FFT;
+    p->pcg_inner = 4;
+    p->pcg_outer = 2;
+    p->pcg_maxit = 1000;
+    p->pcg_tol = 1e-4;
+    p->pcg_omega = M_PI / 2;      // P:260 "damping factor of pi/2"
     return PIC_OK;
 }
 
@@ -847,6 +1020,14 @@ pic_status pic_init(const pic_params* p, int32_t rank, int32_t nranks, const uin
             return bail(PIC_ENCCL);
         }
         if ((st = setup_p2p(c)) != PIC_OK) return bail(st);
+        if (p->solver == PIC_SOLVER_PCG && !c->p2p) {
+            snprintf(c->err, sizeof(c->err), "the PCG solver at P > 1 needs the peer-memory transport");
+            return bail(PIC_EUNSUPPORTED);
+        }
+    }
+    if (c->pcg_x) {   // warm start of the first solve: phi = 0
+        cudaError_t e0 = cudaMemsetAsync(c->pcg_x, 0, sizeof(double) * (size_t)c->ncell, c->stream);
+        if (e0 != cudaSuccess) return bail(fail(c, PIC_ECUDA, "pcg init", e0));
     }
     // twiddles W_n^m = exp(-2 pi i m / n), m < n
     std::vector<double2> tw(g.n);
@@ -881,7 +1062,7 @@ pic_status pic_init(const pic_params* p, int32_t rank, int32_t nranks, const uin
     c->cur = 0;
     if ((st = push_sort_deposit(c, 0)) != PIC_OK) return bail(st);
     if (p->half_kick) {
-        if ((st = solve(c, solve_scale(c), 0)) != PIC_OK) return bail(st);
+        if ((st = solve_field(c, c->deposit_scale, 0)) != PIC_OK) return bail(st);
         pic::launch_half_kick(g, state(c, c->cur), c->np, c->E4, c->stream);
         e = cudaGetLastError();
         if (e != cudaSuccess) return bail(fail(c, PIC_ECUDA, "half_kick", e));
@@ -902,12 +1083,11 @@ pic_status pic_init(const pic_params* p, int32_t rank, int32_t nranks, const uin
 pic_status pic_step(pic_ctx* c, int32_t nsteps, double* ex_energy) {
     PIC_CHECK_CTX(c);
     if (nsteps < 0) return PIC_EINVAL;
-    const double scale = solve_scale(c);
     int32_t done = 0;
     while (done < nsteps) {
         const int chunk = std::min(nsteps - done, kMaxEnergySteps);
         for (int s = 0; s < chunk; ++s) {
-            PIC_TRY(solve(c, scale, s));
+            PIC_TRY(solve_field(c, c->deposit_scale, s));
             PIC_TRY(push_sort_deposit(c, 1));
         }
         std::vector<double> en(2 * (size_t)chunk);
@@ -984,6 +1164,8 @@ pic_status pic_set_particles(pic_ctx* c, const double* xyzuvw, int64_t np) {
     pic::launch_soa_to_pairs(soa, np, state(c, c->cur), c->stream);
     PIC_LAUNCHED(c, "soa_to_pairs");
     c->np = np;
+    if (c->pcg_x)      // PCG: the imported state restarts from phi = 0 (like pic_init)
+        PIC_CUDA(c, cudaMemsetAsync(c->pcg_x, 0, sizeof(double) * (size_t)c->ncell, c->stream));
     PIC_TRY(push_sort_deposit(c, 0));
     c->last_slot = -1;
     return sync_check(c);
@@ -991,9 +1173,15 @@ pic_status pic_set_particles(pic_ctx* c, const double* xyzuvw, int64_t np) {
 
 pic_status pic_get_grid(pic_ctx* c, int32_t which, double* host) {
     PIC_CHECK_CTX(c);
-    if (!host || which < 0 || which > 3) return PIC_EINVAL;
+    if (!host || which < 0 || which > 4 || (which == 4 && !c->pcg_x)) return PIC_EINVAL;
     if (which == 0) {
         PIC_TRY(copy_grid_to_host(c, host, c->rho));
+    } else if (which == 4) {
+        double* scratch = reinterpret_cast<double*>(c->specC);
+        pic::launch_pcg_unsplit(c->g, c->pcg_x, scratch, c->stream);
+        PIC_LAUNCHED(c, "pcg_unsplit");
+        PIC_CUDA(c, cudaMemcpyAsync(host, scratch, sizeof(double) * (size_t)c->ncell,
+                                    cudaMemcpyDeviceToHost, c->stream));
     } else {
         double* scratch = reinterpret_cast<double*>(c->specC);
         pic::launch_e4_extract(c->g, c->E4, which - 1, scratch, c->stream);
@@ -1012,7 +1200,9 @@ pic_status pic_solve_injected(pic_ctx* c, const double* rho_host, double* E_host
     PIC_CHECK_CTX(c);
     if (!rho_host) return PIC_EINVAL;
     PIC_TRY(copy_grid_to_device(c, c->rho, rho_host));
-    PIC_TRY(solve(c, 1.0 / ((double)c->g.n * c->g.n * c->g.n), 0));
+    if (c->pcg_x)      // PCG: solve from phi = 0 (the particles' warm start is reset too)
+        PIC_CUDA(c, cudaMemsetAsync(c->pcg_x, 0, sizeof(double) * (size_t)c->ncell, c->stream));
+    PIC_TRY(solve_field(c, 1.0, 0));
     double en[2];
     PIC_CUDA(c, cudaMemcpyAsync(en, c->energies, sizeof(en), cudaMemcpyDeviceToHost, c->stream));
     if (E_host) {
@@ -1099,6 +1289,18 @@ pic_status pic_launches_per_step(pic_ctx* c, int64_t* launches) {
     // solve 6, push_key 1, scan 3, place 1, reorder_deposit 1; P > 1: arrivals 1, and
     // the NCCL transport's ghost fold 1 or the peer transport's count update 1
     *launches = 12 + (c->g.P > 1 ? 2 : 0);
+    if (c->p.solver == PIC_SOLVER_PCG) *launches += c->pcg_launches - 6;   // the latest PCG solve's count
+    return PIC_OK;
+}
+
+pic_status pic_pcg_stats(pic_ctx* c, int32_t* last_iters, int64_t* total_iters, int64_t* solves,
+                         double* last_relres) {
+    if (!c) return PIC_EINVAL;
+    if (c->p.solver != PIC_SOLVER_PCG) { snprintf(c->err, sizeof(c->err), "not a PCG context"); return PIC_EINVAL; }
+    if (last_iters) *last_iters = c->pcg_last_iters;
+    if (total_iters) *total_iters = c->pcg_total_iters;
+    if (solves) *solves = c->pcg_solves;
+    if (last_relres) *last_relres = c->pcg_last_relres;
     return PIC_OK;
 }
 
