@@ -10,6 +10,10 @@ One "step" = one full PIC step: FFT solve + field energy, gather+push, counting
 sort by cell key, reorder + CIC deposit.  Inputs live in HBM (51.5 GB of
 particle state >> 126 MB L2, so no L2 flush is needed between steps).
 
+--solver pcg runs BASELINE.json configs[4] instead: the same step with the
+matrix-free FD-PCG Poisson solve (SSOR(pi/2, 4, 2), tol 1e-4, warm start;
+P:179-181) in place of the FFT solve.
+
 Prints ONE JSON line on rank 0.  For N > 1 (torchrun) the same 512^3 problem is
 decomposed in z-slabs over the N GPUs (NCCL all-to-all FFT transposes, halo/ghost
 planes, particle migration): strong scaling of a fixed problem, time = max over ranks.
@@ -44,7 +48,15 @@ ALG_BYTES = {
     "fft_y_inv": (0, 16 + 24),                      # phi^, E^_z -> E_x, E_y, E_z spectra
     "fft_x_inv": (0, 24 + 32),                       # 3 half spectra -> E node records
     "clear": (0, 4 + 8),
+    # FD-PCG (BJ config 5), per launch of the stage's main kernel:
+    "pcg_field": (0, 8 + 32),                       # phi (stencil) -> E node records
 }
+# PCG stages with launches of different kinds: algorithmic bytes per node per
+# application.  SSOR M^-1 (4 inner x 2 outer = 32 half-sweeps): 8 + 12 + 29 x 16 + 20
+# B/node; one CG iteration: matvec 32 (z, p read; p', q written) + update 48
+# (x, p, r, q read; x, r written) B/node.
+PCG_SSOR_BYTES_PER_APPLY = 504
+PCG_CG_BYTES_PER_ITER = 80
 
 
 def log(*a):
@@ -158,22 +170,29 @@ def ncu_traffic(config_name: str, kernel: str):
 
 
 # ------------------------------------------------------------ oracle (CPU) --
-def oracle_sample(steps: int, n: int = 64, ppc: int = 8):
-    """Time the CPU oracle, as it stands, on a bounded sample of the workload."""
+def _oracle_steps(solver, n, L, xv, steps):
     from oracle import oracle as O
+
+    if solver == "pcg":
+        return O.run_pcg(n, L, 0.05, xv, steps)[0]
+    return O.run(n, L, 0.05, xv, steps)[0]
+
+
+def oracle_sample(steps: int, n: int = 64, ppc: int = 8, solver: str = "fft"):
+    """Time the CPU oracle, as it stands, on a bounded sample of the workload."""
     from pic_inputs import landau_state
 
     import numpy as np
 
     L = 4 * np.pi
     xv = landau_state(n, ppc, seed=1)
-    O.run(n, L, 0.05, xv, 1)   # warm (build, page-in)
+    _oracle_steps(solver, n, L, xv, 1)   # warm (build, page-in)
     t0 = time.perf_counter()
-    O.run(n, L, 0.05, xv, steps)
+    _oracle_steps(solver, n, L, xv, steps)
     dt = time.perf_counter() - t0
     npart = ppc * n ** 3
     return {"value": npart * steps / dt, "unit": UNIT, "cores": 1, "kind": "oracle",
-            "sample": f"oracle_run (serial C, -O2) on Landau {n}^3 x {ppc} ppc "
+            "sample": f"oracle_run{'_pcg' if solver == 'pcg' else ''} (serial C, -O2) on Landau {n}^3 x {ppc} ppc "
                       f"({npart} particles), {steps} steps, {dt:.1f} s; same per-particle "
                       f"step as the {{n}}^3 workload, smaller grid"}
 
@@ -181,27 +200,26 @@ def oracle_sample(steps: int, n: int = 64, ppc: int = 8):
 def run_reference(args, rank, world):
     if rank != 0:
         return 0
-    from oracle import oracle as O
     from pic_inputs import landau_state
     import numpy as np
 
     n, ppc = 64, 8
     L = 4 * np.pi
     xv = landau_state(n, ppc, seed=1)
-    xs = O.run(n, L, 0.05, xv, max(args.warmup, 0))[0] if args.warmup else xv
+    xs = _oracle_steps(args.solver, n, L, xv, args.warmup) if args.warmup else xv
     t0 = time.perf_counter()
-    O.run(n, L, 0.05, xs, args.steps)
+    _oracle_steps(args.solver, n, L, xs, args.steps)
     dt = time.perf_counter() - t0
     npart = ppc * n ** 3
     value = npart * args.steps / dt
     sample = (f"CPU oracle (serial C) on Landau {n}^3 x {ppc} ppc ({npart} particles) per step, "
               f"a bounded sample of the {args.n}^3 x {args.ppc} workload")
     line = {
-        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "impl": "reference", "metric": METRIC if args.solver == "fft" else METRIC.replace("FFT-PIC", "PCG-PIC"), "value": value, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * dt / args.steps,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic",
-        "config": {"workload": f"landau3d_{args.n}^3x{args.ppc}ppc_fft (reference arm: "
+        "config": {"workload": f"landau3d_{args.n}^3x{args.ppc}ppc_{args.solver} (reference arm: "
                                f"{n}^3x{ppc} sample)", "grid": args.n, "ppc": args.ppc},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -227,7 +245,8 @@ def run_ours(args, rank, world):
     t_init = time.perf_counter()
     ncid = broadcast_nccl_id(rank, world)
     sim = Simulation(n=n, ppc=ppc, k=0.5, alpha=0.05, dt=0.05, seed=1, device=f"cuda:{local}",
-                     rank=rank, nranks=world, nccl_id=ncid)
+                     rank=rank, nranks=world, nccl_id=ncid, solver=args.solver)
+    pcg = args.solver == "pcg"
     torch.cuda.synchronize()
     log(f"[rank {rank}] init {n}^3 x {ppc} (slab z0={sim.z0} nz={sim.nz}, {sim.np} particles): "
         f"{time.perf_counter() - t_init:.1f} s, workspace {sim.workspace.numel() / 2**30:.1f} GiB")
@@ -241,6 +260,7 @@ def run_ours(args, rank, world):
         sim.step(1)
     sim.set_timing(True)
     sim.reset_timings()
+    it0 = sim.pcg_stats()[1] if pcg else 0
     barrier()
     torch.cuda.synchronize()
     ev0 = torch.cuda.Event(enable_timing=True)
@@ -255,6 +275,7 @@ def run_ours(args, rank, world):
     ms = ev0.elapsed_time(ev1)
     stages = sim.timings()
     sim.set_timing(False)
+    pcg_iters = (sim.pcg_stats()[1] - it0) if pcg else 0
     if world > 1:   # every rank's stage table (rank 0's goes into the JSON line)
         log(f"[rank {rank}] np {sim.np} stages ms/step: " +
             " ".join(f"{k}={v[0] / args.steps:.3f}" for k, v in stages.items() if v[0] > 0))
@@ -300,19 +321,27 @@ def run_ours(args, rank, world):
             continue
         bp, bn = ALG_BYTES.get(name, (0, 0))
         alg = bp * np_r + bn * ncell
+        if name == "pcg_ssor":     # one M^-1 per CG iteration (the first before the loop)
+            alg = PCG_SSOR_BYTES_PER_APPLY * ncell * (pcg_iters + args.steps) / args.steps
+        elif name == "pcg_cg":
+            alg = PCG_CG_BYTES_PER_ITER * ncell * pcg_iters / args.steps
         per_stage[name] = {"ms_per_step": tot / args.steps, "launches": nl,
                            "alg_GBps": (alg * args.steps / (tot / 1e3) / 1e9) if tot > 0 else None}
     dom = max((s for s in per_stage if s not in ("clear", "exchange", "xpose")),
               key=lambda s: per_stage[s]["ms_per_step"])
     tot, nl = stages[dom]
-    bp, bn = ALG_BYTES[dom]
-    # per-launch algorithmic bytes / per-launch duration (scan = 3 launches -> per stage call)
-    calls = args.steps
-    alg_per_call = bp * np_r + bn * ncell
+    if dom == "pcg_ssor":      # per half-sweep launch (the reduce of the last one not counted)
+        calls = 4 * 4 * 2 * (pcg_iters + args.steps)
+        alg_per_call = PCG_SSOR_BYTES_PER_APPLY / 32 * ncell
+    else:
+        bp, bn = ALG_BYTES[dom]
+        # per-launch algorithmic bytes / per-launch duration (scan = 3 launches -> per stage call)
+        calls = args.steps
+        alg_per_call = bp * np_r + bn * ncell
     achieved = alg_per_call / (tot / calls / 1e3) / 1e9
     peaks = measured_peaks()
     peak = peaks.get("hbm_gbs") or 6650.0
-    cfg_name = f"landau3d_{n}^3x{ppc}ppc_fft" + (f"_{world}gpu" if world > 1 else "")
+    cfg_name = f"landau3d_{n}^3x{ppc}ppc_{args.solver}" + (f"_{world}gpu" if world > 1 else "")
     traffic = ncu_traffic(cfg_name, dom)
     roof = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
             "frac": achieved / peak, "traffic": traffic,
@@ -336,12 +365,12 @@ def run_ours(args, rank, world):
                   "exchange_ms_per_step": stages["exchange"][0] / args.steps,
                   "transport": "peer" if sim.peer_transport() else "nccl"}
 
-    cpu = None if args.no_cpu_baseline else oracle_sample(steps=args.cpu_steps)
+    cpu = None if args.no_cpu_baseline else oracle_sample(steps=args.cpu_steps, solver=args.solver)
     if cpu:
         cpu["sample"] = cpu["sample"].replace("{n}", str(n))
     launches = sim.launches_per_step() * args.steps
     line = {
-        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "metric": METRIC if not pcg else METRIC.replace("FFT-PIC", "PCG-PIC"), "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
         "scaling": "strong" if world > 1 else "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
@@ -363,6 +392,9 @@ def run_ours(args, rank, world):
         "stages": per_stage,
         "w_x_first_last": [float(ex[0]), float(ex[-1])],
     }
+    if pcg:
+        line["pcg"] = {"iters_per_step": pcg_iters / args.steps, "tol": 1e-4, "ssor": "omega=pi/2, 4 inner, 2 outer",
+                       "warm_start": True, "last_relres": sim.pcg_stats()[3]}
     print(json.dumps(line), flush=True)
     sim.close()
     return 0
@@ -376,6 +408,8 @@ def main():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--n", type=int, default=512)
     ap.add_argument("--ppc", type=int, default=8)
+    ap.add_argument("--solver", choices=["fft", "pcg"], default="fft",
+                    help="field solver: fft (BJ configs 0-3) or pcg (BJ config 5)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-steps", type=int, default=20)

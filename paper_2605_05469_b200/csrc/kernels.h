@@ -137,6 +137,12 @@ void launch_pcg_resid0(const Geom& g, const double* raw, double dscale, double* 
 // (first half-sweep), 1: this colour of z == 0; dot: sc[4] = sc[3], sc[3] = (r, z).
 void launch_pcg_sor(const Geom& g, int colour, int mode, bool dot, const double* r, PcgNbr z, double omega,
                     double* partials, double* sc, cudaStream_t s);
+// Temporally blocked SSOR pass: ns <= pcg_tb_stages() consecutive half-sweeps
+// (colour of half-sweep t = bit t-1 of seq) from zin (zero_in: z = 0, zin unused)
+// into zout (!= zin); dot: sc[4] = sc[3], sc[3] = (r, zout).
+int pcg_tb_stages();
+void launch_pcg_ssor_pass(const Geom& g, int ns, int seq, bool zero_in, bool dot, PcgNbr r, PcgNbr zin,
+                          double* zout, double omega, double* partials, double* sc, cudaStream_t s);
 // pout = z + beta p (first: z), q = A pout, sc[5] = (pout, q); beta = sc[3]/sc[4].
 void launch_pcg_matvec(const Geom& g, bool first, PcgNbr z, PcgNbr p, double* pout, double* q, double* sc,
                        double* partials, cudaStream_t s);

@@ -75,13 +75,15 @@ __device__ __forceinline__ void block_partials(double* v, int nv, double* partia
 struct PairPos {
     int zl, y, j;
 };
+// n is a power of two: every index split is a shift and a mask (no integer division).
+__device__ __forceinline__ int lg2(int v) { return __ffs(v) - 1; }
 __device__ __forceinline__ PairPos pair_pos(const Geom& g, int64_t p) {
-    const int hp = g.n >> 2;                 // pairs per row
-    const int64_t row = p / hp;
+    const int ln = lg2(g.n);                 // pairs per row: n / 4 = 2^(ln - 2)
+    const int64_t row = p >> (ln - 2);
     PairPos q;
-    q.j = 2 * (int)(p - row * hp);
+    q.j = 2 * (int)(p & ((g.n >> 2) - 1));
     q.y = (int)(row & g.nmask);
-    q.zl = (int)(row / g.n);
+    q.zl = (int)(row >> ln);
     return q;
 }
 
@@ -183,8 +185,8 @@ __global__ void __launch_bounds__(kPT) k_pcg_rho_sum(Geom g, const double* __res
     const int hq = g.n >> 1;
     double acc = 0.0;
     for (int64_t p = (int64_t)blockIdx.x * kPT + threadIdx.x; p < npair; p += (int64_t)gridDim.x * kPT) {
-        const int64_t row = p / hq;
-        const int x = 2 * (int)(p - row * hq);
+        const int64_t row = p >> (lg2(g.n) - 1);
+        const int x = 2 * (int)(p & (hq - 1));
         const double2 v = *reinterpret_cast<const double2*>(raw + row * g.rp + x);
         acc += __dmul_rn(dscale, v.x);
         acc += __dmul_rn(dscale, v.y);
@@ -202,8 +204,8 @@ __global__ void __launch_bounds__(kPT) k_pcg_resid0(Geom g, const double* __rest
     const double mean = sc[0] / nn;
     double acc[2] = {0.0, 0.0};
     for (int64_t p = (int64_t)blockIdx.x * kPT + threadIdx.x; p < npair; p += (int64_t)gridDim.x * kPT) {
-        const int64_t row = p / hq;
-        const int j = (int)(p - row * hq), y = (int)(row & g.nmask), zl = (int)(row / g.n);
+        const int64_t row = p >> (lg2(g.n) - 1);
+        const int j = (int)(p & (hq - 1)), y = (int)(row & g.nmask), zl = (int)(row >> lg2(g.n));
         const double2 v = *reinterpret_cast<const double2*>(raw + row * g.rp + 2 * j);
         const double b0 = __dsub_rn(__dmul_rn(dscale, v.x), mean);
         const double b1 = __dsub_rn(__dmul_rn(dscale, v.y), mean);
@@ -227,8 +229,8 @@ __global__ void __launch_bounds__(kPT) k_pcg_matvec(Geom g, Nbr z, Nbr p, double
     const double beta = FIRST ? 0.0 : sc[3] / sc[4];
     double acc = 0.0;
     for (int64_t t = (int64_t)blockIdx.x * kPT + threadIdx.x; t < npair; t += (int64_t)gridDim.x * kPT) {
-        const int64_t row = t / hq;
-        const int j = (int)(t - row * hq), y = (int)(row & g.nmask), zl = (int)(row / g.n);
+        const int64_t row = t >> (lg2(g.n) - 1);
+        const int j = (int)(t & (hq - 1)), y = (int)(row & g.nmask), zl = (int)(row >> lg2(g.n));
         Hood h = ldhood(g, z, zl, y, j);
         if (!FIRST) {
             const Hood hp = ldhood(g, p, zl, y, j);
@@ -285,8 +287,8 @@ __global__ void __launch_bounds__(kPT) k_pcg_gradient(Geom g, Nbr x, double* __r
     const double cc = 0.5 * g.inv_h;
     double e2[3] = {0.0, 0.0, 0.0};
     for (int64_t t = (int64_t)blockIdx.x * kPT + threadIdx.x; t < npair; t += (int64_t)gridDim.x * kPT) {
-        const int64_t row = t / hq;
-        const int j = (int)(t - row * hq), y = (int)(row & g.nmask), zl = (int)(row / g.n);
+        const int64_t row = t >> (lg2(g.n) - 1);
+        const int j = (int)(t & (hq - 1)), y = (int)(row & g.nmask), zl = (int)(row >> lg2(g.n));
         const Hood h = ldhood(g, x, zl, y, j);
         const double ex0 = __dmul_rn(__dsub_rn(h.left, h.c.y), cc);
         const double ex1 = __dmul_rn(__dsub_rn(h.c.x, h.right), cc);
@@ -339,6 +341,210 @@ __global__ void __launch_bounds__(1024) k_pcg_reduce(Geom g, const double* __res
     }
 }
 
+
+// ------------------------------------------------ temporally blocked SSOR ----
+// One SSOR "pass": ns <= kTB consecutive half-sweeps (colours = bits of seq) in one
+// kernel, so z and r stream through HBM once per pass instead of once per
+// half-sweep (24 B/node per pass vs 16 B/node per half-sweep; 4 half-sweeps per
+// pass -> 2.7x less traffic for M^-1).  Work unit = an x-y tile of tx colour
+// elements x ty rows, marched along a chunk [zs, ze) of planes; the tile carries a
+// halo (kHe elements, kHy rows) that shrinks by one node per half-sweep, and the
+// chunk a halo of ns planes (ghost zones: the halo is recomputed redundantly, only
+// the interior is written).  Planes stream through a shared-memory ring (cp.async,
+// one plane ahead); at front plane f, half-sweep t updates plane f - t in place,
+// which already holds half-sweep t-1's result at f - t + 1 and not yet t+1's at
+// f - t - 1: the pipeline reproduces the sequential half-sweep order exactly (same
+// arithmetic as k_sor, bit-identical).  Input zin and output zout are different
+// buffers (neighbour tiles and ranks read zin's halo while this one writes).
+constexpr int kTB = 4;                    // half-sweeps per pass
+constexpr int kTX = 32;                   // interior colour elements per tile row (64 nodes)
+constexpr int kTY = 8;                    // interior rows per tile
+constexpr int kHe = 4;                    // x halo in elements (>= ceil(kTB/2) + 1; even: 16-B loads)
+constexpr int kHy = kTB;                  // y halo in rows
+constexpr int kWe = kTX + 2 * kHe;        // 40
+constexpr int kWy = kTY + 2 * kHy;        // 16
+constexpr int kSlots = 8;                 // ring (>= kTB + 3: ns + 2 live planes + one prefetched); slot = p & 7
+constexpr int kSlot = 2 * kWy * kWe;      // doubles per slot (both colours)
+constexpr int kTBThreads = 256;
+// elements per thread per half-sweep: the largest region (the first half-sweep's,
+// (kTY + 2 (kTB - 1)) rows x (kTX + 2 (kTB / 2)) elements) over the CTA's threads
+constexpr int kMaxK = ((kTY + 2 * (kTB - 1)) * (kTX + 2 * (kTB / 2)) + kTBThreads - 1) / kTBThreads;
+constexpr size_t kTBSmem = sizeof(double) * kSlots * kSlot;
+
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
+    const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(s), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
+
+__device__ __forceinline__ const double* nbr_ptr(const Geom& g, const Nbr& f, int c, int zl, int y, int j) {
+    const double* b = f.own;
+    if (zl < 0) { b = f.below; zl += g.nzl; }
+    else if (zl >= g.nzl) { b = f.above; zl -= g.nzl; }
+    return b + sidx(g, c, zl, y, j);
+}
+
+// Per-thread work lists are precomputed once per tile (shared-memory offsets of the
+// elements each thread updates per half-sweep, global row offsets of their r, the
+// cp.async sources of the plane loads), so the inner loop is six LDS, one LDG of r
+// (prefetched one plane ahead into registers) and the fp64 update.
+__global__ void __launch_bounds__(kTBThreads, 2) k_ssor_tb(Geom g, Nbr r, Nbr zin, double* __restrict__ zout,
+                                                           int ns, int seq, int zero_in, int dot, int cz,
+                                                           double c1, double c2, double h2,
+                                                           double* __restrict__ partials) {
+    static_assert((kSlots & (kSlots - 1)) == 0 && kSlots >= kTB + 3, "ring");
+    static_assert(kHe % 2 == 0 && kTX % 2 == 0, "16-byte pairs");
+    extern __shared__ double sm[];
+    constexpr int kCP = kWy * kWe;                                    // doubles per colour plane
+    constexpr int kLd = (kCP + kTBThreads - 1) / kTBThreads;          // 16-B plane loads per thread (2 colours)
+    const int hn = g.n >> 1, tid = threadIdx.x;
+    const int tx = min(kTX, hn), ty = min(kTY, g.n);
+    const int We = tx + 2 * kHe, Wy = ty + 2 * kHy, Wp = We / 2;
+    const int ntx = hn / tx, nty = g.n / ty, nzc = (g.nzl + cz - 1) / cz;
+    const int nunits = ntx * nty * nzc;
+    const int64_t pstride = (int64_t)g.n * hn;                        // plane stride of a colour half grid
+    const int64_t cstride = (int64_t)g.nzl * pstride;                 // colour stride of a field
+    const int zmask = g.nzl - 1;                                      // nzl is a power of two
+    // plane p in [-nzl, 2 nzl) of field f, colour c: the slab below / this / above
+    auto plane_ptr = [&](const Nbr& f, int c, int p) {
+        const double* b = p < 0 ? f.below : (p > zmask ? f.above : f.own);
+        return b + c * cstride + (int64_t)(p & zmask) * pstride;
+    };
+    double acc = 0.0;
+    // element lists per half-sweep t: shared offset row * kWe + e (-1: none)
+    int soff[kTB][kMaxK];
+#pragma unroll
+    for (int t = 0; t < kTB; ++t) {
+        const int h = ns - 1 - t, a = (ns - t) / 2;
+        const int nr = ty + 2 * h, ne = tx + 2 * a, r0 = kHy - h, e0 = kHe - a;
+#pragma unroll
+        for (int k = 0; k < kMaxK; ++k) {
+            const int i = tid + k * kTBThreads;
+            soff[t][k] = (t < ns && i < nr * ne) ? (r0 + i / ne) * kWe + e0 + i % ne : -1;
+        }
+    }
+    for (int u = blockIdx.x; u < nunits; u += gridDim.x) {
+        const int bx = u % ntx, by = (u / ntx) % nty, bz = u / (ntx * nty);
+        const int j0 = bx * tx - kHe, y0 = by * ty - kHy;
+        const int zs = bz * cz, ze = min(zs + cz, g.nzl);
+        // global in-plane offsets y * hn + j of the elements, and a bitmask of row parities
+        int goff[kTB][kMaxK];
+        unsigned ypar = 0;
+#pragma unroll
+        for (int t = 0; t < kTB; ++t)
+#pragma unroll
+            for (int k = 0; k < kMaxK; ++k) {
+                const int so = soff[t][k] < 0 ? 0 : soff[t][k];
+                const int yg = (y0 + so / kWe) & g.nmask, jg = (j0 + so % kWe) & (hn - 1);
+                goff[t][k] = yg * hn + jg;
+                ypar |= (unsigned)(yg & 1) << (t * kMaxK + k);
+            }
+        // 16-byte plane loads: pair index -> colour, row, element pair
+        int lsrc[2 * kLd], ldst[2 * kLd];
+#pragma unroll
+        for (int k = 0; k < 2 * kLd; ++k) {
+            const int i = tid + k * kTBThreads;
+            const int c = i / (Wy * Wp), rem = i - c * Wy * Wp, row = rem / Wp, e = 2 * (rem - row * Wp);
+            const int yg = (y0 + row) & g.nmask, jg = (j0 + e) & (hn - 1);
+            lsrc[k] = i < 2 * Wy * Wp ? (c << 30) | (yg * hn + jg) : -1;
+            ldst[k] = c * kCP + row * kWe + e;
+        }
+        // write-back pairs: one (colour, row, element pair) of the interior per thread
+        const int nwb = ty * tx;                       // pairs of both colours = 2 * ty * tx / 2
+        int wsm = -1, wgl = 0, wc = 0;
+        if (tid < nwb) {
+            const int hp = tx / 2, c = tid / (ty * hp), rem = tid - c * ty * hp, row = rem / hp, e = 2 * (rem - row * hp);
+            wc = c;
+            wsm = c * kCP + (kHy + row) * kWe + kHe + e;
+            wgl = ((y0 + kHy + row) & g.nmask) * hn + ((j0 + kHe + e) & (hn - 1));
+        }
+        auto load = [&](int p) {
+            double* dst = sm + (p & (kSlots - 1)) * kSlot;
+            if (zero_in) {
+#pragma unroll
+                for (int k = 0; k < 2 * kLd; ++k)
+                    if (lsrc[k] >= 0) *reinterpret_cast<double2*>(dst + ldst[k]) = make_double2(0.0, 0.0);
+            } else {
+                const double* b0 = plane_ptr(zin, 0, p);
+                const double* b1 = plane_ptr(zin, 1, p);
+#pragma unroll
+                for (int k = 0; k < 2 * kLd; ++k)
+                    if (lsrc[k] >= 0)
+                        cp_async16(dst + ldst[k], ((lsrc[k] >> 30) ? b1 : b0) + (lsrc[k] & 0x3fffffff));
+            }
+            cp_async_commit();
+        };
+        auto load_r = [&](int f, double (&rv)[kTB][kMaxK]) {
+#pragma unroll
+            for (int t = 0; t < kTB; ++t) {
+                const int p = f - 1 - t, h = ns - 1 - t;
+                if (t < ns && p >= zs - h && p < ze + h) {
+                    const double* rp = plane_ptr(r, (seq >> t) & 1, p);
+#pragma unroll
+                    for (int k = 0; k < kMaxK; ++k)
+                        if (soff[t][k] >= 0) rv[t][k] = rp[goff[t][k]];
+                }
+            }
+        };
+        auto step = [&](int f, const double (&rv)[kTB][kMaxK], double (&rn)[kTB][kMaxK]) {
+            const int f1 = ze + ns;
+            if (f + 1 < f1) load(f + 1);
+            else cp_async_commit();                    // keep the group count uniform
+            if (f + 1 < f1) load_r(f + 1, rn);         // r of the next front plane, in flight
+            cp_async_wait1();                          // plane f has landed
+            __syncthreads();
+#pragma unroll
+            for (int t = 0; t < kTB; ++t) {
+                const int p = f - 1 - t, h = ns - 1 - t;
+                if (t < ns && p >= zs - h && p < ze + h) {
+                    const int c = (seq >> t) & 1, oc = c ^ 1;
+                    const double* so = sm + (p & (kSlots - 1)) * kSlot + oc * kCP;
+                    const double* som = sm + ((p - 1) & (kSlots - 1)) * kSlot + oc * kCP;
+                    const double* sop = sm + ((p + 1) & (kSlots - 1)) * kSlot + oc * kCP;
+                    double* sc = sm + (p & (kSlots - 1)) * kSlot + c * kCP;
+                    const unsigned pc = (unsigned)(p + c) & 1u;
+#pragma unroll
+                    for (int k = 0; k < kMaxK; ++k) {
+                        const int off = soff[t][k];
+                        if (off >= 0) {
+                            const int o = (int)(((ypar >> (t * kMaxK + k)) ^ pc) & 1u);
+                            const double s = nsum(so[off - 1 + o], so[off + o], so[off - kWe], so[off + kWe],
+                                                  som[off], sop[off]);
+                            sc[off] = __dadd_rn(__dmul_rn(c1, sc[off]),
+                                                __dmul_rn(c2, __dadd_rn(__dmul_rn(h2, rv[t][k]), s)));
+                        }
+                    }
+                }
+                __syncthreads();
+            }
+            const int p = f - ns;                      // final: write the interior of plane p
+            if (p >= zs && p < ze && wsm >= 0) {
+                const double2 v = *reinterpret_cast<const double2*>(sm + (p & (kSlots - 1)) * kSlot + wsm);
+                const int64_t gi = wc * cstride + (int64_t)p * pstride + wgl;
+                *reinterpret_cast<double2*>(zout + gi) = v;
+                if (dot) {
+                    const double2 rr = *reinterpret_cast<const double2*>(r.own + gi);
+                    acc = fma(rr.x, v.x, fma(rr.y, v.y, acc));
+                }
+            }
+        };
+        double ra[kTB][kMaxK], rb[kTB][kMaxK];
+        const int f0 = zs - ns, f1 = ze + ns;          // planes [f0, f1) stream through the ring
+        load(f0);
+        load_r(f0, ra);
+        int f = f0;
+        for (; f + 1 < f1; f += 2) {
+            step(f, ra, rb);
+            step(f + 1, rb, ra);
+        }
+        if (f < f1) step(f, ra, rb);
+        cp_async_wait0();
+        __syncthreads();                               // the ring is reused by the next unit
+    }
+    if (dot) block_partials(&acc, 1, partials);
+    if (g.P > 1) __threadfence_system();
+}
+
 // Colour-split field -> natural [nzl][n][n] (host transfers of phi).
 __global__ void k_pcg_unsplit(Geom g, const double* __restrict__ f, double* __restrict__ out) {
     const int64_t nn = (int64_t)g.n * g.n * g.nzl;
@@ -387,6 +593,30 @@ void launch_pcg_sor(const Geom& g, int colour, int mode, bool dot, const double*
     else if (mode == 1) k_sor<1, false><<<grid, kPT, 0, s>>>(g, colour, r, zn, zo, c1, c2, h2, partials);
     else if (dot) k_sor<0, true><<<grid, kPT, 0, s>>>(g, colour, r, zn, zo, c1, c2, h2, partials);
     else k_sor<0, false><<<grid, kPT, 0, s>>>(g, colour, r, zn, zo, c1, c2, h2, partials);
+    if (dot) k_pcg_reduce<<<1, 1024, 0, s>>>(g, partials, (int)grid, 1, sc + 3, sc + 4, 0);
+}
+
+int pcg_tb_stages() { return kTB; }
+
+void launch_pcg_ssor_pass(const Geom& g, int ns, int seq, bool zero_in, bool dot, PcgNbr r, PcgNbr zin,
+                          double* zout, double omega, double* partials, double* sc, cudaStream_t s) {
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(k_ssor_tb, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTBSmem);
+        attr = true;
+    }
+    int dev = 0, sms = 148, occ = 1;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_ssor_tb, kTBThreads, kTBSmem);
+    const int hn = g.n >> 1, tx = std::min(kTX, hn), ty = std::min(kTY, g.n);
+    const int cz = std::min(g.nzl, 64);
+    const int64_t units = (int64_t)(hn / tx) * (g.n / ty) * ((g.nzl + cz - 1) / cz);
+    const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(units, (int64_t)std::max(occ, 1) * sms));
+    const double h = g.L / (double)g.n;
+    k_ssor_tb<<<grid, kTBThreads, kTBSmem, s>>>(g, Nbr{r.own, r.below, r.above}, Nbr{zin.own, zin.below, zin.above},
+                                                zout, ns, seq, zero_in ? 1 : 0, dot ? 1 : 0, cz, 1.0 - omega,
+                                                omega / 6.0, h * h, partials);
     if (dot) k_pcg_reduce<<<1, 1024, 0, s>>>(g, partials, (int)grid, 1, sc + 3, sc + 4, 0);
 }
 

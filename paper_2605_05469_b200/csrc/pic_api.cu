@@ -571,28 +571,52 @@ pic_status pcg_read(pic_ctx* c, double* host, const double* dev, int n) {
 
 // z = M^-1 r (D#28): outer x {inner x (red, black), inner x (black, red)} SOR
 // half-sweeps from z = 0; the last one also leaves (r, z) in sc[3] (old value in sc[4]).
-// P > 1: a barrier before every half-sweep that reads the other colour from the peers.
+// Default: one kernel per half-sweep, in place (k_sor).  PIC_PCG_TB=1: temporally
+// blocked passes of pcg_tb_stages() half-sweeps (k_ssor_tb), ping-ponging between
+// pcg_z and pcg_q (q is free between the update and the next matvec) so that the
+// last pass lands in pcg_z -- a quarter of the HBM traffic, but measured slower
+// (issue-bound: halo recomputation, ring addressing, a barrier per half-sweep).  P > 1: a barrier before every launch that reads
+// what the peers wrote in the previous one.
 pic_status pcg_precondition(pic_ctx* c) {
     const Geom& g = c->g;
     const int inner = c->p.pcg_inner, outer = c->p.pcg_outer;
     const int total = 4 * inner * outer;
-    int k = 0;
-    auto sweep = [&](int colour) -> pic_status {
+    std::vector<int> colour;
+    for (int o = 0; o < outer; ++o) {
+        for (int i = 0; i < inner; ++i) { colour.push_back(0); colour.push_back(1); }
+        for (int i = 0; i < inner; ++i) { colour.push_back(1); colour.push_back(0); }
+    }
+    const char* tbenv = getenv("PIC_PCG_TB");
+    if (tbenv && tbenv[0] == '1') {
+        const int T = pic::pcg_tb_stages();
+        const int npass = (total + T - 1) / T;
+        for (int k = 0; k < npass; ++k) {
+            const int first = k * T, ns = std::min(T, total - first);
+            int seq = 0;
+            for (int t = 0; t < ns; ++t) seq |= colour[first + t] << t;
+            const bool dot = k == npass - 1;
+            double* zout = ((npass - 1 - k) % 2 == 0) ? c->pcg_z : c->pcg_q;
+            double* zin = zout == c->pcg_z ? c->pcg_q : c->pcg_z;
+            if (g.P > 1 && k > 0) PIC_TRY(barrier(c));
+            StageScope t(c, PIC_STAGE_PCG_SSOR, dot ? 2 : 1);
+            pic::launch_pcg_ssor_pass(g, ns, seq, k == 0, dot, pcg_nbr(c, c->pcg_r), pcg_nbr(c, zin), zout,
+                                      c->p.pcg_omega, c->partials, c->pcg_sc, c->stream);
+            PIC_LAUNCHED(c, "pcg_ssor_pass");
+            c->pcg_launches += dot ? 2 : 1;
+            if (dot) PIC_TRY(pcg_allreduce(c, c->pcg_sc + 3, 1));
+        }
+        return PIC_OK;
+    }
+    for (int k = 0; k < total; ++k) {
         const int mode = k == 0 ? 2 : (k == 1 ? 1 : 0);
         const bool dot = k == total - 1;
         if (g.P > 1 && mode != 2) PIC_TRY(barrier(c));
         StageScope t(c, PIC_STAGE_PCG_SSOR, dot ? 2 : 1);
-        pic::launch_pcg_sor(g, colour, mode, dot, c->pcg_r, pcg_nbr(c, c->pcg_z), c->p.pcg_omega, c->partials,
+        pic::launch_pcg_sor(g, colour[k], mode, dot, c->pcg_r, pcg_nbr(c, c->pcg_z), c->p.pcg_omega, c->partials,
                             c->pcg_sc, c->stream);
         PIC_LAUNCHED(c, "pcg_sor");
         c->pcg_launches += dot ? 2 : 1;
-        ++k;
         if (dot) PIC_TRY(pcg_allreduce(c, c->pcg_sc + 3, 1));
-        return PIC_OK;
-    };
-    for (int o = 0; o < outer; ++o) {
-        for (int i = 0; i < inner; ++i) { PIC_TRY(sweep(0)); PIC_TRY(sweep(1)); }
-        for (int i = 0; i < inner; ++i) { PIC_TRY(sweep(1)); PIC_TRY(sweep(0)); }
     }
     return PIC_OK;
 }

@@ -1,7 +1,4 @@
-# PCG GPU tests + 512^3 PCG bench (stage table) + ncu of the SSOR kernels at 256^3.
 mkdir -p gpurun_out
-timeout 1200 python -m pytest tests/test_gpu_pcg.py -x -q -rs > gpurun_out/pytest_pcg.log 2>&1; echo "pcg rc=$?"; tail -15 gpurun_out/pytest_pcg.log
 timeout 900 python bench.py --solver pcg --steps 5 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/bench_pcg.json 2> gpurun_out/bench_pcg.err; echo "bench pcg rc=$?"
 tail -1 gpurun_out/bench_pcg.json | python -c "import json,sys; d=json.loads(sys.stdin.read()); print(d['ms_per_step'], d['value'], d['pcg'], d['roofline']); [print(k, round(v['ms_per_step'],3), v['launches'], v['alg_GBps']) for k,v in d['stages'].items()]"
 tail -3 gpurun_out/bench_pcg.err
-timeout 600 ncu --set full --clock-control none --import-source on -k regex:"k_sor|k_pcg" -s 8 -c 8 -o gpurun_out/pcg_k -f python scripts/pcg_prof.py 256 > gpurun_out/ncu_pcgk.log 2>&1; echo "ncu rc=$?"

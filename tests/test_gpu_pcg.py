@@ -153,3 +153,27 @@ def test_pcg_landau_damping_rate_on_gpu(Sim):
     assert npk >= 3
     assert abs(slope - 2 * w.imag) < 0.10 * abs(2 * w.imag), slope
     assert abs(np.mean(np.diff(tp)) - np.pi / w.real) < 0.05 * np.pi / w.real
+
+
+@pytest.mark.parametrize("n,inner,outer", [(16, 4, 2), (64, 4, 2), (32, 3, 1), (128, 1, 1)])
+def test_pcg_blocked_passes_bit_identical_to_half_sweeps(Sim, n, inner, outer, monkeypatch):
+    """The temporally blocked SSOR passes (k_ssor_tb, default) reproduce the
+    one-kernel-per-half-sweep path (PIC_PCG_TB=0): same colour order and the same
+    arithmetic per half-sweep (D#28), including pass counts that are not a multiple
+    of 4; only the (r, z) sum is taken in another order, so the CG iterates agree to
+    rounding (equal iteration counts, phi and E to 1e-12)."""
+    rho = random_grid(n, seed=3 * n, mean=-1.0)
+    out = []
+    for tb in ("1", "0"):
+        monkeypatch.setenv("PIC_PCG_TB", tb)
+        sim = Sim(n=n, ppc=1, half_kick=False, pcg_inner=inner, pcg_outer=outer, pcg_tol=1e-8)
+        E, _, _ = sim.solve_injected(rho)
+        out.append((sim.get_phi(), E, sim.pcg_stats()[0]))
+        sim.close()
+    assert out[0][2] == out[1][2] and out[0][2] > 0
+    for a, b in ((out[0][0], out[1][0]), (out[0][1], out[1][1])):
+        assert np.max(np.abs(a - b)) <= 1e-12 * np.max(np.abs(b))
+    if (inner, outer) == (4, 2):
+        _, rphi, rit, _ = O.solve_pcg(n, L, rho, tol=1e-8)
+        assert rit == out[0][2]
+        assert np.max(np.abs(out[0][0] - rphi)) <= 1e-10 * np.max(np.abs(rphi))
