@@ -39,11 +39,19 @@ def main():
         return obj[0]
 
     L, dt = 4 * np.pi, 0.05
+    solver = os.environ.get("MP_SOLVER", "fft")     # "pcg": BJ config 5 (FD-PCG solve)
+
+    def oracle_run(xv0, nsteps, phi0=None):
+        if solver == "pcg":
+            ref, rex, _, _, _ = O.run_pcg(n, L, dt, xv0, nsteps, phi0=phi0)
+            return ref, rex
+        ref, rex, _, _ = O.run(n, L, dt, xv0, nsteps)
+        return ref, rex
 
     # ---- case 1: import the same global state, step, compare with the oracle
     xv = landau_state(n, ppc, seed=11)
     mine = slab_select(xv, n, L, rank, world)
-    sim = Simulation(n=n, ppc=ppc, half_kick=False, rank=rank, nranks=world, nccl_id=fresh_id())
+    sim = Simulation(n=n, ppc=ppc, half_kick=False, rank=rank, nranks=world, nccl_id=fresh_id(), solver=solver)
     sim.set_particles(mine)
     ex = sim.step(steps)
     got = sim.get_particles()
@@ -59,7 +67,7 @@ def main():
         allk = np.concatenate([p[1] for p in parts])
         order = np.argsort(allk, kind="stable")
         allx, allk = allx[:, order], allk[order]
-        ref, rex, _, _ = O.run(n, L, dt, xv, steps)
+        ref, rex = oracle_run(xv, steps)
         assert allx.shape == ref.shape, (allx.shape, ref.shape)
         assert np.all(np.diff(allk.astype(np.int64)) >= 0)
         flips = int(np.count_nonzero(allk != O.keys(n, L, ref)))
@@ -78,18 +86,21 @@ def main():
     sim.close()
 
     # ---- case 2: the library's own sampler on P ranks
-    sim = Simulation(n=n, ppc=ppc, seed=9, rank=rank, nranks=world, nccl_id=fresh_id())
+    sim = Simulation(n=n, ppc=ppc, seed=9, rank=rank, nranks=world, nccl_id=fresh_id(), solver=solver)
     ex2 = sim.step(10)
     npl = sim.np
     counts = [None] * world
     dist.all_gather_object(counts, npl)
     if rank == 0:
         assert sum(counts) == ppc * n ** 3, counts
-        ref0 = O.init_state(n, ppc, seed=9)
-        _, rex2, _, _ = O.run(n, L, dt, ref0, 10)
+        if solver == "pcg":
+            ref0, phi0 = O.init_state_pcg(n, ppc, seed=9)
+        else:
+            ref0, phi0 = O.init_state(n, ppc, seed=9), None
+        _, rex2 = oracle_run(ref0, 10, phi0)
         rel2 = np.max(np.abs(ex2 - rex2) / rex2)
         assert rel2 <= 1e-9, rel2
-        print(f"MP OK P={world} n={n} ppc={ppc} steps={steps} transport={transport} | {msg1} | "
+        print(f"MP OK P={world} n={n} ppc={ppc} steps={steps} solver={solver} transport={transport} | {msg1} | "
               f"init: W_x rel {rel2:.1e} counts {counts}",
               flush=True)
     sim.close()
