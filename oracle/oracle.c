@@ -607,3 +607,80 @@ void oracle_half_kick_pcg(int32_t n, double L, double dt, int64_t np, double *xv
     free(E);
     free(rho);
 }
+
+/* ================================== external fields and the Boris push ==== *
+ * Eq. 1 / Eq. 3-4: dv/dt = (q/m)(E_int + E_ext + v x B_ext).
+ * B_ext = 0: the leapfrog kick of oracle_push (bit for bit).  B_ext != 0: the Boris
+ * scheme (half kick, rotation, half kick), reading D#32:
+ *   hq = (q/m) dt / 2, t = hq B, s = 2 t / (1 + |t|^2),
+ *   v- = v + hq E, v' = v- + v- x t, v+ = v- + v' x s, v <- v+ + hq E,
+ * with E = E_p + E_ext (E_ext added only when nonzero), fma where written. */
+static void cross3(const double a[3], const double b[3], double c[3]) {
+    c[0] = a[1] * b[2] - a[2] * b[1];
+    c[1] = a[2] * b[0] - a[0] * b[2];
+    c[2] = a[0] * b[1] - a[1] * b[0];
+}
+
+void oracle_boris_coeffs(double dt, const double *b_ext, double t[3], double s[3]) {
+    const double hq = 0.5 * (-1.0 * dt);   /* (q/m) dt / 2, q/m = -1 */
+    for (int d = 0; d < 3; ++d) t[d] = hq * b_ext[d];
+    const double tt = (t[0] * t[0] + t[1] * t[1]) + t[2] * t[2];
+    for (int d = 0; d < 3; ++d) s[d] = (2.0 * t[d]) / (1.0 + tt);
+}
+
+void oracle_push_ext(double L, int64_t np, double *xv, const double *Ep, double dt, const double *b_ext,
+                     const double *e_ext) {
+    const double qm_dt = -1.0 * dt, hq = 0.5 * (-1.0 * dt);
+    const int boris = b_ext && (b_ext[0] != 0.0 || b_ext[1] != 0.0 || b_ext[2] != 0.0);
+    const int eext = e_ext && (e_ext[0] != 0.0 || e_ext[1] != 0.0 || e_ext[2] != 0.0);
+    double t[3] = {0.0, 0.0, 0.0}, s[3] = {0.0, 0.0, 0.0};
+    if (boris) oracle_boris_coeffs(dt, b_ext, t, s);
+    for (int64_t j = 0; j < np; ++j) {
+        double e[3], v[3];
+        for (int d = 0; d < 3; ++d) {
+            e[d] = eext ? Ep[d * np + j] + e_ext[d] : Ep[d * np + j];
+            v[d] = xv[(3 + d) * np + j];
+        }
+        if (!boris) {
+            for (int d = 0; d < 3; ++d) v[d] = fma(qm_dt, e[d], v[d]);
+        } else {
+            double vm[3], vp[3], vs[3], c[3];
+            for (int d = 0; d < 3; ++d) vm[d] = fma(hq, e[d], v[d]);
+            cross3(vm, t, c);
+            for (int d = 0; d < 3; ++d) vp[d] = vm[d] + c[d];
+            cross3(vp, s, c);
+            for (int d = 0; d < 3; ++d) vs[d] = vm[d] + c[d];
+            for (int d = 0; d < 3; ++d) v[d] = fma(hq, e[d], vs[d]);
+        }
+        for (int d = 0; d < 3; ++d) {
+            xv[(3 + d) * np + j] = v[d];
+            xv[d * np + j] = oracle_wrap(fma(v[d], dt, xv[d * np + j]), L);
+        }
+    }
+}
+
+void oracle_run_ext(int32_t n, double L, double dt, int64_t np, double *xv, int32_t nsteps,
+                    double *ex_energy, double *tot_energy, const double *b_ext, const double *e_ext) {
+    const int64_t nn = (int64_t)n * n * n;
+    const double q = -((L * L) * L) / (double)np;
+    double *rho = (double *)malloc(sizeof(double) * (size_t)nn);
+    double *E = (double *)malloc(sizeof(double) * (size_t)nn * 3);
+    double *Ep = (double *)malloc(sizeof(double) * (size_t)(np > 0 ? np : 1) * 3);
+    uint32_t *perm = (uint32_t *)malloc(sizeof(uint32_t) * (size_t)(np > 0 ? np : 1));
+    oracle_sort(n, L, np, xv, perm);
+    for (int32_t s = 0; s < nsteps; ++s) {
+        oracle_deposit(n, L, np, xv, q, rho);
+        oracle_solve_fft(n, L, rho, E);
+        double wx, w;
+        oracle_field_energy(n, L, E, &wx, &w);
+        if (ex_energy) ex_energy[s] = wx;
+        if (tot_energy) tot_energy[s] = w;
+        oracle_gather(n, L, np, xv, E, Ep);
+        oracle_push_ext(L, np, xv, Ep, dt, b_ext, e_ext);
+        oracle_sort(n, L, np, xv, perm);
+    }
+    free(perm);
+    free(Ep);
+    free(E);
+    free(rho);
+}

@@ -97,6 +97,16 @@ void oracle_run_pcg(int32_t n, double L, double dt, int64_t np, double *xv, int3
 void oracle_half_kick_pcg(int32_t n, double L, double dt, int64_t np, double *xv, double *phi, double tol,
                           double omega, int32_t inner, int32_t outer, int32_t maxit);
 
+/* ---- external fields and the Boris push (Eq. 1, 3-4: P:97; D#32) ---- */
+/* t = (q/m)(dt/2) B_ext, s = 2 t / (1 + |t|^2). */
+void oracle_boris_coeffs(double dt, const double *b_ext, double t[3], double s[3]);
+/* Kick (leapfrog if B_ext = 0, else Boris) with E = E_p + E_ext, drift, wrap. */
+void oracle_push_ext(double L, int64_t np, double *xv, const double *Ep, double dt, const double *b_ext,
+                     const double *e_ext);
+/* oracle_run (FFT solve) with uniform external fields B_ext, E_ext. */
+void oracle_run_ext(int32_t n, double L, double dt, int64_t np, double *xv, int32_t nsteps,
+                    double *ex_energy, double *tot_energy, const double *b_ext, const double *e_ext);
+
 #ifdef __cplusplus
 }
 #endif

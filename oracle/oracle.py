@@ -69,6 +69,9 @@ def lib():
             "oracle_run_pcg": (None, [i32, dbl, dbl, i64, dp, i32, dp, dp, dp, dbl, dbl, i32, i32,
                                       i32, C.POINTER(C.c_int32)]),
             "oracle_half_kick_pcg": (None, [i32, dbl, dbl, i64, dp, dp, dbl, dbl, i32, i32, i32]),
+            "oracle_boris_coeffs": (None, [dbl, dp, dp, dp]),
+            "oracle_push_ext": (None, [dbl, i64, dp, dp, dbl, dp, dp]),
+            "oracle_run_ext": (None, [i32, dbl, dbl, i64, dp, i32, dp, dp, dp, dp]),
         }
         for name, (res, args) in sig.items():
             f = getattr(L, name)
@@ -285,3 +288,32 @@ def init_state_pcg(n: int, ppc: int, k: float = 0.5, alpha: float = 0.05, seed: 
     phi = np.zeros((n, n, n))
     lib().oracle_half_kick_pcg(n, L, dt, xv.shape[1], _dp(xv), _dp(phi), tol, omega, inner, outer, maxit)
     return xv, phi
+
+
+# ------------------------------- external fields, Boris push ----
+def _vec3(v):
+    return np.ascontiguousarray(np.zeros(3) if v is None else v, dtype=np.float64)
+
+
+def boris_coeffs(dt: float, b_ext):
+    t, s = np.zeros(3), np.zeros(3)
+    lib().oracle_boris_coeffs(dt, _dp(_vec3(b_ext)), _dp(t), _dp(s))
+    return t, s
+
+
+def push_ext(L: float, xv: np.ndarray, Ep: np.ndarray, dt: float, b_ext=None, e_ext=None) -> np.ndarray:
+    out = np.ascontiguousarray(xv, dtype=np.float64).copy()
+    Ep = np.ascontiguousarray(Ep, dtype=np.float64)
+    b, e = _vec3(b_ext), _vec3(e_ext)
+    lib().oracle_push_ext(L, out.shape[1], _dp(out), _dp(Ep), dt, _dp(b), _dp(e))
+    return out
+
+
+def run_ext(n: int, L: float, dt: float, xv: np.ndarray, nsteps: int, b_ext=None, e_ext=None):
+    """oracle.run with uniform external fields.  Returns (xv, W_x[n], W[n])."""
+    xs = np.ascontiguousarray(xv, dtype=np.float64).copy()
+    ex = np.zeros(max(nsteps, 1))
+    tot = np.zeros(max(nsteps, 1))
+    b, e = _vec3(b_ext), _vec3(e_ext)
+    lib().oracle_run_ext(n, L, dt, xs.shape[1], _dp(xs), nsteps, _dp(ex), _dp(tot), _dp(b), _dp(e))
+    return xs, ex[:nsteps], tot[:nsteps]
