@@ -77,6 +77,10 @@ typedef struct {
     int32_t  pcg_maxit; /* PCG: iteration cap, >= 1; default 1000                         */
     double   pcg_tol;   /* PCG: relative residual tolerance, > 0; default 1e-4    */
     double   pcg_omega; /* PCG: SSOR relaxation, 0 < omega < 2; default pi/2      */
+    double   b_ext[3];  /* uniform external magnetic field (Eq. 1); default 0.  Nonzero:
+                           the push is the Boris scheme (D#32)            */
+    double   e_ext[3];  /* uniform external electric field added to E_int at the particles
+                           (Eq. 1); default 0.  pic_init's half kick uses E_int only     */
 } pic_params;
 
 /* Fill *p with the Landau-damping defaults of P:146 (N=16, ppc=8, k=0.5, alpha=0.05,

@@ -48,6 +48,8 @@ class pic_params(C.Structure):
         ("pcg_maxit", C.c_int32),
         ("pcg_tol", C.c_double),
         ("pcg_omega", C.c_double),
+        ("b_ext", C.c_double * 3),
+        ("e_ext", C.c_double * 3),
     ]
 
 
@@ -126,6 +128,10 @@ def default_params(**kw) -> pic_params:
     for k, v in kw.items():
         if k == "pgrid":
             p.pgrid[0], p.pgrid[1] = v
+        elif k in ("b_ext", "e_ext"):
+            arr = getattr(p, k)
+            for d in range(3):
+                arr[d] = float(v[d])
         else:
             setattr(p, k, v)
     return p
@@ -170,7 +176,8 @@ class Simulation:
                  length=0.0, device=None, rank=0, nranks=1, nccl_id: bytes | None = None,
                  solver="fft", **pcg):
         """solver: "fft" or "pcg" (BJ config 5); pcg keywords
-        pcg_tol, pcg_omega, pcg_inner, pcg_outer, pcg_maxit override P:226 / P:260."""
+        pcg_tol, pcg_omega, pcg_inner, pcg_outer, pcg_maxit override P:226 / P:260;
+        b_ext=(bx, by, bz) / e_ext=(ex, ey, ez): uniform external fields (Eq. 1, D#32)."""
         import torch
 
         self.params = default_params(n=n, ppc=ppc, k=k, alpha=alpha, dt=dt, seed=seed,

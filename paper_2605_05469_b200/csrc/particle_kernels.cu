@@ -280,9 +280,8 @@ __global__ void __launch_bounds__(kThreads, MR ? 3 : 4) k_push_key_brick(Geom g,
                     e1 = __fma_rn(wt, e.y, e1);
                     e2 = __fma_rn(wt, e.z, e2);
                 }
-        v[0] = __fma_rn(g.qm_dt, e0, v[0]);
-        v[1] = __fma_rn(g.qm_dt, e1, v[1]);
-        v[2] = __fma_rn(g.qm_dt, e2, v[2]);
+        double ep[3] = {e0, e1, e2};
+        kick(g, ep, v);
         drift(g, x, v);
         st_zv(cur.zv + 2 * i, make_double2(z0, v[2]), make_double2(v[0], v[1]));   // kicked v in place
         int iz;

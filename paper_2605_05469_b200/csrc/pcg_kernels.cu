@@ -18,6 +18,8 @@
 //
 // Dot products: grid-stride kernels with a fixed grid leave one partial per CTA;
 // k_pcg_reduce sums them in a fixed order (deterministic run to run).
+#include <cstdlib>
+
 #include "kernels.h"
 
 namespace pic {
@@ -140,42 +142,78 @@ __global__ void __launch_bounds__(kPT) k_sor(Geom g, int c, const double* __rest
     if (g.P > 1) __threadfence_system();
 }
 
-// ------------------------------------------------------- natural pairs ------
-// Values of a field at the nodes x = 2j, 2j+1 of row (y, zl) (zl in [-1, nzl]).
-__device__ __forceinline__ double2 ldnat(const Geom& g, const Nbr& f, int zl, int y, int j) {
-    const int c0 = (y + zl) & 1;   // colour of x = 2j (zl + nzl has the parity of zl)
-    return make_double2(ldz(g, f, c0, zl, y, j), ldz(g, f, c0 ^ 1, zl, y, j));
+// 256-bit accesses (LDG/STG.E.ENL2.256): four consecutive elements of a colour row.
+struct Q4 {
+    double v[4];
+};
+__device__ __forceinline__ Q4 ld4(const double* p) {
+    Q4 q;
+    asm volatile("ld.global.v4.f64 {%0, %1, %2, %3}, [%4];"
+                 : "=d"(q.v[0]), "=d"(q.v[1]), "=d"(q.v[2]), "=d"(q.v[3]) : "l"(p));
+    return q;
 }
-__device__ __forceinline__ void stnat(const Geom& g, double* f, int zl, int y, int j, double2 v) {
-    const int c0 = (y + zl) & 1;
-    f[sidx(g, c0, zl, y, j)] = v.x;
-    f[sidx(g, c0 ^ 1, zl, y, j)] = v.y;
+__device__ __forceinline__ void st4(double* p, const Q4& q) {
+    asm volatile("st.global.v4.f64 [%0], {%1, %2, %3, %4};" ::"l"(p), "d"(q.v[0]), "d"(q.v[1]), "d"(q.v[2]),
+                 "d"(q.v[3])
+                 : "memory");
+}
+__device__ __forceinline__ const double* zrow(const Geom& g, const Nbr& f, int c, int zl, int y, int j) {
+    const double* b = f.own;
+    if (zl < 0) { b = f.below; zl += g.nzl; }
+    else if (zl >= g.nzl) { b = f.above; zl -= g.nzl; }
+    return b + sidx(g, c, zl, y, j);
 }
 
-// The seven-point neighbourhood of the node pair (2j, 2j+1): left = node 2j - 1,
-// right = node 2j + 2, and the pairs of rows y +- 1 and planes zl +- 1.
-struct Hood {
-    double2 c, ym, yp, zm, zp;
-    double left, right;
-};
-__device__ __forceinline__ Hood ldhood(const Geom& g, const Nbr& f, int zl, int y, int j) {
-    const int hn = g.n >> 1, c0 = (y + zl) & 1;
-    Hood h;
-    h.c = ldnat(g, f, zl, y, j);
-    h.left = ldz(g, f, c0 ^ 1, zl, y, (j - 1) & (hn - 1));
-    h.right = ldz(g, f, c0, zl, y, (j + 1) & (hn - 1));
-    h.ym = ldnat(g, f, zl, (y - 1) & g.nmask, j);
-    h.yp = ldnat(g, f, zl, (y + 1) & g.nmask, j);
-    h.zm = ldnat(g, f, zl - 1, y, j);
-    h.zp = ldnat(g, f, zl + 1, y, j);
-    return h;
-}
-// -Delta_h at the pair (D#26): (6 x - nb) * ih2, nb in the oracle's order.
-__device__ __forceinline__ double2 apply_A(const Hood& h, double ih2) {
-    const double s0 = nsum(h.left, h.c.y, h.ym.x, h.yp.x, h.zm.x, h.zp.x);
-    const double s1 = nsum(h.c.x, h.right, h.ym.y, h.yp.y, h.zm.y, h.zp.y);
-    return make_double2(__dmul_rn(__dsub_rn(__dmul_rn(6.0, h.c.x), s0), ih2),
-                        __dmul_rn(__dsub_rn(__dmul_rn(6.0, h.c.y), s1), ih2));
+// The half-sweep with four elements j .. j+3 per thread (j = 0 mod 4): every row of
+// the stencil is one 256-bit load, so a thread issues 8 loads for 4 updates (k_sor: 8
+// for 2).  Same arithmetic and order as k_sor (bit-identical results).
+template <int MODE, bool DOT>
+__global__ void __launch_bounds__(kPT) k_sor4(Geom g, int c, const double* __restrict__ r, Nbr z, double* zout,
+                                              double c1, double c2, double h2, double* __restrict__ partials) {
+    const int hn = g.n >> 1, oc = c ^ 1, ln = lg2(g.n);
+    const int64_t nq = (int64_t)g.n * g.nzl * (g.n >> 3);      // quads of one colour
+    double acc = 0.0;
+    for (int64_t p = (int64_t)blockIdx.x * kPT + threadIdx.x; p < nq; p += (int64_t)gridDim.x * kPT) {
+        const int64_t row = p >> (ln - 3);
+        const int j = 4 * (int)(p & ((g.n >> 3) - 1)), y = (int)(row & g.nmask), zl = (int)(row >> ln);
+        const int o = (y + zl + c) & 1;                          // x of element j is 2j + o
+        const int64_t me = sidx(g, c, zl, y, j);
+        const Q4 rv = ld4(r + me);
+        Q4 zn, m;
+        if (MODE == 2) {
+#pragma unroll
+            for (int q = 0; q < 4; ++q) zn.v[q] = __dmul_rn(c2, __dmul_rn(h2, rv.v[q]));
+        } else {
+            m = ld4(zrow(g, z, oc, zl, y, j));
+            const double e = o ? *zrow(g, z, oc, zl, y, (j + 4) & (hn - 1)) : *zrow(g, z, oc, zl, y, (j - 1) & (hn - 1));
+            const Q4 ym = ld4(zrow(g, z, oc, zl, (y - 1) & g.nmask, j));
+            const Q4 yp = ld4(zrow(g, z, oc, zl, (y + 1) & g.nmask, j));
+            const Q4 zm = ld4(zrow(g, z, oc, zl - 1, y, j));
+            const Q4 zp = ld4(zrow(g, z, oc, zl + 1, y, j));
+            Q4 zo;
+            if (MODE == 0) zo = ld4(z.own + me);
+            // other colour at j - 1 + o .. j + 4 + o - 1: element q has x-neighbours w[q], w[q + 1]
+            const double w[5] = {o ? m.v[0] : e, o ? m.v[1] : m.v[0], o ? m.v[2] : m.v[1], o ? m.v[3] : m.v[2],
+                                 o ? e : m.v[3]};
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const double sq = nsum(w[q], w[q + 1], ym.v[q], yp.v[q], zm.v[q], zp.v[q]);
+                const double zq = MODE == 0 ? zo.v[q] : 0.0;
+                zn.v[q] = __dadd_rn(__dmul_rn(c1, zq), __dmul_rn(c2, __dadd_rn(__dmul_rn(h2, rv.v[q]), sq)));
+            }
+        }
+        st4(zout + me, zn);
+        if (DOT) {
+            const Q4 ro = ld4(r + sidx(g, oc, zl, y, j));
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                acc = fma(rv.v[q], zn.v[q], acc);
+                acc = fma(ro.v[q], m.v[q], acc);
+            }
+        }
+    }
+    if (DOT) block_partials(&acc, 1, partials);
+    if (g.P > 1) __threadfence_system();
 }
 
 // sum_m rho_m, rho_m = dscale * raw_m (the raw CIC sums of the pitched rho planes).
@@ -194,121 +232,188 @@ __global__ void __launch_bounds__(kPT) k_pcg_rho_sum(Geom g, const double* __res
     block_partials(&acc, 1, partials);
 }
 
-// r = (rho - mean) - A x (D#27), partials of (b, b) and (r, r).  Thread = natural pair.
-__global__ void __launch_bounds__(kPT) k_pcg_resid0(Geom g, const double* __restrict__ raw, double dscale,
-                                                    const double* __restrict__ sc, double nn, Nbr x,
-                                                    double* __restrict__ r, double ih2,
-                                                    double* __restrict__ partials) {
-    const int64_t npair = (int64_t)g.n * g.nzl * (g.n >> 1);
-    const int hq = g.n >> 1;
+// ------------------------------------------------ natural octets (8 nodes) ---
+// A thread takes the nodes x = 2j .. 2j+7 (j = 0 mod 4) of one row: colour elements
+// j .. j+3 of both colours, one 256-bit load per colour and stencil row (12 loads for
+// 8 nodes, the pair kernels above needed 12 for 2).  Node k of the octet is element
+// k/2 of colour (c0 + k) & 1, c0 = (y + zl) & 1.
+struct Oct {
+    Q4 e, o;     // even / odd nodes of the octet
+    __device__ __forceinline__ double at(int k) const { return (k & 1) ? o.v[k >> 1] : e.v[k >> 1]; }
+};
+__device__ __forceinline__ Oct ldoct(const Geom& g, const Nbr& f, int zl, int y, int j) {
+    const int c0 = (y + zl) & 1;
+    Oct r;
+    r.e = ld4(zrow(g, f, c0, zl, y, j));
+    r.o = ld4(zrow(g, f, c0 ^ 1, zl, y, j));
+    return r;
+}
+__device__ __forceinline__ void stoct(const Geom& g, double* f, int zl, int y, int j, const double v[8]) {
+    const int c0 = (y + zl) & 1;
+    Q4 e, o;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        e.v[q] = v[2 * q];
+        o.v[q] = v[2 * q + 1];
+    }
+    st4(f + sidx(g, c0, zl, y, j), e);
+    st4(f + sidx(g, c0 ^ 1, zl, y, j), o);
+}
+struct Hood8 {
+    Oct c, ym, yp, zm, zp;
+    double left, right;      // nodes 2j - 1 and 2j + 8
+};
+__device__ __forceinline__ Hood8 ldhood8(const Geom& g, const Nbr& f, int zl, int y, int j) {
+    const int hn = g.n >> 1, c0 = (y + zl) & 1;
+    Hood8 h;
+    h.c = ldoct(g, f, zl, y, j);
+    h.left = *zrow(g, f, c0 ^ 1, zl, y, (j - 1) & (hn - 1));
+    h.right = *zrow(g, f, c0, zl, y, (j + 4) & (hn - 1));
+    h.ym = ldoct(g, f, zl, (y - 1) & g.nmask, j);
+    h.yp = ldoct(g, f, zl, (y + 1) & g.nmask, j);
+    h.zm = ldoct(g, f, zl - 1, y, j);
+    h.zp = ldoct(g, f, zl + 1, y, j);
+    return h;
+}
+// h <- h + beta hp, element by element (p' = z + beta p on the whole stencil)
+__device__ __forceinline__ void axpy_hood8(Hood8& h, const Hood8& hp, double beta) {
+    auto u4 = [&](Q4& a, const Q4& b) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) a.v[q] = __dadd_rn(a.v[q], __dmul_rn(beta, b.v[q]));
+    };
+    auto u8 = [&](Oct& a, const Oct& b) { u4(a.e, b.e); u4(a.o, b.o); };
+    u8(h.c, hp.c); u8(h.ym, hp.ym); u8(h.yp, hp.yp); u8(h.zm, hp.zm); u8(h.zp, hp.zp);
+    h.left = __dadd_rn(h.left, __dmul_rn(beta, hp.left));
+    h.right = __dadd_rn(h.right, __dmul_rn(beta, hp.right));
+}
+// -Delta_h at the octet (D#26): (6 x - nb) * ih2, nb in the oracle's order.
+__device__ __forceinline__ void apply_A8(const Hood8& h, double ih2, double out[8]) {
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+        const double xm = k == 0 ? h.left : h.c.at(k - 1);
+        const double xp = k == 7 ? h.right : h.c.at(k + 1);
+        const double sk = nsum(xm, xp, h.ym.at(k), h.yp.at(k), h.zm.at(k), h.zp.at(k));
+        out[k] = __dmul_rn(__dsub_rn(__dmul_rn(6.0, h.c.at(k)), sk), ih2);
+    }
+}
+struct OctPos {
+    int zl, y, j;
+    int64_t row;
+};
+__device__ __forceinline__ OctPos oct_pos(const Geom& g, int64_t t) {
+    const int ln = lg2(g.n);
+    OctPos q;
+    q.row = t >> (ln - 3);                       // n / 8 octets per row
+    q.j = 4 * (int)(t & ((g.n >> 3) - 1));
+    q.y = (int)(q.row & g.nmask);
+    q.zl = (int)(q.row >> ln);
+    return q;
+}
+
+// r = (rho - mean) - A x (D#27), partials of (b, b) and (r, r).  Thread = octet.
+__global__ void __launch_bounds__(kPT) k_pcg_resid0_8(Geom g, const double* __restrict__ raw, double dscale,
+                                                      const double* __restrict__ sc, double nn, Nbr x,
+                                                      double* __restrict__ r, double ih2,
+                                                      double* __restrict__ partials) {
+    const int64_t noct = (int64_t)g.n * g.nzl * (g.n >> 3);
     const double mean = sc[0] / nn;
     double acc[2] = {0.0, 0.0};
-    for (int64_t p = (int64_t)blockIdx.x * kPT + threadIdx.x; p < npair; p += (int64_t)gridDim.x * kPT) {
-        const int64_t row = p >> (lg2(g.n) - 1);
-        const int j = (int)(p & (hq - 1)), y = (int)(row & g.nmask), zl = (int)(row >> lg2(g.n));
-        const double2 v = *reinterpret_cast<const double2*>(raw + row * g.rp + 2 * j);
-        const double b0 = __dsub_rn(__dmul_rn(dscale, v.x), mean);
-        const double b1 = __dsub_rn(__dmul_rn(dscale, v.y), mean);
-        const double2 ax = apply_A(ldhood(g, x, zl, y, j), ih2);
-        const double2 rv = make_double2(__dsub_rn(b0, ax.x), __dsub_rn(b1, ax.y));
-        stnat(g, r, zl, y, j, rv);
-        acc[0] = fma(b0, b0, fma(b1, b1, acc[0]));
-        acc[1] = fma(rv.x, rv.x, fma(rv.y, rv.y, acc[1]));
+    for (int64_t t = (int64_t)blockIdx.x * kPT + threadIdx.x; t < noct; t += (int64_t)gridDim.x * kPT) {
+        const OctPos q = oct_pos(g, t);
+        const double* rp = raw + q.row * g.rp + 2 * q.j;
+        const Q4 v0 = ld4(rp), v1 = ld4(rp + 4);
+        double ax[8], rv[8];
+        apply_A8(ldhood8(g, x, q.zl, q.y, q.j), ih2, ax);
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            const double b = __dsub_rn(__dmul_rn(dscale, k < 4 ? v0.v[k] : v1.v[k - 4]), mean);
+            rv[k] = __dsub_rn(b, ax[k]);
+            acc[0] = fma(b, b, acc[0]);
+            acc[1] = fma(rv[k], rv[k], acc[1]);
+        }
+        stoct(g, r, q.zl, q.y, q.j, rv);
     }
     block_partials(acc, 2, partials);
 }
 
-// p' = z + beta p (first: p' = z), q = A p', partial (p', q).  The neighbours' p'
-// are formed on the fly from z and p, so p' and q are written once.
+// p' = z + beta p (first: p' = z), q = A p', partial (p', q); thread = octet.
 template <bool FIRST>
-__global__ void __launch_bounds__(kPT) k_pcg_matvec(Geom g, Nbr z, Nbr p, double* __restrict__ pout,
-                                                    double* __restrict__ q, const double* __restrict__ sc,
-                                                    double ih2, double* __restrict__ partials) {
-    const int64_t npair = (int64_t)g.n * g.nzl * (g.n >> 1);
-    const int hq = g.n >> 1;
+__global__ void __launch_bounds__(kPT) k_pcg_matvec8(Geom g, Nbr z, Nbr p, double* __restrict__ pout,
+                                                     double* __restrict__ qo, const double* __restrict__ sc,
+                                                     double ih2, double* __restrict__ partials) {
+    const int64_t noct = (int64_t)g.n * g.nzl * (g.n >> 3);
     const double beta = FIRST ? 0.0 : sc[3] / sc[4];
     double acc = 0.0;
-    for (int64_t t = (int64_t)blockIdx.x * kPT + threadIdx.x; t < npair; t += (int64_t)gridDim.x * kPT) {
-        const int64_t row = t >> (lg2(g.n) - 1);
-        const int j = (int)(t & (hq - 1)), y = (int)(row & g.nmask), zl = (int)(row >> lg2(g.n));
-        Hood h = ldhood(g, z, zl, y, j);
-        if (!FIRST) {
-            const Hood hp = ldhood(g, p, zl, y, j);
-            auto upd = [&](double& a, double b) { a = __dadd_rn(a, __dmul_rn(beta, b)); };
-            upd(h.c.x, hp.c.x); upd(h.c.y, hp.c.y);
-            upd(h.ym.x, hp.ym.x); upd(h.ym.y, hp.ym.y);
-            upd(h.yp.x, hp.yp.x); upd(h.yp.y, hp.yp.y);
-            upd(h.zm.x, hp.zm.x); upd(h.zm.y, hp.zm.y);
-            upd(h.zp.x, hp.zp.x); upd(h.zp.y, hp.zp.y);
-            upd(h.left, hp.left); upd(h.right, hp.right);
+    for (int64_t t = (int64_t)blockIdx.x * kPT + threadIdx.x; t < noct; t += (int64_t)gridDim.x * kPT) {
+        const OctPos q = oct_pos(g, t);
+        Hood8 h = ldhood8(g, z, q.zl, q.y, q.j);
+        if (!FIRST) axpy_hood8(h, ldhood8(g, p, q.zl, q.y, q.j), beta);
+        double av[8], pv[8];
+        apply_A8(h, ih2, av);
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            pv[k] = h.c.at(k);
+            acc = fma(pv[k], av[k], acc);
         }
-        const double2 qv = apply_A(h, ih2);
-        stnat(g, pout, zl, y, j, h.c);
-        stnat(g, q, zl, y, j, qv);
-        acc = fma(h.c.x, qv.x, fma(h.c.y, qv.y, acc));
+        stoct(g, pout, q.zl, q.y, q.j, pv);
+        stoct(g, qo, q.zl, q.y, q.j, av);
     }
     block_partials(&acc, 1, partials);
     if (g.P > 1) __threadfence_system();
 }
 
-// x += alpha p ; r -= alpha q ; partial (r, r).  alpha = (r, z) / (p, q).
-__global__ void __launch_bounds__(kPT) k_pcg_update(int64_t n2, int sys_fence, double2* __restrict__ x,
-                                                    const double2* __restrict__ p, double2* __restrict__ r,
-                                                    const double2* __restrict__ q, const double* __restrict__ sc,
-                                                    double* __restrict__ partials) {
-    const double alpha = sc[3] / sc[5];
-    double acc = 0.0;
-    for (int64_t i = (int64_t)blockIdx.x * kPT + threadIdx.x; i < n2; i += (int64_t)gridDim.x * kPT) {
-        const double2 pv = p[i], qv = q[i];
-        double2 xv = x[i], rv = r[i];
-        xv.x = __dadd_rn(xv.x, __dmul_rn(alpha, pv.x));
-        xv.y = __dadd_rn(xv.y, __dmul_rn(alpha, pv.y));
-        rv.x = __dsub_rn(rv.x, __dmul_rn(alpha, qv.x));
-        rv.y = __dsub_rn(rv.y, __dmul_rn(alpha, qv.y));
-        x[i] = xv;
-        r[i] = rv;
-        acc = fma(rv.x, rv.x, fma(rv.y, rv.y, acc));
-    }
-    block_partials(&acc, 1, partials);
-    if (sys_fence) __threadfence_system();     // x is read by the neighbour slabs
-}
-
-__device__ __forceinline__ void st_node4(double* p, double a, double b, double c) {
-    asm volatile("st.global.v4.f64 [%0], {%1, %2, %3, %4};" ::"l"(p), "d"(a), "d"(b), "d"(c), "d"(0.0)
-                 : "memory");
-}
-
-// E = -grad_h phi by central differences (D#30) -> E4 node records (+ plane 0 into
-// `halo`, the halo plane of the slab below), partials of E_d^2.
-__global__ void __launch_bounds__(kPT) k_pcg_gradient(Geom g, Nbr x, double* __restrict__ E4, double* halo,
-                                                      double* __restrict__ partials) {
-    const int64_t npair = (int64_t)g.n * g.nzl * (g.n >> 1);
-    const int hq = g.n >> 1;
+// E = -grad_h phi (D#30) -> E4 node records (+ plane 0 into `halo`), E_d^2 partials.
+__global__ void __launch_bounds__(kPT) k_pcg_gradient8(Geom g, Nbr x, double* __restrict__ E4, double* halo,
+                                                       double* __restrict__ partials) {
+    const int64_t noct = (int64_t)g.n * g.nzl * (g.n >> 3);
     const double cc = 0.5 * g.inv_h;
     double e2[3] = {0.0, 0.0, 0.0};
-    for (int64_t t = (int64_t)blockIdx.x * kPT + threadIdx.x; t < npair; t += (int64_t)gridDim.x * kPT) {
-        const int64_t row = t >> (lg2(g.n) - 1);
-        const int j = (int)(t & (hq - 1)), y = (int)(row & g.nmask), zl = (int)(row >> lg2(g.n));
-        const Hood h = ldhood(g, x, zl, y, j);
-        const double ex0 = __dmul_rn(__dsub_rn(h.left, h.c.y), cc);
-        const double ex1 = __dmul_rn(__dsub_rn(h.c.x, h.right), cc);
-        const double ey0 = __dmul_rn(__dsub_rn(h.ym.x, h.yp.x), cc);
-        const double ey1 = __dmul_rn(__dsub_rn(h.ym.y, h.yp.y), cc);
-        const double ez0 = __dmul_rn(__dsub_rn(h.zm.x, h.zp.x), cc);
-        const double ez1 = __dmul_rn(__dsub_rn(h.zm.y, h.zp.y), cc);
-        const int64_t nd = 4 * (row * g.n + 2 * j);
-        st_node4(E4 + nd, ex0, ey0, ez0);
-        st_node4(E4 + nd + 4, ex1, ey1, ez1);
-        if (halo && zl == 0) {
-            st_node4(halo + nd, ex0, ey0, ez0);
-            st_node4(halo + nd + 4, ex1, ey1, ez1);
+    for (int64_t t = (int64_t)blockIdx.x * kPT + threadIdx.x; t < noct; t += (int64_t)gridDim.x * kPT) {
+        const OctPos q = oct_pos(g, t);
+        const Hood8 h = ldhood8(g, x, q.zl, q.y, q.j);
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            const double xm = k == 0 ? h.left : h.c.at(k - 1);
+            const double xp = k == 7 ? h.right : h.c.at(k + 1);
+            const double ex = __dmul_rn(__dsub_rn(xm, xp), cc);
+            const double ey = __dmul_rn(__dsub_rn(h.ym.at(k), h.yp.at(k)), cc);
+            const double ez = __dmul_rn(__dsub_rn(h.zm.at(k), h.zp.at(k)), cc);
+            const int64_t nd = 4 * (q.row * g.n + 2 * q.j + k);
+            asm volatile("st.global.v4.f64 [%0], {%1, %2, %3, %4};" ::"l"(E4 + nd), "d"(ex), "d"(ey), "d"(ez),
+                         "d"(0.0) : "memory");
+            if (halo && q.zl == 0)
+                asm volatile("st.global.v4.f64 [%0], {%1, %2, %3, %4};" ::"l"(halo + nd), "d"(ex), "d"(ey),
+                             "d"(ez), "d"(0.0) : "memory");
+            e2[0] = fma(ex, ex, e2[0]);
+            e2[1] = fma(ey, ey, e2[1]);
+            e2[2] = fma(ez, ez, e2[2]);
         }
-        e2[0] = fma(ex0, ex0, fma(ex1, ex1, e2[0]));
-        e2[1] = fma(ey0, ey0, fma(ey1, ey1, e2[1]));
-        e2[2] = fma(ez0, ez0, fma(ez1, ez1, e2[2]));
     }
     block_partials(e2, 3, partials);
     if (halo && g.P > 1) __threadfence_system();
+}
+
+// x += alpha p ; r -= alpha q ; partial (r, r) -- 256-bit streams.
+__global__ void __launch_bounds__(kPT) k_pcg_update4(int64_t n4, int sys_fence, double* __restrict__ x,
+                                                     const double* __restrict__ p, double* __restrict__ r,
+                                                     const double* __restrict__ q, const double* __restrict__ sc,
+                                                     double* __restrict__ partials) {
+    const double alpha = sc[3] / sc[5];
+    double acc = 0.0;
+    for (int64_t i = (int64_t)blockIdx.x * kPT + threadIdx.x; i < n4; i += (int64_t)gridDim.x * kPT) {
+        const Q4 pv = ld4(p + 4 * i), qv = ld4(q + 4 * i);
+        Q4 xv = ld4(x + 4 * i), rv = ld4(r + 4 * i);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            xv.v[k] = __dadd_rn(xv.v[k], __dmul_rn(alpha, pv.v[k]));
+            rv.v[k] = __dsub_rn(rv.v[k], __dmul_rn(alpha, qv.v[k]));
+            acc = fma(rv.v[k], rv.v[k], acc);
+        }
+        st4(x + 4 * i, xv);
+        st4(r + 4 * i, rv);
+    }
+    block_partials(&acc, 1, partials);
+    if (sys_fence) __threadfence_system();     // x is read by the neighbour slabs
 }
 
 // One CTA, fixed order: out[k] = sum of partials[k][0..nparts) (k < ncomp).  save:
@@ -371,23 +476,8 @@ constexpr int kTBThreads = 256;
 constexpr int kMaxK = ((kTY + 2 * (kTB - 1)) * (kTX + 2 * (kTB / 2)) + kTBThreads - 1) / kTBThreads;
 constexpr size_t kTBSmem = sizeof(double) * kSlots * kSlot;
 
-__device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
-    const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(s), "l"(gmem) : "memory");
-}
 __device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
 
-__device__ __forceinline__ const double* nbr_ptr(const Geom& g, const Nbr& f, int c, int zl, int y, int j) {
-    const double* b = f.own;
-    if (zl < 0) { b = f.below; zl += g.nzl; }
-    else if (zl >= g.nzl) { b = f.above; zl -= g.nzl; }
-    return b + sidx(g, c, zl, y, j);
-}
-
-// Per-thread work lists are precomputed once per tile (shared-memory offsets of the
-// elements each thread updates per half-sweep, global row offsets of their r, the
-// cp.async sources of the plane loads), so the inner loop is six LDS, one LDG of r
-// (prefetched one plane ahead into registers) and the fp64 update.
 __global__ void __launch_bounds__(kTBThreads, 2) k_ssor_tb(Geom g, Nbr r, Nbr zin, double* __restrict__ zout,
                                                            int ns, int seq, int zero_in, int dot, int cz,
                                                            double c1, double c2, double h2,
@@ -578,7 +668,7 @@ void launch_pcg_resid0(const Geom& g, const double* raw, double dscale, double* 
                        double* r, double* partials, cudaStream_t s) {
     const unsigned grid = pcg_grid(g);
     const double ih2 = g.inv_h * g.inv_h;
-    k_pcg_resid0<<<grid, kPT, 0, s>>>(g, raw, dscale, sc, nn, Nbr{x.own, x.below, x.above}, r, ih2, partials);
+    k_pcg_resid0_8<<<grid, kPT, 0, s>>>(g, raw, dscale, sc, nn, Nbr{x.own, x.below, x.above}, r, ih2, partials);
     k_pcg_reduce<<<1, 1024, 0, s>>>(g, partials, (int)grid, 2, sc + 1, nullptr, 0);
 }
 
@@ -589,10 +679,18 @@ void launch_pcg_sor(const Geom& g, int colour, int mode, bool dot, const double*
     const double h2 = h * h, c1 = 1.0 - omega, c2 = omega / 6.0;
     const Nbr zn{z.own, z.below, z.above};
     double* zo = const_cast<double*>(z.own);
-    if (mode == 2) k_sor<2, false><<<grid, kPT, 0, s>>>(g, colour, r, zn, zo, c1, c2, h2, partials);
-    else if (mode == 1) k_sor<1, false><<<grid, kPT, 0, s>>>(g, colour, r, zn, zo, c1, c2, h2, partials);
-    else if (dot) k_sor<0, true><<<grid, kPT, 0, s>>>(g, colour, r, zn, zo, c1, c2, h2, partials);
-    else k_sor<0, false><<<grid, kPT, 0, s>>>(g, colour, r, zn, zo, c1, c2, h2, partials);
+    static const bool two = [] { const char* e = getenv("PIC_PCG_SOR2"); return e && e[0] == '1'; }();
+    if (two) {   // two elements per thread (the earlier kernel; A/B switch)
+        if (mode == 2) k_sor<2, false><<<grid, kPT, 0, s>>>(g, colour, r, zn, zo, c1, c2, h2, partials);
+        else if (mode == 1) k_sor<1, false><<<grid, kPT, 0, s>>>(g, colour, r, zn, zo, c1, c2, h2, partials);
+        else if (dot) k_sor<0, true><<<grid, kPT, 0, s>>>(g, colour, r, zn, zo, c1, c2, h2, partials);
+        else k_sor<0, false><<<grid, kPT, 0, s>>>(g, colour, r, zn, zo, c1, c2, h2, partials);
+    } else {
+        if (mode == 2) k_sor4<2, false><<<grid, kPT, 0, s>>>(g, colour, r, zn, zo, c1, c2, h2, partials);
+        else if (mode == 1) k_sor4<1, false><<<grid, kPT, 0, s>>>(g, colour, r, zn, zo, c1, c2, h2, partials);
+        else if (dot) k_sor4<0, true><<<grid, kPT, 0, s>>>(g, colour, r, zn, zo, c1, c2, h2, partials);
+        else k_sor4<0, false><<<grid, kPT, 0, s>>>(g, colour, r, zn, zo, c1, c2, h2, partials);
+    }
     if (dot) k_pcg_reduce<<<1, 1024, 0, s>>>(g, partials, (int)grid, 1, sc + 3, sc + 4, 0);
 }
 
@@ -625,25 +723,23 @@ void launch_pcg_matvec(const Geom& g, bool first, PcgNbr z, PcgNbr p, double* po
     const unsigned grid = pcg_grid(g);
     const double ih2 = g.inv_h * g.inv_h;
     const Nbr zn{z.own, z.below, z.above}, pn{p.own, p.below, p.above};
-    if (first) k_pcg_matvec<true><<<grid, kPT, 0, s>>>(g, zn, pn, pout, q, sc, ih2, partials);
-    else k_pcg_matvec<false><<<grid, kPT, 0, s>>>(g, zn, pn, pout, q, sc, ih2, partials);
+    if (first) k_pcg_matvec8<true><<<grid, kPT, 0, s>>>(g, zn, pn, pout, q, sc, ih2, partials);
+    else k_pcg_matvec8<false><<<grid, kPT, 0, s>>>(g, zn, pn, pout, q, sc, ih2, partials);
     k_pcg_reduce<<<1, 1024, 0, s>>>(g, partials, (int)grid, 1, sc + 5, nullptr, 0);
 }
 
 void launch_pcg_update(const Geom& g, double* x, const double* p, double* r, const double* q, double* sc,
                        double* partials, cudaStream_t s) {
     const unsigned grid = pcg_grid(g);
-    const int64_t n2 = (int64_t)g.n * g.n * g.nzl / 2;
-    k_pcg_update<<<grid, kPT, 0, s>>>(n2, g.P > 1, reinterpret_cast<double2*>(x), reinterpret_cast<const double2*>(p),
-                                      reinterpret_cast<double2*>(r), reinterpret_cast<const double2*>(q), sc,
-                                      partials);
+    const int64_t n4 = (int64_t)g.n * g.n * g.nzl / 4;
+    k_pcg_update4<<<grid, kPT, 0, s>>>(n4, g.P > 1, x, p, r, q, sc, partials);
     k_pcg_reduce<<<1, 1024, 0, s>>>(g, partials, (int)grid, 1, sc + 2, nullptr, 0);
 }
 
 void launch_pcg_gradient(const Geom& g, PcgNbr x, double* E4, double* halo, double* partials, double* energies,
                          cudaStream_t s) {
     const unsigned grid = pcg_grid(g);
-    k_pcg_gradient<<<grid, kPT, 0, s>>>(g, Nbr{x.own, x.below, x.above}, E4, halo, partials);
+    k_pcg_gradient8<<<grid, kPT, 0, s>>>(g, Nbr{x.own, x.below, x.above}, E4, halo, partials);
     k_pcg_reduce<<<1, 1024, 0, s>>>(g, partials, (int)grid, 3, energies, nullptr, 1);
 }
 

@@ -170,6 +170,11 @@ pic_status validate(const pic_params* p, int32_t rank, int32_t nranks, char* msg
         snprintf(msg, msz, "PCG: need tol > 0, 0 < omega < 2, inner >= 1, outer >= 1, maxit >= 1");
         return PIC_EINVAL;
     }
+    for (int d = 0; d < 3; ++d)
+        if (!std::isfinite(p->b_ext[d]) || !std::isfinite(p->e_ext[d])) {
+            snprintf(msg, msz, "b_ext / e_ext must be finite");
+            return PIC_EINVAL;
+        }
     const double np = (double)p->ppc * p->n * p->n * p->n / nranks;
     if (np * (nranks > 1 ? 1.3 : 1.0) >= 4294967296.0) {
         snprintf(msg, msz, "N_p per rank = %.0f too large for 32-bit indices", np);
@@ -193,6 +198,16 @@ Geom make_geom(const pic_params* p, int rank, int nranks) {
     g.nzl = p->n / nranks;
     g.mz = ilog2i(g.nzl);
     g.z0 = rank * g.nzl;
+    // external fields (D#32): the coefficients in the oracle's order (oracle_boris_coeffs)
+    g.eext = p->e_ext[0] != 0.0 || p->e_ext[1] != 0.0 || p->e_ext[2] != 0.0;
+    g.boris = p->b_ext[0] != 0.0 || p->b_ext[1] != 0.0 || p->b_ext[2] != 0.0;
+    g.hq = 0.5 * (-1.0 * p->dt);
+    for (int d = 0; d < 3; ++d) {
+        g.ee[d] = p->e_ext[d];
+        g.bt[d] = g.hq * p->b_ext[d];
+    }
+    const double tt = (g.bt[0] * g.bt[0] + g.bt[1] * g.bt[1]) + g.bt[2] * g.bt[2];
+    for (int d = 0; d < 3; ++d) g.bs[d] = (2.0 * g.bt[d]) / (1.0 + tt);
     return g;
 }
 

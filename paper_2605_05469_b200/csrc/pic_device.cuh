@@ -25,6 +25,10 @@ struct Geom {
     // one extra plane (nzl): the ghost of the charge, the halo of the field.
     int P, rank, z0, nzl, mz;
     int64_t cap;    // particle capacity of this rank's arrays (sorted positions beyond it: overflow)
+    // uniform external fields (Eq. 1, D#32): eext -> E += ee; boris -> Boris kick with
+    // hq = (q/m) dt / 2, bt = hq B_ext, bs = 2 bt / (1 + |bt|^2)
+    int eext, boris;
+    double ee[3], bt[3], bs[3], hq;
 };
 
 // Index of node (ix, iy, slab plane izl) in a pitched real grid [nzl + 1][n][rp].
@@ -189,14 +193,40 @@ __device__ __forceinline__ void drift(const Geom& g, double x[3], const double v
     for (int d = 0; d < 3; ++d) x[d] = wrap(__fma_rn(v[d], g.dt, x[d]), g.L);
 }
 
+// The kick of the push (D#32): E += E_ext (when nonzero); B_ext = 0:
+// v <- fma(qm_dt, E, v); else Boris: v- = v + hq E, v' = v- + v- x t,
+// v+ = v- + v' x s, v <- v+ + hq E -- the oracle's operation order (fma where it writes fma).
+__device__ __forceinline__ void kick(const Geom& g, double e[3], double v[3]) {
+    if (g.eext) {
+#pragma unroll
+        for (int d = 0; d < 3; ++d) e[d] = __dadd_rn(e[d], g.ee[d]);
+    }
+    if (!g.boris) {
+#pragma unroll
+        for (int d = 0; d < 3; ++d) v[d] = __fma_rn(g.qm_dt, e[d], v[d]);
+        return;
+    }
+    double vm[3], vp[3];
+#pragma unroll
+    for (int d = 0; d < 3; ++d) vm[d] = __fma_rn(g.hq, e[d], v[d]);
+    vp[0] = __dadd_rn(vm[0], __dsub_rn(__dmul_rn(vm[1], g.bt[2]), __dmul_rn(vm[2], g.bt[1])));
+    vp[1] = __dadd_rn(vm[1], __dsub_rn(__dmul_rn(vm[2], g.bt[0]), __dmul_rn(vm[0], g.bt[2])));
+    vp[2] = __dadd_rn(vm[2], __dsub_rn(__dmul_rn(vm[0], g.bt[1]), __dmul_rn(vm[1], g.bt[0])));
+    const double s0 = __dadd_rn(vm[0], __dsub_rn(__dmul_rn(vp[1], g.bs[2]), __dmul_rn(vp[2], g.bs[1])));
+    const double s1 = __dadd_rn(vm[1], __dsub_rn(__dmul_rn(vp[2], g.bs[0]), __dmul_rn(vp[0], g.bs[2])));
+    const double s2 = __dadd_rn(vm[2], __dsub_rn(__dmul_rn(vp[0], g.bs[1]), __dmul_rn(vp[1], g.bs[0])));
+    v[0] = __fma_rn(g.hq, e[0], s0);
+    v[1] = __fma_rn(g.hq, e[1], s1);
+    v[2] = __fma_rn(g.hq, e[2], s2);
+}
+
 // Gather + leapfrog kick-drift + wrap:
 //   v <- fma(qm_dt, E_p, v) ; x <- wrap(fma(v, dt, x)).
 __device__ __forceinline__ void gather_push(const Geom& g, const double* __restrict__ E4,
                                             double x[3], double v[3]) {
     double ep[3];
     gather_E(g, E4, x, ep);
-#pragma unroll
-    for (int d = 0; d < 3; ++d) v[d] = __fma_rn(g.qm_dt, ep[d], v[d]);
+    kick(g, ep, v);
     drift(g, x, v);
 }
 
