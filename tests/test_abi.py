@@ -93,3 +93,30 @@ def test_stage_names():
     for i, s in enumerate(B.STAGES):
         assert L.pic_stage_name(i).decode() == s
     assert L.pic_stage_name(len(B.STAGES)) is None
+
+
+def test_pcg_defaults_and_validation():
+    """BJ config 5 defaults (P:226 tol 1e-4; P:260 SSOR pi/2, 4 inner, 2 outer); invalid
+    PCG settings and non-finite external fields are PIC_EINVAL; the PCG workspace adds
+    six colour-split fields (x, r, z, two p, q) of 8 B/node."""
+    import math
+
+    p = B.default_params()
+    assert p.solver == B.PIC_SOLVER_FFT
+    assert (p.pcg_inner, p.pcg_outer, p.pcg_maxit) == (4, 2, 1000)
+    assert p.pcg_tol == 1e-4 and p.pcg_omega == math.pi / 2
+    assert tuple(p.b_ext) == (0.0, 0.0, 0.0) and tuple(p.e_ext) == (0.0, 0.0, 0.0)
+    for bad in (dict(pcg_tol=0.0), dict(pcg_omega=2.0), dict(pcg_omega=0.0), dict(pcg_inner=0),
+                dict(pcg_outer=0), dict(pcg_maxit=0), dict(solver=2)):
+        q = B.default_params(**{"solver": B.PIC_SOLVER_PCG, **bad})
+        with pytest.raises(B.PicError) as e:
+            B.workspace_bytes(q)
+        assert e.value.status == B.PIC_EINVAL, bad
+    for bad in (dict(b_ext=(0.0, float("nan"), 0.0)), dict(e_ext=(float("inf"), 0.0, 0.0))):
+        with pytest.raises(B.PicError) as e:
+            B.workspace_bytes(B.default_params(**bad))
+        assert e.value.status == B.PIC_EINVAL
+    n = 64
+    fft = B.workspace_bytes(B.default_params(n=n))
+    pcg = B.workspace_bytes(B.default_params(n=n, solver=B.PIC_SOLVER_PCG))
+    assert 6 * 8 * n ** 3 <= pcg - fft <= 6 * 8 * n ** 3 + 8 * 4096

@@ -177,3 +177,21 @@ def test_pcg_blocked_passes_bit_identical_to_half_sweeps(Sim, n, inner, outer, m
         _, rphi, rit, _ = O.solve_pcg(n, L, rho, tol=1e-8)
         assert rit == out[0][2]
         assert np.max(np.abs(out[0][0] - rphi)) <= 1e-10 * np.max(np.abs(rphi))
+
+
+def test_pcg_nonconvergence_is_reported_not_poisoning(Sim):
+    """pcg_maxit reached -> PIC_ENONCONV with the last iterate's field kept; the context
+    stays usable (D#29, include/pic.h)."""
+    from paper_2605_05469_b200 import PicError
+    from paper_2605_05469_b200._binding import PIC_ENONCONV
+
+    n = 32
+    sim = Sim(n=n, ppc=2, half_kick=False, pcg_tol=1e-14, pcg_maxit=2)
+    sim.set_particles(landau_state(n, 2, seed=1))
+    with pytest.raises(PicError) as e:
+        sim.step(1)
+    assert e.value.status == PIC_ENONCONV
+    it, tot, ns, rel = sim.pcg_stats()
+    assert it == -1 and tot == 2 and rel > 1e-14
+    E = sim.get_grid(1)
+    assert np.all(np.isfinite(E)) and np.max(np.abs(E)) > 0
