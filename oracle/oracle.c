@@ -684,3 +684,151 @@ void oracle_run_ext(int32_t n, double L, double dt, int64_t np, double *xv, int3
     free(E);
     free(rho);
 }
+
+/* ======================================== matrix-free Q1 FEM Poisson solve ==== *
+ * P:183-195 (FEM with first-order Lagrange elements, matrix-free operator, CG;
+ * plain CG for the comparison), P:226 (tol 1e-4), P:260 (warm start).
+ * Readings D#33: element stiffness A^e_ij = int grad b_i . grad b_j over one cube
+ * element by 2x2x2 Gauss quadrature; A x = sum_e scatter(A^e gather_e(x)) with the
+ * periodic DOF map; lumped load b_j = h^3 rho_j minus its mean; E = -grad_h phi by
+ * central differences (shared with the PCG path). */
+
+/* A^e (8 x 8, vertex v = a + 2b + 4c at (a, b, c) h) by 2x2x2 Gauss-Legendre quadrature. */
+void oracle_fem_element_stiffness(double h, double Ae[64]) {
+    const double gp[2] = {0.5 - 0.5 / sqrt(3.0), 0.5 + 0.5 / sqrt(3.0)};   /* points on [0,1] */
+    for (int i = 0; i < 64; ++i) Ae[i] = 0.0;
+    for (int qz = 0; qz < 2; ++qz)
+        for (int qy = 0; qy < 2; ++qy)
+            for (int qx = 0; qx < 2; ++qx) {
+                const double xi[3] = {gp[qx], gp[qy], gp[qz]};
+                double grad[8][3];
+                for (int v = 0; v < 8; ++v) {
+                    const int a[3] = {v & 1, (v >> 1) & 1, (v >> 2) & 1};
+                    double phi[3], dphi[3];
+                    for (int d = 0; d < 3; ++d) {
+                        phi[d] = a[d] ? xi[d] : 1.0 - xi[d];
+                        dphi[d] = (a[d] ? 1.0 : -1.0) / h;           /* d/dx of the 1D basis */
+                    }
+                    grad[v][0] = dphi[0] * phi[1] * phi[2];
+                    grad[v][1] = phi[0] * dphi[1] * phi[2];
+                    grad[v][2] = phi[0] * phi[1] * dphi[2];
+                }
+                const double w = 0.125 * ((h * h) * h);              /* weight x Jacobian */
+                for (int i = 0; i < 8; ++i)
+                    for (int j = 0; j < 8; ++j)
+                        Ae[i * 8 + j] += w * (grad[i][0] * grad[j][0] + grad[i][1] * grad[j][1] +
+                                              grad[i][2] * grad[j][2]);
+            }
+}
+
+/* y = A x, element by element ("the action of the matrix A"). */
+void oracle_fem_apply(int32_t n, double L, const double *x, double *y) {
+    const int64_t nn = (int64_t)n * n * n;
+    double Ae[64];
+    oracle_fem_element_stiffness(L / (double)n, Ae);
+    for (int64_t m = 0; m < nn; ++m) y[m] = 0.0;
+    for (int32_t ez = 0; ez < n; ++ez)
+        for (int32_t ey = 0; ey < n; ++ey)
+            for (int32_t ex = 0; ex < n; ++ex) {
+                int64_t dof[8];
+                double xe[8];
+                for (int v = 0; v < 8; ++v) {
+                    dof[v] = node(n, ex + (v & 1), ey + ((v >> 1) & 1), ez + ((v >> 2) & 1));
+                    xe[v] = x[dof[v]];
+                }
+                for (int i = 0; i < 8; ++i) {
+                    double s = 0.0;
+                    for (int j = 0; j < 8; ++j) s += Ae[i * 8 + j] * xe[j];
+                    y[dof[i]] += s;
+                }
+            }
+}
+
+/* Plain CG on A x = b from the guess in x; ||r||^2 <= tol^2 ||b||^2 (D#29). */
+int32_t oracle_fem_cg(int32_t n, double L, const double *b, double *x, double tol, int32_t maxit,
+                      double *relres) {
+    const int64_t nn = (int64_t)n * n * n;
+    double *r = (double *)malloc(sizeof(double) * (size_t)nn);
+    double *p = (double *)malloc(sizeof(double) * (size_t)nn);
+    double *q = (double *)malloc(sizeof(double) * (size_t)nn);
+    const double bb = dot(nn, b, b), stop = (tol * tol) * bb;
+    int32_t it = 0, status = -1;
+    double rr = 0.0;
+    if (bb == 0.0) {
+        for (int64_t m = 0; m < nn; ++m) x[m] = 0.0;
+        status = 0;
+        goto done;
+    }
+    oracle_fem_apply(n, L, x, q);
+    for (int64_t m = 0; m < nn; ++m) r[m] = b[m] - q[m];
+    rr = dot(nn, r, r);
+    if (rr <= stop) { status = 0; goto done; }
+    memcpy(p, r, sizeof(double) * (size_t)nn);
+    for (it = 1; it <= maxit; ++it) {
+        oracle_fem_apply(n, L, p, q);
+        const double alpha = rr / dot(nn, p, q);
+        for (int64_t m = 0; m < nn; ++m) x[m] = x[m] + alpha * p[m];
+        for (int64_t m = 0; m < nn; ++m) r[m] = r[m] - alpha * q[m];
+        const double rr_new = dot(nn, r, r);
+        if (rr_new <= stop) { rr = rr_new; status = it; break; }
+        const double beta = rr_new / rr;
+        rr = rr_new;
+        for (int64_t m = 0; m < nn; ++m) p[m] = r[m] + beta * p[m];
+    }
+done:
+    if (relres) *relres = bb > 0.0 ? sqrt(rr / bb) : 0.0;
+    free(q);
+    free(p);
+    free(r);
+    return status;
+}
+
+/* The FEM solve of the PIC loop: b_j = h^3 rho_j - mean, CG warm-started from phi,
+ * E = -grad_h phi (central differences).  Returns the iteration count (-1: not converged). */
+int32_t oracle_solve_fem(int32_t n, double L, const double *rho, double *phi, double *E, double tol,
+                         int32_t maxit, double *relres) {
+    const int64_t nn = (int64_t)n * n * n;
+    const double h = L / (double)n, h3 = (h * h) * h;
+    double *b = (double *)malloc(sizeof(double) * (size_t)nn);
+    double mean = 0.0;
+    for (int64_t m = 0; m < nn; ++m) {
+        b[m] = h3 * rho[m];
+        mean += b[m];
+    }
+    mean = mean / (double)nn;
+    for (int64_t m = 0; m < nn; ++m) b[m] = b[m] - mean;
+    int32_t it = oracle_fem_cg(n, L, b, phi, tol, maxit, relres);
+    oracle_gradient_central(n, L, phi, E);
+    free(b);
+    return it;
+}
+
+/* oracle_run with the FEM solve; phi in/out (warm start); iters (nullable) per step. */
+void oracle_run_fem(int32_t n, double L, double dt, int64_t np, double *xv, int32_t nsteps,
+                    double *ex_energy, double *tot_energy, double *phi, double tol, int32_t maxit,
+                    int32_t *iters) {
+    const int64_t nn = (int64_t)n * n * n;
+    const double q = -((L * L) * L) / (double)np;
+    const double qm_dt = -1.0 * dt;
+    double *rho = (double *)malloc(sizeof(double) * (size_t)nn);
+    double *E = (double *)malloc(sizeof(double) * (size_t)nn * 3);
+    double *Ep = (double *)malloc(sizeof(double) * (size_t)(np > 0 ? np : 1) * 3);
+    uint32_t *perm = (uint32_t *)malloc(sizeof(uint32_t) * (size_t)(np > 0 ? np : 1));
+    oracle_sort(n, L, np, xv, perm);
+    for (int32_t s = 0; s < nsteps; ++s) {
+        oracle_deposit(n, L, np, xv, q, rho);
+        int32_t it = oracle_solve_fem(n, L, rho, phi, E, tol, maxit, NULL);
+        if (iters) iters[s] = it;
+        double wx, w;
+        oracle_field_energy(n, L, E, &wx, &w);
+        if (ex_energy) ex_energy[s] = wx;
+        if (tot_energy) tot_energy[s] = w;
+        oracle_gather(n, L, np, xv, E, Ep);
+        oracle_push(L, np, xv, Ep, qm_dt, dt);
+        oracle_sort(n, L, np, xv, perm);
+    }
+    free(perm);
+    free(Ep);
+    free(E);
+    free(rho);
+}

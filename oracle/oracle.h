@@ -107,6 +107,17 @@ void oracle_push_ext(double L, int64_t np, double *xv, const double *Ep, double 
 void oracle_run_ext(int32_t n, double L, double dt, int64_t np, double *xv, int32_t nsteps,
                     double *ex_energy, double *tot_energy, const double *b_ext, const double *e_ext);
 
+/* ---- matrix-free Q1 FEM solve (D#33) ---- */
+void oracle_fem_element_stiffness(double h, double Ae[64]);
+void oracle_fem_apply(int32_t n, double L, const double *x, double *y);
+int32_t oracle_fem_cg(int32_t n, double L, const double *b, double *x, double tol, int32_t maxit,
+                      double *relres);
+int32_t oracle_solve_fem(int32_t n, double L, const double *rho, double *phi, double *E, double tol,
+                         int32_t maxit, double *relres);
+void oracle_run_fem(int32_t n, double L, double dt, int64_t np, double *xv, int32_t nsteps,
+                    double *ex_energy, double *tot_energy, double *phi, double tol, int32_t maxit,
+                    int32_t *iters);
+
 #ifdef __cplusplus
 }
 #endif

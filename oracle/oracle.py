@@ -70,6 +70,11 @@ def lib():
                                       i32, C.POINTER(C.c_int32)]),
             "oracle_half_kick_pcg": (None, [i32, dbl, dbl, i64, dp, dp, dbl, dbl, i32, i32, i32]),
             "oracle_boris_coeffs": (None, [dbl, dp, dp, dp]),
+            "oracle_fem_element_stiffness": (None, [dbl, dp]),
+            "oracle_fem_apply": (None, [i32, dbl, dp, dp]),
+            "oracle_fem_cg": (i32, [i32, dbl, dp, dp, dbl, i32, dp]),
+            "oracle_solve_fem": (i32, [i32, dbl, dp, dp, dp, dbl, i32, dp]),
+            "oracle_run_fem": (None, [i32, dbl, dbl, i64, dp, i32, dp, dp, dp, dbl, i32, C.POINTER(C.c_int32)]),
             "oracle_push_ext": (None, [dbl, i64, dp, dp, dbl, dp, dp]),
             "oracle_run_ext": (None, [i32, dbl, dbl, i64, dp, i32, dp, dp, dp, dp]),
         }
@@ -317,3 +322,47 @@ def run_ext(n: int, L: float, dt: float, xv: np.ndarray, nsteps: int, b_ext=None
     b, e = _vec3(b_ext), _vec3(e_ext)
     lib().oracle_run_ext(n, L, dt, xs.shape[1], _dp(xs), nsteps, _dp(ex), _dp(tot), _dp(b), _dp(e))
     return xs, ex[:nsteps], tot[:nsteps]
+
+
+# ---------------------------------- matrix-free Q1 FEM solve ----
+def fem_element_stiffness(h: float) -> np.ndarray:
+    Ae = np.zeros((8, 8))
+    lib().oracle_fem_element_stiffness(h, _dp(Ae))
+    return Ae
+
+
+def fem_apply(n: int, L: float, x: np.ndarray) -> np.ndarray:
+    x = np.ascontiguousarray(x, dtype=np.float64)
+    y = np.zeros((n, n, n))
+    lib().oracle_fem_apply(n, L, _dp(x), _dp(y))
+    return y
+
+
+def fem_cg(n: int, L: float, b: np.ndarray, x0=None, tol=1e-4, maxit=5000):
+    b = np.ascontiguousarray(b, dtype=np.float64)
+    x = np.zeros((n, n, n)) if x0 is None else np.ascontiguousarray(x0, dtype=np.float64).copy()
+    rel = C.c_double()
+    it = lib().oracle_fem_cg(n, L, _dp(b), _dp(x), tol, maxit, C.byref(rel))
+    return x, it, rel.value
+
+
+def solve_fem(n: int, L: float, rho: np.ndarray, phi0=None, tol=1e-4, maxit=5000):
+    """Returns (E, phi, iterations, relative residual)."""
+    rho = np.ascontiguousarray(rho, dtype=np.float64)
+    phi = np.zeros((n, n, n)) if phi0 is None else np.ascontiguousarray(phi0, dtype=np.float64).copy()
+    E = np.zeros((3, n, n, n))
+    rel = C.c_double()
+    it = lib().oracle_solve_fem(n, L, _dp(rho), _dp(phi), _dp(E), tol, maxit, C.byref(rel))
+    return E, phi, it, rel.value
+
+
+def run_fem(n: int, L: float, dt: float, xv: np.ndarray, nsteps: int, phi0=None, tol=1e-4, maxit=5000):
+    """oracle_run with the FEM solve.  Returns (xv, W_x[n], W[n], phi, iterations[n])."""
+    xs = np.ascontiguousarray(xv, dtype=np.float64).copy()
+    ex = np.zeros(max(nsteps, 1))
+    tot = np.zeros(max(nsteps, 1))
+    phi = np.zeros((n, n, n)) if phi0 is None else np.ascontiguousarray(phi0, dtype=np.float64).copy()
+    its = np.zeros(max(nsteps, 1), dtype=np.int32)
+    lib().oracle_run_fem(n, L, dt, xs.shape[1], _dp(xs), nsteps, _dp(ex), _dp(tot), _dp(phi), tol, maxit,
+                         its.ctypes.data_as(C.POINTER(C.c_int32)))
+    return xs, ex[:nsteps], tot[:nsteps], phi, its[:nsteps]
