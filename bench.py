@@ -175,6 +175,8 @@ def _oracle_steps(solver, n, L, xv, steps):
 
     if solver == "pcg":
         return O.run_pcg(n, L, 0.05, xv, steps)[0]
+    if solver == "fem":
+        return O.run_fem(n, L, 0.05, xv, steps)[0]
     return O.run(n, L, 0.05, xv, steps)[0]
 
 
@@ -192,7 +194,7 @@ def oracle_sample(steps: int, n: int = 64, ppc: int = 8, solver: str = "fft"):
     dt = time.perf_counter() - t0
     npart = ppc * n ** 3
     return {"value": npart * steps / dt, "unit": UNIT, "cores": 1, "kind": "oracle",
-            "sample": f"oracle_run{'_pcg' if solver == 'pcg' else ''} (serial C, -O2) on Landau {n}^3 x {ppc} ppc "
+            "sample": f"oracle_run{'' if solver == 'fft' else '_' + solver} (serial C, -O2) on Landau {n}^3 x {ppc} ppc "
                       f"({npart} particles), {steps} steps, {dt:.1f} s; same per-particle "
                       f"step as the {{n}}^3 workload, smaller grid"}
 
@@ -215,7 +217,7 @@ def run_reference(args, rank, world):
     sample = (f"CPU oracle (serial C) on Landau {n}^3 x {ppc} ppc ({npart} particles) per step, "
               f"a bounded sample of the {args.n}^3 x {args.ppc} workload")
     line = {
-        "impl": "reference", "metric": METRIC if args.solver == "fft" else METRIC.replace("FFT-PIC", "PCG-PIC"), "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "impl": "reference", "metric": METRIC.replace("FFT-PIC", args.solver.upper() + "-PIC"), "value": value, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * dt / args.steps,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic",
@@ -246,7 +248,7 @@ def run_ours(args, rank, world):
     ncid = broadcast_nccl_id(rank, world)
     sim = Simulation(n=n, ppc=ppc, k=0.5, alpha=0.05, dt=0.05, seed=1, device=f"cuda:{local}",
                      rank=rank, nranks=world, nccl_id=ncid, solver=args.solver)
-    pcg = args.solver == "pcg"
+    pcg = args.solver in ("pcg", "fem")     # CG-based solvers (iteration statistics)
     torch.cuda.synchronize()
     log(f"[rank {rank}] init {n}^3 x {ppc} (slab z0={sim.z0} nz={sim.nz}, {sim.np} particles): "
         f"{time.perf_counter() - t_init:.1f} s, workspace {sim.workspace.numel() / 2**30:.1f} GiB")
@@ -323,14 +325,17 @@ def run_ours(args, rank, world):
         alg = bp * np_r + bn * ncell
         if name == "pcg_ssor":     # one M^-1 per CG iteration (the first before the loop)
             alg = PCG_SSOR_BYTES_PER_APPLY * ncell * (pcg_iters + args.steps) / args.steps
-        elif name == "pcg_cg":
+        elif name == "pcg_cg":     # FEM: matvec 32 (r, p read; p', q written) + update 48 B/node
             alg = PCG_CG_BYTES_PER_ITER * ncell * pcg_iters / args.steps
         per_stage[name] = {"ms_per_step": tot / args.steps, "launches": nl,
                            "alg_GBps": (alg * args.steps / (tot / 1e3) / 1e9) if tot > 0 else None}
     dom = max((s for s in per_stage if s not in ("clear", "exchange", "xpose")),
               key=lambda s: per_stage[s]["ms_per_step"])
     tot, nl = stages[dom]
-    if dom == "pcg_ssor":      # per half-sweep launch (the reduce of the last one not counted)
+    if dom == "pcg_cg":        # FEM: per CG iteration (matvec + update and their reductions)
+        calls = pcg_iters
+        alg_per_call = PCG_CG_BYTES_PER_ITER * ncell
+    elif dom == "pcg_ssor":    # per half-sweep launch (the reduce of the last one not counted)
         calls = 4 * 4 * 2 * (pcg_iters + args.steps)
         alg_per_call = PCG_SSOR_BYTES_PER_APPLY / 32 * ncell
     else:
@@ -370,7 +375,7 @@ def run_ours(args, rank, world):
         cpu["sample"] = cpu["sample"].replace("{n}", str(n))
     launches = sim.launches_per_step() * args.steps
     line = {
-        "metric": METRIC if not pcg else METRIC.replace("FFT-PIC", "PCG-PIC"), "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "metric": METRIC.replace("FFT-PIC", args.solver.upper() + "-PIC"), "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
         "scaling": "strong" if world > 1 else "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
@@ -393,7 +398,8 @@ def run_ours(args, rank, world):
         "w_x_first_last": [float(ex[0]), float(ex[-1])],
     }
     if pcg:
-        line["pcg"] = {"iters_per_step": pcg_iters / args.steps, "tol": 1e-4, "ssor": "omega=pi/2, 4 inner, 2 outer",
+        line["pcg"] = {"solver": args.solver, "iters_per_step": pcg_iters / args.steps, "tol": 1e-4,
+                       "preconditioner": "SSOR omega=pi/2, 4 inner, 2 outer" if args.solver == "pcg" else "none (plain CG, P:195)",
                        "warm_start": True, "last_relres": sim.pcg_stats()[3]}
     print(json.dumps(line), flush=True)
     sim.close()
@@ -408,8 +414,8 @@ def main():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--n", type=int, default=512)
     ap.add_argument("--ppc", type=int, default=8)
-    ap.add_argument("--solver", choices=["fft", "pcg"], default="fft",
-                    help="field solver: fft (BJ configs 0-3) or pcg (BJ config 5)")
+    ap.add_argument("--solver", choices=["fft", "pcg", "fem"], default="fft",
+                    help="field solver: fft (BJ configs 0-3), pcg (BJ config 5) or fem (SURVEY §8(f) NEXT-4)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-steps", type=int, default=20)

@@ -59,7 +59,11 @@ typedef enum {
  * warm-started from the previous step's phi, stopped at
  * ||r||_2 <= pcg_tol ||b||_2, E = -grad_h phi by central differences
  * (D#26-D#31). */
-typedef enum { PIC_SOLVER_FFT = 0, PIC_SOLVER_PCG = 1 } pic_solver;
+/* FEM: the matrix-free Q1 finite-element solve of P:183-195: the
+ * trilinear element stiffness assembled on the fly as its 27-point stencil, lumped load
+ * h^3 rho - mean, plain CG with pcg_tol / pcg_maxit, warm start, E by central
+ * differences (D#33). */
+typedef enum { PIC_SOLVER_FFT = 0, PIC_SOLVER_PCG = 1, PIC_SOLVER_FEM = 2 } pic_solver;
 
 typedef struct {
     int32_t  n;         /* cells per dimension (grid N^3); power of two, 16..1024     */
@@ -74,7 +78,7 @@ typedef struct {
     int32_t  solver;    /* pic_solver; default PIC_SOLVER_FFT                             */
     int32_t  pcg_inner; /* PCG: SSOR inner sweeps, >= 1; default 4                */
     int32_t  pcg_outer; /* PCG: SSOR outer iterations, >= 1; default 2            */
-    int32_t  pcg_maxit; /* PCG: iteration cap, >= 1; default 1000                         */
+    int32_t  pcg_maxit; /* PCG / FEM: CG iteration cap, >= 1; default 10000                */
     double   pcg_tol;   /* PCG: relative residual tolerance, > 0; default 1e-4    */
     double   pcg_omega; /* PCG: SSOR relaxation, 0 < omega < 2; default pi/2      */
     double   b_ext[3];  /* uniform external magnetic field (Eq. 1); default 0.  Nonzero:
@@ -168,7 +172,7 @@ pic_status pic_set_particles(pic_ctx *ctx, const double *xyzuvw, int64_t np);
 
 /* Copy this rank's slab of a grid to host [nz][N][N] (P = 1: [N][N][N]): which = 0
  * -> rho (charge density of the current positions, q/h^3 scaled); 1, 2, 3 -> E_x,
- * E_y, E_z of the latest solve; 4 -> phi of the latest PCG solve (PCG only, else
+ * E_y, E_z of the latest solve; 4 -> phi of the latest PCG / FEM solve (else
  * PIC_EINVAL). */
 pic_status pic_get_grid(pic_ctx *ctx, int32_t which, double *host);
 
@@ -214,7 +218,7 @@ const char *pic_stage_name(int32_t stage);
  * with the latest solve's iteration count). */
 pic_status pic_launches_per_step(pic_ctx *ctx, int64_t *launches);
 
-/* PCG solver statistics: iterations of the latest solve (-1: not converged), total
+/* PCG / FEM (CG) solver statistics: iterations of the latest solve (-1: not converged), total
  * iterations and solves since pic_init, relative residual ||r||/||b|| of the latest
  * solve.  Any pointer may be NULL.  PIC_EINVAL for an FFT context. */
 pic_status pic_pcg_stats(pic_ctx *ctx, int32_t *last_iters, int64_t *total_iters, int64_t *solves,

@@ -832,3 +832,23 @@ void oracle_run_fem(int32_t n, double L, double dt, int64_t np, double *xv, int3
     free(E);
     free(rho);
 }
+
+/* Backward half kick with the FEM field; phi (in/out) as in oracle_run_fem. */
+void oracle_half_kick_fem(int32_t n, double L, double dt, int64_t np, double *xv, double *phi, double tol,
+                          int32_t maxit) {
+    const int64_t nn = (int64_t)n * n * n;
+    const double q = -((L * L) * L) / (double)np;
+    double *rho = (double *)malloc(sizeof(double) * (size_t)nn);
+    double *E = (double *)malloc(sizeof(double) * (size_t)nn * 3);
+    double *Ep = (double *)malloc(sizeof(double) * (size_t)(np > 0 ? np : 1) * 3);
+    oracle_deposit(n, L, np, xv, q, rho);
+    oracle_solve_fem(n, L, rho, phi, E, tol, maxit, NULL);
+    oracle_gather(n, L, np, xv, E, Ep);
+    const double hk = -0.5 * (-1.0 * dt);
+    for (int64_t j = 0; j < np; ++j)
+        for (int d = 0; d < 3; ++d)
+            xv[(3 + d) * np + j] = fma(hk, Ep[d * np + j], xv[(3 + d) * np + j]);
+    free(Ep);
+    free(E);
+    free(rho);
+}

@@ -117,6 +117,8 @@ int32_t oracle_solve_fem(int32_t n, double L, const double *rho, double *phi, do
 void oracle_run_fem(int32_t n, double L, double dt, int64_t np, double *xv, int32_t nsteps,
                     double *ex_energy, double *tot_energy, double *phi, double tol, int32_t maxit,
                     int32_t *iters);
+void oracle_half_kick_fem(int32_t n, double L, double dt, int64_t np, double *xv, double *phi, double tol,
+                          int32_t maxit);
 
 #ifdef __cplusplus
 }

@@ -74,6 +74,7 @@ def lib():
             "oracle_fem_apply": (None, [i32, dbl, dp, dp]),
             "oracle_fem_cg": (i32, [i32, dbl, dp, dp, dbl, i32, dp]),
             "oracle_solve_fem": (i32, [i32, dbl, dp, dp, dp, dbl, i32, dp]),
+            "oracle_half_kick_fem": (None, [i32, dbl, dbl, i64, dp, dp, dbl, i32]),
             "oracle_run_fem": (None, [i32, dbl, dbl, i64, dp, i32, dp, dp, dp, dbl, i32, C.POINTER(C.c_int32)]),
             "oracle_push_ext": (None, [dbl, i64, dp, dp, dbl, dp, dp]),
             "oracle_run_ext": (None, [i32, dbl, dbl, i64, dp, i32, dp, dp, dp, dp]),
@@ -366,3 +367,15 @@ def run_fem(n: int, L: float, dt: float, xv: np.ndarray, nsteps: int, phi0=None,
     lib().oracle_run_fem(n, L, dt, xs.shape[1], _dp(xs), nsteps, _dp(ex), _dp(tot), _dp(phi), tol, maxit,
                          its.ctypes.data_as(C.POINTER(C.c_int32)))
     return xs, ex[:nsteps], tot[:nsteps], phi, its[:nsteps]
+
+
+def init_state_fem(n: int, ppc: int, k: float = 0.5, alpha: float = 0.05, seed: int = 1,
+                   dt: float = 0.05, L: float | None = None, tol=1e-4, maxit=5000):
+    """pic_init with the FEM solver: sample, canonicalise, half kick with the FEM field."""
+    if L is None:
+        L = 2.0 * np.pi / k
+    xv = sample_landau(ppc * n ** 3, k, L, alpha, seed)
+    xv, _ = sort(n, L, xv)
+    phi = np.zeros((n, n, n))
+    lib().oracle_half_kick_fem(n, L, dt, xv.shape[1], _dp(xv), _dp(phi), tol, maxit)
+    return xv, phi

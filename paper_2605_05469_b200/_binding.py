@@ -22,8 +22,8 @@ PIC_ENONCONV = -9
 STATUS_NAMES = {0: "PIC_OK", -1: "PIC_EINVAL", -2: "PIC_ENOMEM", -3: "PIC_ECUDA", -4: "PIC_ENCCL",
                 -5: "PIC_ENONFINITE", -6: "PIC_EOVERFLOW", -7: "PIC_EPOISONED",
                 -8: "PIC_EUNSUPPORTED", -9: "PIC_ENONCONV"}
-PIC_SOLVER_FFT, PIC_SOLVER_PCG = 0, 1
-SOLVERS = {"fft": PIC_SOLVER_FFT, "pcg": PIC_SOLVER_PCG}
+PIC_SOLVER_FFT, PIC_SOLVER_PCG, PIC_SOLVER_FEM = 0, 1, 2
+SOLVERS = {"fft": PIC_SOLVER_FFT, "pcg": PIC_SOLVER_PCG, "fem": PIC_SOLVER_FEM}
 
 STAGES = ["fft_x_fwd", "fft_y_fwd", "fft_z_mul", "fft_y_inv", "fft_x_inv", "energy", "clear",
           "push_key", "scan", "place", "reorder_deposit", "exchange", "xpose", "pcg_ssor", "pcg_cg",
@@ -175,7 +175,7 @@ class Simulation:
     def __init__(self, n=16, ppc=8, k=0.5, alpha=0.05, dt=0.05, seed=1, half_kick=True,
                  length=0.0, device=None, rank=0, nranks=1, nccl_id: bytes | None = None,
                  solver="fft", **pcg):
-        """solver: "fft" or "pcg" (BJ config 5); pcg keywords
+        """solver: "fft", "pcg" (BJ config 5) or "fem"; pcg keywords
         pcg_tol, pcg_omega, pcg_inner, pcg_outer, pcg_maxit override P:226 / P:260;
         b_ext=(bx, by, bz) / e_ext=(ex, ey, ez): uniform external fields (Eq. 1, D#32)."""
         import torch

@@ -154,6 +154,20 @@ void launch_pcg_gradient(const Geom& g, PcgNbr x, double* E4, double* halo, doub
                          cudaStream_t s);
 void launch_pcg_unsplit(const Geom& g, const double* f, double* out, cudaStream_t s);
 
+// ------------------------------------------------------ Q1 FEM solve ------
+// (fem_kernels.cu.)  Natural [zl][y][x] fields;
+// scalars sc[]: 0 sum of the load, 1 (b,b), 2 (r,r), 4 previous (r,r), 5 (p,Ap).
+void launch_fem_load_sum(const Geom& g, const double* raw, double dscale, double* partials, double* sc,
+                         cudaStream_t s);
+void launch_fem_resid0(const Geom& g, const double* raw, double dscale, double* sc, double nn, PcgNbr x,
+                       double* r, double* partials, cudaStream_t s);
+void launch_fem_matvec(const Geom& g, bool first, PcgNbr r, PcgNbr p, double* pout, double* q, double* sc,
+                       double* partials, cudaStream_t s);
+void launch_fem_update(const Geom& g, double* x, const double* p, double* r, const double* q, double* sc,
+                       double* partials, cudaStream_t s);
+void launch_fem_gradient(const Geom& g, PcgNbr x, double* E4, double* halo, double* partials, double* energies,
+                         cudaStream_t s);
+
 void particles_set_smem_limits();
 void fft_set_smem_limits();
 

@@ -160,11 +160,11 @@ pic_status validate(const pic_params* p, int32_t rank, int32_t nranks, char* msg
         snprintf(msg, msz, "k L / 2 pi = %g must be a positive integer", m);
         return PIC_EINVAL;
     }
-    if (p->solver != PIC_SOLVER_FFT && p->solver != PIC_SOLVER_PCG) {
-        snprintf(msg, msz, "solver=%d: PIC_SOLVER_FFT (0) or PIC_SOLVER_PCG (1)", p->solver);
+    if (p->solver != PIC_SOLVER_FFT && p->solver != PIC_SOLVER_PCG && p->solver != PIC_SOLVER_FEM) {
+        snprintf(msg, msz, "solver=%d: PIC_SOLVER_FFT (0), PIC_SOLVER_PCG (1) or PIC_SOLVER_FEM (2)", p->solver);
         return PIC_EINVAL;
     }
-    if (p->solver == PIC_SOLVER_PCG &&
+    if (p->solver != PIC_SOLVER_FFT &&
         (!(p->pcg_tol > 0) || !(p->pcg_omega > 0 && p->pcg_omega < 2) || p->pcg_inner < 1 || p->pcg_outer < 1 ||
          p->pcg_maxit < 1)) {
         snprintf(msg, msz, "PCG: need tol > 0, 0 < omega < 2, inner >= 1, outer >= 1, maxit >= 1");
@@ -219,7 +219,7 @@ struct Sizes {
 
 Sizes sizes(const pic_params* p, const Geom& g) {
     Sizes s{};
-    s.pcg = p->solver == PIC_SOLVER_PCG;
+    s.pcg = p->solver == PIC_SOLVER_PCG || p->solver == PIC_SOLVER_FEM;   // the CG vectors
     const int64_t npg = (int64_t)p->ppc * p->n * p->n * p->n;
     s.np_nom = npg / g.P;
     if (g.P == 1) {
@@ -718,9 +718,85 @@ pic_status solve_pcg(pic_ctx* c, double dscale, int slot) {
     return PIC_OK;
 }
 
+// The FEM solve (D#33): load
+// b = h^3 dscale raw - mean, plain CG on the 27-point Q1 stiffness warm-started from
+// pcg_x (natural layout), E = -grad_h phi -> E4 (+ the halo plane of the slab below).
+pic_status solve_fem(pic_ctx* c, double dscale, int slot) {
+    const Geom& g = c->g;
+    double* sc = c->pcg_sc;
+    const double nn = (double)g.n * g.n * g.n;
+    const double tol = c->p.pcg_tol;
+    c->pcg_launches = 0;
+    if (g.P > 1) PIC_TRY(barrier(c));
+    {
+        StageScope t(c, PIC_STAGE_PCG_CG, 4);
+        pic::launch_fem_load_sum(g, c->rho, dscale, c->partials, sc, c->stream);
+        PIC_LAUNCHED(c, "fem_load_sum");
+        PIC_TRY(pcg_allreduce(c, sc, 1));
+        pic::launch_fem_resid0(g, c->rho, dscale, sc, nn, pcg_nbr(c, c->pcg_x), c->pcg_r, c->partials, c->stream);
+        PIC_LAUNCHED(c, "fem_resid0");
+        PIC_TRY(pcg_allreduce(c, sc + 1, 2));
+        c->pcg_launches += 4;
+    }
+    double h[2];
+    PIC_TRY(pcg_read(c, h, sc + 1, 2));
+    const double bb = h[0], stop = (tol * tol) * bb;
+    double rr = h[1];
+    int it = 0;
+    bool converged = false;
+    if (bb == 0.0) {
+        PIC_CUDA(c, cudaMemsetAsync(c->pcg_x, 0, sizeof(double) * (size_t)c->ncell, c->stream));
+        converged = true;
+        rr = 0.0;
+    } else if (rr <= stop) {
+        converged = true;
+    } else {
+        for (it = 1; it <= c->p.pcg_maxit; ++it) {
+            double* pold = c->pcg_p[c->pcg_pi];
+            double* pnew = c->pcg_p[c->pcg_pi ^ 1];
+            StageScope t(c, PIC_STAGE_PCG_CG, 4);
+            pic::launch_fem_matvec(g, it == 1, pcg_nbr(c, c->pcg_r), pcg_nbr(c, pold), pnew, c->pcg_q, sc,
+                                   c->partials, c->stream);          // p = r + beta p, q = A p, sc[5]
+            PIC_LAUNCHED(c, "fem_matvec");
+            PIC_TRY(pcg_allreduce(c, sc + 5, 1));
+            pic::launch_fem_update(g, c->pcg_x, pnew, c->pcg_r, c->pcg_q, sc, c->partials, c->stream);
+            PIC_LAUNCHED(c, "fem_update");
+            PIC_TRY(pcg_allreduce(c, sc + 2, 1));
+            c->pcg_launches += 4;
+            c->pcg_pi ^= 1;
+            PIC_TRY(pcg_read(c, &rr, sc + 2, 1));
+            if (rr <= stop) { converged = true; break; }
+        }
+    }
+    c->pcg_last_iters = converged ? it : -1;
+    c->pcg_total_iters += it > c->p.pcg_maxit ? c->p.pcg_maxit : it;
+    c->pcg_solves += 1;
+    c->pcg_last_relres = bb > 0.0 ? std::sqrt(rr / bb) : 0.0;
+    {
+        StageScope t(c, PIC_STAGE_PCG_FIELD, 2);
+        pic::launch_fem_gradient(g, pcg_nbr(c, c->pcg_x), c->E4, halo_dst(c), c->partials, c->energies + 2 * slot,
+                                 c->stream);
+        PIC_LAUNCHED(c, "fem_gradient");
+        c->pcg_launches += 2;
+    }
+    if (g.P > 1) {
+        StageScope t(c, PIC_STAGE_EXCHANGE, 0);
+        PIC_NCCL(c, ncclAllReduce(c->energies + 2 * slot, c->energies + 2 * slot, 2, ncclDouble, ncclSum,
+                                  c->comm, c->stream));
+    }
+    c->last_slot = slot;
+    if (!converged) {
+        snprintf(c->err, sizeof(c->err), "FEM CG did not converge in %d iterations (relative residual %.3e)",
+                 c->p.pcg_maxit, c->pcg_last_relres);
+        return PIC_ENONCONV;
+    }
+    return PIC_OK;
+}
+
 // The field solve of the configured solver; rho = dscale * (the raw charge planes).
 pic_status solve_field(pic_ctx* c, double dscale, int slot) {
     if (c->p.solver == PIC_SOLVER_PCG) return solve_pcg(c, dscale, slot);
+    if (c->p.solver == PIC_SOLVER_FEM) return solve_fem(c, dscale, slot);
     return solve(c, dscale / ((double)c->g.n * c->g.n * c->g.n), slot);   // 1/N^3 of the whole box
 }
 
@@ -970,7 +1046,7 @@ pic_status pic_params_default(pic_params* p) {
     p->solver = PIC_SOLVER_FFT;
     p->pcg_inner = 4;
     p->pcg_outer = 2;
-    p->pcg_maxit = 1000;
+    p->pcg_maxit = 10000;         // plain CG (FEM) needs ~N iterations
     p->pcg_tol = 1e-4;
     p->pcg_omega = M_PI / 2;      // P:260 "damping factor of pi/2"
     return PIC_OK;
@@ -1059,8 +1135,8 @@ pic_status pic_init(const pic_params* p, int32_t rank, int32_t nranks, const uin
             return bail(PIC_ENCCL);
         }
         if ((st = setup_p2p(c)) != PIC_OK) return bail(st);
-        if (p->solver == PIC_SOLVER_PCG && !c->p2p) {
-            snprintf(c->err, sizeof(c->err), "the PCG solver at P > 1 needs the peer-memory transport");
+        if (p->solver != PIC_SOLVER_FFT && !c->p2p) {
+            snprintf(c->err, sizeof(c->err), "the PCG / FEM solvers at P > 1 need the peer-memory transport");
             return bail(PIC_EUNSUPPORTED);
         }
     }
@@ -1217,8 +1293,12 @@ pic_status pic_get_grid(pic_ctx* c, int32_t which, double* host) {
         PIC_TRY(copy_grid_to_host(c, host, c->rho));
     } else if (which == 4) {
         double* scratch = reinterpret_cast<double*>(c->specC);
-        pic::launch_pcg_unsplit(c->g, c->pcg_x, scratch, c->stream);
-        PIC_LAUNCHED(c, "pcg_unsplit");
+        if (c->p.solver == PIC_SOLVER_PCG) {
+            pic::launch_pcg_unsplit(c->g, c->pcg_x, scratch, c->stream);
+            PIC_LAUNCHED(c, "pcg_unsplit");
+        } else {
+            scratch = c->pcg_x;     // FEM: natural layout already
+        }
         PIC_CUDA(c, cudaMemcpyAsync(host, scratch, sizeof(double) * (size_t)c->ncell,
                                     cudaMemcpyDeviceToHost, c->stream));
     } else {
@@ -1328,14 +1408,14 @@ pic_status pic_launches_per_step(pic_ctx* c, int64_t* launches) {
     // solve 6, push_key 1, scan 3, place 1, reorder_deposit 1; P > 1: arrivals 1, and
     // the NCCL transport's ghost fold 1 or the peer transport's count update 1
     *launches = 12 + (c->g.P > 1 ? 2 : 0);
-    if (c->p.solver == PIC_SOLVER_PCG) *launches += c->pcg_launches - 6;   // the latest PCG solve's count
+    if (c->p.solver != PIC_SOLVER_FFT) *launches += c->pcg_launches - 6;   // the latest CG solve's count
     return PIC_OK;
 }
 
 pic_status pic_pcg_stats(pic_ctx* c, int32_t* last_iters, int64_t* total_iters, int64_t* solves,
                          double* last_relres) {
     if (!c) return PIC_EINVAL;
-    if (c->p.solver != PIC_SOLVER_PCG) { snprintf(c->err, sizeof(c->err), "not a PCG context"); return PIC_EINVAL; }
+    if (c->p.solver == PIC_SOLVER_FFT) { snprintf(c->err, sizeof(c->err), "not a PCG / FEM context"); return PIC_EINVAL; }
     if (last_iters) *last_iters = c->pcg_last_iters;
     if (total_iters) *total_iters = c->pcg_total_iters;
     if (solves) *solves = c->pcg_solves;

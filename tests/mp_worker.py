@@ -45,6 +45,9 @@ def main():
         if solver == "pcg":
             ref, rex, _, _, _ = O.run_pcg(n, L, dt, xv0, nsteps, phi0=phi0)
             return ref, rex
+        if solver == "fem":
+            ref, rex, _, _, _ = O.run_fem(n, L, dt, xv0, nsteps, phi0=phi0)
+            return ref, rex
         ref, rex, _, _ = O.run(n, L, dt, xv0, nsteps)
         return ref, rex
 
@@ -95,6 +98,8 @@ def main():
         assert sum(counts) == ppc * n ** 3, counts
         if solver == "pcg":
             ref0, phi0 = O.init_state_pcg(n, ppc, seed=9)
+        elif solver == "fem":
+            ref0, phi0 = O.init_state_fem(n, ppc, seed=9)
         else:
             ref0, phi0 = O.init_state(n, ppc, seed=9), None
         _, rex2 = oracle_run(ref0, 10, phi0)

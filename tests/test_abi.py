@@ -103,11 +103,11 @@ def test_pcg_defaults_and_validation():
 
     p = B.default_params()
     assert p.solver == B.PIC_SOLVER_FFT
-    assert (p.pcg_inner, p.pcg_outer, p.pcg_maxit) == (4, 2, 1000)
+    assert (p.pcg_inner, p.pcg_outer, p.pcg_maxit) == (4, 2, 10000)
     assert p.pcg_tol == 1e-4 and p.pcg_omega == math.pi / 2
     assert tuple(p.b_ext) == (0.0, 0.0, 0.0) and tuple(p.e_ext) == (0.0, 0.0, 0.0)
     for bad in (dict(pcg_tol=0.0), dict(pcg_omega=2.0), dict(pcg_omega=0.0), dict(pcg_inner=0),
-                dict(pcg_outer=0), dict(pcg_maxit=0), dict(solver=2)):
+                dict(pcg_outer=0), dict(pcg_maxit=0), dict(solver=3)):
         q = B.default_params(**{"solver": B.PIC_SOLVER_PCG, **bad})
         with pytest.raises(B.PicError) as e:
             B.workspace_bytes(q)

@@ -37,19 +37,20 @@ def test_slab_decomposition_matches_oracle(world, n, transport):
     assert "MP OK" in r.stdout and f"transport={transport}" in r.stdout
 
 
+@pytest.mark.parametrize("solver", ["pcg", "fem"])
 @pytest.mark.parametrize("world,n", [(2, 32), (4, 32)])
-def test_slab_decomposition_pcg_matches_oracle(world, n):
-    """The FD-PCG solver (BJ config 5) on z-slabs: the SSOR half-sweeps, the matvec and
-    the gradient read the neighbour slabs' planes over NVLink (peer transport), the
-    dot products are all-reduced; vs the single-domain oracle_run_pcg."""
+def test_slab_decomposition_cg_solvers_match_oracle(world, n, solver):
+    """The FD-PCG (BJ config 5) and Q1 FEM solvers on z-slabs: the stencils read the
+    neighbour slabs' planes over NVLink (peer transport), the dot products are
+    all-reduced; vs the single-domain oracle_run_pcg / oracle_run_fem."""
     if _ngpus() < world:
         pytest.skip(f"needs {world} GPUs")
-    env = dict(os.environ, MP_EXPECT_TRANSPORT="peer", MP_SOLVER="pcg")
+    env = dict(os.environ, MP_EXPECT_TRANSPORT="peer", MP_SOLVER=solver)
     env.pop("PIC_P2P", None)
-    port = 29650 + 10 * world
+    port = 29650 + 10 * world + (solver == "fem")
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
            "--master-addr", "127.0.0.1", "--master-port", str(port),
            os.path.join(ROOT, "tests", "mp_worker.py"), str(n), "8", "20"]
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=ROOT, env=env)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
-    assert "MP OK" in r.stdout and "solver=pcg" in r.stdout
+    assert "MP OK" in r.stdout and f"solver={solver}" in r.stdout
