@@ -87,6 +87,13 @@ enum { DC_N = 0, DC_ARR = 1, DC_LEAVE = 2, DC_MIGRATED = 3 };
 void launch_push_key(const Geom& g, PState cur, const uint32_t* offs, const double* E4, uint32_t* key,
                      uint16_t* rank, uint32_t* count, double2* send, uint32_t* send_count,
                      const SendSegs& segs, const PeerRecv* peers, int* err_flag, cudaStream_t s);
+// Batched peer migration: the leavers push_key staged in this rank's send segments go
+// to each destination's receive buffer at a range reserved with one system atomic on
+// its arrival counter (base[P] scratch); false when PIC_P2P_MIG=1 selects the
+// unbatched path inside push_key.
+bool leavers_batched();
+void launch_leaver_copy(const Geom& g, const double2* send, const SendSegs& segs, const uint32_t* send_count,
+                        uint32_t* base, const PeerRecv& peers, int* err_flag, cudaStream_t s);
 // Arrivals: key/rank at extended index n_old + a.  dcnt != null: n_old and the
 // number of arrivals are read on the device (dcnt[DC_N], dcnt[DC_ARR] <= max_arr).
 void launch_key_arrivals(const Geom& g, const double2* recv, int64_t narr, int64_t n_old, uint32_t* key,

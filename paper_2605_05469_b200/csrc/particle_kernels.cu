@@ -377,6 +377,40 @@ __global__ void k_counts_update(int P, unsigned long long* dcnt, const uint32_t*
 
 __global__ void k_set_u64(unsigned long long* p, unsigned long long v) { *p = v; }
 
+// Peer-memory migration, batched (default): push_key staged the leavers in this rank's
+// local send segments; one thread per destination reserves a contiguous range of the
+// destination's receive buffer (one system-scope atomic per rank pair) ...
+__global__ void k_leaver_reserve(int P, int rank, const uint32_t* __restrict__ send_count, PeerRecv peers,
+                                 const SendSegs segs, uint32_t* __restrict__ base, int* err) {
+    const int r = threadIdx.x;
+    if (r >= P || r == rank) return;
+    const uint32_t n = min(send_count[r], (uint32_t)segs.cap[r]);
+    base[r] = 0;
+    if (n == 0) return;
+    const unsigned long long b = atomicAdd_system(peers.peer_arr[r], (unsigned long long)n);
+    if (b + n > (unsigned long long)peers.recv_cap) atomicExch(err + 2, 1);
+    base[r] = (uint32_t)b;
+}
+// ... and every CTA streams its share of the records over NVLink with coalesced 16-B
+// stores (the per-brick remote atomics and 64-B stores of the unbatched path ran at
+// ~0.1 TB/s and cost 2-3 ms per step at 512^3 on 2-4 GPUs).
+__global__ void __launch_bounds__(256) k_leaver_copy(int P, int rank, const double2* __restrict__ send,
+                                                     const SendSegs segs, const uint32_t* __restrict__ send_count,
+                                                     const uint32_t* __restrict__ base, PeerRecv peers) {
+    for (int r = 0; r < P; ++r) {
+        if (r == rank) continue;
+        const int64_t n = min(send_count[r], (uint32_t)segs.cap[r]);
+        const int64_t b = base[r];
+        const int64_t m = n < peers.recv_cap - b ? n : peers.recv_cap - b;
+        const double2* src = send + 4 * segs.off[r];
+        double2* dst = peers.peer_recv[r] + 4 * b;
+        for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < 4 * m;
+             i += (int64_t)gridDim.x * blockDim.x)
+            dst[i] = __ldcs(src + i);
+    }
+    __threadfence_system();
+}
+
 __global__ void __launch_bounds__(kThreads) k_gkeys(Geom g, PState cur, int64_t np,
                                                     uint32_t* __restrict__ key) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -829,10 +863,25 @@ void launch_push_key(const Geom& g, PState cur, const uint32_t* offs, const doub
     sb.data = send;
     sb.count = send_count;
     sb.segs = segs;
-    if (peers) { sb.peers = *peers; sb.remote = 1; }
+    // peers: the unbatched path (leavers straight into the destination from every brick)
+    // only with PIC_P2P_MIG=1; by default the leavers stay local here and
+    // launch_leaver_copy moves them in one stream per destination
+    static const bool unbatched = [] { const char* e = getenv("PIC_P2P_MIG"); return e && e[0] == '1'; }();
+    if (peers && unbatched) { sb.peers = *peers; sb.remote = 1; }
     static const bool force_mr = getenv("PIC_FORCE_MR") != nullptr;   // diagnostics
     if (g.P > 1 || force_mr) k_push_key_brick<true><<<nbrick, kThreads, 0, s>>>(g, cur, offs, E4, key, rank, count, sb, err_flag);
     else k_push_key_brick<false><<<nbrick, kThreads, 0, s>>>(g, cur, offs, E4, key, rank, count, sb, err_flag);
+}
+
+bool leavers_batched() {
+    const char* e = getenv("PIC_P2P_MIG");
+    return !(e && e[0] == '1');
+}
+
+void launch_leaver_copy(const Geom& g, const double2* send, const SendSegs& segs, const uint32_t* send_count,
+                        uint32_t* base, const PeerRecv& peers, int* err_flag, cudaStream_t s) {
+    k_leaver_reserve<<<1, 32, 0, s>>>(g.P, g.rank, send_count, peers, segs, base, err_flag);
+    k_leaver_copy<<<148 * 2, 256, 0, s>>>(g.P, g.rank, send, segs, send_count, base, peers);
 }
 
 void launch_key_arrivals(const Geom& g, const double2* recv, int64_t narr, int64_t n_old, uint32_t* key,

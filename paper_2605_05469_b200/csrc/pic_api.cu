@@ -835,6 +835,11 @@ pic_status push_sort_deposit(pic_ctx* c, int push) {
             pic::launch_key_import(g, cur, c->np, c->key, c->rank, c->count, c->err_flag, c->stream);
     }
     PIC_LAUNCHED(c, "push_key");
+    if (peer_mig && pic::leavers_batched()) {
+        StageScope t(c, PIC_STAGE_EXCHANGE, 2);
+        pic::launch_leaver_copy(g, c->send, c->segs, c->send_count, c->recv_count, peers, c->err_flag, c->stream);
+        PIC_LAUNCHED(c, "leaver_copy");
+    }
     const int64_t n_old = c->np;
     int64_t narr = 0, nleave = 0, n_bound = n_old;
     const unsigned long long* dc = nullptr;
@@ -1407,7 +1412,7 @@ pic_status pic_launches_per_step(pic_ctx* c, int64_t* launches) {
     if (!c || !launches) return PIC_EINVAL;
     // solve 6, push_key 1, scan 3, place 1, reorder_deposit 1; P > 1: arrivals 1, and
     // the NCCL transport's ghost fold 1 or the peer transport's count update 1
-    *launches = 12 + (c->g.P > 1 ? 2 : 0);
+    *launches = 12 + (c->g.P > 1 ? 2 : 0) + (c->g.P > 1 && c->p2p && pic::leavers_batched() ? 2 : 0);
     if (c->p.solver != PIC_SOLVER_FFT) *launches += c->pcg_launches - 6;   // the latest CG solve's count
     return PIC_OK;
 }
