@@ -246,7 +246,7 @@ def run_ours(args, rank, world):
     np_ = ppc * n ** 3                      # particles of the whole job
     t_init = time.perf_counter()
     ncid = broadcast_nccl_id(rank, world)
-    sim = Simulation(n=n, ppc=ppc, k=0.5, alpha=0.05, dt=0.05, seed=1, device=f"cuda:{local}",
+    sim = Simulation(n=n, ppc=ppc, k=0.5, alpha=0.05, dt=args.dt, seed=1, device=f"cuda:{local}",
                      rank=rank, nranks=world, nccl_id=ncid, solver=args.solver)
     pcg = args.solver in ("pcg", "fem")     # CG-based solvers (iteration statistics)
     torch.cuda.synchronize()
@@ -380,7 +380,7 @@ def run_ours(args, rank, world):
         "scaling": "strong" if world > 1 else "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": cfg_name, "grid": n, "ppc": ppc, "particles": np_,
-                   "k": 0.5, "alpha": 0.05, "dt": 0.05,
+                   "k": 0.5, "alpha": 0.05, "dt": args.dt,
                    "parallelism": "1 GPU" if world == 1 else
                    f"z-slab decomposition over {world} GPUs (NCCL all-to-all FFT transposes; halo "
                    f"plane, ghost plane and particle migration over "
@@ -416,6 +416,7 @@ def main():
     ap.add_argument("--ppc", type=int, default=8)
     ap.add_argument("--solver", choices=["fft", "pcg", "fem"], default="fft",
                     help="field solver: fft (BJ configs 0-3), pcg (BJ config 5) or fem (SURVEY §8(f) NEXT-4)")
+    ap.add_argument("--dt", type=float, default=0.05, help="time step (diagnostics; the workload is dt = 0.05)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-steps", type=int, default=20)
