@@ -14,6 +14,8 @@
 // neighbour slabs (P > 1, peer memory) or wrap (P = 1).  A thread owns four
 // consecutive nodes of a row (256-bit rows) and a CTA walks a chunk of planes for a
 // block of rows (z-march: the stencil's zl +- 1 rows are L1/L2 hits).
+#include <cstdlib>
+
 #include "kernels.h"
 
 namespace pic {
@@ -157,7 +159,8 @@ __global__ void __launch_bounds__(kFT) k_fem_resid0(Geom g, const double* __rest
 }
 
 // p' = r + beta p (first: r), q = A p', partial (p', q); beta = sc[2] / sc[4].
-template <bool FIRST>
+// STORE = false: the operand is already p' (formed by k_fem_paxpy), only q is written.
+template <bool FIRST, bool STORE = true>
 __global__ void __launch_bounds__(kFT) k_fem_matvec(Geom g, FNbr r, FNbr p, double* __restrict__ pout,
                                                     double* __restrict__ q, const double* __restrict__ sc,
                                                     double c0, double c2, double c3, int cz,
@@ -169,13 +172,28 @@ __global__ void __launch_bounds__(kFT) k_fem_matvec(Geom g, FNbr r, FNbr p, doub
         double av[4], pv[4];
         apply_q1(g, r, FIRST ? nullptr : &p, beta, zl, m.y, m.x, c0, c2, c3, av, pv);
         const int64_t o = ((int64_t)zl * g.n + m.y) * g.n + m.x;
-        st4f(pout + o, pv);
+        if (STORE) st4f(pout + o, pv);
         st4f(q + o, av);
 #pragma unroll
         for (int k = 0; k < 4; ++k) acc = fma(pv[k], av[k], acc);
     }
     fblock_partials(&acc, 1, partials);
     if (g.P > 1) __threadfence_system();
+}
+
+// p' = r + beta p, streaming (the split matvec: the stencil then reads one field).
+__global__ void __launch_bounds__(kFT) k_fem_paxpy(int64_t n4, const double* __restrict__ r,
+                                                   const double* __restrict__ p, double* __restrict__ pout,
+                                                   const double* __restrict__ sc) {
+    const double beta = sc[2] / sc[4];
+    for (int64_t i = (int64_t)blockIdx.x * kFT + threadIdx.x; i < n4; i += (int64_t)gridDim.x * kFT) {
+        double rv[4], pv[4];
+        ld4f(r + 4 * i, rv);
+        ld4f(p + 4 * i, pv);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) pv[k] = __dadd_rn(rv[k], __dmul_rn(beta, pv[k]));
+        st4f(pout + 4 * i, pv);
+    }
 }
 
 // x += alpha p ; r -= alpha q ; partial (r, r); alpha = sc[2] / sc[5].
@@ -313,6 +331,29 @@ void launch_fem_matvec(const Geom& g, bool first, PcgNbr r, PcgNbr p, double* po
     const Q1 c = q1_coeffs(g);
     if (first) k_fem_matvec<true><<<grid, kFT, 0, s>>>(g, fn(r), fn(p), pout, q, sc, c.c0, c.c2, c.c3, cz, partials);
     else k_fem_matvec<false><<<grid, kFT, 0, s>>>(g, fn(r), fn(p), pout, q, sc, c.c0, c.c2, c.c3, cz, partials);
+    k_fem_reduce<<<1, 1024, 0, s>>>(g, partials, (int)grid, 1, sc + 5, nullptr, 0);
+}
+
+bool fem_split() {
+    const char* e = getenv("PIC_FEM_SPLIT");
+    return !(e && e[0] == '0');
+}
+
+void launch_fem_paxpy(const Geom& g, const double* r, const double* p, double* pout, const double* sc,
+                      cudaStream_t s) {
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int64_t n4 = (int64_t)g.n * g.n * g.nzl / 4;
+    const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>((n4 + kFT - 1) / kFT, (int64_t)sms * 8));
+    k_fem_paxpy<<<grid, kFT, 0, s>>>(n4, r, p, pout, sc);
+}
+
+void launch_fem_stencil(const Geom& g, PcgNbr p, double* q, double* sc, double* partials, cudaStream_t s) {
+    int cz = 1;
+    const unsigned grid = fmarch_grid(g, &cz);
+    const Q1 c = q1_coeffs(g);
+    k_fem_matvec<true, false><<<grid, kFT, 0, s>>>(g, fn(p), fn(p), nullptr, q, sc, c.c0, c.c2, c.c3, cz, partials);
     k_fem_reduce<<<1, 1024, 0, s>>>(g, partials, (int)grid, 1, sc + 5, nullptr, 0);
 }
 

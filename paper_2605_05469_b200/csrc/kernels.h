@@ -170,6 +170,12 @@ void launch_fem_resid0(const Geom& g, const double* raw, double dscale, double* 
                        double* r, double* partials, cudaStream_t s);
 void launch_fem_matvec(const Geom& g, bool first, PcgNbr r, PcgNbr p, double* pout, double* q, double* sc,
                        double* partials, cudaStream_t s);
+// Split matvec (default; PIC_FEM_SPLIT=0: fused): pout = r + beta p streaming, then
+// q = A pout, sc[5] = (pout, q) with the stencil on one field.
+bool fem_split();
+void launch_fem_paxpy(const Geom& g, const double* r, const double* p, double* pout, const double* sc,
+                      cudaStream_t s);
+void launch_fem_stencil(const Geom& g, PcgNbr p, double* q, double* sc, double* partials, cudaStream_t s);
 void launch_fem_update(const Geom& g, double* x, const double* p, double* r, const double* q, double* sc,
                        double* partials, cudaStream_t s);
 void launch_fem_gradient(const Geom& g, PcgNbr x, double* E4, double* halo, double* partials, double* energies,

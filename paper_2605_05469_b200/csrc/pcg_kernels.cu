@@ -323,15 +323,6 @@ struct OctPos {
     int zl, y, j;
     int64_t row;
 };
-__device__ __forceinline__ OctPos oct_pos(const Geom& g, int64_t t) {
-    const int ln = lg2(g.n);
-    OctPos q;
-    q.row = t >> (ln - 3);                       // n / 8 octets per row
-    q.j = 4 * (int)(t & ((g.n >> 3) - 1));
-    q.y = (int)(q.row & g.nmask);
-    q.zl = (int)(q.row >> ln);
-    return q;
-}
 
 // r = (rho - mean) - A x (D#27), partials of (b, b) and (r, r).  Thread = octet.
 __global__ void __launch_bounds__(kPT) k_pcg_resid0_8(Geom g, const double* __restrict__ raw, double dscale,

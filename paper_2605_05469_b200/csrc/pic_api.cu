@@ -755,8 +755,16 @@ pic_status solve_fem(pic_ctx* c, double dscale, int slot) {
             double* pold = c->pcg_p[c->pcg_pi];
             double* pnew = c->pcg_p[c->pcg_pi ^ 1];
             StageScope t(c, PIC_STAGE_PCG_CG, 4);
-            pic::launch_fem_matvec(g, it == 1, pcg_nbr(c, c->pcg_r), pcg_nbr(c, pold), pnew, c->pcg_q, sc,
-                                   c->partials, c->stream);          // p = r + beta p, q = A p, sc[5]
+            if (it > 1 && pic::fem_split()) {                  // p = r + beta p; q = A p, sc[5]
+                pic::launch_fem_paxpy(g, c->pcg_r, pold, pnew, sc, c->stream);
+                PIC_LAUNCHED(c, "fem_paxpy");
+                if (g.P > 1) PIC_TRY(barrier(c));              // the peers' p is complete
+                pic::launch_fem_stencil(g, pcg_nbr(c, pnew), c->pcg_q, sc, c->partials, c->stream);
+                c->pcg_launches += 1;
+            } else {
+                pic::launch_fem_matvec(g, it == 1, pcg_nbr(c, c->pcg_r), pcg_nbr(c, pold), pnew, c->pcg_q, sc,
+                                       c->partials, c->stream);      // p = r + beta p, q = A p, sc[5]
+            }
             PIC_LAUNCHED(c, "fem_matvec");
             PIC_TRY(pcg_allreduce(c, sc + 5, 1));
             pic::launch_fem_update(g, c->pcg_x, pnew, c->pcg_r, c->pcg_q, sc, c->partials, c->stream);
