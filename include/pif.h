@@ -1,0 +1,87 @@
+/*
+ * pif.h -- C ABI of the Particle-in-Fourier field solve and its NUFFTs
+ * (arxiv 2605.05469 section "Particle-in-Fourier (PIF)", and Appendix A,
+ * P:423-467).  Exported by libpic.so next to pic.h.
+ * "P:n" = PAPER.md line n, "S:n" = SPEC.md line n, "D#k" = DESIGN.md reading k.
+ *
+ * Conventions (as pic.h: PIC_OK or a negative pic_status, no exceptions, no prints):
+ *  - Modes: K_N = (2 pi / L) [-N/2, N/2 - 1]^3, N even, 8 <= N <= 1024.  A mode
+ *    array is N^3 complex values (interleaved re, im doubles) indexed
+ *    [(nz + N/2) N + (ny + N/2)] N + (nx + N/2) (n ascending).
+ *  - Positions: device SoA x[3][np] doubles (x, y, z), each in [0, L).  Weights f[np],
+ *    charges q[np]: device doubles.  Outputs are device buffers owned by the caller.
+ *  - Accuracy eps (1e-4): window of w = ceil(log10(1/eps)) + 2 fine-grid points
+ *    per dimension, the "exponential of semicircle" exp(beta (sqrt(1 - z^2) - 1)),
+ *    beta = 2.30 w, on the sigma = 2 oversampled grid M = 2N (D#34).
+ *  - Device memory: the library allocates none; the caller owns one workspace of
+ *    pic_pif_workspace_bytes() bytes (fine grid M^3 complex, two N^3 complex spectra, the
+ *    FFT's scratch) and the stream; both must outlive the plan.
+ *  - The uniform FFT on the fine grid is cuFFT (Z2Z, work area inside the workspace);
+ *    spreading, interpolation, mode selection, deconvolution and the Poisson step are
+ *    this library's kernels.
+ *  - A CUDA/cuFFT failure poisons the plan: later calls return PIC_EPOISONED.
+ */
+#ifndef PIC_PIF_H
+#define PIC_PIF_H
+#include "pic.h"
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct pic_pif pic_pif;
+
+/* Workspace bytes for modes N, domain length L and accuracy eps (creates and destroys a
+ * cuFFT plan to learn its scratch size: needs a CUDA device).  PIC_EINVAL: N odd or out
+ * of [8, 1024], L <= 0, eps outside [1e-14, 1). */
+pic_status pic_pif_workspace_bytes(int32_t n, double length, double eps, size_t *bytes);
+
+/* Create a plan on the current device over `workspace` (>= pic_pif_workspace_bytes) and
+ * `stream` (cudaStream_t as void*; NULL = legacy default).  Computes the deconvolution
+ * table 1 / psi^(n) on the device.  PIC_ENOMEM: workspace too small. */
+pic_status pic_pif_create(int32_t n, double length, double eps, void *workspace, size_t bytes,
+                          void *stream, pic_pif **out);
+
+/* Type-1 NUFFT, Eq. (p2f) / (type1nufft): fhat(k) = sum_j f_j e^{-i k.x_j}
+ * for k in K_N, computed as D chi F C f.  fhat: device [N^3][2] doubles.  Asynchronous. */
+pic_status pic_nufft_type1(pic_pif *p, int64_t np, const double *x, const double *f, double *fhat);
+
+/* Type-2 NUFFT, Eq. (f2p) / (type2nufft): out_j = sum_k fhat(k) e^{+i k.x_j},
+ * computed as C^T F^-1 chi^T D fhat.  out: device [np][2] doubles.  Asynchronous. */
+pic_status pic_nufft_type2(pic_pif *p, int64_t np, const double *x, const double *fhat, double *out);
+
+/* PIF field solve: rho^ = type-1 of the charges q; phi^ = rho^ / |k|^2 (D#8, k = 0
+ * removed, D#3); E^ = -i k phi^ with the unpaired -N/2 planes dropped (D#36);
+ * E(x_j) = L^-3 type-2(E^)(x_j) (D#35).  E: device [3][np] doubles.  energy (host, 3
+ * doubles, nullable): W_d = 1/(2 L^3) sum_k |E^_d|^2 (D#37); if non-null the call
+ * synchronises the stream.  PIC_ENONFINITE if an energy is NaN/Inf. */
+pic_status pic_pif_solve(pic_pif *p, int64_t np, const double *x, const double *q, double *E,
+                         double *energy);
+
+/* Per-stage device time (CUDA events on the plan's stream) accumulated over the calls since
+ * timing was enabled, ms[PIC_PIF_NSTAGES]; launches[PIC_PIF_NSTAGES] nullable.  Enabling
+ * timing makes every call synchronise at its end. */
+enum {
+    PIC_PIF_SPREAD = 0, /* C: clear + spread the weights onto the fine grid          */
+    PIC_PIF_FFT,        /* F / F^-1 on the M^3 fine grid (cuFFT)                      */
+    PIC_PIF_MODES,      /* chi, D, Poisson, -i k, energy partials (type 1 side)       */
+    PIC_PIF_FILL,       /* chi^T D: the fine grid from the spectrum (type 2 side)     */
+    PIC_PIF_INTERP,     /* C^T: the window sums at the particles                      */
+    PIC_PIF_NSTAGES
+};
+pic_status pic_pif_set_timing(pic_pif *p, int32_t enable);
+pic_status pic_pif_get_timings(pic_pif *p, double *ms, int64_t *launches);
+
+/* Window width w of the plan (fine-grid points per dimension) and fine size M. */
+pic_status pic_pif_window(pic_pif *p, int32_t *w, int32_t *m);
+
+/* Last error message of the plan (or of the last failed create, p = NULL). */
+const char *pic_pif_last_error(const pic_pif *p);
+
+/* Free the host-side plan (the caller frees the workspace). */
+void pic_pif_free(pic_pif *p);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PIC_PIF_H */

@@ -208,3 +208,13 @@ def pif_solve(x: np.ndarray, q: np.ndarray, N: int, L: float, eps: float = 1e-4,
         v = nudft2(Eh[d], x, L) if exact else nufft2(Eh[d], x, L, eps)
         E[d] = v.real / L ** 3
     return E, pif_energy(Eh, L), Eh
+
+
+def nudft1_modes(x: np.ndarray, f: np.ndarray, L: float, modes) -> np.ndarray:
+    """Eq. (p2f) at a list of integer modes (n_x, n_y, n_z) only: sum_j f_j e^{-i k . x_j}
+    (the sampled full-size check)."""
+    out = []
+    for n in modes:
+        k = 2 * np.pi / L * np.asarray(n, dtype=np.float64)
+        out.append(np.sum(f * np.exp(-1j * (k[0] * x[0] + k[1] * x[1] + k[2] * x[2]))))
+    return np.array(out)

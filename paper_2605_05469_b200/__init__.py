@@ -5,6 +5,8 @@ include/pic.h; ``_binding`` is its thin ctypes binding.
 """
 from ._binding import (  # noqa: F401
     PicError,
+    PifSolver,
+    PIF_STAGES,
     Simulation,
     STAGES,
     default_params,

@@ -91,7 +91,20 @@ SYMBOLS = {
     "pic_stage_name": (C.c_char_p, [C.c_int32]),
     "pic_launches_per_step": (C.c_int, [_vp, _i64p]),
     "pic_pcg_stats": (C.c_int, [_vp, C.POINTER(C.c_int32), _i64p, _i64p, _dp]),
+    # include/pif.h
+    "pic_pif_workspace_bytes": (C.c_int, [C.c_int32, C.c_double, C.c_double, C.POINTER(C.c_size_t)]),
+    "pic_pif_create": (C.c_int, [C.c_int32, C.c_double, C.c_double, _vp, C.c_size_t, _vp, C.POINTER(_vp)]),
+    "pic_nufft_type1": (C.c_int, [_vp, C.c_int64, _vp, _vp, _vp]),
+    "pic_nufft_type2": (C.c_int, [_vp, C.c_int64, _vp, _vp, _vp]),
+    "pic_pif_solve": (C.c_int, [_vp, C.c_int64, _vp, _vp, _vp, _dp]),
+    "pic_pif_set_timing": (C.c_int, [_vp, C.c_int32]),
+    "pic_pif_get_timings": (C.c_int, [_vp, _dp, _i64p]),
+    "pic_pif_window": (C.c_int, [_vp, C.POINTER(C.c_int32), C.POINTER(C.c_int32)]),
+    "pic_pif_last_error": (C.c_char_p, [_vp]),
+    "pic_pif_free": (None, [_vp]),
 }
+
+PIF_STAGES = ["spread", "fft", "modes", "fill", "interp"]
 
 _lib = None
 
@@ -307,3 +320,90 @@ class Simulation:
             self.close()
         except Exception:
             pass
+
+
+def _check_pif(st: int, plan=None):
+    if st != PIC_OK:
+        msg = lib().pic_pif_last_error(plan)
+        raise PicError(st, msg.decode() if msg else "")
+
+
+class PifSolver:
+    """Particle-in-Fourier field solve and the type-1 / type-2 NUFFTs (include/pif.h; P:197-221,
+    P:423-467) on the current CUDA device.  Arguments are torch float64 CUDA tensors:
+    positions x of shape (3, np), weights / charges (np,), spectra complex128 (N, N, N)
+    indexed [nz + N/2, ny + N/2, nx + N/2].  The workspace is a torch uint8 tensor owned
+    here; the stream is torch's current stream at construction."""
+
+    def __init__(self, n: int, length: float, eps: float = 1e-4, device=None):
+        import torch
+
+        self.n, self.L, self.eps = n, float(length), float(eps)
+        self.device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+        b = C.c_size_t()
+        with torch.cuda.device(self.device):
+            _check_pif(lib().pic_pif_workspace_bytes(n, self.L, self.eps, C.byref(b)))
+            self.workspace = torch.empty(b.value, dtype=torch.uint8, device=self.device)
+            self.stream = torch.cuda.current_stream(self.device)
+        plan = C.c_void_p()
+        _check_pif(lib().pic_pif_create(n, self.L, self.eps, C.c_void_p(self.workspace.data_ptr()), b.value,
+                                        C.c_void_p(self.stream.cuda_stream), C.byref(plan)))
+        self.plan = plan
+
+    def __del__(self):
+        if getattr(self, "plan", None):
+            lib().pic_pif_free(self.plan)
+            self.plan = None
+
+    def _pos(self, x):
+        import torch
+
+        assert x.dtype == torch.float64 and x.is_cuda and x.dim() == 2 and x.shape[0] == 3 and x.is_contiguous()
+        return x.shape[1]
+
+    def window(self):
+        w, m = C.c_int32(), C.c_int32()
+        _check_pif(lib().pic_pif_window(self.plan, C.byref(w), C.byref(m)), self.plan)
+        return w.value, m.value
+
+    def type1(self, x, f):
+        import torch
+
+        npart = self._pos(x)
+        assert f.dtype == torch.float64 and f.is_contiguous() and f.numel() == npart
+        out = torch.empty((self.n, self.n, self.n), dtype=torch.complex128, device=x.device)
+        _check_pif(lib().pic_nufft_type1(self.plan, npart, C.c_void_p(x.data_ptr()), C.c_void_p(f.data_ptr()),
+                                         C.c_void_p(out.data_ptr())), self.plan)
+        return out
+
+    def type2(self, fhat, x):
+        import torch
+
+        npart = self._pos(x)
+        assert fhat.dtype == torch.complex128 and fhat.is_contiguous() and fhat.shape == (self.n,) * 3
+        out = torch.empty(npart, dtype=torch.complex128, device=x.device)
+        _check_pif(lib().pic_nufft_type2(self.plan, npart, C.c_void_p(x.data_ptr()), C.c_void_p(fhat.data_ptr()),
+                                         C.c_void_p(out.data_ptr())), self.plan)
+        return out
+
+    def solve(self, x, q, E=None, energy: bool = True):
+        """E at the particles (3, np) and, if ``energy``, W = (W_x, W_y, W_z) (synchronises)."""
+        import torch
+
+        npart = self._pos(x)
+        assert q.dtype == torch.float64 and q.is_contiguous() and q.numel() == npart
+        if E is None:
+            E = torch.empty((3, npart), dtype=torch.float64, device=x.device)
+        W = np.zeros(3)
+        _check_pif(lib().pic_pif_solve(self.plan, npart, C.c_void_p(x.data_ptr()), C.c_void_p(q.data_ptr()),
+                                       C.c_void_p(E.data_ptr()), _d(W) if energy else None), self.plan)
+        return E, (W if energy else None)
+
+    def set_timing(self, enable: bool = True):
+        _check_pif(lib().pic_pif_set_timing(self.plan, int(enable)), self.plan)
+
+    def timings(self):
+        ms = np.zeros(len(PIF_STAGES))
+        la = np.zeros(len(PIF_STAGES), dtype=np.int64)
+        _check_pif(lib().pic_pif_get_timings(self.plan, _d(ms), la.ctypes.data_as(_i64p)), self.plan)
+        return {k: (float(ms[i]), int(la[i])) for i, k in enumerate(PIF_STAGES)}

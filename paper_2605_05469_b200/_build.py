@@ -9,6 +9,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(_HERE, "csrc")
 LIB = os.path.join(_HERE, "libpic.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
+CUDA_LIB = os.path.join(os.path.dirname(os.path.dirname(NVCC)), "lib64")   # cuFFT (PIF fine-grid FFT)
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
@@ -32,7 +33,7 @@ def sources():
 
 def headers():
     return sorted(glob.glob(os.path.join(CSRC, "*.cuh")) + glob.glob(os.path.join(CSRC, "*.h"))
-                  + [os.path.join(_HERE, "..", "include", "pic.h")])
+                  + glob.glob(os.path.join(_HERE, "..", "include", "*.h")))
 
 
 def build_lib(force: bool = False, verbose: bool = False) -> str:
@@ -44,7 +45,7 @@ def build_lib(force: bool = False, verbose: bool = False) -> str:
     inc, libdir = nccl_dirs()
     extra = os.environ.get("PIC_NVCC_EXTRA", "").split()   # tuning experiments, e.g. -DPIC_X=1
     cmd = [NVCC, *NVCC_FLAGS, *extra, "-I" + inc, "-o", LIB, *srcs, "-L" + libdir, "-l:libnccl.so.2",
-           "-Xlinker", "-rpath," + libdir]
+           "-Xlinker", "-rpath," + libdir, "-L" + CUDA_LIB, "-lcufft", "-Xlinker", "-rpath," + CUDA_LIB]
     if verbose:
         print(" ".join(cmd))
     subprocess.check_call(cmd)

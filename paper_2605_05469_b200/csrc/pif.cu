@@ -1,0 +1,613 @@
+// pif.cu -- Particle-in-Fourier field solve and the type-1 / type-2 NUFFTs on the GPU
+// (Appendix A; include/pif.h).
+//
+// Pipeline (fine grid M = 2N per dimension, complex [lz][ly][lx]):
+//   type 1  (D chi F C):  k_spread<W> (one thread per particle, w^3 RED.ADD.F64 on the real
+//           parts) -> cuFFT Z2Z forward -> k_select (chi, D) or k_pif_modes (chi, D, Poisson,
+//           -i k, energy partials).
+//   type 2  (C^T F^-1 chi^T D):  k_fill (chi^T D: the selected modes scaled, zero elsewhere)
+//           -> cuFFT Z2Z inverse -> k_interp<W> (one thread per particle, w^3 loads).
+// The PIF solve packs E^_x + i E^_y into one type-2 transform (each is the transform of a
+// Hermitian spectrum, hence real) and E^_z into a second.
+#include <cuda_runtime.h>
+#include <cufft.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <new>
+
+#include "../../include/pif.h"
+
+namespace {
+
+constexpr int kThreads = 256;
+constexpr int kModeBlocks = 1184;      // 148 SMs x 8: the mode kernels' grid (energy partials)
+constexpr int kNq = 64;                // Gauss-Legendre nodes for psi^
+thread_local char g_err[256] = "";
+
+__device__ __forceinline__ double psi_es(double z, double beta) {
+    // exp(beta (sqrt(1 - z^2) - 1)), |z| <= 1 (D#34); separately rounded ops.
+    const double t = __dsub_rn(1.0, __dmul_rn(z, z));
+    if (t < 0.0) return 0.0;
+    return exp(__dmul_rn(beta, __dsub_rn(sqrt(t), 1.0)));
+}
+
+// Fine-grid start index and the W window values of one coordinate (u = x M / L).
+template <int W>
+__device__ __forceinline__ int window_1d(double x, double inv_hf, double beta, int M, double* wv) {
+    const double u = __dmul_rn(x, inv_hf);
+    const double l0d = ceil(__dsub_rn(u, 0.5 * W));
+    const int l0 = (int)l0d;
+#pragma unroll
+    for (int k = 0; k < W; ++k) wv[k] = psi_es(__ddiv_rn(__dsub_rn((double)(l0 + k), u), 0.5 * W), beta);
+    return l0 < 0 ? l0 + M : l0;
+}
+
+__device__ __forceinline__ int wrap_idx(int l, int M) { return l >= M ? l - M : l; }
+
+// C: b_l += f_j psi_z psi_y psi_x, real weights into the real parts.
+template <int W>
+__global__ void __launch_bounds__(kThreads) k_spread(int64_t np, const double* __restrict__ X,
+                                                     const double* __restrict__ f, double* __restrict__ G,
+                                                     int M, double inv_hf, double beta) {
+    const int64_t j = (int64_t)blockIdx.x * kThreads + threadIdx.x;
+    if (j >= np) return;
+    double wx[W], wy[W], wz[W];
+    const int lx = window_1d<W>(X[j], inv_hf, beta, M, wx);
+    const int ly = window_1d<W>(X[np + j], inv_hf, beta, M, wy);
+    const int lz = window_1d<W>(X[2 * np + j], inv_hf, beta, M, wz);
+    const double fj = f[j];
+#pragma unroll 1
+    for (int c = 0; c < W; ++c) {
+        const int iz = wrap_idx(lz + c, M);
+        const double fz = __dmul_rn(fj, wz[c]);
+#pragma unroll 1
+        for (int b = 0; b < W; ++b) {
+            const int iy = wrap_idx(ly + b, M);
+            const double fzy = __dmul_rn(fz, wy[b]);
+            double* row = G + 2 * (((int64_t)iz * M + iy) * M);
+#pragma unroll
+            for (int a = 0; a < W; ++a) atomicAdd(row + 2 * wrap_idx(lx + a, M), __dmul_rn(fzy, wx[a]));
+        }
+    }
+}
+
+// C^T: out_j = sum_l g_l psi_z psi_y psi_x.  o_re / o_im nullable, scaled.
+template <int W>
+__global__ void __launch_bounds__(kThreads) k_interp(int64_t np, const double* __restrict__ X,
+                                                     const double2* __restrict__ G, int M, double inv_hf,
+                                                     double beta, double* __restrict__ o_re,
+                                                     double* __restrict__ o_im, int64_t ostride,
+                                                     double scale) {
+    const int64_t j = (int64_t)blockIdx.x * kThreads + threadIdx.x;
+    if (j >= np) return;
+    double wx[W], wy[W], wz[W];
+    const int lx = window_1d<W>(X[j], inv_hf, beta, M, wx);
+    const int ly = window_1d<W>(X[np + j], inv_hf, beta, M, wy);
+    const int lz = window_1d<W>(X[2 * np + j], inv_hf, beta, M, wz);
+    double sr = 0.0, si = 0.0;
+#pragma unroll 1
+    for (int c = 0; c < W; ++c) {
+        const int iz = wrap_idx(lz + c, M);
+        double yr = 0.0, yi = 0.0;
+#pragma unroll 1
+        for (int b = 0; b < W; ++b) {
+            const int iy = wrap_idx(ly + b, M);
+            const double2* row = G + ((int64_t)iz * M + iy) * M;
+            double xr = 0.0, xi = 0.0;
+#pragma unroll
+            for (int a = 0; a < W; ++a) {
+                const double2 v = __ldg(row + wrap_idx(lx + a, M));
+                xr = fma(v.x, wx[a], xr);
+                xi = fma(v.y, wx[a], xi);
+            }
+            yr = fma(xr, wy[b], yr);
+            yi = fma(xi, wy[b], yi);
+        }
+        sr = fma(yr, wz[c], sr);
+        si = fma(yi, wz[c], si);
+    }
+    if (o_re) o_re[j * ostride] = sr * scale;
+    if (o_im) o_im[j * ostride] = si * scale;
+}
+
+// 1 / psi^(n), n in [-N/2, N/2): Gauss-Legendre (kNq nodes by Newton on P_kNq) of
+// (w/2) int_{-1}^{1} psi(z) cos(pi n w z / M) dz.
+__global__ void k_psihat(int N, int M, int W, double beta, double* __restrict__ dinv) {
+    __shared__ double zs[kNq], as[kNq];
+    const int t = threadIdx.x;
+    if (t < kNq) {
+        double z = cos(M_PI * (t + 0.75) / (kNq + 0.5));
+        double dp = 1.0;
+        for (int it = 0; it < 100; ++it) {
+            double p0 = 1.0, p1 = z;
+            for (int k = 2; k <= kNq; ++k) {
+                const double p2 = ((2.0 * k - 1.0) * z * p1 - (k - 1.0) * p0) / k;
+                p0 = p1;
+                p1 = p2;
+            }
+            dp = kNq * (z * p1 - p0) / (z * z - 1.0);
+            const double dz = p1 / dp;
+            z -= dz;
+            if (fabs(dz) < 1e-16) break;
+        }
+        double p0 = 1.0, p1 = z;
+        for (int k = 2; k <= kNq; ++k) {
+            const double p2 = ((2.0 * k - 1.0) * z * p1 - (k - 1.0) * p0) / k;
+            p0 = p1;
+            p1 = p2;
+        }
+        dp = kNq * (z * p1 - p0) / (z * z - 1.0);
+        zs[t] = z;
+        as[t] = 2.0 / ((1.0 - z * z) * dp * dp);
+    }
+    __syncthreads();
+    for (int i = t; i < N; i += blockDim.x) {
+        const double n = (double)(i - N / 2);
+        double s = 0.0;
+        for (int k = 0; k < kNq; ++k) s += as[k] * psi_es(zs[k], beta) * cos(M_PI * n * zs[k] * W / M);
+        dinv[i] = 1.0 / (0.5 * W * s);
+    }
+}
+
+struct ModeIx {
+    int nx, ny, nz;      // n + N/2 in [0, N)
+    int64_t fine;        // index of n mod M on the fine grid
+};
+__device__ __forceinline__ ModeIx mode_ix(int64_t t, int N, int M) {
+    ModeIx m;
+    m.nx = (int)(t % N);
+    const int64_t r = t / N;
+    m.ny = (int)(r % N);
+    m.nz = (int)(r / N);
+    const int h = N / 2;
+    const int cx = m.nx - h < 0 ? m.nx - h + M : m.nx - h;
+    const int cy = m.ny - h < 0 ? m.ny - h + M : m.ny - h;
+    const int cz = m.nz - h < 0 ? m.nz - h + M : m.nz - h;
+    m.fine = ((int64_t)cz * M + cy) * M + cx;
+    return m;
+}
+
+// chi, D (type 1): fhat[t] = B[n mod M] / (psi^_z psi^_y psi^_x).
+__global__ void __launch_bounds__(kThreads) k_select(int N, int M, const double2* __restrict__ B,
+                                                     const double* __restrict__ dinv, double2* __restrict__ fhat) {
+    const int64_t nm = (int64_t)N * N * N;
+    for (int64_t t = (int64_t)blockIdx.x * kThreads + threadIdx.x; t < nm; t += (int64_t)gridDim.x * kThreads) {
+        const ModeIx m = mode_ix(t, N, M);
+        const double d = dinv[m.nz] * dinv[m.ny] * dinv[m.nx];
+        const double2 v = B[m.fine];
+        fhat[t] = make_double2(v.x * d, v.y * d);
+    }
+}
+
+// chi, D, Poisson, gradient: rho^ = B D; phi^ = rho^/|k|^2; E^_d = -i k_d phi^,
+// zero at k = 0 (D#3) and on the unpaired -N/2 planes (D#36).  A = E^_x + i E^_y, Bz = E^_z;
+// block partials of |E^_d|^2 (fixed order).
+__global__ void __launch_bounds__(kThreads) k_pif_modes(int N, int M, double kunit, const double2* __restrict__ B,
+                                                        const double* __restrict__ dinv, double2* __restrict__ A,
+                                                        double2* __restrict__ Bz, double* __restrict__ partials) {
+    const int64_t nm = (int64_t)N * N * N;
+    double e[3] = {0.0, 0.0, 0.0};
+    for (int64_t t = (int64_t)blockIdx.x * kThreads + threadIdx.x; t < nm; t += (int64_t)gridDim.x * kThreads) {
+        const ModeIx m = mode_ix(t, N, M);
+        const int h = N / 2;
+        double2 ex = make_double2(0.0, 0.0), ey = ex, ez = ex;
+        const double kx = kunit * (m.nx - h), ky = kunit * (m.ny - h), kz = kunit * (m.nz - h);
+        const double k2 = kx * kx + ky * ky + kz * kz;
+        if (m.nx > 0 && m.ny > 0 && m.nz > 0 && k2 != 0.0) {
+            const double d = dinv[m.nz] * dinv[m.ny] * dinv[m.nx];
+            const double2 v = B[m.fine];
+            const double pr = v.x * d / k2, pi = v.y * d / k2;
+            ex = make_double2(kx * pi, -kx * pr);      // -i k phi
+            ey = make_double2(ky * pi, -ky * pr);
+            ez = make_double2(kz * pi, -kz * pr);
+            e[0] += ex.x * ex.x + ex.y * ex.y;
+            e[1] += ey.x * ey.x + ey.y * ey.y;
+            e[2] += ez.x * ez.x + ez.y * ez.y;
+        }
+        A[t] = make_double2(ex.x - ey.y, ex.y + ey.x);
+        Bz[t] = ez;
+    }
+    __shared__ double red[3][kThreads];
+    for (int d = 0; d < 3; ++d) red[d][threadIdx.x] = e[d];
+    __syncthreads();
+    for (int s = kThreads / 2; s > 0; s >>= 1) {
+        if (threadIdx.x < s)
+            for (int d = 0; d < 3; ++d) red[d][threadIdx.x] += red[d][threadIdx.x + s];
+        __syncthreads();
+    }
+    if (threadIdx.x < 3) partials[blockIdx.x * 3 + threadIdx.x] = red[threadIdx.x][0];
+}
+
+__global__ void k_energy(int nblk, const double* __restrict__ partials, double scale, double* __restrict__ out) {
+    if (threadIdx.x < 3) {
+        double s = 0.0;
+        for (int b = 0; b < nblk; ++b) s += partials[b * 3 + threadIdx.x];
+        out[threadIdx.x] = s * scale;
+    }
+}
+
+// chi^T D (type 2): G[l] = S[mode(l)] D(mode) where l = n mod M for some n in K_N, else 0.
+__global__ void __launch_bounds__(kThreads) k_fill(int N, int M, const double2* __restrict__ S,
+                                                   const double* __restrict__ dinv, double2* __restrict__ G) {
+    const int64_t nf = (int64_t)M * M * M;
+    const int h = N / 2;
+    for (int64_t l = (int64_t)blockIdx.x * kThreads + threadIdx.x; l < nf; l += (int64_t)gridDim.x * kThreads) {
+        const int lx = (int)(l % M);
+        const int64_t r = l / M;
+        const int ly = (int)(r % M);
+        const int lz = (int)(r / M);
+        // n = l for l < N/2, l - M for l >= M - N/2; index n + N/2.
+        const int ix = lx < h ? lx + h : (lx >= M - h ? lx - M + h : -1);
+        const int iy = ly < h ? ly + h : (ly >= M - h ? ly - M + h : -1);
+        const int iz = lz < h ? lz + h : (lz >= M - h ? lz - M + h : -1);
+        double2 v = make_double2(0.0, 0.0);
+        if ((ix | iy | iz) >= 0) {
+            const double d = dinv[iz] * dinv[iy] * dinv[ix];
+            const double2 s = S[((int64_t)iz * N + iy) * N + ix];
+            v = make_double2(s.x * d, s.y * d);
+        }
+        G[l] = v;
+    }
+}
+
+inline size_t align256(size_t b) { return (b + 255) & ~(size_t)255; }
+
+}  // namespace
+
+struct pic_pif {
+    int n, M, w;
+    double L, eps, beta, inv_hf;
+    cufftHandle plan;
+    cudaStream_t stream;
+    double2* G;          // fine grid M^3
+    double2* A;          // N^3 spectrum (E^_x + i E^_y)
+    double2* Bz;         // N^3 spectrum (E^_z)
+    double* dinv;        // N: 1 / psi^
+    double* partials;    // kModeBlocks x 3
+    double* energy;      // 3
+    void* fft_work;
+    bool poisoned;
+    bool timing;
+    cudaEvent_t ev[2 * PIC_PIF_NSTAGES * 4];
+    int nev;
+    double ms[PIC_PIF_NSTAGES];
+    int64_t launches[PIC_PIF_NSTAGES];
+    int ev_stage[PIC_PIF_NSTAGES * 4];
+    char err[256];
+};
+
+namespace {
+
+int width_of(double eps) { return (int)std::ceil(std::log10(1.0 / eps)) + 2; }
+
+bool valid(int32_t n, double L, double eps) {
+    return n >= 8 && n <= 1024 && n % 2 == 0 && L > 0 && eps >= 1e-14 && eps < 1.0;
+}
+
+pic_status make_plan(int M, cufftHandle* plan, size_t* work) {
+    if (cufftCreate(plan) != CUFFT_SUCCESS) return PIC_ECUDA;
+    if (cufftSetAutoAllocation(*plan, 0) != CUFFT_SUCCESS ||
+        cufftMakePlan3d(*plan, M, M, M, CUFFT_Z2Z, work) != CUFFT_SUCCESS) {
+        cufftDestroy(*plan);
+        return PIC_ECUDA;
+    }
+    return PIC_OK;
+}
+
+struct Layout {
+    size_t G, A, Bz, dinv, partials, energy, work, total;
+};
+Layout layout(int n, size_t fft_work) {
+    const size_t M = 2 * (size_t)n;
+    Layout o;
+    size_t off = 0;
+    o.G = off;        off += align256(M * M * M * sizeof(double2));
+    o.A = off;        off += align256((size_t)n * n * n * sizeof(double2));
+    o.Bz = off;       off += align256((size_t)n * n * n * sizeof(double2));
+    o.dinv = off;     off += align256((size_t)n * sizeof(double));
+    o.partials = off; off += align256((size_t)kModeBlocks * 3 * sizeof(double));
+    o.energy = off;   off += align256(3 * sizeof(double));
+    o.work = off;     off += align256(fft_work);
+    o.total = off;
+    return o;
+}
+
+#define PIF_CUDA(p, call)                                                                      \
+    do {                                                                                       \
+        cudaError_t e_ = (call);                                                               \
+        if (e_ != cudaSuccess) {                                                               \
+            snprintf((p)->err, sizeof((p)->err), "%s: %s", #call, cudaGetErrorString(e_));     \
+            (p)->poisoned = true;                                                              \
+            return PIC_ECUDA;                                                                  \
+        }                                                                                      \
+    } while (0)
+#define PIF_FFT(p, call)                                                                       \
+    do {                                                                                       \
+        cufftResult r_ = (call);                                                               \
+        if (r_ != CUFFT_SUCCESS) {                                                             \
+            snprintf((p)->err, sizeof((p)->err), "%s: cufft status %d", #call, (int)r_);       \
+            (p)->poisoned = true;                                                              \
+            return PIC_ECUDA;                                                                  \
+        }                                                                                      \
+    } while (0)
+#define PIF_LAUNCHED(p)                                                                        \
+    do {                                                                                       \
+        cudaError_t e_ = cudaGetLastError();                                                   \
+        if (e_ != cudaSuccess) {                                                               \
+            snprintf((p)->err, sizeof((p)->err), "launch: %s", cudaGetErrorString(e_));        \
+            (p)->poisoned = true;                                                              \
+            return PIC_ECUDA;                                                                  \
+        }                                                                                      \
+    } while (0)
+
+struct Stage {
+    pic_pif* p;
+    int s;
+    Stage(pic_pif* p_, int s_) : p(p_), s(s_) {
+        p->launches[s] += 1;
+        if (p->timing && p->nev + 2 <= (int)(sizeof(p->ev) / sizeof(p->ev[0]))) {
+            p->ev_stage[p->nev / 2] = s;
+            cudaEventRecord(p->ev[p->nev], p->stream);
+        }
+    }
+    ~Stage() {
+        if (p->timing && p->nev + 2 <= (int)(sizeof(p->ev) / sizeof(p->ev[0]))) {
+            cudaEventRecord(p->ev[p->nev + 1], p->stream);
+            p->nev += 2;
+        }
+    }
+};
+
+pic_status flush_timing(pic_pif* p) {
+    if (!p->timing) return PIC_OK;
+    PIF_CUDA(p, cudaStreamSynchronize(p->stream));
+    for (int i = 0; i < p->nev; i += 2) {
+        float t = 0.f;
+        PIF_CUDA(p, cudaEventElapsedTime(&t, p->ev[i], p->ev[i + 1]));
+        p->ms[p->ev_stage[i / 2]] += t;
+    }
+    p->nev = 0;
+    return PIC_OK;
+}
+
+unsigned particle_grid(int64_t np) { return (unsigned)((np + kThreads - 1) / kThreads); }
+unsigned stream_grid(int64_t n) {
+    return (unsigned)std::max<int64_t>(1, std::min<int64_t>((n + kThreads - 1) / kThreads, 148 * 16));
+}
+
+template <int W>
+void spread_w(pic_pif* p, int64_t np, const double* X, const double* f) {
+    k_spread<W><<<particle_grid(np), kThreads, 0, p->stream>>>(np, X, f, (double*)p->G, p->M, p->inv_hf, p->beta);
+}
+template <int W>
+void interp_w(pic_pif* p, int64_t np, const double* X, double* ore, double* oim, int64_t os, double sc) {
+    k_interp<W><<<particle_grid(np), kThreads, 0, p->stream>>>(np, X, p->G, p->M, p->inv_hf, p->beta, ore, oim,
+                                                                 os, sc);
+}
+
+#define PIF_W_SWITCH(w, F, ...)                      \
+    switch (w) {                                     \
+        case 3: F<3>(__VA_ARGS__); break;            \
+        case 4: F<4>(__VA_ARGS__); break;            \
+        case 5: F<5>(__VA_ARGS__); break;            \
+        case 6: F<6>(__VA_ARGS__); break;            \
+        case 7: F<7>(__VA_ARGS__); break;            \
+        case 8: F<8>(__VA_ARGS__); break;            \
+        case 9: F<9>(__VA_ARGS__); break;            \
+        case 10: F<10>(__VA_ARGS__); break;          \
+        case 11: F<11>(__VA_ARGS__); break;          \
+        case 12: F<12>(__VA_ARGS__); break;          \
+        case 13: F<13>(__VA_ARGS__); break;          \
+        case 14: F<14>(__VA_ARGS__); break;          \
+        case 15: F<15>(__VA_ARGS__); break;          \
+        default: F<16>(__VA_ARGS__); break;          \
+    }
+
+pic_status spread(pic_pif* p, int64_t np, const double* X, const double* f) {
+    Stage t(p, PIC_PIF_SPREAD);
+    const size_t M = p->M;
+    PIF_CUDA(p, cudaMemsetAsync(p->G, 0, M * M * M * sizeof(double2), p->stream));
+    if (np > 0) PIF_W_SWITCH(p->w, spread_w, p, np, X, f);
+    PIF_LAUNCHED(p);
+    return PIC_OK;
+}
+
+pic_status fft(pic_pif* p, int dir) {
+    Stage t(p, PIC_PIF_FFT);
+    PIF_FFT(p, cufftExecZ2Z(p->plan, (cufftDoubleComplex*)p->G, (cufftDoubleComplex*)p->G, dir));
+    return PIC_OK;
+}
+
+pic_status fill(pic_pif* p, const double2* S) {
+    Stage t(p, PIC_PIF_FILL);
+    const int64_t nf = (int64_t)p->M * p->M * p->M;
+    k_fill<<<stream_grid(nf), kThreads, 0, p->stream>>>(p->n, p->M, S, p->dinv, p->G);
+    PIF_LAUNCHED(p);
+    return PIC_OK;
+}
+
+pic_status interp(pic_pif* p, int64_t np, const double* X, double* ore, double* oim, int64_t os, double sc) {
+    Stage t(p, PIC_PIF_INTERP);
+    if (np > 0) PIF_W_SWITCH(p->w, interp_w, p, np, X, ore, oim, os, sc);
+    PIF_LAUNCHED(p);
+    return PIC_OK;
+}
+
+#define PIF_CHECK(p)                             \
+    do {                                         \
+        if (!(p)) return PIC_EINVAL;             \
+        if ((p)->poisoned) return PIC_EPOISONED; \
+    } while (0)
+
+}  // namespace
+
+extern "C" {
+
+pic_status pic_pif_workspace_bytes(int32_t n, double length, double eps, size_t* bytes) {
+    if (!bytes || !valid(n, length, eps)) {
+        snprintf(g_err, sizeof(g_err), "pic_pif_workspace_bytes: invalid n / length / eps");
+        return PIC_EINVAL;
+    }
+    cufftHandle plan;
+    size_t work = 0;
+    if (make_plan(2 * n, &plan, &work) != PIC_OK) {
+        snprintf(g_err, sizeof(g_err), "cuFFT plan creation failed (M = %d)", 2 * n);
+        return PIC_ECUDA;
+    }
+    cufftDestroy(plan);
+    *bytes = layout(n, work).total;
+    return PIC_OK;
+}
+
+pic_status pic_pif_create(int32_t n, double length, double eps, void* workspace, size_t bytes, void* stream,
+                          pic_pif** out) {
+    if (!out || !workspace || !valid(n, length, eps)) {
+        snprintf(g_err, sizeof(g_err), "pic_pif_create: invalid argument");
+        return PIC_EINVAL;
+    }
+    *out = nullptr;
+    pic_pif* p = new (std::nothrow) pic_pif();
+    if (!p) return PIC_ENOMEM;
+    p->n = n;
+    p->M = 2 * n;
+    p->w = width_of(eps);
+    p->L = length;
+    p->eps = eps;
+    p->beta = 2.30 * p->w;
+    p->inv_hf = (double)p->M / length;
+    p->stream = (cudaStream_t)stream;
+    size_t work = 0;
+    if (make_plan(p->M, &p->plan, &work) != PIC_OK) {
+        snprintf(g_err, sizeof(g_err), "cuFFT plan creation failed (M = %d)", p->M);
+        delete p;
+        return PIC_ECUDA;
+    }
+    const Layout o = layout(n, work);
+    if (bytes < o.total) {
+        snprintf(g_err, sizeof(g_err), "workspace %zu bytes < %zu", bytes, o.total);
+        cufftDestroy(p->plan);
+        delete p;
+        return PIC_ENOMEM;
+    }
+    char* b = (char*)workspace;
+    p->G = (double2*)(b + o.G);
+    p->A = (double2*)(b + o.A);
+    p->Bz = (double2*)(b + o.Bz);
+    p->dinv = (double*)(b + o.dinv);
+    p->partials = (double*)(b + o.partials);
+    p->energy = (double*)(b + o.energy);
+    p->fft_work = b + o.work;
+    if (cufftSetWorkArea(p->plan, p->fft_work) != CUFFT_SUCCESS ||
+        cufftSetStream(p->plan, p->stream) != CUFFT_SUCCESS) {
+        snprintf(g_err, sizeof(g_err), "cuFFT work area / stream");
+        cufftDestroy(p->plan);
+        delete p;
+        return PIC_ECUDA;
+    }
+    for (auto& e : p->ev) cudaEventCreate(&e);
+    k_psihat<<<1, 256, 0, p->stream>>>(n, p->M, p->w, p->beta, p->dinv);
+    if (cudaGetLastError() != cudaSuccess) {
+        snprintf(g_err, sizeof(g_err), "k_psihat launch failed");
+        pic_pif_free(p);
+        return PIC_ECUDA;
+    }
+    *out = p;
+    return PIC_OK;
+}
+
+pic_status pic_nufft_type1(pic_pif* p, int64_t np, const double* x, const double* f, double* fhat) {
+    PIF_CHECK(p);
+    if (np < 0 || (np > 0 && (!x || !f)) || !fhat) return PIC_EINVAL;
+    if (pic_status s = spread(p, np, x, f)) return s;
+    if (pic_status s = fft(p, CUFFT_FORWARD)) return s;
+    {
+        Stage t(p, PIC_PIF_MODES);
+        const int64_t nm = (int64_t)p->n * p->n * p->n;
+        k_select<<<stream_grid(nm), kThreads, 0, p->stream>>>(p->n, p->M, p->G, p->dinv, (double2*)fhat);
+        PIF_LAUNCHED(p);
+    }
+    return flush_timing(p);
+}
+
+pic_status pic_nufft_type2(pic_pif* p, int64_t np, const double* x, const double* fhat, double* out) {
+    PIF_CHECK(p);
+    if (np < 0 || (np > 0 && (!x || !out)) || !fhat) return PIC_EINVAL;
+    if (pic_status s = fill(p, (const double2*)fhat)) return s;
+    if (pic_status s = fft(p, CUFFT_INVERSE)) return s;
+    if (pic_status s = interp(p, np, x, out, out + 1, 2, 1.0)) return s;
+    return flush_timing(p);
+}
+
+pic_status pic_pif_solve(pic_pif* p, int64_t np, const double* x, const double* q, double* E, double* energy) {
+    PIF_CHECK(p);
+    if (np < 0 || (np > 0 && (!x || !q || !E))) return PIC_EINVAL;
+    if (pic_status s = spread(p, np, x, q)) return s;                       // C
+    if (pic_status s = fft(p, CUFFT_FORWARD)) return s;                     // F
+    {
+        Stage t(p, PIC_PIF_MODES);                                          // chi, D, Poisson
+        const double kunit = 2.0 * M_PI / p->L;
+        k_pif_modes<<<kModeBlocks, kThreads, 0, p->stream>>>(p->n, p->M, kunit, p->G, p->dinv, p->A, p->Bz,
+                                                              p->partials);
+        k_energy<<<1, 32, 0, p->stream>>>(kModeBlocks, p->partials, 0.5 / (p->L * p->L * p->L), p->energy);
+        PIF_LAUNCHED(p);
+    }
+    const double sc = 1.0 / (p->L * p->L * p->L);                           // D#35
+    if (pic_status s = fill(p, p->A)) return s;                             // E_x + i E_y
+    if (pic_status s = fft(p, CUFFT_INVERSE)) return s;
+    if (pic_status s = interp(p, np, x, E, E + np, 1, sc)) return s;
+    if (pic_status s = fill(p, p->Bz)) return s;                            // E_z
+    if (pic_status s = fft(p, CUFFT_INVERSE)) return s;
+    if (pic_status s = interp(p, np, x, E + 2 * np, nullptr, 1, sc)) return s;
+    if (energy) {
+        PIF_CUDA(p, cudaMemcpyAsync(energy, p->energy, 3 * sizeof(double), cudaMemcpyDeviceToHost, p->stream));
+        PIF_CUDA(p, cudaStreamSynchronize(p->stream));
+        for (int d = 0; d < 3; ++d)
+            if (!std::isfinite(energy[d])) {
+                snprintf(p->err, sizeof(p->err), "PIF field energy %d is not finite", d);
+                return PIC_ENONFINITE;
+            }
+    }
+    return flush_timing(p);
+}
+
+pic_status pic_pif_set_timing(pic_pif* p, int32_t enable) {
+    PIF_CHECK(p);
+    p->timing = enable != 0;
+    p->nev = 0;
+    for (int s = 0; s < PIC_PIF_NSTAGES; ++s) {
+        p->ms[s] = 0.0;
+        p->launches[s] = 0;
+    }
+    return PIC_OK;
+}
+
+pic_status pic_pif_get_timings(pic_pif* p, double* ms, int64_t* launches) {
+    PIF_CHECK(p);
+    for (int s = 0; s < PIC_PIF_NSTAGES; ++s) {
+        if (ms) ms[s] = p->ms[s];
+        if (launches) launches[s] = p->launches[s];
+    }
+    return PIC_OK;
+}
+
+pic_status pic_pif_window(pic_pif* p, int32_t* w, int32_t* m) {
+    if (!p) return PIC_EINVAL;
+    if (w) *w = p->w;
+    if (m) *m = p->M;
+    return PIC_OK;
+}
+
+const char* pic_pif_last_error(const pic_pif* p) { return p ? p->err : g_err; }
+
+void pic_pif_free(pic_pif* p) {
+    if (!p) return;
+    cufftDestroy(p->plan);
+    for (auto& e : p->ev)
+        if (e) cudaEventDestroy(e);
+    delete p;
+}
+
+}  // extern "C"

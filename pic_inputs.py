@@ -46,3 +46,15 @@ def random_field(n: int, seed: int = 1) -> np.ndarray:
     """A random (3, N, N, N) float64 vector field (e.g. an injected E)."""
     rng = np.random.Generator(np.random.PCG64(seed))
     return rng.standard_normal((3, n, n, n))
+
+
+def random_weights(np_: int, seed: int = 1) -> np.ndarray:
+    """Standard-normal float64 weights (NUFFT type-1 inputs)."""
+    rng = np.random.Generator(np.random.PCG64(seed))
+    return rng.standard_normal(np_)
+
+
+def random_spectrum(n: int, seed: int = 1) -> np.ndarray:
+    """A random complex128 (N, N, N) mode array (NUFFT type-2 inputs)."""
+    rng = np.random.Generator(np.random.PCG64(seed))
+    return rng.standard_normal((n, n, n)) + 1j * rng.standard_normal((n, n, n))

@@ -1,5 +1,5 @@
 """CPU-side checks of the C ABI library: it loads, exports every symbol
-include/pic.h declares, and its host-only entry points (parameter validation,
+include/pic.h and include/pif.h declare, and its host-only entry points (parameter validation,
 workspace sizing) behave as documented.  No compute call needs a GPU here."""
 import os
 import re
@@ -13,7 +13,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
 def _declared_functions():
-    src = open(os.path.join(ROOT, "include", "pic.h")).read()
+    src = "".join(open(os.path.join(ROOT, "include", h)).read() for h in ("pic.h", "pif.h"))
     src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
     return sorted(set(re.findall(r"\b(pic_[a-z_]+)\s*\(", src)))
 
@@ -120,3 +120,17 @@ def test_pcg_defaults_and_validation():
     fft = B.workspace_bytes(B.default_params(n=n))
     pcg = B.workspace_bytes(B.default_params(n=n, solver=B.PIC_SOLVER_PCG))
     assert 6 * 8 * n ** 3 <= pcg - fft <= 6 * 8 * n ** 3 + 8 * 4096
+
+
+def test_pif_parameter_validation_without_gpu():
+    """include/pif.h: invalid N (odd, < 8, > 1024), L <= 0 or eps outside [1e-14, 1) are
+    rejected before any CUDA call."""
+    import ctypes as C
+
+    b = C.c_size_t()
+    for n, L, eps in [(7, 1.0, 1e-4), (4, 1.0, 1e-4), (2048, 1.0, 1e-4), (16, 0.0, 1e-4), (16, 1.0, 1.5),
+                      (16, 1.0, 1e-20)]:
+        assert pkg.lib().pic_pif_workspace_bytes(n, L, eps, C.byref(b)) == B.PIC_EINVAL
+    assert pkg.lib().pic_nufft_type1(None, 1, None, None, None) == B.PIC_EINVAL
+    assert pkg.lib().pic_pif_solve(None, 1, None, None, None, None) == B.PIC_EINVAL
+    assert B.PIF_STAGES == ["spread", "fft", "modes", "fill", "interp"]

@@ -1,0 +1,117 @@
+"""GPU parity of the Particle-in-Fourier solve and its NUFFTs (include/pif.h; P:197-221,
+Appendix A; readings D#34-D#37) against oracle/nufft.py on
+the same seeded inputs.  Both sides use the same window (ES, w = ceil(log10 1/eps) + 2,
+beta = 2.30 w, sigma = 2) and differ only in rounding order (atomic spreading order,
+cuFFT vs numpy FFT, libm ulps), so
+  type 1 vs oracle nufft1 ..................... 1e-11 of sum |f|
+  type 2 vs oracle nufft2 ..................... 1e-11 of sum |f^|
+  PIF E at particles / energies vs oracle ...... 1e-10 of max |E| / relative
+and, at sizes beyond the oracle's, sampled modes against the direct NUDFT sum (within
+eps sum |f|) and the closed-form field and energy of a lattice-sampled cosine density."""
+import numpy as np
+import pytest
+
+from oracle import nufft as U
+from pic_inputs import landau_state, random_spectrum, random_weights
+
+pytestmark = pytest.mark.gpu
+
+L = 4 * np.pi
+
+
+@pytest.fixture(scope="module")
+def torch_dev():
+    import torch
+
+    torch.cuda.set_device(0)
+    return torch
+
+
+def _x(torch, xv):
+    return torch.from_numpy(np.ascontiguousarray(xv[:3])).cuda()
+
+
+@pytest.mark.parametrize("N,np_,eps", [(16, 3000, 1e-4), (12, 777, 1e-4), (8, 500, 1e-6), (16, 0, 1e-4)])
+def test_type1_matches_oracle(torch_dev, N, np_, eps):
+    from paper_2605_05469_b200 import PifSolver
+
+    torch = torch_dev
+    xv = landau_state(4, 1, L=L, np_=max(np_, 1), seed=3)[:, :np_]
+    f = random_weights(np_, seed=4)
+    P = PifSolver(N, L, eps)
+    g = P.type1(_x(torch, xv), torch.from_numpy(f).cuda()).cpu().numpy()
+    if np_ == 0:
+        assert np.all(g == 0)
+        return
+    ref = U.nufft1(xv[:3], f, N, L, eps)
+    assert np.abs(g - ref).max() <= 1e-11 * np.abs(f).sum()
+    assert np.abs(g - U.nudft1(xv[:3], f, N, L)).max() <= eps * np.abs(f).sum()
+
+
+@pytest.mark.parametrize("N,np_", [(16, 400), (10, 123)])
+def test_type2_matches_oracle(torch_dev, N, np_):
+    from paper_2605_05469_b200 import PifSolver
+
+    torch = torch_dev
+    xv = landau_state(4, 1, L=L, np_=np_, seed=5)
+    fh = random_spectrum(N, seed=6)
+    P = PifSolver(N, L, 1e-4)
+    g = P.type2(torch.from_numpy(fh).cuda(), _x(torch, xv)).cpu().numpy()
+    ref = U.nufft2(fh, xv[:3], L, 1e-4)
+    assert np.abs(g - ref).max() <= 1e-11 * np.abs(fh).sum()
+    assert np.abs(g - U.nudft2(fh, xv[:3], L)).max() <= 1e-4 * np.abs(fh).sum()
+
+
+@pytest.mark.parametrize("N,ppc", [(16, 2), (8, 8)])
+def test_pif_solve_matches_oracle(torch_dev, N, ppc):
+    from paper_2605_05469_b200 import PifSolver
+
+    torch = torch_dev
+    Lk = 2 * np.pi / 0.5
+    xv = landau_state(N, ppc, L=Lk, seed=7)
+    npart = xv.shape[1]
+    q = np.full(npart, -Lk ** 3 / npart)          # D#2 macro charge
+    P = PifSolver(N, Lk, 1e-4)
+    E, W = P.solve(_x(torch, xv), torch.from_numpy(q).cuda())
+    E = E.cpu().numpy()
+    Eo, Wo, _ = U.pif_solve(xv[:3], q, N, Lk, 1e-4)
+    assert np.abs(E - Eo).max() <= 1e-10 * np.abs(Eo).max()
+    assert np.allclose(W, Wo, rtol=1e-10, atol=0)
+
+
+def test_pif_cosine_lattice_closed_form_at_size(torch_dev):
+    """2^21 particles on a 128^3 lattice, weights h^3 (1 + alpha cos(k1 x)), N = 64 modes:
+    E_x = alpha sin(k1 x) / k1, E_y = E_z = 0, W_x = alpha^2 L^3 / (4 k1^2)."""
+    from paper_2605_05469_b200 import PifSolver
+
+    torch = torch_dev
+    Nl, alpha = 128, 0.05
+    k1 = 2 * np.pi / L
+    h = L / Nl
+    g = torch.arange(Nl, dtype=torch.float64, device="cuda") * h + 0.21 * h
+    Z, Y, X = torch.meshgrid(g, g, g, indexing="ij")
+    x = torch.stack([X.reshape(-1), Y.reshape(-1), Z.reshape(-1)]).contiguous()
+    q = (h ** 3 * (1 + alpha * torch.cos(k1 * x[0]))).contiguous()
+    P = PifSolver(64, L, 1e-4)
+    E, W = P.solve(x, q)
+    scale = alpha / k1
+    assert (E[0] - alpha * torch.sin(k1 * x[0]) / k1).abs().max().item() < 1e-4 * scale
+    assert E[1:].abs().max().item() < 1e-4 * scale
+    assert abs(W[0] - alpha ** 2 * L ** 3 / (4 * k1 ** 2)) < 1e-4 * W[0]
+
+
+def test_type1_sampled_modes_at_size(torch_dev):
+    """128^3 x 8 Landau particles, N = 128: 6 sampled modes against the direct sum (Eq. p2f)."""
+    from paper_2605_05469_b200 import PifSolver
+
+    torch = torch_dev
+    N = 128
+    Lk = 2 * np.pi / 0.5
+    xv = landau_state(N, 8, L=Lk, seed=11)
+    f = random_weights(xv.shape[1], seed=12)
+    P = PifSolver(N, Lk, 1e-4)
+    g = P.type1(_x(torch, xv), torch.from_numpy(f).cuda()).cpu().numpy()
+    modes = [(0, 0, 0), (1, 0, 0), (0, -1, 2), (-64, 5, 63), (17, -33, -64), (63, 63, 63)]
+    ref = U.nudft1_modes(xv[:3], f, Lk, modes)
+    got = np.array([g[n[2] + N // 2, n[1] + N // 2, n[0] + N // 2] for n in modes])
+    assert np.abs(got - ref).max() <= 1e-4 * np.abs(f).sum()
