@@ -177,6 +177,11 @@ def _oracle_steps(solver, n, L, xv, steps):
         return O.run_pcg(n, L, 0.05, xv, steps)[0]
     if solver == "fem":
         return O.run_fem(n, L, 0.05, xv, steps)[0]
+    if solver == "pif":
+        import numpy as np
+        from oracle import nufft as U
+
+        return U.pif_run(n, L, 0.05, xv, np.full(xv.shape[1], -L ** 3 / xv.shape[1]), steps)[0]
     return O.run(n, L, 0.05, xv, steps)[0]
 
 
@@ -205,7 +210,7 @@ def run_reference(args, rank, world):
     from pic_inputs import landau_state
     import numpy as np
 
-    n, ppc = 64, 8
+    n, ppc = (16, 8) if args.solver == "pif" else (64, 8)
     L = 4 * np.pi
     xv = landau_state(n, ppc, seed=1)
     xs = _oracle_steps(args.solver, n, L, xv, args.warmup) if args.warmup else xv
@@ -214,7 +219,7 @@ def run_reference(args, rank, world):
     dt = time.perf_counter() - t0
     npart = ppc * n ** 3
     value = npart * args.steps / dt
-    sample = (f"CPU oracle (serial C) on Landau {n}^3 x {ppc} ppc ({npart} particles) per step, "
+    sample = (f"CPU oracle ({'numpy, oracle/nufft.py' if args.solver == 'pif' else 'serial C'}) on Landau {n}^3 x {ppc} ppc ({npart} particles) per step, "
               f"a bounded sample of the {args.n}^3 x {args.ppc} workload")
     line = {
         "impl": "reference", "metric": METRIC.replace("FFT-PIC", args.solver.upper() + "-PIC"), "value": value, "unit": UNIT, "n_gpus": args.gpus,
@@ -406,6 +411,150 @@ def run_ours(args, rank, world):
     return 0
 
 
+# ------------------------------------------------------------ PIF arm (NEXT-2) --
+# Algorithmic bytes: spread reads x, y, z, q (32 B) per particle and writes the
+# M^3 complex fine grid once (16 B per fine point, the memset included); interp reads x, y, z
+# (24 B) and writes 16 B (E_x, E_y pass) or 8 B (E_z pass) per particle and reads the grid
+# once (16 B per fine point); push reads x, v, E and writes x, v (120 B) per particle.
+def pif_alg_bytes(stage: str, npart: int, n: int) -> float:
+    M3 = (2 * n) ** 3
+    return {"spread": 32 * npart + 16 * M3, "interp": 24 * npart + 12 * npart + 16 * M3,
+            "push": 120 * npart, "fill": 16 * M3, "modes": 48 * n ** 3}.get(stage, 0.0)
+
+
+def run_pif(args, rank, world):
+    """PIF time loop (pic_pif_step: PIF solve + leapfrog push) on N^3 modes x ppc particles per
+    cell; N > 1: independent replicas (the PIF solve is not decomposed: "replicas only")."""
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    local = int(os.environ.get("LOCAL_RANK", 0))
+    torch.cuda.set_device(local)
+    from paper_2605_05469_b200 import PifSolver, PIF_STAGES
+
+    n, ppc = args.n, args.ppc
+    L = 4 * np.pi
+    npart = ppc * n ** 3
+    h = L / n
+    gen = torch.Generator(device="cuda").manual_seed(1 + rank)
+    x = torch.empty((3, npart), dtype=torch.float64, device="cuda")
+    cell = torch.arange(npart, device="cuda", dtype=torch.int64) // ppc
+    for d, c in enumerate([cell % n, (cell // n) % n, cell // (n * n)]):
+        x[d] = (c.double() + torch.rand(npart, dtype=torch.float64, device="cuda", generator=gen)) * h
+    del cell
+    v = torch.randn((3, npart), dtype=torch.float64, device="cuda", generator=gen)
+    q = torch.full((npart,), -L ** 3 / npart, dtype=torch.float64, device="cuda")
+    E = torch.empty_like(x)
+    P = PifSolver(n, L, 1e-4)
+    stream = P.stream
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    if args.warmup:
+        P.step(x, v, q, nsteps=args.warmup, E=E)
+    barrier()
+    torch.cuda.synchronize()
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        ev0.record(stream)
+        ex = P.step(x, v, q, nsteps=args.steps, E=E)
+        ev1.record(stream)
+        ev1.synchronize()
+    barrier()
+    ms = reduce_max(ev0.elapsed_time(ev1), world)
+    # per-stage split from a separate timed pass (the timed region above runs without events)
+    P.set_timing(True)
+    P.step(x, v, q, nsteps=2, E=E, energy=False)
+    tm = P.timings()
+    P.set_timing(False)
+    value = world * npart * args.steps / (ms / 1e3)
+
+    e2e = None
+    if not args.no_e2e:
+        hx = torch.empty((3, npart), dtype=torch.float64, pin_memory=True)
+        hv = torch.empty((3, npart), dtype=torch.float64, pin_memory=True)
+        hx.copy_(x)
+        hv.copy_(v)
+        barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        x.copy_(hx, non_blocking=True)
+        v.copy_(hv, non_blocking=True)
+        P.step(x, v, q, nsteps=args.steps, E=E)
+        hx.copy_(x)
+        hv.copy_(v)
+        torch.cuda.synchronize()
+        t_e2e = reduce_max(time.perf_counter() - t0, world)
+        e2e = {"value": world * npart * args.steps / t_e2e, "unit": UNIT,
+               "h2d_bytes_per_step": 48 * npart / args.steps,
+               "d2h_bytes_per_step": (48 * npart + 8 * args.steps) / args.steps,
+               "what": "x, v from pinned host + pic_pif_step(K) with per-step W_x to host + x, v back; "
+                       "wall clock, max over ranks; bytes per rank"}
+        del hx, hv
+    if rank != 0:
+        return 0
+    stages = {}
+    for k, (t, nl) in tm.items():
+        if nl:
+            per = 2   # steps of the split pass
+            stages[k] = {"ms_per_step": t / per, "launches_per_step": nl / per,
+                         "alg_GBps": pif_alg_bytes(k, npart, n) * (nl / per) / (t / per / 1e3) / 1e9
+                         if k != "fft" else None}
+    dom = max((k for k in stages if k != "fft"), key=lambda k: stages[k]["ms_per_step"])
+    per_launch_ms = stages[dom]["ms_per_step"] / stages[dom]["launches_per_step"]
+    alg = pif_alg_bytes(dom, npart, n)
+    peaks = measured_peaks()
+    peak = peaks.get("hbm_gbs") or 6650.0
+    roof = {"bound": "hbm", "kernel": dom, "achieved": alg / (per_launch_ms / 1e3) / 1e9, "peak": peak,
+            "unit": "GB/s", "frac": alg / (per_launch_ms / 1e3) / 1e9 / peak,
+            "traffic": ncu_traffic(f"pif_{n}^3x{ppc}", dom),
+            "peak_source": "measured (MEASURED_PEAKS.json hbm_gbs)" if peaks.get("hbm_gbs") else "fallback 6650 GB/s",
+            "alg_bytes_per_launch": alg,
+            "note": "the window spreading is bound by fp64 L2 atomics (w^3 = 216 per particle), not by "
+                    "its algorithmic HBM bytes; see DESIGN §6f"}
+    cpu = None
+    if not args.no_cpu_baseline:
+        from oracle import nufft as U
+        from pic_inputs import landau_state
+
+        cn, cppc, csteps = 16, 8, 2
+        xv = landau_state(cn, cppc, seed=1, L=L)
+        qq = np.full(xv.shape[1], -L ** 3 / xv.shape[1])
+        t0 = time.perf_counter()
+        U.pif_run(cn, L, 0.05, xv, qq, csteps)
+        dt_c = time.perf_counter() - t0
+        cpu = {"value": xv.shape[1] * csteps / dt_c, "unit": UNIT, "cores": 1, "kind": "oracle",
+               "sample": f"oracle/nufft.py pif_run (numpy, per-particle Python loops) on {cn}^3 modes x {cppc} "
+                         f"ppc ({xv.shape[1]} particles), {csteps} steps, {dt_c:.1f} s"}
+    w, M = P.window()
+    line = {
+        "metric": METRIC.replace("FFT-PIC", "PIF-PIC"), "value": value, "unit": UNIT,
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic",
+        "config": {"workload": f"pif_{n}^3x{ppc}", "modes": n, "ppc": ppc, "particles": npart, "eps": 1e-4,
+                   "window_w": w, "fine_grid": M, "dt": 0.05,
+                   "input": "uniform density, particles in cell order (x fastest) with uniform jitter, "
+                            "Maxwellian v (torch RNG on the device)",
+                   "parallelism": "1 GPU" if world == 1 else f"{world} independent replicas",
+                   "l2": "inputs larger than L2 (x, v, E, q: 80 B x N_p; fine grid 16 B x (2N)^3)"},
+        "roofline": roof,
+        "cpu_baseline": cpu,
+        "e2e": e2e,
+        "gpu_launches": int(sum(s["launches_per_step"] for s in stages.values()) * args.steps) + 2 * args.steps,
+        "gpu_launches_note": "kernels + cuFFT executions per step x steps (the energy reduce counted with modes)",
+        "clocks": clk.summary(),
+        "stages": stages,
+        "w_x_first_last": [float(ex[0]), float(ex[-1])],
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -414,8 +563,9 @@ def main():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--n", type=int, default=512)
     ap.add_argument("--ppc", type=int, default=8)
-    ap.add_argument("--solver", choices=["fft", "pcg", "fem"], default="fft",
-                    help="field solver: fft (BJ configs 0-3), pcg (BJ config 5) or fem (SURVEY §8(f) NEXT-4)")
+    ap.add_argument("--solver", choices=["fft", "pcg", "fem", "pif"], default="fft",
+                    help="field solver: fft (BJ configs 0-3), pcg (BJ config 5), fem (SURVEY §8(f) NEXT-4) "
+                         "or pif (Particle-in-Fourier, NEXT-2; N^3 modes, eps 1e-4)")
     ap.add_argument("--dt", type=float, default=0.05, help="time step (diagnostics; the workload is dt = 0.05)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -432,7 +582,7 @@ def main():
 
         torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", 0)))
         dist.init_process_group("nccl")
-    rc = run_ours(args, rank, world)
+    rc = run_pif(args, rank, world) if args.solver == "pif" else run_ours(args, rank, world)
     if world > 1:
         import torch.distributed as dist
 

@@ -58,6 +58,15 @@ pic_status pic_nufft_type2(pic_pif *p, int64_t np, const double *x, const double
 pic_status pic_pif_solve(pic_pif *p, int64_t np, const double *x, const double *q, double *E,
                          double *energy);
 
+/* PIF time loop (Fig. 1, with the PIF solve in place of deposit + solve + gather):
+ * nsteps x { E = pic_pif_solve(x); W_x(t_n) -> ex_energy[n] (D#12); v += qm dt E;
+ * x += v dt; wrap into [0, L) (D#9, the PIC push) }.  x, v: device [3][np] (updated in
+ * place); q: device [np]; E: device [3][np] scratch (holds the last step's field).
+ * ex_energy: host [nsteps] or NULL (one synchronisation at the end).  PIC_EINVAL: nsteps
+ * outside [1, 4096]. */
+pic_status pic_pif_step(pic_pif *p, int64_t np, double *x, double *v, const double *q, double *E,
+                        double qm, double dt, int32_t nsteps, double *ex_energy);
+
 /* Per-stage device time (CUDA events on the plan's stream) accumulated over the calls since
  * timing was enabled, ms[PIC_PIF_NSTAGES]; launches[PIC_PIF_NSTAGES] nullable.  Enabling
  * timing makes every call synchronise at its end. */
@@ -67,6 +76,7 @@ enum {
     PIC_PIF_MODES,      /* chi, D, Poisson, -i k, energy partials (type 1 side)       */
     PIC_PIF_FILL,       /* chi^T D: the fine grid from the spectrum (type 2 side)     */
     PIC_PIF_INTERP,     /* C^T: the window sums at the particles                      */
+    PIC_PIF_PUSH,       /* pic_pif_step: kick, drift, wrap                             */
     PIC_PIF_NSTAGES
 };
 pic_status pic_pif_set_timing(pic_pif *p, int32_t enable);

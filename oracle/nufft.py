@@ -218,3 +218,19 @@ def nudft1_modes(x: np.ndarray, f: np.ndarray, L: float, modes) -> np.ndarray:
         k = 2 * np.pi / L * np.asarray(n, dtype=np.float64)
         out.append(np.sum(f * np.exp(-1j * (k[0] * x[0] + k[1] * x[1] + k[2] * x[2]))))
     return np.array(out)
+
+
+def pif_run(N: int, L: float, dt: float, xv: np.ndarray, q: np.ndarray, nsteps: int, eps: float = 1e-4):
+    """The PIF time loop (Fig. 1, with the PIF solve of P:203-214 in place of
+    deposit + solve + gather): each step E = pif_solve(x_n), W_x(t_n) recorded (D#12), then
+    the leapfrog kick-drift-wrap of the PIC oracle (q/m = -1, D#2, D#9).
+    Returns (xv after nsteps, W_x[nsteps])."""
+    from oracle import oracle as O
+
+    xs = np.ascontiguousarray(xv, dtype=np.float64).copy()
+    ex = np.zeros(nsteps)
+    for s in range(nsteps):
+        E, W, _ = pif_solve(xs[:3], q, N, L, eps)
+        ex[s] = W[0]
+        xs = O.push(L, xs, E, -dt, dt)
+    return xs, ex

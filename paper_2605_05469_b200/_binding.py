@@ -97,6 +97,7 @@ SYMBOLS = {
     "pic_nufft_type1": (C.c_int, [_vp, C.c_int64, _vp, _vp, _vp]),
     "pic_nufft_type2": (C.c_int, [_vp, C.c_int64, _vp, _vp, _vp]),
     "pic_pif_solve": (C.c_int, [_vp, C.c_int64, _vp, _vp, _vp, _dp]),
+    "pic_pif_step": (C.c_int, [_vp, C.c_int64, _vp, _vp, _vp, _vp, C.c_double, C.c_double, C.c_int32, _dp]),
     "pic_pif_set_timing": (C.c_int, [_vp, C.c_int32]),
     "pic_pif_get_timings": (C.c_int, [_vp, _dp, _i64p]),
     "pic_pif_window": (C.c_int, [_vp, C.POINTER(C.c_int32), C.POINTER(C.c_int32)]),
@@ -104,7 +105,7 @@ SYMBOLS = {
     "pic_pif_free": (None, [_vp]),
 }
 
-PIF_STAGES = ["spread", "fft", "modes", "fill", "interp"]
+PIF_STAGES = ["spread", "fft", "modes", "fill", "interp", "push"]
 
 _lib = None
 
@@ -398,6 +399,22 @@ class PifSolver:
         _check_pif(lib().pic_pif_solve(self.plan, npart, C.c_void_p(x.data_ptr()), C.c_void_p(q.data_ptr()),
                                        C.c_void_p(E.data_ptr()), _d(W) if energy else None), self.plan)
         return E, (W if energy else None)
+
+    def step(self, x, v, q, nsteps: int = 1, qm: float = -1.0, dt: float = 0.05, E=None, energy: bool = True):
+        """The PIF time loop (pic_pif_step): x, v (3, np) updated in place; returns W_x per step
+        (synchronises) or None."""
+        import torch
+
+        npart = self._pos(x)
+        assert v.dtype == torch.float64 and v.is_contiguous() and v.shape == x.shape
+        assert q.dtype == torch.float64 and q.is_contiguous() and q.numel() == npart
+        if E is None:
+            E = torch.empty_like(x)
+        ex = np.zeros(max(nsteps, 1))
+        _check_pif(lib().pic_pif_step(self.plan, npart, C.c_void_p(x.data_ptr()), C.c_void_p(v.data_ptr()),
+                                      C.c_void_p(q.data_ptr()), C.c_void_p(E.data_ptr()), qm, dt, nsteps,
+                                      _d(ex) if energy else None), self.plan)
+        return ex[:nsteps] if energy else None
 
     def set_timing(self, enable: bool = True):
         _check_pif(lib().pic_pif_set_timing(self.plan, int(enable)), self.plan)

@@ -24,7 +24,8 @@ namespace {
 
 constexpr int kThreads = 256;
 constexpr int kModeBlocks = 1184;      // 148 SMs x 8: the mode kernels' grid (energy partials)
-constexpr int kNq = 64;                // Gauss-Legendre nodes for psi^
+constexpr int kNq = 64;               // Gauss-Legendre nodes for psi^
+constexpr int kMaxSteps = 4096;        // pic_pif_step energy history
 thread_local char g_err[256] = "";
 
 __device__ __forceinline__ double psi_es(double z, double beta) {
@@ -221,11 +222,35 @@ __global__ void __launch_bounds__(kThreads) k_pif_modes(int N, int M, double kun
     if (threadIdx.x < 3) partials[blockIdx.x * 3 + threadIdx.x] = red[threadIdx.x][0];
 }
 
-__global__ void k_energy(int nblk, const double* __restrict__ partials, double scale, double* __restrict__ out) {
+__global__ void k_energy(int nblk, const double* __restrict__ partials, double scale, double* __restrict__ out,
+                         double* __restrict__ hist) {
     if (threadIdx.x < 3) {
         double s = 0.0;
         for (int b = 0; b < nblk; ++b) s += partials[b * 3 + threadIdx.x];
         out[threadIdx.x] = s * scale;
+        if (hist && threadIdx.x == 0) *hist = s * scale;
+    }
+}
+
+// Leapfrog kick-drift-wrap (D#9; the PIC push): v += qm_dt E; x += v dt; x into [0, L).
+__global__ void __launch_bounds__(kThreads) k_pif_push(int64_t np, double* __restrict__ X, double* __restrict__ V,
+                                                       const double* __restrict__ E, double qm_dt, double dt,
+                                                       double L) {
+    const int64_t j = (int64_t)blockIdx.x * kThreads + threadIdx.x;
+    if (j >= np) return;
+#pragma unroll
+    for (int d = 0; d < 3; ++d) {
+        const int64_t i = d * np + j;
+        const double v = __dadd_rn(V[i], __dmul_rn(qm_dt, E[i]));
+        double x = __dadd_rn(X[i], __dmul_rn(v, dt));
+        if (x >= L) {
+            x = __dsub_rn(x, L);
+        } else if (x < 0.0) {
+            x = __dadd_rn(x, L);
+            if (x >= L) x = 0.0;
+        }
+        V[i] = v;
+        X[i] = x;
     }
 }
 
@@ -268,14 +293,16 @@ struct pic_pif {
     double* dinv;        // N: 1 / psi^
     double* partials;    // kModeBlocks x 3
     double* energy;      // 3
+    double* hist;        // kMaxSteps: W_x per step of pic_pif_step
+    int hist_slot;       // -1: no history write
     void* fft_work;
     bool poisoned;
     bool timing;
-    cudaEvent_t ev[2 * PIC_PIF_NSTAGES * 4];
+    cudaEvent_t ev[512];
     int nev;
     double ms[PIC_PIF_NSTAGES];
     int64_t launches[PIC_PIF_NSTAGES];
-    int ev_stage[PIC_PIF_NSTAGES * 4];
+    int ev_stage[256];
     char err[256];
 };
 
@@ -298,7 +325,7 @@ pic_status make_plan(int M, cufftHandle* plan, size_t* work) {
 }
 
 struct Layout {
-    size_t G, A, Bz, dinv, partials, energy, work, total;
+    size_t G, A, Bz, dinv, partials, energy, hist, work, total;
 };
 Layout layout(int n, size_t fft_work) {
     const size_t M = 2 * (size_t)n;
@@ -310,6 +337,7 @@ Layout layout(int n, size_t fft_work) {
     o.dinv = off;     off += align256((size_t)n * sizeof(double));
     o.partials = off; off += align256((size_t)kModeBlocks * 3 * sizeof(double));
     o.energy = off;   off += align256(3 * sizeof(double));
+    o.hist = off;     off += align256(kMaxSteps * sizeof(double));
     o.work = off;     off += align256(fft_work);
     o.total = off;
     return o;
@@ -499,6 +527,8 @@ pic_status pic_pif_create(int32_t n, double length, double eps, void* workspace,
     p->dinv = (double*)(b + o.dinv);
     p->partials = (double*)(b + o.partials);
     p->energy = (double*)(b + o.energy);
+    p->hist = (double*)(b + o.hist);
+    p->hist_slot = -1;
     p->fft_work = b + o.work;
     if (cufftSetWorkArea(p->plan, p->fft_work) != CUFFT_SUCCESS ||
         cufftSetStream(p->plan, p->stream) != CUFFT_SUCCESS) {
@@ -541,9 +571,11 @@ pic_status pic_nufft_type2(pic_pif* p, int64_t np, const double* x, const double
     return flush_timing(p);
 }
 
-pic_status pic_pif_solve(pic_pif* p, int64_t np, const double* x, const double* q, double* E, double* energy) {
-    PIF_CHECK(p);
-    if (np < 0 || (np > 0 && (!x || !q || !E))) return PIC_EINVAL;
+}  // extern "C"
+
+namespace {
+
+pic_status solve_core(pic_pif* p, int64_t np, const double* x, const double* q, double* E) {
     if (pic_status s = spread(p, np, x, q)) return s;                       // C
     if (pic_status s = fft(p, CUFFT_FORWARD)) return s;                     // F
     {
@@ -551,7 +583,8 @@ pic_status pic_pif_solve(pic_pif* p, int64_t np, const double* x, const double* 
         const double kunit = 2.0 * M_PI / p->L;
         k_pif_modes<<<kModeBlocks, kThreads, 0, p->stream>>>(p->n, p->M, kunit, p->G, p->dinv, p->A, p->Bz,
                                                               p->partials);
-        k_energy<<<1, 32, 0, p->stream>>>(kModeBlocks, p->partials, 0.5 / (p->L * p->L * p->L), p->energy);
+        k_energy<<<1, 32, 0, p->stream>>>(kModeBlocks, p->partials, 0.5 / (p->L * p->L * p->L), p->energy,
+                                          p->hist_slot >= 0 ? p->hist + p->hist_slot : nullptr);
         PIF_LAUNCHED(p);
     }
     const double sc = 1.0 / (p->L * p->L * p->L);                           // D#35
@@ -560,13 +593,51 @@ pic_status pic_pif_solve(pic_pif* p, int64_t np, const double* x, const double* 
     if (pic_status s = interp(p, np, x, E, E + np, 1, sc)) return s;
     if (pic_status s = fill(p, p->Bz)) return s;                            // E_z
     if (pic_status s = fft(p, CUFFT_INVERSE)) return s;
-    if (pic_status s = interp(p, np, x, E + 2 * np, nullptr, 1, sc)) return s;
+    return interp(p, np, x, E + 2 * np, nullptr, 1, sc);
+}
+
+}  // namespace
+
+extern "C" {
+
+pic_status pic_pif_solve(pic_pif* p, int64_t np, const double* x, const double* q, double* E, double* energy) {
+    PIF_CHECK(p);
+    if (np < 0 || (np > 0 && (!x || !q || !E))) return PIC_EINVAL;
+    p->hist_slot = -1;
+    if (pic_status s = solve_core(p, np, x, q, E)) return s;
     if (energy) {
         PIF_CUDA(p, cudaMemcpyAsync(energy, p->energy, 3 * sizeof(double), cudaMemcpyDeviceToHost, p->stream));
         PIF_CUDA(p, cudaStreamSynchronize(p->stream));
         for (int d = 0; d < 3; ++d)
             if (!std::isfinite(energy[d])) {
                 snprintf(p->err, sizeof(p->err), "PIF field energy %d is not finite", d);
+                return PIC_ENONFINITE;
+            }
+    }
+    return flush_timing(p);
+}
+
+pic_status pic_pif_step(pic_pif* p, int64_t np, double* x, double* v, const double* q, double* E, double qm,
+                        double dt, int32_t nsteps, double* ex_energy) {
+    PIF_CHECK(p);
+    if (np < 0 || (np > 0 && (!x || !v || !q || !E)) || nsteps < 1 || nsteps > kMaxSteps) return PIC_EINVAL;
+    const double qm_dt = qm * dt;
+    for (int s = 0; s < nsteps; ++s) {
+        p->hist_slot = s;
+        pic_status st = solve_core(p, np, x, q, E);
+        p->hist_slot = -1;
+        if (st) return st;
+        Stage t(p, PIC_PIF_PUSH);
+        if (np > 0) k_pif_push<<<particle_grid(np), kThreads, 0, p->stream>>>(np, x, v, E, qm_dt, dt, p->L);
+        PIF_LAUNCHED(p);
+    }
+    if (ex_energy) {
+        PIF_CUDA(p, cudaMemcpyAsync(ex_energy, p->hist, nsteps * sizeof(double), cudaMemcpyDeviceToHost,
+                                    p->stream));
+        PIF_CUDA(p, cudaStreamSynchronize(p->stream));
+        for (int s = 0; s < nsteps; ++s)
+            if (!std::isfinite(ex_energy[s])) {
+                snprintf(p->err, sizeof(p->err), "PIF field energy of step %d is not finite", s);
                 return PIC_ENONFINITE;
             }
     }

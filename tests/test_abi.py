@@ -133,4 +133,4 @@ def test_pif_parameter_validation_without_gpu():
         assert pkg.lib().pic_pif_workspace_bytes(n, L, eps, C.byref(b)) == B.PIC_EINVAL
     assert pkg.lib().pic_nufft_type1(None, 1, None, None, None) == B.PIC_EINVAL
     assert pkg.lib().pic_pif_solve(None, 1, None, None, None, None) == B.PIC_EINVAL
-    assert B.PIF_STAGES == ["spread", "fft", "modes", "fill", "interp"]
+    assert B.PIF_STAGES == ["spread", "fft", "modes", "fill", "interp", "push"]

@@ -159,3 +159,29 @@ def test_pif_mirrored_pair_forces_opposite_and_exact_hook():
     assert np.abs(Ee[:, 0] + Ee[:, 1]).max() < 1e-12 * scale
     assert np.abs(E[:, 0] + E[:, 1]).max() < 2e-4 * scale
     assert np.abs(E - Ee).max() < 1e-4 * scale * 10
+
+
+def test_pif_run_conserves_momentum_and_streams_freely():
+    """P:203-214 + P:124-137: equal charges, type 2 the exact adjoint of type 1 ->
+    sum_j E(x_j) = L^-3 sum_k conj(rho^) (-i k rho^ / |k|^2) = 0 (antisymmetric in k), so
+    total momentum is conserved to rounding; a uniform lattice (alpha = 0) feels no field
+    and streams freely (x + n v dt, wrapped)."""
+    from pic_inputs import landau_state
+
+    Lk = 2 * np.pi / 0.5
+    xv = landau_state(4, 4, L=Lk, seed=21, alpha=0.3)
+    q = np.full(xv.shape[1], -Lk ** 3 / xv.shape[1])
+    p0 = xv[3:].sum(axis=1)
+    xs, ex = U.pif_run(4, Lk, 0.05, xv, q, 3)
+    assert np.abs(xs[3:].sum(axis=1) - p0).max() < 1e-11 * np.abs(xv[3:]).sum()
+    assert np.all(ex > 0)
+    h = Lk / 4
+    g = np.arange(4) * h + 0.5 * h
+    X, Y, Z = np.meshgrid(g, g, g, indexing="ij")
+    lat = np.zeros((6, 64))
+    lat[:3] = np.stack([X.ravel(), Y.ravel(), Z.ravel()])
+    lat[3] = 0.7
+    ql = np.full(64, -Lk ** 3 / 64)
+    xs, ex = U.pif_run(4, Lk, 0.05, lat, ql, 2)
+    assert np.abs(xs[3] - 0.7).max() < 1e-12 and np.all(ex < 1e-20)
+    assert np.abs(xs[0] - np.mod(lat[0] + 2 * 0.05 * 0.7, Lk)).max() < 1e-12
