@@ -446,7 +446,7 @@ def run_pif(args, rank, world):
     v = torch.randn((3, npart), dtype=torch.float64, device="cuda", generator=gen)
     q = torch.full((npart,), -L ** 3 / npart, dtype=torch.float64, device="cuda")
     E = torch.empty_like(x)
-    P = PifSolver(n, L, 1e-4)
+    P = PifSolver(n, L, 1e-4, np_max=0 if args.pif_atomic else npart)
     stream = P.stream
 
     def barrier():
@@ -568,6 +568,7 @@ def main():
                          "or pif (Particle-in-Fourier, NEXT-2; N^3 modes, eps 1e-4)")
     ap.add_argument("--dt", type=float, default=0.05, help="time step (diagnostics; the workload is dt = 0.05)")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--pif-atomic", action="store_true", help="PIF: global-atomic spreading (no bins)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-steps", type=int, default=20)
     args = ap.parse_args()

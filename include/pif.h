@@ -31,16 +31,20 @@ extern "C" {
 
 typedef struct pic_pif pic_pif;
 
-/* Workspace bytes for modes N, domain length L and accuracy eps (creates and destroys a
- * cuFFT plan to learn its scratch size: needs a CUDA device).  PIC_EINVAL: N odd or out
- * of [8, 1024], L <= 0, eps outside [1e-14, 1). */
-pic_status pic_pif_workspace_bytes(int32_t n, double length, double eps, size_t *bytes);
+/* Workspace bytes for modes N, domain length L, accuracy eps and up to np_max particles per
+ * call (creates and destroys a cuFFT plan to learn its scratch size: needs a CUDA device).
+ * np_max > 0 reserves the binned path (4 B per particle + 12 B per bin of 8^3 fine cells):
+ * particles counting-sorted into bins, spreading through shared-memory tiles; it applies
+ * when 2N is a multiple of 8 and w <= 8 (eps >= 1e-6) and np <= np_max (else, or with
+ * PIC_PIF_BINNED=0 in the environment, one global atomic per window point).  PIC_EINVAL: N
+ * odd or out of [8, 1024], L <= 0, eps outside [1e-14, 1), np_max outside [0, 2^32). */
+pic_status pic_pif_workspace_bytes(int32_t n, double length, double eps, int64_t np_max, size_t *bytes);
 
 /* Create a plan on the current device over `workspace` (>= pic_pif_workspace_bytes) and
  * `stream` (cudaStream_t as void*; NULL = legacy default).  Computes the deconvolution
  * table 1 / psi^(n) on the device.  PIC_ENOMEM: workspace too small. */
-pic_status pic_pif_create(int32_t n, double length, double eps, void *workspace, size_t bytes,
-                          void *stream, pic_pif **out);
+pic_status pic_pif_create(int32_t n, double length, double eps, int64_t np_max, void *workspace,
+                          size_t bytes, void *stream, pic_pif **out);
 
 /* Type-1 NUFFT, Eq. (p2f) / (type1nufft): fhat(k) = sum_j f_j e^{-i k.x_j}
  * for k in K_N, computed as D chi F C f.  fhat: device [N^3][2] doubles.  Asynchronous. */
@@ -77,6 +81,7 @@ enum {
     PIC_PIF_FILL,       /* chi^T D: the fine grid from the spectrum (type 2 side)     */
     PIC_PIF_INTERP,     /* C^T: the window sums at the particles                      */
     PIC_PIF_PUSH,       /* pic_pif_step: kick, drift, wrap                             */
+    PIC_PIF_BIN,        /* binned path: counting sort of the particles into bins       */
     PIC_PIF_NSTAGES
 };
 pic_status pic_pif_set_timing(pic_pif *p, int32_t enable);

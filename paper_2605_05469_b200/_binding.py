@@ -92,8 +92,9 @@ SYMBOLS = {
     "pic_launches_per_step": (C.c_int, [_vp, _i64p]),
     "pic_pcg_stats": (C.c_int, [_vp, C.POINTER(C.c_int32), _i64p, _i64p, _dp]),
     # include/pif.h
-    "pic_pif_workspace_bytes": (C.c_int, [C.c_int32, C.c_double, C.c_double, C.POINTER(C.c_size_t)]),
-    "pic_pif_create": (C.c_int, [C.c_int32, C.c_double, C.c_double, _vp, C.c_size_t, _vp, C.POINTER(_vp)]),
+    "pic_pif_workspace_bytes": (C.c_int, [C.c_int32, C.c_double, C.c_double, C.c_int64, C.POINTER(C.c_size_t)]),
+    "pic_pif_create": (C.c_int, [C.c_int32, C.c_double, C.c_double, C.c_int64, _vp, C.c_size_t, _vp,
+                                 C.POINTER(_vp)]),
     "pic_nufft_type1": (C.c_int, [_vp, C.c_int64, _vp, _vp, _vp]),
     "pic_nufft_type2": (C.c_int, [_vp, C.c_int64, _vp, _vp, _vp]),
     "pic_pif_solve": (C.c_int, [_vp, C.c_int64, _vp, _vp, _vp, _dp]),
@@ -105,7 +106,7 @@ SYMBOLS = {
     "pic_pif_free": (None, [_vp]),
 }
 
-PIF_STAGES = ["spread", "fft", "modes", "fill", "interp", "push"]
+PIF_STAGES = ["spread", "fft", "modes", "fill", "interp", "push", "bin"]
 
 _lib = None
 
@@ -336,18 +337,20 @@ class PifSolver:
     indexed [nz + N/2, ny + N/2, nx + N/2].  The workspace is a torch uint8 tensor owned
     here; the stream is torch's current stream at construction."""
 
-    def __init__(self, n: int, length: float, eps: float = 1e-4, device=None):
+    def __init__(self, n: int, length: float, eps: float = 1e-4, device=None, np_max: int = 0):
+        """np_max > 0 reserves the binned (shared-memory tile) path for up to np_max particles."""
         import torch
 
-        self.n, self.L, self.eps = n, float(length), float(eps)
+        self.n, self.L, self.eps, self.np_max = n, float(length), float(eps), int(np_max)
         self.device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
         b = C.c_size_t()
         with torch.cuda.device(self.device):
-            _check_pif(lib().pic_pif_workspace_bytes(n, self.L, self.eps, C.byref(b)))
+            _check_pif(lib().pic_pif_workspace_bytes(n, self.L, self.eps, self.np_max, C.byref(b)))
             self.workspace = torch.empty(b.value, dtype=torch.uint8, device=self.device)
             self.stream = torch.cuda.current_stream(self.device)
         plan = C.c_void_p()
-        _check_pif(lib().pic_pif_create(n, self.L, self.eps, C.c_void_p(self.workspace.data_ptr()), b.value,
+        _check_pif(lib().pic_pif_create(n, self.L, self.eps, self.np_max, C.c_void_p(self.workspace.data_ptr()),
+                                        b.value,
                                         C.c_void_p(self.stream.cuda_stream), C.byref(plan)))
         self.plan = plan
 

@@ -18,13 +18,13 @@ npart = N ** 3 * ppc
 h = L / N
 x = torch.empty((3, npart), dtype=torch.float64, device="cuda")
 cell = torch.arange(npart, device="cuda", dtype=torch.int64) // ppc
-if order == "random":
+if order.startswith("random"):
     cell = cell[torch.randperm(npart, device="cuda", generator=g)]
 for d, c in enumerate([cell % N, (cell // N) % N, cell // (N * N)]):
     x[d] = (c.double() + torch.rand(npart, dtype=torch.float64, device="cuda", generator=g)) * h
 del cell
 q = torch.full((npart,), -L ** 3 / npart, dtype=torch.float64, device="cuda")
-P = PifSolver(N, L, 1e-4)
+P = PifSolver(N, L, 1e-4, np_max=0 if order.endswith('atomic') else npart)
 E = torch.empty_like(x)
 P.solve(x, q, E)
 torch.cuda.synchronize()

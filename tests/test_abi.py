@@ -130,7 +130,8 @@ def test_pif_parameter_validation_without_gpu():
     b = C.c_size_t()
     for n, L, eps in [(7, 1.0, 1e-4), (4, 1.0, 1e-4), (2048, 1.0, 1e-4), (16, 0.0, 1e-4), (16, 1.0, 1.5),
                       (16, 1.0, 1e-20)]:
-        assert pkg.lib().pic_pif_workspace_bytes(n, L, eps, C.byref(b)) == B.PIC_EINVAL
+        assert pkg.lib().pic_pif_workspace_bytes(n, L, eps, 0, C.byref(b)) == B.PIC_EINVAL
+    assert pkg.lib().pic_pif_workspace_bytes(16, 1.0, 1e-4, -1, C.byref(b)) == B.PIC_EINVAL
     assert pkg.lib().pic_nufft_type1(None, 1, None, None, None) == B.PIC_EINVAL
     assert pkg.lib().pic_pif_solve(None, 1, None, None, None, None) == B.PIC_EINVAL
-    assert B.PIF_STAGES == ["spread", "fft", "modes", "fill", "interp", "push"]
+    assert B.PIF_STAGES == ["spread", "fft", "modes", "fill", "interp", "push", "bin"]

@@ -31,14 +31,16 @@ def _x(torch, xv):
     return torch.from_numpy(np.ascontiguousarray(xv[:3])).cuda()
 
 
-@pytest.mark.parametrize("N,np_,eps", [(16, 3000, 1e-4), (12, 777, 1e-4), (8, 500, 1e-6), (16, 0, 1e-4)])
-def test_type1_matches_oracle(torch_dev, N, np_, eps):
+@pytest.mark.parametrize("binned", [True, False])
+@pytest.mark.parametrize("N,np_,eps", [(16, 3000, 1e-4), (12, 777, 1e-4), (8, 500, 1e-6), (16, 0, 1e-4),
+                                       (10, 300, 1e-4), (8, 400, 1e-2)])
+def test_type1_matches_oracle(torch_dev, N, np_, eps, binned):
     from paper_2605_05469_b200 import PifSolver
 
     torch = torch_dev
     xv = landau_state(4, 1, L=L, np_=max(np_, 1), seed=3)[:, :np_]
     f = random_weights(np_, seed=4)
-    P = PifSolver(N, L, eps)
+    P = PifSolver(N, L, eps, np_max=np_ if binned else 0)
     g = P.type1(_x(torch, xv), torch.from_numpy(f).cuda()).cpu().numpy()
     if np_ == 0:
         assert np.all(g == 0)
@@ -48,22 +50,24 @@ def test_type1_matches_oracle(torch_dev, N, np_, eps):
     assert np.abs(g - U.nudft1(xv[:3], f, N, L)).max() <= eps * np.abs(f).sum()
 
 
-@pytest.mark.parametrize("N,np_", [(16, 400), (10, 123)])
-def test_type2_matches_oracle(torch_dev, N, np_):
+@pytest.mark.parametrize("binned", [True, False])
+@pytest.mark.parametrize("N,np_", [(16, 400), (10, 123), (8, 333)])
+def test_type2_matches_oracle(torch_dev, N, np_, binned):
     from paper_2605_05469_b200 import PifSolver
 
     torch = torch_dev
     xv = landau_state(4, 1, L=L, np_=np_, seed=5)
     fh = random_spectrum(N, seed=6)
-    P = PifSolver(N, L, 1e-4)
+    P = PifSolver(N, L, 1e-4, np_max=np_ if binned else 0)
     g = P.type2(torch.from_numpy(fh).cuda(), _x(torch, xv)).cpu().numpy()
     ref = U.nufft2(fh, xv[:3], L, 1e-4)
     assert np.abs(g - ref).max() <= 1e-11 * np.abs(fh).sum()
     assert np.abs(g - U.nudft2(fh, xv[:3], L)).max() <= 1e-4 * np.abs(fh).sum()
 
 
+@pytest.mark.parametrize("binned", [True, False])
 @pytest.mark.parametrize("N,ppc", [(16, 2), (8, 8)])
-def test_pif_solve_matches_oracle(torch_dev, N, ppc):
+def test_pif_solve_matches_oracle(torch_dev, N, ppc, binned):
     from paper_2605_05469_b200 import PifSolver
 
     torch = torch_dev
@@ -71,7 +75,7 @@ def test_pif_solve_matches_oracle(torch_dev, N, ppc):
     xv = landau_state(N, ppc, L=Lk, seed=7)
     npart = xv.shape[1]
     q = np.full(npart, -Lk ** 3 / npart)          # D#2 macro charge
-    P = PifSolver(N, Lk, 1e-4)
+    P = PifSolver(N, Lk, 1e-4, np_max=npart if binned else 0)
     E, W = P.solve(_x(torch, xv), torch.from_numpy(q).cuda())
     E = E.cpu().numpy()
     Eo, Wo, _ = U.pif_solve(xv[:3], q, N, Lk, 1e-4)
@@ -92,7 +96,7 @@ def test_pif_cosine_lattice_closed_form_at_size(torch_dev):
     Z, Y, X = torch.meshgrid(g, g, g, indexing="ij")
     x = torch.stack([X.reshape(-1), Y.reshape(-1), Z.reshape(-1)]).contiguous()
     q = (h ** 3 * (1 + alpha * torch.cos(k1 * x[0]))).contiguous()
-    P = PifSolver(64, L, 1e-4)
+    P = PifSolver(64, L, 1e-4, np_max=x.shape[1])
     E, W = P.solve(x, q)
     scale = alpha / k1
     assert (E[0] - alpha * torch.sin(k1 * x[0]) / k1).abs().max().item() < 1e-4 * scale
@@ -109,7 +113,7 @@ def test_type1_sampled_modes_at_size(torch_dev):
     Lk = 2 * np.pi / 0.5
     xv = landau_state(N, 8, L=Lk, seed=11)
     f = random_weights(xv.shape[1], seed=12)
-    P = PifSolver(N, Lk, 1e-4)
+    P = PifSolver(N, Lk, 1e-4, np_max=xv.shape[1])
     g = P.type1(_x(torch, xv), torch.from_numpy(f).cuda()).cpu().numpy()
     modes = [(0, 0, 0), (1, 0, 0), (0, -1, 2), (-64, 5, 63), (17, -33, -64), (63, 63, 63)]
     ref = U.nudft1_modes(xv[:3], f, Lk, modes)
@@ -117,8 +121,9 @@ def test_type1_sampled_modes_at_size(torch_dev):
     assert np.abs(got - ref).max() <= 1e-4 * np.abs(f).sum()
 
 
+@pytest.mark.parametrize("binned", [True, False])
 @pytest.mark.parametrize("N,ppc,nsteps", [(8, 4, 10), (16, 1, 3)])
-def test_pif_step_matches_oracle_run(torch_dev, N, ppc, nsteps):
+def test_pif_step_matches_oracle_run(torch_dev, N, ppc, nsteps, binned):
     """pic_pif_step vs oracle pif_run (PIF solve + the PIC leapfrog push + wrap), Landau
     alpha = 0.3: W_x per step 1e-9 relative, x (periodic) and v within 1e-9 after the steps;
     total momentum conserved (1e-11)."""
@@ -129,7 +134,7 @@ def test_pif_step_matches_oracle_run(torch_dev, N, ppc, nsteps):
     xv = landau_state(N, ppc, L=Lk, seed=23, alpha=0.3)
     npart = xv.shape[1]
     q = np.full(npart, -Lk ** 3 / npart)
-    P = PifSolver(N, Lk, 1e-4)
+    P = PifSolver(N, Lk, 1e-4, np_max=npart if binned else 0)
     x = torch.from_numpy(np.ascontiguousarray(xv[:3])).cuda()
     v = torch.from_numpy(np.ascontiguousarray(xv[3:])).cuda()
     ex = P.step(x, v, torch.from_numpy(q).cuda(), nsteps=nsteps, qm=-1.0, dt=0.05)
@@ -140,3 +145,22 @@ def test_pif_step_matches_oracle_run(torch_dev, N, ppc, nsteps):
     assert dx.max() < 1e-9 * Lk
     assert np.abs(v.cpu().numpy() - xo[3:]).max() < 1e-9
     assert np.abs(v.cpu().numpy().sum(axis=1) - xv[3:].sum(axis=1)).max() < 1e-11 * np.abs(xv[3:]).sum()
+
+
+def test_binned_equals_atomic_path_at_size(torch_dev):
+    """128^3 x 8 Landau particles, N = 128: the binned (tile) and the atomic paths of the PIF
+    solve agree to rounding (1e-11 of max |E|), and a particle count above np_max falls back."""
+    from paper_2605_05469_b200 import PifSolver
+
+    torch = torch_dev
+    Lk = 2 * np.pi / 0.5
+    xv = landau_state(128, 8, L=Lk, seed=31)
+    npart = xv.shape[1]
+    x = _x(torch, xv)
+    q = torch.full((npart,), -Lk ** 3 / npart, dtype=torch.float64, device="cuda")
+    Eb, Wb = PifSolver(128, Lk, 1e-4, np_max=npart).solve(x, q)
+    Ea, Wa = PifSolver(128, Lk, 1e-4).solve(x, q)
+    Es, Ws = PifSolver(128, Lk, 1e-4, np_max=npart // 2).solve(x, q)
+    scale = Ea.abs().max().item()
+    assert (Eb - Ea).abs().max().item() < 1e-11 * scale
+    assert np.allclose(Wb, Wa, rtol=1e-11) and np.allclose(Ws, Wa, rtol=1e-11)
