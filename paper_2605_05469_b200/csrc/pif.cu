@@ -349,6 +349,17 @@ __global__ void __launch_bounds__(32) k_spread_tiled(const double* __restrict__ 
     const int bx = bin % nb, by = (bin / nb) % nb, bz = bin / (nb * nb);
     const int ox = kB * bx - TL::H, oy = kB * by - TL::H, oz = kB * bz - TL::H;
     for (int i = lane; i < TL::N3; i += 32) tile[i] = 0.0;
+    // this lane's window points pp = lane + 32 i: tile offsets and packed (a, b, c), fixed for
+    // every particle (the per-particle part of the index is kb)
+    constexpr int NP = (W * W * W + 31) / 32;
+    int po[NP], pa[NP];
+#pragma unroll
+    for (int i = 0; i < NP; ++i) {
+        const int pp = min(lane + 32 * i, W * W * W - 1);
+        const int a = pp % W, b = (pp / W) % W, c = pp / (W * W);
+        po[i] = (c * T + b) * T + a;
+        pa[i] = a | (b << 8) | (c << 16);
+    }
     for (uint32_t base = beg; base < end; base += 32) {
         const uint32_t jj = base + lane;
         if (jj < end) {
@@ -362,13 +373,15 @@ __global__ void __launch_bounds__(32) k_spread_tiled(const double* __restrict__ 
         __syncwarp();
         const int cnt = (int)min(32u, end - base);
         for (int k = 0; k < cnt; ++k) {
-            const int kx = so[k * 3], ky = so[k * 3 + 1], kz = so[k * 3 + 2];
+            const int kb = (so[k * 3 + 2] * T + so[k * 3 + 1]) * T + so[k * 3];
             const double* w = sw + k * 3 * W;
 #pragma unroll
-            for (int pp = lane; pp < W * W * W; pp += 32) {
-                const int a = pp % W, b = (pp / W) % W, c = pp / (W * W);
-                double* t = tile + ((kz + c) * T + (ky + b)) * T + (kx + a);
-                *t += __dmul_rn(__dmul_rn(w[2 * W + c], w[W + b]), w[a]);
+            for (int i = 0; i < NP; ++i) {
+                if (i < NP - 1 || lane + 32 * i < W * W * W) {
+                    const int a = pa[i] & 0xff, b = (pa[i] >> 8) & 0xff, c = pa[i] >> 16;
+                    double* t = tile + kb + po[i];
+                    *t += __dmul_rn(__dmul_rn(w[2 * W + c], w[W + b]), w[a]);
+                }
             }
             __syncwarp();
         }
@@ -381,7 +394,7 @@ __global__ void __launch_bounds__(32) k_spread_tiled(const double* __restrict__ 
             gx = gx < 0 ? gx + M : (gx >= M ? gx - M : gx);
             gy = gy < 0 ? gy + M : (gy >= M ? gy - M : gy);
             gz = gz < 0 ? gz + M : (gz >= M ? gz - M : gz);
-            atomicAdd((double*)(G + ((int64_t)gz * M + gy) * M + gx), v);
+            atomicAdd(G + 2 * (((int64_t)gz * M + gy) * M + gx), v);   // real part of the interleaved complex
         }
     }
 }
