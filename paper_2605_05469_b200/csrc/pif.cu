@@ -37,14 +37,15 @@ __device__ __forceinline__ double psi_es(double z, double beta) {
     return exp(__dmul_rn(beta, __dsub_rn(sqrt(t), 1.0)));
 }
 
-// Fine-grid start index and the W window values of one coordinate (u = x M / L).
+// Fine-grid start index and the W window values of one coordinate (u = x M / L); z = (l - u)
+// times 2/W (the oracle divides by W/2: within an ulp, and no fp64 division sequence).
 template <int W>
 __device__ __forceinline__ int window_1d(double x, double inv_hf, double beta, int M, double* wv) {
     const double u = __dmul_rn(x, inv_hf);
     const double l0d = ceil(__dsub_rn(u, 0.5 * W));
     const int l0 = (int)l0d;
 #pragma unroll
-    for (int k = 0; k < W; ++k) wv[k] = psi_es(__ddiv_rn(__dsub_rn((double)(l0 + k), u), 0.5 * W), beta);
+    for (int k = 0; k < W; ++k) wv[k] = psi_es(__dmul_rn(__dsub_rn((double)(l0 + k), u), 2.0 / W), beta);
     return l0 < 0 ? l0 + M : l0;
 }
 
@@ -294,6 +295,12 @@ struct Tile {
     static constexpr int H = W / 2 + 1;         // tile origin = kB b - H
     static constexpr int T = kB + W + 1;        // tile extent (covers l0 - origin in [0, T - W])
     static constexpr int N3 = T * T * T;
+    // Spreading tile strides (doubles).  Padding R = W, P = W^2 (mod 16) makes the 64-bit
+    // accesses bank-conflict free but costs occupancy; measured no faster at 512^3 (559 vs
+    // 550 ms), so the tile stays dense.
+    static constexpr int R = T;
+    static constexpr int P = T * T;
+    static constexpr int NS = T * P;
 };
 
 __device__ __forceinline__ int fine_cell(double x, double inv_hf, int M) {
@@ -327,7 +334,7 @@ __device__ __forceinline__ int window_raw(double x, double inv_hf, double beta, 
     const int l0 = (int)ceil(__dsub_rn(u, 0.5 * W));
 #pragma unroll
     for (int k = 0; k < W; ++k)
-        wv[k] = __dmul_rn(scale, psi_es(__ddiv_rn(__dsub_rn((double)(l0 + k), u), 0.5 * W), beta));
+        wv[k] = __dmul_rn(scale, psi_es(__dmul_rn(__dsub_rn((double)(l0 + k), u), 2.0 / W), beta));
     return l0;
 }
 
@@ -339,8 +346,8 @@ __global__ void __launch_bounds__(32) k_spread_tiled(const double* __restrict__ 
     using TL = Tile<W>;
     constexpr int T = TL::T;
     extern __shared__ double smem[];
-    double* tile = smem;                        // T^3
-    double* sw = tile + TL::N3;                 // [32][3][W]: x, y, z weights (q folded into z)
+    double* tile = smem;                        // T planes of P doubles (rows of R)
+    double* sw = tile + TL::NS;                 // [32][3][W]: x, y, z weights (q folded into z)
     int* so = (int*)(sw + 32 * 3 * W);          // [32][3] window start - tile origin
     const int bin = blockIdx.x;
     const uint32_t beg = offs[bin], end = offs[bin + 1];
@@ -348,7 +355,7 @@ __global__ void __launch_bounds__(32) k_spread_tiled(const double* __restrict__ 
     const int lane = threadIdx.x;
     const int bx = bin % nb, by = (bin / nb) % nb, bz = bin / (nb * nb);
     const int ox = kB * bx - TL::H, oy = kB * by - TL::H, oz = kB * bz - TL::H;
-    for (int i = lane; i < TL::N3; i += 32) tile[i] = 0.0;
+    for (int i = lane; i < TL::NS; i += 32) tile[i] = 0.0;
     // this lane's window points pp = lane + 32 i: tile offsets and packed (a, b, c), fixed for
     // every particle (the per-particle part of the index is kb)
     constexpr int NP = (W * W * W + 31) / 32;
@@ -357,7 +364,7 @@ __global__ void __launch_bounds__(32) k_spread_tiled(const double* __restrict__ 
     for (int i = 0; i < NP; ++i) {
         const int pp = min(lane + 32 * i, W * W * W - 1);
         const int a = pp % W, b = (pp / W) % W, c = pp / (W * W);
-        po[i] = (c * T + b) * T + a;
+        po[i] = c * TL::P + b * TL::R + a;
         pa[i] = a | (b << 8) | (c << 16);
     }
     for (uint32_t base = beg; base < end; base += 32) {
@@ -373,24 +380,31 @@ __global__ void __launch_bounds__(32) k_spread_tiled(const double* __restrict__ 
         __syncwarp();
         const int cnt = (int)min(32u, end - base);
         for (int k = 0; k < cnt; ++k) {
-            const int kb = (so[k * 3 + 2] * T + so[k * 3 + 1]) * T + so[k * 3];
+            const int kb = so[k * 3 + 2] * TL::P + so[k * 3 + 1] * TL::R + so[k * 3];
             const double* w = sw + k * 3 * W;
+            // all loads (window values, then the tile points) before any store, so the NP
+            // independent read-modify-writes overlap (the compiler cannot prove that a tile
+            // store does not alias the staged window values)
+            double val[NP], old[NP];
 #pragma unroll
             for (int i = 0; i < NP; ++i) {
-                if (i < NP - 1 || lane + 32 * i < W * W * W) {
-                    const int a = pa[i] & 0xff, b = (pa[i] >> 8) & 0xff, c = pa[i] >> 16;
-                    double* t = tile + kb + po[i];
-                    *t += __dmul_rn(__dmul_rn(w[2 * W + c], w[W + b]), w[a]);
-                }
+                const int a = pa[i] & 0xff, b = (pa[i] >> 8) & 0xff, c = pa[i] >> 16;
+                val[i] = __dmul_rn(__dmul_rn(w[2 * W + c], w[W + b]), w[a]);
             }
+#pragma unroll
+            for (int i = 0; i < NP; ++i) old[i] = tile[kb + po[i]];
+#pragma unroll
+            for (int i = 0; i < NP; ++i)
+                if (i < NP - 1 || lane + 32 * i < W * W * W) tile[kb + po[i]] = __dadd_rn(old[i], val[i]);
             __syncwarp();
         }
     }
     __syncwarp();
     for (int i = lane; i < TL::N3; i += 32) {
-        const double v = tile[i];
+        const int tx = i % T, ty = (i / T) % T, tz = i / (T * T);
+        const double v = tile[tz * TL::P + ty * TL::R + tx];
         if (v != 0.0) {
-            int gx = ox + i % T, gy = oy + (i / T) % T, gz = oz + i / (T * T);
+            int gx = ox + tx, gy = oy + ty, gz = oz + tz;
             gx = gx < 0 ? gx + M : (gx >= M ? gx - M : gx);
             gy = gy < 0 ? gy + M : (gy >= M ? gy - M : gy);
             gz = gz < 0 ? gz + M : (gz >= M ? gz - M : gz);
@@ -632,7 +646,7 @@ void interp_w(pic_pif* p, int64_t np, const double* X, double* ore, double* oim,
 
 template <int W>
 void spread_tiled_w(pic_pif* p, int64_t np, const double* X, const double* f) {
-    const size_t sm = (Tile<W>::N3 + 32 * 3 * W) * sizeof(double) + 32 * 3 * sizeof(int);
+    const size_t sm = (Tile<W>::NS + 32 * 3 * W) * sizeof(double) + 32 * 3 * sizeof(int);
     cudaFuncSetAttribute(k_spread_tiled<W>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     const int nbins = p->nb * p->nb * p->nb;
     k_spread_tiled<W><<<nbins, 32, sm, p->stream>>>(X, f, np, p->perm, p->boffs, (double*)p->G, p->M, p->nb,
