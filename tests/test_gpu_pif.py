@@ -164,3 +164,30 @@ def test_binned_equals_atomic_path_at_size(torch_dev):
     scale = Ea.abs().max().item()
     assert (Eb - Ea).abs().max().item() < 1e-11 * scale
     assert np.allclose(Wb, Wa, rtol=1e-11) and np.allclose(Ws, Wa, rtol=1e-11)
+
+
+def test_pif_landau_damping_rate():
+    """P:140-146, P:231-232 with the PIF scheme: 16^3 modes, 128^3 x 8 Landau
+    particles (alpha = 0.05), backward half kick, 260 steps of pic_pif_step: the slope of the
+    W_x peaks for t <= 12 within 10% of 2 gamma of the dispersion relation and their spacing
+    within 5% of pi / omega_r (D#20, D#21)."""
+    from landau_fit import dispersion_root, fit_damping_rate
+    from paper_2605_05469_b200 import PifSolver
+
+    torch = torch_dev
+    Lk = 2 * np.pi / 0.5
+    xv = landau_state(128, 8, L=Lk, seed=41)
+    npart = xv.shape[1]
+    x = torch.from_numpy(np.ascontiguousarray(xv[:3])).cuda()
+    v = torch.from_numpy(np.ascontiguousarray(xv[3:])).cuda()
+    q = torch.full((npart,), -Lk ** 3 / npart, dtype=torch.float64, device="cuda")
+    P = PifSolver(16, Lk, 1e-4, np_max=npart)
+    E, _ = P.solve(x, q)
+    v -= (-1.0) * 0.5 * 0.05 * E          # v_{-1/2} = v_0 - (q/m) dt/2 E(x_0) (D#9)
+    ex = P.step(x, v, q, nsteps=260, qm=-1.0, dt=0.05)
+    w = dispersion_root(0.5)
+    t = np.arange(260) * 0.05
+    slope, npk, tp = fit_damping_rate(t, ex, t_max=12.0)
+    assert npk >= 5
+    assert abs(slope - 2 * w.imag) < 0.10 * abs(2 * w.imag), slope
+    assert abs(np.mean(np.diff(tp)) - np.pi / w.real) < 0.05 * np.pi / w.real
