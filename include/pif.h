@@ -33,8 +33,10 @@ typedef struct pic_pif pic_pif;
 
 /* Workspace bytes for modes N, domain length L, accuracy eps and up to np_max particles per
  * call (creates and destroys a cuFFT plan to learn its scratch size: needs a CUDA device).
- * np_max > 0 reserves the binned path (4 B per particle + 12 B per bin of 8^3 fine cells):
- * particles counting-sorted into bins, spreading through shared-memory tiles; it applies
+ * np_max > 0 reserves the binned path (4 B per particle + 12 B per bin of 8^3 fine cells, and
+ * a second M^3 complex fine grid so the PIF solve gathers E_x, E_y, E_z in one pass;
+ * PIC_PIF_SPLIT_INTERP=1 keeps two passes): particles counting-sorted into bins, spreading
+ * and interpolation through shared-memory tiles; it applies
  * when 2N is a multiple of 8 and w <= 8 (eps >= 1e-6) and np <= np_max (else, or with
  * PIC_PIF_BINNED=0 in the environment, one global atomic per window point).  PIC_EINVAL: N
  * odd or out of [8, 1024], L <= 0, eps outside [1e-14, 1), np_max outside [0, 2^32). */

@@ -314,7 +314,11 @@ __global__ void __launch_bounds__(kThreads) k_bin_count(int64_t np, const double
     if (j >= np) return;
     const int bx = fine_cell(X[j], inv_hf, M) / kB, by = fine_cell(X[np + j], inv_hf, M) / kB,
               bz = fine_cell(X[2 * np + j], inv_hf, M) / kB;
-    atomicAdd(cnt + ((int64_t)bz * nb + by) * nb + bx, 1u);
+    const uint32_t bin = (uint32_t)(((int64_t)bz * nb + by) * nb + bx);
+    // warp-aggregated: one atomic per distinct bin among the warp's active lanes
+    const unsigned act = __activemask();
+    const unsigned grp = __match_any_sync(act, bin);
+    if ((threadIdx.x & 31) == __ffs(grp) - 1) atomicAdd(cnt + bin, (uint32_t)__popc(grp));
 }
 
 __global__ void __launch_bounds__(kThreads) k_bin_place(int64_t np, const double* __restrict__ X, int M, int nb,
@@ -324,7 +328,18 @@ __global__ void __launch_bounds__(kThreads) k_bin_place(int64_t np, const double
     if (j >= np) return;
     const int bx = fine_cell(X[j], inv_hf, M) / kB, by = fine_cell(X[np + j], inv_hf, M) / kB,
               bz = fine_cell(X[2 * np + j], inv_hf, M) / kB;
-    perm[atomicAdd(cursor + ((int64_t)bz * nb + by) * nb + bx, 1u)] = (uint32_t)j;
+    const uint32_t bin = (uint32_t)(((int64_t)bz * nb + by) * nb + bx);
+    // warp-aggregated and order-preserving inside the warp: the lanes of one bin take
+    // consecutive slots in lane order, so runs of particles that are contiguous in memory stay
+    // contiguous in the bin (coalesced particle reads in the spread / gather)
+    const unsigned act = __activemask();
+    const unsigned grp = __match_any_sync(act, bin);
+    const int lane = threadIdx.x & 31;
+    const int leader = __ffs(grp) - 1;
+    uint32_t base = 0;
+    if (lane == leader) base = atomicAdd(cursor + bin, (uint32_t)__popc(grp));
+    base = __shfl_sync(grp, base, leader);
+    perm[base + __popc(grp & ((1u << lane) - 1u))] = (uint32_t)j;
 }
 
 // Unwrapped window start and the W values of one coordinate (the same arithmetic as window_1d).
@@ -467,6 +482,71 @@ __global__ void __launch_bounds__(128) k_interp_tiled(const double* __restrict__
     }
 }
 
+
+// PIF gather of all three components in one pass (binned path): tile of G1 = E_x + i E_y
+// (complex) and of the real part of G2 = E_z; the window is computed once per particle.
+template <int W>
+__global__ void __launch_bounds__(256) k_interp3_tiled(const double* __restrict__ X, int64_t np,
+                                                       const uint32_t* __restrict__ perm,
+                                                       const uint32_t* __restrict__ offs,
+                                                       const double2* __restrict__ G1,
+                                                       const double2* __restrict__ G2, int M, int nb,
+                                                       double inv_hf, double beta, double* __restrict__ E,
+                                                       double scale) {
+    using TL = Tile<W>;
+    constexpr int T = TL::T;
+    extern __shared__ double2 g1[];             // T^3 complex, then T^3 real
+    double* g2 = (double*)(g1 + TL::N3);
+    const int bin = blockIdx.x;
+    const uint32_t beg = offs[bin], end = offs[bin + 1];
+    if (beg == end) return;
+    const int bx = bin % nb, by = (bin / nb) % nb, bz = bin / (nb * nb);
+    const int ox = kB * bx - TL::H, oy = kB * by - TL::H, oz = kB * bz - TL::H;
+    for (int i = threadIdx.x; i < TL::N3; i += blockDim.x) {
+        int gx = ox + i % T, gy = oy + (i / T) % T, gz = oz + i / (T * T);
+        gx = gx < 0 ? gx + M : (gx >= M ? gx - M : gx);
+        gy = gy < 0 ? gy + M : (gy >= M ? gy - M : gy);
+        gz = gz < 0 ? gz + M : (gz >= M ? gz - M : gz);
+        const int64_t gi = ((int64_t)gz * M + gy) * M + gx;
+        g1[i] = __ldg(G1 + gi);
+        g2[i] = __ldg((const double*)(G2 + gi));
+    }
+    __syncthreads();
+    for (uint32_t jj = beg + threadIdx.x; jj < end; jj += blockDim.x) {
+        const int64_t j = perm[jj];
+        double wx[W], wy[W], wz[W];
+        const int kx = window_raw<W>(X[j], inv_hf, beta, wx, 1.0) - ox;
+        const int ky = window_raw<W>(X[np + j], inv_hf, beta, wy, 1.0) - oy;
+        const int kz = window_raw<W>(X[2 * np + j], inv_hf, beta, wz, 1.0) - oz;
+        double sr = 0.0, si = 0.0, sz = 0.0;
+#pragma unroll 1
+        for (int c = 0; c < W; ++c) {
+            double yr = 0.0, yi = 0.0, yz = 0.0;
+#pragma unroll
+            for (int b = 0; b < W; ++b) {
+                const int r = ((kz + c) * T + (ky + b)) * T + kx;
+                double xr = 0.0, xi = 0.0, xz = 0.0;
+#pragma unroll
+                for (int a = 0; a < W; ++a) {
+                    const double2 v = g1[r + a];
+                    xr = fma(v.x, wx[a], xr);
+                    xi = fma(v.y, wx[a], xi);
+                    xz = fma(g2[r + a], wx[a], xz);
+                }
+                yr = fma(xr, wy[b], yr);
+                yi = fma(xi, wy[b], yi);
+                yz = fma(xz, wy[b], yz);
+            }
+            sr = fma(yr, wz[c], sr);
+            si = fma(yi, wz[c], si);
+            sz = fma(yz, wz[c], sz);
+        }
+        E[j] = sr * scale;
+        E[np + j] = si * scale;
+        E[2 * np + j] = sz * scale;
+    }
+}
+
 inline size_t align256(size_t b) { return (b + 255) & ~(size_t)255; }
 
 }  // namespace
@@ -477,6 +557,7 @@ struct pic_pif {
     cufftHandle plan;
     cudaStream_t stream;
     double2* G;          // fine grid M^3
+    double2* G2;         // second fine grid (binned PIF solve: E_z), or null
     double2* A;          // N^3 spectrum (E^_x + i E^_y)
     double2* Bz;         // N^3 spectrum (E^_z)
     double* dinv;        // N: 1 / psi^
@@ -488,6 +569,7 @@ struct pic_pif {
     int64_t np_max;      // binned path capacity (0: atomic path only)
     int nb;              // bins per dimension (M / kB)
     bool binned;         // binned spread / interp in use
+    bool split_interp;   // PIC_PIF_SPLIT_INTERP=1: two gather passes (E_x + i E_y, then E_z)
     uint32_t* bcnt;      // nb^3 + 1 counts -> offsets
     uint32_t* boffs;     // nb^3 + 1 offsets (exclusive scan)
     uint32_t* bcur;      // nb^3 cursors
@@ -523,7 +605,7 @@ pic_status make_plan(int M, cufftHandle* plan, size_t* work) {
 }
 
 struct Layout {
-    size_t G, A, Bz, dinv, partials, energy, hist, work, bcnt, boffs, bcur, perm, scan, total;
+    size_t G, A, Bz, dinv, partials, energy, hist, work, bcnt, boffs, bcur, perm, scan, G2, total;
 };
 bool binnable(int n, int w) { return (2 * n) % kB == 0 && w <= 8; }
 size_t scan_tmp_bytes(int64_t nbins) {
@@ -549,6 +631,7 @@ Layout layout(int n, size_t fft_work, int64_t np_max, int w) {
     o.bcur = off;     off += nbins ? align256(nbins * 4) : 0;
     o.perm = off;     off += nbins ? align256((size_t)np_max * 4) : 0;
     o.scan = off;     off += nbins ? align256(scan_tmp_bytes(nbins + 1)) : 0;
+    o.G2 = off;       off += nbins ? align256(M * M * M * sizeof(double2)) : 0;
     o.total = off;
     return o;
 }
@@ -660,6 +743,14 @@ void interp_tiled_w(pic_pif* p, int64_t np, const double* X, double* ore, double
     k_interp_tiled<W><<<nbins, 128, sm, p->stream>>>(X, np, p->perm, p->boffs, p->G, p->M, p->nb, p->inv_hf,
                                                      p->beta, ore, oim, os, sc);
 }
+template <int W>
+void interp3_tiled_w(pic_pif* p, int64_t np, const double* X, double* E, double sc) {
+    const size_t sm = Tile<W>::N3 * (sizeof(double2) + sizeof(double));
+    cudaFuncSetAttribute(k_interp3_tiled<W>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    const int nbins = p->nb * p->nb * p->nb;
+    k_interp3_tiled<W><<<nbins, 256, sm, p->stream>>>(X, np, p->perm, p->boffs, p->G, p->G2, p->M, p->nb,
+                                                      p->inv_hf, p->beta, E, sc);
+}
 #define PIF_W_SWITCH_SMALL(w, F, ...)                \
     switch (w) {                                     \
         case 3: F<3>(__VA_ARGS__); break;            \
@@ -708,16 +799,17 @@ pic_status spread(pic_pif* p, int64_t np, const double* X, const double* f) {
     return PIC_OK;
 }
 
-pic_status fft(pic_pif* p, int dir) {
+pic_status fft(pic_pif* p, int dir, double2* grid = nullptr) {
     Stage t(p, PIC_PIF_FFT);
-    PIF_FFT(p, cufftExecZ2Z(p->plan, (cufftDoubleComplex*)p->G, (cufftDoubleComplex*)p->G, dir));
+    double2* g = grid ? grid : p->G;
+    PIF_FFT(p, cufftExecZ2Z(p->plan, (cufftDoubleComplex*)g, (cufftDoubleComplex*)g, dir));
     return PIC_OK;
 }
 
-pic_status fill(pic_pif* p, const double2* S) {
+pic_status fill(pic_pif* p, const double2* S, double2* grid = nullptr) {
     Stage t(p, PIC_PIF_FILL);
     const int64_t nf = (int64_t)p->M * p->M * p->M;
-    k_fill<<<stream_grid(nf), kThreads, 0, p->stream>>>(p->n, p->M, S, p->dinv, p->G);
+    k_fill<<<stream_grid(nf), kThreads, 0, p->stream>>>(p->n, p->M, S, p->dinv, grid ? grid : p->G);
     PIF_LAUNCHED(p);
     return PIC_OK;
 }
@@ -805,11 +897,14 @@ pic_status pic_pif_create(int32_t n, double length, double eps, int64_t np_max, 
     {
         const char* e = getenv("PIC_PIF_BINNED");
         const bool use = (np_max > 0 && binnable(n, p->w)) && !(e && e[0] == '0');
+        const char* si = getenv("PIC_PIF_SPLIT_INTERP");
+        p->split_interp = si && si[0] == '1';
         p->np_max = use ? np_max : 0;
         p->bcnt = use ? (uint32_t*)(b + o.bcnt) : nullptr;
         p->boffs = use ? (uint32_t*)(b + o.boffs) : nullptr;
         p->bcur = use ? (uint32_t*)(b + o.bcur) : nullptr;
         p->perm = use ? (uint32_t*)(b + o.perm) : nullptr;
+        p->G2 = use ? (double2*)(b + o.G2) : nullptr;
         p->scan_tmp = use ? (void*)(b + o.scan) : nullptr;
         const int64_t nbins = (int64_t)p->nb * p->nb * p->nb;
         p->scan_bytes = use ? scan_tmp_bytes(nbins + 1) : 0;
@@ -875,6 +970,16 @@ pic_status solve_core(pic_pif* p, int64_t np, const double* x, const double* q, 
         PIF_LAUNCHED(p);
     }
     const double sc = 1.0 / (p->L * p->L * p->L);                           // D#35
+    if (p->binned && p->G2 && !p->split_interp) {                          // one gather pass
+        if (pic_status s = fill(p, p->A)) return s;                         // E_x + i E_y -> G
+        if (pic_status s = fft(p, CUFFT_INVERSE)) return s;
+        if (pic_status s = fill(p, p->Bz, p->G2)) return s;                 // E_z -> G2
+        if (pic_status s = fft(p, CUFFT_INVERSE, p->G2)) return s;
+        Stage t(p, PIC_PIF_INTERP);
+        PIF_W_SWITCH_SMALL(p->w, interp3_tiled_w, p, np, x, E, sc);
+        PIF_LAUNCHED(p);
+        return PIC_OK;
+    }
     if (pic_status s = fill(p, p->A)) return s;                             // E_x + i E_y
     if (pic_status s = fft(p, CUFFT_INVERSE)) return s;
     if (pic_status s = interp(p, np, x, E, E + np, 1, sc)) return s;

@@ -191,3 +191,21 @@ def test_pif_landau_damping_rate():
     assert npk >= 5
     assert abs(slope - 2 * w.imag) < 0.10 * abs(2 * w.imag), slope
     assert abs(np.mean(np.diff(tp)) - np.pi / w.real) < 0.05 * np.pi / w.real
+
+
+def test_one_pass_gather_equals_two_pass(torch_dev, monkeypatch):
+    """Binned PIF solve: the one-pass gather of (E_x + i E_y, E_z) from two fine grids equals
+    the two-pass gather (PIC_PIF_SPLIT_INTERP=1) to rounding."""
+    from paper_2605_05469_b200 import PifSolver
+
+    torch = torch_dev
+    Lk = 2 * np.pi / 0.5
+    xv = landau_state(32, 8, L=Lk, seed=43)
+    npart = xv.shape[1]
+    x = _x(torch, xv)
+    q = torch.full((npart,), -Lk ** 3 / npart, dtype=torch.float64, device="cuda")
+    E1, W1 = PifSolver(32, Lk, 1e-4, np_max=npart).solve(x, q)
+    monkeypatch.setenv("PIC_PIF_SPLIT_INTERP", "1")
+    E2, W2 = PifSolver(32, Lk, 1e-4, np_max=npart).solve(x, q)
+    assert (E1 - E2).abs().max().item() <= 1e-13 * E2.abs().max().item()
+    assert np.allclose(W1, W2, rtol=1e-13)
