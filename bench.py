@@ -412,14 +412,17 @@ def run_ours(args, rank, world):
 
 
 # ------------------------------------------------------------ PIF arm (NEXT-2) --
-# Algorithmic bytes: spread reads x, y, z, q (32 B) per particle and writes the
-# M^3 complex fine grid once (16 B per fine point, the memset included); interp reads x, y, z
-# (24 B) and writes 16 B (E_x, E_y pass) or 8 B (E_z pass) per particle and reads the grid
-# once (16 B per fine point); push reads x, v, E and writes x, v (120 B) per particle.
-def pif_alg_bytes(stage: str, npart: int, n: int) -> float:
+# Algorithmic bytes per launch: spread reads x, y, z, q and its perm entry (36 B)
+# per particle and writes the M^3 complex fine grid once (16 B per fine point, the memset
+# included); the one-pass gather reads x, y, z and perm (28 B), writes E (24 B) per particle
+# and reads the two fine grids once (16 + 8 B per fine point) -- the two-pass gather, per
+# launch, 28 + 12 B per particle and 16 B per fine point; push reads x, v, E and writes x, v
+# (120 B) per particle; bin: x, y, z read twice + perm written (52 B) per particle.
+def pif_alg_bytes(stage: str, npart: int, n: int, launches_per_step: float = 1.0) -> float:
     M3 = (2 * n) ** 3
-    return {"spread": 32 * npart + 16 * M3, "interp": 24 * npart + 12 * npart + 16 * M3,
-            "push": 120 * npart, "fill": 16 * M3, "modes": 48 * n ** 3}.get(stage, 0.0)
+    interp = (52 * npart + 24 * M3) if launches_per_step <= 1 else (40 * npart + 16 * M3)
+    return {"spread": 36 * npart + 16 * M3, "interp": interp, "push": 120 * npart,
+            "fill": 16 * M3, "modes": 48 * n ** 3, "bin": 52 * npart}.get(stage, 0.0)
 
 
 def run_pif(args, rank, world):
@@ -502,11 +505,11 @@ def run_pif(args, rank, world):
         if nl:
             per = 2   # steps of the split pass
             stages[k] = {"ms_per_step": t / per, "launches_per_step": nl / per,
-                         "alg_GBps": pif_alg_bytes(k, npart, n) * (nl / per) / (t / per / 1e3) / 1e9
+                         "alg_GBps": pif_alg_bytes(k, npart, n, nl / per) * (nl / per) / (t / per / 1e3) / 1e9
                          if k != "fft" else None}
     dom = max((k for k in stages if k != "fft"), key=lambda k: stages[k]["ms_per_step"])
     per_launch_ms = stages[dom]["ms_per_step"] / stages[dom]["launches_per_step"]
-    alg = pif_alg_bytes(dom, npart, n)
+    alg = pif_alg_bytes(dom, npart, n, stages[dom]["launches_per_step"])
     peaks = measured_peaks()
     peak = peaks.get("hbm_gbs") or 6650.0
     roof = {"bound": "hbm", "kernel": dom, "achieved": alg / (per_launch_ms / 1e3) / 1e9, "peak": peak,
@@ -514,8 +517,10 @@ def run_pif(args, rank, world):
             "traffic": ncu_traffic(f"pif_{n}^3x{ppc}", dom),
             "peak_source": "measured (MEASURED_PEAKS.json hbm_gbs)" if peaks.get("hbm_gbs") else "fallback 6650 GB/s",
             "alg_bytes_per_launch": alg,
-            "note": "the window spreading is bound by fp64 L2 atomics (w^3 = 216 per particle), not by "
-                    "its algorithmic HBM bytes; see DESIGN §6f"}
+            "note": "the binned spread / gather are bound by shared-memory wavefronts (ncu: L1/shared "
+                    "89% of peak for the gather, W^3 = 216 window points per particle), not by their "
+                    "algorithmic HBM bytes; traffic well above algorithmic = particle reads / E writes "
+                    "through perm once the particles have moved; see DESIGN §6f"}
     cpu = None
     if not args.no_cpu_baseline:
         from oracle import nufft as U

@@ -166,7 +166,7 @@ def test_binned_equals_atomic_path_at_size(torch_dev):
     assert np.allclose(Wb, Wa, rtol=1e-11) and np.allclose(Ws, Wa, rtol=1e-11)
 
 
-def test_pif_landau_damping_rate():
+def test_pif_landau_damping_rate(torch_dev):
     """P:140-146, P:231-232 with the PIF scheme: 16^3 modes, 128^3 x 8 Landau
     particles (alpha = 0.05), backward half kick, 260 steps of pic_pif_step: the slope of the
     W_x peaks for t <= 12 within 10% of 2 gamma of the dispersion relation and their spacing
