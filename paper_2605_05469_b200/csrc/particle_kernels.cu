@@ -547,23 +547,26 @@ __global__ void __launch_bounds__(kThreads) k_place(const uint32_t* __restrict__
     // peer-memory transport: the entry count is on the device, and a sorted position
     // beyond the arrays (a slab over capacity) is dropped and flagged
     if (dcnt) np = min(np, (int64_t)(dcnt[DC_N] + dcnt[DC_ARR]));
-    const int64_t i0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * 4;
-    if (i0 >= np) return;
-    auto put = [&](uint32_t k, uint32_t r, int64_t i) {
-        if (k == kNoKey) return;
-        const uint32_t pos = __ldg(offs + k) + r;
-        if (pos < (uint64_t)cap) perm[pos] = (uint32_t)i;
+    // Consecutive lanes take consecutive particles (four strided passes per CTA), so a
+    // warp's 32 perm stores land in the ~4 cells those particles arrive in: a handful of
+    // 32-B sectors per store instruction instead of ~16 with four particles per thread
+    // (ncu: the old mapping was L2-request bound at 74% L2 throughput, 1.6 TB/s DRAM).
+    const int64_t base = (int64_t)blockIdx.x * (4 * kThreads) + threadIdx.x;
+    uint32_t k[4], r[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        const int64_t i = base + q * kThreads;
+        k[q] = i < np ? __ldg(key + i) : kNoKey;
+        r[q] = i < np ? __ldg(rank + i) : 0u;
+    }
+    uint32_t pos[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) pos[q] = k[q] == kNoKey ? 0u : __ldg(offs + k[q]) + r[q];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        if (k[q] == kNoKey) continue;
+        if (pos[q] < (uint64_t)cap) perm[pos[q]] = (uint32_t)(base + q * kThreads);
         else atomicExch(err + 2, 1);
-    };
-    if (i0 + 4 <= np) {
-        const uint4 k4 = __ldg(reinterpret_cast<const uint4*>(key + i0));
-        const uint2 r4 = __ldg(reinterpret_cast<const uint2*>(rank + i0));
-        put(k4.x, r4.x & 0xffffu, i0);
-        put(k4.y, r4.x >> 16, i0 + 1);
-        put(k4.z, r4.y & 0xffffu, i0 + 2);
-        put(k4.w, r4.y >> 16, i0 + 3);
-    } else {
-        for (int64_t i = i0; i < np; ++i) put(__ldg(key + i), __ldg(rank + i), i);
     }
 }
 
