@@ -632,13 +632,19 @@ __device__ __forceinline__ int chunk_end(const uint32_t* soffs, int ca, int cap)
 // index) -- the order of the single-domain oracle's global stable sort (D#15).
 // Chunk capacity (particles staged per pass; a brick holds ~ppc * 256): 1344 lets
 // three CTAs share an SM, which measured faster than two with whole-brick chunks.
+#ifndef PIC_RD_CAP
+#define PIC_RD_CAP 1344
+#endif
+#ifndef PIC_RD_MINB
+#define PIC_RD_MINB 3
+#endif
 template <bool MR>
 struct ReorderCap {
-    static constexpr int value = MR ? 1248 : 1344;   // MR: + the slot -> entry array
+    static constexpr int value = MR ? PIC_RD_CAP * 13 / 14 : PIC_RD_CAP;   // MR: + the slot -> entry array
 };
 
 template <bool PUSH, bool MR>
-__global__ void __launch_bounds__(kThreads, 3) k_reorder_deposit(
+__global__ void __launch_bounds__(kThreads, PIC_RD_MINB) k_reorder_deposit(
     Geom g, const uint32_t* __restrict__ offs, const uint32_t* __restrict__ perm, PState cur,
     const double2* __restrict__ recv, int64_t n_old, const unsigned long long* __restrict__ dcnt, PState nxt,
     double* __restrict__ rho, double* ghost, int* __restrict__ err) {
