@@ -234,6 +234,14 @@ __host__ __device__ inline int x_rows(int n) { int r = 2048 / (n / 2); return r 
 __host__ __device__ inline int xi_rows(int n) { int r = 512 / (n / 2); return r < 1 ? 1 : r; }
 __host__ __device__ constexpr int y_tw(int n) { int t = 2048 / n; return t > 8 ? 8 : (t < 1 ? 1 : t); }
 __host__ __device__ constexpr int z_tw(int n) { int t = 2048 / n; return t > 8 ? 8 : (t < 1 ? 1 : t); }
+// columns per z-pass tile (compile-time knob for A/B: -DPIC_ZMUL_TWN=1024 halves the tile)
+#ifndef PIC_ZMUL_TWN
+#define PIC_ZMUL_TWN 2048
+#endif
+#ifndef PIC_ZMUL_MINB
+#define PIC_ZMUL_MINB 2
+#endif
+__host__ __device__ constexpr int zmul_tw(int n) { int t = PIC_ZMUL_TWN / n; return t > 8 ? 8 : (t < 1 ? 1 : t); }
 
 // Every pass is a persistent loop over tiles (grid = resident CTAs): the input of
 // tile t + gridDim is copied into the shared input buffer with cp.async as soon as
@@ -387,11 +395,11 @@ __global__ void __launch_bounds__(kThreads, 2) k_fft_y(Geom g, SpecLayout sl, Sp
 // components PACKED [q][c][zl][yl][px] (q = z / nzl) for the return transpose (or
 // REMOTE).
 template <int LOGN>
-__global__ void __launch_bounds__(kThreads, 2) k_fft_z_mul(Geom g, const double2* __restrict__ pencil,
+__global__ void __launch_bounds__(kThreads, PIC_ZMUL_MINB) k_fft_z_mul(Geom g, const double2* __restrict__ pencil,
                                                            SpecLayout out, double scale,
                                                            const double2* __restrict__ tw) {
     extern __shared__ double2 smx[];
-    constexpr int n = 1 << LOGN, TW = z_tw(n);
+    constexpr int n = 1 << LOGN, TW = zmul_tw(n);
     constexpr int ls = col_stride(n, TW);
     const int nyl = n / g.P;
     double2* in = smx;               // [n][TW]
@@ -681,7 +689,7 @@ void launch_fft_y_field(const Geom& g, SpecLayout src, SpecLayout dst, const dou
 
 void launch_fft_z_mul(const Geom& g, const double2* pencil, SpecLayout out, double scale,
                       const double2* tw, cudaStream_t s) {
-    const int TW = z_tw(g.n), ntiles = (g.n / 2 + 1 + TW - 1) / TW;
+    const int TW = zmul_tw(g.n), ntiles = (g.n / 2 + 1 + TW - 1) / TW;
     const size_t smem = sizeof(double2) * (size_t)TW * (g.n + 2 * col_stride(g.n, TW));
     const int64_t nt = (int64_t)(g.n / g.P) * ntiles;
     // one tile per CTA: the pass is bound by its four transforms, not its input
