@@ -41,6 +41,24 @@ def test_uniforms_are_53bit_grid_and_counter_based():
     assert not np.array_equal(u, O.uniforms(8, 12345))
 
 
+def test_uniforms_word_layout_matches_random123_kat():
+    """SURVEY c.1 Init 1 / D#10: (seed 0, particle j 0, block b 0) is the first Random123
+    vector (counter 0, key 0 -> r0..r3, golden/philox4x32_10_kat.txt), so u_0 and u_1 must
+    be ((r0 | r1 << 32) >> 11) 2^-53 and ((r2 | r3 << 32) >> 11) 2^-53.  A swapped word
+    order, a wrong shift or a dropped high word fails here."""
+    rows = [l.split() for l in open(os.path.join(GOLDEN, "philox4x32_10_kat.txt"))
+            if l.strip() and not l.startswith("#")]
+    r = [int(t, 16) for t in rows[0][6:10]]
+    assert [int(t, 16) for t in rows[0][:6]] == [0] * 6
+    u = O.uniforms(0, 0)
+    w0 = r[0] | (r[1] << 32)
+    w1 = r[2] | (r[3] << 32)
+    assert u[0] == (w0 >> 11) * 2.0 ** -53
+    assert u[1] == (w1 >> 11) * 2.0 ** -53
+    # written out from the published words: 0xe169c58d6627e8d5 >> 11, 0x9b00dbd8bc57ac4c >> 11
+    assert u[0] == 0x1C2D38B1ACC4FD * 2.0 ** -53 and u[1] == 0x13601B7B178AF5 * 2.0 ** -53
+
+
 def test_sampler_alpha0_is_uniform_ks():
     """alpha = 0 degenerates to uniform; KS below the 1% critical value."""
     xv = O.sample_landau(200_000, K, L, 0.0, 3)
@@ -311,6 +329,36 @@ def test_push_free_streaming_and_constant_kick():
     Ep[0] = 1.0
     out = O.push(L, xv, Ep, -0.05, 0.05)                 # q/m = -1 => v_x decreases by dt
     np.testing.assert_allclose(out[3], xv[3] - 0.05, rtol=0, atol=1e-15)
+
+
+def test_half_kick_single_mode_closed_form():
+    """S:180 / D#9: the backward half kick is v_{-1/2} = v_0 - (q/m) E(x_0) dt/2 = v_0 + E dt/2.
+
+    Particles sit exactly on the nodes of a 16^3 grid, c_i = 2 + cos(pi i_x / 2) of them on
+    every node of x-plane i_x (integers 3, 2, 1, 2), so the CIC deposit is exactly
+    rho = (q/h^3)(2 + cos(k4 x)) with k4 = 2 pi 4 / L and q = -L^3/N_p = -h^3/2.
+    The k = 0 mode is removed, so E_x = -(1/2) sin(k4 x)/k4 and E_y = E_z = 0
+    (P:175 with D#8), and a particle on a node gathers its node's value exactly.  Hence
+    v_x changes by -(dt/4) sin(k4 x)/k4: a sign slip or a missing 1/2 fails here."""
+    n, dt = 16, 0.05
+    h = L / n
+    pos = []
+    for iz in range(n):
+        for iy in range(n):
+            for ix in range(n):
+                c = 2 + [1, 0, -1, 0][ix % 4]
+                pos += [(ix * h, iy * h, iz * h)] * c
+    pos = np.array(pos).T
+    assert pos.shape[1] == 2 * n ** 3
+    rng = np.random.default_rng(3)
+    xv = np.concatenate([pos, rng.standard_normal((3, pos.shape[1]))])
+    out = O.half_kick(n, L, dt, xv)
+    assert np.array_equal(out[:3], xv[:3])                       # x unchanged
+    k4 = 2 * np.pi * 4 / L
+    ex = -0.5 * np.sin(k4 * xv[0]) / k4
+    np.testing.assert_allclose(out[3] - xv[3], ex * dt / 2, rtol=0, atol=1e-13)
+    np.testing.assert_allclose(out[4:] - xv[4:], 0.0, rtol=0, atol=1e-13)
+    assert np.abs(out[3] - xv[3]).max() > 0.9 * 0.25 * dt / k4   # the odd planes do move
 
 
 def test_wrap_cases():
