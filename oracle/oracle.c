@@ -14,6 +14,19 @@
 #include <stdlib.h>
 #include <string.h>
 
+/* ------------------------------------------------------------ threads ---- *
+ * SURVEY c.1 "Implementation of the oracle" / c.5 "Oracle modes": threads = 1 is
+ * the serial, bitwise-reproducible parity mode; threads > 1 is the
+ * OpenMP-deterministic mode (fixed thread count, static schedules, a stable
+ * two-level sort that equals the serial one, a two-colour z-slab deposit and
+ * fixed-order reductions).  Only the deposit's and the energy's summation order
+ * depend on the thread count; every other stage computes bit-identical results
+ * (the same per-particle / per-line arithmetic). */
+static int g_threads = 1;
+
+void oracle_set_threads(int32_t t) { g_threads = t < 1 ? 1 : t; }
+int32_t oracle_get_threads(void) { return g_threads; }
+
 /* ------------------------------------------------------------------ RNG ---- */
 /* Philox4x32-10 (Salmon et al., Random123), D#10. */
 static void mulhilo32(uint32_t a, uint32_t b, uint32_t *hi, uint32_t *lo) {
@@ -86,6 +99,7 @@ static double landau_position(double u, double k, double L, double alpha) {
 void oracle_sample_landau(int64_t np, double k, double L, double alpha, uint64_t seed,
                           double *xv) {
     const double two_pi = 6.283185307179586476925286766559;
+#pragma omp parallel for schedule(static) num_threads(g_threads)
     for (int64_t j = 0; j < np; ++j) {
         double u[8];
         oracle_uniforms(seed, (uint64_t)j, u);
@@ -119,6 +133,7 @@ uint32_t oracle_morton_key(int32_t ix, int32_t iy, int32_t iz, int32_t n) {
 
 void oracle_keys(int32_t n, double L, int64_t np, const double *xv, uint32_t *keys) {
     const double inv_h = (double)n / L;
+#pragma omp parallel for schedule(static) num_threads(g_threads)
     for (int64_t j = 0; j < np; ++j) {
         int32_t ix = oracle_cell_index(xv[0 * np + j], inv_h, n);
         int32_t iy = oracle_cell_index(xv[1 * np + j], inv_h, n);
@@ -127,23 +142,72 @@ void oracle_keys(int32_t n, double L, int64_t np, const double *xv, uint32_t *ke
     }
 }
 
+/* OpenMP-deterministic stable sort (threads > 1): a stable partition of the
+ * particle indices into T contiguous key ranges (per-chunk histograms, fixed
+ * chunk order), then a stable counting sort of each range by key.  Both steps
+ * keep index order among equal keys, so perm equals the serial counting sort's. */
+static void sort_perm_parallel(int64_t np, const uint32_t *keys, int64_t ncell, uint32_t *perm, int T) {
+    int64_t *hist = (int64_t *)calloc((size_t)T * T, sizeof(int64_t));   /* [chunk][range] */
+    uint32_t *part = (uint32_t *)malloc(sizeof(uint32_t) * (size_t)(np > 0 ? np : 1));
+    int64_t *rstart = (int64_t *)calloc((size_t)T + 1, sizeof(int64_t));
+#pragma omp parallel for schedule(static, 1) num_threads(T)
+    for (int c = 0; c < T; ++c) {
+        const int64_t j0 = np * c / T, j1 = np * (c + 1) / T;
+        for (int64_t j = j0; j < j1; ++j) hist[(int64_t)c * T + (int64_t)keys[j] * T / ncell] += 1;
+    }
+    int64_t run = 0;
+    for (int b = 0; b < T; ++b) {         /* range-major, chunk-minor: stable */
+        rstart[b] = run;
+        for (int c = 0; c < T; ++c) {
+            const int64_t v = hist[(int64_t)c * T + b];
+            hist[(int64_t)c * T + b] = run;
+            run += v;
+        }
+    }
+    rstart[T] = run;
+#pragma omp parallel for schedule(static, 1) num_threads(T)
+    for (int c = 0; c < T; ++c) {
+        const int64_t j0 = np * c / T, j1 = np * (c + 1) / T;
+        for (int64_t j = j0; j < j1; ++j) part[hist[(int64_t)c * T + (int64_t)keys[j] * T / ncell]++] = (uint32_t)j;
+    }
+#pragma omp parallel for schedule(static, 1) num_threads(T)
+    for (int b = 0; b < T; ++b) {
+        const int64_t k0 = (b * ncell + T - 1) / T, k1 = ((b + 1) * ncell + T - 1) / T;   /* keys of range b */
+        int64_t *start = (int64_t *)calloc((size_t)(k1 - k0) + 1, sizeof(int64_t));
+        for (int64_t i = rstart[b]; i < rstart[b + 1]; ++i) start[keys[part[i]] - k0 + 1] += 1;
+        for (int64_t k = 0; k < k1 - k0; ++k) start[k + 1] += start[k];
+        for (int64_t i = rstart[b]; i < rstart[b + 1]; ++i) perm[rstart[b] + start[keys[part[i]] - k0]++] = part[i];
+        free(start);
+    }
+    free(rstart);
+    free(part);
+    free(hist);
+}
+
 void oracle_sort(int32_t n, double L, int64_t np, double *xv, uint32_t *perm) {
     /* Stable counting sort by cell key: ties keep the current order (D#14). */
     const int64_t ncell = (int64_t)n * n * n;
+    const int T = g_threads;
     uint32_t *keys = (uint32_t *)malloc(sizeof(uint32_t) * (size_t)(np > 0 ? np : 1));
-    int64_t *start = (int64_t *)calloc((size_t)ncell + 1, sizeof(int64_t));
     double *tmp = (double *)malloc(sizeof(double) * (size_t)(np > 0 ? np : 1));
     oracle_keys(n, L, np, xv, keys);
-    for (int64_t j = 0; j < np; ++j) start[keys[j] + 1] += 1;
-    for (int64_t c = 0; c < ncell; ++c) start[c + 1] += start[c];
-    for (int64_t j = 0; j < np; ++j) perm[start[keys[j]]++] = (uint32_t)j;
+    if (T == 1) {
+        int64_t *start = (int64_t *)calloc((size_t)ncell + 1, sizeof(int64_t));
+        for (int64_t j = 0; j < np; ++j) start[keys[j] + 1] += 1;
+        for (int64_t c = 0; c < ncell; ++c) start[c + 1] += start[c];
+        for (int64_t j = 0; j < np; ++j) perm[start[keys[j]]++] = (uint32_t)j;
+        free(start);
+    } else {
+        sort_perm_parallel(np, keys, ncell, perm, T);
+    }
     for (int a = 0; a < 6; ++a) {
         double *col = xv + (int64_t)a * np;
+#pragma omp parallel for schedule(static) num_threads(T)
         for (int64_t i = 0; i < np; ++i) tmp[i] = col[perm[i]];
-        memcpy(col, tmp, sizeof(double) * (size_t)np);
+#pragma omp parallel for schedule(static) num_threads(T)
+        for (int64_t i = 0; i < np; ++i) col[i] = tmp[i];
     }
     free(tmp);
-    free(start);
     free(keys);
 }
 
@@ -152,28 +216,75 @@ static int64_t node(int32_t n, int32_t ix, int32_t iy, int32_t iz) {
     return ((int64_t)((iz % n + n) % n) * n + ((iy % n + n) % n)) * n + ((ix % n + n) % n);
 }
 
+/* The eight CIC corner weights of particle j added to rho. */
+static void deposit_one(int32_t n, double inv_h, int64_t np, const double *xv, int64_t j, double *rho) {
+    int32_t i[3];
+    double w[3][2];
+    for (int d = 0; d < 3; ++d) {
+        double s = xv[d * np + j] * inv_h;
+        i[d] = oracle_cell_index(xv[d * np + j], inv_h, n);
+        double f = s - (double)i[d];
+        w[d][0] = 1.0 - f;
+        w[d][1] = f;
+    }
+    for (int c = 0; c < 2; ++c)
+        for (int b = 0; b < 2; ++b)
+            for (int a = 0; a < 2; ++a) {
+                double wt = (w[0][a] * w[1][b]) * w[2][c];
+                rho[node(n, i[0] + a, i[1] + b, i[2] + c)] += wt;
+            }
+}
+
+/* OpenMP-deterministic deposit (threads > 1, SURVEY c.5): S (even, <= n) z-slabs of
+ * cell planes; slab s = the particles whose cell plane iz has iz S / n = s, kept in
+ * index order by a stable partition.  A slab touches its own node planes and the
+ * next one, so slabs of one colour (s mod 2) never share a node: colour 0, then
+ * colour 1, each slab summed in index order.  Deterministic for a fixed S. */
+static void deposit_slabs(int32_t n, double inv_h, int64_t np, const double *xv, double *rho, int T) {
+    int S = 2 * T;
+    if (S > n) S = n;
+    int64_t *hist = (int64_t *)calloc((size_t)T * S, sizeof(int64_t));   /* [chunk][slab] */
+    int64_t *sstart = (int64_t *)calloc((size_t)S + 1, sizeof(int64_t));
+    uint32_t *idx = (uint32_t *)malloc(sizeof(uint32_t) * (size_t)(np > 0 ? np : 1));
+#pragma omp parallel for schedule(static, 1) num_threads(T)
+    for (int c = 0; c < T; ++c)
+        for (int64_t j = np * c / T; j < np * (c + 1) / T; ++j)
+            hist[(int64_t)c * S + (int64_t)oracle_cell_index(xv[2 * np + j], inv_h, n) * S / n] += 1;
+    int64_t run = 0;
+    for (int s = 0; s < S; ++s) {
+        sstart[s] = run;
+        for (int c = 0; c < T; ++c) {
+            const int64_t v = hist[(int64_t)c * S + s];
+            hist[(int64_t)c * S + s] = run;
+            run += v;
+        }
+    }
+    sstart[S] = run;
+#pragma omp parallel for schedule(static, 1) num_threads(T)
+    for (int c = 0; c < T; ++c)
+        for (int64_t j = np * c / T; j < np * (c + 1) / T; ++j)
+            idx[hist[(int64_t)c * S + (int64_t)oracle_cell_index(xv[2 * np + j], inv_h, n) * S / n]++] = (uint32_t)j;
+    for (int colour = 0; colour < 2; ++colour) {
+#pragma omp parallel for schedule(static, 1) num_threads(T)
+        for (int s = colour; s < S; s += 2)
+            for (int64_t i = sstart[s]; i < sstart[s + 1]; ++i) deposit_one(n, inv_h, np, xv, idx[i], rho);
+    }
+    free(idx);
+    free(sstart);
+    free(hist);
+}
+
 void oracle_deposit(int32_t n, double L, int64_t np, const double *xv, double q, double *rho) {
     const double inv_h = (double)n / L;
     const int64_t nn = (int64_t)n * n * n;
     for (int64_t m = 0; m < nn; ++m) rho[m] = 0.0;
-    for (int64_t j = 0; j < np; ++j) {
-        int32_t i[3];
-        double w[3][2];
-        for (int d = 0; d < 3; ++d) {
-            double s = xv[d * np + j] * inv_h;
-            i[d] = oracle_cell_index(xv[d * np + j], inv_h, n);
-            double f = s - (double)i[d];
-            w[d][0] = 1.0 - f;
-            w[d][1] = f;
-        }
-        for (int c = 0; c < 2; ++c)
-            for (int b = 0; b < 2; ++b)
-                for (int a = 0; a < 2; ++a) {
-                    double wt = (w[0][a] * w[1][b]) * w[2][c];
-                    rho[node(n, i[0] + a, i[1] + b, i[2] + c)] += wt;
-                }
+    if (g_threads == 1) {
+        for (int64_t j = 0; j < np; ++j) deposit_one(n, inv_h, np, xv, j, rho);
+    } else {
+        deposit_slabs(n, inv_h, np, xv, rho, g_threads);
     }
     const double scale = q * ((inv_h * inv_h) * inv_h);
+#pragma omp parallel for schedule(static) num_threads(g_threads)
     for (int64_t m = 0; m < nn; ++m) rho[m] = scale * rho[m];
 }
 
@@ -207,10 +318,14 @@ static void fft_line(double complex *a, int32_t n, int64_t stride, int sign) {
 }
 
 static void fft3d(double complex *c, int32_t n, int sign) {
+    /* every line is transformed by the same code whatever the thread count */
+#pragma omp parallel for schedule(static) num_threads(g_threads)
     for (int32_t iz = 0; iz < n; ++iz)          /* along x */
         for (int32_t iy = 0; iy < n; ++iy) fft_line(c + ((int64_t)iz * n + iy) * n, n, 1, sign);
+#pragma omp parallel for schedule(static) num_threads(g_threads)
     for (int32_t iz = 0; iz < n; ++iz)          /* along y */
         for (int32_t ix = 0; ix < n; ++ix) fft_line(c + (int64_t)iz * n * n + ix, n, n, sign);
+#pragma omp parallel for schedule(static) num_threads(g_threads)
     for (int32_t iy = 0; iy < n; ++iy)          /* along z */
         for (int32_t ix = 0; ix < n; ++ix) fft_line(c + (int64_t)iy * n + ix, n, (int64_t)n * n, sign);
 }
@@ -240,8 +355,10 @@ double oracle_solve_fft(int32_t n, double L, const double *rho, double *E) {
     const int64_t nn = (int64_t)n * n * n;
     double complex *rh = (double complex *)malloc(sizeof(double complex) * (size_t)nn);
     double complex *eh = (double complex *)malloc(sizeof(double complex) * (size_t)nn * 3);
+#pragma omp parallel for schedule(static) num_threads(g_threads)
     for (int64_t m = 0; m < nn; ++m) rh[m] = rho[m];
     fft3d(rh, n, -1);
+#pragma omp parallel for schedule(static) num_threads(g_threads)
     for (int32_t iz = 0; iz < n; ++iz)
         for (int32_t iy = 0; iy < n; ++iy)
             for (int32_t ix = 0; ix < n; ++ix) {
@@ -253,6 +370,7 @@ double oracle_solve_fft(int32_t n, double L, const double *rho, double *E) {
     double max_imag = 0.0;
     for (int d = 0; d < 3; ++d) {
         fft3d(eh + d * nn, n, +1);
+#pragma omp parallel for schedule(static) num_threads(g_threads) reduction(max : max_imag)
         for (int64_t m = 0; m < nn; ++m) {
             double complex v = eh[d * nn + m] / (double)nn;
             E[d * nn + m] = creal(v);
@@ -307,10 +425,25 @@ void oracle_field_energy(int32_t n, double L, const double *E, double *wx, doubl
     const double h = L / (double)n;
     const double h3 = (h * h) * h;
     double sx = 0.0, s = 0.0;
-    for (int64_t m = 0; m < nn; ++m) {
-        double ex = E[m], ey = E[nn + m], ez = E[2 * nn + m];
-        sx += ex * ex;
-        s += ex * ex + ey * ey + ez * ez;
+    if (g_threads == 1) {
+        for (int64_t m = 0; m < nn; ++m) {
+            double ex = E[m], ey = E[nn + m], ez = E[2 * nn + m];
+            sx += ex * ex;
+            s += ex * ex + ey * ey + ez * ez;
+        }
+    } else {          /* fixed-order reduction: T sequential chunk sums, added in chunk order */
+        const int T = g_threads;
+        double *px = (double *)calloc((size_t)T, sizeof(double)), *ps = (double *)calloc((size_t)T, sizeof(double));
+#pragma omp parallel for schedule(static, 1) num_threads(T)
+        for (int c = 0; c < T; ++c)
+            for (int64_t m = nn * c / T; m < nn * (c + 1) / T; ++m) {
+                double ex = E[m], ey = E[nn + m], ez = E[2 * nn + m];
+                px[c] += ex * ex;
+                ps[c] += ex * ex + ey * ey + ez * ez;
+            }
+        for (int c = 0; c < T; ++c) { sx += px[c]; s += ps[c]; }
+        free(px);
+        free(ps);
     }
     *wx = 0.5 * h3 * sx;
     *w = 0.5 * h3 * s;
@@ -321,6 +454,7 @@ void oracle_gather(int32_t n, double L, int64_t np, const double *xv, const doub
                    double *Ep) {
     const double inv_h = (double)n / L;
     const int64_t nn = (int64_t)n * n * n;
+#pragma omp parallel for schedule(static) num_threads(g_threads)
     for (int64_t j = 0; j < np; ++j) {
         int32_t i[3];
         double w[3][2];
@@ -344,6 +478,7 @@ void oracle_gather(int32_t n, double L, int64_t np, const double *xv, const doub
 }
 
 void oracle_push(double L, int64_t np, double *xv, const double *Ep, double qm_dt, double dt) {
+#pragma omp parallel for schedule(static) num_threads(g_threads)
     for (int64_t j = 0; j < np; ++j) {
         for (int d = 0; d < 3; ++d) {
             double v = fma(qm_dt, Ep[d * np + j], xv[(3 + d) * np + j]);   /* kick */
@@ -366,6 +501,7 @@ void oracle_half_kick(int32_t n, double L, double dt, int64_t np, double *xv) {
     oracle_solve_fft(n, L, rho, E);
     oracle_gather(n, L, np, xv, E, Ep);
     const double hk = -0.5 * (qm * dt);    /* v_{-1/2} = v_0 - (q/m) E dt/2 */
+#pragma omp parallel for schedule(static) num_threads(g_threads)
     for (int64_t j = 0; j < np; ++j)
         for (int d = 0; d < 3; ++d)
             xv[(3 + d) * np + j] = fma(hk, Ep[d * np + j], xv[(3 + d) * np + j]);

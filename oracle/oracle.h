@@ -26,6 +26,13 @@
 extern "C" {
 #endif
 
+/* Thread count of every oracle function (SURVEY c.5): 1 (default) = serial,
+ * bitwise-reproducible parity mode; T > 1 = OpenMP-deterministic mode -- results
+ * identical to serial except the summation order of the deposit (two-colour
+ * z-slabs) and of the field energy (T fixed chunks), deterministic for a fixed T. */
+void oracle_set_threads(int32_t threads);
+int32_t oracle_get_threads(void);
+
 /* Philox4x32-10 counter-based RNG (D#10); out = philox(ctr, key). */
 void oracle_philox4x32_10(const uint32_t ctr[4], const uint32_t key[2], uint32_t out[4]);
 /* The 8 uniforms u_0..u_7 in [0,1) of particle j (D#10). */

@@ -21,7 +21,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 _SRC = os.path.join(_HERE, "oracle.c")
 _LIB = os.path.join(_HERE, "liboracle.so")
 
-CFLAGS = ["-O2", "-std=c11", "-ffp-contract=off", "-fno-fast-math", "-fPIC", "-shared"]
+CFLAGS = ["-O2", "-std=c11", "-ffp-contract=off", "-fno-fast-math", "-fopenmp", "-fPIC", "-shared"]
 
 
 def build(force: bool = False) -> str:
@@ -46,6 +46,8 @@ def lib():
         i32, i64, u64, dbl = C.c_int32, C.c_int64, C.c_uint64, C.c_double
         sig = {
             "oracle_philox4x32_10": (None, [u32p, u32p, u32p]),
+            "oracle_set_threads": (None, [i32]),
+            "oracle_get_threads": (i32, []),
             "oracle_uniforms": (None, [u64, u64, dp]),
             "oracle_sample_landau": (None, [i64, dbl, dbl, dbl, u64, dp]),
             "oracle_cell_index": (i32, [dbl, dbl, i32]),
@@ -99,6 +101,30 @@ def _up(a):
         return None
     assert a.dtype == np.uint32 and a.flags.c_contiguous
     return a.ctypes.data_as(C.POINTER(C.c_uint32))
+
+
+def set_threads(t: int) -> None:
+    """1 = serial parity mode (default); T > 1 = OpenMP-deterministic mode (SURVEY c.5)."""
+    lib().oracle_set_threads(int(t))
+
+
+def get_threads() -> int:
+    return int(lib().oracle_get_threads())
+
+
+class threads:
+    """with threads(T): ... runs the oracle in the OpenMP-deterministic mode, then restores."""
+
+    def __init__(self, t: int):
+        self.t = t
+
+    def __enter__(self):
+        self.old = get_threads()
+        set_threads(self.t)
+        return self
+
+    def __exit__(self, *a):
+        set_threads(self.old)
 
 
 def philox(ctr, key):

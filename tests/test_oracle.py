@@ -402,6 +402,40 @@ def test_run_momentum_conservation_and_determinism():
     assert np.all(np.diff(O.keys(n, L, xs).astype(np.int64)) >= 0)   # canonical order
 
 
+@pytest.mark.parametrize("threads", [3, 8])
+def test_openmp_deterministic_mode(threads):
+    """SURVEY c.1/c.5 "OpenMP-deterministic mode": with T threads the sort is still the
+    stable sort (numpy's stable argsort), the two-colour slab deposit conserves charge
+    exactly and equals the serial deposit up to summation order, and whole runs are
+    bitwise reproducible at fixed T and agree with the serial mode within the BJ
+    tolerances (energies 1e-10, x, v 1e-12, permutation bit-exact)."""
+    n = 32
+    xv = landau_state(n, 8, seed=23)
+    keys = O.keys(n, L, xv)
+    with O.threads(threads):
+        assert O.get_threads() == threads
+        xs, perm = O.sort(n, L, xv)
+        assert np.array_equal(perm, np.argsort(keys, kind="stable").astype(np.uint32))
+        q = -L ** 3 / xv.shape[1]
+        rho = O.deposit(n, L, xs, q)
+        h = L / n
+        assert rho.sum() * h ** 3 == pytest.approx(-L ** 3, rel=1e-12)
+    rho_ref = O.deposit(n, L, xs, q)
+    assert np.abs(rho - rho_ref).max() <= 1e-14 * np.abs(rho_ref).max()
+    with O.threads(threads):
+        a = O.run(n, L, 0.05, xv, 5, want_perm=True)
+        b = O.run(n, L, 0.05, xv, 5, want_perm=True)
+    assert O.get_threads() == 1
+    for u, v in zip(a, b):
+        assert np.array_equal(u, v)                    # deterministic for a fixed thread count
+    s = O.run(n, L, 0.05, xv, 5, want_perm=True)
+    assert np.array_equal(a[3], s[3])
+    assert np.all(np.abs(a[1] - s[1]) <= 1e-10 * s[1])
+    dx = np.abs(a[0][:3] - s[0][:3])
+    assert np.minimum(dx, L - dx).max() / L <= 1e-12
+    assert (np.abs(a[0][3:] - s[0][3:]) / np.maximum(np.abs(s[0][3:]), 1)).max() <= 1e-12
+
+
 def test_alpha0_no_growth():
     """alpha = 0 at 16^3 x 8: no growth above 10x W_x(0) over 100 steps."""
     n = 16
