@@ -37,19 +37,21 @@ UNIT = "particle-pushes/s"
 
 # Algorithmic bytes per launch:
 # per particle, per grid node (ncell = N^3).
+# Layout padding is not counted: an E node is 24 B (E_x, E_y, E_z; the 4th double of the
+# 32-B record is padding), and the kick's store is v (24 B; z is rewritten unchanged).
 ALG_BYTES = {
     "reorder_deposit": (4 + 48 + 48, 4 + 16),        # perm, x/v gather, x'/v' store | offs, rho RMW
-    "push_key": (48 + 32 + 4 + 2, 32 + 8),           # x/v read, kicked v (2 pair streams), key, rank | E tile, count RMW
+    "push_key": (48 + 24 + 4 + 2, 24 + 8),           # x/v read, kicked v, key, rank | E tile, count RMW
     "place": (4 + 2 + 4, 4),                         # key, rank read, perm write | offs
     "scan": (0, 16),                                 # count read x2, offs + cursor write
     "fft_x_fwd": (0, 8 + 8),
     "fft_y_fwd": (0, 8 + 8),
     "fft_z_mul": (0, 8 + 16),                       # rho^ pencil -> phi^, E^_z
     "fft_y_inv": (0, 16 + 24),                      # phi^, E^_z -> E_x, E_y, E_z spectra
-    "fft_x_inv": (0, 24 + 32),                       # 3 half spectra -> E node records
+    "fft_x_inv": (0, 24 + 24),                       # 3 half spectra -> E node records (24 B each)
     "clear": (0, 4 + 8),
     # FD-PCG (BJ config 5), per launch of the stage's main kernel:
-    "pcg_field": (0, 8 + 32),                       # phi (stencil) -> E node records
+    "pcg_field": (0, 8 + 24),                       # phi (stencil) -> E node records
 }
 # PCG stages with launches of different kinds: algorithmic bytes per node per
 # application.  SSOR M^-1 (4 inner x 2 outer = 32 half-sweeps): 8 + 12 + 29 x 16 + 20
@@ -185,50 +187,109 @@ def _oracle_steps(solver, n, L, xv, steps):
     return O.run(n, L, 0.05, xv, steps)[0]
 
 
-def oracle_sample(steps: int, n: int = 64, ppc: int = 8, solver: str = "fft"):
-    """Time the CPU oracle, as it stands, on a bounded sample of the workload."""
-    from pic_inputs import landau_state
+def host_cpu():
+    """lscpu model name and the number of physical cores (unique (core, socket) pairs)."""
+    model, cores = None, None
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for line in out.splitlines():
+            if line.startswith("Model name:"):
+                model = line.split(":", 1)[1].strip()
+        out = subprocess.run(["lscpu", "-p=CORE,SOCKET"], capture_output=True, text=True, timeout=10).stdout
+        cores = len({l for l in out.splitlines() if l and not l.startswith("#")}) or None
+    except Exception:
+        pass
+    return model, cores or os.cpu_count() or 1
 
+
+def oracle_leg(n: int, ppc: int, steps: int, threads: int, solver: str = "fft"):
+    """Time the CPU oracle, as it stands, for `steps` steps of Landau n^3 x ppc on `threads`
+    threads (1 = the serial parity mode, > 1 = the OpenMP-deterministic mode, SURVEY c.5).
+    The initial state is the oracle's own sampler (untimed); the timed call is oracle_run,
+    which also canonicalises the (already sorted) input once."""
     import numpy as np
+    from oracle import oracle as O
 
     L = 4 * np.pi
-    xv = landau_state(n, ppc, seed=1)
-    _oracle_steps(solver, n, L, xv, 1)   # warm (build, page-in)
-    t0 = time.perf_counter()
-    _oracle_steps(solver, n, L, xv, steps)
-    dt = time.perf_counter() - t0
-    npart = ppc * n ** 3
-    return {"value": npart * steps / dt, "unit": UNIT, "cores": 1, "kind": "oracle",
-            "sample": f"oracle_run{'' if solver == 'fft' else '_' + solver} (serial C, -O2) on Landau {n}^3 x {ppc} ppc "
-                      f"({npart} particles), {steps} steps, {dt:.1f} s; same per-particle "
-                      f"step as the {{n}}^3 workload, smaller grid"}
+    with O.threads(threads):
+        xv = O.sample_landau(ppc * n ** 3, 0.5, L, 0.05, 1)
+        xv, _ = O.sort(n, L, xv)
+        t0 = time.perf_counter()
+        _oracle_steps(solver, n, L, xv, steps)
+        dt = time.perf_counter() - t0
+    del xv
+    return ppc * n ** 3 * steps / dt, dt
+
+
+def oracle_sample(steps: int, n: int = 64, ppc: int = 8, solver: str = "fft", bench_n: int = 512,
+                  omp_n: int = 256, omp_steps: int = 1):
+    """cpu_baseline: the oracle as it stands on the box's host cores, two legs (BASELINE.md
+    §3, SURVEY d.7): serial on a 64^3 sample, and the OpenMP-deterministic mode on all
+    physical cores on a larger sample (omp_n^3, or the bench config itself with
+    --cpu-full).  The line's value is the all-cores leg."""
+    model, cores = host_cpu()
+    v1, t1 = oracle_leg(n, ppc, steps, 1, solver)
+    if solver in ("fft",):
+        vT, tT = oracle_leg(omp_n, ppc, omp_steps, cores, solver)
+        sample = (f"oracle_run (C, -O2, OpenMP-deterministic mode, {cores} threads = all physical cores of "
+                  f"'{model}') on Landau {omp_n}^3 x {ppc} ppc ({ppc * omp_n ** 3} particles), {omp_steps} step(s), "
+                  f"{tT:.1f} s" + ("" if omp_n == bench_n else
+                                    f"; the {bench_n}^3 workload's per-particle step extrapolated from this sample") +
+                  f". Serial leg (1 core, the parity mode): {n}^3 x {ppc} ppc, {steps} steps, {t1:.1f} s, "
+                  f"{v1:.3e} pushes/s")
+        return {"value": vT, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample,
+                "serial": {"value": v1, "unit": UNIT, "cores": 1, "grid": n, "steps": steps},
+                "host": {"model": model, "physical_cores": cores}, "same_config": omp_n == bench_n}
+    return {"value": v1, "unit": UNIT, "cores": 1, "kind": "oracle",
+            "sample": f"oracle_run_{solver} (serial C, -O2) on Landau {n}^3 x {ppc} ppc "
+                      f"({ppc * n ** 3} particles), {steps} steps, {t1:.1f} s; the {bench_n}^3 workload's "
+                      f"per-particle step extrapolated from this sample",
+            "host": {"model": model, "physical_cores": cores}, "same_config": False}
 
 
 def run_reference(args, rank, world):
+    """The reference arm of this tier: the CPU oracle as it stands (BJ north_star: "the oracle
+    timed on the box's own host cores"), OpenMP-deterministic mode on all physical cores;
+    every step a bounded sample of the workload (rank 0 only; the other ranks exit 0)."""
     if rank != 0:
         return 0
-    from pic_inputs import landau_state
     import numpy as np
+    from oracle import oracle as O
 
-    n, ppc = (16, 8) if args.solver == "pif" else (64, 8)
+    model, cores = host_cpu()
+    if args.solver == "pif":
+        from pic_inputs import landau_state
+
+        n, ppc, threads = 16, 8, 1
+        xv = landau_state(n, ppc, seed=1)
+    else:
+        n, ppc = args.ref_n, args.ppc
+        threads = 1 if args.solver in ("pcg", "fem") else cores
+        with O.threads(threads):
+            xv = O.sample_landau(ppc * n ** 3, 0.5, 4 * np.pi, 0.05, 1)
     L = 4 * np.pi
-    xv = landau_state(n, ppc, seed=1)
-    xs = _oracle_steps(args.solver, n, L, xv, args.warmup) if args.warmup else xv
-    t0 = time.perf_counter()
-    _oracle_steps(args.solver, n, L, xs, args.steps)
-    dt = time.perf_counter() - t0
+    with O.threads(threads):
+        xs = _oracle_steps(args.solver, n, L, xv, args.warmup) if args.warmup else xv
+        t0 = time.perf_counter()
+        _oracle_steps(args.solver, n, L, xs, args.steps)
+        dt = time.perf_counter() - t0
     npart = ppc * n ** 3
     value = npart * args.steps / dt
-    sample = (f"CPU oracle ({'numpy, oracle/nufft.py' if args.solver == 'pif' else 'serial C'}) on Landau {n}^3 x {ppc} ppc ({npart} particles) per step, "
-              f"a bounded sample of the {args.n}^3 x {args.ppc} workload")
+    what = ("numpy, oracle/nufft.py" if args.solver == "pif" else
+            f"C, OpenMP-deterministic mode, {threads} threads" if threads > 1 else "serial C")
+    sample = (f"CPU oracle ({what}) on Landau {n}^3 x {ppc} ppc ({npart} particles) per step, host "
+              f"'{model}' ({cores} physical cores); a bounded sample of the {args.n}^3 x {args.ppc} "
+              f"workload: the per-particle step rate is extrapolated to it" if n != args.n else "")
     line = {
         "impl": "reference", "metric": METRIC.replace("FFT-PIC", args.solver.upper() + "-PIC"), "value": value, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * dt / args.steps,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic",
         "config": {"workload": f"landau3d_{args.n}^3x{args.ppc}ppc_{args.solver} (reference arm: "
-                               f"{n}^3x{ppc} sample)", "grid": args.n, "ppc": args.ppc},
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample},
+                               f"{n}^3x{ppc} sample)", "grid": args.n, "ppc": args.ppc, "sample_grid": n,
+                   "same_config": n == args.n},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "oracle", "sample": sample,
+                         "host": {"model": model, "physical_cores": cores}},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -256,7 +317,9 @@ def run_ours(args, rank, world):
     pcg = args.solver in ("pcg", "fem")     # CG-based solvers (iteration statistics)
     torch.cuda.synchronize()
     log(f"[rank {rank}] init {n}^3 x {ppc} (slab z0={sim.z0} nz={sim.nz}, {sim.np} particles): "
-        f"{time.perf_counter() - t_init:.1f} s, workspace {sim.workspace.numel() / 2**30:.1f} GiB")
+        f"{time.perf_counter() - t_init:.1f} s, workspace {sim.workspace.numel() / 2**30:.1f} GiB"
+        + (f"; libpic NCCL communicator nranks={world}, transport "
+           f"{'peer' if sim.peer_transport() else 'nccl'}" if world > 1 else ""))
     stream = sim.stream
 
     def barrier():
@@ -302,7 +365,10 @@ def run_ours(args, rank, world):
         t0 = time.perf_counter()
         sim.set_particles(hv)                 # H2D of the state (+ sort + deposit)
         e2e_ex = sim.step(args.steps)        # per-step energies D2H
-        hv = np.empty((6, sim.np))          # the state after K steps (size changes with migration)
+        if sim.np != host.shape[1]:          # the slab's particle count changed (migration)
+            del hv, host
+            host = torch.empty((6, sim.np), dtype=torch.float64, pin_memory=True)
+        hv = host.numpy()                    # pinned readback of the state after K steps
         sim.get_particles(out=hv)
         torch.cuda.synchronize()
         t_e2e = reduce_max(time.perf_counter() - t0, world)
@@ -310,9 +376,9 @@ def run_ours(args, rank, world):
         e2e = {"value": np_ * args.steps / t_e2e, "unit": UNIT,
                "h2d_bytes_per_step": state_bytes / args.steps,
                "d2h_bytes_per_step": (state_bytes + 8 * args.steps) / args.steps,
-               "what": "pic_set_particles(host pinned state) + pic_step(K) with per-step W_x to host "
-                       "+ pic_get_particles(host); wall clock, max over ranks; bytes per rank"}
-        del host
+               "what": "pic_set_particles(pinned host state) + pic_step(K) with per-step W_x to host "
+                       "+ pic_get_particles(pinned host); wall clock, max over ranks; bytes per rank"}
+        del hv, host
 
     if rank != 0:
         sim.close()
@@ -375,9 +441,10 @@ def run_ours(args, rank, world):
                   "exchange_ms_per_step": stages["exchange"][0] / args.steps,
                   "transport": "peer" if sim.peer_transport() else "nccl"}
 
-    cpu = None if args.no_cpu_baseline else oracle_sample(steps=args.cpu_steps, solver=args.solver)
-    if cpu:
-        cpu["sample"] = cpu["sample"].replace("{n}", str(n))
+    cpu = None
+    if not args.no_cpu_baseline:
+        cpu = oracle_sample(steps=args.cpu_steps, solver=args.solver, bench_n=n,
+                            omp_n=n if args.cpu_full else args.cpu_omp_n, omp_steps=1)
     launches = sim.launches_per_step() * args.steps
     line = {
         "metric": METRIC.replace("FFT-PIC", args.solver.upper() + "-PIC"), "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
@@ -575,19 +642,46 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--pif-atomic", action="store_true", help="PIF: global-atomic spreading (no bins)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--cpu-steps", type=int, default=20)
+    ap.add_argument("--cpu-steps", type=int, default=2, help="serial oracle leg: steps at 64^3")
+    ap.add_argument("--cpu-omp-n", type=int, default=256, help="all-cores oracle leg: grid of the sample")
+    ap.add_argument("--cpu-full", action="store_true",
+                    help="all-cores oracle leg on the bench config itself (512^3: ~60 GB host RAM, minutes)")
+    ap.add_argument("--ref-n", type=int, default=128,
+                    help="reference arm: grid of the per-step oracle sample (the workload is --n)")
     args = ap.parse_args()
 
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        # one process per GPU: re-launch this command under torchrun (the driver's own
+        # launch sets WORLD_SIZE and lands below)
+        import socket
+
+        with socket.socket() as sk:
+            sk.bind(("127.0.0.1", 0))
+            port = sk.getsockname()[1]
+        env = dict(os.environ)
+        env.setdefault("NCCL_DEBUG", "INFO")
+        env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+               "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__), *sys.argv[1:]]
+        log("relaunching under torchrun: " + " ".join(cmd))
+        return subprocess.call(cmd, env=env)
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
+    if world != args.gpus:
+        log(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}: refusing to print a line whose "
+            f"n_gpus differs from --gpus")
+        return 2
     if args.impl == "reference":
         return run_reference(args, rank, world)
     if world > 1:
         import torch
         import torch.distributed as dist
 
+        os.environ.setdefault("NCCL_DEBUG", "INFO")          # the communicator's init lines (nranks)
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
         torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", 0)))
         dist.init_process_group("nccl")
+        log(f"[rank {rank}] torch.distributed NCCL process group: world_size={dist.get_world_size()}")
     rc = run_pif(args, rank, world) if args.solver == "pif" else run_ours(args, rank, world)
     if world > 1:
         import torch.distributed as dist

@@ -102,6 +102,17 @@ pic_status pic_nccl_unique_id(uint8_t id[128]);
 pic_status pic_slab(const pic_params *p, int32_t rank, int32_t nranks, int32_t *z0, int32_t *nz,
                     int64_t *capacity);
 
+/* Owner rank of each of np positions under the decomposition of pic_slab:
+ * the rank whose slab holds the cell plane i_z = min(floor(z inv_h), N - 1), inv_h =
+ * (double)N / L (D#5), i.e. the rank each particle must be given to in pic_set_particles.
+ *   xyz   : host doubles [3][np] (x, y, z rows; xyzuvw of pic_set_particles may be passed),
+ *           every coordinate in [0, L).
+ *   owner : host int32 [np], written.
+ * Pure host function (no context, no device).  PIC_EINVAL: invalid parameters (as
+ * pic_workspace_bytes), NULL pointers with np > 0, or a z outside [0, L). */
+pic_status pic_owner_ranks(const pic_params *p, int32_t nranks, const double *xyz, int64_t np,
+                           int32_t *owner);
+
 /* Bytes of device workspace pic_init needs for these parameters (rank/nranks as in
  * pic_init).  PIC_EINVAL on invalid parameters. */
 pic_status pic_workspace_bytes(const pic_params *p, int32_t rank, int32_t nranks, size_t *bytes);
@@ -115,7 +126,8 @@ pic_status pic_workspace_bytes(const pic_params *p, int32_t rank, int32_t nranks
  *   workspace : device pointer, >= pic_workspace_bytes(), caller-owned.
  *   cuda_stream: cudaStream_t (void*); NULL = legacy default stream.
  * PIC_EINVAL: alpha not in [0,1), ppc <= 0, N not a power of two in [16,1024],
- *   k <= 0, dt <= 0, k L / 2 pi not a positive integer, N_p per rank >= 2^32 / 1.3,
+ *   k <= 0, dt <= 0, k L / 2 pi not a positive integer, a rank's particle index space
+ *   (capacity + migration receive buffer) >= 2^32,
  *   nranks not in {1,2,4,8}, N/nranks < 4, pgrid != {1, nranks}.
  * PIC_EINVAL also: solver not a pic_solver; PCG settings out of range.
  * PIC_EUNSUPPORTED: a pencil grid (pgrid = {Py > 1, Pz}); the PCG solver at nranks > 1
@@ -157,9 +169,25 @@ pic_status pic_migrated(pic_ctx *ctx, int64_t *migrated);
  * Always 0 at P = 1. */
 pic_status pic_peer_transport(pic_ctx *ctx, int32_t *peer);
 
-/* Copy the particle state to host xyzuvw[6][np] in canonical order (sorted by
- * cell key, ties by the current order).  Synchronous. */
+/* Copy THIS RANK's particle state to host xyzuvw[6][np] (np = pic_num_particles) in
+ * canonical order (sorted by cell key, ties by the current order: at P > 1 the rank's
+ * slab of the global order, SURVEY c.5).  Synchronous.  Not collective. */
 pic_status pic_get_particles(pic_ctx *ctx, double *xyzuvw, int64_t np);
+
+/* Collective (every rank of the context calls it; SURVEY §8(b) "rank 0 gathers when
+ * nranks > 1"): rank 0 receives the particles of every rank in the global canonical
+ * order -- a stable sort by the global Morton cell key of the rank-ordered
+ * concatenation; a cell belongs to one rank, so ties keep that rank's canonical order,
+ * which is the single-domain order (D#15).
+ *   xyzuvw   : rank 0: host doubles [6][np_total]; other ranks: ignored (may be NULL).
+ *   np_total : rank 0: the capacity of xyzuvw in particles, must equal the total;
+ *              other ranks: ignored.
+ *   np_out   : nullable; every rank receives the total particle count.
+ * Pass xyzuvw = NULL on every rank to query the total only.  P = 1: pic_get_particles.
+ * Staged through rank 0's idle particle buffer (one rank at a time, NCCL send/recv);
+ * the global sort runs on rank 0's host.  PIC_EINVAL on rank 0 (and on every rank, the
+ * decision is shared) if np_total differs from the total. */
+pic_status pic_gather_particles(pic_ctx *ctx, double *xyzuvw, int64_t np_total, int64_t *np_out);
 
 /* (PCG: also resets the warm start phi to 0.)
  * Replace the particle state from host xyzuvw[6][np] (P = 1: np = N_p; P > 1: this

@@ -12,6 +12,7 @@ from ._binding import (  # noqa: F401
     default_params,
     lib,
     nccl_unique_id,
+    owner_ranks,
     slab,
     slab_select,
     workspace_bytes,

@@ -69,6 +69,8 @@ SYMBOLS = {
     "pic_nccl_unique_id": (C.c_int, [C.c_void_p]),
     "pic_slab": (C.c_int, [C.POINTER(pic_params), C.c_int32, C.c_int32, C.POINTER(C.c_int32),
                            C.POINTER(C.c_int32), _i64p]),
+    "pic_owner_ranks": (C.c_int, [C.POINTER(pic_params), C.c_int32, _dp, C.c_int64, C.POINTER(C.c_int32)]),
+    "pic_gather_particles": (C.c_int, [_vp, _dp, C.c_int64, _i64p]),
     "pic_migrated": (C.c_int, [_vp, _i64p]),
     "pic_peer_transport": (C.c_int, [_vp, C.POINTER(C.c_int32)]),
     "pic_workspace_bytes": (C.c_int, [C.POINTER(pic_params), C.c_int32, C.c_int32, C.POINTER(C.c_size_t)]),
@@ -165,12 +167,20 @@ def nccl_unique_id() -> bytes:
     return bytes(buf)
 
 
+def owner_ranks(xv: np.ndarray, n: int, L: float, nranks: int) -> np.ndarray:
+    """Owner rank of every particle of xv[6][np] (or [3][np]) -- pic_owner_ranks."""
+    xv = np.ascontiguousarray(xv, dtype=np.float64)
+    p = default_params(n=n, k=2 * np.pi / L, length=L, pgrid=(1, nranks))
+    out = np.empty(xv.shape[1], dtype=np.int32)
+    _check(lib().pic_owner_ranks(C.byref(p), nranks, _d(xv), xv.shape[1],
+                                 out.ctypes.data_as(C.POINTER(C.c_int32))))
+    return out
+
+
 def slab_select(xv: np.ndarray, n: int, L: float, rank: int, nranks: int) -> np.ndarray:
-    """The particles of a global state xv[6][np] that rank owns (cell plane in its
-    z-slab), in their global order -- what each rank passes to set_particles."""
-    nz = n // nranks
-    iz = np.minimum(np.floor(xv[2] * (n / L)).astype(np.int64), n - 1)
-    return np.ascontiguousarray(xv[:, (iz >= rank * nz) & (iz < (rank + 1) * nz)])
+    """The particles of a global state xv[6][np] that rank owns (pic_owner_ranks), in
+    their global order -- what each rank passes to set_particles."""
+    return np.ascontiguousarray(xv[:, owner_ranks(xv, n, L, nranks) == rank])
 
 
 def slab(p: pic_params, rank: int, nranks: int):
@@ -251,6 +261,20 @@ class Simulation:
         assert out.shape == (6, npl)
         _check(lib().pic_get_particles(self.ctx, _d(out), npl), self.ctx)
         return out
+
+    def gather_particles(self, out: np.ndarray | None = None):
+        """Collective: rank 0 returns every rank's particles in the global canonical order
+        (pic_gather_particles); the other ranks return None."""
+        tot = C.c_int64()
+        _check(lib().pic_gather_particles(self.ctx, None, 0, C.byref(tot)), self.ctx)
+        if self.rank == 0:
+            if out is None:
+                out = np.zeros((6, tot.value))
+            assert out.shape == (6, tot.value) and out.flags.c_contiguous
+            _check(lib().pic_gather_particles(self.ctx, _d(out), tot.value, None), self.ctx)
+            return out
+        _check(lib().pic_gather_particles(self.ctx, None, 0, None), self.ctx)
+        return None
 
     def set_particles(self, xv: np.ndarray):
         xv = np.ascontiguousarray(xv, dtype=np.float64)

@@ -718,19 +718,23 @@ void launch_energy_reduce(const Geom& g, const double* partials, double* energie
     k_energy_reduce<<<1, 1024, 0, s>>>(g, partials, (int)x_inv_grid(g), energies);
 }
 
-// Opt every FFT kernel into > 48 KB of dynamic shared memory once.
-void fft_set_smem_limits() {
+// Opt every FFT kernel into > 48 KB of dynamic shared memory (per device: the caller
+// runs it once for each device); the first failure is returned.
+cudaError_t fft_set_smem_limits() {
     const int big = 200 * 1024;
+    cudaError_t e = cudaSuccess;
+    auto chk = [&](cudaError_t r) { if (e == cudaSuccess) e = r; };
     for (int lg = 3; lg <= 9; ++lg) {
-        PIC_X_SWITCH(lg, (cudaFuncSetAttribute(k_fft_x_fwd<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, big),
-                          cudaFuncSetAttribute(k_fft_x_inv<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, big)))
+        PIC_X_SWITCH(lg, (chk(cudaFuncSetAttribute(k_fft_x_fwd<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, big)),
+                          chk(cudaFuncSetAttribute(k_fft_x_inv<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, big))))
     }
     for (int lg = 4; lg <= 10; ++lg) {
-        PIC_YZ_SWITCH(lg, (cudaFuncSetAttribute(k_fft_y<-1, K, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, big),
-                           cudaFuncSetAttribute(k_fft_y<+1, K, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, big),
-                           cudaFuncSetAttribute(k_fft_y<+1, K, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, big),
-                           cudaFuncSetAttribute(k_fft_z_mul<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, big)))
+        PIC_YZ_SWITCH(lg, (chk(cudaFuncSetAttribute(k_fft_y<-1, K, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, big)),
+                           chk(cudaFuncSetAttribute(k_fft_y<+1, K, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, big)),
+                           chk(cudaFuncSetAttribute(k_fft_y<+1, K, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, big)),
+                           chk(cudaFuncSetAttribute(k_fft_z_mul<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, big))))
     }
+    return e;
 }
 
 }  // namespace pic

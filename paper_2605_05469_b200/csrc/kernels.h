@@ -181,7 +181,10 @@ void launch_fem_update(const Geom& g, double* x, const double* p, double* r, con
 void launch_fem_gradient(const Geom& g, PcgNbr x, double* E4, double* halo, double* partials, double* energies,
                          cudaStream_t s);
 
-void particles_set_smem_limits();
-void fft_set_smem_limits();
+cudaError_t particles_set_smem_limits();
+cudaError_t fft_set_smem_limits();
+// Largest cell population the reorder handles (particles staged per chunk; a larger
+// cell sets the overflow flag): PIC_RD_CAP at P = 1, 13/14 of it at P > 1.
+int reorder_cell_capacity(int nranks);
 
 }  // namespace pic

@@ -820,12 +820,15 @@ constexpr size_t reorder_smem() {
 
 }  // namespace
 
-void particles_set_smem_limits() {
-    cudaFuncSetAttribute(k_reorder_deposit<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)reorder_smem<false>());
-    cudaFuncSetAttribute(k_reorder_deposit<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)reorder_smem<false>());
-    cudaFuncSetAttribute(k_reorder_deposit<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)reorder_smem<true>());
-    cudaFuncSetAttribute(k_reorder_deposit<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)reorder_smem<true>());
+cudaError_t particles_set_smem_limits() {
+    cudaError_t e = cudaFuncSetAttribute(k_reorder_deposit<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)reorder_smem<false>());
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(k_reorder_deposit<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)reorder_smem<false>());
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(k_reorder_deposit<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)reorder_smem<true>());
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(k_reorder_deposit<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)reorder_smem<true>());
+    return e;
 }
+
+int reorder_cell_capacity(int nranks) { return nranks > 1 ? ReorderCap<true>::value : ReorderCap<false>::value; }
 
 void launch_sample(const Geom& g, PState st, int64_t np, double k, double alpha, uint64_t seed,
                    cudaStream_t s) {

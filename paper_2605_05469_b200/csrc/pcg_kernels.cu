@@ -742,13 +742,12 @@ int pcg_tb_stages() { return kTB; }
 
 void launch_pcg_ssor_pass(const Geom& g, int ns, int seq, bool zero_in, bool dot, PcgNbr r, PcgNbr zin,
                           double* zout, double omega, double* partials, double* sc, cudaStream_t s) {
-    static bool attr = false;
-    if (!attr) {
-        cudaFuncSetAttribute(k_ssor_tb, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTBSmem);
-        attr = true;
-    }
+    static unsigned attr = 0;          // per device (bit d): the opt-in is a device attribute
     int dev = 0, sms = 148, occ = 1;
     cudaGetDevice(&dev);
+    if (dev < 32 && !(attr & (1u << dev)) &&
+        cudaFuncSetAttribute(k_ssor_tb, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTBSmem) == cudaSuccess)
+        attr |= 1u << dev;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_ssor_tb, kTBThreads, kTBSmem);
     const int hn = g.n >> 1, tx = std::min(kTX, hn), ty = std::min(kTY, g.n);

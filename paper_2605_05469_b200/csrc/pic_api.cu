@@ -12,11 +12,12 @@
 //   SCATTER reorder_deposit (sorted gather + drift + stream out + CIC deposit; the charge
 //           of node plane nzl goes to the next slab's plane 0)
 // P > 1 has two transports.  Peer memory (default): every rank's workspace is mapped
-// (CUDA IPC, NVLink); fft_y_fwd / fft_z_mul store their transpose blocks, fft_x_inv
-// the halo plane, push_key the leavers and reorder_deposit the ghost charge straight
-// into the receiving GPU's buffers, and [xpose] is a stream barrier.  NCCL (PIC_P2P=0
-// or no IPC): [xpose] = ncclAlltoAll, halo/ghost planes by ncclSend/Recv, leavers by
-// counts all-to-all + grouped send/recv.
+// (CUDA IPC, NVLink); fft_x_inv writes the halo plane of the slab below, push_key stages
+// the leavers and k_leaver_copy streams them into the destination's receive buffer, the
+// ghost charge plane is pulled over NVLink by the slab above (k_add_plane after a
+// barrier); the FFT transposes stay ncclAlltoAll (the peer-store variant, PIC_P2P=2,
+// measured slower).  NCCL (PIC_P2P=0 or no IPC): [xpose] = ncclAlltoAll, halo/ghost
+// planes by ncclSend/Recv, leavers by counts all-to-all + grouped send/recv.
 #include <nccl.h>
 
 #include <algorithm>
@@ -175,11 +176,6 @@ pic_status validate(const pic_params* p, int32_t rank, int32_t nranks, char* msg
             snprintf(msg, msz, "b_ext / e_ext must be finite");
             return PIC_EINVAL;
         }
-    const double np = (double)p->ppc * p->n * p->n * p->n / nranks;
-    if (np * (nranks > 1 ? 1.3 : 1.0) >= 4294967296.0) {
-        snprintf(msg, msz, "N_p per rank = %.0f too large for 32-bit indices", np);
-        return PIC_EINVAL;
-    }
     return PIC_OK;
 }
 
@@ -249,6 +245,17 @@ Sizes sizes(const pic_params* p, const Geom& g) {
     }
     s.nkey = s.np_cap + s.recv_cap;
     return s;
+}
+
+// The arrays indexed with uint32 (key, rank, perm, offs; the old index packed in a
+// leaver's record) span the extended index space nkey = capacity + receive buffer.
+pic_status validate_sizes(const Sizes& z, char* msg, size_t msz) {
+    if ((double)z.nkey >= 4294967295.0 || (double)z.np_cap >= 4294967295.0) {
+        snprintf(msg, msz, "particle index space of a rank (capacity %lld + receive buffer %lld) too large "
+                 "for 32-bit indices", (long long)z.np_cap, (long long)z.recv_cap);
+        return PIC_EINVAL;
+    }
+    return PIC_OK;
 }
 
 // Carve the workspace; returns the bytes needed (pointers set when c != nullptr).
@@ -438,6 +445,20 @@ T* on_rank(const pic_ctx* c, int r, T* local) {
 // complete (they end with a system fence) when any rank's work after it starts.
 pic_status barrier(pic_ctx* c) {
     PIC_NCCL(c, ncclAllReduce(c->bar, c->bar, 1, ncclInt, ncclSum, c->comm, c->stream));
+    return PIC_OK;
+}
+
+// A decision every rank must take together (a rank that bails out alone
+// leaves its peers blocked in the next collective): 1 if any rank passes local != 0.
+// Synchronises the stream.
+pic_status agree_any(pic_ctx* c, int local, int* any) {
+    *any = local;
+    if (c->g.P == 1) return PIC_OK;
+    int* d = c->bar + 2;
+    PIC_CUDA(c, cudaMemcpyAsync(d, &local, sizeof(int), cudaMemcpyHostToDevice, c->stream));
+    PIC_NCCL(c, ncclAllReduce(d, d, 1, ncclInt, ncclMax, c->comm, c->stream));
+    PIC_CUDA(c, cudaMemcpyAsync(any, d, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+    PIC_CUDA(c, cudaStreamSynchronize(c->stream));
     return PIC_OK;
 }
 
@@ -865,12 +886,18 @@ pic_status push_sort_deposit(pic_ctx* c, int push) {
         PIC_CUDA(c, cudaMemcpyAsync(sc, c->send_count, sizeof(uint32_t) * g.P, cudaMemcpyDeviceToHost, c->stream));
         PIC_CUDA(c, cudaMemcpyAsync(rc, c->recv_count, sizeof(uint32_t) * g.P, cudaMemcpyDeviceToHost, c->stream));
         PIC_CUDA(c, cudaStreamSynchronize(c->stream));
+        int over = 0;
         for (int r = 0; r < g.P; ++r) {
-            if (sc[r] > (uint32_t)c->segs.cap[r]) return fail(c, PIC_EOVERFLOW, "migration send segment overflow");
+            if (sc[r] > (uint32_t)c->segs.cap[r]) over = 1;
             nleave += sc[r];
             narr += rc[r];
         }
-        if (narr > c->recv_cap) return fail(c, PIC_EOVERFLOW, "migration receive buffer overflow");
+        if (narr > c->recv_cap) over = 1;
+        int any = 0;
+        PIC_TRY(agree_any(c, over, &any));       // every rank returns, none is left in the send/recv
+        if (any)
+            return fail(c, PIC_EOVERFLOW, over ? "migration send segment or receive buffer overflow"
+                                               : "migration overflow on another rank");
         PIC_NCCL(c, ncclGroupStart());
         int64_t roff = 0;
         for (int r = 0; r < g.P; ++r) {
@@ -889,7 +916,13 @@ pic_status push_sort_deposit(pic_ctx* c, int push) {
         n_bound = n_old + narr;
     }
     const int64_t n_new = n_old - nleave + narr;
-    if (!peer_mig && n_new > c->np_cap) return fail(c, PIC_EOVERFLOW, "slab holds more particles than its capacity");
+    if (!peer_mig && push && g.P > 1) {
+        int any = 0;
+        PIC_TRY(agree_any(c, n_new > c->np_cap, &any));
+        if (any) return fail(c, PIC_EOVERFLOW, "a slab holds more particles than its capacity");
+    } else if (!peer_mig && n_new > c->np_cap) {
+        return fail(c, PIC_EOVERFLOW, "slab holds more particles than its capacity");
+    }
     { StageScope t(c, PIC_STAGE_SCAN, 3); pic::launch_scan(c->count, c->offs, c->ncell, c->scan_scratch, c->stream); }
     PIC_LAUNCHED(c, "scan");
     { StageScope t(c, PIC_STAGE_PLACE, 1); pic::launch_place(c->key, c->rank, n_bound, c->offs, c->perm, dc, c->np_cap, c->err_flag, c->stream); }
@@ -930,8 +963,13 @@ pic_status sync_check(pic_ctx* c) {
         PIC_CUDA(c, cudaMemset(c->err_flag + 1, 0, sizeof(int)));
         return fail(c, PIC_EINVAL, "imported position outside [0, L) or outside this rank's slab");
     }
-    if (flag[0] || flag[2])
-        return fail(c, PIC_EOVERFLOW, "capacity exceeded: > 2048 particles in one cell or a full migration segment (D#23)");
+    if (flag[0] || flag[2]) {
+        char what[256];
+        snprintf(what, sizeof(what),
+                 "capacity exceeded: > %d particles in one cell, or a slab / migration segment full (D#23, D#25)",
+                 pic::reorder_cell_capacity(c->g.P));
+        return fail(c, PIC_EOVERFLOW, what);
+    }
     if (c->g.P > 1 && c->comm) {
         ncclResult_t ar = ncclSuccess;
         if (ncclCommGetAsyncError(c->comm, &ar) == ncclSuccess && ar != ncclSuccess) {
@@ -1081,7 +1119,12 @@ pic_status pic_workspace_bytes(const pic_params* p, int32_t rank, int32_t nranks
     if (st != PIC_OK) { snprintf(g_init_error, sizeof(g_init_error), "%s", msg); return st; }
     if (!bytes) return PIC_EINVAL;
     const Geom g = make_geom(p, rank, nranks);
-    *bytes = carve(nullptr, g, sizes(p, g), nullptr);
+    const Sizes z = sizes(p, g);
+    if ((st = validate_sizes(z, msg, sizeof(msg))) != PIC_OK) {
+        snprintf(g_init_error, sizeof(g_init_error), "%s", msg);
+        return st;
+    }
+    *bytes = carve(nullptr, g, z, nullptr);
     return PIC_OK;
 }
 
@@ -1110,6 +1153,10 @@ pic_status pic_init(const pic_params* p, int32_t rank, int32_t nranks, const uin
     }
     const Geom g = make_geom(p, rank, nranks);
     const Sizes z = sizes(p, g);
+    if ((st = validate_sizes(z, msg, sizeof(msg))) != PIC_OK) {
+        snprintf(g_init_error, sizeof(g_init_error), "%s", msg);
+        return st;
+    }
     const size_t need = carve(nullptr, g, z, nullptr);
     if (!workspace || workspace_bytes < need) {
         snprintf(g_init_error, sizeof(g_init_error), "workspace %zu B < %zu B needed", workspace_bytes, need);
@@ -1128,8 +1175,22 @@ pic_status pic_init(const pic_params* p, int32_t rank, int32_t nranks, const uin
     c->stream = reinterpret_cast<cudaStream_t>(cuda_stream);
     carve(c, c->g, z, reinterpret_cast<char*>(workspace));
 
-    static bool smem_set = false;
-    if (!smem_set) { pic::fft_set_smem_limits(); pic::particles_set_smem_limits(); smem_set = true; }
+    // the dynamic shared-memory opt-in is a per-device attribute: set it once per device
+    static unsigned smem_set = 0;      // bit d: device d done
+    {
+        int dev = 0;
+        cudaError_t e0 = cudaGetDevice(&dev);
+        if (e0 == cudaSuccess && dev < 32 && !(smem_set & (1u << dev))) {
+            e0 = pic::fft_set_smem_limits();
+            if (e0 == cudaSuccess) e0 = pic::particles_set_smem_limits();
+            if (e0 == cudaSuccess) smem_set |= 1u << dev;
+        }
+        if (e0 != cudaSuccess) {
+            snprintf(g_init_error, sizeof(g_init_error), "shared-memory opt-in: %s", cudaGetErrorString(e0));
+            delete c;
+            return PIC_ECUDA;
+        }
+    }
 
     auto bail = [&](pic_status s) {
         snprintf(g_init_error, sizeof(g_init_error), "%s", c->err);
@@ -1181,7 +1242,9 @@ pic_status pic_init(const pic_params* p, int32_t rank, int32_t nranks, const uin
         e = cudaMemcpyAsync(&total, c->perm + nblk, sizeof(uint32_t), cudaMemcpyDeviceToHost, c->stream);
         if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
         if (e != cudaSuccess) return bail(fail(c, PIC_ECUDA, "sample count", e));
-        if ((int64_t)total > c->np_cap) return bail(fail(c, PIC_EOVERFLOW, "slab capacity exceeded at init"));
+        int any = 0;
+        if ((st = agree_any(c, (int64_t)total > c->np_cap, &any)) != PIC_OK) return bail(st);
+        if (any) return bail(fail(c, PIC_EOVERFLOW, "slab capacity exceeded at init (on this or another rank)"));
         c->np = total;
         pic::launch_sample_write(g, state(c, 0), c->np_glob, p->k, p->alpha, p->seed, c->perm, c->stream);
     }
@@ -1282,6 +1345,111 @@ pic_status pic_get_particles(pic_ctx* c, double* xyzuvw, int64_t np) {
     PIC_LAUNCHED(c, "pairs_to_soa");
     PIC_CUDA(c, cudaMemcpyAsync(xyzuvw, soa, sizeof(double) * 6 * (size_t)np, cudaMemcpyDeviceToHost, c->stream));
     return sync_check(c);
+}
+
+pic_status pic_gather_particles(pic_ctx* c, double* xyzuvw, int64_t np_total, int64_t* np_out) {
+    PIC_CHECK_CTX(c);
+    const Geom& g = c->g;
+    if (g.P == 1) {
+        if (np_out) *np_out = c->np;
+        if (!xyzuvw) return PIC_OK;
+        return pic_get_particles(c, xyzuvw, np_total);
+    }
+    PIC_TRY(sync_check(c));               // np up to date (peer transport: device counts)
+    // every rank's count (int64) -> all ranks
+    int64_t* dcounts = reinterpret_cast<int64_t*>(c->specC);     // scratch outside a solve
+    int64_t mine = c->np;
+    std::vector<int64_t> counts(g.P);
+    PIC_CUDA(c, cudaMemcpyAsync(dcounts + 8, &mine, sizeof(int64_t), cudaMemcpyHostToDevice, c->stream));
+    PIC_NCCL(c, ncclAllGather(dcounts + 8, dcounts, 1, ncclInt64, c->comm, c->stream));
+    PIC_CUDA(c, cudaMemcpyAsync(counts.data(), dcounts, sizeof(int64_t) * g.P, cudaMemcpyDeviceToHost, c->stream));
+    PIC_CUDA(c, cudaStreamSynchronize(c->stream));
+    int64_t total = 0;
+    for (int r = 0; r < g.P; ++r) total += counts[r];
+    if (np_out) *np_out = total;
+    int want = 0;                          // rank 0 decides whether to gather, every rank follows
+    if (g.rank == 0) want = xyzuvw ? (np_total == total ? 1 : 2) : 0;
+    int* dflag = c->bar + 3;
+    PIC_CUDA(c, cudaMemcpyAsync(dflag, &want, sizeof(int), cudaMemcpyHostToDevice, c->stream));
+    PIC_NCCL(c, ncclBroadcast(dflag, dflag, 1, ncclInt, 0, c->comm, c->stream));
+    PIC_CUDA(c, cudaMemcpyAsync(&want, dflag, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+    PIC_CUDA(c, cudaStreamSynchronize(c->stream));
+    if (want == 0) return PIC_OK;
+    if (want == 2) {
+        snprintf(c->err, sizeof(c->err), "pic_gather_particles: np_total %lld != %lld particles on all ranks",
+                 (long long)np_total, (long long)total);
+        return PIC_EINVAL;
+    }
+    // this rank's canonical SoA [6][np_r] in its idle buffer; rank 0 copies its own, then
+    // receives rank r's into the same buffer (every rank's np_r <= the common capacity)
+    double* soa = reinterpret_cast<double*>(c->part[c->cur ^ 1][0]);
+    pic::launch_pairs_to_soa(state(c, c->cur), c->np, soa, c->stream);
+    PIC_LAUNCHED(c, "pairs_to_soa");
+    int64_t off = 0;
+    for (int r = 0; r < g.P; ++r) {
+        const int64_t nr = counts[r];
+        if (r > 0 && nr > 0) {
+            PIC_NCCL(c, ncclGroupStart());
+            if (g.rank == r) PIC_NCCL(c, ncclSend(soa, (size_t)(6 * nr), ncclDouble, 0, c->comm, c->stream));
+            if (g.rank == 0) PIC_NCCL(c, ncclRecv(soa, (size_t)(6 * nr), ncclDouble, r, c->comm, c->stream));
+            PIC_NCCL(c, ncclGroupEnd());
+        }
+        if (g.rank == 0 && nr > 0) {
+            PIC_CUDA(c, cudaMemcpy2DAsync(xyzuvw + off, sizeof(double) * (size_t)total, soa, sizeof(double) * (size_t)nr,
+                                          sizeof(double) * (size_t)nr, 6, cudaMemcpyDeviceToHost, c->stream));
+            PIC_CUDA(c, cudaStreamSynchronize(c->stream));   // the buffer is reused for the next rank
+        }
+        off += nr;
+    }
+    PIC_TRY(sync_check(c));
+    if (g.rank != 0 || total == 0) return PIC_OK;
+    // global canonical order: stable counting sort by the global Morton cell key (D#5, D#14)
+    const int64_t ncell = (int64_t)g.n * g.n * g.n;
+    auto cell = [&](double x) {
+        int i = (int)std::floor(x * g.inv_h);
+        return i > g.n - 1 ? g.n - 1 : (i < 0 ? 0 : i);
+    };
+    auto morton = [&](int ix, int iy, int iz) {
+        uint32_t k = 0;
+        for (int b = 0; (1 << b) < g.n; ++b)
+            k |= ((uint32_t)((ix >> b) & 1) << (3 * b)) | ((uint32_t)((iy >> b) & 1) << (3 * b + 1)) |
+                 ((uint32_t)((iz >> b) & 1) << (3 * b + 2));
+        return k;
+    };
+    std::vector<uint32_t> key((size_t)total);
+    for (int64_t j = 0; j < total; ++j)
+        key[j] = morton(cell(xyzuvw[j]), cell(xyzuvw[total + j]), cell(xyzuvw[2 * total + j]));
+    std::vector<int64_t> start((size_t)ncell + 1, 0);
+    for (int64_t j = 0; j < total; ++j) start[key[j] + 1] += 1;
+    for (int64_t k = 0; k < ncell; ++k) start[k + 1] += start[k];
+    std::vector<int64_t> dst((size_t)total);
+    for (int64_t j = 0; j < total; ++j) dst[j] = start[key[j]]++;
+    std::vector<double> tmp((size_t)total);
+    for (int a = 0; a < 6; ++a) {
+        double* col = xyzuvw + (int64_t)a * total;
+        for (int64_t j = 0; j < total; ++j) tmp[dst[j]] = col[j];
+        std::memcpy(col, tmp.data(), sizeof(double) * (size_t)total);
+    }
+    return PIC_OK;
+}
+
+pic_status pic_owner_ranks(const pic_params* p, int32_t nranks, const double* xyz, int64_t np, int32_t* owner) {
+    char msg[256];
+    pic_status st = validate(p, 0, nranks, msg, sizeof(msg));
+    if (st != PIC_OK) { snprintf(g_init_error, sizeof(g_init_error), "%s", msg); return st; }
+    if (np < 0 || (np > 0 && (!xyz || !owner))) return PIC_EINVAL;
+    const Geom g = make_geom(p, 0, nranks);
+    const double* z = xyz + 2 * np;
+    for (int64_t j = 0; j < np; ++j) {
+        if (!(z[j] >= 0.0 && z[j] < g.L)) {
+            snprintf(g_init_error, sizeof(g_init_error), "pic_owner_ranks: z[%lld] outside [0, L)", (long long)j);
+            return PIC_EINVAL;
+        }
+        int iz = (int)std::floor(z[j] * g.inv_h);      // D#5: floor(z inv_h), clamped to N - 1
+        iz = iz > g.n - 1 ? g.n - 1 : iz;
+        owner[j] = iz / g.nzl;
+    }
+    return PIC_OK;
 }
 
 pic_status pic_set_particles(pic_ctx* c, const double* xyzuvw, int64_t np) {

@@ -682,6 +682,12 @@ struct Stage {
     }
 };
 
+#define PIC_TRY_PIF(expr)                   \
+    do {                                    \
+        pic_status s_ = (expr);             \
+        if (s_ != PIC_OK) return s_;        \
+    } while (0)
+
 pic_status flush_timing(pic_pif* p) {
     if (!p->timing) return PIC_OK;
     PIF_CUDA(p, cudaStreamSynchronize(p->stream));
@@ -1019,9 +1025,14 @@ pic_status pic_pif_step(pic_pif* p, int64_t np, double* x, double* v, const doub
         pic_status st = solve_core(p, np, x, q, E);
         p->hist_slot = -1;
         if (st) return st;
-        Stage t(p, PIC_PIF_PUSH);
-        if (np > 0) k_pif_push<<<particle_grid(np), kThreads, 0, p->stream>>>(np, x, v, E, qm_dt, dt, p->L);
-        PIF_LAUNCHED(p);
+        {
+            Stage t(p, PIC_PIF_PUSH);
+            if (np > 0) k_pif_push<<<particle_grid(np), kThreads, 0, p->stream>>>(np, x, v, E, qm_dt, dt, p->L);
+            PIF_LAUNCHED(p);
+        }
+        // with timing on, collect every step's events (the pool holds 256 event pairs, so a
+        // long call would otherwise drop the later steps' stage times)
+        if (p->timing) PIC_TRY_PIF(flush_timing(p));
     }
     if (ex_energy) {
         PIF_CUDA(p, cudaMemcpyAsync(ex_energy, p->hist, nsteps * sizeof(double), cudaMemcpyDeviceToHost,

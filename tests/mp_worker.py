@@ -60,6 +60,7 @@ def main():
     got = sim.get_particles()
     keys, _ = sim.keys_perm()
     mig = sim.migrated()
+    gathered = sim.gather_particles()       # pic_gather_particles: rank 0, global canonical order
     transport = "peer" if sim.peer_transport() else "nccl"
     want = os.environ.get("MP_EXPECT_TRANSPORT")
     assert want is None or want == transport, f"transport {transport}, expected {want}"
@@ -70,6 +71,8 @@ def main():
         allk = np.concatenate([p[1] for p in parts])
         order = np.argsort(allk, kind="stable")
         allx, allk = allx[:, order], allk[order]
+        # the library's rank-0 gather equals the merge of the ranks' exports bit for bit
+        assert gathered is not None and np.array_equal(gathered, allx)
         ref, rex = oracle_run(xv, steps)
         assert allx.shape == ref.shape, (allx.shape, ref.shape)
         assert np.all(np.diff(allk.astype(np.int64)) >= 0)

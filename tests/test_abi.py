@@ -135,3 +135,25 @@ def test_pif_parameter_validation_without_gpu():
     assert pkg.lib().pic_nufft_type1(None, 1, None, None, None) == B.PIC_EINVAL
     assert pkg.lib().pic_pif_solve(None, 1, None, None, None, None) == B.PIC_EINVAL
     assert B.PIF_STAGES == ["spread", "fft", "modes", "fill", "interp", "push", "bin"]
+
+
+def test_owner_ranks_partition_by_slab():
+    """pic_owner_ranks: rank = the slab of the cell plane floor(z N / L)
+    clamped to N - 1 (D#5), restated here; z = L is rejected."""
+    import numpy as np
+    from paper_2605_05469_b200 import owner_ranks
+    from paper_2605_05469_b200._binding import PicError
+
+    n, L = 32, 4 * np.pi
+    rng = np.random.default_rng(5)
+    xv = rng.random((6, 10000)) * L
+    xv[2, :4] = [0.0, np.nextafter(L, 0), 15.999999 * L / n, 16 * L / n]
+    for world in (1, 2, 4, 8):
+        own = owner_ranks(xv, n, L, world)
+        iz = np.minimum(np.floor(xv[2] * (n / L)).astype(np.int64), n - 1)
+        assert np.array_equal(own, iz // (n // world))
+    assert list(owner_ranks(xv, n, L, 2)[:4]) == [0, 1, 0, 1]
+    bad = xv.copy()
+    bad[2, 7] = L
+    with pytest.raises(PicError):
+        owner_ranks(bad, n, L, 2)
