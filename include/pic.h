@@ -246,6 +246,16 @@ const char *pic_stage_name(int32_t stage);
  * with the latest solve's iteration count). */
 pic_status pic_launches_per_step(pic_ctx *ctx, int64_t *launches);
 
+/* Diagnostics (not part of the step): time `reps` launches of a bandwidth
+ * probe on this context's live data with the permutation of the latest sort --
+ * mode 0: streaming copy of the particle state (96 B per particle), 1: the reorder's
+ * gather alone through perm (100 B), 2: the place pattern alone, a 4-B scatter through
+ * perm (8 B), 3: streaming read of the state (48 B).  The idle particle buffer and the
+ * key array are overwritten (scratch between steps); the state is unchanged.
+ * *ms = mean milliseconds per launch (CUDA events), *bytes = bytes per launch.
+ * PIC_EINVAL: unknown mode or reps < 1.  Synchronous. */
+pic_status pic_diag_bandwidth(pic_ctx *ctx, int32_t mode, int32_t reps, double *ms, double *bytes);
+
 /* PCG / FEM (CG) solver statistics: iterations of the latest solve (-1: not converged), total
  * iterations and solves since pic_init, relative residual ||r||/||b|| of the latest
  * solve.  Any pointer may be NULL.  PIC_EINVAL for an FFT context. */

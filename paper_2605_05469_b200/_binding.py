@@ -92,6 +92,7 @@ SYMBOLS = {
     "pic_reset_timings": (C.c_int, [_vp]),
     "pic_stage_name": (C.c_char_p, [C.c_int32]),
     "pic_launches_per_step": (C.c_int, [_vp, _i64p]),
+    "pic_diag_bandwidth": (C.c_int, [_vp, C.c_int32, C.c_int32, _dp, _dp]),
     "pic_pcg_stats": (C.c_int, [_vp, C.POINTER(C.c_int32), _i64p, _i64p, _dp]),
     # include/pif.h
     "pic_pif_workspace_bytes": (C.c_int, [C.c_int32, C.c_double, C.c_double, C.c_int64, C.POINTER(C.c_size_t)]),
@@ -261,6 +262,12 @@ class Simulation:
         assert out.shape == (6, npl)
         _check(lib().pic_get_particles(self.ctx, _d(out), npl), self.ctx)
         return out
+
+    def diag_bandwidth(self, mode: int, reps: int = 3):
+        """(ms per launch, bytes per launch) of a bandwidth probe (pic_diag_bandwidth)."""
+        ms, b = C.c_double(), C.c_double()
+        _check(lib().pic_diag_bandwidth(self.ctx, mode, reps, C.byref(ms), C.byref(b)), self.ctx)
+        return ms.value, b.value
 
     def gather_particles(self, out: np.ndarray | None = None):
         """Collective: rank 0 returns every rank's particles in the global canonical order

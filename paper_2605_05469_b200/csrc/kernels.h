@@ -181,6 +181,10 @@ void launch_fem_update(const Geom& g, double* x, const double* p, double* r, con
 void launch_fem_gradient(const Geom& g, PcgNbr x, double* E4, double* halo, double* partials, double* energies,
                          cudaStream_t s);
 
+// Bandwidth probes (diag_kernels.cu): returns the bytes one launch moves, < 0 for an
+// unknown mode.
+double launch_diag(int mode, PState cur, PState idle, const uint32_t* perm, uint32_t* scratch, int64_t np,
+                   double* sink, cudaStream_t s);
 cudaError_t particles_set_smem_limits();
 cudaError_t fft_set_smem_limits();
 // Largest cell population the reorder handles (particles staged per chunk; a larger

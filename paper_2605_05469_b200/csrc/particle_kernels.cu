@@ -258,6 +258,10 @@ __global__ void __launch_bounds__(kThreads, MR ? 3 : 4) k_push_key_brick(Geom g,
     __syncthreads();
     double xn[3], vn[3];
     if (P0 + t < P1) load_particle(cur, P0 + t, xn, vn);
+    // The count atomic's return (the arrival rank) is consumed one iteration later, so
+    // its L2 round trip overlaps the next particle's gather and push instead of
+    // stalling the warp (ncu r01: 59% of the stalls sat on the returned rank).
+    uint32_t r_prev = 0u, i_prev = 0xffffffffu;
     for (uint32_t i = P0 + t; i < P1; i += kThreads) {
         double x[3] = {xn[0], xn[1], xn[2]}, v[3] = {vn[0], vn[1], vn[2]};
         // next particle's loads in flight while this one waits on its count atomic
@@ -311,8 +315,16 @@ __global__ void __launch_bounds__(kThreads, MR ? 3 : 4) k_push_key_brick(Geom g,
         }
         key[i] = k;
         const uint32_t r = atomicAdd(count + k, 1u);
-        if (r > 0xffffu) atomicExch(err, 1);
-        rank[i] = (uint16_t)r;
+        if (i_prev != 0xffffffffu) {
+            if (r_prev > 0xffffu) atomicExch(err, 1);
+            rank[i_prev] = (uint16_t)r_prev;
+        }
+        r_prev = r;
+        i_prev = i;
+    }
+    if (i_prev != 0xffffffffu) {
+        if (r_prev > 0xffffu) atomicExch(err, 1);
+        rank[i_prev] = (uint16_t)r_prev;
     }
     if (MR) {      // one global atomic per destination, then the staged payloads
         __syncthreads();

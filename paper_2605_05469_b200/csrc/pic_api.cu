@@ -82,6 +82,8 @@ struct pic_ctx {
     double2* specB = nullptr;     // ky-pencil (P = 1: rho)
     double2* specC = nullptr;     // 3 components: z-pass out, y-inverse out
     double2* specD = nullptr;     // return transpose receive (P = 1: specC)
+    bool spec_alias = false;      // P = 1: specC/specD inside the idle particle buffer (bind_spec)
+    size_t spec_unit = 0;
     double* E4 = nullptr;         // (nzl + 1) planes of node records (E_x, E_y, E_z, 0)
     double* ghost = nullptr;      // P > 1: received ghost plane of rho
     double2* tw = nullptr;
@@ -258,6 +260,15 @@ pic_status validate_sizes(const Sizes& z, char* msg, size_t msz) {
     return PIC_OK;
 }
 
+// P = 1 with spec_alias: point the spectral scratch at the particle buffer that does not
+// hold the state (cur ^ 1).  Called before every use of specC / specD.
+void bind_spec(pic_ctx* c) {
+    if (!c->spec_alias) return;
+    char* idle = reinterpret_cast<char*>(c->part[c->cur ^ 1][0]);
+    c->specC = reinterpret_cast<double2*>(idle);
+    c->specD = reinterpret_cast<double2*>(idle + c->spec_unit);
+}
+
 // Carve the workspace; returns the bytes needed (pointers set when c != nullptr).
 size_t carve(pic_ctx* c, const Geom& g, const Sizes& z, char* base) {
     size_t off = 0;
@@ -288,7 +299,12 @@ size_t carve(pic_ctx* c, const Geom& g, const Sizes& z, char* base) {
     char* rh = take(plane * (size_t)(g.nzl + 1));
     char* sA = g.P > 1 ? take(unit) : nullptr;
     char* sB = g.P > 1 ? take(unit) : nullptr;
-    char* sC = take(3 * unit);
+    // P = 1: the three spectral components live in the idle particle buffer when it is
+    // large enough (48 B x capacity >= 3 units; ppc >= 1 at N >= 32): the solve runs
+    // between a reorder and the next push, when that buffer holds nothing.  Saves
+    // 24 B per node (26 GB at 1024^3, which makes 1024^3 x 1 ppc fit one GPU).
+    const bool spec_alias = g.P == 1 && 48 * (size_t)z.np_cap >= 3 * unit;
+    char* sC = spec_alias ? nullptr : take(3 * unit);
     char* sD = g.P > 1 ? take(2 * unit) : nullptr;
     char* e4 = take(sizeof(double) * 4 * (size_t)g.n * g.n * (g.nzl + 1));
     char* gh = g.P > 1 ? take(plane) : nullptr;
@@ -322,10 +338,13 @@ size_t carve(pic_ctx* c, const Geom& g, const Sizes& z, char* base) {
         c->rho = reinterpret_cast<double*>(rh);
         c->specA = g.P > 1 ? reinterpret_cast<double2*>(sA) : reinterpret_cast<double2*>(rh);
         c->specB = g.P > 1 ? reinterpret_cast<double2*>(sB) : reinterpret_cast<double2*>(rh);
+        c->spec_alias = spec_alias;
+        c->spec_unit = unit;
         c->specC = reinterpret_cast<double2*>(sC);
         // P = 1: the z pass's two components go to units 1-2 of specC; the field y pass
         // reads each tile whole before writing units 0-2 over the same footprint
         c->specD = reinterpret_cast<double2*>(g.P > 1 ? sD : sC + unit);
+        if (spec_alias) bind_spec(c);
         c->E4 = reinterpret_cast<double*>(e4);
         c->ghost = reinterpret_cast<double*>(gh);
         c->tw = reinterpret_cast<double2*>(tw);
@@ -537,6 +556,7 @@ pic_status fold_rho_ghost(pic_ctx* c) {
 // halo plane, energies (summed over ranks) -> ring slot.
 pic_status solve(pic_ctx* c, double scale, int slot) {
     const Geom& g = c->g;
+    bind_spec(c);
     const size_t unit = (size_t)g.nzl * g.n * g.px;   // complex per slab half spectrum
     const SpecLayout S0{reinterpret_cast<double2*>(c->rho), 0, 1, nullptr};
     SpecLayout A{c->specA, 1, 1, nullptr};          // forward transpose, send side
@@ -1469,6 +1489,7 @@ pic_status pic_set_particles(pic_ctx* c, const double* xyzuvw, int64_t np) {
 
 pic_status pic_get_grid(pic_ctx* c, int32_t which, double* host) {
     PIC_CHECK_CTX(c);
+    bind_spec(c);
     if (!host || which < 0 || which > 4 || (which == 4 && !c->pcg_x)) return PIC_EINVAL;
     if (which == 0) {
         PIC_TRY(copy_grid_to_host(c, host, c->rho));
@@ -1506,6 +1527,7 @@ pic_status pic_solve_injected(pic_ctx* c, const double* rho_host, double* E_host
     double en[2];
     PIC_CUDA(c, cudaMemcpyAsync(en, c->energies, sizeof(en), cudaMemcpyDeviceToHost, c->stream));
     if (E_host) {
+        bind_spec(c);
         double* scratch = reinterpret_cast<double*>(c->specC);
         for (int d = 0; d < 3; ++d) {
             pic::launch_e4_extract(c->g, c->E4, d, scratch, c->stream);
@@ -1525,6 +1547,7 @@ pic_status pic_solve_injected(pic_ctx* c, const double* rho_host, double* E_host
 
 pic_status pic_push_injected(pic_ctx* c, const double* E_host) {
     PIC_CHECK_CTX(c);
+    bind_spec(c);
     if (!E_host) return PIC_EINVAL;
     double* sc = reinterpret_cast<double*>(c->specC);   // scratch: 3 compact slab components
     double* const comp[3] = {sc, sc + c->ncell, sc + 2 * c->ncell};
@@ -1590,6 +1613,30 @@ pic_status pic_launches_per_step(pic_ctx* c, int64_t* launches) {
     // the NCCL transport's ghost fold 1 or the peer transport's count update 1
     *launches = 12 + (c->g.P > 1 ? 2 : 0) + (c->g.P > 1 && c->p2p && pic::leavers_batched() ? 2 : 0);
     if (c->p.solver != PIC_SOLVER_FFT) *launches += c->pcg_launches - 6;   // the latest CG solve's count
+    return PIC_OK;
+}
+
+pic_status pic_diag_bandwidth(pic_ctx* c, int32_t mode, int32_t reps, double* ms, double* bytes) {
+    PIC_CHECK_CTX(c);
+    if (reps < 1 || mode < 0 || mode > 3) return PIC_EINVAL;
+    PIC_TRY(sync_check(c));
+    cudaEvent_t e0, e1;
+    PIC_CUDA(c, cudaEventCreate(&e0));
+    PIC_CUDA(c, cudaEventCreate(&e1));
+    double b = 0.0;
+    PIC_CUDA(c, cudaEventRecord(e0, c->stream));
+    for (int r = 0; r < reps; ++r)
+        b = pic::launch_diag(mode, state(c, c->cur), state(c, c->cur ^ 1), c->perm, c->key, c->np,
+                             c->partials, c->stream);
+    PIC_CUDA(c, cudaEventRecord(e1, c->stream));
+    PIC_CUDA(c, cudaEventSynchronize(e1));
+    float t = 0.f;
+    PIC_CUDA(c, cudaEventElapsedTime(&t, e0, e1));
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    PIC_LAUNCHED(c, "diag");
+    if (ms) *ms = t / reps;
+    if (bytes) *bytes = b;
     return PIC_OK;
 }
 

@@ -7,6 +7,8 @@ BASELINE.json north_star):
   W_x per step ....................................... 1e-10 relative
   x, v after 20 steps ................................ 1e-12 (periodic |dx|/L, |dv|/max(|v|,1))
 """
+import os
+
 import numpy as np
 import pytest
 
@@ -101,12 +103,16 @@ def test_deposit_special_positions(Sim):
     assert np.max(np.abs(rho - ref)) <= 1e-14 * np.max(np.abs(ref))
 
 
-@pytest.mark.parametrize("n", [16, 64])
+@pytest.mark.parametrize("n", [16, 64, 128, 256])
 def test_solve_matches_oracle(Sim, n):
+    """Element-wise solve parity.  At 128^3 and 256^3 every persistent CTA of the x / y
+    passes handles several tiles, so the cp.async next-tile prefetch path runs under the
+    element-wise check (at 64^3 each CTA gets at most one tile)."""
     rho = random_grid(n, seed=n, mean=-1.0)
     sim = Sim(n=n, ppc=1, half_kick=False)
     E, wx, w = sim.solve_injected(rho)
-    ref, _ = O.solve_fft(n, L, rho)
+    with O.threads(min(16, os.cpu_count() or 1)):     # OpenMP mode: the same per-line FFT arithmetic
+        ref, _ = O.solve_fft(n, L, rho)
     assert np.max(np.abs(E - ref)) <= 1e-12 * np.max(np.abs(ref))
     rwx, rw = O.field_energy(n, L, ref)
     assert abs(wx - rwx) <= 1e-12 * rwx and abs(w - rw) <= 1e-12 * rw
