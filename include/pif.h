@@ -5,7 +5,8 @@
  * "P:n" = PAPER.md line n, "S:n" = SPEC.md line n, "D#k" = DESIGN.md reading k.
  *
  * Conventions (as pic.h: PIC_OK or a negative pic_status, no exceptions, no prints):
- *  - Modes: K_N = (2 pi / L) [-N/2, N/2 - 1]^3, N even, 8 <= N <= 1024.  A mode
+ *  - Modes: K_N = (2 pi / L) [-N/2, N/2 - 1]^3, N a power of two, 8 <= N <= 512 (the fine
+ *    grid M = 2N is transformed by the repo's own FFT passes, M <= 1024).  A mode
  *    array is N^3 complex values (interleaved re, im doubles) indexed
  *    [(nz + N/2) N + (ny + N/2)] N + (nx + N/2) (n ascending).
  *  - Positions: device SoA x[3][np] doubles (x, y, z), each in [0, L).  Weights f[np],
@@ -15,11 +16,11 @@
  *    beta = 2.30 w, on the sigma = 2 oversampled grid M = 2N (D#34).
  *  - Device memory: the library allocates none; the caller owns one workspace of
  *    pic_pif_workspace_bytes() bytes (fine grid M^3 complex, two N^3 complex spectra, the
- *    FFT's scratch) and the stream; both must outlive the plan.
- *  - The uniform FFT on the fine grid is cuFFT (Z2Z, work area inside the workspace);
- *    spreading, interpolation, mode selection, deconvolution and the Poisson step are
- *    this library's kernels.
- *  - A CUDA/cuFFT failure poisons the plan: later calls return PIC_EPOISONED.
+ *    FFT's twiddle table) and the stream; both must outlive the plan.
+ *  - The uniform FFT on the fine grid is this library's radix-8 Stockham passes (in-place
+ *    C2C, one pass per axis; the passes of the FFT-PIC solve), like
+ *    the spreading, interpolation, mode selection, deconvolution and Poisson step.
+ *  - A CUDA failure poisons the plan: later calls return PIC_EPOISONED.
  */
 #ifndef PIC_PIF_H
 #define PIC_PIF_H
@@ -32,14 +33,14 @@ extern "C" {
 typedef struct pic_pif pic_pif;
 
 /* Workspace bytes for modes N, domain length L, accuracy eps and up to np_max particles per
- * call (creates and destroys a cuFFT plan to learn its scratch size: needs a CUDA device).
+ * call (pure host function).
  * np_max > 0 reserves the binned path (4 B per particle + 12 B per bin of 8^3 fine cells, and
  * a second M^3 complex fine grid so the PIF solve gathers E_x, E_y, E_z in one pass;
  * PIC_PIF_SPLIT_INTERP=1 keeps two passes): particles counting-sorted into bins, spreading
  * and interpolation through shared-memory tiles; it applies
  * when 2N is a multiple of 8 and w <= 8 (eps >= 1e-6) and np <= np_max (else, or with
  * PIC_PIF_BINNED=0 in the environment, one global atomic per window point).  PIC_EINVAL: N
- * odd or out of [8, 1024], L <= 0, eps outside [1e-14, 1), np_max outside [0, 2^32). */
+ * not a power of two in [8, 512], L <= 0, eps outside [1e-14, 1), np_max outside [0, 2^32). */
 pic_status pic_pif_workspace_bytes(int32_t n, double length, double eps, int64_t np_max, size_t *bytes);
 
 /* Create a plan on the current device over `workspace` (>= pic_pif_workspace_bytes) and
@@ -78,7 +79,7 @@ pic_status pic_pif_step(pic_pif *p, int64_t np, double *x, double *v, const doub
  * timing makes every call synchronise at its end. */
 enum {
     PIC_PIF_SPREAD = 0, /* C: clear + spread the weights onto the fine grid          */
-    PIC_PIF_FFT,        /* F / F^-1 on the M^3 fine grid (cuFFT)                      */
+    PIC_PIF_FFT,        /* F / F^-1 on the M^3 fine grid (own C2C passes)             */
     PIC_PIF_MODES,      /* chi, D, Poisson, -i k, energy partials (type 1 side)       */
     PIC_PIF_FILL,       /* chi^T D: the fine grid from the spectrum (type 2 side)     */
     PIC_PIF_INTERP,     /* C^T: the window sums at the particles                      */

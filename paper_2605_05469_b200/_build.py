@@ -9,7 +9,6 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(_HERE, "csrc")
 LIB = os.path.join(_HERE, "libpic.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
-CUDA_LIB = os.path.join(os.path.dirname(os.path.dirname(NVCC)), "lib64")   # cuFFT (PIF fine-grid FFT)
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
@@ -45,7 +44,7 @@ def build_lib(force: bool = False, verbose: bool = False) -> str:
     inc, libdir = nccl_dirs()
     extra = os.environ.get("PIC_NVCC_EXTRA", "").split()   # tuning experiments, e.g. -DPIC_X=1
     cmd = [NVCC, *NVCC_FLAGS, *extra, "-I" + inc, "-o", LIB, *srcs, "-L" + libdir, "-l:libnccl.so.2",
-           "-Xlinker", "-rpath," + libdir, "-L" + CUDA_LIB, "-lcufft", "-Xlinker", "-rpath," + CUDA_LIB]
+           "-Xlinker", "-rpath," + libdir]
     if verbose:
         print(" ".join(cmd))
     subprocess.check_call(cmd)

@@ -601,6 +601,56 @@ __global__ void __launch_bounds__(1024) k_energy_reduce(Geom g, const double* __
     }
 }
 
+// ---------------------------------------------------- complex 3D FFT ------
+// In-place C2C transform of an M^3 complex grid [z][y][x] (M = 2^LOGN <= 1024), one pass
+// per axis, unnormalised, sign SIGN (the PIF fine grid: F and F^-1 of P:459-466, DESIGN
+// §6f).  A tile of kC2C elements is read whole into shared memory by stage 0 before the
+// last stage writes it back, so every pass is in place.  x: kC2C / M contiguous rows;
+// y, z: TW = kC2C / M adjacent x columns (each row access one contiguous 16 TW-byte run)
+// of one z plane (y pass) or one y row (z pass).  tw = W_M^m, m < M.
+constexpr int kC2C = 4096;
+__host__ __device__ constexpr int c2c_lines(int M) { return kC2C / M > 8 ? 8 : (kC2C / M < 1 ? 1 : kC2C / M); }
+
+template <int SIGN, int LOGN>
+__global__ void __launch_bounds__(kThreads, 3) k_c2c_rows(double2* __restrict__ g, int64_t nrows,
+                                                          const double2* __restrict__ tw) {
+    extern __shared__ double2 smx[];
+    constexpr int M = 1 << LOGN, R = c2c_lines(M), ls = M + M / 8 + 1;
+    for (int64_t t = blockIdx.x; t * R < nrows; t += gridDim.x) {
+        double2* base = g + t * R * M;
+        const int rows = (int)min((int64_t)R, nrows - t * R);
+        auto src = [&](int l, int e) { return base[(int64_t)l * M + e]; };
+        auto dst = [&](int l, int e, double2 v) { base[(int64_t)l * M + e] = v; };
+        fft_lines<SIGN, false, LOGN, 2, true>(smx, rows, ls, tw, 0, src, dst);
+        __syncthreads();
+    }
+}
+
+// keep > 0: only the lines whose x column (and, with keep_outer, whose outer index) lies in
+// [0, keep) or [M - keep, M) are transformed -- the PIF's mode box K_N (keep = N/2): the
+// inverse transform's other lines are zero (so skipping them is exact), the forward
+// transform's other outputs are never read.
+__device__ __forceinline__ bool c2c_in_box(int64_t i, int M, int keep) { return i < keep || i >= M - keep; }
+
+template <int SIGN, int LOGN>
+__global__ void __launch_bounds__(kThreads, 3) k_c2c_cols(double2* __restrict__ g, int64_t outer_stride,
+                                                          int64_t line_stride_g, const double2* __restrict__ tw,
+                                                          int keep, int keep_outer) {
+    extern __shared__ double2 smx[];
+    constexpr int M = 1 << LOGN, TW = c2c_lines(M), ls = col_stride(M, TW), nct = M / TW;
+    for (int64_t t = blockIdx.x; t < (int64_t)M * nct; t += gridDim.x) {
+        const int64_t o = t / nct, ct = t - o * nct;
+        if (keep > 0 && ((keep_outer && !c2c_in_box(o, M, keep)) ||
+                         !(c2c_in_box(ct * TW, M, keep) || c2c_in_box(ct * TW + TW - 1, M, keep))))
+            continue;
+        double2* base = g + o * outer_stride + ct * TW;
+        auto src = [&](int l, int e) { return base[e * line_stride_g + l]; };
+        auto dst = [&](int l, int e, double2 v) { base[e * line_stride_g + l] = v; };
+        fft_lines<SIGN, false, LOGN, 2, false>(smx, TW, ls, tw, 0, src, dst);
+        __syncthreads();
+    }
+}
+
 }  // namespace
 
 constexpr int kMaxPartials = 4096;
@@ -702,6 +752,37 @@ void launch_fft_x_inv(const Geom& g, const double2* spec, double* E4, double* ha
     const size_t smem = x_inv_smem(g);
     const unsigned grid = x_inv_grid(g);
     PIC_X_SWITCH(ilog2(g.n / 2), (k_fft_x_inv<K><<<grid, kThreads, smem, s>>>(g, spec, E4, halo, tw, partials)))
+}
+
+// In-place 3D C2C FFT of an M^3 complex grid, M a power of two in [16, 1024]: x, y, z passes
+// forward (sign -1), z, y, x inverse (+1); keep > 0 restricts the y and z passes to the
+// lines that meet the box [0, keep) u [M - keep, M) (see c2c_in_box).
+cudaError_t launch_fft_c2c_3d(double2* grid, int M, int sign, const double2* tw, cudaStream_t s, int keep) {
+    const int lg = ilog2(M);
+    if ((1 << lg) != M || lg < 4 || lg > 10) return cudaErrorInvalidValue;
+    const int64_t M2 = (int64_t)M * M;
+    const int R = c2c_lines(M);
+    const size_t srow = sizeof(double2) * (size_t)R * (M + M / 8 + 1);
+    const size_t scol = sizeof(double2) * (size_t)R * col_stride(M, R);
+    const int64_t ntile = M2 * M / ((int64_t)R * M);
+    cudaError_t e = cudaSuccess;
+#define PIC_C2C_ROWS(SG)                                                                                               \
+    (e = cudaFuncSetAttribute(k_c2c_rows<SG, K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)srow),              \
+     (e == cudaSuccess ? (k_c2c_rows<SG, K><<<persistent_grid(k_c2c_rows<SG, K>, srow, ntile), kThreads, srow, s>>>(   \
+          grid, M2, tw), 0) : 0))
+#define PIC_C2C_COLS(SG, OS, LS, KO)                                                                                   \
+    (e = e == cudaSuccess ? cudaFuncSetAttribute(k_c2c_cols<SG, K>, cudaFuncAttributeMaxDynamicSharedMemorySize,       \
+                                                 (int)scol) : e,                                                       \
+     (e == cudaSuccess ? (k_c2c_cols<SG, K><<<persistent_grid(k_c2c_cols<SG, K>, scol, ntile), kThreads, scol, s>>>(   \
+          grid, OS, LS, tw, keep, KO), 0) : 0))
+    if (sign < 0) {
+        PIC_YZ_SWITCH(lg, (PIC_C2C_ROWS(-1), PIC_C2C_COLS(-1, M2, (int64_t)M, 0), PIC_C2C_COLS(-1, (int64_t)M, M2, 1)))
+    } else {
+        PIC_YZ_SWITCH(lg, (PIC_C2C_COLS(+1, (int64_t)M, M2, 1), PIC_C2C_COLS(+1, M2, (int64_t)M, 0), PIC_C2C_ROWS(+1)))
+    }
+#undef PIC_C2C_ROWS
+#undef PIC_C2C_COLS
+    return e == cudaSuccess ? cudaGetLastError() : e;
 }
 
 void launch_e4_extract(const Geom& g, const double* E4, int d, double* out, cudaStream_t s) {

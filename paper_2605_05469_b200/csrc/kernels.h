@@ -42,6 +42,12 @@ void launch_fft_z_mul(const Geom& g, const double2* pencil, SpecLayout out, doub
 void launch_fft_x_inv(const Geom& g, const double2* spec, double* E4, double* halo, const double2* tw,
                       double* partials, cudaStream_t s);
 void launch_energy_reduce(const Geom& g, const double* partials, double* energies, cudaStream_t s);
+// In-place unnormalised 3D C2C FFT of an M^3 complex grid [z][y][x], M = 2^k in [16, 1024],
+// sign -1 (e^{-i k.x}) or +1; tw = W_M^m, m < M (the PIF fine grid, pif.cu).  keep > 0: the
+// y / z passes only touch lines meeting the box [0, keep) u [M - keep, M) in x (and in the
+// outer y of the z pass): exact for an inverse transform of a spectrum that is zero outside
+// that box, and for a forward transform whose outputs outside it are not read.
+cudaError_t launch_fft_c2c_3d(double2* grid, int M, int sign, const double2* tw, cudaStream_t s, int keep = 0);
 // E4 component d <-> compact [nzl][n][n] doubles (host transfers of the field).
 void launch_e4_extract(const Geom& g, const double* E4, int d, double* out, cudaStream_t s);
 void launch_e4_pack(const Geom& g, const double* const comp[3], double* E4, cudaStream_t s);

@@ -3,14 +3,15 @@
 //
 // Pipeline (fine grid M = 2N per dimension, complex [lz][ly][lx]):
 //   type 1  (D chi F C):  k_spread<W> (one thread per particle, w^3 RED.ADD.F64 on the real
-//           parts) -> cuFFT Z2Z forward -> k_select (chi, D) or k_pif_modes (chi, D, Poisson,
+//           parts) -> forward 3D FFT -> k_select (chi, D) or k_pif_modes (chi, D, Poisson,
 //           -i k, energy partials).
 //   type 2  (C^T F^-1 chi^T D):  k_fill (chi^T D: the selected modes scaled, zero elsewhere)
-//           -> cuFFT Z2Z inverse -> k_interp<W> (one thread per particle, w^3 loads).
+//           -> inverse 3D FFT -> k_interp<W> (one thread per particle, w^3 loads).
+// F is the repo's own radix-8 Stockham FFT (fft_kernels.cu, launch_fft_c2c_3d: one in-place
+// pass per axis on the M^3 complex grid), not a library call.
 // The PIF solve packs E^_x + i E^_y into one type-2 transform (each is the transform of a
 // Hermitian spectrum, hence real) and E^_z into a second.
 #include <cuda_runtime.h>
-#include <cufft.h>
 #include <cub/device/device_scan.cuh>
 
 #include <algorithm>
@@ -21,6 +22,7 @@
 #include <new>
 
 #include "../../include/pif.h"
+#include "kernels.h"
 
 namespace {
 
@@ -28,6 +30,7 @@ constexpr int kThreads = 256;
 constexpr int kModeBlocks = 1184;      // 148 SMs x 8: the mode kernels' grid (energy partials)
 constexpr int kNq = 64;               // Gauss-Legendre nodes for psi^
 constexpr int kMaxSteps = 4096;        // pic_pif_step energy history
+constexpr int kForward = -1, kInverse = +1;   // F: e^{-i k.x}; F^-1: e^{+i k.x}, unnormalised
 thread_local char g_err[256] = "";
 
 __device__ __forceinline__ double psi_es(double z, double beta) {
@@ -554,8 +557,8 @@ inline size_t align256(size_t b) { return (b + 255) & ~(size_t)255; }
 struct pic_pif {
     int n, M, w;
     double L, eps, beta, inv_hf;
-    cufftHandle plan;
     cudaStream_t stream;
+    double2* tw;         // M twiddles W_M^m = exp(-2 pi i m / M) of the fine-grid FFT
     double2* G;          // fine grid M^3
     double2* G2;         // second fine grid (binned PIF solve: E_z), or null
     double2* A;          // N^3 spectrum (E^_x + i E^_y)
@@ -565,7 +568,6 @@ struct pic_pif {
     double* energy;      // 3
     double* hist;        // kMaxSteps: W_x per step of pic_pif_step
     int hist_slot;       // -1: no history write
-    void* fft_work;
     int64_t np_max;      // binned path capacity (0: atomic path only)
     int nb;              // bins per dimension (M / kB)
     bool binned;         // binned spread / interp in use
@@ -590,22 +592,13 @@ namespace {
 
 int width_of(double eps) { return (int)std::ceil(std::log10(1.0 / eps)) + 2; }
 
+// The fine grid M = 2n must be a power of two the FFT passes handle (16 .. 1024).
 bool valid(int32_t n, double L, double eps) {
-    return n >= 8 && n <= 1024 && n % 2 == 0 && L > 0 && eps >= 1e-14 && eps < 1.0;
-}
-
-pic_status make_plan(int M, cufftHandle* plan, size_t* work) {
-    if (cufftCreate(plan) != CUFFT_SUCCESS) return PIC_ECUDA;
-    if (cufftSetAutoAllocation(*plan, 0) != CUFFT_SUCCESS ||
-        cufftMakePlan3d(*plan, M, M, M, CUFFT_Z2Z, work) != CUFFT_SUCCESS) {
-        cufftDestroy(*plan);
-        return PIC_ECUDA;
-    }
-    return PIC_OK;
+    return n >= 8 && n <= 512 && (n & (n - 1)) == 0 && L > 0 && eps >= 1e-14 && eps < 1.0;
 }
 
 struct Layout {
-    size_t G, A, Bz, dinv, partials, energy, hist, work, bcnt, boffs, bcur, perm, scan, G2, total;
+    size_t G, A, Bz, dinv, partials, energy, hist, tw, bcnt, boffs, bcur, perm, scan, G2, total;
 };
 bool binnable(int n, int w) { return (2 * n) % kB == 0 && w <= 8; }
 size_t scan_tmp_bytes(int64_t nbins) {
@@ -613,7 +606,7 @@ size_t scan_tmp_bytes(int64_t nbins) {
     cub::DeviceScan::ExclusiveSum(nullptr, b, (const uint32_t*)nullptr, (uint32_t*)nullptr, (int)nbins);
     return b;
 }
-Layout layout(int n, size_t fft_work, int64_t np_max, int w) {
+Layout layout(int n, int64_t np_max, int w) {
     const size_t M = 2 * (size_t)n;
     Layout o;
     size_t off = 0;
@@ -624,7 +617,7 @@ Layout layout(int n, size_t fft_work, int64_t np_max, int w) {
     o.partials = off; off += align256((size_t)kModeBlocks * 3 * sizeof(double));
     o.energy = off;   off += align256(3 * sizeof(double));
     o.hist = off;     off += align256(kMaxSteps * sizeof(double));
-    o.work = off;     off += align256(fft_work);
+    o.tw = off;       off += align256(M * sizeof(double2));
     const int64_t nbins = (np_max > 0 && binnable(n, w)) ? (int64_t)(M / kB) * (M / kB) * (M / kB) : 0;
     o.bcnt = off;     off += nbins ? align256((nbins + 1) * 4) : 0;
     o.boffs = off;    off += nbins ? align256((nbins + 1) * 4) : 0;
@@ -641,15 +634,6 @@ Layout layout(int n, size_t fft_work, int64_t np_max, int w) {
         cudaError_t e_ = (call);                                                               \
         if (e_ != cudaSuccess) {                                                               \
             snprintf((p)->err, sizeof((p)->err), "%s: %s", #call, cudaGetErrorString(e_));     \
-            (p)->poisoned = true;                                                              \
-            return PIC_ECUDA;                                                                  \
-        }                                                                                      \
-    } while (0)
-#define PIF_FFT(p, call)                                                                       \
-    do {                                                                                       \
-        cufftResult r_ = (call);                                                               \
-        if (r_ != CUFFT_SUCCESS) {                                                             \
-            snprintf((p)->err, sizeof((p)->err), "%s: cufft status %d", #call, (int)r_);       \
             (p)->poisoned = true;                                                              \
             return PIC_ECUDA;                                                                  \
         }                                                                                      \
@@ -808,7 +792,9 @@ pic_status spread(pic_pif* p, int64_t np, const double* X, const double* f) {
 pic_status fft(pic_pif* p, int dir, double2* grid = nullptr) {
     Stage t(p, PIC_PIF_FFT);
     double2* g = grid ? grid : p->G;
-    PIF_FFT(p, cufftExecZ2Z(p->plan, (cufftDoubleComplex*)g, (cufftDoubleComplex*)g, dir));
+    // only the lines that meet the mode box K_N: the inverse transform's input is zero
+    // outside it (k_fill), the forward transform's output is read only inside it
+    PIF_CUDA(p, pic::launch_fft_c2c_3d(g, p->M, dir, p->tw, p->stream, p->n / 2));
     return PIC_OK;
 }
 
@@ -848,14 +834,7 @@ pic_status pic_pif_workspace_bytes(int32_t n, double length, double eps, int64_t
         snprintf(g_err, sizeof(g_err), "pic_pif_workspace_bytes: invalid n / length / eps");
         return PIC_EINVAL;
     }
-    cufftHandle plan;
-    size_t work = 0;
-    if (make_plan(2 * n, &plan, &work) != PIC_OK) {
-        snprintf(g_err, sizeof(g_err), "cuFFT plan creation failed (M = %d)", 2 * n);
-        return PIC_ECUDA;
-    }
-    cufftDestroy(plan);
-    *bytes = layout(n, work, np_max, width_of(eps)).total;
+    *bytes = layout(n, np_max, width_of(eps)).total;
     return PIC_OK;
 }
 
@@ -876,16 +855,9 @@ pic_status pic_pif_create(int32_t n, double length, double eps, int64_t np_max, 
     p->beta = 2.30 * p->w;
     p->inv_hf = (double)p->M / length;
     p->stream = (cudaStream_t)stream;
-    size_t work = 0;
-    if (make_plan(p->M, &p->plan, &work) != PIC_OK) {
-        snprintf(g_err, sizeof(g_err), "cuFFT plan creation failed (M = %d)", p->M);
-        delete p;
-        return PIC_ECUDA;
-    }
-    const Layout o = layout(n, work, np_max, p->w);
+    const Layout o = layout(n, np_max, p->w);
     if (bytes < o.total) {
         snprintf(g_err, sizeof(g_err), "workspace %zu bytes < %zu", bytes, o.total);
-        cufftDestroy(p->plan);
         delete p;
         return PIC_ENOMEM;
     }
@@ -898,7 +870,7 @@ pic_status pic_pif_create(int32_t n, double length, double eps, int64_t np_max, 
     p->energy = (double*)(b + o.energy);
     p->hist = (double*)(b + o.hist);
     p->hist_slot = -1;
-    p->fft_work = b + o.work;
+    p->tw = (double2*)(b + o.tw);
     p->nb = p->M / kB;
     {
         const char* e = getenv("PIC_PIF_BINNED");
@@ -915,12 +887,20 @@ pic_status pic_pif_create(int32_t n, double length, double eps, int64_t np_max, 
         const int64_t nbins = (int64_t)p->nb * p->nb * p->nb;
         p->scan_bytes = use ? scan_tmp_bytes(nbins + 1) : 0;
     }
-    if (cufftSetWorkArea(p->plan, p->fft_work) != CUFFT_SUCCESS ||
-        cufftSetStream(p->plan, p->stream) != CUFFT_SUCCESS) {
-        snprintf(g_err, sizeof(g_err), "cuFFT work area / stream");
-        cufftDestroy(p->plan);
-        delete p;
-        return PIC_ECUDA;
+    {   // twiddles of the fine-grid FFT: W_M^m = exp(-2 pi i m / M), m < M
+        double2* tw = (double2*)std::malloc(sizeof(double2) * p->M);
+        if (!tw) { delete p; return PIC_ENOMEM; }
+        for (int m = 0; m < p->M; ++m) {
+            const double a = 2.0 * M_PI * (double)m / (double)p->M;
+            tw[m] = make_double2(std::cos(a), -std::sin(a));
+        }
+        const cudaError_t e = cudaMemcpy(p->tw, tw, sizeof(double2) * p->M, cudaMemcpyHostToDevice);
+        std::free(tw);
+        if (e != cudaSuccess) {
+            snprintf(g_err, sizeof(g_err), "twiddle upload: %s", cudaGetErrorString(e));
+            delete p;
+            return PIC_ECUDA;
+        }
     }
     for (auto& e : p->ev) cudaEventCreate(&e);
     k_psihat<<<1, 256, 0, p->stream>>>(n, p->M, p->w, p->beta, p->dinv);
@@ -938,7 +918,7 @@ pic_status pic_nufft_type1(pic_pif* p, int64_t np, const double* x, const double
     if (np < 0 || (np > 0 && (!x || !f)) || !fhat) return PIC_EINVAL;
     if (pic_status s = bin(p, np, x)) return s;
     if (pic_status s = spread(p, np, x, f)) return s;
-    if (pic_status s = fft(p, CUFFT_FORWARD)) return s;
+    if (pic_status s = fft(p, kForward)) return s;
     {
         Stage t(p, PIC_PIF_MODES);
         const int64_t nm = (int64_t)p->n * p->n * p->n;
@@ -953,7 +933,7 @@ pic_status pic_nufft_type2(pic_pif* p, int64_t np, const double* x, const double
     if (np < 0 || (np > 0 && (!x || !out)) || !fhat) return PIC_EINVAL;
     if (pic_status s = bin(p, np, x)) return s;
     if (pic_status s = fill(p, (const double2*)fhat)) return s;
-    if (pic_status s = fft(p, CUFFT_INVERSE)) return s;
+    if (pic_status s = fft(p, kInverse)) return s;
     if (pic_status s = interp(p, np, x, out, out + 1, 2, 1.0)) return s;
     return flush_timing(p);
 }
@@ -965,7 +945,7 @@ namespace {
 pic_status solve_core(pic_pif* p, int64_t np, const double* x, const double* q, double* E) {
     if (pic_status s = bin(p, np, x)) return s;                             // sort into bins
     if (pic_status s = spread(p, np, x, q)) return s;                       // C
-    if (pic_status s = fft(p, CUFFT_FORWARD)) return s;                     // F
+    if (pic_status s = fft(p, kForward)) return s;                     // F
     {
         Stage t(p, PIC_PIF_MODES);                                          // chi, D, Poisson
         const double kunit = 2.0 * M_PI / p->L;
@@ -978,19 +958,19 @@ pic_status solve_core(pic_pif* p, int64_t np, const double* x, const double* q, 
     const double sc = 1.0 / (p->L * p->L * p->L);                           // D#35
     if (p->binned && p->G2 && !p->split_interp) {                          // one gather pass
         if (pic_status s = fill(p, p->A)) return s;                         // E_x + i E_y -> G
-        if (pic_status s = fft(p, CUFFT_INVERSE)) return s;
+        if (pic_status s = fft(p, kInverse)) return s;
         if (pic_status s = fill(p, p->Bz, p->G2)) return s;                 // E_z -> G2
-        if (pic_status s = fft(p, CUFFT_INVERSE, p->G2)) return s;
+        if (pic_status s = fft(p, kInverse, p->G2)) return s;
         Stage t(p, PIC_PIF_INTERP);
         PIF_W_SWITCH_SMALL(p->w, interp3_tiled_w, p, np, x, E, sc);
         PIF_LAUNCHED(p);
         return PIC_OK;
     }
     if (pic_status s = fill(p, p->A)) return s;                             // E_x + i E_y
-    if (pic_status s = fft(p, CUFFT_INVERSE)) return s;
+    if (pic_status s = fft(p, kInverse)) return s;
     if (pic_status s = interp(p, np, x, E, E + np, 1, sc)) return s;
     if (pic_status s = fill(p, p->Bz)) return s;                            // E_z
-    if (pic_status s = fft(p, CUFFT_INVERSE)) return s;
+    if (pic_status s = fft(p, kInverse)) return s;
     return interp(p, np, x, E + 2 * np, nullptr, 1, sc);
 }
 
@@ -1078,7 +1058,6 @@ const char* pic_pif_last_error(const pic_pif* p) { return p ? p->err : g_err; }
 
 void pic_pif_free(pic_pif* p) {
     if (!p) return;
-    cufftDestroy(p->plan);
     for (auto& e : p->ev)
         if (e) cudaEventDestroy(e);
     delete p;

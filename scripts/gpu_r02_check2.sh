@@ -1,0 +1,10 @@
+# PIF (own FFT, mode-box skipping) + pipelined reorder: parity, MR kernels forced at P = 1, bench lines
+mkdir -p gpurun_out
+export PYTHONPATH=$PWD
+timeout 1200 python -m pytest tests/test_gpu_pif.py -x -q > gpurun_out/c2_pif_pytest.log 2>&1; echo "pif pytest rc=$?"; tail -1 gpurun_out/c2_pif_pytest.log
+timeout 900 python -m pytest tests/test_gpu_parity.py tests/test_gpu_boris.py -x -q > gpurun_out/c2_pytest.log 2>&1; echo "pytest rc=$?"; tail -1 gpurun_out/c2_pytest.log
+PIC_FORCE_MR=1 timeout 900 python -m pytest tests/test_gpu_parity.py -x -q -k "twenty or bit_exact or deposit or init" > gpurun_out/c2_pytest_mr.log 2>&1; echo "pytest MR rc=$?"; tail -1 gpurun_out/c2_pytest_mr.log
+timeout 900 python bench.py --no-e2e --no-cpu-baseline > gpurun_out/c2_bench.json 2> gpurun_out/c2_bench.err; echo "bench rc=$?"; python -c "
+import json; d=json.loads(open('gpurun_out/c2_bench.json').read().strip().splitlines()[-1]); print(d['ms_per_step'], {k:round(v['ms_per_step'],3) for k,v in d['stages'].items()})"
+timeout 900 python bench.py --solver pif --n 512 --steps 3 --warmup 3 --no-e2e --no-cpu-baseline > gpurun_out/c2_pif_bench.json 2> gpurun_out/c2_pif_bench.err; echo "pif bench rc=$?"; python -c "
+import json; d=json.loads(open('gpurun_out/c2_pif_bench.json').read().strip().splitlines()[-1]); print(d['ms_per_step'], {k:round(v['ms_per_step'],2) for k,v in d['stages'].items()})"

@@ -157,3 +157,15 @@ def test_owner_ranks_partition_by_slab():
     bad[2, 7] = L
     with pytest.raises(PicError):
         owner_ranks(bad, n, L, 2)
+
+
+def test_pif_sizes_rejected_on_the_host():
+    """include/pif.h: the fine grid M = 2N goes through the library's own power-of-two FFT
+    passes, so N must be a power of two in [8, 512] (host-only check, no GPU)."""
+    import ctypes as C
+    import numpy as np
+
+    for n, ok in ((8, True), (512, True), (12, False), (1024, False), (4, False)):
+        b = C.c_size_t()
+        st = B.lib().pic_pif_workspace_bytes(n, 4 * np.pi, 1e-4, 0, C.byref(b))
+        assert (st == 0) == ok, (n, st)
