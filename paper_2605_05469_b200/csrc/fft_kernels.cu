@@ -241,6 +241,9 @@ __host__ __device__ constexpr int z_tw(int n) { int t = 2048 / n; return t > 8 ?
 #ifndef PIC_ZMUL_MINB
 #define PIC_ZMUL_MINB 2
 #endif
+#ifndef PIC_ZMUL_DIRECT
+#define PIC_ZMUL_DIRECT 0
+#endif
 __host__ __device__ constexpr int zmul_tw(int n) { int t = PIC_ZMUL_TWN / n; return t > 8 ? 8 : (t < 1 ? 1 : t); }
 
 // Every pass is a persistent loop over tiles (grid = resident CTAs): the input of
@@ -402,9 +405,15 @@ __global__ void __launch_bounds__(kThreads, PIC_ZMUL_MINB) k_fft_z_mul(Geom g, c
     constexpr int n = 1 << LOGN, TW = zmul_tw(n);
     constexpr int ls = col_stride(n, TW);
     const int nyl = n / g.P;
+#if PIC_ZMUL_DIRECT   // stage 0 reads global memory directly: no input buffer (one tile per CTA)
+    double2* s1 = smx;               // [TW][ls] forward result
+    double2* s2 = s1 + TW * ls;      // [TW][ls] inverse work
+    double2* in = nullptr;
+#else
     double2* in = smx;               // [n][TW]
     double2* s1 = smx + n * TW;      // [TW][ls] forward result
     double2* s2 = s1 + TW * ls;      // [TW][ls] inverse work
+#endif
     constexpr int ntiles = (n / 2 + 1 + TW - 1) / TW;
     const int64_t ntile = (int64_t)nyl * ntiles;
     const int64_t zstride = (int64_t)nyl * g.px;
@@ -421,11 +430,21 @@ __global__ void __launch_bounds__(kThreads, PIC_ZMUL_MINB) k_fft_z_mul(Geom g, c
     const double kf = 6.283185307179586476925286766559 / g.L;
     constexpr int half = n / 2;
     int64_t t = blockIdx.x;
+#if !PIC_ZMUL_DIRECT
     if (t < ntile) prefetch(t);
+#endif
     for (; t < ntile; t += gridDim.x) {
         const int yl = (int)(t / ntiles), kx0 = (int)(t - (int64_t)yl * ntiles) * TW;
         const int ncol = min(TW, n / 2 + 1 - kx0);
         const int ky = g.rank * nyl + yl;
+#if PIC_ZMUL_DIRECT
+        {
+            const double2* pin = pencil + (int64_t)yl * g.px + kx0;
+            auto src = [&](int l, int e) { return l < ncol ? pin[e * zstride + l] : make_double2(0.0, 0.0); };
+            auto dst = [&](int, int, double2) {};
+            fft_lines<-1, true, LOGN, 1, false>(s1, TW, ls, tw, 0, src, dst);
+        }
+#else
         cp_async_wait0();
         __syncthreads();
         {
@@ -434,6 +453,7 @@ __global__ void __launch_bounds__(kThreads, PIC_ZMUL_MINB) k_fft_z_mul(Geom g, c
             auto next = [&]() { if (t + gridDim.x < ntile) prefetch(t + gridDim.x); };
             fft_lines<-1, true, LOGN, 1, false>(s1, TW, ls, tw, 0, src, dst, next);
         }
+#endif
         const double kyv = kf * (double)(ky < half ? ky : ky - n);
         // phi^ = rho^ scale / |k|^2 in place (0 at k = 0): one division per mode
         for (int i = threadIdx.x; i < TW * n; i += blockDim.x) {
@@ -740,7 +760,7 @@ void launch_fft_y_field(const Geom& g, SpecLayout src, SpecLayout dst, const dou
 void launch_fft_z_mul(const Geom& g, const double2* pencil, SpecLayout out, double scale,
                       const double2* tw, cudaStream_t s) {
     const int TW = zmul_tw(g.n), ntiles = (g.n / 2 + 1 + TW - 1) / TW;
-    const size_t smem = sizeof(double2) * (size_t)TW * (g.n + 2 * col_stride(g.n, TW));
+    const size_t smem = sizeof(double2) * (size_t)TW * ((PIC_ZMUL_DIRECT ? 0 : g.n) + 2 * col_stride(g.n, TW));
     const int64_t nt = (int64_t)(g.n / g.P) * ntiles;
     // one tile per CTA: the pass is bound by its four transforms, not its input
     // loads, and measured faster without the persistent loop

@@ -237,7 +237,11 @@ __global__ void __launch_bounds__(kThreads, MR ? 3 : 4) k_push_key_brick(Geom g,
                                                              uint16_t* __restrict__ rank,
                                                              uint32_t* __restrict__ count,
                                                              SendBuf sb, int* __restrict__ err) {
-    __shared__ double4 etile[9 * 9 * 5];
+    // E tile in x-pairs: entry (z, y, x) = (E_d(x), E_d(x + 1)) for d = x, y, z, so the two
+    // x corners of one (y, z) corner pair are three 16-B shared loads (48 B) instead of two
+    // 32-B node records (64 B): a quarter less shared-memory traffic per particle
+    // (ncu r01: the kernel ran at 79% of the L1/shared throughput)
+    __shared__ double2 ptile[5 * 9 * 8][3];
     __shared__ double2 lbuf[MR ? kLeaveCap : 1][4];      // leavers of this brick (P > 1)
     __shared__ uint8_t ldst[MR ? kLeaveCap : 1];
     __shared__ uint32_t lcount[8], lbase[8], nleave;
@@ -250,7 +254,17 @@ __global__ void __launch_bounds__(kThreads, MR ? 3 : 4) k_push_key_brick(Geom g,
         const int64_t m = ((int64_t)(bz + nz) * g.n + ((by + ny) & g.nmask)) * g.n + ((bx + nx) & g.nmask);
         double ex, ey, ez;
         ldg_node(E4 + 4 * m, ex, ey, ez);
-        etile[q] = make_double4(ex, ey, ez, 0.0);
+        const int row = (nz * 9 + ny) * 8;
+        if (nx < 8) {
+            ptile[row + nx][0].x = ex;
+            ptile[row + nx][1].x = ey;
+            ptile[row + nx][2].x = ez;
+        }
+        if (nx > 0) {
+            ptile[row + nx - 1][0].y = ex;
+            ptile[row + nx - 1][1].y = ey;
+            ptile[row + nx - 1][2].y = ez;
+        }
     }
     if (t < 8) lcount[t] = 0;
     if (t == 0) nleave = 0;
@@ -271,15 +285,18 @@ __global__ void __launch_bounds__(kThreads, MR ? 3 : 4) k_push_key_brick(Geom g,
 #pragma unroll
         for (int c = 0; c < 2; ++c)
 #pragma unroll
-            for (int b = 0; b < 2; ++b)
-#pragma unroll
-                for (int a = 0; a < 2; ++a) {
-                    const double wt = __dmul_rn(__dmul_rn(w[0][a], w[1][b]), w[2][c]);
-                    const double4 e = etile[((lz + c) * 9 + (ly + b)) * 9 + (lx + a)];
-                    e0 = __fma_rn(wt, e.x, e0);
-                    e1 = __fma_rn(wt, e.y, e1);
-                    e2 = __fma_rn(wt, e.z, e2);
-                }
+            for (int b = 0; b < 2; ++b) {
+                const double2* pe = ptile[((lz + c) * 9 + (ly + b)) * 8 + lx];
+                const double2 px = pe[0], py = pe[1], pz = pe[2];
+                const double wt0 = __dmul_rn(__dmul_rn(w[0][0], w[1][b]), w[2][c]);
+                const double wt1 = __dmul_rn(__dmul_rn(w[0][1], w[1][b]), w[2][c]);
+                e0 = __fma_rn(wt0, px.x, e0);          // corner order z, y, x (x inner): a = 0 ...
+                e1 = __fma_rn(wt0, py.x, e1);
+                e2 = __fma_rn(wt0, pz.x, e2);
+                e0 = __fma_rn(wt1, px.y, e0);          // ... then a = 1, as the oracle (D#17)
+                e1 = __fma_rn(wt1, py.y, e1);
+                e2 = __fma_rn(wt1, pz.y, e2);
+            }
         double ep[3] = {e0, e1, e2};
         kick(g, ep, v);
         drift(g, x, v);
@@ -630,23 +647,17 @@ __device__ __forceinline__ int chunk_end(const uint32_t* soffs, int ca, int cap)
 // their sender); the index rank puts them after the residents of their cell, and
 // a fix-up pass re-sorts the (few) cells holding arrivals by (old global key, old
 // index) -- the order of the single-domain oracle's global stable sort (D#15).
-//
-// Software pipeline over the chunks of a brick (two chunk buffers): while chunk k's
-// charge is summed (thread per cell, fp64 weights), the gather of chunk k + 1 is
-// already in flight, and chunk k + 2's perm entries are loaded behind it:
-//   [rank k+1, issue gather k+1] -> deposit k -> [perm k+2] -> wait -> drift + store k+1
-// (r02: the deposit alone cost 3.5 ms of the 29 ms kernel when it waited for nothing).
-// Chunk capacity (particles per buffer; a brick holds ~ppc * 256, so ~4 chunks): two
-// buffers of PIC_RD_CAP particles let three CTAs share an SM.
+// Chunk capacity (particles staged per pass; a brick holds ~ppc * 256): 1344 lets
+// three CTAs share an SM, which measured faster than two with whole-brick chunks.
 #ifndef PIC_RD_CAP
-#define PIC_RD_CAP 640
+#define PIC_RD_CAP 1344
 #endif
 #ifndef PIC_RD_MINB
 #define PIC_RD_MINB 3
 #endif
 template <bool MR>
 struct ReorderCap {
-    static constexpr int value = MR ? PIC_RD_CAP * 15 / 16 : PIC_RD_CAP;   // MR: + the slot -> entry array
+    static constexpr int value = MR ? PIC_RD_CAP * 13 / 14 : PIC_RD_CAP;   // MR: + the slot -> entry array
 };
 
 template <bool PUSH, bool MR>
@@ -655,16 +666,17 @@ __global__ void __launch_bounds__(kThreads, PIC_RD_MINB) k_reorder_deposit(
     const double2* __restrict__ recv, int64_t n_old, const unsigned long long* __restrict__ dcnt, PState nxt,
     double* __restrict__ rho, double* ghost, int* __restrict__ err) {
     constexpr int CAP = ReorderCap<MR>::value;
-    static_assert(CAP % 4 == 0, "chunk capacity: a multiple of 4 (16-B words of sperm)");
     if (MR && dcnt) n_old = (int64_t)dcnt[DC_N];
 
     extern __shared__ double dyn_smem[];
-    double2* spb = reinterpret_cast<double2*>(dyn_smem);               // [2][3][CAP]: (x, y), (z, vz), (vx, vy)
-    uint32_t* spermb = reinterpret_cast<uint32_t*>(spb + 6 * CAP);     // [2][CAP + 4] (16-B aligned)
-    uint32_t* soffs = spermb + 2 * (CAP + 4);                          // [kBrick + 1] (+3 pad)
-    uint32_t* sE = soffs + kBrick + 4;                                   // [CAP] (MR): entry at slot
-    double* tile = reinterpret_cast<double*>(sE + (MR ? CAP : 0));      // [9*9*5]
-    uint8_t* scell = reinterpret_cast<uint8_t*>(tile + 9 * 9 * 5);      // [CAP + 4]
+    double2* sp0 = reinterpret_cast<double2*>(dyn_smem);               // [CAP] (x, y)
+    double2* sp1 = sp0 + CAP;                                            // [CAP] (z, vz)
+    double2* sp2 = sp1 + CAP;                                            // [CAP] (vx, vy)
+    double* tile = reinterpret_cast<double*>(sp2 + CAP);                // [9*9*5]
+    uint32_t* sperm = reinterpret_cast<uint32_t*>(tile + 9 * 9 * 5);    // [CAP]
+    uint32_t* soffs = sperm + CAP;                                       // [kBrick + 1]
+    uint32_t* sE = soffs + kBrick + 1;                                   // [CAP] (MR): entry at slot
+    uint8_t* scell = reinterpret_cast<uint8_t*>(sE + (MR ? CAP : 0));   // [CAP]
     const int t = threadIdx.x;
     const uint32_t c0 = blockIdx.x * kBrick;
     int bx, by, bz;
@@ -674,53 +686,34 @@ __global__ void __launch_bounds__(kThreads, PIC_RD_MINB) k_reorder_deposit(
     for (int q = t; q < 9 * 9 * 5; q += kThreads) tile[q] = 0.0;
     __syncthreads();
 
-    auto sp0 = [&](int b) { return spb + (3 * b) * CAP; };
-    auto sp1 = [&](int b) { return spb + (3 * b + 1) * CAP; };
-    auto sp2 = [&](int b) { return spb + (3 * b + 2) * CAP; };
-    auto sperm = [&](int b) { return spermb + b * (CAP + 4); };
-    // perm entries of chunk [a, e) -> sperm(b) (cp.async, 4 B through L1); false when the
-    // chunk cannot be staged (a cell over capacity, or past the slab's capacity)
-    auto chunk_ok = [&](int a, int e) {
-        return soffs[a + 1] - soffs[a] <= (uint32_t)CAP && (int64_t)soffs[e] <= g.cap;
-    };
-    auto load_perm = [&](int b, int a, int e) {
-        const uint32_t Pa = soffs[a];
-        const int n = (int)(soffs[e] - Pa);
-        uint32_t* sp = sperm(b);
-        for (int p = t; p < n; p += kThreads) cp_async4(sp + p, perm + Pa + p);
-        cp_async_commit();
-    };
-    // chunk [a, e) in buffer b: cells' slot ranges, then stable rank -> cp.async of each
-    // particle into its sorted slot.  The rank is the number of entries of the same cell
-    // with a smaller index, counted over aligned 16-B words of sperm (and 4-B words of
-    // scell): an entry counts if its cell is earlier in the chunk, or the same with a
-    // smaller index; the earlier cells' entries of the first word are subtracted, later
-    // cells' never count, the padding (cell 0xff, index 0xffffffff) never counts.
-    auto rank_gather = [&](int b, int a, int e) {
-        const uint32_t Pa = soffs[a];
-        const int n = (int)(soffs[e] - Pa);
-        uint32_t* sp = sperm(b);
-        if (t >= a && t < e)
-            for (int p = (int)(soffs[t] - Pa); p < (int)(soffs[t + 1] - Pa); ++p) scell[p] = (uint8_t)t;
-        if (t < 4) {
-            sp[n + t] = 0xffffffffu;
-            scell[n + t] = 0xffu;
+    double acc[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) acc[q] = 0.0;
+    int ca = 0;
+    while (ca < kBrick) {
+        if (soffs[ca + 1] - soffs[ca] > (uint32_t)CAP) {
+            if (t == 0) atomicExch(err, 1);
+            return;
         }
+        const int cb = chunk_end(soffs, ca, CAP);
+        const uint32_t P0 = soffs[ca];
+        const int cnt = (int)(soffs[cb] - P0);
+        if ((int64_t)P0 + cnt > g.cap) {     // slab over capacity (flagged by place)
+            if (t == 0) atomicExch(err + 2, 1);
+            return;
+        }
+        for (int p = t; p < cnt; p += kThreads) sperm[p] = __ldcs(perm + P0 + p);   // read once
+        const bool mine = t >= ca && t < cb;
+        const int s0 = mine ? (int)(soffs[t] - P0) : 0, s1 = mine ? (int)(soffs[t + 1] - P0) : 0;
+        for (int p = s0; p < s1; ++p) scell[p] = (uint8_t)t;
         __syncthreads();
-        double2 *d0 = sp0(b), *d1 = sp1(b), *d2 = sp2(b);
-        for (int p = t; p < n; p += kThreads) {
+        // stable rank -> cp.async of the particle into its sorted slot
+        for (int p = t; p < cnt; p += kThreads) {
             const int c = scell[p];
-            const int q0 = (int)(soffs[c] - Pa), q1 = (int)(soffs[c + 1] - Pa);
-            const uint32_t j = sp[p];
-            int r = (q0 & ~3) - q0;
-            for (int q = q0 & ~3; q < q1; q += 4) {
-                const uint4 v = *reinterpret_cast<const uint4*>(sp + q);
-                const uint32_t cc = *reinterpret_cast<const uint32_t*>(scell + q);
-                const int e0 = (int)(cc & 0xffu), e1 = (int)((cc >> 8) & 0xffu);
-                const int e2 = (int)((cc >> 16) & 0xffu), e3 = (int)(cc >> 24);
-                r += (e0 < c || (e0 == c && v.x < j)) + (e1 < c || (e1 == c && v.y < j)) +
-                     (e2 < c || (e2 == c && v.z < j)) + (e3 < c || (e3 == c && v.w < j));
-            }
+            const int q0 = (int)(soffs[c] - P0), q1 = (int)(soffs[c + 1] - P0);
+            const uint32_t j = sperm[p];
+            int r = 0;
+            for (int q = q0; q < q1; ++q) r += sperm[q] < j;
             const int o = q0 + r;
             if (MR) sE[o] = j;
             const double2* src0 = cur.xy + j;
@@ -730,40 +723,12 @@ __global__ void __launch_bounds__(kThreads, PIC_RD_MINB) k_reorder_deposit(
                 const double2* d = recv + 4 * ((int64_t)j - n_old);
                 src0 = d; src1 = d + 1; src2 = d + 2;
             }
-            cp_async16(d0 + o, src0);
-            cp_async16(d1 + o, src1);
-            cp_async16(d2 + o, src2);
+            cp_async16(sp0 + o, src0);
+            cp_async16(sp1 + o, src1);
+            cp_async16(sp2 + o, src2);
         }
-        cp_async_commit();
-    };
-    auto fail = [&](int code) {
-        cp_async_wait_all();
-        if (t == 0) atomicExch(err + code, 1);
-    };
-
-    double acc[8];
-#pragma unroll
-    for (int q = 0; q < 8; ++q) acc[q] = 0.0;
-    // prologue: perm of chunk 0 -> rank + gather chunk 0; perm of chunk 1 behind it
-    int ca = 0, cb = chunk_end(soffs, 0, CAP);
-    if (soffs[1] - soffs[0] > (uint32_t)CAP) { fail(0); return; }
-    if ((int64_t)soffs[cb] > g.cap) { fail(2); return; }
-    load_perm(0, ca, cb);
-    cp_async_wait_all();
-    __syncthreads();
-    rank_gather(0, ca, cb);
-    int cc = cb < kBrick ? chunk_end(soffs, cb, CAP) : cb;           // chunk k + 1 = [cb, cc)
-    if (cb < kBrick && chunk_ok(cb, cc)) load_perm(1, cb, cc);
-    int b = 0;
-    while (true) {
-        // chunk k = [ca, cb) in buffer b: its gather (and chunk k + 1's perm) complete
         cp_async_wait_all();
         __syncthreads();
-        const uint32_t P0 = soffs[ca];
-        const int cnt = (int)(soffs[cb] - P0);
-        const bool mine = t >= ca && t < cb;
-        const int s0 = mine ? (int)(soffs[t] - P0) : 0, s1 = mine ? (int)(soffs[t + 1] - P0) : 0;
-        double2 *x0 = sp0(b), *x1 = sp1(b), *x2 = sp2(b);
         if (MR) {   // cells holding arrivals: insertion sort by (old global key, old index)
             bool any = false;
             for (int p = s0; p < s1; ++p) any |= sE[p] >= n_old;
@@ -772,7 +737,7 @@ __global__ void __launch_bounds__(kThreads, PIC_RD_MINB) k_reorder_deposit(
                     const uint32_t e = sE[slot];
                     if (e >= n_old)
                         return (unsigned long long)__double_as_longlong(recv[4 * ((int64_t)e - n_old) + 3].x);
-                    const double x[3] = {x0[slot].x, x0[slot].y, x1[slot].x};   // x_n (not yet drifted)
+                    const double x[3] = {sp0[slot].x, sp0[slot].y, sp1[slot].x};   // x_n (not yet drifted)
                     return (unsigned long long)gkey_of(g, x) | ((unsigned long long)e << 32);
                 };
                 auto less = [](unsigned long long u, unsigned long long v) {
@@ -781,64 +746,44 @@ __global__ void __launch_bounds__(kThreads, PIC_RD_MINB) k_reorder_deposit(
                 };
                 for (int a = s0 + 1; a < s1; ++a) {
                     const unsigned long long ta = tie(a);
-                    const double2 r0 = x0[a], r1 = x1[a], r2 = x2[a];
+                    const double2 r0 = sp0[a], r1 = sp1[a], r2 = sp2[a];
                     const uint32_t ea = sE[a];
-                    int q = a - 1;
-                    while (q >= s0 && less(ta, tie(q))) {
-                        x0[q + 1] = x0[q]; x1[q + 1] = x1[q]; x2[q + 1] = x2[q]; sE[q + 1] = sE[q];
-                        --q;
+                    int b = a - 1;
+                    while (b >= s0 && less(ta, tie(b))) {
+                        sp0[b + 1] = sp0[b]; sp1[b + 1] = sp1[b]; sp2[b + 1] = sp2[b]; sE[b + 1] = sE[b];
+                        --b;
                     }
-                    x0[q + 1] = r0; x1[q + 1] = r1; x2[q + 1] = r2; sE[q + 1] = ea;
+                    sp0[b + 1] = r0; sp1[b + 1] = r1; sp2[b + 1] = r2; sE[b + 1] = ea;
                 }
             }
             __syncthreads();
         }
         // drift in place (v is already kicked; arrivals arrive drifted), coalesced stores
         for (int p = t; p < cnt; p += kThreads) {
-            double2 a = x0[p], c = x1[p];
-            const double2 e = x2[p];
+            double2 a = sp0[p], b = sp1[p];
+            const double2 e = sp2[p];
             if (PUSH && !(MR && sE[p] >= n_old)) {
-                double x[3] = {a.x, a.y, c.x};
-                const double v[3] = {e.x, e.y, c.y};
+                double x[3] = {a.x, a.y, b.x};
+                const double v[3] = {e.x, e.y, b.y};
                 drift(g, x, v);
                 a = make_double2(x[0], x[1]);
-                c = make_double2(x[2], c.y);
-                x0[p] = a;
-                x1[p] = c;
+                b = make_double2(x[2], b.y);
+                sp0[p] = a;
+                sp1[p] = b;
             }
             const int64_t o = (int64_t)P0 + p;
             __stcs(nxt.xy + o, a);        // write-once: evict first, keep L2 for the gather
-            st_zv_cs(nxt.zv + 2 * o, c, e);
+            st_zv_cs(nxt.zv + 2 * o, b, e);
         }
         __syncthreads();
-        // chunk k + 1: rank + gather into the other buffer (its perm is in sperm(b ^ 1))
-        const bool more = cb < kBrick;
-        int cd = cc;
-        if (more) {
-            if (soffs[cb + 1] - soffs[cb] > (uint32_t)CAP) { fail(0); return; }
-            if ((int64_t)soffs[cc] > g.cap) { fail(2); return; }
-            rank_gather(b ^ 1, cb, cc);
-            // chunk k + 2's perm into this buffer's sperm (chunk k no longer reads it)
-            cd = cc < kBrick ? chunk_end(soffs, cc, CAP) : cc;
-            if (cc < kBrick && chunk_ok(cc, cd)) load_perm(b, cc, cd);
-        }
-        // CIC charge of chunk k while chunk k + 1 is in flight: thread per cell, its
-        // particles in stable order from shared memory
-#ifdef PIC_RD_SKIP_DEPOSIT   // diagnostics only (no charge): the cost of the deposit
-        for (int p = s1; p < s1; ++p) {
-#else
+        // CIC charge: thread per cell, its particles in stable order from shared memory
         for (int p = s0; p < s1; ++p) {
-#endif
-            const double x[3] = {x0[p].x, x0[p].y, x1[p].x};
+            const double x[3] = {sp0[p].x, sp0[p].y, sp1[p].x};
             cic_acc(g, x, acc);
         }
-        if (!more) break;
+        __syncthreads();
         ca = cb;
-        cb = cc;
-        cc = cd;
-        b ^= 1;
     }
-    __syncthreads();
     fold_flush(g, tile, acc, t, bx, by, bz, rho, ghost);
     if (MR && bz + 4 == g.nzl && ghost != rho + (int64_t)g.nzl * g.n * g.rp)
         __threadfence_system();   // peer ghost atomics (PIC_P2P_GHOST=2) complete before the barrier
@@ -886,8 +831,8 @@ inline unsigned blocks(int64_t n, int t) { return (unsigned)((n + t - 1) / t); }
 template <bool MR>
 constexpr size_t reorder_smem() {
     constexpr int CAP = ReorderCap<MR>::value;
-    return sizeof(double2) * 6 * CAP + sizeof(double) * 9 * 9 * 5 +
-           sizeof(uint32_t) * (2 * (CAP + 4) + kBrick + 4 + (MR ? CAP : 0)) + CAP + 4;
+    return sizeof(double2) * 3 * CAP + sizeof(double) * 9 * 9 * 5 +
+           sizeof(uint32_t) * (CAP + kBrick + 1 + (MR ? CAP : 0)) + CAP;
 }
 
 }  // namespace
