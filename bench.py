@@ -312,8 +312,9 @@ def run_ours(args, rank, world):
     np_ = ppc * n ** 3                      # particles of the whole job
     t_init = time.perf_counter()
     ncid = broadcast_nccl_id(rank, world)
+    pgrid = tuple(int(v) for v in args.pgrid.split("x")) if args.pgrid else (1, world)
     sim = Simulation(n=n, ppc=ppc, k=0.5, alpha=0.05, dt=args.dt, seed=1, device=f"cuda:{local}",
-                     rank=rank, nranks=world, nccl_id=ncid, solver=args.solver)
+                     rank=rank, nranks=world, nccl_id=ncid, solver=args.solver, pgrid=pgrid)
     pcg = args.solver in ("pcg", "fem")     # CG-based solvers (iteration statistics)
     torch.cuda.synchronize()
     log(f"[rank {rank}] init {n}^3 x {ppc} (slab z0={sim.z0} nz={sim.nz}, {sim.np} particles): "
@@ -417,7 +418,8 @@ def run_ours(args, rank, world):
     achieved = alg_per_call / (tot / calls / 1e3) / 1e9
     peaks = measured_peaks()
     peak = peaks.get("hbm_gbs") or 6650.0
-    cfg_name = f"landau3d_{n}^3x{ppc}ppc_{args.solver}" + (f"_{world}gpu" if world > 1 else "")
+    cfg_name = (f"landau3d_{n}^3x{ppc}ppc_{args.solver}" + (f"_{world}gpu" if world > 1 else "")
+                + (f"_pencil{pgrid[0]}x{pgrid[1]}" if pgrid[0] > 1 else ""))
     traffic = ncu_traffic(cfg_name, dom)
     roof = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
             "frac": achieved / peak, "traffic": traffic,
@@ -454,9 +456,12 @@ def run_ours(args, rank, world):
         "config": {"workload": cfg_name, "grid": n, "ppc": ppc, "particles": np_,
                    "k": 0.5, "alpha": 0.05, "dt": args.dt,
                    "parallelism": "1 GPU" if world == 1 else
-                   f"z-slab decomposition over {world} GPUs (NCCL all-to-all FFT transposes; halo "
-                   f"plane, ghost plane and particle migration over "
-                   f"{'NVLink peer memory' if nvlink['transport'] == 'peer' else 'NCCL send/recv'})",
+                   (f"pencil decomposition {pgrid[0]}x{pgrid[1]} (y x z) over {world} GPUs (y-group "
+                    f"all-to-all to the FFT's z-slabs and back, NCCL all-to-all FFT transposes, ghost/halo "
+                    f"row and plane and particle migration over NCCL send/recv)" if pgrid[0] > 1 else
+                    f"z-slab decomposition over {world} GPUs (NCCL all-to-all FFT transposes; halo "
+                    f"plane, ghost plane and particle migration over "
+                    f"{'NVLink peer memory' if nvlink['transport'] == 'peer' else 'NCCL send/recv'})"),
                    "migrated_per_step": migrated / args.steps,
                    "l2": "inputs larger than L2 (particle state 48 B x N_p / N per rank)"},
         "roofline": roof,
@@ -639,6 +644,7 @@ def main():
                     help="field solver: fft (BJ configs 0-3), pcg (BJ config 5), fem (SURVEY §8(f) NEXT-4) "
                          "or pif (Particle-in-Fourier, NEXT-2; N^3 modes, eps 1e-4)")
     ap.add_argument("--dt", type=float, default=0.05, help="time step (diagnostics; the workload is dt = 0.05)")
+    ap.add_argument("--pgrid", default=None, help="PyxPz rank grid (pencils, e.g. 2x4); default z-slabs 1xN")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--pif-atomic", action="store_true", help="PIF: global-atomic spreading (no bins)")
     ap.add_argument("--no-cpu-baseline", action="store_true")

@@ -74,7 +74,9 @@ typedef struct {
     double   dt;        /* time step > 0; default 0.05 (D#9)                   */
     uint64_t seed;      /* Philox4x32-10 key of the initial sampler (D#10)            */
     int32_t  half_kick; /* 1: v stored at half steps, backward half kick at init */
-    int32_t  pgrid[2];  /* {Py, Pz} rank grid: {1, nranks} (z-slabs; pencils not built) */
+    int32_t  pgrid[2];  /* {Py, Pz} rank grid, Py Pz = nranks: {1, nranks} = z-slabs (default),
+                           Py > 1 = pencils over (y, z) (BJ config 4); rank
+                           r = pz Py + py owns y in [py N/Py, +N/Py), z in [pz N/Pz, +N/Pz) */
     int32_t  solver;    /* pic_solver; default PIC_SOLVER_FFT                             */
     int32_t  pcg_inner; /* PCG: SSOR inner sweeps, >= 1; default 4                */
     int32_t  pcg_outer; /* PCG: SSOR outer iterations, >= 1; default 2            */
@@ -92,24 +94,34 @@ typedef struct {
  * settings of P:226 / P:260 (tol 1e-4, SSOR omega = pi/2, 4 inner, 2 outer). */
 pic_status pic_params_default(pic_params *p);
 
-/* Multi-GPU (one process per GPU, nranks in {1, 2, 4, 8}): rank r owns the z-slab of
- * cell/node planes [r N/P, (r+1) N/P) and the particles whose cell lies in it
- * (SURVEY §8(e)).  Rank 0 creates the NCCL id (128 bytes), the caller broadcasts it
+/* Multi-GPU (one process per GPU, nranks in {1, 2, 4, 8}): rank r = pz Py + py
+ * owns the cells/nodes with z in [pz N/Pz, +N/Pz) and y in [py N/Py, +N/Py) (pgrid = {Py, Pz};
+ * Py = 1: z-slabs) and the particles whose cell lies there.  The field solve always runs on
+ * z-slabs of N/nranks planes (slab index = rank): pencils redistribute the charge to them and
+ * the field back with one all-to-all in the y-group (the Py ranks sharing pz) each way, around
+ * the slab FFT's own all-to-all transposes.  Pencils use the NCCL transport and
+ * the FFT solver.  Rank 0 creates the NCCL id (128 bytes), the caller broadcasts it
  * (torch.distributed) and every rank passes it to pic_init. */
 pic_status pic_nccl_unique_id(uint8_t id[128]);
 
-/* The slab of a rank: first plane z0, planes nz, particle capacity of the rank. */
+/* The z range of a rank's domain: first plane z0, planes nz, particle capacity of the rank. */
 pic_status pic_slab(const pic_params *p, int32_t rank, int32_t nranks, int32_t *z0, int32_t *nz,
                     int64_t *capacity);
 
-/* Owner rank of each of np positions under the decomposition of pic_slab:
- * the rank whose slab holds the cell plane i_z = min(floor(z inv_h), N - 1), inv_h =
- * (double)N / L (D#5), i.e. the rank each particle must be given to in pic_set_particles.
+/* The domain of a rank: rows [y0, y0 + ny), planes [z0, z0 + nz), particle capacity (any
+ * pointer nullable).  PIC_EINVAL / PIC_EUNSUPPORTED as pic_workspace_bytes. */
+pic_status pic_domain(const pic_params *p, int32_t rank, int32_t nranks, int32_t *y0, int32_t *ny, int32_t *z0,
+                      int32_t *nz, int64_t *capacity);
+
+/* Owner rank of each of np positions under the decomposition of pic_domain:
+ * the rank whose domain holds the cell row i_y and plane i_z, i_d = min(floor(x_d inv_h),
+ * N - 1), inv_h = (double)N / L (D#5), i.e. the rank each particle must be given to in
+ * pic_set_particles.
  *   xyz   : host doubles [3][np] (x, y, z rows; xyzuvw of pic_set_particles may be passed),
- *           every coordinate in [0, L).
+ *           y and z in [0, L).
  *   owner : host int32 [np], written.
  * Pure host function (no context, no device).  PIC_EINVAL: invalid parameters (as
- * pic_workspace_bytes), NULL pointers with np > 0, or a z outside [0, L). */
+ * pic_workspace_bytes), NULL pointers with np > 0, or a y or z outside [0, L). */
 pic_status pic_owner_ranks(const pic_params *p, int32_t nranks, const double *xyz, int64_t np,
                            int32_t *owner);
 
@@ -128,10 +140,11 @@ pic_status pic_workspace_bytes(const pic_params *p, int32_t rank, int32_t nranks
  * PIC_EINVAL: alpha not in [0,1), ppc <= 0, N not a power of two in [16,1024],
  *   k <= 0, dt <= 0, k L / 2 pi not a positive integer, a rank's particle index space
  *   (capacity + migration receive buffer) >= 2^32,
- *   nranks not in {1,2,4,8}, N/nranks < 4, pgrid != {1, nranks}.
+ *   nranks not in {1,2,4,8}, N/nranks < 4, Py Pz != nranks, pencils with N/Py < 8 or N/Pz < 4.
  * PIC_EINVAL also: solver not a pic_solver; PCG settings out of range.
- * PIC_EUNSUPPORTED: a pencil grid (pgrid = {Py > 1, Pz}); the PCG solver at nranks > 1
- *   without the peer-memory transport (it reads the neighbour slabs' planes over NVLink);
+ * PIC_EUNSUPPORTED: a pencil grid (Py > 1) with the PCG / FEM solver; the PCG / FEM solver
+ *   at nranks > 1 without the peer-memory transport (it reads the neighbour slabs' planes
+ *   over NVLink);
  * PIC_ENCCL: NCCL init failed.
  * PIC_ENOMEM: workspace_bytes too small.  PIC_ECUDA: a kernel failed. */
 pic_status pic_init(const pic_params *p, int32_t rank, int32_t nranks, const uint8_t *nccl_id,

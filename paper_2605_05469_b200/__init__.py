@@ -10,6 +10,7 @@ from ._binding import (  # noqa: F401
     Simulation,
     STAGES,
     default_params,
+    domain,
     lib,
     nccl_unique_id,
     owner_ranks,

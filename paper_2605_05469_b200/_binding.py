@@ -69,6 +69,8 @@ SYMBOLS = {
     "pic_nccl_unique_id": (C.c_int, [C.c_void_p]),
     "pic_slab": (C.c_int, [C.POINTER(pic_params), C.c_int32, C.c_int32, C.POINTER(C.c_int32),
                            C.POINTER(C.c_int32), _i64p]),
+    "pic_domain": (C.c_int, [C.POINTER(pic_params), C.c_int32, C.c_int32, C.POINTER(C.c_int32),
+                             C.POINTER(C.c_int32), C.POINTER(C.c_int32), C.POINTER(C.c_int32), _i64p]),
     "pic_owner_ranks": (C.c_int, [C.POINTER(pic_params), C.c_int32, _dp, C.c_int64, C.POINTER(C.c_int32)]),
     "pic_gather_particles": (C.c_int, [_vp, _dp, C.c_int64, _i64p]),
     "pic_migrated": (C.c_int, [_vp, _i64p]),
@@ -168,20 +170,29 @@ def nccl_unique_id() -> bytes:
     return bytes(buf)
 
 
-def owner_ranks(xv: np.ndarray, n: int, L: float, nranks: int) -> np.ndarray:
-    """Owner rank of every particle of xv[6][np] (or [3][np]) -- pic_owner_ranks."""
+def owner_ranks(xv: np.ndarray, n: int, L: float, nranks: int, pgrid=None) -> np.ndarray:
+    """Owner rank of every particle of xv[6][np] (or [3][np]) -- pic_owner_ranks; pgrid =
+    (Py, Pz), default z-slabs (1, nranks)."""
     xv = np.ascontiguousarray(xv, dtype=np.float64)
-    p = default_params(n=n, k=2 * np.pi / L, length=L, pgrid=(1, nranks))
+    p = default_params(n=n, k=2 * np.pi / L, length=L, pgrid=pgrid or (1, nranks))
     out = np.empty(xv.shape[1], dtype=np.int32)
     _check(lib().pic_owner_ranks(C.byref(p), nranks, _d(xv), xv.shape[1],
                                  out.ctypes.data_as(C.POINTER(C.c_int32))))
     return out
 
 
-def slab_select(xv: np.ndarray, n: int, L: float, rank: int, nranks: int) -> np.ndarray:
+def slab_select(xv: np.ndarray, n: int, L: float, rank: int, nranks: int, pgrid=None) -> np.ndarray:
     """The particles of a global state xv[6][np] that rank owns (pic_owner_ranks), in
     their global order -- what each rank passes to set_particles."""
-    return np.ascontiguousarray(xv[:, owner_ranks(xv, n, L, nranks) == rank])
+    return np.ascontiguousarray(xv[:, owner_ranks(xv, n, L, nranks, pgrid) == rank])
+
+
+def domain(p: pic_params, rank: int, nranks: int):
+    """(y0, ny, z0, nz, capacity) of a rank's domain (pic_domain)."""
+    v = [C.c_int32() for _ in range(4)]
+    cap = C.c_int64()
+    _check(lib().pic_domain(C.byref(p), rank, nranks, *[C.byref(x) for x in v], C.byref(cap)))
+    return tuple(x.value for x in v) + (cap.value,)
 
 
 def slab(p: pic_params, rank: int, nranks: int):
@@ -200,7 +211,7 @@ class Simulation:
 
     def __init__(self, n=16, ppc=8, k=0.5, alpha=0.05, dt=0.05, seed=1, half_kick=True,
                  length=0.0, device=None, rank=0, nranks=1, nccl_id: bytes | None = None,
-                 solver="fft", **pcg):
+                 solver="fft", pgrid=None, **pcg):
         """solver: "fft", "pcg" (BJ config 5) or "fem"; pcg keywords
         pcg_tol, pcg_omega, pcg_inner, pcg_outer, pcg_maxit override P:226 / P:260;
         b_ext=(bx, by, bz) / e_ext=(ex, ey, ez): uniform external fields (Eq. 1, D#32)."""
@@ -208,10 +219,10 @@ class Simulation:
 
         self.params = default_params(n=n, ppc=ppc, k=k, alpha=alpha, dt=dt, seed=seed,
                                      half_kick=int(bool(half_kick)), length=length,
-                                     pgrid=(1, nranks), solver=SOLVERS[solver], **pcg)
+                                     pgrid=tuple(pgrid) if pgrid else (1, nranks), solver=SOLVERS[solver], **pcg)
         self.solver = solver
         self.rank, self.nranks = rank, nranks
-        self.z0, self.nz, self.capacity = slab(self.params, rank, nranks)
+        self.y0, self.ny, self.z0, self.nz, self.capacity = domain(self.params, rank, nranks)
         self.device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
         nbytes = workspace_bytes(self.params, rank, nranks)
         with torch.cuda.device(self.device):
@@ -289,13 +300,13 @@ class Simulation:
         _check(lib().pic_set_particles(self.ctx, _d(xv), xv.shape[1]), self.ctx)
 
     def get_grid(self, which: int) -> np.ndarray:
-        out = np.zeros((self.nz, self.n, self.n))
+        out = np.zeros((self.nz, self.ny, self.n))
         _check(lib().pic_get_grid(self.ctx, which, _d(out)), self.ctx)
         return out
 
     def solve_injected(self, rho: np.ndarray):
         rho = np.ascontiguousarray(rho, dtype=np.float64)
-        E = np.zeros((3, self.nz, self.n, self.n))
+        E = np.zeros((3, self.nz, self.ny, self.n))
         a, b = C.c_double(), C.c_double()
         _check(lib().pic_solve_injected(self.ctx, _d(rho), _d(E), C.byref(a), C.byref(b)), self.ctx)
         return E, a.value, b.value

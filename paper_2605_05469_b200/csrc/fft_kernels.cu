@@ -574,15 +574,23 @@ __global__ void __launch_bounds__(kThreads, 3) k_fft_x_inv(Geom g, const double2
     if (halo && g.P > 1) __threadfence_system();
 }
 
-__global__ void k_e4_extract(const double* __restrict__ E4, int64_t nn, int d, double* __restrict__ out) {
-    const int64_t m = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (m < nn) out[m] = E4[4 * m + d];
+// compact [nzl][nyl][n] index m <-> node record of E4 [nzl + 1][nyr][n] (pencils skip the
+// halo row of every plane)
+__device__ __forceinline__ int64_t e4_node(const Geom& g, int64_t m) {
+    const int64_t rowc = m >> ilog2(g.n), x = m & (g.n - 1);
+    const int64_t zl = rowc / g.nyl, yl = rowc - zl * g.nyl;
+    return (zl * g.nyr + yl) * g.n + x;
 }
 
-__global__ void k_e4_pack(const double* __restrict__ a, const double* __restrict__ b,
+__global__ void k_e4_extract(Geom g, const double* __restrict__ E4, int64_t nn, int d, double* __restrict__ out) {
+    const int64_t m = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (m < nn) out[m] = E4[4 * e4_node(g, m) + d];
+}
+
+__global__ void k_e4_pack(Geom g, const double* __restrict__ a, const double* __restrict__ b,
                           const double* __restrict__ c, int64_t nn, double* __restrict__ E4) {
     const int64_t m = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (m < nn) st_node(E4 + 4 * m, a[m], b[m], c[m]);
+    if (m < nn) st_node(E4 + 4 * e4_node(g, m), a[m], b[m], c[m]);
 }
 
 // One CTA, fixed summation order (deterministic): energies = (W_x, W).
@@ -806,13 +814,13 @@ cudaError_t launch_fft_c2c_3d(double2* grid, int M, int sign, const double2* tw,
 }
 
 void launch_e4_extract(const Geom& g, const double* E4, int d, double* out, cudaStream_t s) {
-    const int64_t nn = (int64_t)g.n * g.n * g.nzl;
-    k_e4_extract<<<(unsigned)((nn + 255) / 256), 256, 0, s>>>(E4, nn, d, out);
+    const int64_t nn = (int64_t)g.n * g.nyl * g.nzl;
+    k_e4_extract<<<(unsigned)((nn + 255) / 256), 256, 0, s>>>(g, E4, nn, d, out);
 }
 
 void launch_e4_pack(const Geom& g, const double* const comp[3], double* E4, cudaStream_t s) {
-    const int64_t nn = (int64_t)g.n * g.n * g.nzl;
-    k_e4_pack<<<(unsigned)((nn + 255) / 256), 256, 0, s>>>(comp[0], comp[1], comp[2], nn, E4);
+    const int64_t nn = (int64_t)g.n * g.nyl * g.nzl;
+    k_e4_pack<<<(unsigned)((nn + 255) / 256), 256, 0, s>>>(g, comp[0], comp[1], comp[2], nn, E4);
 }
 
 void launch_energy_reduce(const Geom& g, const double* partials, double* energies, cudaStream_t s) {

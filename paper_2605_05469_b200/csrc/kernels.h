@@ -129,6 +129,9 @@ void launch_reorder_deposit(const Geom& g, const uint32_t* offs, const uint32_t*
                             int push, double* rho_buf, double* ghost, int* err_flag, cudaStream_t s);
 void launch_sort_segments(const uint32_t* offs, int64_t ncell, uint32_t* perm, cudaStream_t s);
 void launch_half_kick(const Geom& g, PState cur, int64_t np, const double* E4, cudaStream_t s);
+// dst[r * dpitch + i] += src[r * spitch + i] (doubles), i < width, r < height
+void launch_add_rows(double* dst, int64_t dpitch, const double* src, int64_t spitch, int64_t width, int64_t height,
+                     cudaStream_t s);
 void launch_add_plane(double* dst, const double* src, int64_t n, cudaStream_t s);
 // -------------------------------------------------------- FD-PCG solve ----
 // (pcg_kernels.cu; BJ config 5, D#26-D#31.)  Fields are

@@ -73,9 +73,13 @@ __device__ __forceinline__ void landau_particle(const Geom& g, const double u[8]
     v[2] = r2 * cos(two_pi * u[6]);
 }
 
-__device__ __forceinline__ bool owns_z(const Geom& g, double z) {
-    const int iz = cell_of(__dmul_rn(z, g.inv_h), g.n);
-    return iz >= g.z0 && iz < g.z0 + g.nzl;
+// Ownership of particle j at P > 1 from its y and z only (u_1, u_2): slabs need z alone.
+__device__ __forceinline__ bool owns_yz(const Geom& g, const double u[8], double k, double alpha) {
+    const int iz = cell_of(__dmul_rn(landau_x(g, u[2], k, alpha), g.inv_h), g.n);
+    if (iz < g.z0 || iz >= g.z0 + g.nzl) return false;
+    if (g.Py == 1) return true;
+    const int iy = cell_of(__dmul_rn(landau_x(g, u[1], k, alpha), g.inv_h), g.n);
+    return iy >= g.y0 && iy < g.y0 + g.nyl;
 }
 
 // P = 1: particle j at index j.
@@ -100,7 +104,7 @@ __global__ void __launch_bounds__(kThreads) k_sample_count(Geom g, int64_t npg, 
     if (j < npg) {
         double u[8];
         uniforms((uint64_t)j, s0, s1, u);
-        own = owns_z(g, landau_x(g, u[2], k, alpha));
+        own = owns_yz(g, u, k, alpha);
     }
     const uint32_t b = __popc(__ballot_sync(0xffffffffu, own));
     if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = b;
@@ -123,7 +127,7 @@ __global__ void __launch_bounds__(kThreads) k_sample_write(Geom g, PState st, in
     bool own = false;
     if (j < npg) {
         uniforms((uint64_t)j, s0, s1, u);
-        own = owns_z(g, landau_x(g, u[2], k, alpha));
+        own = owns_yz(g, u, k, alpha);
     }
     const unsigned bal = __ballot_sync(0xffffffffu, own);
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -178,11 +182,12 @@ __global__ void __launch_bounds__(kThreads) k_key_import(Geom g, PState cur, int
 #pragma unroll
         for (int d = 0; d < 3; ++d)
             if (!(x[d] >= 0.0 && x[d] < g.L)) { x[d] = 0.0; bad = true; }
-        int iz = 0;
-        uint32_t k = key_of(g, x, &iz);
-        if (iz < g.z0 || iz >= g.z0 + g.nzl) {
+        int iz = 0, iy = 0;
+        uint32_t k = key_of(g, x, &iz, &iy);
+        if (!in_domain(g, iy, iz)) {
+            x[1] = ((double)g.y0 + 0.5) / g.inv_h;
             x[2] = ((double)g.z0 + 0.5) / g.inv_h;
-            k = key_of(g, x, &iz);
+            k = key_of(g, x, &iz, &iy);
             bad = true;
         }
         if (bad) {
@@ -251,7 +256,7 @@ __global__ void __launch_bounds__(kThreads, MR ? 3 : 4) k_push_key_brick(Geom g,
     unlkey(g, c0, bx, by, bz);    // bz: slab plane
     for (int q = t; q < 9 * 9 * 5; q += kThreads) {
         const int nx = q % 9, ny = (q / 9) % 9, nz = q / 81;
-        const int64_t m = ((int64_t)(bz + nz) * g.n + ((by + ny) & g.nmask)) * g.n + ((bx + nx) & g.nmask);
+        const int64_t m = ((int64_t)(bz + nz) * g.nyr + yrow(g, by + ny)) * g.n + ((bx + nx) & g.nmask);
         double ex, ey, ez;
         ldg_node(E4 + 4 * m, ex, ey, ez);
         const int row = (nz * 9 + ny) * 8;
@@ -280,7 +285,7 @@ __global__ void __launch_bounds__(kThreads, MR ? 3 : 4) k_push_key_brick(Geom g,
         int ii[3];
         double w[3][2];
         cic_weights(g, x, ii, w);
-        const int lx = ii[0] - bx, ly = ii[1] - by, lz = ii[2] - g.z0 - bz;
+        const int lx = ii[0] - bx, ly = ii[1] - g.y0 - by, lz = ii[2] - g.z0 - bz;
         double e0 = 0.0, e1 = 0.0, e2 = 0.0;
 #pragma unroll
         for (int c = 0; c < 2; ++c)
@@ -301,10 +306,10 @@ __global__ void __launch_bounds__(kThreads, MR ? 3 : 4) k_push_key_brick(Geom g,
         kick(g, ep, v);
         drift(g, x, v);
         st_zv(cur.zv + 2 * i, make_double2(z0, v[2]), make_double2(v[0], v[1]));   // kicked v in place
-        int iz;
-        const uint32_t k = key_of(g, x, &iz);
-        if (MR && (iz < g.z0 || iz >= g.z0 + g.nzl)) {   // leaver: staged, sent below
-            const int dr = iz >> g.mz;
+        int iz, iy;
+        const uint32_t k = key_of(g, x, &iz, &iy);
+        if (MR && !in_domain(g, iy, iz)) {   // leaver: staged, sent below
+            const int dr = owner_of(g, iy, iz);
             const double xo[3] = {x0, y0, z0};
             const uint32_t oldg = gkey_of(g, xo);           // its tie key (D#15)
             const double2 p0 = make_double2(x[0], x[1]), p1 = make_double2(x[2], v[2]),
@@ -369,9 +374,9 @@ __global__ void __launch_bounds__(kThreads) k_key_arrivals(Geom g, const double2
          a += (int64_t)gridDim.x * blockDim.x) {
         const double2 p0 = recv[4 * a], p1 = recv[4 * a + 1];
         const double x[3] = {p0.x, p0.y, p1.x};
-        int iz;
-        uint32_t k = key_of(g, x, &iz);
-        if (iz < g.z0 || iz >= g.z0 + g.nzl) { atomicExch(err + 1, 1); k = 0; }
+        int iz, iy;
+        uint32_t k = key_of(g, x, &iz, &iy);
+        if (!in_domain(g, iy, iz)) { atomicExch(err + 1, 1); k = 0; }
         key[n_old + a] = k;
         const uint32_t r = atomicAdd(count + k, 1u);
         if (r > 0xffffu) atomicExch(err, 1);
@@ -604,7 +609,11 @@ __device__ __forceinline__ void fold_flush(const Geom& g, double* tile, const do
         const double val = tile[q];
         if (val == 0.0) continue;
         const int nx = q % 9, ny = (q / 9) % 9, nz = q / 81;
-        const int ix = (bx + nx) & g.nmask, iy = (by + ny) & g.nmask, iz = bz + nz;
+        const int ix = (bx + nx) & g.nmask, iy = yrow(g, by + ny), iz = bz + nz;
+        if (g.Py > 1) {                     // pencils: the local grid holds the ghost row and
+            atomicAdd(rho + gidx(g, ix, iy, iz), val);   // plane; folded into the neighbours after
+            continue;
+        }
         if (iz == g.nzl) {                  // node plane of the next slab (or own plane 0, P = 1)
             if (g.P > 1) atomicAdd_system(ghost + gidx(g, ix, iy, 0), val);
             else atomicAdd(ghost + gidx(g, ix, iy, 0), val);
@@ -785,7 +794,7 @@ __global__ void __launch_bounds__(kThreads, PIC_RD_MINB) k_reorder_deposit(
         ca = cb;
     }
     fold_flush(g, tile, acc, t, bx, by, bz, rho, ghost);
-    if (MR && bz + 4 == g.nzl && ghost != rho + (int64_t)g.nzl * g.n * g.rp)
+    if (MR && bz + 4 == g.nzl && ghost != rho + (int64_t)g.nzl * g.nyr * g.rp)
         __threadfence_system();   // peer ghost atomics (PIC_P2P_GHOST=2) complete before the barrier
 }
 
@@ -823,6 +832,16 @@ __global__ void k_add_plane(double2* __restrict__ dst, const double2* __restrict
     if (i < n2) {
         const double2 a = dst[i], b = src[i];
         dst[i] = make_double2(a.x + b.x, a.y + b.y);
+    }
+}
+
+// dst[r * dpitch + i] += src[r * spitch + i], i < width, r < height (pencil ghost rows)
+__global__ void k_add_rows(double* __restrict__ dst, int64_t dpitch, const double* __restrict__ src,
+                           int64_t spitch, int64_t width, int64_t height) {
+    const int64_t tot = width * height;
+    for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < tot; q += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t r = q / width, i = q - r * width;
+        dst[r * dpitch + i] += src[r * spitch + i];
     }
 }
 
@@ -887,7 +906,7 @@ void launch_key_import(const Geom& g, PState cur, int64_t np, uint32_t* key, uin
 void launch_push_key(const Geom& g, PState cur, const uint32_t* offs, const double* E4, uint32_t* key,
                      uint16_t* rank, uint32_t* count, double2* send, uint32_t* send_count,
                      const SendSegs& segs, const PeerRecv* peers, int* err_flag, cudaStream_t s) {
-    const unsigned nbrick = (unsigned)(((int64_t)g.n * g.n * g.nzl) / kBrick);
+    const unsigned nbrick = (unsigned)(((int64_t)g.n * g.nyl * g.nzl) / kBrick);
     SendBuf sb{};
     sb.data = send;
     sb.count = send_count;
@@ -955,7 +974,7 @@ void launch_place(const uint32_t* key, const uint16_t* rank, int64_t np, const u
 void launch_reorder_deposit(const Geom& g, const uint32_t* offs, const uint32_t* perm, PState cur,
                             const double2* recv, int64_t n_old, const unsigned long long* dcnt, PState nxt,
                             int push, double* rho_buf, double* ghost, int* err_flag, cudaStream_t s) {
-    const unsigned nbrick = (unsigned)(((int64_t)g.n * g.n * g.nzl) / kBrick);
+    const unsigned nbrick = (unsigned)(((int64_t)g.n * g.nyl * g.nzl) / kBrick);
     static const bool force_mr = getenv("PIC_FORCE_MR") != nullptr;   // diagnostics
     if (g.P == 1 && !force_mr) {
         if (push)
@@ -977,6 +996,13 @@ void launch_sort_segments(const uint32_t* offs, int64_t ncell, uint32_t* perm, c
 void launch_half_kick(const Geom& g, PState cur, int64_t np, const double* E4, cudaStream_t s) {
     if (np == 0) return;
     k_half_kick<<<blocks(np, kThreads), kThreads, 0, s>>>(g, cur, np, E4);
+}
+
+void launch_add_rows(double* dst, int64_t dpitch, const double* src, int64_t spitch, int64_t width, int64_t height,
+                     cudaStream_t s) {
+    if (width * height == 0) return;
+    k_add_rows<<<std::min<unsigned>(blocks(width * height, kThreads), 148u * 8u), kThreads, 0, s>>>(
+        dst, dpitch, src, spitch, width, height);
 }
 
 void launch_add_plane(double* dst, const double* src, int64_t n, cudaStream_t s) {

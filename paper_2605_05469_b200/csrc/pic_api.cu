@@ -59,7 +59,9 @@ int ilog2i(int v) {
 
 struct pic_ctx {
     pic_params p{};
-    Geom g{};
+    Geom g{};                     // this rank's particle / real-space domain (slab or pencil)
+    Geom gs{};                    // the FFT's z-slab geometry (== g for slabs, Py = 1)
+    bool pencil = false;          // Py > 1: pencil domains; the solve redistributes to z-slabs
     int64_t np = 0;               // particles on this rank now
     int64_t np_cap = 0;           // capacity of the particle arrays of this rank
     int64_t np_glob = 0;          // N_p of the whole box
@@ -100,6 +102,16 @@ struct pic_ctx {
     int64_t recv_cap = 0;
     int64_t migrated = 0;         // particles sent by this rank (all steps)
     ncclComm_t comm = nullptr;
+    // pencils (Py > 1): the y-group communicator (the Py ranks sharing pz), the FFT's slab
+    // buffers, and the staging buffers of the redistributions and ghost folds
+    ncclComm_t ycomm = nullptr;
+    double* rho_s = nullptr;      // slab S0 [nzs + 1][n][rp] (== rho for slabs)
+    double* E4_s = nullptr;       // slab field [nzs + 1][n][n][4] (== E4 for slabs)
+    double* xr[2] = {};           // rho pencil -> slab all-to-all: send, recv [Py][nzs][nyl][rp]
+    double* xe[2] = {};           // E4 slab -> pencil all-to-all: send, recv [Py][nzs + 1][nyl + 1][n][4]
+    double* fold[2] = {};         // ghost plane / row staging: send, recv (max(nyr rp, nzl rp) doubles)
+    bool pen_alias = false;       // the pencil scratch in the idle particle buffer (bind_pencil)
+    char* pen_own = nullptr;      // else its own space
     // peer-memory transport (P > 1): every rank's workspace mapped into this process
     // (CUDA IPC over NVLink); transposes, halo/ghost planes and migration are stores
     // and atomics of the producing kernels into the peers' buffers, ordered by
@@ -145,13 +157,17 @@ pic_status validate(const pic_params* p, int32_t rank, int32_t nranks, char* msg
         snprintf(msg, msz, "nranks=%d rank=%d: nranks must be 1, 2, 4 or 8", nranks, rank);
         return PIC_EINVAL;
     }
-    if (!(p->pgrid[0] == 1 && p->pgrid[1] == nranks)) {
-        snprintf(msg, msz, "pgrid = {%d, %d}: this build decomposes in z-slabs only, pgrid = {1, nranks}",
-                 p->pgrid[0], p->pgrid[1]);
-        return p->pgrid[0] * p->pgrid[1] == nranks && p->pgrid[0] > 0 ? PIC_EUNSUPPORTED : PIC_EINVAL;
+    const int Py = p->pgrid[0], Pz = p->pgrid[1];
+    if (!(Py >= 1 && Pz >= 1 && Py * Pz == nranks)) {
+        snprintf(msg, msz, "pgrid = {%d, %d}: need Py * Pz == nranks = %d", Py, Pz, nranks);
+        return PIC_EINVAL;
     }
     if (!is_pow2(p->n) || p->n < 16 || p->n > 1024) { snprintf(msg, msz, "n=%d: power of two in [16,1024]", p->n); return PIC_EINVAL; }
-    if (p->n / nranks < 4) { snprintf(msg, msz, "n/nranks = %d: slabs need >= 4 planes", p->n / nranks); return PIC_EINVAL; }
+    if (p->n / nranks < 4) { snprintf(msg, msz, "n/nranks = %d: the FFT's z-slabs need >= 4 planes", p->n / nranks); return PIC_EINVAL; }
+    if (Py > 1 && (p->n / Py < 8 || p->n / Pz < 4)) {
+        snprintf(msg, msz, "pencils {%d, %d}: need n/Py >= 8 rows and n/Pz >= 4 planes", Py, Pz);
+        return PIC_EINVAL;
+    }
     if (p->ppc <= 0 || p->ppc > 1024) { snprintf(msg, msz, "ppc=%d: must be in [1,1024]", p->ppc); return PIC_EINVAL; }
     if (!(p->k > 0) || !std::isfinite(p->k)) { snprintf(msg, msz, "k must be > 0"); return PIC_EINVAL; }
     if (!(p->alpha >= 0 && p->alpha < 1)) { snprintf(msg, msz, "alpha=%g: need 0 <= alpha < 1", p->alpha); return PIC_EINVAL; }
@@ -167,6 +183,10 @@ pic_status validate(const pic_params* p, int32_t rank, int32_t nranks, char* msg
         snprintf(msg, msz, "solver=%d: PIC_SOLVER_FFT (0), PIC_SOLVER_PCG (1) or PIC_SOLVER_FEM (2)", p->solver);
         return PIC_EINVAL;
     }
+    if (Py > 1 && p->solver != PIC_SOLVER_FFT) {
+        snprintf(msg, msz, "pencils (pgrid = {%d, %d}) run the FFT solver only; PCG / FEM decompose in z-slabs", Py, Pz);
+        return PIC_EUNSUPPORTED;
+    }
     if (p->solver != PIC_SOLVER_FFT &&
         (!(p->pcg_tol > 0) || !(p->pcg_omega > 0 && p->pcg_omega < 2) || p->pcg_inner < 1 || p->pcg_outer < 1 ||
          p->pcg_maxit < 1)) {
@@ -181,6 +201,20 @@ pic_status validate(const pic_params* p, int32_t rank, int32_t nranks, char* msg
     return PIC_OK;
 }
 
+// The FFT's z-slab geometry of a rank: nzs = n / P planes at z0 = rank nzs, every row.
+Geom slab_geom(const Geom& g) {
+    Geom s = g;
+    s.Py = 1;
+    s.nzl = g.n / g.P;
+    s.mz = ilog2i(s.nzl);
+    s.z0 = g.rank * s.nzl;
+    s.nyl = g.n;
+    s.my = ilog2i(g.n);
+    s.y0 = 0;
+    s.nyr = g.n;
+    return s;
+}
+
 Geom make_geom(const pic_params* p, int rank, int nranks) {
     Geom g{};
     g.n = p->n;
@@ -193,9 +227,15 @@ Geom make_geom(const pic_params* p, int rank, int nranks) {
     g.qm_dt = -1.0 * p->dt;     // q/m = -1
     g.P = nranks;
     g.rank = rank;
-    g.nzl = p->n / nranks;
+    g.Py = p->pgrid[0] > 0 ? p->pgrid[0] : 1;
+    const int Pz = nranks / g.Py, py = rank % g.Py, pz = rank / g.Py;
+    g.nzl = p->n / Pz;
     g.mz = ilog2i(g.nzl);
-    g.z0 = rank * g.nzl;
+    g.z0 = pz * g.nzl;
+    g.nyl = p->n / g.Py;
+    g.my = ilog2i(g.nyl);
+    g.y0 = py * g.nyl;
+    g.nyr = g.Py > 1 ? g.nyl + 1 : p->n;
     // external fields (D#32): the coefficients in the oracle's order (oracle_boris_coeffs)
     g.eext = p->e_ext[0] != 0.0 || p->e_ext[1] != 0.0 || p->e_ext[2] != 0.0;
     g.boris = p->b_ext[0] != 0.0 || p->b_ext[1] != 0.0 || p->b_ext[2] != 0.0;
@@ -225,25 +265,37 @@ Sizes sizes(const pic_params* p, const Geom& g) {
         s.recv_cap = 0;
         s.send_len = 0;
     } else {
-        // slab imbalance <= alpha (density (1 + alpha cos k z)), plus fluctuations
-        s.np_cap = (int64_t)(s.np_nom * (1.0 + p->alpha) * 1.05) + 65536;
+        // domain imbalance <= alpha per decomposed dimension (density (1 + alpha cos k z),
+        // times (1 + alpha cos k y) for pencils), plus fluctuations
+        // (the mean of 1 + alpha cos over a block of L / Py rows is at most
+        // 1 + alpha sin(pi / Py) / (pi / Py))
+        const double fy = g.Py > 1 ? 1.0 + p->alpha * std::sin(M_PI / g.Py) / (M_PI / g.Py) : 1.0;
+        const double imb = (1.0 + p->alpha) * fy;
+        s.np_cap = (int64_t)(s.np_nom * imb * 1.05) + 65536;
         // a slab of nzl planes loses ~ E[max(v_z, 0)] dt / (nzl h) per step to each z
         // neighbour (1.3% at 512^3 / 8 ranks): neighbour segments hold 4%
         // of the slab, the others (only reached by |v_z| dt > nzl h) 0.2%; at
         // 1024^3 / 8 ranks this keeps the rank's workspace at ~144 GiB
         const int nb = (int)std::min<int64_t>(s.np_cap, (int64_t)(0.04 * s.np_cap) + 4096);
         const int far = (int)std::min<int64_t>(nb, (int64_t)(0.002 * s.np_cap) + 4096);
-        const int up = (g.rank + 1) % g.P, dn = (g.rank + g.P - 1) % g.P;
-        int64_t off = 0;
+        // face neighbours (one block index differs by one, periodic, the other equal): the
+        // z neighbours of a slab, the four around a pencil; a particle reaches any other
+        // rank (a pencil's diagonal neighbours included) only by crossing two faces in one
+        // step, ~(1.3%)^2 of the particles at 512^3 / 8 ranks
+        const int Py = g.Py, Pz = g.P / g.Py, py = g.rank % Py, pz = g.rank / Py;
+        auto near1 = [](int a, int b, int m) { const int d = ((a - b) % m + m) % m; return d == 1 || d == m - 1; };
+        int64_t off = 0, rc = 0;
         for (int r = 0; r < g.P; ++r) {
-            const int cap = r == g.rank ? 0 : (r == up || r == dn ? nb : far);
+            const int ry = r % Py, rz = r / Py;
+            const bool nbr = r != g.rank && ((ry == py && near1(rz, pz, Pz)) || (rz == pz && near1(ry, py, Py)));
+            const int cap = r == g.rank ? 0 : (nbr ? nb : far);
             s.segs.off[r] = off;
             s.segs.cap[r] = cap;
             off += cap;
+            rc += cap;          // the relation is symmetric: r sends this rank as much room
         }
         s.send_len = off;
-        // arrivals: every source's segment towards this rank (its neighbours' are nb)
-        s.recv_cap = g.P == 2 ? nb : 2 * (int64_t)nb + (int64_t)(g.P - 3) * far;
+        s.recv_cap = rc;
     }
     s.nkey = s.np_cap + s.recv_cap;
     return s;
@@ -258,6 +310,34 @@ pic_status validate_sizes(const Sizes& z, char* msg, size_t msz) {
         return PIC_EINVAL;
     }
     return PIC_OK;
+}
+
+// Pencils: the solve's slab S0 [nzs + 1][n][rp], slab field [nzs + 1][n][n][4] and the
+// redistribution staging (xr: 2 x [Py][nzs][nyl][rp], xe: 2 x [Py][nzs + 1][nyl + 1][n][4]).
+size_t pencil_scratch_bytes(const Geom& g) {
+    const int nzs = g.n / g.P;
+    return sizeof(double) * ((size_t)(nzs + 1) * g.n * g.rp + 4 * (size_t)(nzs + 1) * g.n * g.n +
+                             2 * (size_t)g.nzl * g.nyl * g.rp + 2 * 4 * (size_t)g.Py * (nzs + 1) * (g.nyl + 1) * g.n);
+}
+
+// Point the pencil scratch (pencil_scratch_bytes) at its space: the idle particle buffer
+// (cur ^ 1) when pen_alias, else the context's own.  Called before every use.
+void bind_pencil(pic_ctx* c) {
+    if (!c->pencil) return;
+    const Geom& g = c->g;
+    const int nzs = g.n / g.P;
+    char* b = c->pen_alias ? reinterpret_cast<char*>(c->part[c->cur ^ 1][0]) : c->pen_own;
+    auto take = [&](size_t doubles) {
+        double* p = reinterpret_cast<double*>(b);
+        b += align_up(sizeof(double) * doubles, 256);
+        return p;
+    };
+    c->rho_s = take((size_t)(nzs + 1) * g.n * g.rp);
+    c->E4_s = take(4 * (size_t)(nzs + 1) * g.n * g.n);
+    c->xr[0] = take((size_t)g.nzl * g.nyl * g.rp);
+    c->xr[1] = take((size_t)g.nzl * g.nyl * g.rp);
+    c->xe[0] = take(4 * (size_t)g.Py * (nzs + 1) * (g.nyl + 1) * g.n);
+    c->xe[1] = take(4 * (size_t)g.Py * (nzs + 1) * (g.nyl + 1) * g.n);
 }
 
 // P = 1 with spec_alias: point the spectral scratch at the particle buffer that does not
@@ -278,9 +358,12 @@ size_t carve(pic_ctx* c, const Geom& g, const Sizes& z, char* base) {
         off += bytes;
         return ptr;
     };
-    const int64_t ncell = (int64_t)g.n * g.n * g.nzl;
-    const size_t plane = sizeof(double) * (size_t)g.n * g.rp;          // one pitched real plane
-    const size_t unit = sizeof(double2) * (size_t)g.nzl * g.n * g.px;   // one slab half spectrum
+    const Geom gs = slab_geom(g);                                       // the FFT's slab
+    const bool pencil = g.Py > 1;
+    const int64_t ncell = (int64_t)g.n * g.nyl * g.nzl;
+    const size_t plane = sizeof(double) * (size_t)g.nyr * g.rp;        // one pitched real plane (domain)
+    const size_t splane = sizeof(double) * (size_t)g.n * g.rp;         // one pitched real plane (slab)
+    const size_t unit = sizeof(double2) * (size_t)gs.nzl * g.n * g.px;  // one slab half spectrum
     for (int b = 0; b < 2; ++b) {      // XY then ZV back to back (48 B x cap: also the SoA scratch)
         char* xy = take(sizeof(double2) * (size_t)z.np_cap);
         char* zv = take(2 * sizeof(double2) * (size_t)z.np_cap);
@@ -306,8 +389,17 @@ size_t carve(pic_ctx* c, const Geom& g, const Sizes& z, char* base) {
     const bool spec_alias = g.P == 1 && 48 * (size_t)z.np_cap >= 3 * unit;
     char* sC = spec_alias ? nullptr : take(3 * unit);
     char* sD = g.P > 1 ? take(2 * unit) : nullptr;
-    char* e4 = take(sizeof(double) * 4 * (size_t)g.n * g.n * (g.nzl + 1));
+    char* e4 = take(sizeof(double) * 4 * (size_t)g.n * g.nyr * (g.nzl + 1));
     char* gh = g.P > 1 ? take(plane) : nullptr;
+    // pencils: the FFT's slab S0 and field and the redistribution staging live only inside
+    // the solve, so they sit in the idle particle buffer when it is large enough (bind_pencil;
+    // 16 GB of the 58 GB at 1024^3 x 8 / 8 ranks), else in their own space
+    const size_t fo_b = sizeof(double) * (size_t)g.rp * std::max(g.nyr, g.nzl);
+    const size_t pen_b = pencil_scratch_bytes(g);
+    const bool pen_alias = pencil && 48 * (size_t)z.np_cap >= pen_b + 6 * 256;
+    char* pen = pencil && !pen_alias ? take(pen_b + 6 * 256) : nullptr;
+    char* fo0 = pencil ? take(fo_b) : nullptr;
+    char* fo1 = pencil ? take(fo_b) : nullptr;
     char* tw = take(sizeof(double2) * (size_t)g.n);
     char* pa = take(sizeof(double) * 3 * (size_t)pic::energy_partials(g));
     char* en = take(sizeof(double) * 2 * kMaxEnergySteps);
@@ -338,6 +430,7 @@ size_t carve(pic_ctx* c, const Geom& g, const Sizes& z, char* base) {
         c->rho = reinterpret_cast<double*>(rh);
         c->specA = g.P > 1 ? reinterpret_cast<double2*>(sA) : reinterpret_cast<double2*>(rh);
         c->specB = g.P > 1 ? reinterpret_cast<double2*>(sB) : reinterpret_cast<double2*>(rh);
+        (void)splane;
         c->spec_alias = spec_alias;
         c->spec_unit = unit;
         c->specC = reinterpret_cast<double2*>(sC);
@@ -346,6 +439,12 @@ size_t carve(pic_ctx* c, const Geom& g, const Sizes& z, char* base) {
         c->specD = reinterpret_cast<double2*>(g.P > 1 ? sD : sC + unit);
         if (spec_alias) bind_spec(c);
         c->E4 = reinterpret_cast<double*>(e4);
+        c->rho_s = reinterpret_cast<double*>(rh);
+        c->E4_s = reinterpret_cast<double*>(e4);
+        c->pen_alias = pen_alias;
+        c->pen_own = pen;
+        c->fold[0] = reinterpret_cast<double*>(fo0);
+        c->fold[1] = reinterpret_cast<double*>(fo1);
         c->ghost = reinterpret_cast<double*>(gh);
         c->tw = reinterpret_cast<double2*>(tw);
         c->partials = reinterpret_cast<double*>(pa);
@@ -483,14 +582,117 @@ pic_status agree_any(pic_ctx* c, int local, int* any) {
 
 // E halo plane nzl = the next slab's plane 0 (P = 1 and the peer-memory transport:
 // written by fft_x_inv itself).
+// The FFT's slab field: halo plane nzs = the next slab's plane 0 (slab order = rank order).
 pic_status fill_E_halo(pic_ctx* c) {
-    const Geom& g = c->g;
+    const Geom& g = c->gs;
     if (g.P == 1 || c->p2p) return PIC_OK;
     const size_t pl = (size_t)4 * g.n * g.n;   // doubles per E4 plane
-    double* halo = c->E4 + pl * g.nzl;
+    double* halo = c->E4_s + pl * g.nzl;
     PIC_NCCL(c, ncclGroupStart());
-    PIC_NCCL(c, ncclSend(c->E4, pl, ncclDouble, down(c), c->comm, c->stream));
+    PIC_NCCL(c, ncclSend(c->E4_s, pl, ncclDouble, down(c), c->comm, c->stream));
     PIC_NCCL(c, ncclRecv(halo, pl, ncclDouble, up(c), c->comm, c->stream));
+    PIC_NCCL(c, ncclGroupEnd());
+    return PIC_OK;
+}
+
+// ---------------------------------------------------------------- pencils ----
+// Rank r = pz Py + py owns y in [py nyl, +nyl), z in [pz nzl, +nzl).  The FFT runs on z-slabs
+// of nzs = n / P planes (slab index = rank): the Py ranks of a y-group (same pz) hold the same
+// nzl planes, split in y, and their slabs are those planes split in z (py's slab: planes
+// [py nzs, +nzs) of the group's block) -- so each direction is one all-to-all in the y-group.
+int pen_rank(const pic_ctx* c, int py, int pz) {
+    const int Py = c->g.Py, Pz = c->g.P / Py;
+    return ((pz % Pz + Pz) % Pz) * Py + ((py % Py) + Py) % Py;
+}
+
+// rho of the pencil [nzl][nyl] -> the slab S0 [nzs][n] (rows y = qs nyl + yl from rank qs).
+pic_status pencil_to_slab_rho(pic_ctx* c) {
+    const Geom& g = c->g;
+    const int nzs = c->gs.nzl, Py = g.Py;
+    const size_t rp8 = sizeof(double) * g.rp;
+    const size_t blk = (size_t)nzs * g.nyl * g.rp;          // doubles per destination
+    for (int q = 0; q < Py; ++q)       // planes [q nzs, +nzs), rows 0 .. nyl-1 of each (skip the ghost row)
+        PIC_CUDA(c, cudaMemcpy2DAsync(c->xr[0] + q * blk, g.nyl * rp8, c->rho + (size_t)q * nzs * g.nyr * g.rp,
+                                      g.nyr * rp8, g.nyl * rp8, nzs, cudaMemcpyDeviceToDevice, c->stream));
+    PIC_NCCL(c, ncclAlltoAll(c->xr[0], c->xr[1], blk, ncclDouble, c->ycomm, c->stream));
+    for (int q = 0; q < Py; ++q)       // from rank q of the group: its rows of my slab planes
+        PIC_CUDA(c, cudaMemcpy2DAsync(c->rho_s + (size_t)q * g.nyl * g.rp, (size_t)g.n * rp8, c->xr[1] + q * blk,
+                                      g.nyl * rp8, g.nyl * rp8, nzs, cudaMemcpyDeviceToDevice, c->stream));
+    return PIC_OK;
+}
+
+// The slab field E4_s (planes 0 .. nzs, the last one its halo) -> the pencil E4 [nzl + 1][nyl + 1]:
+// rank q of the group gets rows [q nyl, q nyl + nyl] (the last one wrapping) of the slab's
+// nzs + 1 planes; the pencil's plane qs nzs + nzs comes twice (rank qs's halo, rank qs + 1's
+// plane 0: the same values).
+pic_status slab_to_pencil_E(pic_ctx* c) {
+    const Geom& g = c->g;
+    const int nzs = c->gs.nzl, Py = g.Py;
+    const size_t row8 = sizeof(double) * 4 * g.n, plane8 = row8 * g.n;     // slab E4 row / plane bytes
+    const size_t blk = (size_t)(nzs + 1) * (g.nyl + 1) * 4 * g.n;          // doubles per destination
+    for (int q = 0; q < Py; ++q) {
+        double* dst = c->xe[0] + q * blk;
+        PIC_CUDA(c, cudaMemcpy2DAsync(dst, (g.nyl + 1) * row8, c->E4_s + (size_t)q * g.nyl * 4 * g.n, plane8,
+                                      g.nyl * row8, nzs + 1, cudaMemcpyDeviceToDevice, c->stream));
+        const int yh = ((q + 1) * g.nyl) & g.nmask;                        // the halo row (periodic)
+        PIC_CUDA(c, cudaMemcpy2DAsync(dst + (size_t)g.nyl * 4 * g.n, (g.nyl + 1) * row8,
+                                      c->E4_s + (size_t)yh * 4 * g.n, plane8, row8, nzs + 1,
+                                      cudaMemcpyDeviceToDevice, c->stream));
+    }
+    PIC_NCCL(c, ncclAlltoAll(c->xe[0], c->xe[1], blk, ncclDouble, c->ycomm, c->stream));
+    for (int q = 0; q < Py; ++q)       // planes [q nzs, q nzs + nzs] of the pencil, rows 0 .. nyl
+        PIC_CUDA(c, cudaMemcpyAsync(c->E4 + (size_t)q * nzs * g.nyr * 4 * g.n, c->xe[1] + q * blk,
+                                    sizeof(double) * blk, cudaMemcpyDeviceToDevice, c->stream));
+    return PIC_OK;
+}
+
+// Ghost charge of a pencil (raw CIC sums on plane nzl and row nyl of the local grid) folded
+// into the owners: the ghost plane (rows 0 .. nyl, i.e. with the edge) to the +z neighbour's
+// plane 0, then the ghost row of planes 0 .. nzl-1 (the edge now included at plane 0 of the
+// +z neighbour) to the +y neighbour's row 0.
+pic_status fold_ghost_pencil(pic_ctx* c) {
+    const Geom& g = c->g;
+    const int Py = g.Py, py = g.rank % Py, pz = g.rank / Py;
+    const int64_t plane = (int64_t)g.nyr * g.rp;
+    PIC_NCCL(c, ncclGroupStart());
+    PIC_NCCL(c, ncclSend(c->rho + plane * g.nzl, (size_t)plane, ncclDouble, pen_rank(c, py, pz + 1), c->comm, c->stream));
+    PIC_NCCL(c, ncclRecv(c->fold[1], (size_t)plane, ncclDouble, pen_rank(c, py, pz - 1), c->comm, c->stream));
+    PIC_NCCL(c, ncclGroupEnd());
+    pic::launch_add_plane(c->rho, c->fold[1], plane, c->stream);
+    PIC_LAUNCHED(c, "add_plane");
+    const size_t rp8 = sizeof(double) * g.rp;
+    PIC_CUDA(c, cudaMemcpy2DAsync(c->fold[0], rp8, c->rho + (size_t)g.nyl * g.rp, plane * sizeof(double), rp8,
+                                  g.nzl, cudaMemcpyDeviceToDevice, c->stream));
+    PIC_NCCL(c, ncclGroupStart());
+    PIC_NCCL(c, ncclSend(c->fold[0], (size_t)g.nzl * g.rp, ncclDouble, pen_rank(c, py + 1, pz), c->comm, c->stream));
+    PIC_NCCL(c, ncclRecv(c->fold[1], (size_t)g.nzl * g.rp, ncclDouble, pen_rank(c, py - 1, pz), c->comm, c->stream));
+    PIC_NCCL(c, ncclGroupEnd());
+    pic::launch_add_rows(c->rho, plane, c->fold[1], g.rp, g.rp, g.nzl, c->stream);
+    PIC_LAUNCHED(c, "add_rows");
+    return PIC_OK;
+}
+
+// Halo row and plane of a pencil's E4 written outside the solve (pic_push_injected): the
+// halo row of planes 0 .. nzl-1 from the +y neighbour's row 0, then the halo plane (rows
+// 0 .. nyl: with the edge) from the +z neighbour's plane 0.
+pic_status halo_pencil(pic_ctx* c) {
+    const Geom& g = c->g;
+    bind_pencil(c);
+    const int Py = g.Py, py = g.rank % Py, pz = g.rank / Py;
+    const size_t row = (size_t)4 * g.n, plane = row * g.nyr;            // doubles
+    double* tmp0 = c->xe[0];
+    double* tmp1 = c->xe[1];
+    PIC_CUDA(c, cudaMemcpy2DAsync(tmp0, row * sizeof(double), c->E4, plane * sizeof(double), row * sizeof(double),
+                                  g.nzl, cudaMemcpyDeviceToDevice, c->stream));
+    PIC_NCCL(c, ncclGroupStart());
+    PIC_NCCL(c, ncclSend(tmp0, row * g.nzl, ncclDouble, pen_rank(c, py - 1, pz), c->comm, c->stream));
+    PIC_NCCL(c, ncclRecv(tmp1, row * g.nzl, ncclDouble, pen_rank(c, py + 1, pz), c->comm, c->stream));
+    PIC_NCCL(c, ncclGroupEnd());
+    PIC_CUDA(c, cudaMemcpy2DAsync(c->E4 + row * g.nyl, plane * sizeof(double), tmp1, row * sizeof(double),
+                                  row * sizeof(double), g.nzl, cudaMemcpyDeviceToDevice, c->stream));
+    PIC_NCCL(c, ncclGroupStart());
+    PIC_NCCL(c, ncclSend(c->E4, plane, ncclDouble, pen_rank(c, py, pz - 1), c->comm, c->stream));
+    PIC_NCCL(c, ncclRecv(c->E4 + plane * g.nzl, plane, ncclDouble, pen_rank(c, py, pz + 1), c->comm, c->stream));
     PIC_NCCL(c, ncclGroupEnd());
     return PIC_OK;
 }
@@ -498,6 +700,7 @@ pic_status fill_E_halo(pic_ctx* c) {
 // Halo plane of a field written outside the solve (pic_push_injected).
 pic_status refresh_halo(pic_ctx* c) {
     const Geom& g = c->g;
+    if (c->pencil) return halo_pencil(c);
     const size_t pl = (size_t)4 * g.n * g.n;
     double* halo = c->E4 + pl * g.nzl;
     if (g.P == 1) {
@@ -513,8 +716,8 @@ pic_status refresh_halo(pic_ctx* c) {
 
 // Destination of fft_x_inv's copy of plane 0: the halo plane of the slab below.
 double* halo_dst(pic_ctx* c) {
-    const Geom& g = c->g;
-    double* own = c->E4 + (size_t)4 * g.n * g.n * g.nzl;
+    const Geom& g = c->gs;
+    double* own = c->E4_s + (size_t)4 * g.n * g.n * g.nzl;
     if (g.P == 1) return own;
     return c->p2p ? on_rank(c, down(c), own) : nullptr;
 }
@@ -524,7 +727,7 @@ double* ghost_dst(pic_ctx* c) {
     const Geom& g = c->g;
     if (g.P == 1) return c->rho;
     if (c->ghost_p2p) return on_rank(c, up(c), c->rho);   // PIC_P2P_GHOST=2 (slower, see below)
-    return c->rho + (int64_t)g.n * g.rp * g.nzl;
+    return c->rho + (int64_t)g.nyr * g.rp * g.nzl;
 }
 
 // NCCL transport: rho ghost plane nzl (charge of the next slab's plane 0) folded into its owner.
@@ -535,6 +738,7 @@ double* ghost_dst(pic_ctx* c) {
 pic_status fold_rho_ghost(pic_ctx* c) {
     const Geom& g = c->g;
     if (g.P == 1 || c->ghost_p2p) return PIC_OK;
+    if (c->pencil) return fold_ghost_pencil(c);
     const int64_t pl = (int64_t)g.n * g.rp;
     double* ghost = c->rho + pl * g.nzl;
     if (c->p2p) {
@@ -555,10 +759,15 @@ pic_status fold_rho_ghost(pic_ctx* c) {
 // rho (raw CIC sums of the slab, scaled by `scale` in the multiply) -> E4 with its
 // halo plane, energies (summed over ranks) -> ring slot.
 pic_status solve(pic_ctx* c, double scale, int slot) {
-    const Geom& g = c->g;
+    const Geom& g = c->gs;            // the FFT runs on z-slabs (pencils: redistributed first)
     bind_spec(c);
+    bind_pencil(c);
+    if (c->pencil) {
+        StageScope t(c, PIC_STAGE_XPOSE, 0);
+        PIC_TRY(pencil_to_slab_rho(c));
+    }
     const size_t unit = (size_t)g.nzl * g.n * g.px;   // complex per slab half spectrum
-    const SpecLayout S0{reinterpret_cast<double2*>(c->rho), 0, 1, nullptr};
+    const SpecLayout S0{reinterpret_cast<double2*>(c->rho_s), 0, 1, nullptr};
     SpecLayout A{c->specA, 1, 1, nullptr};          // forward transpose, send side
     SpecLayout Cz{g.P > 1 ? c->specC : c->specD, 1, 2, nullptr};   // return transpose, send side
     const SpecLayout D{c->specD, 1, 2, nullptr};
@@ -572,7 +781,7 @@ pic_status solve(pic_ctx* c, double scale, int slot) {
         A.peer = c->peer_tab;
         Cz.peer = c->peer_tab + 8;
     }
-    { StageScope t(c, PIC_STAGE_FFT_X_FWD, 1); pic::launch_fft_x_fwd(g, c->rho, c->tw, c->stream); }
+    { StageScope t(c, PIC_STAGE_FFT_X_FWD, 1); pic::launch_fft_x_fwd(g, c->rho_s, c->tw, c->stream); }
     PIC_LAUNCHED(c, "fft_x_fwd");
     { StageScope t(c, PIC_STAGE_FFT_Y_FWD, 1); pic::launch_fft_y(g, S0, A, 1, 0, c->tw, c->stream); }
     PIC_LAUNCHED(c, "fft_y_fwd");
@@ -592,7 +801,7 @@ pic_status solve(pic_ctx* c, double scale, int slot) {
     PIC_LAUNCHED(c, "fft_y_inv");
     {
         StageScope t(c, PIC_STAGE_FFT_X_INV, 1);
-        pic::launch_fft_x_inv(g, c->specC, c->E4, halo_dst(c), c->tw, c->partials, c->stream);
+        pic::launch_fft_x_inv(g, c->specC, c->E4_s, halo_dst(c), c->tw, c->partials, c->stream);
     }
     PIC_LAUNCHED(c, "fft_x_inv");
     { StageScope t(c, PIC_STAGE_ENERGY, 1); pic::launch_energy_reduce(g, c->partials, c->energies + 2 * slot, c->stream); }
@@ -602,6 +811,10 @@ pic_status solve(pic_ctx* c, double scale, int slot) {
         PIC_NCCL(c, ncclAllReduce(c->energies + 2 * slot, c->energies + 2 * slot, 2, ncclDouble, ncclSum,
                                   c->comm, c->stream));
         PIC_TRY(fill_E_halo(c));
+    }
+    if (c->pencil) {
+        StageScope t(c, PIC_STAGE_XPOSE, 0);
+        PIC_TRY(slab_to_pencil_E(c));
     }
     c->last_slot = slot;
     return PIC_OK;
@@ -858,7 +1071,7 @@ pic_status push_sort_deposit(pic_ctx* c, int push) {
     {
         StageScope t(c, PIC_STAGE_CLEAR, 0);
         PIC_CUDA(c, cudaMemsetAsync(c->count, 0, sizeof(uint32_t) * (size_t)c->ncell, c->stream));
-        PIC_CUDA(c, cudaMemsetAsync(c->rho, 0, sizeof(double) * (size_t)g.n * g.rp * (g.nzl + 1), c->stream));
+        PIC_CUDA(c, cudaMemsetAsync(c->rho, 0, sizeof(double) * (size_t)g.nyr * g.rp * (g.nzl + 1), c->stream));
         if (g.P > 1) PIC_CUDA(c, cudaMemsetAsync(c->send_count, 0, sizeof(uint32_t) * g.P, c->stream));
         if (g.P > 1 && c->p2p && !push) pic::launch_set_u64(c->dcnt + pic::DC_N, (unsigned long long)c->np, c->stream);
     }
@@ -1002,20 +1215,23 @@ pic_status sync_check(pic_ctx* c) {
     return PIC_OK;
 }
 
-// Slab grid [nzl][n][n] host <-> pitched device planes [nzl][n][rp].
+// Domain grid [nzl][nyl][n] host <-> pitched device planes [nzl][nyr][rp] (pencils skip the
+// ghost row of every plane).
 pic_status copy_grid_to_device(pic_ctx* c, double* dst, const double* host) {
     const Geom& g = c->g;
-    PIC_CUDA(c, cudaMemcpy2DAsync(dst, sizeof(double) * g.rp, host, sizeof(double) * g.n,
-                                  sizeof(double) * g.n, (size_t)g.n * g.nzl, cudaMemcpyHostToDevice,
-                                  c->stream));
+    for (int z = 0; z < (g.Py > 1 ? g.nzl : 1); ++z)
+        PIC_CUDA(c, cudaMemcpy2DAsync(dst + (size_t)z * g.nyr * g.rp, sizeof(double) * g.rp,
+                                      host + (size_t)z * g.nyl * g.n, sizeof(double) * g.n, sizeof(double) * g.n,
+                                      (size_t)g.nyl * (g.Py > 1 ? 1 : g.nzl), cudaMemcpyHostToDevice, c->stream));
     return PIC_OK;
 }
 
 pic_status copy_grid_to_host(pic_ctx* c, double* host, const double* src) {
     const Geom& g = c->g;
-    PIC_CUDA(c, cudaMemcpy2DAsync(host, sizeof(double) * g.n, src, sizeof(double) * g.rp,
-                                  sizeof(double) * g.n, (size_t)g.n * g.nzl, cudaMemcpyDeviceToHost,
-                                  c->stream));
+    for (int z = 0; z < (g.Py > 1 ? g.nzl : 1); ++z)
+        PIC_CUDA(c, cudaMemcpy2DAsync(host + (size_t)z * g.nyl * g.n, sizeof(double) * g.n,
+                                      src + (size_t)z * g.nyr * g.rp, sizeof(double) * g.rp, sizeof(double) * g.n,
+                                      (size_t)g.nyl * (g.Py > 1 ? 1 : g.nzl), cudaMemcpyDeviceToHost, c->stream));
     return PIC_OK;
 }
 
@@ -1160,6 +1376,20 @@ pic_status pic_slab(const pic_params* p, int32_t rank, int32_t nranks, int32_t* 
     return PIC_OK;
 }
 
+pic_status pic_domain(const pic_params* p, int32_t rank, int32_t nranks, int32_t* y0, int32_t* ny, int32_t* z0,
+                      int32_t* nz, int64_t* capacity) {
+    char msg[256];
+    pic_status st = validate(p, rank, nranks, msg, sizeof(msg));
+    if (st != PIC_OK) { snprintf(g_init_error, sizeof(g_init_error), "%s", msg); return st; }
+    const Geom g = make_geom(p, rank, nranks);
+    if (y0) *y0 = g.y0;
+    if (ny) *ny = g.nyl;
+    if (z0) *z0 = g.z0;
+    if (nz) *nz = g.nzl;
+    if (capacity) *capacity = sizes(p, g).np_cap;
+    return PIC_OK;
+}
+
 pic_status pic_init(const pic_params* p, int32_t rank, int32_t nranks, const uint8_t* nccl_id,
                     void* workspace, size_t workspace_bytes, void* cuda_stream, pic_ctx** out) {
     if (!out) return PIC_EINVAL;
@@ -1187,9 +1417,11 @@ pic_status pic_init(const pic_params* p, int32_t rank, int32_t nranks, const uin
     c->p = *p;
     c->g = g;
     c->g.cap = z.np_cap;
+    c->gs = slab_geom(c->g);
+    c->pencil = g.Py > 1;
     c->ws = reinterpret_cast<char*>(workspace);
     c->np_glob = (int64_t)p->ppc * p->n * p->n * p->n;
-    c->ncell = (int64_t)g.n * g.n * g.nzl;
+    c->ncell = (int64_t)g.n * g.nyl * g.nzl;
     c->q = -((g.L * g.L) * g.L) / (double)c->np_glob;
     c->deposit_scale = c->q * ((g.inv_h * g.inv_h) * g.inv_h);
     c->stream = reinterpret_cast<cudaStream_t>(cuda_stream);
@@ -1216,6 +1448,7 @@ pic_status pic_init(const pic_params* p, int32_t rank, int32_t nranks, const uin
         snprintf(g_init_error, sizeof(g_init_error), "%s", c->err);
         for (int r = 0; r < 8; ++r)
             if (c->ipc_open[r]) cudaIpcCloseMemHandle(c->ipc_open[r]);
+        if (c->ycomm) ncclCommDestroy(c->ycomm);
         if (c->comm) ncclCommDestroy(c->comm);
         delete c;
         return s;
@@ -1228,7 +1461,17 @@ pic_status pic_init(const pic_params* p, int32_t rank, int32_t nranks, const uin
             snprintf(c->err, sizeof(c->err), "ncclCommInitRank: %s", ncclGetErrorString(r));
             return bail(PIC_ENCCL);
         }
-        if ((st = setup_p2p(c)) != PIC_OK) return bail(st);
+        if (c->pencil) {
+            // the y-group (ranks sharing pz) for the pencil <-> slab redistributions; pencils
+            // use the NCCL transport (the peer-memory paths are written for z-slabs)
+            r = ncclCommSplit(c->comm, rank / g.Py, rank % g.Py, &c->ycomm, nullptr);
+            if (r != ncclSuccess) {
+                snprintf(c->err, sizeof(c->err), "ncclCommSplit: %s", ncclGetErrorString(r));
+                return bail(PIC_ENCCL);
+            }
+        } else if ((st = setup_p2p(c)) != PIC_OK) {
+            return bail(st);
+        }
         if (p->solver != PIC_SOLVER_FFT && !c->p2p) {
             snprintf(c->err, sizeof(c->err), "the PCG / FEM solvers at P > 1 need the peer-memory transport");
             return bail(PIC_EUNSUPPORTED);
@@ -1332,6 +1575,7 @@ void pic_free(pic_ctx* c) {
     for (cudaEvent_t e : c->ev_pool) cudaEventDestroy(e);
     for (int r = 0; r < 8; ++r)
         if (c->ipc_open[r]) cudaIpcCloseMemHandle(c->ipc_open[r]);
+    if (c->ycomm) ncclCommDestroy(c->ycomm);
     if (c->comm) ncclCommDestroy(c->comm);
     delete c;
 }
@@ -1459,15 +1703,18 @@ pic_status pic_owner_ranks(const pic_params* p, int32_t nranks, const double* xy
     if (st != PIC_OK) { snprintf(g_init_error, sizeof(g_init_error), "%s", msg); return st; }
     if (np < 0 || (np > 0 && (!xyz || !owner))) return PIC_EINVAL;
     const Geom g = make_geom(p, 0, nranks);
+    const double* y = xyz + np;
     const double* z = xyz + 2 * np;
     for (int64_t j = 0; j < np; ++j) {
-        if (!(z[j] >= 0.0 && z[j] < g.L)) {
-            snprintf(g_init_error, sizeof(g_init_error), "pic_owner_ranks: z[%lld] outside [0, L)", (long long)j);
+        if (!(z[j] >= 0.0 && z[j] < g.L) || !(y[j] >= 0.0 && y[j] < g.L)) {
+            snprintf(g_init_error, sizeof(g_init_error), "pic_owner_ranks: y/z[%lld] outside [0, L)", (long long)j);
             return PIC_EINVAL;
         }
-        int iz = (int)std::floor(z[j] * g.inv_h);      // D#5: floor(z inv_h), clamped to N - 1
+        int iz = (int)std::floor(z[j] * g.inv_h);      // D#5: floor(x inv_h), clamped to N - 1
         iz = iz > g.n - 1 ? g.n - 1 : iz;
-        owner[j] = iz / g.nzl;
+        int iy = (int)std::floor(y[j] * g.inv_h);
+        iy = iy > g.n - 1 ? g.n - 1 : iy;
+        owner[j] = (iz / g.nzl) * g.Py + iy / g.nyl;   // rank = pz Py + py (slabs: Py = 1)
     }
     return PIC_OK;
 }

@@ -20,10 +20,14 @@ struct Geom {
     double inv_h;   // (double)n / L  (D#5)
     double dt;      // time step
     double qm_dt;   // (q/m) dt = -dt
-    // z-slab decomposition over P ranks (P = 1: the whole box): this rank owns the
-    // cell/node planes z0 .. z0 + nzl - 1, nzl = n / P = 2^mz.  Local grids carry
-    // one extra plane (nzl): the ghost of the charge, the halo of the field.
+    // Domain decomposition over P = Py Pz ranks (P = 1: the whole box), rank = pz Py + py:
+    // this rank owns the cells/nodes with z in [z0, z0 + nzl), nzl = n / Pz = 2^mz, and y
+    // in [y0, y0 + nyl), nyl = n / Py = 2^my (Py = 1: z-slabs, y0 = 0, nyl = n).  Local
+    // real-space grids carry one extra plane (nzl) -- the ghost of the charge, the halo of
+    // the field -- and, for pencils (Py > 1), one extra row per plane (nyl): nyr rows per
+    // plane, n for slabs, nyl + 1 for pencils.
     int P, rank, z0, nzl, mz;
+    int Py, y0, nyl, my, nyr;
     int64_t cap;    // particle capacity of this rank's arrays (sorted positions beyond it: overflow)
     // uniform external fields (Eq. 1, D#32): eext -> E += ee; boris -> Boris kick with
     // hq = (q/m) dt / 2, bt = hq B_ext, bs = 2 bt / (1 + |bt|^2)
@@ -31,9 +35,19 @@ struct Geom {
     double ee[3], bt[3], bs[3], hq;
 };
 
-// Index of node (ix, iy, slab plane izl) in a pitched real grid [nzl + 1][n][rp].
-__device__ __forceinline__ int64_t gidx(const Geom& g, int ix, int iy, int izl) {
-    return ((int64_t)izl * g.n + iy) * g.rp + ix;
+// Index of node (ix, local row iyl, local plane izl) in a pitched real grid [nzl + 1][nyr][rp].
+__device__ __forceinline__ int64_t gidx(const Geom& g, int ix, int iyl, int izl) {
+    return ((int64_t)izl * g.nyr + iyl) * g.rp + ix;
+}
+
+// Local row of the node row v = (local cell row) + (0 or 1): slabs hold every row, so it
+// wraps periodically; pencils hold rows 0 .. nyl (row nyl: the ghost / halo row).
+__device__ __forceinline__ int yrow(const Geom& g, int v) { return g.Py > 1 ? v : (v & g.nmask); }
+
+// Owner rank of global cell (iy, iz), and whether this rank owns it.
+__device__ __forceinline__ int owner_of(const Geom& g, int iy, int iz) { return (iz >> g.mz) * g.Py + (iy >> g.my); }
+__device__ __forceinline__ bool in_domain(const Geom& g, int iy, int iz) {
+    return iz >= g.z0 && iz < g.z0 + g.nzl && iy >= g.y0 && iy < g.y0 + g.nyl;
 }
 
 // Cell index along one dimension: floor(x * inv_h), clamped to [0, n-1] (D#5).
@@ -88,11 +102,13 @@ __device__ __forceinline__ uint32_t gkey_of(const Geom& g, const double x[3]) {
     return morton(i0, i1, i2);
 }
 
-// Rank-local key of cell (ix, iy, izl) of the slab: the global Morton key with the
-// slab's constant z bits (>= mz) removed -- low 3 mz bits interleave (x, y, izl),
-// the rest interleave the high bits of (x, y).  Dense on [0, n^2 nzl) and monotone
-// with the global key on the slab, so the rank's sorted array is the global sorted
-// array restricted to the slab.  P = 1: the global Morton key.
+// Rank-local key of cell (ix, iyl, izl) of this rank's domain: the global Morton key with
+// the domain's constant bits (y bits >= my, z bits >= mz) squeezed out -- for bit
+// b < m1 = min(my, mz) the triple (x, y, z), for m1 <= b < m2 = max(my, mz) the pair (x, y)
+// or (x, z), above m2 x alone.  Dense on [0, n nyl nzl) and monotone with the global key on
+// the domain, so the rank's sorted array is the global sorted array restricted to it; the
+// low 8 bits are still x0 y0 z0 x1 y1 z1 x2 y2 (nyl >= 8, nzl >= 4), so a 256-key brick is
+// 8 x 8 x 4 cells.  P = 1: the global Morton key.
 __device__ __forceinline__ uint32_t spread2(uint32_t v) {
     v &= 0x3ffu;
     v = (v | (v << 8)) & 0x00FF00FFu;
@@ -109,24 +125,34 @@ __device__ __forceinline__ uint32_t compact2(uint32_t v) {
     v = (v ^ (v >> 8)) & 0x0000FFFFu;
     return v;
 }
-__device__ __forceinline__ uint32_t lkey(const Geom& g, int ix, int iy, int izl) {
-    const uint32_t m = (1u << g.mz) - 1u;
-    return morton(ix & m, iy & m, izl) | ((spread2(ix >> g.mz) | (spread2(iy >> g.mz) << 1)) << (3 * g.mz));
+__device__ __forceinline__ uint32_t lkey(const Geom& g, int ix, int iyl, int izl) {
+    const int m1 = g.my < g.mz ? g.my : g.mz, m2 = g.my < g.mz ? g.mz : g.my;
+    const uint32_t k1 = (1u << m1) - 1u;
+    const uint32_t lo = morton(ix & k1, iyl & k1, izl & k1);
+    const uint32_t other = (uint32_t)(g.my > g.mz ? iyl : izl) >> m1;   // the longer local dimension
+    const uint32_t mid = spread2(((uint32_t)ix >> m1) & ((1u << (m2 - m1)) - 1u)) | (spread2(other) << 1);
+    return lo | (mid << (3 * m1)) | (((uint32_t)ix >> m2) << (3 * m1 + 2 * (m2 - m1)));
 }
-__device__ __forceinline__ void unlkey(const Geom& g, uint32_t k, int& ix, int& iy, int& izl) {
-    const uint32_t lo = k & ((1u << (3 * g.mz)) - 1u), hi = k >> (3 * g.mz);
-    ix = (int)(compact3(lo) | (compact2(hi) << g.mz));
-    iy = (int)(compact3(lo >> 1) | (compact2(hi >> 1) << g.mz));
-    izl = (int)compact3(lo >> 2);
+__device__ __forceinline__ void unlkey(const Geom& g, uint32_t k, int& ix, int& iyl, int& izl) {
+    const int m1 = g.my < g.mz ? g.my : g.mz, m2 = g.my < g.mz ? g.mz : g.my;
+    const uint32_t lo = k & ((1u << (3 * m1)) - 1u);
+    const uint32_t mid = (k >> (3 * m1)) & ((1u << (2 * (m2 - m1))) - 1u);
+    const uint32_t hi = k >> (3 * m1 + 2 * (m2 - m1));
+    ix = (int)(compact3(lo) | (compact2(mid) << m1) | (hi << m2));
+    const int other = (int)(compact2(mid >> 1) << m1);
+    iyl = (int)compact3(lo >> 1) | (g.my > g.mz ? other : 0);
+    izl = (int)compact3(lo >> 2) | (g.mz > g.my ? other : 0);
 }
 
-// Local key of the cell of x on this rank; *izg = its global z plane.
-__device__ __forceinline__ uint32_t key_of(const Geom& g, const double x[3], int* izg = nullptr) {
+// Local key of the cell of x on this rank; *iyg / *izg = its global y row / z plane.
+__device__ __forceinline__ uint32_t key_of(const Geom& g, const double x[3], int* izg = nullptr,
+                                           int* iyg = nullptr) {
     int i0 = cell_of(__dmul_rn(x[0], g.inv_h), g.n);
     int i1 = cell_of(__dmul_rn(x[1], g.inv_h), g.n);
     int i2 = cell_of(__dmul_rn(x[2], g.inv_h), g.n);
     if (izg) *izg = i2;
-    return lkey(g, i0, i1, i2 - g.z0);
+    if (iyg) *iyg = i1;
+    return lkey(g, i0, i1 - g.y0, i2 - g.z0);
 }
 
 // CIC weights of one position: cell index i[d] and w[d][0] = 1 - f, w[d][1] = f,
@@ -143,7 +169,7 @@ __device__ __forceinline__ void cic_weights(const Geom& g, const double x[3], in
     }
 }
 
-// One 32-byte node record (E_x, E_y, E_z, 0) of the field grid E4[n][n][n][4]:
+// One 32-byte node record (E_x, E_y, E_z, 0) of the field grid E4[nzl + 1][nyr][n][4]:
 // a single 256-bit read-only load (LDG.E.ENL2.256).
 __device__ __forceinline__ void ldg_node(const double* __restrict__ p, double& ex, double& ey,
                                          double& ez) {
@@ -167,7 +193,7 @@ __device__ __forceinline__ void gather_E(const Geom& g, const double* __restrict
     for (int c = 0; c < 2; ++c) {
 #pragma unroll
         for (int b = 0; b < 2; ++b) {
-            const int64_t row = ((int64_t)(i[2] - g.z0 + c) * g.n + ((i[1] + b) & g.nmask)) * g.n;
+            const int64_t row = ((int64_t)(i[2] - g.z0 + c) * g.nyr + yrow(g, i[1] - g.y0 + b)) * g.n;
 #pragma unroll
             for (int a = 0; a < 2; ++a) {
                 const double wt = __dmul_rn(__dmul_rn(w[0][a], w[1][b]), w[2][c]);

@@ -40,6 +40,8 @@ def main():
 
     L, dt = 4 * np.pi, 0.05
     solver = os.environ.get("MP_SOLVER", "fft")     # "pcg": BJ config 5 (FD-PCG solve)
+    pg = os.environ.get("MP_PGRID")                 # "PyxPz": pencils (default z-slabs)
+    pgrid = tuple(int(v) for v in pg.split("x")) if pg else (1, world)
 
     def oracle_run(xv0, nsteps, phi0=None):
         if solver == "pcg":
@@ -53,8 +55,9 @@ def main():
 
     # ---- case 1: import the same global state, step, compare with the oracle
     xv = landau_state(n, ppc, seed=11)
-    mine = slab_select(xv, n, L, rank, world)
-    sim = Simulation(n=n, ppc=ppc, half_kick=False, rank=rank, nranks=world, nccl_id=fresh_id(), solver=solver)
+    mine = slab_select(xv, n, L, rank, world, pgrid)
+    sim = Simulation(n=n, ppc=ppc, half_kick=False, rank=rank, nranks=world, nccl_id=fresh_id(), solver=solver,
+                     pgrid=pgrid)
     sim.set_particles(mine)
     ex = sim.step(steps)
     got = sim.get_particles()
@@ -92,7 +95,8 @@ def main():
     sim.close()
 
     # ---- case 2: the library's own sampler on P ranks
-    sim = Simulation(n=n, ppc=ppc, seed=9, rank=rank, nranks=world, nccl_id=fresh_id(), solver=solver)
+    sim = Simulation(n=n, ppc=ppc, seed=9, rank=rank, nranks=world, nccl_id=fresh_id(), solver=solver,
+                     pgrid=pgrid)
     ex2 = sim.step(10)
     npl = sim.np
     counts = [None] * world
@@ -108,7 +112,8 @@ def main():
         _, rex2 = oracle_run(ref0, 10, phi0)
         rel2 = np.max(np.abs(ex2 - rex2) / rex2)
         assert rel2 <= 1e-9, rel2
-        print(f"MP OK P={world} n={n} ppc={ppc} steps={steps} solver={solver} transport={transport} | {msg1} | "
+        print(f"MP OK P={world} pgrid={pgrid[0]}x{pgrid[1]} n={n} ppc={ppc} steps={steps} solver={solver} "
+              f"transport={transport} | {msg1} | "
               f"init: W_x rel {rel2:.1e} counts {counts}",
               flush=True)
     sim.close()

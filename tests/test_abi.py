@@ -46,8 +46,8 @@ def test_invalid_parameters_rejected(bad):
 
 
 def test_multi_rank_geometry():
-    """z-slabs: rank r owns planes [r N/P, (r+1) N/P); pgrid must be
-    {1, P}; P in {1, 2, 4, 8}; slabs need >= 4 planes; pencils are not built."""
+    """z-slabs: rank r owns planes [r N/P, (r+1) N/P); Py Pz = P; P in
+    {1, 2, 4, 8}; the FFT's slabs need >= 4 planes; pencils run the FFT solver only."""
     for P in (1, 2, 4, 8):
         p = B.default_params(n=64, pgrid=(1, P))
         zs = [B.slab(p, r, P) for r in range(P)]
@@ -60,8 +60,11 @@ def test_multi_rank_geometry():
         B.workspace_bytes(B.default_params(n=64, pgrid=(1, 1)), rank=0, nranks=2)
     assert e.value.status == B.PIC_EINVAL
     with pytest.raises(B.PicError) as e:
-        B.workspace_bytes(B.default_params(n=64, pgrid=(2, 2)), rank=0, nranks=4)
+        B.workspace_bytes(B.default_params(n=64, pgrid=(2, 2), solver=1), rank=0, nranks=4)
     assert e.value.status == B.PIC_EUNSUPPORTED
+    with pytest.raises(B.PicError) as e:       # pencil rows: n / Py >= 8
+        B.workspace_bytes(B.default_params(n=16, pgrid=(4, 1)), rank=0, nranks=4)
+    assert e.value.status == B.PIC_EINVAL
     with pytest.raises(B.PicError) as e:
         B.workspace_bytes(B.default_params(n=16, pgrid=(1, 8)), rank=0, nranks=8)
     assert e.value.status == B.PIC_EINVAL
@@ -169,3 +172,33 @@ def test_pif_sizes_rejected_on_the_host():
         b = C.c_size_t()
         st = B.lib().pic_pif_workspace_bytes(n, 4 * np.pi, 1e-4, 0, C.byref(b))
         assert (st == 0) == ok, (n, st)
+
+
+@pytest.mark.parametrize("Py,Pz", [(2, 1), (2, 2), (2, 4), (4, 2), (8, 1)])
+def test_pencil_domains_partition_the_box(Py, Pz):
+    """Pencils (BJ config 4): rank r = pz Py + py owns rows [py N/Py, +N/Py) and
+    planes [pz N/Pz, +N/Pz); the domains tile the box; pic_owner_ranks follows the same rule
+    (restated here); every rank's workspace fits a B200 at 1024^3 x 8 ppc on 8 ranks."""
+    import numpy as np
+    from paper_2605_05469_b200 import owner_ranks
+
+    n, P = 64, Py * Pz
+    p = B.default_params(n=n, pgrid=(Py, Pz))
+    cover = np.zeros((n, n), dtype=int)
+    for r in range(P):
+        y0, ny, z0, nz, cap = B.domain(p, r, P)
+        assert (y0, ny, z0, nz) == ((r % Py) * n // Py, n // Py, (r // Py) * n // Pz, n // Pz)
+        cover[z0:z0 + nz, y0:y0 + ny] += 1
+        assert cap >= 8 * n ** 3 // P
+    assert np.all(cover == 1)
+    L = 4 * np.pi
+    rng = np.random.default_rng(7)
+    xv = rng.random((6, 5000)) * L
+    own = owner_ranks(xv, n, L, P, (Py, Pz))
+    iy = np.minimum(np.floor(xv[1] * (n / L)).astype(int), n - 1)
+    iz = np.minimum(np.floor(xv[2] * (n / L)).astype(int), n - 1)
+    assert np.array_equal(own, (iz // (n // Pz)) * Py + iy // (n // Py))
+    if P == 8:
+        big = B.default_params(n=1024, ppc=8, pgrid=(Py, Pz))
+        for r in range(P):
+            assert B.workspace_bytes(big, r, P) < 170 * 2 ** 30
