@@ -665,8 +665,10 @@ def main():
             sk.bind(("127.0.0.1", 0))
             port = sk.getsockname()[1]
         env = dict(os.environ)
-        env.setdefault("NCCL_DEBUG", "INFO")
-        env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+        if env.get("NCCL_DEBUG", "").upper() not in ("INFO", "TRACE"):
+            env["NCCL_DEBUG"] = "INFO"                   # the communicators' init lines (nranks)
+            env["NCCL_DEBUG_SUBSYS"] = "INIT"
+        env.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")   # keep stdout for the JSON line
         cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
                "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__), *sys.argv[1:]]
         log("relaunching under torchrun: " + " ".join(cmd))
@@ -683,8 +685,10 @@ def main():
         import torch
         import torch.distributed as dist
 
-        os.environ.setdefault("NCCL_DEBUG", "INFO")          # the communicator's init lines (nranks)
-        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+        if os.environ.get("NCCL_DEBUG", "").upper() not in ("INFO", "TRACE"):
+            os.environ["NCCL_DEBUG"] = "INFO"                # the communicators' init lines (nranks)
+            os.environ["NCCL_DEBUG_SUBSYS"] = "INIT"
+        os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
         torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", 0)))
         dist.init_process_group("nccl")
         log(f"[rank {rank}] torch.distributed NCCL process group: world_size={dist.get_world_size()}")

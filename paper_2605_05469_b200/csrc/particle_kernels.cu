@@ -607,6 +607,9 @@ __device__ __forceinline__ void fold_flush(const Geom& g, double* tile, const do
     }
     for (int q = t; q < 9 * 9 * 5; q += kThreads) {
         const double val = tile[q];
+#ifdef PIC_RD_SKIP_FLUSH     // diagnostics only (no charge): the cost of the global flush
+        if (val != 12345.0) continue;
+#endif
         if (val == 0.0) continue;
         const int nx = q % 9, ny = (q / 9) % 9, nz = q / 81;
         const int ix = (bx + nx) & g.nmask, iy = yrow(g, by + ny), iz = bz + nz;
