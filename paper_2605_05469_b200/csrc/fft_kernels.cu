@@ -244,6 +244,9 @@ __host__ __device__ constexpr int z_tw(int n) { int t = 2048 / n; return t > 8 ?
 #ifndef PIC_ZMUL_DIRECT
 #define PIC_ZMUL_DIRECT 0
 #endif
+#ifndef PIC_XINV_DIRECT
+#define PIC_XINV_DIRECT 0
+#endif
 __host__ __device__ constexpr int zmul_tw(int n) { int t = PIC_ZMUL_TWN / n; return t > 8 ? 8 : (t < 1 ? 1 : t); }
 
 // Every pass is a persistent loop over tiles (grid = resident CTAs): the input of
@@ -511,10 +514,16 @@ __global__ void __launch_bounds__(kThreads, 3) k_fft_x_inv(Geom g, const double2
     __shared__ double red[3][kThreads / 32];
     constexpr int len = 1 << LOGN;
     const int R = xi_rows(g.n), ls = line_stride(len), px = g.px;
+#if PIC_XINV_DIRECT   // stage 0 reads the spectra from global memory (L1): no staging buffer
+    double2* in = nullptr;
+    double2* sm = smx;                   // [3 R][ls]
+#else
     double2* in = smx;                   // [3][R][px]
     double2* sm = smx + 3 * R * px;      // [3 R][ls]
+#endif
     const int64_t nrows = (int64_t)g.nzl * g.n, ntile = (nrows + R - 1) / R;
     auto prefetch = [&](int64_t t) {
+        if (PIC_XINV_DIRECT) return;
         const int64_t row0 = t * R;
         const int per = (int)min((int64_t)R, nrows - row0) * px;
         for (int i = threadIdx.x; i < 3 * per; i += blockDim.x) {
@@ -533,8 +542,13 @@ __global__ void __launch_bounds__(kThreads, 3) k_fft_x_inv(Geom g, const double2
         __syncthreads();
         auto src = [&](int l, int k) {          // line l = rl * 3 + d
             const int rl = l / 3, d = l - 3 * rl;
+#if PIC_XINV_DIRECT
+            const double2* X = spec + ((int64_t)d * nrows + row0 + rl) * px;
+            const double2 xk = __ldg(X + k), xc = conj2(__ldg(X + len - k));
+#else
             const double2* X = in + (d * R + rl) * px;
             const double2 xk = X[k], xc = conj2(X[len - k]);
+#endif
             const double2 ze = cadd(xk, xc);
             const double2 zo = cmul(csub(xk, xc), conj2(__ldg(tw + k)));
             return make_double2(ze.x - zo.y, ze.y + zo.x);
@@ -728,7 +742,7 @@ static size_t x_fwd_smem(const Geom& g) {
 }
 static size_t x_inv_smem(const Geom& g) {
     const int len = g.n / 2, R = xi_rows(g.n);
-    return sizeof(double2) * 3 * (size_t)R * (g.px + line_stride(len));
+    return sizeof(double2) * 3 * (size_t)R * ((PIC_XINV_DIRECT ? 0 : g.px) + line_stride(len));
 }
 static int64_t x_tiles(const Geom& g, int R) { return ((int64_t)g.nzl * g.n + R - 1) / R; }
 

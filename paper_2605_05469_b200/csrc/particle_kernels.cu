@@ -232,7 +232,12 @@ __device__ __forceinline__ double2* leave_rec(const SendBuf& sb, int dr, uint32_
     return slot < (uint64_t)sb.peers.recv_cap ? sb.peers.peer_recv[dr] + (int64_t)slot * 4 : nullptr;
 }
 
-constexpr int kLeaveCap = 128;   // leavers staged per brick before one atomic per destination
+// Leavers staged per brick before one atomic per destination.  A brick on a slab face
+// loses ~20% of its ~2048 particles per step (the thermal displacement is ~2 cells against
+// a 4-cell brick), so 128 slots overflowed on every face brick and the overflow took one
+// global atomic per particle on a single counter per destination (r02: the P > 1 push_key
+// cost +55% per particle at P = 4).  320 slots plus a warp-aggregated overflow.
+constexpr int kLeaveCap = 320;
 
 template <bool MR>
 __global__ void __launch_bounds__(kThreads, MR ? 3 : 4) k_push_key_brick(Geom g, PState cur,
@@ -320,8 +325,13 @@ __global__ void __launch_bounds__(kThreads, MR ? 3 : 4) k_push_key_brick(Geom g,
                 lbuf[s][0] = p0; lbuf[s][1] = p1; lbuf[s][2] = p2; lbuf[s][3] = p3;
                 ldst[s] = (uint8_t)dr;
                 atomicAdd(&lcount[dr], 1u);
-            } else {                                  // rare: straight to the global buffer
-                double2* d = leave_rec(sb, dr, leave_reserve(sb, dr, 1u));
+            } else {      // staging full: straight to the global buffer, one reserve per warp and destination
+                const unsigned grp = __match_any_sync(__activemask(), dr);
+                const int lead = __ffs(grp) - 1, lane = threadIdx.x & 31;
+                uint32_t base = 0;
+                if (lane == lead) base = leave_reserve(sb, dr, (uint32_t)__popc(grp));
+                base = __shfl_sync(grp, base, lead) + (uint32_t)__popc(grp & ((1u << lane) - 1u));
+                double2* d = leave_rec(sb, dr, base);
                 if (d) {
                     d[0] = p0; d[1] = p1; d[2] = p2; d[3] = p3;
                 } else {
@@ -593,25 +603,57 @@ __global__ void __launch_bounds__(kThreads) k_place(const uint32_t* __restrict__
 }
 
 // Node tile of a brick: 9 x 9 x 5 nodes, slab planes bz .. bz + 4 (the last one
-// possibly the ghost plane nzl); x and y wrap periodically.
+// possibly the ghost plane nzl); x and y wrap periodically (pencils: local rows, the last
+// one the ghost row).  Rows are kTileRow = 10 doubles apart so each starts 16-B aligned.
+constexpr int kTileRow = 10;
+constexpr int kTileSize = 5 * 9 * kTileRow;
+#ifndef PIC_RD_BULK      // r02 A/B at 512^3: 29.09 ms with the bulk row flush, 28.71 with atomics
+#define PIC_RD_BULK 0
+#endif
+
+__device__ __forceinline__ void bulk_add_f64(double* gdst, const double* ssrc, unsigned bytes) {
+    const unsigned s = (unsigned)__cvta_generic_to_shared(ssrc);
+    asm volatile("cp.reduce.async.bulk.global.shared::cta.bulk_group.add.f64 [%0], [%1], %2;"
+                 ::"l"(gdst), "r"(s), "r"(bytes) : "memory");
+}
+
 __device__ __forceinline__ void fold_flush(const Geom& g, double* tile, const double acc[8], int t,
                                            int bx, int by, int bz, double* __restrict__ rho,
                                            double* ghost) {
     const int lx = (int)compact3((uint32_t)t), ly = (int)compact3((uint32_t)t >> 1),
               lz = (int)compact3((uint32_t)t >> 2);
+    // local destinations (one GPU, pencils, or the slabs' own ghost plane): each tile row's
+    // first 8 nodes (64 B, 16-B aligned in shared and global memory) go out as one bulk
+    // fp64 reduction (UBLKRED: 45 per brick instead of 360 atomics), the 9th as an atomic
+    const bool bulk = PIC_RD_BULK && (g.P == 1 || g.Py > 1 || ghost == rho + (int64_t)g.nzl * g.nyr * g.rp);
 #pragma unroll
     for (int q = 0; q < 8; ++q) {
         const int a = q & 1, b = (q >> 1) & 1, c = q >> 2;
-        tile[((lz + c) * 9 + (ly + b)) * 9 + (lx + a)] += acc[q];
+        tile[((lz + c) * 9 + (ly + b)) * kTileRow + (lx + a)] += acc[q];
+        if (bulk && q == 7) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         __syncthreads();
     }
+    if (bulk) {
+        if (t < 45) {
+            const int ny = t % 9, nz = t / 9;
+            const int iy = yrow(g, by + ny), iz = bz + nz;
+            double* row = (g.Py == 1 && iz == g.nzl) ? ghost + gidx(g, 0, iy, 0) : rho + gidx(g, 0, iy, iz);
+            const double* trow = tile + t * kTileRow;
+            bulk_add_f64(row + bx, trow, 64);
+            asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+            const double v8 = trow[8];
+            if (v8 != 0.0) atomicAdd(row + ((bx + 8) & g.nmask), v8);
+            asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+        }
+        return;
+    }
     for (int q = t; q < 9 * 9 * 5; q += kThreads) {
-        const double val = tile[q];
+        const int nx = q % 9, ny = (q / 9) % 9, nz = q / 81;
+        const double val = tile[(nz * 9 + ny) * kTileRow + nx];
 #ifdef PIC_RD_SKIP_FLUSH     // diagnostics only (no charge): the cost of the global flush
         if (val != 12345.0) continue;
 #endif
         if (val == 0.0) continue;
-        const int nx = q % 9, ny = (q / 9) % 9, nz = q / 81;
         const int ix = (bx + nx) & g.nmask, iy = yrow(g, by + ny), iz = bz + nz;
         if (g.Py > 1) {                     // pencils: the local grid holds the ghost row and
             atomicAdd(rho + gidx(g, ix, iy, iz), val);   // plane; folded into the neighbours after
@@ -667,6 +709,7 @@ __device__ __forceinline__ int chunk_end(const uint32_t* soffs, int ca, int cap)
 #ifndef PIC_RD_MINB
 #define PIC_RD_MINB 3
 #endif
+
 template <bool MR>
 struct ReorderCap {
     static constexpr int value = MR ? PIC_RD_CAP * 13 / 14 : PIC_RD_CAP;   // MR: + the slot -> entry array
@@ -684,8 +727,8 @@ __global__ void __launch_bounds__(kThreads, PIC_RD_MINB) k_reorder_deposit(
     double2* sp0 = reinterpret_cast<double2*>(dyn_smem);               // [CAP] (x, y)
     double2* sp1 = sp0 + CAP;                                            // [CAP] (z, vz)
     double2* sp2 = sp1 + CAP;                                            // [CAP] (vx, vy)
-    double* tile = reinterpret_cast<double*>(sp2 + CAP);                // [9*9*5]
-    uint32_t* sperm = reinterpret_cast<uint32_t*>(tile + 9 * 9 * 5);    // [CAP]
+    double* tile = reinterpret_cast<double*>(sp2 + CAP);                // [kTileSize] (16-B aligned)
+    uint32_t* sperm = reinterpret_cast<uint32_t*>(tile + kTileSize);    // [CAP]
     uint32_t* soffs = sperm + CAP;                                       // [kBrick + 1]
     uint32_t* sE = soffs + kBrick + 1;                                   // [CAP] (MR): entry at slot
     uint8_t* scell = reinterpret_cast<uint8_t*>(sE + (MR ? CAP : 0));   // [CAP]
@@ -695,7 +738,7 @@ __global__ void __launch_bounds__(kThreads, PIC_RD_MINB) k_reorder_deposit(
     unlkey(g, c0, bx, by, bz);
     soffs[t] = offs[c0 + t];
     if (t == 0) soffs[kBrick] = offs[c0 + kBrick];
-    for (int q = t; q < 9 * 9 * 5; q += kThreads) tile[q] = 0.0;
+    for (int q = t; q < kTileSize; q += kThreads) tile[q] = 0.0;
     __syncthreads();
 
     double acc[8];
@@ -853,7 +896,7 @@ inline unsigned blocks(int64_t n, int t) { return (unsigned)((n + t - 1) / t); }
 template <bool MR>
 constexpr size_t reorder_smem() {
     constexpr int CAP = ReorderCap<MR>::value;
-    return sizeof(double2) * 3 * CAP + sizeof(double) * 9 * 9 * 5 +
+    return sizeof(double2) * 3 * CAP + sizeof(double) * kTileSize +
            sizeof(uint32_t) * (CAP + kBrick + 1 + (MR ? CAP : 0)) + CAP;
 }
 
