@@ -113,10 +113,11 @@ void launch_set_u64(unsigned long long* p, unsigned long long v, cudaStream_t s)
 // global Morton keys of the state (export)
 void launch_gkeys(const Geom& g, PState cur, int64_t np, uint32_t* key, cudaStream_t s);
 size_t scan_scratch_bytes(int64_t n);
-void launch_scan(const uint32_t* count, uint32_t* offs, int64_t n, uint32_t* scratch, cudaStream_t s);
+// offs = exclusive scan of count; cursor: also leave offs in count (the place cursors)
+void launch_scan(uint32_t* count, uint32_t* offs, int64_t n, uint32_t* scratch, cudaStream_t s, bool cursor = false);
 // dcnt != null: the entries are dcnt[DC_N] + dcnt[DC_ARR] (<= np, read on the device).
 // Sorted positions >= cap are dropped and flag err_flag[2].
-void launch_place(const uint32_t* key, const uint16_t* rank, int64_t np, const uint32_t* offs,
+void launch_place(const uint32_t* key, const uint16_t* rank, int64_t np, const uint32_t* offs, uint32_t* cursor,
                   uint32_t* perm, const unsigned long long* dcnt, int64_t cap, int* err_flag, cudaStream_t s);
 // Per brick: stable order inside each cell, gather through perm (entries >= n_old
 // from recv; dcnt != null: n_old = dcnt[DC_N]), drift residents (push=1), store

@@ -23,6 +23,21 @@
 
 #include "kernels.h"
 
+// PIC_PLACE_ATOMIC: 1 = the cell count of the push is a fire-and-forget reduction (RED: no
+// returned rank to wait for) and place takes each particle's position from a cursor per
+// cell (the scan leaves offs in `count`, place does atomicAdd on it); 0 (default) = the
+// push's count atomics return the arrival ranks (stored, 2 B per particle; issued in
+// batches so their round trips overlap) and place reads offs[key] + rank.  Both give the
+// same per-cell multiset of positions; the stable order inside a cell is restored by
+// reorder_deposit either way.  r02 at 512^3: 1 moved the atomic latency from push_key
+// (19.9 -> 16.3 ms) into place (7.1 -> 10.3 ms), a net loss.
+#ifndef PIC_PLACE_ATOMIC
+#define PIC_PLACE_ATOMIC 0
+#endif
+#ifndef PIC_ATOM_BATCH      // particles per batch of returned count atomics in push_key
+#define PIC_ATOM_BATCH 1        // r02 A/B at 512^3: 1, 2, 4, 8 -> 19.97, 20.21, 20.19, 19.94 ms
+#endif
+
 namespace pic {
 
 namespace {
@@ -195,9 +210,13 @@ __global__ void __launch_bounds__(kThreads) k_key_import(Geom g, PState cur, int
             store_particle(cur, i, x, v);
         }
         key[i] = k;
-        const uint32_t r = atomicAdd(count + k, 1u);
-        if (r > 0xffffu) atomicExch(err, 1);
-        rank[i] = (uint16_t)r;
+        if (PIC_PLACE_ATOMIC) {
+            atomicAdd(count + k, 1u);
+        } else {
+            const uint32_t r = atomicAdd(count + k, 1u);
+            if (r > 0xffffu) atomicExch(err, 1);
+            rank[i] = (uint16_t)r;
+        }
     }
 }
 
@@ -282,69 +301,91 @@ __global__ void __launch_bounds__(kThreads, MR ? 3 : 4) k_push_key_brick(Geom g,
     __syncthreads();
     double xn[3], vn[3];
     if (P0 + t < P1) load_particle(cur, P0 + t, xn, vn);
-    for (uint32_t i = P0 + t; i < P1; i += kThreads) {
-        double x[3] = {xn[0], xn[1], xn[2]}, v[3] = {vn[0], vn[1], vn[2]};
-        // next particle's loads in flight while this one waits on its count atomic
-        if (i + kThreads < P1) load_particle(cur, i + kThreads, xn, vn);
-        const double x0 = x[0], y0 = x[1], z0 = x[2];
-        int ii[3];
-        double w[3][2];
-        cic_weights(g, x, ii, w);
-        const int lx = ii[0] - bx, ly = ii[1] - g.y0 - by, lz = ii[2] - g.z0 - bz;
-        double e0 = 0.0, e1 = 0.0, e2 = 0.0;
+    // The count atomics return each particle's arrival rank; with PIC_ATOM_BATCH > 1 they are
+    // issued in batches after the batch's pushes so their round trips overlap.  Measured
+    // without gain: the cost of the returned rank is the L2 atomic itself (a fire-and-forget
+    // RED count made push_key 3.6 ms faster, see PIC_PLACE_ATOMIC), not its exposed latency.
+    constexpr int kAtomBatch = PIC_PLACE_ATOMIC ? 1 : PIC_ATOM_BATCH;
+    for (uint32_t i0 = P0 + t; i0 < P1; i0 += kAtomBatch * kThreads) {
+        uint32_t kq[kAtomBatch];
 #pragma unroll
-        for (int c = 0; c < 2; ++c)
+        for (int u = 0; u < kAtomBatch; ++u) {
+            const uint32_t i = i0 + u * kThreads;
+            kq[u] = kNoKey;
+            if (i >= P1) continue;
+            double x[3] = {xn[0], xn[1], xn[2]}, v[3] = {vn[0], vn[1], vn[2]};
+            // next particle's loads in flight while this one is pushed
+            if (i + kThreads < P1) load_particle(cur, i + kThreads, xn, vn);
+            const double x0 = x[0], y0 = x[1], z0 = x[2];
+            int ii[3];
+            double w[3][2];
+            cic_weights(g, x, ii, w);
+            const int lx = ii[0] - bx, ly = ii[1] - g.y0 - by, lz = ii[2] - g.z0 - bz;
+            double e0 = 0.0, e1 = 0.0, e2 = 0.0;
 #pragma unroll
-            for (int b = 0; b < 2; ++b) {
-                const double2* pe = ptile[((lz + c) * 9 + (ly + b)) * 8 + lx];
-                const double2 px = pe[0], py = pe[1], pz = pe[2];
-                const double wt0 = __dmul_rn(__dmul_rn(w[0][0], w[1][b]), w[2][c]);
-                const double wt1 = __dmul_rn(__dmul_rn(w[0][1], w[1][b]), w[2][c]);
-                e0 = __fma_rn(wt0, px.x, e0);          // corner order z, y, x (x inner): a = 0 ...
-                e1 = __fma_rn(wt0, py.x, e1);
-                e2 = __fma_rn(wt0, pz.x, e2);
-                e0 = __fma_rn(wt1, px.y, e0);          // ... then a = 1, as the oracle (D#17)
-                e1 = __fma_rn(wt1, py.y, e1);
-                e2 = __fma_rn(wt1, pz.y, e2);
-            }
-        double ep[3] = {e0, e1, e2};
-        kick(g, ep, v);
-        drift(g, x, v);
-        st_zv(cur.zv + 2 * i, make_double2(z0, v[2]), make_double2(v[0], v[1]));   // kicked v in place
-        int iz, iy;
-        const uint32_t k = key_of(g, x, &iz, &iy);
-        if (MR && !in_domain(g, iy, iz)) {   // leaver: staged, sent below
-            const int dr = owner_of(g, iy, iz);
-            const double xo[3] = {x0, y0, z0};
-            const uint32_t oldg = gkey_of(g, xo);           // its tie key (D#15)
-            const double2 p0 = make_double2(x[0], x[1]), p1 = make_double2(x[2], v[2]),
-                          p2 = make_double2(v[0], v[1]),
-                          p3 = make_double2(__longlong_as_double((long long)((uint64_t)oldg | ((uint64_t)i << 32))), 0.0);
-            const uint32_t s = atomicAdd(&nleave, 1u);
-            if (s < (uint32_t)kLeaveCap) {
-                lbuf[s][0] = p0; lbuf[s][1] = p1; lbuf[s][2] = p2; lbuf[s][3] = p3;
-                ldst[s] = (uint8_t)dr;
-                atomicAdd(&lcount[dr], 1u);
-            } else {      // staging full: straight to the global buffer, one reserve per warp and destination
-                const unsigned grp = __match_any_sync(__activemask(), dr);
-                const int lead = __ffs(grp) - 1, lane = threadIdx.x & 31;
-                uint32_t base = 0;
-                if (lane == lead) base = leave_reserve(sb, dr, (uint32_t)__popc(grp));
-                base = __shfl_sync(grp, base, lead) + (uint32_t)__popc(grp & ((1u << lane) - 1u));
-                double2* d = leave_rec(sb, dr, base);
-                if (d) {
-                    d[0] = p0; d[1] = p1; d[2] = p2; d[3] = p3;
-                } else {
-                    atomicExch(err + 2, 1);
+            for (int c = 0; c < 2; ++c)
+#pragma unroll
+                for (int b = 0; b < 2; ++b) {
+                    const double2* pe = ptile[((lz + c) * 9 + (ly + b)) * 8 + lx];
+                    const double2 px = pe[0], py = pe[1], pz = pe[2];
+                    const double wt0 = __dmul_rn(__dmul_rn(w[0][0], w[1][b]), w[2][c]);
+                    const double wt1 = __dmul_rn(__dmul_rn(w[0][1], w[1][b]), w[2][c]);
+                    e0 = __fma_rn(wt0, px.x, e0);          // corner order z, y, x (x inner): a = 0 ...
+                    e1 = __fma_rn(wt0, py.x, e1);
+                    e2 = __fma_rn(wt0, pz.x, e2);
+                    e0 = __fma_rn(wt1, px.y, e0);          // ... then a = 1, as the oracle (D#17)
+                    e1 = __fma_rn(wt1, py.y, e1);
+                    e2 = __fma_rn(wt1, pz.y, e2);
                 }
+            double ep[3] = {e0, e1, e2};
+            kick(g, ep, v);
+            drift(g, x, v);
+            st_zv(cur.zv + 2 * i, make_double2(z0, v[2]), make_double2(v[0], v[1]));   // kicked v in place
+            int iz, iy;
+            const uint32_t k = key_of(g, x, &iz, &iy);
+            if (MR && !in_domain(g, iy, iz)) {   // leaver: staged, sent below
+                const int dr = owner_of(g, iy, iz);
+                const double xo[3] = {x0, y0, z0};
+                const uint32_t oldg = gkey_of(g, xo);           // its tie key (D#15)
+                const double2 p0 = make_double2(x[0], x[1]), p1 = make_double2(x[2], v[2]),
+                              p2 = make_double2(v[0], v[1]),
+                              p3 = make_double2(__longlong_as_double((long long)((uint64_t)oldg | ((uint64_t)i << 32))), 0.0);
+                const uint32_t s = atomicAdd(&nleave, 1u);
+                if (s < (uint32_t)kLeaveCap) {
+                    lbuf[s][0] = p0; lbuf[s][1] = p1; lbuf[s][2] = p2; lbuf[s][3] = p3;
+                    ldst[s] = (uint8_t)dr;
+                    atomicAdd(&lcount[dr], 1u);
+                } else {      // staging full: straight to the global buffer, one reserve per warp and destination
+                    const unsigned grp = __match_any_sync(__activemask(), dr);
+                    const int lead = __ffs(grp) - 1, lane = threadIdx.x & 31;
+                    uint32_t base = 0;
+                    if (lane == lead) base = leave_reserve(sb, dr, (uint32_t)__popc(grp));
+                    base = __shfl_sync(grp, base, lead) + (uint32_t)__popc(grp & ((1u << lane) - 1u));
+                    double2* d = leave_rec(sb, dr, base);
+                    if (d) {
+                        d[0] = p0; d[1] = p1; d[2] = p2; d[3] = p3;
+                    } else {
+                        atomicExch(err + 2, 1);
+                    }
+                }
+                key[i] = kNoKey;
+                continue;
             }
-            key[i] = kNoKey;
-            continue;
+            key[i] = k;
+            if (PIC_PLACE_ATOMIC) atomicAdd(count + k, 1u);          // RED: nothing to wait for
+            else kq[u] = k;
         }
-        key[i] = k;
-        const uint32_t r = atomicAdd(count + k, 1u);
-        if (r > 0xffffu) atomicExch(err, 1);
-        rank[i] = (uint16_t)r;
+        if (!PIC_PLACE_ATOMIC) {
+            uint32_t rq[kAtomBatch];
+#pragma unroll
+            for (int u = 0; u < kAtomBatch; ++u) rq[u] = kq[u] != kNoKey ? atomicAdd(count + kq[u], 1u) : 0u;
+#pragma unroll
+            for (int u = 0; u < kAtomBatch; ++u)
+                if (kq[u] != kNoKey) {
+                    if (rq[u] > 0xffffu) atomicExch(err, 1);
+                    rank[i0 + u * kThreads] = (uint16_t)rq[u];
+                }
+        }
     }
     if (MR) {      // one global atomic per destination, then the staged payloads
         __syncthreads();
@@ -388,9 +429,13 @@ __global__ void __launch_bounds__(kThreads) k_key_arrivals(Geom g, const double2
         uint32_t k = key_of(g, x, &iz, &iy);
         if (!in_domain(g, iy, iz)) { atomicExch(err + 1, 1); k = 0; }
         key[n_old + a] = k;
-        const uint32_t r = atomicAdd(count + k, 1u);
-        if (r > 0xffffu) atomicExch(err, 1);
-        rank[n_old + a] = (uint16_t)r;
+        if (PIC_PLACE_ATOMIC) {
+            atomicAdd(count + k, 1u);
+        } else {
+            const uint32_t r = atomicAdd(count + k, 1u);
+            if (r > 0xffffu) atomicExch(err, 1);
+            rank[n_old + a] = (uint16_t)r;
+        }
     }
 }
 
@@ -517,9 +562,9 @@ __global__ void __launch_bounds__(1024) k_scan_bsum(uint32_t* __restrict__ bsum,
     }
 }
 
-__global__ void __launch_bounds__(kThreads) k_scan_apply(const uint32_t* __restrict__ count,
+__global__ void __launch_bounds__(kThreads) k_scan_apply(uint32_t* __restrict__ count,
                                                          uint32_t* __restrict__ offs, int64_t ncell,
-                                                         const uint32_t* __restrict__ bsum) {
+                                                         const uint32_t* __restrict__ bsum, int cursor) {
     __shared__ uint32_t ws[kThreads / 32];
     const int64_t base = (int64_t)blockIdx.x * kScanTile + (int64_t)threadIdx.x * 16;
     uint32_t v[16];
@@ -558,11 +603,19 @@ __global__ void __launch_bounds__(kThreads) k_scan_apply(const uint32_t* __restr
     }
     if (full) {
         uint4* po = reinterpret_cast<uint4*>(offs + base);
+        uint4* pc = reinterpret_cast<uint4*>(count + base);
 #pragma unroll
-        for (int q = 0; q < 4; ++q) po[q] = make_uint4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+        for (int q = 0; q < 4; ++q) {
+            const uint4 o = make_uint4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+            po[q] = o;
+            if (cursor) pc[q] = o;          // the counts become the place cursors (offs)
+        }
     } else {
         for (int q = 0; q < 16; ++q)
-            if (base + q < ncell) offs[base + q] = v[q];
+            if (base + q < ncell) {
+                offs[base + q] = v[q];
+                if (cursor) count[base + q] = v[q];
+            }
     }
     if (ncell > base && ncell <= base + 16) offs[ncell] = run;   // owner of the last cell: total
 }
@@ -572,7 +625,7 @@ __global__ void __launch_bounds__(kThreads) k_scan_apply(const uint32_t* __restr
 // leavers (key = kNoKey) are skipped.
 __global__ void __launch_bounds__(kThreads) k_place(const uint32_t* __restrict__ key,
                                                     const uint16_t* __restrict__ rank, int64_t np,
-                                                    const uint32_t* __restrict__ offs,
+                                                    uint32_t* __restrict__ offs,
                                                     uint32_t* __restrict__ perm,
                                                     const unsigned long long* __restrict__ dcnt,
                                                     int64_t cap, int* __restrict__ err) {
@@ -589,11 +642,12 @@ __global__ void __launch_bounds__(kThreads) k_place(const uint32_t* __restrict__
     for (int q = 0; q < 4; ++q) {
         const int64_t i = base + q * kThreads;
         k[q] = i < np ? __ldg(key + i) : kNoKey;
-        r[q] = i < np ? __ldg(rank + i) : 0u;
+        r[q] = (i < np && !PIC_PLACE_ATOMIC) ? __ldg(rank + i) : 0u;
     }
     uint32_t pos[4];
 #pragma unroll
-    for (int q = 0; q < 4; ++q) pos[q] = k[q] == kNoKey ? 0u : __ldg(offs + k[q]) + r[q];
+    for (int q = 0; q < 4; ++q)
+        pos[q] = k[q] == kNoKey ? 0u : (PIC_PLACE_ATOMIC ? atomicAdd(offs + k[q], 1u) : __ldg(offs + k[q]) + r[q]);
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
         if (k[q] == kNoKey) continue;
@@ -1004,17 +1058,19 @@ size_t scan_scratch_bytes(int64_t n) {
     return sizeof(uint32_t) * (size_t)(blocks(n, kScanTile) + 1);
 }
 
-void launch_scan(const uint32_t* count, uint32_t* offs, int64_t n, uint32_t* scratch, cudaStream_t s) {
+void launch_scan(uint32_t* count, uint32_t* offs, int64_t n, uint32_t* scratch, cudaStream_t s, bool cursor) {
     const unsigned nb = blocks(n, kScanTile);
     k_scan_reduce<<<nb, kThreads, 0, s>>>(count, n, scratch);
     k_scan_bsum<<<1, 1024, 0, s>>>(scratch, (int)nb);
-    k_scan_apply<<<nb, kThreads, 0, s>>>(count, offs, n, scratch);
+    k_scan_apply<<<nb, kThreads, 0, s>>>(count, offs, n, scratch, cursor && PIC_PLACE_ATOMIC);
 }
 
-void launch_place(const uint32_t* key, const uint16_t* rank, int64_t np, const uint32_t* offs,
+void launch_place(const uint32_t* key, const uint16_t* rank, int64_t np, const uint32_t* offs, uint32_t* cursor,
                   uint32_t* perm, const unsigned long long* dcnt, int64_t cap, int* err_flag, cudaStream_t s) {
     if (np == 0) return;
-    k_place<<<blocks((np + 3) / 4, kThreads), kThreads, 0, s>>>(key, rank, np, offs, perm, dcnt, cap, err_flag);
+    k_place<<<blocks((np + 3) / 4, kThreads), kThreads, 0, s>>>(key, rank, np,
+                                                                 PIC_PLACE_ATOMIC ? cursor : const_cast<uint32_t*>(offs),
+                                                                 perm, dcnt, cap, err_flag);
 }
 
 void launch_reorder_deposit(const Geom& g, const uint32_t* offs, const uint32_t* perm, PState cur,
