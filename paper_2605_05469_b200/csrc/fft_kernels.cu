@@ -247,6 +247,9 @@ __host__ __device__ constexpr int z_tw(int n) { int t = 2048 / n; return t > 8 ?
 #ifndef PIC_XINV_DIRECT
 #define PIC_XINV_DIRECT 0
 #endif
+#ifndef PIC_ZMUL_FUSED
+#define PIC_ZMUL_FUSED 0
+#endif
 __host__ __device__ constexpr int zmul_tw(int n) { int t = PIC_ZMUL_TWN / n; return t > 8 ? 8 : (t < 1 ? 1 : t); }
 
 // Every pass is a persistent loop over tiles (grid = resident CTAs): the input of
@@ -469,6 +472,34 @@ __global__ void __launch_bounds__(kThreads, PIC_ZMUL_MINB) k_fft_z_mul(Geom g, c
             r = make_double2(f * r.x, f * r.y);
         }
         __syncthreads();
+#if PIC_ZMUL_FUSED   // both inverse transforms in one fft_lines call: 2 TW lines, two items per thread
+        {
+            constexpr int ls2 = col_stride(n, 2 * TW);
+            auto src = [&](int l, int kz) {
+                const int d = l >= TW, lc = l - d * TW;
+                double2 e = make_double2(0.0, 0.0);
+                if (lc < ncol) {
+                    const double2 r = s1[lc * ls + pidx(kz)];
+                    if (d == 0) {
+                        e = r;                                       // phi^
+                    } else if (kz != half) {
+                        const double kd = kf * (double)(kz < half ? kz : kz - n);
+                        e = make_double2(kd * r.y, -kd * r.x);       // E^_z = -i k_z phi^
+                    }
+                }
+                return e;
+            };
+            auto dst = [&](int l, int z, double2 v) {
+                const int d = l >= TW, lc = l - d * TW;
+                if (lc < ncol) {
+                    const int q = z >> g.mz, zl = z - (q << g.mz);
+                    xpose_row(g, out, q, d, zl, yl)[kx0 + lc] = v;
+                }
+            };
+            fft_lines<+1, false, LOGN, 2, false>(s2, 2 * TW, ls2, tw, 0, src, dst);
+            __syncthreads();
+        }
+#else
         for (int d = 0; d < 2; ++d) {
             auto src = [&](int l, int kz) {
                 double2 e = make_double2(0.0, 0.0);
@@ -491,6 +522,7 @@ __global__ void __launch_bounds__(kThreads, PIC_ZMUL_MINB) k_fft_z_mul(Geom g, c
             };
             fft_lines<+1, false, LOGN, 1, false>(s2, TW, ls, tw, 0, src, dst);
         }
+#endif
     }
     if (out.packed == 2) __threadfence_system();
 }
@@ -605,6 +637,37 @@ __global__ void k_e4_pack(Geom g, const double* __restrict__ a, const double* __
                           const double* __restrict__ c, int64_t nn, double* __restrict__ E4) {
     const int64_t m = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (m < nn) st_node(E4 + 4 * e4_node(g, m), a[m], b[m], c[m]);
+}
+
+// Pencils (pic_api.cu slab_to_pencil_E): the slab field's node records -> the y-group send
+// blocks [q][nzs + 1][nyl + 1][n][3] (rows q nyl .. q nyl + nyl, the last one wrapping; 24 B per
+// node instead of the 32-B record), and the received blocks -> the pencil's node records.
+__global__ void k_e4_pencil_pack(const double* __restrict__ E4s, int n, int nzs, int nyl, int Py,
+                                 double* __restrict__ send) {
+    const int64_t per = (int64_t)(nzs + 1) * (nyl + 1) * n, tot = per * Py;
+    for (int64_t m = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; m < tot; m += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t q = m / per, rem = m - q * per;
+        const int x = (int)(rem % n);
+        const int64_t pr = rem / n;
+        const int r = (int)(pr % (nyl + 1)), p = (int)(pr / (nyl + 1));
+        const int y = (int)((q * nyl + r) & (n - 1));
+        double ex, ey, ez;
+        ldg_node(E4s + 4 * (((int64_t)p * n + y) * n + x), ex, ey, ez);
+        double* d = send + 3 * m;
+        d[0] = ex;
+        d[1] = ey;
+        d[2] = ez;
+    }
+}
+
+__global__ void k_e4_pencil_unpack(const double* __restrict__ recv, int n, int nzs, int nyl, int Py,
+                                   double* __restrict__ E4) {
+    const int64_t per = (int64_t)(nzs + 1) * (nyl + 1) * n, tot = per * Py;
+    for (int64_t m = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; m < tot; m += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t q = m / per, rem = m - q * per;            // from rank q: pencil planes q nzs ..
+        const double* s = recv + 3 * m;
+        st_node(E4 + 4 * ((int64_t)q * nzs * (nyl + 1) * n + rem), s[0], s[1], s[2]);
+    }
 }
 
 // One CTA, fixed summation order (deterministic): energies = (W_x, W).
@@ -782,7 +845,9 @@ void launch_fft_y_field(const Geom& g, SpecLayout src, SpecLayout dst, const dou
 void launch_fft_z_mul(const Geom& g, const double2* pencil, SpecLayout out, double scale,
                       const double2* tw, cudaStream_t s) {
     const int TW = zmul_tw(g.n), ntiles = (g.n / 2 + 1 + TW - 1) / TW;
-    const size_t smem = sizeof(double2) * (size_t)TW * ((PIC_ZMUL_DIRECT ? 0 : g.n) + 2 * col_stride(g.n, TW));
+    const size_t smem = sizeof(double2) * ((size_t)TW * ((PIC_ZMUL_DIRECT ? 0 : g.n) + col_stride(g.n, TW)) +
+                                            (PIC_ZMUL_FUSED ? 2 * (size_t)TW * col_stride(g.n, 2 * TW)
+                                                            : (size_t)TW * col_stride(g.n, TW)));
     const int64_t nt = (int64_t)(g.n / g.P) * ntiles;
     // one tile per CTA: the pass is bound by its four transforms, not its input
     // loads, and measured faster without the persistent loop
@@ -835,6 +900,14 @@ void launch_e4_extract(const Geom& g, const double* E4, int d, double* out, cuda
 void launch_e4_pack(const Geom& g, const double* const comp[3], double* E4, cudaStream_t s) {
     const int64_t nn = (int64_t)g.n * g.nyl * g.nzl;
     k_e4_pack<<<(unsigned)((nn + 255) / 256), 256, 0, s>>>(g, comp[0], comp[1], comp[2], nn, E4);
+}
+
+void launch_e4_pencil_pack(const double* E4s, int n, int nzs, int nyl, int Py, double* send, cudaStream_t s) {
+    k_e4_pencil_pack<<<148 * 8, 256, 0, s>>>(E4s, n, nzs, nyl, Py, send);
+}
+
+void launch_e4_pencil_unpack(const double* recv, int n, int nzs, int nyl, int Py, double* E4, cudaStream_t s) {
+    k_e4_pencil_unpack<<<148 * 8, 256, 0, s>>>(recv, n, nzs, nyl, Py, E4);
 }
 
 void launch_energy_reduce(const Geom& g, const double* partials, double* energies, cudaStream_t s) {

@@ -42,6 +42,10 @@ void launch_fft_z_mul(const Geom& g, const double2* pencil, SpecLayout out, doub
 void launch_fft_x_inv(const Geom& g, const double2* spec, double* E4, double* halo, const double2* tw,
                       double* partials, cudaStream_t s);
 void launch_energy_reduce(const Geom& g, const double* partials, double* energies, cudaStream_t s);
+// Pencils: slab field E4s [nzs + 1][n][n][4] -> y-group send blocks [Py][nzs + 1][nyl + 1][n][3] (rows
+// q nyl .. q nyl + nyl, periodic), and received blocks -> the pencil field [nzl + 1][nyl + 1][n][4].
+void launch_e4_pencil_pack(const double* E4s, int n, int nzs, int nyl, int Py, double* send, cudaStream_t s);
+void launch_e4_pencil_unpack(const double* recv, int n, int nzs, int nyl, int Py, double* E4, cudaStream_t s);
 // In-place unnormalised 3D C2C FFT of an M^3 complex grid [z][y][x], M = 2^k in [16, 1024],
 // sign -1 (e^{-i k.x}) or +1; tw = W_M^m, m < M (the PIF fine grid, pif.cu).  keep > 0: the
 // y / z passes only touch lines meeting the box [0, keep) u [M - keep, M) in x (and in the

@@ -628,21 +628,12 @@ pic_status pencil_to_slab_rho(pic_ctx* c) {
 pic_status slab_to_pencil_E(pic_ctx* c) {
     const Geom& g = c->g;
     const int nzs = c->gs.nzl, Py = g.Py;
-    const size_t row8 = sizeof(double) * 4 * g.n, plane8 = row8 * g.n;     // slab E4 row / plane bytes
-    const size_t blk = (size_t)(nzs + 1) * (g.nyl + 1) * 4 * g.n;          // doubles per destination
-    for (int q = 0; q < Py; ++q) {
-        double* dst = c->xe[0] + q * blk;
-        PIC_CUDA(c, cudaMemcpy2DAsync(dst, (g.nyl + 1) * row8, c->E4_s + (size_t)q * g.nyl * 4 * g.n, plane8,
-                                      g.nyl * row8, nzs + 1, cudaMemcpyDeviceToDevice, c->stream));
-        const int yh = ((q + 1) * g.nyl) & g.nmask;                        // the halo row (periodic)
-        PIC_CUDA(c, cudaMemcpy2DAsync(dst + (size_t)g.nyl * 4 * g.n, (g.nyl + 1) * row8,
-                                      c->E4_s + (size_t)yh * 4 * g.n, plane8, row8, nzs + 1,
-                                      cudaMemcpyDeviceToDevice, c->stream));
-    }
+    const size_t blk = (size_t)(nzs + 1) * (g.nyl + 1) * 3 * g.n;          // doubles per destination (24 B/node)
+    pic::launch_e4_pencil_pack(c->E4_s, g.n, nzs, g.nyl, Py, c->xe[0], c->stream);
+    PIC_LAUNCHED(c, "e4_pencil_pack");
     PIC_NCCL(c, ncclAlltoAll(c->xe[0], c->xe[1], blk, ncclDouble, c->ycomm, c->stream));
-    for (int q = 0; q < Py; ++q)       // planes [q nzs, q nzs + nzs] of the pencil, rows 0 .. nyl
-        PIC_CUDA(c, cudaMemcpyAsync(c->E4 + (size_t)q * nzs * g.nyr * 4 * g.n, c->xe[1] + q * blk,
-                                    sizeof(double) * blk, cudaMemcpyDeviceToDevice, c->stream));
+    pic::launch_e4_pencil_unpack(c->xe[1], g.n, nzs, g.nyl, Py, c->E4, c->stream);
+    PIC_LAUNCHED(c, "e4_pencil_unpack");
     return PIC_OK;
 }
 
@@ -1858,7 +1849,9 @@ pic_status pic_launches_per_step(pic_ctx* c, int64_t* launches) {
     if (!c || !launches) return PIC_EINVAL;
     // solve 6, push_key 1, scan 3, place 1, reorder_deposit 1; P > 1: arrivals 1, and
     // the NCCL transport's ghost fold 1 or the peer transport's count update 1
-    *launches = 12 + (c->g.P > 1 ? 2 : 0) + (c->g.P > 1 && c->p2p && pic::leavers_batched() ? 2 : 0);
+    // pencils: + the ghost row fold and the field's pack / unpack around the y-group all-to-all
+    *launches = 12 + (c->g.P > 1 ? 2 : 0) + (c->g.P > 1 && c->p2p && pic::leavers_batched() ? 2 : 0) +
+                (c->pencil ? 3 : 0);
     if (c->p.solver != PIC_SOLVER_FFT) *launches += c->pcg_launches - 6;   // the latest CG solve's count
     return PIC_OK;
 }
