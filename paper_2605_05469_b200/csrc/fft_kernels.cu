@@ -250,6 +250,9 @@ __host__ __device__ constexpr int z_tw(int n) { int t = 2048 / n; return t > 8 ?
 #ifndef PIC_ZMUL_FUSED
 #define PIC_ZMUL_FUSED 0
 #endif
+#ifndef PIC_FFTY_MINB       // resident CTAs per SM the y passes are compiled for
+#define PIC_FFTY_MINB 2
+#endif
 __host__ __device__ constexpr int zmul_tw(int n) { int t = PIC_ZMUL_TWN / n; return t > 8 ? 8 : (t < 1 ? 1 : t); }
 
 // Every pass is a persistent loop over tiles (grid = resident CTAs): the input of
@@ -336,7 +339,7 @@ __device__ __forceinline__ double2* dst_row(const Geom& g, const SpecLayout& L, 
 // E_y = -i k_y phi (applied to the input, zero on the k_y Nyquist row; D#6), an
 // E_z tile one.
 template <int SIGN, int LOGN, bool EMODE>
-__global__ void __launch_bounds__(kThreads, 2) k_fft_y(Geom g, SpecLayout sl, SpecLayout dl, int ncomp,
+__global__ void __launch_bounds__(kThreads, PIC_FFTY_MINB) k_fft_y(Geom g, SpecLayout sl, SpecLayout dl, int ncomp,
                                                        const double2* __restrict__ tw) {
     extern __shared__ double2 smx[];
     constexpr int n = 1 << LOGN, TW = y_tw(n);
