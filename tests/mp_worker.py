@@ -92,6 +92,28 @@ def main():
         assert dx <= 1e-12 and dv <= 1e-12, (dx, dv)
         assert total_mig > 0, "no particle migrated"
         msg1 = f"import: W_x rel {rel:.1e} dx/L {dx:.1e} dv {dv:.1e} migrated {total_mig} key flips {flips}"
+    else:
+        msg1 = ""
+
+    # ---- case 1b (FFT solver): an injected charge grid, each rank its own block -> E blocks
+    # vs the oracle's single-domain solve (1e-12 of max |E|): the pencil <-> slab
+    # redistributions and the slab transposes element by element
+    if solver == "fft":
+        from pic_inputs import random_grid
+
+        rho = random_grid(n, seed=17, mean=-1.0)
+        y0, ny, z0, nz = sim.y0, sim.ny, sim.z0, sim.nz
+        Eb, _, _ = sim.solve_injected(np.ascontiguousarray(rho[z0:z0 + nz, y0:y0 + ny, :]))
+        blocks = [None] * world
+        dist.all_gather_object(blocks, (y0, ny, z0, nz, Eb))
+        if rank == 0:
+            Eg = np.zeros((3, n, n, n))
+            for (by0, bny, bz0, bnz, e) in blocks:
+                Eg[:, bz0:bz0 + bnz, by0:by0 + bny, :] = e
+            Eref, _ = O.solve_fft(n, L, rho)
+            err = np.abs(Eg - Eref).max() / np.abs(Eref).max()
+            assert err <= 1e-12, f"injected solve rel err {err}"
+            msg1 += f" | injected solve rel err {err:.1e}"
     sim.close()
 
     # ---- case 2: the library's own sampler on P ranks
