@@ -87,6 +87,17 @@ enum {
     PIC_PIF_BIN,        /* binned path: counting sort of the particles into bins       */
     PIC_PIF_NSTAGES
 };
+/* Decomposed PIF over nranks processes (one GPU each; collective: every rank calls it once
+ * after pic_pif_create, with the NCCL id rank 0 made by pic_nccl_unique_id): each rank holds
+ * its own particles; from then on pic_nufft_type1 and the PIF solve (pic_pif_solve,
+ * pic_pif_step) sum the selected modes over the ranks (ncclAllReduce of N^3 complex) before
+ * the Poisson step, so every rank has the field of all the particles, the energies are
+ * global, and each rank's type-2 gather serves its own particles (the paper's PIF
+ * parallelisation: the particle sums are distributed, the modes reduced).
+ * Every rank calls every later function of the plan collectively.  nranks == 1: no-op.
+ * PIC_EINVAL: bad rank / nranks, NULL id, or already attached.  PIC_ENCCL: init failed. */
+pic_status pic_pif_attach_nccl(pic_pif *p, int32_t rank, int32_t nranks, const uint8_t nccl_id[128]);
+
 pic_status pic_pif_set_timing(pic_pif *p, int32_t enable);
 pic_status pic_pif_get_timings(pic_pif *p, double *ms, int64_t *launches);
 

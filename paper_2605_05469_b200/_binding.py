@@ -104,6 +104,7 @@ SYMBOLS = {
     "pic_nufft_type2": (C.c_int, [_vp, C.c_int64, _vp, _vp, _vp]),
     "pic_pif_solve": (C.c_int, [_vp, C.c_int64, _vp, _vp, _vp, _dp]),
     "pic_pif_step": (C.c_int, [_vp, C.c_int64, _vp, _vp, _vp, _vp, C.c_double, C.c_double, C.c_int32, _dp]),
+    "pic_pif_attach_nccl": (C.c_int, [_vp, C.c_int32, C.c_int32, C.c_void_p]),
     "pic_pif_set_timing": (C.c_int, [_vp, C.c_int32]),
     "pic_pif_get_timings": (C.c_int, [_vp, _dp, _i64p]),
     "pic_pif_window": (C.c_int, [_vp, C.POINTER(C.c_int32), C.POINTER(C.c_int32)]),
@@ -379,8 +380,11 @@ class PifSolver:
     indexed [nz + N/2, ny + N/2, nx + N/2].  The workspace is a torch uint8 tensor owned
     here; the stream is torch's current stream at construction."""
 
-    def __init__(self, n: int, length: float, eps: float = 1e-4, device=None, np_max: int = 0):
-        """np_max > 0 reserves the binned (shared-memory tile) path for up to np_max particles."""
+    def __init__(self, n: int, length: float, eps: float = 1e-4, device=None, np_max: int = 0, rank: int = 0,
+                 nranks: int = 1, nccl_id: bytes | None = None):
+        """np_max > 0 reserves the binned (shared-memory tile) path for up to np_max particles.
+        nranks > 1: the decomposed PIF (pic_pif_attach_nccl): each rank passes its own particles,
+        the modes are summed over the ranks."""
         import torch
 
         self.n, self.L, self.eps, self.np_max = n, float(length), float(eps), int(np_max)
@@ -395,6 +399,9 @@ class PifSolver:
                                         b.value,
                                         C.c_void_p(self.stream.cuda_stream), C.byref(plan)))
         self.plan = plan
+        if nranks > 1:
+            idbuf = (C.c_uint8 * 128).from_buffer_copy(nccl_id)
+            _check_pif(lib().pic_pif_attach_nccl(self.plan, rank, nranks, idbuf), self.plan)
 
     def __del__(self):
         if getattr(self, "plan", None):

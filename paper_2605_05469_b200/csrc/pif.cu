@@ -13,6 +13,7 @@
 // Hermitian spectrum, hence real) and E^_z into a second.
 #include <cuda_runtime.h>
 #include <cub/device/device_scan.cuh>
+#include <nccl.h>
 
 #include <algorithm>
 #include <cmath>
@@ -207,6 +208,43 @@ __global__ void __launch_bounds__(kThreads) k_pif_modes(int N, int M, double kun
             const double d = dinv[m.nz] * dinv[m.ny] * dinv[m.nx];
             const double2 v = B[m.fine];
             const double pr = v.x * d / k2, pi = v.y * d / k2;
+            ex = make_double2(kx * pi, -kx * pr);      // -i k phi
+            ey = make_double2(ky * pi, -ky * pr);
+            ez = make_double2(kz * pi, -kz * pr);
+            e[0] += ex.x * ex.x + ex.y * ex.y;
+            e[1] += ey.x * ey.x + ey.y * ey.y;
+            e[2] += ez.x * ez.x + ez.y * ez.y;
+        }
+        A[t] = make_double2(ex.x - ey.y, ex.y + ey.x);
+        Bz[t] = ez;
+    }
+    __shared__ double red[3][kThreads];
+    for (int d = 0; d < 3; ++d) red[d][threadIdx.x] = e[d];
+    __syncthreads();
+    for (int s = kThreads / 2; s > 0; s >>= 1) {
+        if (threadIdx.x < s)
+            for (int d = 0; d < 3; ++d) red[d][threadIdx.x] += red[d][threadIdx.x + s];
+        __syncthreads();
+    }
+    if (threadIdx.x < 3) partials[blockIdx.x * 3 + threadIdx.x] = red[threadIdx.x][0];
+}
+
+// Decomposed PIF (P > 1): the same Poisson step and gradient as k_pif_modes, from the selected
+// and deconvolved modes rho^ (k_select, then summed over the ranks), in place: A = rho^ on
+// input, E^_x + i E^_y on output; Bz = E^_z; block partials of |E^_d|^2 (fixed order).
+__global__ void __launch_bounds__(kThreads) k_pif_field(int N, double kunit, double2* __restrict__ A,
+                                                        double2* __restrict__ Bz, double* __restrict__ partials) {
+    const int64_t nm = (int64_t)N * N * N;
+    double e[3] = {0.0, 0.0, 0.0};
+    for (int64_t t = (int64_t)blockIdx.x * kThreads + threadIdx.x; t < nm; t += (int64_t)gridDim.x * kThreads) {
+        const int h = N / 2;
+        const int nx = (int)(t % N), ny = (int)((t / N) % N), nz = (int)(t / ((int64_t)N * N));
+        double2 ex = make_double2(0.0, 0.0), ey = ex, ez = ex;
+        const double kx = kunit * (nx - h), ky = kunit * (ny - h), kz = kunit * (nz - h);
+        const double k2 = kx * kx + ky * ky + kz * kz;
+        if (nx > 0 && ny > 0 && nz > 0 && k2 != 0.0) {
+            const double2 v = A[t];
+            const double pr = v.x / k2, pi = v.y / k2;
             ex = make_double2(kx * pi, -kx * pr);      // -i k phi
             ey = make_double2(ky * pi, -ky * pr);
             ez = make_double2(kz * pi, -kz * pr);
@@ -559,6 +597,8 @@ struct pic_pif {
     double L, eps, beta, inv_hf;
     cudaStream_t stream;
     double2* tw;         // M twiddles W_M^m = exp(-2 pi i m / M) of the fine-grid FFT
+    ncclComm_t comm;     // decomposed PIF (pic_pif_attach_nccl): the modes are summed over the ranks
+    int nranks;
     double2* G;          // fine grid M^3
     double2* G2;         // second fine grid (binned PIF solve: E_z), or null
     double2* A;          // N^3 spectrum (E^_x + i E^_y)
@@ -924,6 +964,12 @@ pic_status pic_nufft_type1(pic_pif* p, int64_t np, const double* x, const double
         const int64_t nm = (int64_t)p->n * p->n * p->n;
         k_select<<<stream_grid(nm), kThreads, 0, p->stream>>>(p->n, p->M, p->G, p->dinv, (double2*)fhat);
         PIF_LAUNCHED(p);
+        if (p->comm &&
+            ncclAllReduce(fhat, fhat, 2 * (size_t)nm, ncclDouble, ncclSum, p->comm, p->stream) != ncclSuccess) {
+            snprintf(p->err, sizeof(p->err), "ncclAllReduce of the type-1 sums failed");
+            p->poisoned = true;
+            return PIC_ENCCL;
+        }
     }
     return flush_timing(p);
 }
@@ -949,8 +995,20 @@ pic_status solve_core(pic_pif* p, int64_t np, const double* x, const double* q, 
     {
         Stage t(p, PIC_PIF_MODES);                                          // chi, D, Poisson
         const double kunit = 2.0 * M_PI / p->L;
-        k_pif_modes<<<kModeBlocks, kThreads, 0, p->stream>>>(p->n, p->M, kunit, p->G, p->dinv, p->A, p->Bz,
-                                                              p->partials);
+        if (p->comm) {   // decomposed: this rank's rho^ (chi, D), summed over the ranks, then Poisson
+            const int64_t nm = (int64_t)p->n * p->n * p->n;
+            k_select<<<stream_grid(nm), kThreads, 0, p->stream>>>(p->n, p->M, p->G, p->dinv, p->A);
+            PIF_LAUNCHED(p);
+            if (ncclAllReduce(p->A, p->A, 2 * (size_t)nm, ncclDouble, ncclSum, p->comm, p->stream) != ncclSuccess) {
+                snprintf(p->err, sizeof(p->err), "ncclAllReduce of the modes failed");
+                p->poisoned = true;
+                return PIC_ENCCL;
+            }
+            k_pif_field<<<kModeBlocks, kThreads, 0, p->stream>>>(p->n, kunit, p->A, p->Bz, p->partials);
+        } else {
+            k_pif_modes<<<kModeBlocks, kThreads, 0, p->stream>>>(p->n, p->M, kunit, p->G, p->dinv, p->A, p->Bz,
+                                                                  p->partials);
+        }
         k_energy<<<1, 32, 0, p->stream>>>(kModeBlocks, p->partials, 0.5 / (p->L * p->L * p->L), p->energy,
                                           p->hist_slot >= 0 ? p->hist + p->hist_slot : nullptr);
         PIF_LAUNCHED(p);
@@ -1054,10 +1112,28 @@ pic_status pic_pif_window(pic_pif* p, int32_t* w, int32_t* m) {
     return PIC_OK;
 }
 
+pic_status pic_pif_attach_nccl(pic_pif* p, int32_t rank, int32_t nranks, const uint8_t* nccl_id) {
+    PIF_CHECK(p);
+    if (p->comm || nranks < 1 || rank < 0 || rank >= nranks || (nranks > 1 && !nccl_id)) return PIC_EINVAL;
+    if (nranks == 1) return PIC_OK;
+    ncclUniqueId u;
+    std::memcpy(&u, nccl_id, sizeof(u));
+    const ncclResult_t r = ncclCommInitRank(&p->comm, nranks, u, rank);
+    if (r != ncclSuccess) {
+        snprintf(p->err, sizeof(p->err), "ncclCommInitRank: %s", ncclGetErrorString(r));
+        p->comm = nullptr;
+        return PIC_ENCCL;
+    }
+    p->nranks = nranks;
+    return PIC_OK;
+}
+
 const char* pic_pif_last_error(const pic_pif* p) { return p ? p->err : g_err; }
 
 void pic_pif_free(pic_pif* p) {
     if (!p) return;
+    if (p->stream) cudaStreamSynchronize(p->stream);
+    if (p->comm) ncclCommDestroy(p->comm);
     for (auto& e : p->ev)
         if (e) cudaEventDestroy(e);
     delete p;

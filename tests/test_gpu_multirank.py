@@ -74,3 +74,19 @@ def test_pencil_decomposition_matches_oracle(world, n, pgrid):
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=ROOT, env=env)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
     assert "MP OK" in r.stdout and f"pgrid={pgrid}" in r.stdout
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_decomposed_pif_matches_oracle(world):
+    """The decomposed PIF (SURVEY §8(f) NEXT-2 on P ranks): particle shares on
+    P GPUs, the selected modes all-reduced; vs oracle/nufft.py on the whole particle set (E
+    1e-10, energies 1e-10, type 1 1e-11, 3 steps of the time loop W_x 1e-10, x, v 1e-12)."""
+    if _ngpus() < world:
+        pytest.skip(f"needs {world} GPUs")
+    port = 29800 + world
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port),
+           os.path.join(ROOT, "tests", "mp_pif_worker.py"), "16", "2", "3"]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=ROOT)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    assert "MP PIF OK" in r.stdout
