@@ -499,7 +499,7 @@ def pif_alg_bytes(stage: str, npart: int, n: int, launches_per_step: float = 1.0
 
 def run_pif(args, rank, world):
     """PIF time loop (pic_pif_step: PIF solve + leapfrog push) on N^3 modes x ppc particles per
-    cell; N > 1: independent replicas (the PIF solve is not decomposed: "replicas only")."""
+    cell; N > 1: the decomposed PIF (particle shares, the selected modes all-reduced)."""
     import numpy as np
     import torch
     import torch.distributed as dist
