@@ -719,12 +719,16 @@ __global__ void __launch_bounds__(1024) k_energy_reduce(Geom g, const double* __
 constexpr int kC2C = 4096;
 __host__ __device__ constexpr int c2c_lines(int M) { return kC2C / M > 8 ? 8 : (kC2C / M < 1 ? 1 : kC2C / M); }
 
+// pmask (nullable): pmask[z] == 0 marks a z plane no one reads (PIF: outside every particle
+// tile): the x pass skips its rows, the y pass (mask_outer) the plane.
 template <int SIGN, int LOGN>
 __global__ void __launch_bounds__(kThreads, 3) k_c2c_rows(double2* __restrict__ g, int64_t nrows,
-                                                          const double2* __restrict__ tw) {
+                                                          const double2* __restrict__ tw,
+                                                          const uint32_t* __restrict__ pmask) {
     extern __shared__ double2 smx[];
     constexpr int M = 1 << LOGN, R = c2c_lines(M), ls = M + M / 8 + 1;
     for (int64_t t = blockIdx.x; t * R < nrows; t += gridDim.x) {
+        if (pmask && !pmask[(t * R) >> LOGN]) continue;        // R <= M rows: one plane per tile
         double2* base = g + t * R * M;
         const int rows = (int)min((int64_t)R, nrows - t * R);
         auto src = [&](int l, int e) { return base[(int64_t)l * M + e]; };
@@ -743,11 +747,13 @@ __device__ __forceinline__ bool c2c_in_box(int64_t i, int M, int keep) { return 
 template <int SIGN, int LOGN>
 __global__ void __launch_bounds__(kThreads, 3) k_c2c_cols(double2* __restrict__ g, int64_t outer_stride,
                                                           int64_t line_stride_g, const double2* __restrict__ tw,
-                                                          int keep, int keep_outer) {
+                                                          int keep, int keep_outer,
+                                                          const uint32_t* __restrict__ pmask) {
     extern __shared__ double2 smx[];
     constexpr int M = 1 << LOGN, TW = c2c_lines(M), ls = col_stride(M, TW), nct = M / TW;
     for (int64_t t = blockIdx.x; t < (int64_t)M * nct; t += gridDim.x) {
         const int64_t o = t / nct, ct = t - o * nct;
+        if (pmask && !pmask[o]) continue;                       // the y pass: outer = z plane
         if (keep > 0 && ((keep_outer && !c2c_in_box(o, M, keep)) ||
                          !(c2c_in_box(ct * TW, M, keep) || c2c_in_box(ct * TW + TW - 1, M, keep))))
             continue;
@@ -867,7 +873,8 @@ void launch_fft_x_inv(const Geom& g, const double2* spec, double* E4, double* ha
 // In-place 3D C2C FFT of an M^3 complex grid, M a power of two in [16, 1024]: x, y, z passes
 // forward (sign -1), z, y, x inverse (+1); keep > 0 restricts the y and z passes to the
 // lines that meet the box [0, keep) u [M - keep, M) (see c2c_in_box).
-cudaError_t launch_fft_c2c_3d(double2* grid, int M, int sign, const double2* tw, cudaStream_t s, int keep) {
+cudaError_t launch_fft_c2c_3d(double2* grid, int M, int sign, const double2* tw, cudaStream_t s, int keep,
+                              const uint32_t* pmask) {
     const int lg = ilog2(M);
     if ((1 << lg) != M || lg < 4 || lg > 10) return cudaErrorInvalidValue;
     const int64_t M2 = (int64_t)M * M;
@@ -879,16 +886,18 @@ cudaError_t launch_fft_c2c_3d(double2* grid, int M, int sign, const double2* tw,
 #define PIC_C2C_ROWS(SG)                                                                                               \
     (e = cudaFuncSetAttribute(k_c2c_rows<SG, K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)srow),              \
      (e == cudaSuccess ? (k_c2c_rows<SG, K><<<persistent_grid(k_c2c_rows<SG, K>, srow, ntile), kThreads, srow, s>>>(   \
-          grid, M2, tw), 0) : 0))
-#define PIC_C2C_COLS(SG, OS, LS, KO)                                                                                   \
+          grid, M2, tw, pmask), 0) : 0))
+#define PIC_C2C_COLS(SG, OS, LS, KO, PM)                                                                               \
     (e = e == cudaSuccess ? cudaFuncSetAttribute(k_c2c_cols<SG, K>, cudaFuncAttributeMaxDynamicSharedMemorySize,       \
                                                  (int)scol) : e,                                                       \
      (e == cudaSuccess ? (k_c2c_cols<SG, K><<<persistent_grid(k_c2c_cols<SG, K>, scol, ntile), kThreads, scol, s>>>(   \
-          grid, OS, LS, tw, keep, KO), 0) : 0))
+          grid, OS, LS, tw, keep, KO, PM), 0) : 0))
     if (sign < 0) {
-        PIC_YZ_SWITCH(lg, (PIC_C2C_ROWS(-1), PIC_C2C_COLS(-1, M2, (int64_t)M, 0), PIC_C2C_COLS(-1, (int64_t)M, M2, 1)))
+        PIC_YZ_SWITCH(lg, (PIC_C2C_ROWS(-1), PIC_C2C_COLS(-1, M2, (int64_t)M, 0, pmask),
+                           PIC_C2C_COLS(-1, (int64_t)M, M2, 1, nullptr)))
     } else {
-        PIC_YZ_SWITCH(lg, (PIC_C2C_COLS(+1, (int64_t)M, M2, 1), PIC_C2C_COLS(+1, M2, (int64_t)M, 0), PIC_C2C_ROWS(+1)))
+        PIC_YZ_SWITCH(lg, (PIC_C2C_COLS(+1, (int64_t)M, M2, 1, nullptr), PIC_C2C_COLS(+1, M2, (int64_t)M, 0, pmask),
+                           PIC_C2C_ROWS(+1)))
     }
 #undef PIC_C2C_ROWS
 #undef PIC_C2C_COLS

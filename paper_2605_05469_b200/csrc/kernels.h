@@ -51,7 +51,10 @@ void launch_e4_pencil_unpack(const double* recv, int n, int nzs, int nyl, int Py
 // y / z passes only touch lines meeting the box [0, keep) u [M - keep, M) in x (and in the
 // outer y of the z pass): exact for an inverse transform of a spectrum that is zero outside
 // that box, and for a forward transform whose outputs outside it are not read.
-cudaError_t launch_fft_c2c_3d(double2* grid, int M, int sign, const double2* tw, cudaStream_t s, int keep = 0);
+// pmask (nullable): planes z with pmask[z] == 0 are neither written by the forward input nor
+// read after the inverse (PIF: outside every particle tile), so the x and y passes skip them.
+cudaError_t launch_fft_c2c_3d(double2* grid, int M, int sign, const double2* tw, cudaStream_t s, int keep = 0,
+                              const uint32_t* pmask = nullptr);
 // E4 component d <-> compact [nzl][n][n] doubles (host transfers of the field).
 void launch_e4_extract(const Geom& g, const double* E4, int d, double* out, cudaStream_t s);
 void launch_e4_pack(const Geom& g, const double* const comp[3], double* E4, cudaStream_t s);

@@ -12,7 +12,6 @@
 // The PIF solve packs E^_x + i E^_y into one type-2 transform (each is the transform of a
 // Hermitian spectrum, hence real) and E^_z into a second.
 #include <cuda_runtime.h>
-#include <cub/device/device_scan.cuh>
 #include <nccl.h>
 
 #include <algorithm>
@@ -383,6 +382,27 @@ __global__ void __launch_bounds__(kThreads) k_bin_place(int64_t np, const double
     perm[base + __popc(grp & ((1u << lane) - 1u))] = (uint32_t)j;
 }
 
+// Bin z layers holding particles (a bin of kB^3 fine cells at layer bz is nonempty).
+__global__ void k_bin_layers(const uint32_t* __restrict__ boffs, int64_t nbins, int nb, uint32_t* __restrict__ lmask) {
+    for (int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; b < nbins; b += (int64_t)gridDim.x * blockDim.x)
+        if (boffs[b + 1] > boffs[b]) lmask[b / ((int64_t)nb * nb)] = 1u;
+}
+
+// Fine plane z is used if the tile of a nonempty layer reaches it: layer bz's tiles cover planes
+// kB bz - H .. kB bz - H + T - 1 (mod M), T = kB + W + 1 (the binned spread / gather tiles).
+__global__ void k_plane_mask(const uint32_t* __restrict__ lmask, int nb, int M, int H, int W,
+                             uint32_t* __restrict__ pmask) {
+    const int z = blockIdx.x * blockDim.x + threadIdx.x;
+    if (z >= M) return;
+    const int T = kB + W + 1;
+    uint32_t used = 0;
+    for (int bz = 0; bz < nb && !used; ++bz) {
+        const int d = ((z - (kB * bz - H)) % M + M) % M;        // z's offset inside layer bz's reach
+        if (d < T) used = lmask[bz];
+    }
+    pmask[z] = used;
+}
+
 // Unwrapped window start and the W values of one coordinate (the same arithmetic as window_1d).
 template <int W>
 __device__ __forceinline__ int window_raw(double x, double inv_hf, double beta, double* wv, double scale) {
@@ -618,6 +638,8 @@ struct pic_pif {
     uint32_t* perm;      // np_max particle indices in bin order
     void* scan_tmp;
     size_t scan_bytes;
+    uint32_t* pmask;     // [M] fine-grid z planes reached by the binned particles' tiles
+    uint32_t* lmask;     // [nb] bin z layers holding particles
     bool poisoned;
     bool timing;
     cudaEvent_t ev[512];
@@ -638,14 +660,11 @@ bool valid(int32_t n, double L, double eps) {
 }
 
 struct Layout {
-    size_t G, A, Bz, dinv, partials, energy, hist, tw, bcnt, boffs, bcur, perm, scan, G2, total;
+    size_t G, A, Bz, dinv, partials, energy, hist, tw, bcnt, boffs, bcur, perm, scan, pmask, G2, total;
 };
 bool binnable(int n, int w) { return (2 * n) % kB == 0 && w <= 8; }
-size_t scan_tmp_bytes(int64_t nbins) {
-    size_t b = 0;
-    cub::DeviceScan::ExclusiveSum(nullptr, b, (const uint32_t*)nullptr, (uint32_t*)nullptr, (int)nbins);
-    return b;
-}
+// the bins' exclusive scan is the PIC path's own (particle_kernels.cu launch_scan)
+size_t scan_tmp_bytes(int64_t nbins) { return pic::scan_scratch_bytes(nbins); }
 Layout layout(int n, int64_t np_max, int w) {
     const size_t M = 2 * (size_t)n;
     Layout o;
@@ -663,7 +682,8 @@ Layout layout(int n, int64_t np_max, int w) {
     o.boffs = off;    off += nbins ? align256((nbins + 1) * 4) : 0;
     o.bcur = off;     off += nbins ? align256(nbins * 4) : 0;
     o.perm = off;     off += nbins ? align256((size_t)np_max * 4) : 0;
-    o.scan = off;     off += nbins ? align256(scan_tmp_bytes(nbins + 1)) : 0;
+    o.scan = off;     off += nbins ? align256(scan_tmp_bytes(nbins)) : 0;
+    o.pmask = off;    off += nbins ? align256((M + (M / kB)) * sizeof(uint32_t)) : 0;
     o.G2 = off;       off += nbins ? align256(M * M * M * sizeof(double2)) : 0;
     o.total = off;
     return o;
@@ -800,13 +820,16 @@ pic_status bin(pic_pif* p, int64_t np, const double* X) {
     PIF_CUDA(p, cudaMemsetAsync(p->bcnt, 0, (nbins + 1) * sizeof(uint32_t), p->stream));
     k_bin_count<<<particle_grid(np), kThreads, 0, p->stream>>>(np, X, p->M, p->nb, p->inv_hf, p->bcnt);
     PIF_LAUNCHED(p);
-    size_t tb = p->scan_bytes;
-    if (cub::DeviceScan::ExclusiveSum(p->scan_tmp, tb, p->bcnt, p->boffs, (int)(nbins + 1), p->stream) !=
-        cudaSuccess) {
-        snprintf(p->err, sizeof(p->err), "bin scan failed");
-        p->poisoned = true;
-        return PIC_ECUDA;
-    }
+    pic::launch_scan(p->bcnt, p->boffs, nbins, (uint32_t*)p->scan_tmp, p->stream);
+    PIF_LAUNCHED(p);
+    // the fine-grid planes the particles' bin tiles reach (decomposed PIF: a rank's particles
+    // occupy a few planes, the x and y passes skip the others)
+    PIF_CUDA(p, cudaMemsetAsync(p->lmask, 0, p->nb * sizeof(uint32_t), p->stream));
+    k_bin_layers<<<(unsigned)std::max<int64_t>(1, std::min<int64_t>((nbins + kThreads - 1) / kThreads, 148 * 8)),
+                   kThreads, 0, p->stream>>>(p->boffs, nbins, p->nb, p->lmask);
+    k_plane_mask<<<(p->M + kThreads - 1) / kThreads, kThreads, 0, p->stream>>>(p->lmask, p->nb, p->M,
+                                                                              p->w / 2 + 1, p->w, p->pmask);
+    PIF_LAUNCHED(p);
     PIF_CUDA(p, cudaMemcpyAsync(p->bcur, p->boffs, nbins * sizeof(uint32_t), cudaMemcpyDeviceToDevice, p->stream));
     k_bin_place<<<particle_grid(np), kThreads, 0, p->stream>>>(np, X, p->M, p->nb, p->inv_hf, p->bcur, p->perm);
     PIF_LAUNCHED(p);
@@ -834,7 +857,7 @@ pic_status fft(pic_pif* p, int dir, double2* grid = nullptr) {
     double2* g = grid ? grid : p->G;
     // only the lines that meet the mode box K_N: the inverse transform's input is zero
     // outside it (k_fill), the forward transform's output is read only inside it
-    PIF_CUDA(p, pic::launch_fft_c2c_3d(g, p->M, dir, p->tw, p->stream, p->n / 2));
+    PIF_CUDA(p, pic::launch_fft_c2c_3d(g, p->M, dir, p->tw, p->stream, p->n / 2, p->binned ? p->pmask : nullptr));
     return PIC_OK;
 }
 
@@ -925,7 +948,9 @@ pic_status pic_pif_create(int32_t n, double length, double eps, int64_t np_max, 
         p->G2 = use ? (double2*)(b + o.G2) : nullptr;
         p->scan_tmp = use ? (void*)(b + o.scan) : nullptr;
         const int64_t nbins = (int64_t)p->nb * p->nb * p->nb;
-        p->scan_bytes = use ? scan_tmp_bytes(nbins + 1) : 0;
+        p->scan_bytes = use ? scan_tmp_bytes(nbins) : 0;
+        p->pmask = use ? (uint32_t*)(b + o.pmask) : nullptr;
+        p->lmask = use ? p->pmask + p->M : nullptr;
     }
     {   // twiddles of the fine-grid FFT: W_M^m = exp(-2 pi i m / M), m < M
         double2* tw = (double2*)std::malloc(sizeof(double2) * p->M);

@@ -83,6 +83,33 @@ def test_pif_solve_matches_oracle(torch_dev, N, ppc, binned):
     assert np.allclose(W, Wo, rtol=1e-10, atol=0)
 
 
+@pytest.mark.parametrize("band", [(0.30, 0.45), (0.9, 1.0)])
+def test_pif_solve_particles_in_a_z_band(torch_dev, band):
+    """Particles confined to a z band (the decomposed PIF's rank shares; the second band
+    wraps its window tiles through z = 0): the fine-grid x and y passes skip the planes no
+    bin tile reaches, exactly -- E at the particles, energies and type 1 vs the oracle."""
+    from paper_2605_05469_b200 import PifSolver
+
+    torch = torch_dev
+    N = 32
+    Lk = 2 * np.pi / 0.5
+    rng = np.random.default_rng(13)
+    npart = 6000
+    xv = np.concatenate([rng.random((2, npart)) * Lk,
+                         (band[0] + (band[1] - band[0]) * rng.random((1, npart))) * Lk,
+                         rng.standard_normal((3, npart))])
+    xv[2] = np.minimum(xv[2], np.nextafter(Lk, 0))
+    q = np.full(npart, -Lk ** 3 / npart)
+    P = PifSolver(N, Lk, 1e-4, np_max=npart)
+    E, W = P.solve(_x(torch, xv), torch.from_numpy(q).cuda())
+    Eo, Wo, _ = U.pif_solve(xv[:3], q, N, Lk, 1e-4)
+    assert np.abs(E.cpu().numpy() - Eo).max() <= 1e-10 * np.abs(Eo).max()
+    assert np.allclose(W, Wo, rtol=1e-10, atol=0)
+    f = random_weights(npart, seed=14)
+    g = P.type1(_x(torch, xv), torch.from_numpy(f).cuda()).cpu().numpy()
+    assert np.abs(g - U.nufft1(xv[:3], f, N, Lk, 1e-4)).max() <= 1e-11 * np.abs(f).sum()
+
+
 def test_pif_cosine_lattice_closed_form_at_size(torch_dev):
     """2^21 particles on a 128^3 lattice, weights h^3 (1 + alpha cos(k1 x)), N = 64 modes:
     E_x = alpha sin(k1 x) / k1, E_y = E_z = 0, W_x = alpha^2 L^3 / (4 k1^2)."""
