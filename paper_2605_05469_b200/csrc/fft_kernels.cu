@@ -673,6 +673,30 @@ __global__ void k_e4_pencil_unpack(const double* __restrict__ recv, int n, int n
     }
 }
 
+// Transpose by pulling (peer transport, PIC_XPOSE_PULL=1): rank `rank` copies block `rank` of
+// every rank q's send buffer (src_tab[q], mapped over NVLink) to block q of dst -- the
+// all-to-all's data movement as one streaming kernel of 16-B loads, four in flight per thread.
+__global__ void __launch_bounds__(256) k_xpose_pull(double2* __restrict__ dst, double2* const* __restrict__ src_tab,
+                                                    int64_t blk, int rank, int P) {
+    const int64_t tot = blk * P, stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t i0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i0 < tot; i0 += 4 * stride) {
+        double2 v[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int64_t i = i0 + u * stride;
+            if (i < tot) {
+                const int64_t q = i / blk;
+                v[u] = __ldcs(src_tab[q] + rank * blk + (i - q * blk));
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int64_t i = i0 + u * stride;
+            if (i < tot) dst[i] = v[u];
+        }
+    }
+}
+
 // One CTA, fixed summation order (deterministic): energies = (W_x, W).
 __global__ void __launch_bounds__(1024) k_energy_reduce(Geom g, const double* __restrict__ partials,
                                                         int nparts, double* __restrict__ energies) {
@@ -920,6 +944,10 @@ void launch_e4_pencil_pack(const double* E4s, int n, int nzs, int nyl, int Py, d
 
 void launch_e4_pencil_unpack(const double* recv, int n, int nzs, int nyl, int Py, double* E4, cudaStream_t s) {
     k_e4_pencil_unpack<<<148 * 8, 256, 0, s>>>(recv, n, nzs, nyl, Py, E4);
+}
+
+void launch_xpose_pull(double2* dst, double2* const* src_tab, int64_t blk, int rank, int P, cudaStream_t s) {
+    k_xpose_pull<<<148 * 4, 256, 0, s>>>(dst, src_tab, blk, rank, P);
 }
 
 void launch_energy_reduce(const Geom& g, const double* partials, double* energies, cudaStream_t s) {

@@ -42,6 +42,8 @@ void launch_fft_z_mul(const Geom& g, const double2* pencil, SpecLayout out, doub
 void launch_fft_x_inv(const Geom& g, const double2* spec, double* E4, double* halo, const double2* tw,
                       double* partials, cudaStream_t s);
 void launch_energy_reduce(const Geom& g, const double* partials, double* energies, cudaStream_t s);
+// dst[q blk + e] = src_tab[q][rank blk + e] (complex), q < P: an all-to-all by peer pulls.
+void launch_xpose_pull(double2* dst, double2* const* src_tab, int64_t blk, int rank, int P, cudaStream_t s);
 // Pencils: slab field E4s [nzs + 1][n][n][4] -> y-group send blocks [Py][nzs + 1][nyl + 1][n][3] (rows
 // q nyl .. q nyl + nyl, periodic), and received blocks -> the pencil field [nzl + 1][nyl + 1][n][4].
 void launch_e4_pencil_pack(const double* E4s, int n, int nzs, int nyl, int Py, double* send, cudaStream_t s);

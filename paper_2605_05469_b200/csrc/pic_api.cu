@@ -119,7 +119,8 @@ struct pic_ctx {
     bool p2p = false;
     bool xpose_p2p = false;               // transposes too (PIC_P2P=2; slower, see solve())
     bool ghost_p2p = false;               // ghost charge by peer atomics (else the NCCL fold)
-    double2** peer_tab = nullptr;         // device [2][8]: every rank's specB, specD
+    double2** peer_tab = nullptr;         // device [4][8]: every rank's specB, specD, specA, specC
+    bool xpose_pull = false;              // transposes by peer pulls (PIC_XPOSE_PULL=1)
     char* ws = nullptr;                   // this rank's workspace base
     char* peer_ws[8] = {};                // rank r's workspace base in this address space
     void* ipc_open[8] = {};               // mapped peer allocations (closed by pic_free)
@@ -407,7 +408,7 @@ size_t carve(pic_ctx* c, const Geom& g, const Sizes& z, char* base) {
     char* sd = g.P > 1 ? take(sizeof(double2) * 4 * (size_t)z.send_len) : nullptr;
     char* sc = take(sizeof(uint32_t) * 2 * 8);
     char* br = take(sizeof(int) * 4);
-    char* pt = take(sizeof(double2*) * 16);
+    char* pt = take(sizeof(double2*) * 32);
     char* dc = take(sizeof(unsigned long long) * 4);
     char* rv = g.P > 1 ? take(sizeof(double2) * 4 * (size_t)z.recv_cap) : nullptr;
     char* pv[6] = {};
@@ -778,15 +779,30 @@ pic_status solve(pic_ctx* c, double scale, int slot) {
     PIC_LAUNCHED(c, "fft_y_fwd");
     if (g.P > 1) {
         StageScope t(c, PIC_STAGE_XPOSE, 0);
-        if (xpose_p2p) PIC_TRY(barrier(c));
-        else PIC_NCCL(c, ncclAlltoAll(c->specA, c->specB, 2 * unit / g.P, ncclDouble, c->comm, c->stream));
+        if (xpose_p2p) {
+            PIC_TRY(barrier(c));
+        } else if (c->xpose_pull) {          // every send buffer complete, then pull my blocks
+            PIC_TRY(barrier(c));
+            pic::launch_xpose_pull(c->specB, c->peer_tab + 16, (int64_t)(unit / g.P), g.rank, g.P, c->stream);
+            PIC_LAUNCHED(c, "xpose_pull");
+        } else {
+            PIC_NCCL(c, ncclAlltoAll(c->specA, c->specB, 2 * unit / g.P, ncclDouble, c->comm, c->stream));
+        }
     }
     { StageScope t(c, PIC_STAGE_FFT_Z_MUL, 1); pic::launch_fft_z_mul(g, c->specB, Cz, scale, c->tw, c->stream); }
     PIC_LAUNCHED(c, "fft_z_mul");
     if (g.P > 1) {
         StageScope t(c, PIC_STAGE_XPOSE, 0);
-        if (xpose_p2p) PIC_TRY(barrier(c));
-        else PIC_NCCL(c, ncclAlltoAll(c->specC, c->specD, 4 * unit / g.P, ncclDouble, c->comm, c->stream));
+        if (xpose_p2p) {
+            PIC_TRY(barrier(c));
+        } else if (c->xpose_pull) {          // pull, then wait until every rank has pulled from my specC
+            PIC_TRY(barrier(c));             // before the field y pass overwrites it
+            pic::launch_xpose_pull(c->specD, c->peer_tab + 24, (int64_t)(2 * unit / g.P), g.rank, g.P, c->stream);
+            PIC_LAUNCHED(c, "xpose_pull");
+            PIC_TRY(barrier(c));
+        } else {
+            PIC_NCCL(c, ncclAlltoAll(c->specC, c->specD, 4 * unit / g.P, ncclDouble, c->comm, c->stream));
+        }
     }
     { StageScope t(c, PIC_STAGE_FFT_Y_INV, 1); pic::launch_fft_y_field(g, D, C, c->tw, c->stream); }
     PIC_LAUNCHED(c, "fft_y_inv");
@@ -1290,13 +1306,17 @@ pic_status setup_p2p(pic_ctx* c) {
     c->p2p = agreed != 0;
     c->xpose_p2p = c->p2p && env && env[0] == '2';
     if (c->p2p) {
-        double2* tab[16] = {};
+        double2* tab[32] = {};
         for (int r = 0; r < g.P; ++r) {
             tab[r] = on_rank(c, r, c->specB);
             tab[8 + r] = on_rank(c, r, c->specD);
+            tab[16 + r] = on_rank(c, r, c->specA);
+            tab[24 + r] = on_rank(c, r, c->specC);
         }
         PIC_CUDA(c, cudaMemcpy(c->peer_tab, tab, sizeof(tab), cudaMemcpyHostToDevice));
     }
+    const char* xenv = getenv("PIC_XPOSE_PULL");
+    c->xpose_pull = c->p2p && !c->xpose_p2p && xenv && xenv[0] == '1';
     const char* genv = getenv("PIC_P2P_GHOST");
     c->ghost_p2p = c->p2p && genv && genv[0] == '2';
     return PIC_OK;
