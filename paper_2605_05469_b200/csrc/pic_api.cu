@@ -18,6 +18,10 @@
 // barrier); the FFT transposes stay ncclAlltoAll (the peer-store variant, PIC_P2P=2,
 // measured slower).  NCCL (PIC_P2P=0 or no IPC): [xpose] = ncclAlltoAll, halo/ghost
 // planes by ncclSend/Recv, leavers by counts all-to-all + grouped send/recv.
+// Pencils (pgrid = {Py > 1, Pz}, NCCL transport): a rank owns y and z blocks; the SOLVE is
+// wrapped by a y-group all-to-all of the charge to the FFT's z-slabs and one of the field
+// back (pencil_to_slab_rho, slab_to_pencil_E), and the ghost charge is folded in two phases
+// (plane to +z, then row to +y: fold_ghost_pencil).
 #include <nccl.h>
 
 #include <algorithm>
