@@ -101,7 +101,7 @@ enum { DC_N = 0, DC_ARR = 1, DC_LEAVE = 2, DC_MIGRATED = 3 };
 // receive buffer (full -> err_flag[2]) and counted in send_count[dest].
 void launch_push_key(const Geom& g, PState cur, const uint32_t* offs, const double* E4, uint32_t* key,
                      uint16_t* rank, uint32_t* count, double2* send, uint32_t* send_count,
-                     const SendSegs& segs, const PeerRecv* peers, int* err_flag, cudaStream_t s);
+                     const SendSegs& segs, const PeerRecv* peers, uint32_t* bprev, int* err_flag, cudaStream_t s);
 // Batched peer migration: the leavers push_key staged in this rank's send segments go
 // to each destination's receive buffer at a range reserved with one system atomic on
 // its arrival counter (base[P] scratch); false when PIC_P2P_MIG=1 selects the
@@ -136,7 +136,8 @@ void launch_place(const uint32_t* key, const uint16_t* rank, int64_t np, const u
 // fold), with system-scope atomics on the planes two GPUs share when P > 1.
 void launch_reorder_deposit(const Geom& g, const uint32_t* offs, const uint32_t* perm, PState cur,
                             const double2* recv, int64_t n_old, const unsigned long long* dcnt, PState nxt,
-                            int push, double* rho_buf, double* ghost, int* err_flag, cudaStream_t s);
+                            int push, double* rho_buf, double* ghost, const uint32_t* bprev, int* err_flag,
+                            cudaStream_t s);
 void launch_sort_segments(const uint32_t* offs, int64_t ncell, uint32_t* perm, cudaStream_t s);
 void launch_half_kick(const Geom& g, PState cur, int64_t np, const double* E4, cudaStream_t s);
 // dst[r * dpitch + i] += src[r * spitch + i] (doubles), i < width, r < height

@@ -37,6 +37,16 @@
 #ifndef PIC_ATOM_BATCH      // particles per batch of returned count atomics in push_key
 #define PIC_ATOM_BATCH 1        // r02 A/B at 512^3: 1, 2, 4, 8 -> 19.97, 20.21, 20.19, 19.94 ms
 #endif
+// PIC_PK_AGG: 1 = push_key (P = 1) counts arrivals per brick first: a shared-memory histogram
+// over a window around the brick (AggWin) gives each particle its rank among the brick's
+// arrivals in that cell, then one returned global atomic per non-empty window cell
+// reserves the brick's block of arrival ranks (about half as many global atomics as
+// particles); particles landing outside the window take one global atomic each as before.
+// Measured (r02, 512^3): push_key 20.7 vs 20.0 ms -- the shared histogram, the second
+// pass and the extra barriers cost more than the halved returned atomics save.  Off.
+#ifndef PIC_PK_AGG
+#define PIC_PK_AGG 0
+#endif
 
 namespace pic {
 
@@ -258,6 +268,27 @@ __device__ __forceinline__ double2* leave_rec(const SendBuf& sb, int dr, uint32_
 // cost +55% per particle at P = 4).  320 slots plus a warp-aggregated overflow.
 constexpr int kLeaveCap = 320;
 
+// Arrival window of a brick (PIC_PK_AGG): its 8 x 8 x 4 cells +- 4 in x and y and +- 3 in z
+// (2560 cells).  With the thermal displacement of ~2 cells per step about 7% of the particles
+// land outside.  Shared memory per CTA: the count and the key of each window cell (20 KB)
+// and the (bin, rank in bin) of the brick's first kInfoCap particles (9 KB), beside the
+// 17 KB E tile: 4 CTAs per SM.  P > 1 keeps the direct count atomics (the leaver staging
+// uses that shared memory).
+struct AggWin {
+    static constexpr int H = 4, HZ = 3, WX = 8 + 2 * H, WY = 8 + 2 * H, WZ = 4 + 2 * HZ, NB = WX * WY * WZ;
+    // bin of local cell (ix, iyl, izl) for the brick at (bx, by, bz), -1 outside the window;
+    // coordinates wrap where the rank's domain spans the whole periodic dimension
+    static __device__ __forceinline__ int bin(const Geom& g, int ix, int iyl, int izl, int bx, int by, int bz) {
+        const int dx = (ix - bx + H) & g.nmask;
+        int dy = iyl - by + H, dz = izl - bz + HZ;
+        if (g.nyl == g.n) dy &= g.nmask;
+        if (g.nzl == g.n) dz &= g.nmask;
+        if ((unsigned)dx >= (unsigned)WX || (unsigned)dy >= (unsigned)WY || (unsigned)dz >= (unsigned)WZ) return -1;
+        return (dz * WY + dy) * WX + dx;
+    }
+};
+constexpr int kInfoCap = 2304;      // particles per brick with a shared (bin, rank) record
+
 template <bool MR>
 __global__ void __launch_bounds__(kThreads, MR ? 3 : 4) k_push_key_brick(Geom g, PState cur,
                                                              const uint32_t* __restrict__ offs,
@@ -265,7 +296,8 @@ __global__ void __launch_bounds__(kThreads, MR ? 3 : 4) k_push_key_brick(Geom g,
                                                              uint32_t* __restrict__ key,
                                                              uint16_t* __restrict__ rank,
                                                              uint32_t* __restrict__ count,
-                                                             SendBuf sb, int* __restrict__ err) {
+                                                             SendBuf sb, uint32_t* __restrict__ bprev,
+                                                             int* __restrict__ err) {
     // E tile in x-pairs: entry (z, y, x) = (E_d(x), E_d(x + 1)) for d = x, y, z, so the two
     // x corners of one (y, z) corner pair are three 16-B shared loads (48 B) instead of two
     // 32-B node records (64 B): a quarter less shared-memory traffic per particle
@@ -274,6 +306,10 @@ __global__ void __launch_bounds__(kThreads, MR ? 3 : 4) k_push_key_brick(Geom g,
     __shared__ double2 lbuf[MR ? kLeaveCap : 1][4];      // leavers of this brick (P > 1)
     __shared__ uint8_t ldst[MR ? kLeaveCap : 1];
     __shared__ uint32_t lcount[8], lbase[8], nleave;
+    constexpr bool kAgg = PIC_PK_AGG && !PIC_PLACE_ATOMIC && PIC_ATOM_BATCH == 1 && !MR;
+    using Win = AggWin;
+    __shared__ uint32_t hist[kAgg ? Win::NB : 1], binkey[kAgg ? Win::NB : 1];
+    __shared__ uint32_t info[kAgg ? kInfoCap : 1];      // bin | rank in bin << 12, ~0: no record
     const int t = threadIdx.x;
     const uint32_t c0 = blockIdx.x * kBrick;
     int bx, by, bz;
@@ -297,7 +333,13 @@ __global__ void __launch_bounds__(kThreads, MR ? 3 : 4) k_push_key_brick(Geom g,
     }
     if (t < 8) lcount[t] = 0;
     if (t == 0) nleave = 0;
+    if (kAgg)
+        for (int b = t; b < Win::NB; b += kThreads) hist[b] = 0;
     const uint32_t P0 = __ldg(offs + c0), P1 = __ldg(offs + c0 + kBrick);
+    if (bprev && t == 0) {        // this order's brick ranges, for the reorder's L2 prefetch
+        bprev[blockIdx.x] = P0;
+        if (blockIdx.x == gridDim.x - 1) bprev[gridDim.x] = P1;
+    }
     __syncthreads();
     double xn[3], vn[3];
     if (P0 + t < P1) load_particle(cur, P0 + t, xn, vn);
@@ -341,8 +383,8 @@ __global__ void __launch_bounds__(kThreads, MR ? 3 : 4) k_push_key_brick(Geom g,
             kick(g, ep, v);
             drift(g, x, v);
             st_zv(cur.zv + 2 * i, make_double2(z0, v[2]), make_double2(v[0], v[1]));   // kicked v in place
-            int iz, iy;
-            const uint32_t k = key_of(g, x, &iz, &iy);
+            int iz, iy, ix;
+            const uint32_t k = key_of(g, x, &iz, &iy, &ix);
             if (MR && !in_domain(g, iy, iz)) {   // leaver: staged, sent below
                 const int dr = owner_of(g, iy, iz);
                 const double xo[3] = {x0, y0, z0};
@@ -372,10 +414,26 @@ __global__ void __launch_bounds__(kThreads, MR ? 3 : 4) k_push_key_brick(Geom g,
                 continue;
             }
             key[i] = k;
-            if (PIC_PLACE_ATOMIC) atomicAdd(count + k, 1u);          // RED: nothing to wait for
-            else kq[u] = k;
+            if (kAgg) {       // rank among the brick's arrivals in the cell, offset below
+                const uint32_t li = i - P0;
+                const int b = li < (uint32_t)kInfoCap ? Win::bin(g, ix, iy - g.y0, iz - g.z0, bx, by, bz) : -1;
+                if (b >= 0) {
+                    const uint32_t lr = atomicAdd(&hist[b], 1u);
+                    if (lr == 0) binkey[b] = k;
+                    info[li] = (uint32_t)b | (lr << 12);
+                } else {
+                    const uint32_t r = atomicAdd(count + k, 1u);
+                    if (r > 0xffffu) atomicExch(err, 1);
+                    rank[i] = (uint16_t)r;
+                    if (li < (uint32_t)kInfoCap) info[li] = ~0u;
+                }
+            } else if (PIC_PLACE_ATOMIC) {
+                atomicAdd(count + k, 1u);          // RED: nothing to wait for
+            } else {
+                kq[u] = k;
+            }
         }
-        if (!PIC_PLACE_ATOMIC) {
+        if (!PIC_PLACE_ATOMIC && !kAgg) {
             uint32_t rq[kAtomBatch];
 #pragma unroll
             for (int u = 0; u < kAtomBatch; ++u) rq[u] = kq[u] != kNoKey ? atomicAdd(count + kq[u], 1u) : 0u;
@@ -385,6 +443,31 @@ __global__ void __launch_bounds__(kThreads, MR ? 3 : 4) k_push_key_brick(Geom g,
                     if (rq[u] > 0xffffu) atomicExch(err, 1);
                     rank[i0 + u * kThreads] = (uint16_t)rq[u];
                 }
+        }
+    }
+    if (kAgg) {    // one returned global atomic per non-empty window cell: the brick's base rank
+        __syncthreads();
+        constexpr int kPer = (Win::NB + kThreads - 1) / kThreads;
+        uint32_t cb[kPer], rb[kPer];      // all of this thread's bins' atomics in flight at once
+#pragma unroll
+        for (int u = 0; u < kPer; ++u) {
+            const int b = t + u * kThreads;
+            cb[u] = b < Win::NB ? hist[b] : 0u;
+        }
+#pragma unroll
+        for (int u = 0; u < kPer; ++u)
+            if (cb[u]) rb[u] = atomicAdd(count + binkey[t + u * kThreads], cb[u]);
+#pragma unroll
+        for (int u = 0; u < kPer; ++u)
+            if (cb[u]) hist[t + u * kThreads] = rb[u];
+        __syncthreads();
+        const uint32_t Pe = min(P1, P0 + (uint32_t)kInfoCap);
+        for (uint32_t i = P0 + t; i < Pe; i += kThreads) {
+            const uint32_t v = info[i - P0];
+            if (v == ~0u) continue;
+            const uint32_t r = hist[v & 0xfffu] + (v >> 12);
+            if (r > 0xffffu) atomicExch(err, 1);
+            rank[i] = (uint16_t)r;
         }
     }
     if (MR) {      // one global atomic per destination, then the staged payloads
@@ -763,6 +846,23 @@ __device__ __forceinline__ int chunk_end(const uint32_t* soffs, int ca, int cap)
 #ifndef PIC_RD_MINB
 #define PIC_RD_MINB 3
 #endif
+// PIC_RD_PF: L2 prefetch distance in bricks (0 = off, the default).  The gather's sources are
+// the particles of the neighbouring bricks in the previous order (the thermal displacement
+// is ~2 cells), ~94% of them within +-1000 bricks in Morton order at 512^3.  Brick b
+// prefetches the previous order's particles of brick b + PIC_RD_PF into L2 (two bulk TMA
+// prefetches, or per-thread line prefetches with PIC_RD_PF_MODE=1), so that DRAM reads the
+// sources as one sequential stream ahead of the gather wavefront.  Measured (r02, ncu at
+// 512^3): at 256..2048 bricks ahead the prefetched lines are gone before the gather
+// (DRAM reads 73 -> 122..128 GB, +2.8 ms); at 64 ahead they are mostly used (DRAM reads
+// 80.7 GB, so ~60% of the gather bytes came from the prefetch) and the kernel is still
+// not faster (29.5 vs 28.4 ms): the scattered gather is bound on the L2 side, not by the
+// DRAM access pattern.
+#ifndef PIC_RD_PF
+#define PIC_RD_PF 0
+#endif
+#ifndef PIC_RD_PF_MODE      // 0: two bulk (TMA) prefetches per brick; 1: per-thread 128-B line prefetches
+#define PIC_RD_PF_MODE 0
+#endif
 
 template <bool MR>
 struct ReorderCap {
@@ -773,9 +873,29 @@ template <bool PUSH, bool MR>
 __global__ void __launch_bounds__(kThreads, PIC_RD_MINB) k_reorder_deposit(
     Geom g, const uint32_t* __restrict__ offs, const uint32_t* __restrict__ perm, PState cur,
     const double2* __restrict__ recv, int64_t n_old, const unsigned long long* __restrict__ dcnt, PState nxt,
-    double* __restrict__ rho, double* ghost, int* __restrict__ err) {
+    double* __restrict__ rho, double* ghost, const uint32_t* __restrict__ bprev, int* __restrict__ err) {
     constexpr int CAP = ReorderCap<MR>::value;
     if (MR && dcnt) n_old = (int64_t)dcnt[DC_N];
+    if (PIC_RD_PF > 0 && bprev && (PIC_RD_PF_MODE == 1 || threadIdx.x == 0)) {
+        auto pf = [&](uint32_t b) {
+            const uint32_t a0 = bprev[b], a1 = bprev[b + 1];
+            if (a1 <= a0) return;
+            if (PIC_RD_PF_MODE == 1) {       // per-thread line prefetches over the range
+                const char* x0 = reinterpret_cast<const char*>(cur.xy + a0);
+                const char* z0 = reinterpret_cast<const char*>(cur.zv + 2 * (int64_t)a0);
+                const uint32_t nx = (16u * (a1 - a0) + 127u) / 128u, nz = (32u * (a1 - a0) + 127u) / 128u;
+                for (uint32_t q = threadIdx.x; q < nx + nz; q += blockDim.x) {
+                    const char* a = q < nx ? x0 + 128 * (size_t)q : z0 + 128 * (size_t)(q - nx);
+                    asm volatile("prefetch.global.L2::evict_last [%0];" ::"l"(a));
+                }
+            } else {
+                prefetch_l2_bulk(cur.xy + a0, 16u * (a1 - a0));
+                prefetch_l2_bulk(cur.zv + 2 * (int64_t)a0, 32u * (a1 - a0));
+            }
+        };
+        if (blockIdx.x < (unsigned)PIC_RD_PF) pf(blockIdx.x);
+        if (blockIdx.x + (unsigned)PIC_RD_PF < gridDim.x) pf(blockIdx.x + PIC_RD_PF);
+    }
 
     extern __shared__ double dyn_smem[];
     double2* sp0 = reinterpret_cast<double2*>(dyn_smem);               // [CAP] (x, y)
@@ -1005,7 +1125,7 @@ void launch_key_import(const Geom& g, PState cur, int64_t np, uint32_t* key, uin
 
 void launch_push_key(const Geom& g, PState cur, const uint32_t* offs, const double* E4, uint32_t* key,
                      uint16_t* rank, uint32_t* count, double2* send, uint32_t* send_count,
-                     const SendSegs& segs, const PeerRecv* peers, int* err_flag, cudaStream_t s) {
+                     const SendSegs& segs, const PeerRecv* peers, uint32_t* bprev, int* err_flag, cudaStream_t s) {
     const unsigned nbrick = (unsigned)(((int64_t)g.n * g.nyl * g.nzl) / kBrick);
     SendBuf sb{};
     sb.data = send;
@@ -1017,8 +1137,9 @@ void launch_push_key(const Geom& g, PState cur, const uint32_t* offs, const doub
     static const bool unbatched = [] { const char* e = getenv("PIC_P2P_MIG"); return e && e[0] == '1'; }();
     if (peers && unbatched) { sb.peers = *peers; sb.remote = 1; }
     static const bool force_mr = getenv("PIC_FORCE_MR") != nullptr;   // diagnostics
-    if (g.P > 1 || force_mr) k_push_key_brick<true><<<nbrick, kThreads, 0, s>>>(g, cur, offs, E4, key, rank, count, sb, err_flag);
-    else k_push_key_brick<false><<<nbrick, kThreads, 0, s>>>(g, cur, offs, E4, key, rank, count, sb, err_flag);
+    if (PIC_RD_PF == 0) bprev = nullptr;       // only the reorder's L2 prefetch reads it
+    if (g.P > 1 || force_mr) k_push_key_brick<true><<<nbrick, kThreads, 0, s>>>(g, cur, offs, E4, key, rank, count, sb, bprev, err_flag);
+    else k_push_key_brick<false><<<nbrick, kThreads, 0, s>>>(g, cur, offs, E4, key, rank, count, sb, bprev, err_flag);
 }
 
 bool leavers_batched() {
@@ -1075,19 +1196,20 @@ void launch_place(const uint32_t* key, const uint16_t* rank, int64_t np, const u
 
 void launch_reorder_deposit(const Geom& g, const uint32_t* offs, const uint32_t* perm, PState cur,
                             const double2* recv, int64_t n_old, const unsigned long long* dcnt, PState nxt,
-                            int push, double* rho_buf, double* ghost, int* err_flag, cudaStream_t s) {
+                            int push, double* rho_buf, double* ghost, const uint32_t* bprev, int* err_flag,
+                            cudaStream_t s) {
     const unsigned nbrick = (unsigned)(((int64_t)g.n * g.nyl * g.nzl) / kBrick);
     static const bool force_mr = getenv("PIC_FORCE_MR") != nullptr;   // diagnostics
     if (g.P == 1 && !force_mr) {
         if (push)
-            k_reorder_deposit<true, false><<<nbrick, kThreads, reorder_smem<false>(), s>>>(g, offs, perm, cur, recv, n_old, dcnt, nxt, rho_buf, ghost, err_flag);
+            k_reorder_deposit<true, false><<<nbrick, kThreads, reorder_smem<false>(), s>>>(g, offs, perm, cur, recv, n_old, dcnt, nxt, rho_buf, ghost, bprev, err_flag);
         else
-            k_reorder_deposit<false, false><<<nbrick, kThreads, reorder_smem<false>(), s>>>(g, offs, perm, cur, recv, n_old, dcnt, nxt, rho_buf, ghost, err_flag);
+            k_reorder_deposit<false, false><<<nbrick, kThreads, reorder_smem<false>(), s>>>(g, offs, perm, cur, recv, n_old, dcnt, nxt, rho_buf, ghost, bprev, err_flag);
     } else {
         if (push)
-            k_reorder_deposit<true, true><<<nbrick, kThreads, reorder_smem<true>(), s>>>(g, offs, perm, cur, recv, n_old, dcnt, nxt, rho_buf, ghost, err_flag);
+            k_reorder_deposit<true, true><<<nbrick, kThreads, reorder_smem<true>(), s>>>(g, offs, perm, cur, recv, n_old, dcnt, nxt, rho_buf, ghost, bprev, err_flag);
         else
-            k_reorder_deposit<false, true><<<nbrick, kThreads, reorder_smem<true>(), s>>>(g, offs, perm, cur, recv, n_old, dcnt, nxt, rho_buf, ghost, err_flag);
+            k_reorder_deposit<false, true><<<nbrick, kThreads, reorder_smem<true>(), s>>>(g, offs, perm, cur, recv, n_old, dcnt, nxt, rho_buf, ghost, bprev, err_flag);
     }
 }
 

@@ -82,6 +82,7 @@ struct pic_ctx {
     uint32_t* perm = nullptr;     // [np_cap]
     uint32_t* count = nullptr;
     uint32_t* offs = nullptr;
+    uint32_t* bprev = nullptr;        // [nbrick + 1] brick ranges of the particle order push_key read
     uint32_t* scan_scratch = nullptr;
     double* rho = nullptr;        // (nzl + 1) pitched real planes; half spectrum S0 in the solve
     double2* specA = nullptr;     // forward transpose send (P = 1: rho)
@@ -383,6 +384,7 @@ size_t carve(pic_ctx* c, const Geom& g, const Sizes& z, char* base) {
     char* pm = take(sizeof(uint32_t) * (size_t)std::max(z.np_cap, nblk + 1));
     char* cn = take(sizeof(uint32_t) * (size_t)ncell);
     char* of = take(sizeof(uint32_t) * (size_t)(ncell + 1));
+    char* bp = take(sizeof(uint32_t) * (size_t)(ncell / 256 + 1));
     char* ss = take(pic::scan_scratch_bytes(std::max(ncell, nblk)));
     char* rh = take(plane * (size_t)(g.nzl + 1));
     char* sA = g.P > 1 ? take(unit) : nullptr;
@@ -431,6 +433,7 @@ size_t carve(pic_ctx* c, const Geom& g, const Sizes& z, char* base) {
         c->perm = reinterpret_cast<uint32_t*>(pm);
         c->count = reinterpret_cast<uint32_t*>(cn);
         c->offs = reinterpret_cast<uint32_t*>(of);
+        c->bprev = reinterpret_cast<uint32_t*>(bp);
         c->scan_scratch = reinterpret_cast<uint32_t*>(ss);
         c->rho = reinterpret_cast<double*>(rh);
         c->specA = g.P > 1 ? reinterpret_cast<double2*>(sA) : reinterpret_cast<double2*>(rh);
@@ -1103,7 +1106,7 @@ pic_status push_sort_deposit(pic_ctx* c, int push) {
         StageScope t(c, PIC_STAGE_PUSH_KEY, 1);
         if (push)
             pic::launch_push_key(g, cur, c->offs, c->E4, c->key, c->rank, c->count, c->send, c->send_count,
-                                 c->segs, peer_mig ? &peers : nullptr, c->err_flag, c->stream);
+                                 c->segs, peer_mig ? &peers : nullptr, c->bprev, c->err_flag, c->stream);
         else
             pic::launch_key_import(g, cur, c->np, c->key, c->rank, c->count, c->err_flag, c->stream);
     }
@@ -1174,7 +1177,7 @@ pic_status push_sort_deposit(pic_ctx* c, int push) {
     {
         StageScope t(c, PIC_STAGE_REORDER_DEPOSIT, 1);
         pic::launch_reorder_deposit(g, c->offs, c->perm, cur, c->recv, n_old, dc, nxt, push, c->rho, ghost_dst(c),
-                                    c->err_flag, c->stream);
+                                    push ? c->bprev : nullptr, c->err_flag, c->stream);
     }
     PIC_LAUNCHED(c, "reorder_deposit");
     if (peer_mig) {

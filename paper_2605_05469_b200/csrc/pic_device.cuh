@@ -144,14 +144,15 @@ __device__ __forceinline__ void unlkey(const Geom& g, uint32_t k, int& ix, int& 
     izl = (int)compact3(lo >> 2) | (g.mz > g.my ? other : 0);
 }
 
-// Local key of the cell of x on this rank; *iyg / *izg = its global y row / z plane.
+// Local key of the cell of x on this rank; *ixg / *iyg / *izg = its global cell indices.
 __device__ __forceinline__ uint32_t key_of(const Geom& g, const double x[3], int* izg = nullptr,
-                                           int* iyg = nullptr) {
+                                           int* iyg = nullptr, int* ixg = nullptr) {
     int i0 = cell_of(__dmul_rn(x[0], g.inv_h), g.n);
     int i1 = cell_of(__dmul_rn(x[1], g.inv_h), g.n);
     int i2 = cell_of(__dmul_rn(x[2], g.inv_h), g.n);
     if (izg) *izg = i2;
     if (iyg) *iyg = i1;
+    if (ixg) *ixg = i0;
     return lkey(g, i0, i1 - g.y0, i2 - g.z0);
 }
 
@@ -297,6 +298,11 @@ __device__ __forceinline__ void store_particle(const PState& s, int64_t i, const
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
     const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s), "l"(gmem) : "memory");
+}
+// Bulk prefetch of a contiguous global range into L2 (TMA unit; 16-B aligned, size a
+// multiple of 16), issued by one thread, no completion to wait for.
+__device__ __forceinline__ void prefetch_l2_bulk(const void* gmem, uint32_t bytes) {
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(gmem), "r"(bytes) : "memory");
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait0() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
