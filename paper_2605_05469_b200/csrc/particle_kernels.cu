@@ -962,27 +962,37 @@ __global__ void __launch_bounds__(kThreads, PIC_RD_MINB) k_reorder_deposit(
             bool any = false;
             for (int p = s0; p < s1; ++p) any |= sE[p] >= n_old;
             if (any) {
-                auto tie = [&](int slot) -> unsigned long long {
-                    const uint32_t e = sE[slot];
-                    if (e >= n_old)
-                        return (unsigned long long)__double_as_longlong(recv[4 * ((int64_t)e - n_old) + 3].x);
-                    const double x[3] = {sp0[slot].x, sp0[slot].y, sp1[slot].x};   // x_n (not yet drifted)
-                    return (unsigned long long)gkey_of(g, x) | ((unsigned long long)e << 32);
+                // the old global key of every slot once (sperm is free after the gather; the
+                // old index is sE for residents, the record's high word for arrivals), then an
+                // insertion sort on the cached keys: residents are already in order, arrivals
+                // move past them (r02: recomputing the resident keys inside the comparison
+                // loop made the last slab's reorder ~0.8 ms slower, whose arrivals from both
+                // faces sort in front of the residents)
+                auto rec = [&](uint32_t e) {
+                    return (unsigned long long)__double_as_longlong(recv[4 * ((int64_t)e - n_old) + 3].x);
                 };
-                auto less = [](unsigned long long u, unsigned long long v) {
-                    const uint32_t ug = (uint32_t)u, vg = (uint32_t)v;
-                    return ug < vg || (ug == vg && (uint32_t)(u >> 32) < (uint32_t)(v >> 32));
-                };
+                for (int p = s0; p < s1; ++p) {
+                    const uint32_t e = sE[p];
+                    if (e >= n_old) {
+                        sperm[p] = (uint32_t)rec(e);
+                    } else {
+                        const double x[3] = {sp0[p].x, sp0[p].y, sp1[p].x};   // x_n (not yet drifted)
+                        sperm[p] = gkey_of(g, x);
+                    }
+                }
+                auto oldi = [&](uint32_t e) { return e >= n_old ? (uint32_t)(rec(e) >> 32) : e; };
                 for (int a = s0 + 1; a < s1; ++a) {
-                    const unsigned long long ta = tie(a);
+                    const uint32_t ga = sperm[a], ea = sE[a];
                     const double2 r0 = sp0[a], r1 = sp1[a], r2 = sp2[a];
-                    const uint32_t ea = sE[a];
                     int b = a - 1;
-                    while (b >= s0 && less(ta, tie(b))) {
-                        sp0[b + 1] = sp0[b]; sp1[b + 1] = sp1[b]; sp2[b + 1] = sp2[b]; sE[b + 1] = sE[b];
+                    while (b >= s0) {
+                        const uint32_t gb = sperm[b];
+                        if (!(ga < gb || (ga == gb && oldi(ea) < oldi(sE[b])))) break;
+                        sp0[b + 1] = sp0[b]; sp1[b + 1] = sp1[b]; sp2[b + 1] = sp2[b];
+                        sE[b + 1] = sE[b]; sperm[b + 1] = gb;
                         --b;
                     }
-                    sp0[b + 1] = r0; sp1[b + 1] = r1; sp2[b + 1] = r2; sE[b + 1] = ea;
+                    sp0[b + 1] = r0; sp1[b + 1] = r1; sp2[b + 1] = r2; sE[b + 1] = ea; sperm[b + 1] = ga;
                 }
             }
             __syncthreads();
