@@ -15,7 +15,7 @@ matrix-free FD-PCG Poisson solve (SSOR(pi/2, 4, 2), tol 1e-4, warm start;
 P:179-181) in place of the FFT solve.
 
 Prints ONE JSON line on rank 0.  For N > 1 (torchrun) the same 512^3 problem is
-decomposed in z-slabs over the N GPUs (NCCL all-to-all FFT transposes, halo/ghost
+decomposed in z-slabs over the N GPUs (FFT transposes by copy-engine pulls over NVLink, halo/ghost
 planes, particle migration): strong scaling of a fixed problem, time = max over ranks.
 """
 from __future__ import annotations
@@ -459,7 +459,8 @@ def run_ours(args, rank, world):
                    (f"pencil decomposition {pgrid[0]}x{pgrid[1]} (y x z) over {world} GPUs (y-group "
                     f"all-to-all to the FFT's z-slabs and back, NCCL all-to-all FFT transposes, ghost/halo "
                     f"row and plane and particle migration over NCCL send/recv)" if pgrid[0] > 1 else
-                    f"z-slab decomposition over {world} GPUs (NCCL all-to-all FFT transposes; halo "
+                    f"z-slab decomposition over {world} GPUs (FFT transposes: "
+                    f"{'copy-engine pulls over NVLink' if nvlink['transport'] == 'peer' else 'NCCL all-to-all'}; halo "
                     f"plane, ghost plane and particle migration over "
                     f"{'NVLink peer memory' if nvlink['transport'] == 'peer' else 'NCCL send/recv'})"),
                    "migrated_per_step": migrated / args.steps,

@@ -15,8 +15,9 @@
 // (CUDA IPC, NVLink); fft_x_inv writes the halo plane of the slab below, push_key stages
 // the leavers and k_leaver_copy streams them into the destination's receive buffer, the
 // ghost charge plane is pulled over NVLink by the slab above (k_add_plane after a
-// barrier); the FFT transposes stay ncclAlltoAll (the peer-store variant, PIC_P2P=2,
-// measured slower).  NCCL (PIC_P2P=0 or no IPC): [xpose] = ncclAlltoAll, halo/ghost
+// barrier); the FFT transposes are copy-engine pulls of each peer's block after a barrier
+// (ncclAlltoAll with PIC_XPOSE_PULL=0; the peer-store variant, PIC_P2P=2, measured
+// slower).  NCCL (PIC_P2P=0 or no IPC): [xpose] = ncclAlltoAll, halo/ghost
 // planes by ncclSend/Recv, leavers by counts all-to-all + grouped send/recv.
 // Pencils (pgrid = {Py > 1, Pz}, NCCL transport): a rank owns y and z blocks; the SOLVE is
 // wrapped by a y-group all-to-all of the charge to the FFT's z-slabs and one of the field
@@ -125,7 +126,10 @@ struct pic_ctx {
     bool xpose_p2p = false;               // transposes too (PIC_P2P=2; slower, see solve())
     bool ghost_p2p = false;               // ghost charge by peer atomics (else the NCCL fold)
     double2** peer_tab = nullptr;         // device [4][8]: every rank's specB, specD, specA, specC
-    bool xpose_pull = false;              // transposes by peer pulls (PIC_XPOSE_PULL=1)
+    bool xpose_pull = false;              // transposes by peer pulls (PIC_XPOSE_PULL=1: kernel, 2: copy engines)
+    bool xpose_ce = false;                // PIC_XPOSE_PULL=2
+    cudaStream_t side[8] = {};            // copy-engine pulls, one stream per source rank
+    cudaEvent_t side_ev[9] = {};
     char* ws = nullptr;                   // this rank's workspace base
     char* peer_ws[8] = {};                // rank r's workspace base in this address space
     void* ipc_open[8] = {};               // mapped peer allocations (closed by pic_free)
@@ -713,6 +717,30 @@ pic_status refresh_halo(pic_ctx* c) {
     return barrier(c);
 }
 
+// Peer-pull transpose (after a barrier: every send side complete): block rank of rank q's
+// send buffer src -> block q of dst, blk complex elements per block.  PIC_XPOSE_PULL=1: one
+// kernel reads all peers over NVLink; 2: one copy-engine memcpy per source rank, each on
+// its own stream (staggered start, so that the ranks do not all read one peer at once).
+pic_status xpose_pull(pic_ctx* c, double2* dst, double2* src, double2* const* src_tab, int64_t blk) {
+    const Geom& g = c->gs;
+    if (!c->xpose_ce) {
+        pic::launch_xpose_pull(dst, src_tab, blk, g.rank, g.P, c->stream);
+        PIC_LAUNCHED(c, "xpose_pull");
+        return PIC_OK;
+    }
+    PIC_CUDA(c, cudaEventRecord(c->side_ev[8], c->stream));
+    for (int i = 0; i < g.P; ++i) {
+        const int q = (g.rank + i) % g.P;
+        const double2* from = (q == g.rank ? src : on_rank(c, q, src)) + (size_t)g.rank * blk;
+        PIC_CUDA(c, cudaStreamWaitEvent(c->side[i], c->side_ev[8], 0));
+        PIC_CUDA(c, cudaMemcpyAsync(dst + (size_t)q * blk, from, sizeof(double2) * (size_t)blk,
+                                    cudaMemcpyDeviceToDevice, c->side[i]));
+        PIC_CUDA(c, cudaEventRecord(c->side_ev[i], c->side[i]));
+        PIC_CUDA(c, cudaStreamWaitEvent(c->stream, c->side_ev[i], 0));
+    }
+    return PIC_OK;
+}
+
 // Destination of fft_x_inv's copy of plane 0: the halo plane of the slab below.
 double* halo_dst(pic_ctx* c) {
     const Geom& g = c->gs;
@@ -771,9 +799,9 @@ pic_status solve(pic_ctx* c, double scale, int slot) {
     SpecLayout Cz{g.P > 1 ? c->specC : c->specD, 1, 2, nullptr};   // return transpose, send side
     const SpecLayout D{c->specD, 1, 2, nullptr};
     const SpecLayout C{c->specC, 0, 3, nullptr};
-    // The transposes stay NCCL all-to-alls on both transports: storing the 64-byte
-    // column runs of the y/z passes straight into the peers (SpecLayout REMOTE) was
-    // measured slower at P = 2 (z pass 0.95 -> 2.6 ms, more than the all-to-all saves).
+    // Transposes: copy-engine pulls on the peer transport (xpose_pull), else NCCL all-to-alls.
+    // Storing the 64-byte column runs of the y/z passes straight into the peers (SpecLayout
+    // REMOTE, PIC_P2P=2) was measured slower at P = 2 (z pass 0.95 -> 2.6 ms).
     const bool xpose_p2p = c->p2p && c->xpose_p2p;
     if (xpose_p2p) {
         A.packed = Cz.packed = 2;
@@ -790,8 +818,7 @@ pic_status solve(pic_ctx* c, double scale, int slot) {
             PIC_TRY(barrier(c));
         } else if (c->xpose_pull) {          // every send buffer complete, then pull my blocks
             PIC_TRY(barrier(c));
-            pic::launch_xpose_pull(c->specB, c->peer_tab + 16, (int64_t)(unit / g.P), g.rank, g.P, c->stream);
-            PIC_LAUNCHED(c, "xpose_pull");
+            PIC_TRY(xpose_pull(c, c->specB, c->specA, c->peer_tab + 16, (int64_t)(unit / g.P)));
         } else {
             PIC_NCCL(c, ncclAlltoAll(c->specA, c->specB, 2 * unit / g.P, ncclDouble, c->comm, c->stream));
         }
@@ -804,8 +831,7 @@ pic_status solve(pic_ctx* c, double scale, int slot) {
             PIC_TRY(barrier(c));
         } else if (c->xpose_pull) {          // pull, then wait until every rank has pulled from my specC
             PIC_TRY(barrier(c));             // before the field y pass overwrites it
-            pic::launch_xpose_pull(c->specD, c->peer_tab + 24, (int64_t)(2 * unit / g.P), g.rank, g.P, c->stream);
-            PIC_LAUNCHED(c, "xpose_pull");
+            PIC_TRY(xpose_pull(c, c->specD, c->specC, c->peer_tab + 24, (int64_t)(2 * unit / g.P)));
             PIC_TRY(barrier(c));
         } else {
             PIC_NCCL(c, ncclAlltoAll(c->specC, c->specD, 4 * unit / g.P, ncclDouble, c->comm, c->stream));
@@ -1322,8 +1348,20 @@ pic_status setup_p2p(pic_ctx* c) {
         }
         PIC_CUDA(c, cudaMemcpy(c->peer_tab, tab, sizeof(tab), cudaMemcpyHostToDevice));
     }
+    // FFT transposes on the peer transport: copy-engine pulls by default (r02 at 512^3 on 4 GPUs:
+    // 0.98 ms per step against 1.29 for ncclAlltoAll and 1.97 for the pull kernel);
+    // PIC_XPOSE_PULL=0 keeps ncclAlltoAll, 1 the pull kernel
     const char* xenv = getenv("PIC_XPOSE_PULL");
-    c->xpose_pull = c->p2p && !c->xpose_p2p && xenv && xenv[0] == '1';
+    const char xm = xenv && xenv[0] ? xenv[0] : '2';
+    c->xpose_pull = c->p2p && !c->xpose_p2p && (xm == '1' || xm == '2');
+    c->xpose_ce = c->xpose_pull && xm == '2';
+    if (c->xpose_ce) {
+        for (int r = 0; r < g.P; ++r) {
+            PIC_CUDA(c, cudaStreamCreateWithFlags(&c->side[r], cudaStreamNonBlocking));
+            PIC_CUDA(c, cudaEventCreateWithFlags(&c->side_ev[r], cudaEventDisableTiming));
+        }
+        PIC_CUDA(c, cudaEventCreateWithFlags(&c->side_ev[8], cudaEventDisableTiming));
+    }
     const char* genv = getenv("PIC_P2P_GHOST");
     c->ghost_p2p = c->p2p && genv && genv[0] == '2';
     return PIC_OK;
@@ -1591,6 +1629,11 @@ void pic_free(pic_ctx* c) {
     if (!c) return;
     if (c->stream) cudaStreamSynchronize(c->stream);
     for (cudaEvent_t e : c->ev_pool) cudaEventDestroy(e);
+    for (int r = 0; r < 8; ++r) {
+        if (c->side[r]) cudaStreamDestroy(c->side[r]);
+        if (c->side_ev[r]) cudaEventDestroy(c->side_ev[r]);
+    }
+    if (c->side_ev[8]) cudaEventDestroy(c->side_ev[8]);
     for (int r = 0; r < 8; ++r)
         if (c->ipc_open[r]) cudaIpcCloseMemHandle(c->ipc_open[r]);
     if (c->ycomm) ncclCommDestroy(c->ycomm);
