@@ -457,7 +457,8 @@ def run_ours(args, rank, world):
                    "k": 0.5, "alpha": 0.05, "dt": args.dt,
                    "parallelism": "1 GPU" if world == 1 else
                    (f"pencil decomposition {pgrid[0]}x{pgrid[1]} (y x z) over {world} GPUs (y-group "
-                    f"all-to-all to the FFT's z-slabs and back, NCCL all-to-all FFT transposes, ghost/halo "
+                    f"redistribution to the FFT's z-slabs and back and the FFT transposes by copy-engine pulls "
+                    f"over NVLink when every rank maps the others (else NCCL all-to-all), ghost/halo "
                     f"row and plane and particle migration over NCCL send/recv)" if pgrid[0] > 1 else
                     f"z-slab decomposition over {world} GPUs (FFT transposes: "
                     f"{'copy-engine pulls over NVLink' if nvlink['transport'] == 'peer' else 'NCCL all-to-all'}; halo "

@@ -98,9 +98,10 @@ pic_status pic_params_default(pic_params *p);
  * owns the cells/nodes with z in [pz N/Pz, +N/Pz) and y in [py N/Py, +N/Py) (pgrid = {Py, Pz};
  * Py = 1: z-slabs) and the particles whose cell lies there.  The field solve always runs on
  * z-slabs of N/nranks planes (slab index = rank): pencils redistribute the charge to them and
- * the field back with one all-to-all in the y-group (the Py ranks sharing pz) each way, around
- * the slab FFT's own all-to-all transposes.  Pencils use the NCCL transport and
- * the FFT solver.  Rank 0 creates the NCCL id (128 bytes), the caller broadcasts it
+ * the field back with one exchange in the y-group (the Py ranks sharing pz) each way, around
+ * the slab FFT's own transposes.  With every workspace mapped (CUDA IPC) the
+ * transposes and the y-group exchanges are copy-engine pulls of the peers' blocks, else NCCL
+ * all-to-alls; pencils keep NCCL for migration, halos and ghost folds, and the FFT solver.  Rank 0 creates the NCCL id (128 bytes), the caller broadcasts it
  * (torch.distributed) and every rank passes it to pic_init. */
 pic_status pic_nccl_unique_id(uint8_t id[128]);
 
@@ -174,12 +175,12 @@ pic_status pic_num_particles(pic_ctx *ctx, int64_t *np);
 /* Particles this rank has sent to other ranks since pic_init (migration, P > 1). */
 pic_status pic_migrated(pic_ctx *ctx, int64_t *migrated);
 
-/* Transport of the P > 1 exchanges: *peer = 1 when every rank's workspace is
- * mapped (CUDA IPC over NVLink) and the transposes, halo/ghost planes and
- * migration are stores of the producing kernels into the peers' buffers; 0 for
- * the NCCL transport (all-to-all, send/recv), used when the mapping is not
- * possible on every rank or when the environment sets PIC_P2P=0 at pic_init.
- * Always 0 at P = 1. */
+/* Transport of the P > 1 exchanges of z-slabs: *peer = 1 when every rank's workspace is
+ * mapped (CUDA IPC over NVLink): halo/ghost planes and migration go through the peers'
+ * buffers and the FFT transposes are copy-engine pulls; 0 for the NCCL transport
+ * (all-to-all, send/recv), used when the mapping is not possible on every rank, when the
+ * environment sets PIC_P2P=0 at pic_init, and for pencils (whose solve still pulls over
+ * the mapping when it exists).  Always 0 at P = 1. */
 pic_status pic_peer_transport(pic_ctx *ctx, int32_t *peer);
 
 /* Copy THIS RANK's particle state to host xyzuvw[6][np] (np = pic_num_particles) in

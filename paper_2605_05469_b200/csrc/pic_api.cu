@@ -19,10 +19,11 @@
 // (ncclAlltoAll with PIC_XPOSE_PULL=0; the peer-store variant, PIC_P2P=2, measured
 // slower).  NCCL (PIC_P2P=0 or no IPC): [xpose] = ncclAlltoAll, halo/ghost
 // planes by ncclSend/Recv, leavers by counts all-to-all + grouped send/recv.
-// Pencils (pgrid = {Py > 1, Pz}, NCCL transport): a rank owns y and z blocks; the SOLVE is
-// wrapped by a y-group all-to-all of the charge to the FFT's z-slabs and one of the field
-// back (pencil_to_slab_rho, slab_to_pencil_E), and the ghost charge is folded in two phases
-// (plane to +z, then row to +y: fold_ghost_pencil).
+// Pencils (pgrid = {Py > 1, Pz}): a rank owns y and z blocks; the SOLVE is wrapped by a
+// y-group redistribution of the charge to the FFT's z-slabs and one of the field back
+// (pencil_to_slab_rho, slab_to_pencil_E: copy-engine pulls over the IPC mapping, else NCCL
+// all-to-alls), and the ghost charge is folded in two phases (plane to +z, then row to +y:
+// fold_ghost_pencil); migration, halos and ghost folds use NCCL.
 #include <nccl.h>
 
 #include <algorithm>
@@ -128,6 +129,8 @@ struct pic_ctx {
     double2** peer_tab = nullptr;         // device [4][8]: every rank's specB, specD, specA, specC
     bool xpose_pull = false;              // transposes by peer pulls (PIC_XPOSE_PULL=1: kernel, 2: copy engines)
     bool xpose_ce = false;                // PIC_XPOSE_PULL=2
+    bool ipc = false;                     // every rank's workspace mapped (peer_ws); p2p = ipc on z-slabs
+    bool pen_ce = false;                  // pencils: y-group redistributions by copy-engine pulls
     cudaStream_t side[8] = {};            // copy-engine pulls, one stream per source rank
     cudaEvent_t side_ev[9] = {};
     char* ws = nullptr;                   // this rank's workspace base
@@ -618,10 +621,37 @@ int pen_rank(const pic_ctx* c, int py, int pz) {
 }
 
 // rho of the pencil [nzl][nyl] -> the slab S0 [nzs][n] (rows y = qs nyl + yl from rank qs).
+// Copy-engine pulls of the y-group redistributions (pen_ce): one 2D copy per group member
+// on its own stream (staggered start), joined into the library stream.
+template <class F>
+pic_status group_pulls(pic_ctx* c, F copy) {
+    const Geom& g = c->g;
+    const int Py = g.Py, py = g.rank % Py;
+    PIC_CUDA(c, cudaEventRecord(c->side_ev[8], c->stream));
+    for (int i = 0; i < Py; ++i) {
+        const int q = (py + i) % Py;
+        PIC_CUDA(c, cudaStreamWaitEvent(c->side[i], c->side_ev[8], 0));
+        PIC_TRY(copy(q, c->side[i]));
+        PIC_CUDA(c, cudaEventRecord(c->side_ev[i], c->side[i]));
+        PIC_CUDA(c, cudaStreamWaitEvent(c->stream, c->side_ev[i], 0));
+    }
+    return PIC_OK;
+}
+
 pic_status pencil_to_slab_rho(pic_ctx* c) {
     const Geom& g = c->g;
     const int nzs = c->gs.nzl, Py = g.Py;
     const size_t rp8 = sizeof(double) * g.rp;
+    if (c->pen_ce) {     // after a barrier (every pencil's rho folded): my slab planes of each member's rows
+        const int py = g.rank % Py, pz = g.rank / Py;
+        PIC_TRY(barrier(c));
+        return group_pulls(c, [&](int q, cudaStream_t s) -> pic_status {
+            const double* src = on_rank(c, pen_rank(c, q, pz), c->rho) + (size_t)py * nzs * g.nyr * g.rp;
+            PIC_CUDA(c, cudaMemcpy2DAsync(c->rho_s + (size_t)q * g.nyl * g.rp, (size_t)g.n * rp8, src,
+                                          g.nyr * rp8, g.nyl * rp8, nzs, cudaMemcpyDeviceToDevice, s));
+            return PIC_OK;
+        });
+    }
     const size_t blk = (size_t)nzs * g.nyl * g.rp;          // doubles per destination
     for (int q = 0; q < Py; ++q)       // planes [q nzs, +nzs), rows 0 .. nyl-1 of each (skip the ghost row)
         PIC_CUDA(c, cudaMemcpy2DAsync(c->xr[0] + q * blk, g.nyl * rp8, c->rho + (size_t)q * nzs * g.nyr * g.rp,
@@ -640,6 +670,22 @@ pic_status pencil_to_slab_rho(pic_ctx* c) {
 pic_status slab_to_pencil_E(pic_ctx* c) {
     const Geom& g = c->g;
     const int nzs = c->gs.nzl, Py = g.Py;
+    if (c->pen_ce) {     // 32-B node records pulled as they are: no pack / unpack kernels
+        const int py = g.rank % Py, pz = g.rank / Py;
+        const size_t row8 = sizeof(double) * 4 * g.n;
+        PIC_TRY(barrier(c));        // every slab field (and its halo plane) complete
+        PIC_TRY(group_pulls(c, [&](int qs, cudaStream_t s) -> pic_status {
+            const double* src = on_rank(c, pen_rank(c, qs, pz), c->E4_s);
+            double* dst = c->E4 + (size_t)qs * nzs * g.nyr * 4 * g.n;
+            PIC_CUDA(c, cudaMemcpy2DAsync(dst, g.nyr * row8, src + (size_t)py * g.nyl * 4 * g.n, g.n * row8,
+                                          g.nyl * row8, nzs + 1, cudaMemcpyDeviceToDevice, s));
+            const int yw = (py * g.nyl + g.nyl) & (g.n - 1);        // halo row nyl (wraps at the last py)
+            PIC_CUDA(c, cudaMemcpy2DAsync(dst + (size_t)g.nyl * 4 * g.n, g.nyr * row8, src + (size_t)yw * 4 * g.n,
+                                          g.n * row8, row8, nzs + 1, cudaMemcpyDeviceToDevice, s));
+            return PIC_OK;
+        }));
+        return barrier(c);          // nobody overwrites its slab field (idle particle buffer) before all pulled
+    }
     const size_t blk = (size_t)(nzs + 1) * (g.nyl + 1) * 3 * g.n;          // doubles per destination (24 B/node)
     pic::launch_e4_pencil_pack(c->E4_s, g.n, nzs, g.nyl, Py, c->xe[0], c->stream);
     PIC_LAUNCHED(c, "e4_pencil_pack");
@@ -1285,9 +1331,16 @@ pic_status setup_p2p(pic_ctx* c) {
     struct Rec {
         cudaIpcMemHandle_t h;
         long long off;
+        long long lay[5];     // on_rank() needs the same carve on every rank
         int ok, pad;
     };
     Rec mine{};
+    const long long lay[5] = {(long long)(reinterpret_cast<char*>(c->rho) - c->ws),
+                              (long long)(reinterpret_cast<char*>(c->part[1][0]) - c->ws),
+                              (long long)(reinterpret_cast<char*>(c->specA) - c->ws),
+                              (long long)(reinterpret_cast<char*>(c->E4) - c->ws),
+                              (long long)(reinterpret_cast<char*>(c->specD) - c->ws)};
+    for (int k = 0; k < 5; ++k) mine.lay[k] = lay[k];
     const char* env = getenv("PIC_P2P");
     int ok = !(env && env[0] == '0');
     if (ok) {
@@ -1314,7 +1367,10 @@ pic_status setup_p2p(pic_ctx* c) {
     PIC_NCCL(c, ncclAllGather(dsend, drecv, sizeof(Rec), ncclUint8, c->comm, c->stream));
     PIC_CUDA(c, cudaMemcpyAsync(all.data(), drecv, sizeof(Rec) * g.P, cudaMemcpyDeviceToHost, c->stream));
     PIC_CUDA(c, cudaStreamSynchronize(c->stream));
-    for (int r = 0; r < g.P; ++r) ok = ok && all[r].ok;
+    for (int r = 0; r < g.P; ++r) {
+        ok = ok && all[r].ok;
+        for (int k = 0; k < 5; ++k) ok = ok && all[r].lay[k] == lay[k];
+    }
     for (int r = 0; r < g.P && ok; ++r) {
         if (r == g.rank) continue;
         void* ptr = nullptr;
@@ -1336,9 +1392,12 @@ pic_status setup_p2p(pic_ctx* c) {
         for (int r = 0; r < g.P; ++r)
             if (c->ipc_open[r]) { cudaIpcCloseMemHandle(c->ipc_open[r]); c->ipc_open[r] = nullptr; }
     }
-    c->p2p = agreed != 0;
+    // pencils map the workspaces too, but only the FFT transposes and the y-group
+    // redistributions use them (migration, halos and ghost folds stay NCCL)
+    c->ipc = agreed != 0;
+    c->p2p = c->ipc && !c->pencil;
     c->xpose_p2p = c->p2p && env && env[0] == '2';
-    if (c->p2p) {
+    if (c->ipc) {
         double2* tab[32] = {};
         for (int r = 0; r < g.P; ++r) {
             tab[r] = on_rank(c, r, c->specB);
@@ -1353,9 +1412,11 @@ pic_status setup_p2p(pic_ctx* c) {
     // PIC_XPOSE_PULL=0 keeps ncclAlltoAll, 1 the pull kernel
     const char* xenv = getenv("PIC_XPOSE_PULL");
     const char xm = xenv && xenv[0] ? xenv[0] : '2';
-    c->xpose_pull = c->p2p && !c->xpose_p2p && (xm == '1' || xm == '2');
+    c->xpose_pull = c->ipc && !c->xpose_p2p && (xm == '1' || xm == '2');
     c->xpose_ce = c->xpose_pull && xm == '2';
-    if (c->xpose_ce) {
+    const char* penv = getenv("PIC_PENCIL_PULL");          // 0: the NCCL y-group all-to-alls
+    c->pen_ce = c->ipc && c->pencil && !(penv && penv[0] == '0');
+    if (c->xpose_ce || c->pen_ce) {
         for (int r = 0; r < g.P; ++r) {
             PIC_CUDA(c, cudaStreamCreateWithFlags(&c->side[r], cudaStreamNonBlocking));
             PIC_CUDA(c, cudaEventCreateWithFlags(&c->side_ev[r], cudaEventDisableTiming));
@@ -1518,16 +1579,15 @@ pic_status pic_init(const pic_params* p, int32_t rank, int32_t nranks, const uin
             return bail(PIC_ENCCL);
         }
         if (c->pencil) {
-            // the y-group (ranks sharing pz) for the pencil <-> slab redistributions; pencils
-            // use the NCCL transport (the peer-memory paths are written for z-slabs)
+            // the y-group (ranks sharing pz) for the pencil <-> slab redistributions (NCCL
+            // fallback); pencils keep the NCCL transport for migration, halos and ghost folds
             r = ncclCommSplit(c->comm, rank / g.Py, rank % g.Py, &c->ycomm, nullptr);
             if (r != ncclSuccess) {
                 snprintf(c->err, sizeof(c->err), "ncclCommSplit: %s", ncclGetErrorString(r));
                 return bail(PIC_ENCCL);
             }
-        } else if ((st = setup_p2p(c)) != PIC_OK) {
-            return bail(st);
         }
+        if ((st = setup_p2p(c)) != PIC_OK) return bail(st);
         if (p->solver != PIC_SOLVER_FFT && !c->p2p) {
             snprintf(c->err, sizeof(c->err), "the PCG / FEM solvers at P > 1 need the peer-memory transport");
             return bail(PIC_EUNSUPPORTED);
