@@ -131,6 +131,7 @@ struct pic_ctx {
     bool xpose_ce = false;                // PIC_XPOSE_PULL=2
     bool ipc = false;                     // every rank's workspace mapped (peer_ws); p2p = ipc on z-slabs
     bool pen_ce = false;                  // pencils: y-group redistributions by copy-engine pulls
+    bool mig_p2p = false;                 // particle migration through the peers' receive buffers
     cudaStream_t side[8] = {};            // copy-engine pulls, one stream per source rank
     cudaEvent_t side_ev[9] = {};
     char* ws = nullptr;                   // this rank's workspace base
@@ -1153,13 +1154,13 @@ pic_status solve_field(pic_ctx* c, double dscale, int slot) {
 // cell key in cur^1 and their charge is deposited; cur flips.
 pic_status push_sort_deposit(pic_ctx* c, int push) {
     const Geom& g = c->g;
-    const bool peer_mig = push && g.P > 1 && c->p2p;
+    const bool peer_mig = push && g.P > 1 && c->mig_p2p;
     {
         StageScope t(c, PIC_STAGE_CLEAR, 0);
         PIC_CUDA(c, cudaMemsetAsync(c->count, 0, sizeof(uint32_t) * (size_t)c->ncell, c->stream));
         PIC_CUDA(c, cudaMemsetAsync(c->rho, 0, sizeof(double) * (size_t)g.nyr * g.rp * (g.nzl + 1), c->stream));
         if (g.P > 1) PIC_CUDA(c, cudaMemsetAsync(c->send_count, 0, sizeof(uint32_t) * g.P, c->stream));
-        if (g.P > 1 && c->p2p && !push) pic::launch_set_u64(c->dcnt + pic::DC_N, (unsigned long long)c->np, c->stream);
+        if (g.P > 1 && c->mig_p2p && !push) pic::launch_set_u64(c->dcnt + pic::DC_N, (unsigned long long)c->np, c->stream);
     }
     if (g.P > 1 && c->p2p && !push) {   // peers add ghost charge only after everyone cleared
         StageScope t(c, PIC_STAGE_EXCHANGE, 0);    // (in a step, the barrier after the push orders it)
@@ -1331,16 +1332,18 @@ pic_status setup_p2p(pic_ctx* c) {
     struct Rec {
         cudaIpcMemHandle_t h;
         long long off;
-        long long lay[5];     // on_rank() needs the same carve on every rank
+        long long lay[7];     // on_rank() needs the same carve on every rank
         int ok, pad;
     };
     Rec mine{};
-    const long long lay[5] = {(long long)(reinterpret_cast<char*>(c->rho) - c->ws),
+    const long long lay[7] = {(long long)(reinterpret_cast<char*>(c->rho) - c->ws),
                               (long long)(reinterpret_cast<char*>(c->part[1][0]) - c->ws),
                               (long long)(reinterpret_cast<char*>(c->specA) - c->ws),
                               (long long)(reinterpret_cast<char*>(c->E4) - c->ws),
-                              (long long)(reinterpret_cast<char*>(c->specD) - c->ws)};
-    for (int k = 0; k < 5; ++k) mine.lay[k] = lay[k];
+                              (long long)(reinterpret_cast<char*>(c->specD) - c->ws),
+                              (long long)(reinterpret_cast<char*>(c->recv) - c->ws),
+                              (long long)c->recv_cap};
+    for (int k = 0; k < 7; ++k) mine.lay[k] = lay[k];
     const char* env = getenv("PIC_P2P");
     int ok = !(env && env[0] == '0');
     if (ok) {
@@ -1369,7 +1372,7 @@ pic_status setup_p2p(pic_ctx* c) {
     PIC_CUDA(c, cudaStreamSynchronize(c->stream));
     for (int r = 0; r < g.P; ++r) {
         ok = ok && all[r].ok;
-        for (int k = 0; k < 5; ++k) ok = ok && all[r].lay[k] == lay[k];
+        for (int k = 0; k < 7; ++k) ok = ok && all[r].lay[k] == lay[k];
     }
     for (int r = 0; r < g.P && ok; ++r) {
         if (r == g.rank) continue;
@@ -1396,6 +1399,11 @@ pic_status setup_p2p(pic_ctx* c) {
     // redistributions use them (migration, halos and ghost folds stay NCCL)
     c->ipc = agreed != 0;
     c->p2p = c->ipc && !c->pencil;
+    // migration through the peers' receive buffers: z-slabs with the peer transport; pencils
+    // with PIC_PENCIL_MIG=1 (r02 at 512^3 on 2 x 2: exchange 1.35 -> 1.21 ms but the step
+    // 20.6 -> 21.0 ms, the solve's pulls slower by 0.5 ms; off by default)
+    const char* menv = getenv("PIC_PENCIL_MIG");
+    c->mig_p2p = c->p2p || (c->ipc && c->pencil && menv && menv[0] == '1');
     c->xpose_p2p = c->p2p && env && env[0] == '2';
     if (c->ipc) {
         double2* tab[32] = {};
@@ -1642,7 +1650,7 @@ pic_status pic_init(const pic_params* p, int32_t rank, int32_t nranks, const uin
     }
     if ((st = sync_check(c)) != PIC_OK) return bail(st);
     c->migrated = 0;
-    if (c->p2p) {
+    if (c->mig_p2p) {
         pic::launch_set_u64(c->dcnt + pic::DC_MIGRATED, 0ull, c->stream);
         if ((st = sync_check(c)) != PIC_OK) return bail(st);
     }
@@ -1980,7 +1988,7 @@ pic_status pic_launches_per_step(pic_ctx* c, int64_t* launches) {
     // solve 6, push_key 1, scan 3, place 1, reorder_deposit 1; P > 1: arrivals 1, and
     // the NCCL transport's ghost fold 1 or the peer transport's count update 1
     // pencils: + the ghost row fold and the field's pack / unpack around the y-group all-to-all
-    *launches = 12 + (c->g.P > 1 ? 2 : 0) + (c->g.P > 1 && c->p2p && pic::leavers_batched() ? 2 : 0) +
+    *launches = 12 + (c->g.P > 1 ? 2 : 0) + (c->g.P > 1 && c->mig_p2p && pic::leavers_batched() ? 2 : 0) +
                 (c->pencil ? 3 : 0);
     if (c->p.solver != PIC_SOLVER_FFT) *launches += c->pcg_launches - 6;   // the latest CG solve's count
     return PIC_OK;
