@@ -340,14 +340,14 @@ __device__ __forceinline__ double2* dst_row(const Geom& g, const SpecLayout& L, 
 // E_z tile one.
 template <int SIGN, int LOGN, bool EMODE>
 __global__ void __launch_bounds__(kThreads, PIC_FFTY_MINB) k_fft_y(Geom g, SpecLayout sl, SpecLayout dl, int ncomp,
-                                                       const double2* __restrict__ tw) {
+                                                       const double2* __restrict__ tw, int64_t tbeg, int64_t tend) {
     extern __shared__ double2 smx[];
     constexpr int n = 1 << LOGN, TW = y_tw(n);
     constexpr int ls = col_stride(n, TW);
     double2* in = smx;               // [n][TW]
     double2* sm = smx + n * TW;      // [TW][ls]
     constexpr int ntiles = (n / 2 + 1 + TW - 1) / TW;
-    const int64_t ntile = (int64_t)ncomp * g.nzl * ntiles;
+    const int64_t ntile = tend;      // tiles [tbeg, tend) of ncomp * nzl * ntiles (plane-major per component)
     auto prefetch = [&](int64_t t) {
         const int d = (int)(t / ((int64_t)g.nzl * ntiles));
         const int r = (int)(t - (int64_t)d * g.nzl * ntiles);
@@ -360,7 +360,7 @@ __global__ void __launch_bounds__(kThreads, PIC_FFTY_MINB) k_fft_y(Geom g, SpecL
         cp_async_commit();
     };
     const double kf = 6.283185307179586476925286766559 / g.L;
-    int64_t t = blockIdx.x;
+    int64_t t = tbeg + blockIdx.x;
     if (t < ntile) prefetch(t);
     for (; t < ntile; t += gridDim.x) {
         const int d = (int)(t / ((int64_t)g.nzl * ntiles));
@@ -409,7 +409,7 @@ __global__ void __launch_bounds__(kThreads, PIC_FFTY_MINB) k_fft_y(Geom g, SpecL
 template <int LOGN>
 __global__ void __launch_bounds__(kThreads, PIC_ZMUL_MINB) k_fft_z_mul(Geom g, const double2* __restrict__ pencil,
                                                            SpecLayout out, double scale,
-                                                           const double2* __restrict__ tw) {
+                                                           const double2* __restrict__ tw, int64_t tbeg, int64_t tend) {
     extern __shared__ double2 smx[];
     constexpr int n = 1 << LOGN, TW = zmul_tw(n);
     constexpr int ls = col_stride(n, TW);
@@ -424,7 +424,7 @@ __global__ void __launch_bounds__(kThreads, PIC_ZMUL_MINB) k_fft_z_mul(Geom g, c
     double2* s2 = s1 + TW * ls;      // [TW][ls] inverse work
 #endif
     constexpr int ntiles = (n / 2 + 1 + TW - 1) / TW;
-    const int64_t ntile = (int64_t)nyl * ntiles;
+    const int64_t ntile = tend;      // tiles [tbeg, tend) of nyl * ntiles (ky-row-major)
     const int64_t zstride = (int64_t)nyl * g.px;
     auto prefetch = [&](int64_t t) {
         const int yl = (int)(t / ntiles), kx0 = (int)(t - (int64_t)yl * ntiles) * TW;
@@ -438,7 +438,7 @@ __global__ void __launch_bounds__(kThreads, PIC_ZMUL_MINB) k_fft_z_mul(Geom g, c
     };
     const double kf = 6.283185307179586476925286766559 / g.L;
     constexpr int half = n / 2;
-    int64_t t = blockIdx.x;
+    int64_t t = tbeg + blockIdx.x;
 #if !PIC_ZMUL_DIRECT
     if (t < ntile) prefetch(t);
 #endif
@@ -857,34 +857,47 @@ void launch_fft_x_fwd(const Geom& g, double* S0, const double2* tw, cudaStream_t
     PIC_X_SWITCH(ilog2(g.n / 2), (k_fft_x_fwd<K><<<persistent_grid(k_fft_x_fwd<K>, smem, nt), kThreads, smem, s>>>(g, S0, tw)))
 }
 
+int fft_plane_tiles(int n) {
+    const int TW = y_tw(n);
+    return (n / 2 + 1 + TW - 1) / TW;
+}
+int fft_zrow_tiles(int n) {
+    const int TW = zmul_tw(n);
+    return (n / 2 + 1 + TW - 1) / TW;
+}
+
 void launch_fft_y(const Geom& g, SpecLayout src, SpecLayout dst, int ncomp, int inverse,
-                  const double2* tw, cudaStream_t s) {
+                  const double2* tw, cudaStream_t s, int64_t tbeg, int64_t tend) {
     const int TW = y_tw(g.n), ntiles = (g.n / 2 + 1 + TW - 1) / TW;
     const size_t smem = sizeof(double2) * (size_t)TW * (g.n + col_stride(g.n, TW));
-    const int64_t nt = (int64_t)ncomp * g.nzl * ntiles;
+    if (tend < 0) tend = (int64_t)ncomp * g.nzl * ntiles;
+    const int64_t nt = tend - tbeg;
+    if (nt <= 0) return;
     if (inverse)
-        PIC_YZ_SWITCH(ilog2(g.n), (k_fft_y<+1, K, false><<<persistent_grid(k_fft_y<+1, K, false>, smem, nt), kThreads, smem, s>>>(g, src, dst, ncomp, tw)))
+        PIC_YZ_SWITCH(ilog2(g.n), (k_fft_y<+1, K, false><<<persistent_grid(k_fft_y<+1, K, false>, smem, nt), kThreads, smem, s>>>(g, src, dst, ncomp, tw, tbeg, tend)))
     else
-        PIC_YZ_SWITCH(ilog2(g.n), (k_fft_y<-1, K, false><<<persistent_grid(k_fft_y<-1, K, false>, smem, nt), kThreads, smem, s>>>(g, src, dst, ncomp, tw)))
+        PIC_YZ_SWITCH(ilog2(g.n), (k_fft_y<-1, K, false><<<persistent_grid(k_fft_y<-1, K, false>, smem, nt), kThreads, smem, s>>>(g, src, dst, ncomp, tw, tbeg, tend)))
 }
 
 void launch_fft_y_field(const Geom& g, SpecLayout src, SpecLayout dst, const double2* tw, cudaStream_t s) {
     const int TW = y_tw(g.n), ntiles = (g.n / 2 + 1 + TW - 1) / TW;
     const size_t smem = sizeof(double2) * (size_t)TW * (g.n + col_stride(g.n, TW));
     const int64_t nt = (int64_t)2 * g.nzl * ntiles;
-    PIC_YZ_SWITCH(ilog2(g.n), (k_fft_y<+1, K, true><<<persistent_grid(k_fft_y<+1, K, true>, smem, nt), kThreads, smem, s>>>(g, src, dst, 2, tw)))
+    PIC_YZ_SWITCH(ilog2(g.n), (k_fft_y<+1, K, true><<<persistent_grid(k_fft_y<+1, K, true>, smem, nt), kThreads, smem, s>>>(g, src, dst, 2, tw, 0, nt)))
 }
 
 void launch_fft_z_mul(const Geom& g, const double2* pencil, SpecLayout out, double scale,
-                      const double2* tw, cudaStream_t s) {
+                      const double2* tw, cudaStream_t s, int64_t tbeg, int64_t tend) {
     const int TW = zmul_tw(g.n), ntiles = (g.n / 2 + 1 + TW - 1) / TW;
     const size_t smem = sizeof(double2) * ((size_t)TW * ((PIC_ZMUL_DIRECT ? 0 : g.n) + col_stride(g.n, TW)) +
                                             (PIC_ZMUL_FUSED ? 2 * (size_t)TW * col_stride(g.n, 2 * TW)
                                                             : (size_t)TW * col_stride(g.n, TW)));
-    const int64_t nt = (int64_t)(g.n / g.P) * ntiles;
+    if (tend < 0) tend = (int64_t)(g.n / g.P) * ntiles;
+    const int64_t nt = tend - tbeg;
+    if (nt <= 0) return;
     // one tile per CTA: the pass is bound by its four transforms, not its input
     // loads, and measured faster without the persistent loop
-    PIC_YZ_SWITCH(ilog2(g.n), (k_fft_z_mul<K><<<(unsigned)nt, kThreads, smem, s>>>(g, pencil, out, scale, tw)))
+    PIC_YZ_SWITCH(ilog2(g.n), (k_fft_z_mul<K><<<(unsigned)nt, kThreads, smem, s>>>(g, pencil, out, scale, tw, tbeg, tend)))
 }
 
 void launch_fft_x_inv(const Geom& g, const double2* spec, double* E4, double* halo, const double2* tw,

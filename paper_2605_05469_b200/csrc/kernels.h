@@ -26,8 +26,12 @@ int energy_partials(const Geom& g);
 // rows of rho (nzl * n, real, pitch rp doubles) -> R2C in place
 void launch_fft_x_fwd(const Geom& g, double* S0, const double2* tw, cudaStream_t s);
 // y FFT of component(s) d < ncomp of src -> dst (may alias src with the same layout)
+// tiles [tbeg, tend) only (default all): a tile is TW kx columns of one plane, fft_plane_tiles(n)
+// tiles per plane, planes in order within each component
 void launch_fft_y(const Geom& g, SpecLayout src, SpecLayout dst, int ncomp, int inverse,
-                  const double2* tw, cudaStream_t s);
+                  const double2* tw, cudaStream_t s, int64_t tbeg = 0, int64_t tend = -1);
+int fft_plane_tiles(int n);
+int fft_zrow_tiles(int n);
 // Inverse y pass of the field: src (PACKED, 2 components: phi^, E^_z after the inverse
 // z pass) -> dst NORMAL 3 components: E_x = -i k_x phi, E_y = -i k_y phi, E_z.
 void launch_fft_y_field(const Geom& g, SpecLayout src, SpecLayout dst, const double2* tw, cudaStream_t s);
@@ -35,7 +39,7 @@ void launch_fft_y_field(const Geom& g, SpecLayout src, SpecLayout dst, const dou
 // phi^ = rho^ scale / |k|^2, 2 inverse z FFTs (phi^, E^_z = -i k_z phi^, D#6) -> out
 // PACKED or REMOTE (2 components; q = z / nzl).  ky0 = rank * nyl.
 void launch_fft_z_mul(const Geom& g, const double2* pencil, SpecLayout out, double scale,
-                      const double2* tw, cudaStream_t s);
+                      const double2* tw, cudaStream_t s, int64_t tbeg = 0, int64_t tend = -1);   // tiles: fft_zrow_tiles(n) per ky row
 // 3 components NORMAL (spec + d * nzl*n*px) -> E4 slab planes 0..nzl-1 + energy
 // partials; plane 0 is also written to `halo` (the halo plane nzl of the slab below,
 // on its GPU; P = 1: this slab's own), if not null.

@@ -129,6 +129,7 @@ struct pic_ctx {
     double2** peer_tab = nullptr;         // device [4][8]: every rank's specB, specD, specA, specC
     bool xpose_pull = false;              // transposes by peer pulls (PIC_XPOSE_PULL=1: kernel, 2: copy engines)
     bool xpose_ce = false;                // PIC_XPOSE_PULL=2
+    bool xpose_split = false;             // PIC_XPOSE_SPLIT: pulls overlapped with the y / z pass halves
     bool ipc = false;                     // every rank's workspace mapped (peer_ws); p2p = ipc on z-slabs
     bool pen_ce = false;                  // pencils: y-group redistributions by copy-engine pulls
     bool mig_p2p = false;                 // particle migration through the peers' receive buffers
@@ -788,6 +789,32 @@ pic_status xpose_pull(pic_ctx* c, double2* dst, double2* src, double2* const* sr
     return PIC_OK;
 }
 
+// One part of every transpose block by copy-engine pulls: dst block q + off <- rank q's src
+// block rank + off, width bytes x height rows at pitch bytes, forked from the library stream
+// (join: the library stream waits for all of them).
+pic_status xpose_part(pic_ctx* c, double2* dst, double2* src, int64_t blk, int64_t off, size_t width,
+                      size_t height, size_t pitch, bool join) {
+    const Geom& g = c->gs;
+    PIC_CUDA(c, cudaEventRecord(c->side_ev[8], c->stream));
+    for (int i = 0; i < g.P; ++i) {
+        const int q = (g.rank + i) % g.P;
+        const double2* from = (q == g.rank ? src : on_rank(c, q, src)) + (size_t)g.rank * blk + off;
+        PIC_CUDA(c, cudaStreamWaitEvent(c->side[i], c->side_ev[8], 0));
+        PIC_CUDA(c, cudaMemcpy2DAsync(dst + (size_t)q * blk + off, pitch, from, pitch, width, height,
+                                      cudaMemcpyDeviceToDevice, c->side[i]));
+        if (join) {
+            PIC_CUDA(c, cudaEventRecord(c->side_ev[i], c->side[i]));
+            PIC_CUDA(c, cudaStreamWaitEvent(c->stream, c->side_ev[i], 0));
+        }
+    }
+    return PIC_OK;
+}
+
+// The split transposes (PIC_XPOSE_SPLIT; pencils by default): both halves non-empty.
+bool xpose_split(const pic_ctx* c) {
+    return c->gs.P > 1 && c->xpose_ce && c->xpose_split && c->gs.nzl >= 2;
+}
+
 // Destination of fft_x_inv's copy of plane 0: the halo plane of the slab below.
 double* halo_dst(pic_ctx* c) {
     const Geom& g = c->gs;
@@ -857,6 +884,48 @@ pic_status solve(pic_ctx* c, double scale, int slot) {
     }
     { StageScope t(c, PIC_STAGE_FFT_X_FWD, 1); pic::launch_fft_x_fwd(g, c->rho_s, c->tw, c->stream); }
     PIC_LAUNCHED(c, "fft_x_fwd");
+    if (xpose_split(c)) {
+        // copy-engine transposes overlapped with the passes that produce them: the y pass in two
+        // plane halves (the first half's blocks are pulled while the second is transformed),
+        // the z pass in two ky-row halves likewise
+        const int64_t pt = pic::fft_plane_tiles(g.n), zt = pic::fft_zrow_tiles(g.n);
+        const int h = g.nzl / 2, nz = g.nzl;                    // nyl = nzl on the FFT's slabs
+        const int64_t blkA = (int64_t)(unit / g.P), blkC = 2 * blkA;
+        const size_t row = sizeof(double2) * (size_t)g.px;
+        { StageScope t(c, PIC_STAGE_FFT_Y_FWD, 1); pic::launch_fft_y(g, S0, A, 1, 0, c->tw, c->stream, 0, h * pt); }
+        PIC_LAUNCHED(c, "fft_y_fwd");
+        {
+            StageScope t(c, PIC_STAGE_XPOSE, 0);
+            PIC_TRY(barrier(c));
+            PIC_TRY(xpose_part(c, c->specB, c->specA, blkA, 0, h * nz * row, 1, h * nz * row, false));
+        }
+        { StageScope t(c, PIC_STAGE_FFT_Y_FWD, 1); pic::launch_fft_y(g, S0, A, 1, 0, c->tw, c->stream, h * pt, nz * pt); }
+        PIC_LAUNCHED(c, "fft_y_fwd");
+        {
+            StageScope t(c, PIC_STAGE_XPOSE, 0);
+            PIC_TRY(barrier(c));
+            PIC_TRY(xpose_part(c, c->specB, c->specA, blkA, (int64_t)h * nz * g.px, (nz - h) * nz * row, 1,
+                               (nz - h) * nz * row, true));
+        }
+        { StageScope t(c, PIC_STAGE_FFT_Z_MUL, 1); pic::launch_fft_z_mul(g, c->specB, Cz, scale, c->tw, c->stream, 0, h * zt); }
+        PIC_LAUNCHED(c, "fft_z_mul");
+        {
+            StageScope t(c, PIC_STAGE_XPOSE, 0);
+            PIC_TRY(barrier(c));
+            PIC_TRY(xpose_part(c, c->specD, c->specC, blkC, 0, h * row, 2 * nz, nz * row, false));
+        }
+        {
+            StageScope t(c, PIC_STAGE_FFT_Z_MUL, 1);
+            pic::launch_fft_z_mul(g, c->specB, Cz, scale, c->tw, c->stream, h * zt, nz * zt);
+        }
+        PIC_LAUNCHED(c, "fft_z_mul");
+        {
+            StageScope t(c, PIC_STAGE_XPOSE, 0);
+            PIC_TRY(barrier(c));
+            PIC_TRY(xpose_part(c, c->specD, c->specC, blkC, (int64_t)h * g.px, (nz - h) * row, 2 * nz, nz * row, true));
+            PIC_TRY(barrier(c));             // every rank has pulled from my specC before the field y pass
+        }
+    } else {
     { StageScope t(c, PIC_STAGE_FFT_Y_FWD, 1); pic::launch_fft_y(g, S0, A, 1, 0, c->tw, c->stream); }
     PIC_LAUNCHED(c, "fft_y_fwd");
     if (g.P > 1) {
@@ -883,6 +952,7 @@ pic_status solve(pic_ctx* c, double scale, int slot) {
         } else {
             PIC_NCCL(c, ncclAlltoAll(c->specC, c->specD, 4 * unit / g.P, ncclDouble, c->comm, c->stream));
         }
+    }
     }
     { StageScope t(c, PIC_STAGE_FFT_Y_INV, 1); pic::launch_fft_y_field(g, D, C, c->tw, c->stream); }
     PIC_LAUNCHED(c, "fft_y_inv");
@@ -1422,6 +1492,10 @@ pic_status setup_p2p(pic_ctx* c) {
     const char xm = xenv && xenv[0] ? xenv[0] : '2';
     c->xpose_pull = c->ipc && !c->xpose_p2p && (xm == '1' || xm == '2');
     c->xpose_ce = c->xpose_pull && xm == '2';
+    // split transposes (r02, 512^3 on 4 GPUs): pencils 2 x 2 20.60 -> 20.45 ms, slabs 19.37 ->
+    // 19.33 / 19.79 ms (no gain, more spread): on for pencils, PIC_XPOSE_SPLIT=0/1 overrides
+    const char* senv = getenv("PIC_XPOSE_SPLIT");
+    c->xpose_split = c->xpose_ce && (senv && senv[0] ? senv[0] == '1' : c->pencil);
     const char* penv = getenv("PIC_PENCIL_PULL");          // 0: the NCCL y-group all-to-alls
     c->pen_ce = c->ipc && c->pencil && !(penv && penv[0] == '0');
     if (c->xpose_ce || c->pen_ce) {
@@ -1989,7 +2063,7 @@ pic_status pic_launches_per_step(pic_ctx* c, int64_t* launches) {
     // the NCCL transport's ghost fold 1 or the peer transport's count update 1
     // pencils: + the ghost row fold and the field's pack / unpack around the y-group all-to-all
     *launches = 12 + (c->g.P > 1 ? 2 : 0) + (c->g.P > 1 && c->mig_p2p && pic::leavers_batched() ? 2 : 0) +
-                (c->pencil ? 3 : 0);
+                (c->pencil ? (c->pen_ce ? 1 : 3) : 0) + (xpose_split(c) ? 2 : 0);
     if (c->p.solver != PIC_SOLVER_FFT) *launches += c->pcg_launches - 6;   // the latest CG solve's count
     return PIC_OK;
 }
