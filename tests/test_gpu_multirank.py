@@ -56,18 +56,22 @@ def test_slab_decomposition_cg_solvers_match_oracle(world, n, solver):
     assert "MP OK" in r.stdout and f"solver={solver}" in r.stdout
 
 
-@pytest.mark.parametrize("world,n,pgrid", [(2, 32, "2x1"), (4, 32, "2x2"), (8, 64, "2x4"), (8, 64, "4x2")])
-def test_pencil_decomposition_matches_oracle(world, n, pgrid):
+@pytest.mark.parametrize("world,n,pgrid,pulls", [(2, 32, "2x1", "ce"), (4, 32, "2x2", "ce"), (4, 32, "4x1", "ce"),
+                                                (4, 32, "2x2", "nccl"), (8, 64, "2x4", "ce"), (8, 64, "4x2", "ce")])
+def test_pencil_decomposition_matches_oracle(world, n, pgrid, pulls):
     """Pencils over (y, z) (BJ config 4): particles and the real-space grid on
     Py x Pz domains (ghost row/plane folds and halos over NCCL, migration to the face and
-    diagonal neighbours), the FFT on z-slabs after a y-group all-to-all; vs the
-    single-domain oracle (W_x 1e-10 every step, x, v 1e-12 after 20 steps) and the library
-    sampler on the pencils vs the oracle's."""
+    diagonal neighbours), the FFT on z-slabs after a y-group exchange (copy-engine pulls over
+    the IPC mapping, or with pulls="nccl" the NCCL all-to-alls); vs the single-domain oracle
+    (W_x 1e-10 every step, x, v 1e-12 after 20 steps) and the library sampler on the pencils
+    vs the oracle's."""
     if _ngpus() < world:
         pytest.skip(f"needs {world} GPUs")
     env = dict(os.environ, MP_EXPECT_TRANSPORT="nccl", MP_PGRID=pgrid)
     env.pop("PIC_P2P", None)
-    port = 29700 + 10 * world + int(pgrid[0])
+    if pulls == "nccl":
+        env.update(PIC_PENCIL_PULL="0", PIC_XPOSE_PULL="0")
+    port = 29700 + 10 * world + int(pgrid[0]) + (5 if pulls == "nccl" else 0)
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
            "--master-addr", "127.0.0.1", "--master-port", str(port),
            os.path.join(ROOT, "tests", "mp_worker.py"), str(n), "8", "20"]
