@@ -131,7 +131,8 @@ void launch_scan(uint32_t* count, uint32_t* offs, int64_t n, uint32_t* scratch, 
 // dcnt != null: the entries are dcnt[DC_N] + dcnt[DC_ARR] (<= np, read on the device).
 // Sorted positions >= cap are dropped and flag err_flag[2].
 void launch_place(const uint32_t* key, const uint16_t* rank, int64_t np, const uint32_t* offs, uint32_t* cursor,
-                  uint32_t* perm, const unsigned long long* dcnt, int64_t cap, int* err_flag, cudaStream_t s);
+                  uint32_t* perm, const unsigned long long* dcnt, int64_t cap, int* err_flag, cudaStream_t s,
+                  const Geom* g = nullptr, const uint32_t* bprev = nullptr);
 // Per brick: stable order inside each cell, gather through perm (entries >= n_old
 // from recv; dcnt != null: n_old = dcnt[DC_N]), drift residents (push=1), store
 // sorted into nxt, deposit the CIC weight sums into rho_buf planes 0..nzl-1; the

@@ -34,6 +34,13 @@
 #ifndef PIC_PLACE_ATOMIC
 #define PIC_PLACE_ATOMIC 0
 #endif
+// PIC_PLACE_AGG (with PIC_PLACE_ATOMIC=1, P = 1): place takes its cursor positions per source
+// brick -- a shared-memory histogram of the brick's particles over the window around it
+// (AggWin) and one returned cursor atomic per non-empty window cell -- instead of one
+// returned atomic per particle.
+#ifndef PIC_PLACE_AGG
+#define PIC_PLACE_AGG 0
+#endif
 #ifndef PIC_ATOM_BATCH      // particles per batch of returned count atomics in push_key
 #define PIC_ATOM_BATCH 1        // r02 A/B at 512^3: 1, 2, 4, 8 -> 19.97, 20.21, 20.19, 19.94 ms
 #endif
@@ -1147,7 +1154,7 @@ void launch_push_key(const Geom& g, PState cur, const uint32_t* offs, const doub
     static const bool unbatched = [] { const char* e = getenv("PIC_P2P_MIG"); return e && e[0] == '1'; }();
     if (peers && unbatched) { sb.peers = *peers; sb.remote = 1; }
     static const bool force_mr = getenv("PIC_FORCE_MR") != nullptr;   // diagnostics
-    if (PIC_RD_PF == 0) bprev = nullptr;       // only the reorder's L2 prefetch reads it
+    if (PIC_RD_PF == 0 && !(PIC_PLACE_AGG && PIC_PLACE_ATOMIC)) bprev = nullptr;   // the reorder's prefetch / place_agg
     if (g.P > 1 || force_mr) k_push_key_brick<true><<<nbrick, kThreads, 0, s>>>(g, cur, offs, E4, key, rank, count, sb, bprev, err_flag);
     else k_push_key_brick<false><<<nbrick, kThreads, 0, s>>>(g, cur, offs, E4, key, rank, count, sb, bprev, err_flag);
 }
@@ -1196,9 +1203,72 @@ void launch_scan(uint32_t* count, uint32_t* offs, int64_t n, uint32_t* scratch, 
     k_scan_apply<<<nb, kThreads, 0, s>>>(count, offs, n, scratch, cursor && PIC_PLACE_ATOMIC);
 }
 
+// PIC_PLACE_AGG: CTA b places the particles of brick b of the order push_key read
+// ([bprev[b], bprev[b + 1])): rank within the brick's arrivals in each window cell by a
+// shared atomic, one returned cursor atomic per non-empty window cell for the block base,
+// then perm[base + rank] = i; particles landing outside the window take their own atomic.
+__global__ void __launch_bounds__(kThreads) k_place_agg(Geom g, const uint32_t* __restrict__ key,
+                                                        const uint32_t* __restrict__ bprev,
+                                                        uint32_t* __restrict__ cursor, uint32_t* __restrict__ perm,
+                                                        int64_t cap, int* __restrict__ err) {
+    using Win = AggWin;
+    __shared__ uint32_t hist[Win::NB], binkey[Win::NB], info[kInfoCap];
+    const int t = threadIdx.x;
+    int bx, by, bz;
+    unlkey(g, blockIdx.x * kBrick, bx, by, bz);
+    for (int b = t; b < Win::NB; b += kThreads) hist[b] = 0;
+    const uint32_t P0 = bprev[blockIdx.x], P1 = bprev[blockIdx.x + 1];
+    __syncthreads();
+    for (uint32_t i = P0 + t; i < P1; i += kThreads) {
+        const uint32_t k = __ldg(key + i), li = i - P0;
+        int ix, iyl, izl;
+        unlkey(g, k, ix, iyl, izl);
+        const int b = li < (uint32_t)kInfoCap ? Win::bin(g, ix, iyl, izl, bx, by, bz) : -1;
+        if (b >= 0) {
+            const uint32_t lr = atomicAdd(&hist[b], 1u);
+            if (lr == 0) binkey[b] = k;
+            info[li] = (uint32_t)b | (lr << 12);
+        } else {
+            const uint32_t pos = atomicAdd(cursor + k, 1u);
+            if (pos < (uint64_t)cap) perm[pos] = i;
+            else atomicExch(err + 2, 1);
+            if (li < (uint32_t)kInfoCap) info[li] = ~0u;
+        }
+    }
+    __syncthreads();
+    constexpr int kPer = (Win::NB + kThreads - 1) / kThreads;
+    uint32_t cb[kPer], rb[kPer];
+#pragma unroll
+    for (int u = 0; u < kPer; ++u) {
+        const int b = t + u * kThreads;
+        cb[u] = b < Win::NB ? hist[b] : 0u;
+    }
+#pragma unroll
+    for (int u = 0; u < kPer; ++u)
+        if (cb[u]) rb[u] = atomicAdd(cursor + binkey[t + u * kThreads], cb[u]);
+#pragma unroll
+    for (int u = 0; u < kPer; ++u)
+        if (cb[u]) hist[t + u * kThreads] = rb[u];
+    __syncthreads();
+    const uint32_t Pe = min(P1, P0 + (uint32_t)kInfoCap);
+    for (uint32_t i = P0 + t; i < Pe; i += kThreads) {
+        const uint32_t v = info[i - P0];
+        if (v == ~0u) continue;
+        const uint32_t pos = hist[v & 0xfffu] + (v >> 12);
+        if (pos < (uint64_t)cap) perm[pos] = i;
+        else atomicExch(err + 2, 1);
+    }
+}
+
 void launch_place(const uint32_t* key, const uint16_t* rank, int64_t np, const uint32_t* offs, uint32_t* cursor,
-                  uint32_t* perm, const unsigned long long* dcnt, int64_t cap, int* err_flag, cudaStream_t s) {
+                  uint32_t* perm, const unsigned long long* dcnt, int64_t cap, int* err_flag, cudaStream_t s,
+                  const Geom* g, const uint32_t* bprev) {
     if (np == 0) return;
+    if (PIC_PLACE_AGG && PIC_PLACE_ATOMIC && g && g->P == 1 && bprev) {
+        const unsigned nbrick = (unsigned)(((int64_t)g->n * g->nyl * g->nzl) / kBrick);
+        k_place_agg<<<nbrick, kThreads, 0, s>>>(*g, key, bprev, cursor, perm, cap, err_flag);
+        return;
+    }
     k_place<<<blocks((np + 3) / 4, kThreads), kThreads, 0, s>>>(key, rank, np,
                                                                  PIC_PLACE_ATOMIC ? cursor : const_cast<uint32_t*>(offs),
                                                                  perm, dcnt, cap, err_flag);

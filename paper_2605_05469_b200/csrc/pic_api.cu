@@ -1315,7 +1315,8 @@ pic_status push_sort_deposit(pic_ctx* c, int push) {
     }
     { StageScope t(c, PIC_STAGE_SCAN, 3); pic::launch_scan(c->count, c->offs, c->ncell, c->scan_scratch, c->stream, true); }
     PIC_LAUNCHED(c, "scan");
-    { StageScope t(c, PIC_STAGE_PLACE, 1); pic::launch_place(c->key, c->rank, n_bound, c->offs, c->count, c->perm, dc, c->np_cap, c->err_flag, c->stream); }
+    { StageScope t(c, PIC_STAGE_PLACE, 1); pic::launch_place(c->key, c->rank, n_bound, c->offs, c->count, c->perm, dc, c->np_cap, c->err_flag, c->stream,
+                                                                      &g, push ? c->bprev : nullptr); }
     PIC_LAUNCHED(c, "place");
     {
         StageScope t(c, PIC_STAGE_REORDER_DEPOSIT, 1);
